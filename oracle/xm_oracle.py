@@ -1,0 +1,787 @@
+"""XM oracle — plain, slow, obviously-correct fp64 CPU implementation.
+
+*** TEST INFRASTRUCTURE ONLY. ***  Only ``tests/``, ``__graft_entry__.smoke()``
+and ``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+module.  The product path (``paper_2502_04640_b200``) never imports it and
+shares no code with it; the only common dependency is the seeded input
+generator ``synth/`` (which holds none of the method's arithmetic).
+
+Citations: ``P:n`` = reference PAPER.md line n, ``S:n`` = SPEC.md line n.
+Readings of garbled / silent passages follow SURVEY.md §8(c) (C1..C21) and are
+listed in DESIGN.md §"Readings".
+
+Conventions (DESIGN.md §"Notation"): the BM factor is stored TALL,
+Y = Uᵀ ∈ ℝ^{n×r}, n = 3N, row-major; frame i owns rows 3i..3i+2, the block
+Y_i = Ū_iᵀ ∈ ℝ^{3×r}.  Frame 0 is the paper's anchored frame 1.
+Inner products are Frobenius over the whole n×r array (reading C4).
+
+Every function is pinned by ``tests/test_oracle_*.py`` against the paper /
+mathematics (closed forms, brute force, invariants); no function here is
+"parity unpinned".
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+from typing import Optional
+
+import numpy as np
+import scipy.linalg as sla
+import scipy.sparse as sp
+
+EPS = np.finfo(np.float64).eps
+
+
+class OracleError(RuntimeError):
+    """Raised with one of the status names of include/xm.h (e.g. 'EINVAL')."""
+
+    def __init__(self, code: str, msg: str):
+        super().__init__(f"{code}: {msg}")
+        self.code = code
+
+
+# =============================================================================
+# H1  Ingest + validate   (C17)
+# =============================================================================
+
+def validate(N: int, M: int, frame, landmark, pts, w=None):
+    """Validate a view graph and drop duplicate (frame, landmark) pairs.
+
+    * indices in range, w > 0, finite points, depth ũ_z > 0   (C17)
+    * duplicates: keep the first occurrence
+    * every frame observed; the bipartite frame–landmark graph restricted to
+      observed landmarks is connected (Lemma 1 P:1197 needs it)
+
+    Returns (frame, landmark, pts, w, n_duplicates).
+    """
+    frame = np.asarray(frame, dtype=np.int64)
+    landmark = np.asarray(landmark, dtype=np.int64)
+    pts = np.asarray(pts, dtype=np.float64).reshape(-1, 3)
+    E = frame.shape[0]
+    w = np.ones(E) if w is None else np.asarray(w, dtype=np.float64)
+    if N < 1 or M < 1 or E < 1:
+        raise OracleError("EINVAL", "empty view graph")
+    if landmark.shape[0] != E or pts.shape[0] != E or w.shape[0] != E:
+        raise OracleError("EINVAL", "array length mismatch")
+    if frame.min() < 0 or frame.max() >= N or landmark.min() < 0 or landmark.max() >= M:
+        raise OracleError("EINVAL", "index out of range")
+    if not (np.all(np.isfinite(pts)) and np.all(np.isfinite(w))):
+        raise OracleError("EINVAL", "non-finite value")
+    if np.any(w <= 0):
+        raise OracleError("EINVAL", "non-positive weight")
+    if np.any(pts[:, 2] <= 0):
+        raise OracleError("EINVAL", "non-positive depth")
+    # keep first duplicate, preserve input order otherwise
+    seen = {}
+    keep = np.zeros(E, dtype=bool)
+    for e in range(E):
+        key = (int(frame[e]), int(landmark[e]))
+        if key not in seen:
+            seen[key] = e
+            keep[e] = True
+    n_dup = int(E - keep.sum())
+    frame, landmark, pts, w = frame[keep], landmark[keep], pts[keep], w[keep]
+    if np.any(np.bincount(frame, minlength=N) == 0):
+        raise OracleError("EDISCONNECTED", "a frame has no observation")
+    if connected_components(N, M, frame, landmark) != 1:
+        raise OracleError("EDISCONNECTED", "graph numerically disconnected")
+    return frame, landmark, pts, w, n_dup
+
+
+def connected_components(N: int, M: int, frame, landmark) -> int:
+    """Number of components of the bipartite graph on frames ∪ observed
+    landmarks, by breadth-first search."""
+    adj_f = [[] for _ in range(N)]
+    adj_l = {}
+    for i, k in zip(np.asarray(frame).tolist(), np.asarray(landmark).tolist()):
+        adj_f[i].append(k)
+        adj_l.setdefault(k, []).append(i)
+    seen_f = [False] * N
+    seen_l = set()
+    comps = 0
+    for s0 in range(N):
+        if seen_f[s0]:
+            continue
+        comps += 1
+        stack = [("f", s0)]
+        seen_f[s0] = True
+        while stack:
+            kind, v = stack.pop()
+            if kind == "f":
+                for k in adj_f[v]:
+                    if k not in seen_l:
+                        seen_l.add(k)
+                        stack.append(("l", k))
+            else:
+                for i in adj_l[v]:
+                    if not seen_f[i]:
+                        seen_f[i] = True
+                        stack.append(("f", i))
+    return comps
+
+
+# =============================================================================
+# H3  Co-visibility (BSR) pattern of S
+# =============================================================================
+
+def s_pattern(N: int, frame, landmark):
+    """Block pattern {(i,j): i = j or ∃k observed by both i and j}.
+
+    Returned as CSR over frames: rowptr int64 [N+1], colidx int32 sorted per
+    row.  This is the structural sparsity of S = H_UU after landmark
+    elimination (Q itself is block-dense for connected graphs, F1)."""
+    rows = [set([i]) for i in range(N)]
+    tracks = {}
+    for i, k in zip(np.asarray(frame).tolist(), np.asarray(landmark).tolist()):
+        tracks.setdefault(k, []).append(i)
+    for fs in tracks.values():
+        for a in fs:
+            rows[a].update(fs)
+    rowptr = np.zeros(N + 1, dtype=np.int64)
+    cols = []
+    for i in range(N):
+        c = sorted(rows[i])
+        cols.extend(c)
+        rowptr[i + 1] = rowptr[i] + len(c)
+    return rowptr, np.asarray(cols, dtype=np.int32)
+
+
+# =============================================================================
+# H4/H5  The data matrix Q   (Prop. 1; App. A)
+# =============================================================================
+
+@dataclasses.dataclass
+class DataMatrix:
+    Q: np.ndarray        # n×n, symmetric PSD (Prop. 1)
+    S: np.ndarray        # n×n   H_UU after landmark elimination
+    C: np.ndarray        # N×n   H_tU
+    K: np.ndarray        # N×N   H_tt
+    L: np.ndarray        # Cholesky factor of K̄ = K[1:,1:]   ((N−1)×(N−1))
+    G: np.ndarray        # L⁻¹ C̄, C̄ = C[1:, :]             ((N−1)×n)
+    W: np.ndarray        # per-landmark total weight W_k = Σ_{e∈k} w_e (Q_3 diag)
+    frame: np.ndarray
+    landmark: np.ndarray
+    pts: np.ndarray
+    w: np.ndarray
+    N: int
+    M: int
+
+    @property
+    def n(self):
+        return 3 * self.N
+
+    @property
+    def normF(self):
+        return float(np.linalg.norm(self.Q))
+
+
+def quadratic_form(N: int, M: int, frame, landmark, pts, w):
+    """H = Σ_e w_e b_e b_eᵀ over the stacked variables [Y-rows; t; p].
+
+    The SBA objective Eq. (3) with the unknowns stacked as
+    Zext = [Y; T; P] ∈ ℝ^{(3N+N+M)×r} (rows: the 3N rows of Y = Uᵀ, then t_iᵀ,
+    then p_kᵀ) is Σ_e w_e ‖b_eᵀ Zext‖² = tr(Zextᵀ H Zext), where b_e has ũ_e
+    at rows 3i..3i+2, +1 at t_i and −1 at p_k (App. A P:1161-1167 with
+    vec(U) read row-wise; reading C1)."""
+    E = len(frame)
+    n = 3 * N
+    rows = np.repeat(np.arange(E), 5)
+    cols = np.empty((E, 5), dtype=np.int64)
+    vals = np.empty((E, 5))
+    for a in range(3):
+        cols[:, a] = 3 * frame + a
+        vals[:, a] = pts[:, a]
+    cols[:, 3] = n + frame
+    vals[:, 3] = 1.0
+    cols[:, 4] = n + N + landmark
+    vals[:, 4] = -1.0
+    B = sp.csr_matrix((vals.ravel(), (rows, cols.ravel())), shape=(E, n + N + M))
+    H = (B.T @ sp.diags(w) @ B).tocsr()
+    return H
+
+
+def build_Q(N: int, M: int, frame, landmark, pts, w=None, validate_input=True) -> DataMatrix:
+    """Q = Schur complement of H onto the U (Y-row) block after deleting t_0.
+
+    Two exact elimination stages (SURVEY §8(c) "plain definitions"):
+      1. landmarks: H_pp = Q_3 = diag(W_k) is diagonal, so
+         H_z = H_zz − H_zp diag(W)⁻¹ H_pz exactly (z = [Y-rows; t]);
+      2. translations, with t_0 = 0 (anchoring P:137, C2): K̄ = K[1:,1:],
+         L = chol(K̄), G = L⁻¹C̄, Q = S − GᵀG   (= S − C̄ᵀ K̄⁻¹ C̄).
+    Equivalent to App. A's Q := AᵀQ_tpA + V_tpA + AᵀV_tpᵀ + Q_1 with
+    the sign of A corrected (reading C1); the SPEC's principal-submatrix
+    choice.  Raises EDISCONNECTED if K̄ is not positive definite.
+    """
+    if validate_input:
+        frame, landmark, pts, w, _ = validate(N, M, frame, landmark, pts, w)
+    else:
+        frame = np.asarray(frame, np.int64)
+        landmark = np.asarray(landmark, np.int64)
+        pts = np.asarray(pts, np.float64).reshape(-1, 3)
+        w = np.ones(len(frame)) if w is None else np.asarray(w, np.float64)
+    n = 3 * N
+    H = quadratic_form(N, M, frame, landmark, pts, w)
+    nz = n + N
+    Hzz = H[:nz, :nz]
+    Hzp = H[:nz, nz:]
+    Hpp = H[nz:, nz:]
+    W = np.asarray(Hpp.diagonal()).copy()
+    off = Hpp - sp.diags(W)
+    assert off.nnz == 0 or np.abs(off.data).max() == 0.0, "H_pp must be diagonal"
+    Winv = np.zeros(M)
+    obs = W > 0
+    Winv[obs] = 1.0 / W[obs]                    # unobserved landmarks: no term
+    Hz = (Hzz - Hzp @ sp.diags(Winv) @ Hzp.T).toarray()
+    S = Hz[:n, :n].copy()
+    C = Hz[n:, :n].copy()
+    K = Hz[n:, n:].copy()
+    if N == 1:
+        L = np.zeros((0, 0))
+        G = np.zeros((0, n))
+        Q = S.copy()
+    else:
+        Kb = K[1:, 1:]
+        try:
+            L = np.linalg.cholesky(Kb)
+        except np.linalg.LinAlgError:
+            raise OracleError("EDISCONNECTED", "graph numerically disconnected")
+        if np.min(np.diag(L)) <= 1e-12 * math.sqrt(max(np.max(np.abs(np.diag(Kb))), 1e-300)):
+            raise OracleError("EDISCONNECTED", "graph numerically disconnected")
+        G = sla.solve_triangular(L, C[1:, :], lower=True)
+        Q = S - G.T @ G
+    Q = 0.5 * (Q + Q.T)
+    return DataMatrix(Q=Q, S=S, C=C, K=K, L=L, G=G, W=W, frame=frame, landmark=landmark,
+                      pts=pts, w=w, N=N, M=M)
+
+
+# =============================================================================
+# Manifold calculus  (Prop. 4/5 P:360-374; C4, C5)
+# =============================================================================
+
+def sym(A):
+    """sym(A) = (A + Aᵀ)/2 on the trailing 3×3 axes."""
+    return 0.5 * (A + np.swapaxes(A, -1, -2))
+
+
+def sym0(A):
+    """sym₀(A) = sym(A) − (tr A / 3) I₃ (traceless symmetric part)."""
+    S = sym(A)
+    tr = np.trace(S, axis1=-2, axis2=-1)
+    return S - (tr / 3.0)[..., None, None] * np.eye(3)
+
+
+def blocks(Y):
+    """View Y (n×r) as N blocks Y_i ∈ ℝ^{3×r}."""
+    n, r = Y.shape
+    return Y.reshape(n // 3, 3, r)
+
+
+def alphas(Y):
+    """α_i = ‖Y_i‖_F² / 3 = s_i² (Y_iY_iᵀ = α_i I₃ on the manifold)."""
+    B = blocks(Y)
+    return np.einsum("ijk,ijk->i", B, B) / 3.0
+
+
+def multipliers(Y, QY):
+    """Λ_i: least-squares solution of (QY)_i = Λ_i Y_i over the constraint
+    span of block i (Thm 1 Eq. (18); App. A.4).
+
+    Block 0 (six constraints X_00 = I₃):  Λ_0 = sym((QY)_0 Y_0ᵀ)      (Y_0Y_0ᵀ = I)
+    Block i ≥ 1 (B¹..B⁵ = traceless symmetric): Λ_i = sym₀((QY)_i Y_iᵀ)/α_i.
+    Returns (N, 3, 3)."""
+    B = blocks(Y)
+    G = blocks(QY)
+    GYt = np.einsum("iar,ibr->iab", G, B)
+    Lam = sym0(GYt) / alphas(Y)[:, None, None]
+    Lam[0] = sym(GYt[0])
+    return Lam
+
+
+def project(Y, V):
+    """Orthogonal (Frobenius) projection onto the tangent space at Y (C4):
+    P_i(W) = W − sym₀(W Y_iᵀ) Y_i / α_i   (i ≥ 1: scale × Stiefel),
+    P_0(W) = W − sym(W Y_0ᵀ) Y_0          (anchor: Stiefel)."""
+    B = blocks(Y)
+    W = blocks(V)
+    WYt = np.einsum("iar,ibr->iab", W, B)
+    Lam = sym0(WYt) / alphas(Y)[:, None, None]
+    Lam[0] = sym(WYt[0])
+    out = W - np.einsum("iab,ibr->iar", Lam, B)
+    return out.reshape(V.shape)
+
+
+def block_apply(Lam, V):
+    """blkdiag(Λ) V."""
+    return np.einsum("iab,ibr->iar", Lam, blocks(V)).reshape(V.shape)
+
+
+def cost(Q, Y):
+    """f(Y) = tr(Q U Uᵀ)… = tr(Yᵀ Q Y) = ⟨Y, QY⟩ (Eq. (17)/(23) objective)."""
+    return float(np.vdot(Y, Q @ Y))
+
+
+def rgrad(Y, QY):
+    """Riemannian gradient = P(2QY) = 2(QY − blkdiag(Λ)Y) = 2 Z(y)Y (C5)."""
+    Lam = multipliers(Y, QY)
+    return 2.0 * (QY - block_apply(Lam, Y)), Lam
+
+
+def hess(Q, Y, Lam, V):
+    """Riemannian Hessian (analytic HVP; reading C5):
+    Hess[V] = P(2QV − 2 blkdiag(Λ) V)."""
+    return project(Y, 2.0 * (Q @ V) - 2.0 * block_apply(Lam, V))
+
+
+def _gram_schmidt_rows(Mx):
+    """Modified Gram–Schmidt on the 3 rows of each 3×r block (P:522
+    "Gram-Schmidt process on every batch of 3×r matrices"); positive diagonal
+    by construction.  Zero pivot → ERETRACT (C20)."""
+    out = np.empty_like(Mx)
+    for i in range(Mx.shape[0]):
+        A = Mx[i].copy()
+        scale = np.linalg.norm(A)
+        for a in range(3):
+            v = A[a].copy()
+            for b in range(a):
+                v -= np.dot(v, out[i, b]) * out[i, b]
+            nv = np.linalg.norm(v)
+            if not (nv > 1e-14 * scale):
+                raise OracleError("ERETRACT", "retraction failure (zero pivot)")
+            out[i, a] = v / nv
+    return out
+
+
+def retract(Y, V, c_floor=1e-3):
+    """Retraction on (ℝ₊ × St(r,3))^{N−1} × St(r,3) (readings C6, C7).
+
+    Block i ≥ 1, with s = √α_i, R̂ = Y_i/s:
+        δ_s = ⟨V_i, R̂⟩/3,  W = V_i − δ_s R̂,
+        s′ = max(s + δ_s, c_f s),  R̂′ = GS(R̂ + W/s),  Y_i′ = s′ R̂′.
+    Anchor: Y_0′ = GS(Y_0 + V_0)."""
+    B = blocks(Y)
+    Vb = blocks(V)
+    a = alphas(Y)
+    s = np.sqrt(a)
+    Rh = B / s[:, None, None]
+    ds = np.einsum("iar,iar->i", Vb, Rh) / 3.0
+    Wt = Vb - ds[:, None, None] * Rh
+    s_new = np.maximum(s + ds, c_floor * s)
+    Mx = Rh + Wt / s[:, None, None]
+    Mx[0] = B[0] + Vb[0]
+    s_new[0] = 1.0
+    Rn = _gram_schmidt_rows(Mx)
+    return (s_new[:, None, None] * Rn).reshape(Y.shape)
+
+
+# =============================================================================
+# O5  truncated CG (Steihaug–Toint)   (C8)
+# =============================================================================
+
+def tcg(hvp, Y, g, Delta, kappa=0.1, theta=1.0, max_inner=500):
+    """Steihaug–Toint tCG in Manopt's form (no preconditioner).
+
+    Returns (eta, Heta, n_hvp, stop) with stop ∈ {'negcurv', 'exceeded',
+    'converged', 'maxinner'}."""
+    eta = np.zeros_like(g)
+    Heta = np.zeros_like(g)
+    r = g.copy()
+    z = float(np.vdot(r, r))
+    r0 = math.sqrt(z)
+    delta = -r
+    e_Pe = 0.0
+    e_Pd = 0.0
+    d_Pd = z
+    n_hvp = 0
+    stop = "maxinner"
+    for _ in range(max_inner):
+        Hd = hvp(delta)
+        n_hvp += 1
+        d_Hd = float(np.vdot(delta, Hd))
+        alpha = z / d_Hd if d_Hd != 0.0 else math.inf
+        e_Pe_new = e_Pe + 2.0 * alpha * e_Pd + alpha * alpha * d_Pd
+        if d_Hd <= 0.0 or e_Pe_new >= Delta * Delta:
+            tau = (-e_Pd + math.sqrt(e_Pd * e_Pd + d_Pd * (Delta * Delta - e_Pe))) / d_Pd
+            eta = eta + tau * delta
+            Heta = Heta + tau * Hd
+            stop = "negcurv" if d_Hd <= 0.0 else "exceeded"
+            break
+        eta = eta + alpha * delta
+        Heta = Heta + alpha * Hd
+        e_Pe = e_Pe_new
+        r = project(Y, r + alpha * Hd)
+        z_old = z
+        z = float(np.vdot(r, r))
+        if math.sqrt(z) <= r0 * min(r0 ** theta, kappa):
+            stop = "converged"
+            break
+        beta = z / z_old
+        delta = -r + beta * delta
+        e_Pd = beta * (e_Pd + alpha * d_Pd)
+        d_Pd = z + beta * beta * d_Pd
+    return eta, Heta, n_hvp, stop
+
+
+@dataclasses.dataclass
+class Options:
+    """Defaults: SURVEY §8(c) C7, C8, C11, C19."""
+    grad_tol: float = 1e-10          # relative to max(1, ‖Q‖_F)
+    delta0_coef: float = 0.1         # Δ₀ = 0.1·√(3N)
+    delta_max_mult: float = 10.0     # Δ̄ = 10 Δ₀
+    rho_prime: float = 0.1
+    tcg_kappa: float = 0.1
+    tcg_theta: float = 1.0
+    tcg_max_inner: int = 500
+    max_outer: int = 5000
+    scale_floor: float = 1e-3
+    refresh_every: int = 50          # fresh QY every 50 accepted steps (C21)
+    eig_tol: float = 1e-8
+    cert_tol: float = 1e-6
+    lanczos_max: int = 3000
+    rank_cap: int = 10
+    seed: int = 0
+
+
+@dataclasses.dataclass
+class RTRResult:
+    Y: np.ndarray
+    QY: np.ndarray
+    f: float
+    grad_norm: float
+    converged: bool
+    outer: int
+    n_hvp: int
+    n_spmm: int
+
+
+def rtr(Q, Y0, opts: Options, normQ: Optional[float] = None) -> RTRResult:
+    """Riemannian trust region with tCG (Manopt structure; O4).
+
+    TR ratio with the cancellation-free Δf = 2⟨QY, D⟩ + ⟨D, QD⟩, D = Y′ − Y
+    (reading C21)."""
+    n = Q.shape[0]
+    N = n // 3
+    normQ = float(np.linalg.norm(Q)) if normQ is None else normQ
+    tol = opts.grad_tol * max(1.0, normQ)
+    Delta_bar = opts.delta_max_mult * opts.delta0_coef * math.sqrt(3 * N)
+    Delta = opts.delta0_coef * math.sqrt(3 * N)
+    Y = Y0.copy()
+    QY = Q @ Y
+    n_spmm = 1
+    g, Lam = rgrad(Y, QY)
+    f = float(np.vdot(Y, QY))
+    n_hvp = 0
+    accepts = 0
+    converged = False
+    it = 0
+    for it in range(opts.max_outer + 1):
+        gn = float(np.linalg.norm(g))
+        if gn <= tol:
+            converged = True
+            break
+        if it == opts.max_outer:
+            break
+
+        def hvp(V):
+            return hess(Q, Y, Lam, V)
+
+        eta, Heta, nh, stop = tcg(hvp, Y, g, Delta, opts.tcg_kappa, opts.tcg_theta,
+                                  opts.tcg_max_inner)
+        n_hvp += nh
+        n_spmm += nh
+        Yn = retract(Y, eta, opts.scale_floor)
+        D = Yn - Y
+        QD = Q @ D
+        n_spmm += 1
+        df = 2.0 * float(np.vdot(QY, D)) + float(np.vdot(D, QD))
+        model_dec = -float(np.vdot(g, eta)) - 0.5 * float(np.vdot(eta, Heta))
+        reg = max(1.0, abs(f)) * EPS * 1e3
+        rho = (-df + reg) / (model_dec + reg)
+        if not (rho >= 0.25) or math.isnan(rho):
+            Delta = Delta / 4.0
+        elif rho > 0.75 and stop in ("negcurv", "exceeded"):
+            Delta = min(2.0 * Delta, Delta_bar)
+        if rho > opts.rho_prime:
+            Y = Yn
+            accepts += 1
+            if accepts % opts.refresh_every == 0:
+                QY = Q @ Y
+                n_spmm += 1
+            else:
+                QY = QY + QD
+            f = float(np.vdot(Y, QY))
+            g, Lam = rgrad(Y, QY)
+    QY = Q @ Y                      # fresh before any certificate (O4)
+    n_spmm += 1
+    g, _ = rgrad(Y, QY)
+    return RTRResult(Y=Y, QY=QY, f=float(np.vdot(Y, QY)), grad_norm=float(np.linalg.norm(g)),
+                     converged=converged, outer=it, n_hvp=n_hvp, n_spmm=n_spmm)
+
+
+# =============================================================================
+# O6  Certificate: Λ, Z = Q − blkdiag(Λ), λ_min(Z)  (Alg. 1 l.9-12 P:396-402;
+#     Thm 1; C10, C11, C19)
+# =============================================================================
+
+def z_matrix(Q, Lam):
+    """Z(y) = Q − Σ y_i A_i = Q − blkdiag(Λ) (Eq. (16))."""
+    Z = Q.copy()
+    for i in range(Lam.shape[0]):
+        Z[3 * i:3 * i + 3, 3 * i:3 * i + 3] -= Lam[i]
+    return Z
+
+
+def dense_min_eig(Z):
+    """Brute force λ_min, v of a small symmetric Z (numpy eigh)."""
+    ev, V = np.linalg.eigh(Z)
+    v = V[:, 0]
+    j = int(np.argmax(np.abs(v)))
+    if v[j] < 0:
+        v = -v
+    return float(ev[0]), v
+
+
+def lanczos_min_eig(apply_Z, n, tol_abs, max_steps=3000, seed=0):
+    """Lanczos with full re-orthogonalisation (reading C19) for the
+    smallest eigenpair of a symmetric operator.  Start vector: the shared
+    counter-based generator (synth.scenes.splitmix64_uniform).
+
+    Stops when |β_k s_k| ≤ tol_abs for the smallest Ritz pair, or on
+    breakdown / max_steps.  Returns (λ_min, v, steps, residual)."""
+    from synth.scenes import splitmix64_uniform
+    q = splitmix64_uniform(seed, n)
+    q /= np.linalg.norm(q)
+    Vb = [q]
+    alphas_l, betas = [], []
+    lam, s_vec, res = math.nan, None, math.inf
+    k = 0
+    for k in range(1, min(max_steps, n) + 1):
+        w = apply_Z(Vb[-1])
+        a = float(np.dot(Vb[-1], w))
+        alphas_l.append(a)
+        Vm = np.array(Vb)
+        w = w - Vm.T @ (Vm @ w)          # full re-orthogonalisation (two passes)
+        w = w - Vm.T @ (Vm @ w)
+        b = float(np.linalg.norm(w))
+        if k > 1:   # smallest Ritz pair of the tridiagonal T_k (library eigensolver)
+            T_ev, T_vec = sla.eigh_tridiagonal(np.array(alphas_l), np.array(betas),
+                                               select="i", select_range=(0, 0))
+        else:
+            T_ev, T_vec = np.array([a]), np.array([[1.0]])
+        lam = float(T_ev[0])
+        s_vec = T_vec[:, 0]
+        res = abs(b * s_vec[-1])
+        if res <= tol_abs or b <= 1e-300 or k == n:
+            break
+        betas.append(b)
+        Vb.append(w / b)
+    Vm = np.array(Vb[:len(s_vec)])
+    v = Vm.T @ s_vec
+    v /= np.linalg.norm(v)
+    j = int(np.argmax(np.abs(v)))
+    if v[j] < 0:
+        v = -v
+    return lam, v, k, res
+
+
+@dataclasses.dataclass
+class Certificate:
+    lambda_min: float
+    v: np.ndarray
+    rho_dual: float        # b·y = tr Λ_0
+    Lam: np.ndarray
+    kkt_resid: float       # ‖Z Y‖_F
+    grad_norm: float
+    lanczos_steps: int
+    trace_X: float
+
+
+def certificate(Q, Y, opts: Options, QY=None, dense: bool = False, normQ=None) -> Certificate:
+    QY = Q @ Y if QY is None else QY
+    g, Lam = rgrad(Y, QY)
+    normQ = float(np.linalg.norm(Q)) if normQ is None else normQ
+    ZY = QY - block_apply(Lam, Y)
+    if dense:
+        lam, v = dense_min_eig(z_matrix(Q, Lam))
+        steps = 0
+    else:
+        def apply_Z(x):
+            X = x.reshape(-1, 1)
+            return (Q @ X - block_apply(Lam, X)).ravel()
+        lam, v, steps, _ = lanczos_min_eig(apply_Z, Q.shape[0],
+                                           opts.eig_tol * max(1.0, normQ),
+                                           opts.lanczos_max, opts.seed)
+    return Certificate(lambda_min=lam, v=v, rho_dual=float(np.trace(Lam[0])), Lam=Lam,
+                       kkt_resid=float(np.linalg.norm(ZY)), grad_norm=float(np.linalg.norm(g)),
+                       lanczos_steps=steps, trace_X=float(np.vdot(Y, Y)))
+
+
+# =============================================================================
+# O7  Riemannian staircase (Algorithm 1; Thm 2; C9)
+# =============================================================================
+
+def escape(Q, Y, QY, v, max_halvings=60, c_floor=1e-3):
+    """Y₊ = Retr_{[Y,0]}(α[0, v]) with α = 1, ½, … until f decreases
+    (Alg. 1 l.14-22; D = [0; vᵀ] is tangent at [Y, 0], Thm 2, reading C9).
+    Δf computed cancellation-free (C21).  Returns (Y₊, α, Δf)."""
+    n, r = Y.shape
+    Yz = np.concatenate([Y, np.zeros((n, 1))], axis=1)
+    QYz = np.concatenate([QY, np.zeros((n, 1))], axis=1)
+    Dir = np.zeros((n, r + 1))
+    Dir[:, r] = v
+    alpha = 1.0
+    for _ in range(max_halvings + 1):
+        Yp = retract(Yz, alpha * Dir, c_floor)
+        D = Yp - Yz
+        df = 2.0 * float(np.vdot(QYz, D)) + float(np.vdot(D, Q @ D))
+        if df < 0.0:
+            return Yp, alpha, df
+        alpha *= 0.5
+    raise OracleError("EESCAPE", "escape failed")
+
+
+@dataclasses.dataclass
+class StaircaseResult:
+    Y: np.ndarray
+    QY: np.ndarray
+    f: float
+    r: int
+    certified: bool
+    converged: bool
+    cert: Certificate
+    ranks: list
+    n_hvp: int
+    n_spmm: int
+    outer: int
+
+
+def staircase(dm_or_Q, opts: Options = None, Y0=None, r0=3, dense_cert=False) -> StaircaseResult:
+    """Algorithm 1: init U⁰ = [I₃,…,I₃] at r = 3 unless Y0 is given."""
+    opts = opts or Options()
+    Q = dm_or_Q.Q if isinstance(dm_or_Q, DataMatrix) else dm_or_Q
+    n = Q.shape[0]
+    N = n // 3
+    normQ = float(np.linalg.norm(Q))
+    if Y0 is None:
+        Y = np.zeros((n, r0))
+        for i in range(N):
+            Y[3 * i:3 * i + 3, 0:3] = np.eye(3)
+    else:
+        Y = np.array(Y0, dtype=np.float64)
+    ranks = [Y.shape[1]]
+    n_hvp = n_spmm = outer = 0
+    while True:
+        res = rtr(Q, Y, opts, normQ)
+        n_hvp += res.n_hvp
+        n_spmm += res.n_spmm
+        outer += res.outer
+        cert = certificate(Q, res.Y, opts, QY=res.QY, dense=dense_cert, normQ=normQ)
+        ok = cert.lambda_min >= -opts.cert_tol * max(1.0, normQ)
+        r = res.Y.shape[1]
+        if ok or not res.converged or r >= opts.rank_cap:
+            return StaircaseResult(Y=res.Y, QY=res.QY, f=res.f, r=r,
+                                   certified=bool(ok and res.converged),
+                                   converged=res.converged, cert=cert, ranks=ranks,
+                                   n_hvp=n_hvp, n_spmm=n_spmm, outer=outer)
+        Y, _, _ = escape(Q, res.Y, res.QY, cert.v, c_floor=opts.scale_floor)
+        ranks.append(Y.shape[1])
+
+
+# =============================================================================
+# O8  Rounding + recovery  (Eq. (4), Eq. (9) P:219-234;
+#     S:436-471; C16, C20)
+# =============================================================================
+
+def _polar(B):
+    U, sv, Vt = np.linalg.svd(B)
+    return U @ Vt, U, sv, Vt
+
+
+@dataclasses.dataclass
+class Solution:
+    R: np.ndarray       # (N,3,3) SO(3), camera→world (Eq. (3))
+    s: np.ndarray       # (N,)
+    t: np.ndarray       # (N,3)
+    p: np.ndarray       # (M,3)  (NaN for unobserved landmarks)
+    n_flipped: int
+    Yr: np.ndarray      # rounded, gauge-fixed factor (n×3) = Ūᵀ
+    rho_hat: float      # f(Yr) = tr(Q Ū ᵀŪ)
+    edge_objective: float  # Eq. (3) evaluated directly at (R, s, t, p)
+
+
+def round_recover(dm: DataMatrix, Y) -> Solution:
+    """Rounding: top-3 eigenvectors of X = YYᵀ via the r×r Gram YᵀY,
+    Y₃ = Y W₃; per block: s_i = ‖B_i‖_F/√3, polar → O(3); gauge fix
+    U* = R̄_0ᵀ Ū (Eq. (12)) with s_0 renormalised to 1 (C16);
+    det < 0 ⇒ nearest SO(3) (Eq. (9)).  Recovery (Eq. (4)):
+    T = −K̄⁻¹ C̄ Y₃ (t_0 = 0), p_k = Σ_{e∈k} w_e (Ū_i ũ_e + t_i)/W_k."""
+    N, M = dm.N, dm.M
+    n, r = Y.shape
+    ev, Wv = np.linalg.eigh(Y.T @ Y)
+    W3 = Wv[:, ::-1][:, :3] if r >= 3 else Wv
+    Y3 = Y @ W3
+    Ub = blocks(Y3).transpose(0, 2, 1)       # Ū_i = Y3_iᵀ (3×3)
+    O0, _, _, _ = _polar(Ub[0])
+    s0 = np.linalg.norm(Ub[0]) / math.sqrt(3.0)
+    if not s0 > 1e-12:
+        raise OracleError("EDEGENERATE", "degenerate block")
+    Ub = np.einsum("ba,ibc->iac", O0, Ub) / s0     # O0ᵀ Ū_i / s0
+    R = np.empty((N, 3, 3))
+    s = np.empty(N)
+    flips = 0
+    for i in range(N):
+        si = np.linalg.norm(Ub[i]) / math.sqrt(3.0)
+        if not si > 1e-12:
+            raise OracleError("EDEGENERATE", "degenerate block")
+        Ri, U, sv, Vt = _polar(Ub[i])
+        if np.linalg.det(Ri) < 0:
+            U = U.copy()
+            U[:, 2] = -U[:, 2]
+            Ri = U @ Vt
+            flips += 1
+        R[i], s[i] = Ri, si
+    R[0] = np.eye(3)
+    s[0] = 1.0
+    Ubar = s[:, None, None] * R
+    Yr = Ubar.transpose(0, 2, 1).reshape(n, 3)
+    # Eq. (4): translations, then landmarks
+    t = np.zeros((N, 3))
+    if N > 1:
+        t[1:] = -sla.cho_solve((dm.L, True), dm.C[1:, :] @ Yr)
+    x_e = np.einsum("eab,eb->ea", Ubar[dm.frame], dm.pts) + t[dm.frame]
+    p = np.full((M, 3), np.nan)
+    acc = np.zeros((M, 3))
+    np.add.at(acc, dm.landmark, dm.w[:, None] * x_e)
+    obs = dm.W > 0
+    p[obs] = acc[obs] / dm.W[obs, None]
+    resid = x_e - p[dm.landmark]
+    edge_obj = float(np.sum(dm.w * np.sum(resid * resid, axis=1)))
+    return Solution(R=R, s=s, t=t, p=p, n_flipped=flips, Yr=Yr,
+                    rho_hat=float(np.vdot(Yr, dm.Q @ Yr)), edge_objective=edge_obj)
+
+
+# =============================================================================
+# O9  Report: suboptimality   (Eq. (13); App. E; C10)
+# =============================================================================
+
+def suboptimality(rho_hat, rho_lower):
+    """η = (ρ̂ − ρ_lower)/(1 + |ρ̂| + |ρ_lower|)   (Eq. (13))."""
+    return (rho_hat - rho_lower) / (1.0 + abs(rho_hat) + abs(rho_lower))
+
+
+def report(cert: Certificate, rho_hat: float):
+    """ρ_lower = ρ_dual + min(0, λ_min)·tr X̂ (reading C10); η per Eq. (13);
+    η_E per App. E as printed (max(0, λ_min))."""
+    rho_lower = cert.rho_dual + min(0.0, cert.lambda_min) * cert.trace_X
+    lowE = max(0.0, cert.lambda_min) * cert.trace_X + cert.rho_dual
+    return dict(rho_lower=rho_lower, eta=suboptimality(rho_hat, rho_lower),
+                eta_E=(rho_hat - lowE) / (1.0 + abs(rho_hat) + abs(lowE)))
+
+
+def solve(scene_or_arrays, opts: Options = None, Y0=None, dense_cert=False):
+    """End to end: build Q → staircase → certificate → round/recover → report."""
+    s = scene_or_arrays
+    dm = build_Q(s.N, s.M, s.frame, s.landmark, s.pts, s.w)
+    st = staircase(dm, opts, Y0=Y0, dense_cert=dense_cert)
+    sol = round_recover(dm, st.Y)
+    rep = report(st.cert, sol.rho_hat)
+    return dm, st, sol, rep

@@ -1,0 +1,475 @@
+"""Pins for the CPU oracle (oracle/xm_oracle.py) against what the paper and the
+mathematics fix — never against the oracle's own formulas.
+
+Each test names the passage it pins.  Brute-force references here (dense least
+squares over (t, p), dense eigendecomposition, the paper's printed B¹..B⁵,
+Umeyama's closed form, finite differences) are independent of the oracle's
+Schur-complement / projection formulas, so a dropped term, a wrong sign or a
+transposed operand in the oracle fails one of them.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import xm_oracle as xo
+from synth.scenes import make_scene, random_factor, random_tangent_ambient
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def gt_factor(sc):
+    """Y_gt = [s_0R_0, …]ᵀ stacked: Y_i = (s_i R_i)ᵀ."""
+    return np.concatenate([(sc.s[i] * sc.R[i]).T for i in range(sc.N)], axis=0)
+
+
+def brute_marginal_objective(sc, Y):
+    """min_{t (t_0=0), p} Σ_e w_e‖Y_iᵀũ_e + t_i − p_k‖² by dense weighted least
+    squares, one coordinate at a time (Eq. (3) P:104-109 at fixed U; the
+    SPEC's marginal_objective_oracle S:151-159)."""
+    N, M = sc.N, sc.M
+    E = len(sc.frame)
+    r = Y.shape[1]
+    A = np.zeros((E, (N - 1) + M))
+    for e in range(E):
+        i, k = sc.frame[e], sc.landmark[e]
+        if i >= 1:
+            A[e, i - 1] = 1.0
+        A[e, (N - 1) + k] = -1.0
+    sw = np.sqrt(sc.w)
+    total = 0.0
+    for c in range(r):
+        b = np.array([Y[3 * sc.frame[e]:3 * sc.frame[e] + 3, c] @ sc.pts[e] for e in range(E)])
+        x, *_ = np.linalg.lstsq(sw[:, None] * A, -sw * b, rcond=None)
+        res = A @ x + b
+        total += float(np.sum(sc.w * res * res))
+    return total
+
+
+# ----------------------------------------------------------------------------- Q
+def test_golden_laplacian_two_frames_one_landmark():
+    g = GOLD["laplacian_2frames_1landmark"]
+    pts = np.array([[0.1, 0.2, 1.0], [0.3, -0.1, 2.0]])
+    H = xo.quadratic_form(2, 1, np.array([0, 1]), np.array([0, 0]), pts, np.ones(2)).toarray()
+    Qtp = H[6:, 6:]                                  # (t_0, t_1, p_0) block
+    np.testing.assert_array_equal(Qtp, np.array(g["Q_tp"], float))
+
+
+def test_golden_two_edges_one_frame_degree():
+    g = GOLD["two_edges_one_frame"]
+    pts = np.array([[0.1, 0.2, 1.0], [0.3, -0.1, 2.0]])
+    H = xo.quadratic_form(1, 2, np.array([0, 0]), np.array([0, 1]), pts, np.array(g["weights"])).toarray()
+    assert H[3, 3] == g["Q2"]                       # t_0 diagonal = weighted degree
+
+
+def test_laplacian_rows_sum_to_zero_and_degrees():
+    """Q_tp·1 = 0, diag(Q_2)=frame degrees, diag(Q_3)=landmark degrees."""
+    sc = make_scene(6, 40, "unordered", seed=3, vis_prob=0.5, weights="uniform")
+    H = xo.quadratic_form(sc.N, sc.M, sc.frame.astype(int), sc.landmark.astype(int), sc.pts, sc.w).toarray()
+    n = 3 * sc.N
+    Qtp = H[n:, n:]
+    assert np.abs(Qtp @ np.ones(sc.N + sc.M)).max() < 1e-12
+    np.testing.assert_allclose(np.diag(Qtp)[:sc.N], np.bincount(sc.frame, sc.w, sc.N), rtol=1e-15)
+    np.testing.assert_allclose(np.diag(Qtp)[sc.N:], np.bincount(sc.landmark, sc.w, sc.M), rtol=1e-15)
+    # single edge U-U block = w ũ ũᵀ
+    H1 = xo.quadratic_form(1, 1, np.array([0]), np.array([0]), np.array([[0.3, -0.2, 1.5]]), np.array([2.0])).toarray()
+    v = np.array([0.3, -0.2, 1.5])
+    np.testing.assert_allclose(H1[:3, :3], 2.0 * np.outer(v, v), rtol=1e-15)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_prop1_equivalence_brute_force(seed):
+    """Prop. 1, acceptance 1: tr(QUᵀU) = min_{t,p} Eq.(3)."""
+    rng = np.random.default_rng(seed)
+    N = int(rng.integers(2, 8))
+    M = int(rng.integers(5, 30))
+    sc = make_scene(N, M, "unordered", seed=seed, vis_prob=0.5, weights="uniform",
+                    sigma_d=0.1, sigma_u=0.01)
+    dm = xo.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+    for r in (3, 4, 5):
+        Y = random_factor(N, r, seed * 10 + r, anchor_identity=(r == 3))
+        f_q = float(np.vdot(Y, dm.Q @ Y))
+        f_b = brute_marginal_objective(sc, Y)
+        assert abs(f_q - f_b) <= 1e-9 * max(1.0, abs(f_b)), (r, f_q, f_b)
+
+
+def test_N1_gives_zero_Q():
+    """N = 1 ⇒ Q = 0."""
+    sc = make_scene(1, 7, "unordered", seed=0, vis_prob=1.0)
+    dm = xo.build_Q(1, 7, sc.frame, sc.landmark, sc.pts, sc.w)
+    assert np.abs(dm.Q).max() < 1e-13
+
+
+def test_noise_free_null_space_is_ground_truth():
+    """F1 / S:149: noise-free ⇒ Q ⪰ 0, 3-dim null space spanned by Y_gt, f(Y_gt)=0."""
+    sc = make_scene(12, 200, "unordered", seed=1, vis_prob=0.4)
+    dm = xo.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+    ev = np.linalg.eigvalsh(dm.Q)
+    nQ = dm.normF
+    assert ev[0] >= -1e-9 * nQ
+    assert np.all(np.abs(ev[:3]) <= 1e-10 * nQ) and ev[3] > 1e-3 * nQ
+    Yg = gt_factor(sc)
+    assert np.linalg.norm(dm.Q @ Yg) <= 1e-10 * nQ
+    # Q symmetric
+    assert np.abs(dm.Q - dm.Q.T).max() <= 1e-12 * nQ
+
+
+def test_anchor_independence_and_singletons():
+    """F2 (reading C2): grounding another translation gives the same Q;
+    F10: singleton landmarks do not change Q."""
+    sc = make_scene(5, 30, "unordered", seed=4, vis_prob=0.5, sigma_d=0.2, weights="uniform")
+    dm = xo.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+    H = xo.quadratic_form(sc.N, sc.M, sc.frame.astype(int), sc.landmark.astype(int), sc.pts, sc.w).toarray()
+    n = 3 * sc.N
+    for ground in (2, 4):
+        keep = [j for j in range(n, n + sc.N + sc.M) if j != n + ground]
+        Huu, Hux, Hxx = H[:n, :n], H[:n, keep], H[np.ix_(keep, keep)]
+        Qg = Huu - Hux @ np.linalg.solve(Hxx, Hux.T)
+        np.testing.assert_allclose(Qg, dm.Q, atol=1e-10 * dm.normF)
+    # add two singleton landmarks
+    fr = np.concatenate([sc.frame, [1, 3]])
+    lm = np.concatenate([sc.landmark, [sc.M, sc.M + 1]])
+    pts = np.concatenate([sc.pts, [[0.1, 0.2, 3.0], [-0.3, 0.1, 5.0]]])
+    w = np.concatenate([sc.w, [0.7, 0.9]])
+    dm2 = xo.build_Q(sc.N, sc.M + 2, fr, lm, pts, w)
+    np.testing.assert_allclose(dm2.Q, dm.Q, atol=1e-12 * dm.normF)
+
+
+def test_gauge_invariance():
+    """f(Y O) = f(Y) for orthogonal O (r×r)."""
+    sc = make_scene(6, 40, "unordered", seed=5, vis_prob=0.5, sigma_d=0.1)
+    dm = xo.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+    Y = random_factor(sc.N, 4, 2)
+    O, _ = np.linalg.qr(np.random.default_rng(0).standard_normal((4, 4)))
+    assert abs(xo.cost(dm.Q, Y @ O) - xo.cost(dm.Q, Y)) <= 1e-12 * abs(xo.cost(dm.Q, Y))
+
+
+def test_s_pattern_matches_numeric_structure():
+    """H3 pattern = nonzero 3×3 block structure of S (random weights ⇒ no
+    accidental cancellation)."""
+    sc = make_scene(15, 60, "loop", seed=2, window=4)
+    dm = xo.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+    rowptr, colidx = xo.s_pattern(sc.N, sc.frame, sc.landmark)
+    blk = np.abs(dm.S).reshape(sc.N, 3, sc.N, 3).max(axis=(1, 3)) > 0
+    for i in range(sc.N):
+        np.testing.assert_array_equal(colidx[rowptr[i]:rowptr[i + 1]], np.nonzero(blk[i])[0])
+    # Q itself is block-dense for a connected graph (F1)
+    qblk = np.abs(dm.Q).reshape(sc.N, 3, sc.N, 3).max(axis=(1, 3)) > 0
+    assert qblk.all()
+
+
+# --------------------------------------------------------------------- manifold
+@pytest.fixture(scope="module")
+def small_problem():
+    sc = make_scene(7, 60, "unordered", seed=11, vis_prob=0.5, sigma_d=0.2, sigma_u=0.01)
+    dm = xo.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+    return sc, dm
+
+
+@pytest.mark.parametrize("r", [3, 4, 5])
+def test_projection_properties(small_problem, r):
+    """Tangent space of {Y_0Y_0ᵀ = I, Y_iY_iᵀ = α_iI}: the derivative
+    of the constraints gives sym(V_0Y_0ᵀ) = 0, sym₀(V_iY_iᵀ) = 0; projection is
+    idempotent, self-adjoint, and the radial direction is kept."""
+    sc, dm = small_problem
+    Y = random_factor(sc.N, r, 7)
+    A = random_tangent_ambient(sc.N, r, 1)
+    B = random_tangent_ambient(sc.N, r, 2)
+    V = xo.project(Y, A)
+    for i in range(sc.N):
+        M_ = V[3 * i:3 * i + 3] @ Y[3 * i:3 * i + 3].T
+        Ms = 0.5 * (M_ + M_.T)
+        if i == 0:
+            assert np.abs(Ms).max() < 1e-12
+        else:
+            assert np.abs(Ms - np.trace(Ms) / 3 * np.eye(3)).max() < 1e-12
+        # normal component = (traceless) symmetric × Y_i
+        Nn = (A - V)[3 * i:3 * i + 3] @ Y[3 * i:3 * i + 3].T
+        assert np.abs(Nn - Nn.T).max() < 1e-10
+        if i > 0:
+            assert abs(np.trace(Nn)) < 1e-10
+    np.testing.assert_allclose(xo.project(Y, V), V, atol=1e-12)
+    assert abs(np.vdot(xo.project(Y, A), B) - np.vdot(A, xo.project(Y, B))) < 1e-10
+    PY = xo.project(Y, Y)
+    np.testing.assert_allclose(PY[3:], Y[3:], atol=1e-12)
+    assert np.abs(PY[:3]).max() < 1e-12
+
+
+def test_multipliers_match_paper_B_matrices(small_problem):
+    """Λ_i solves (QY)_i ≈ (Σ_ℓ y_ℓ B^ℓ) Y_i in least squares with the B¹..B⁵
+    printed in App. A.4 — 5 unknowns per block; anchor: 6."""
+    sc, dm = small_problem
+    Y = random_factor(sc.N, 4, 3)
+    QY = dm.Q @ Y
+    Lam = xo.multipliers(Y, QY)
+    Bs = [np.array([[1, 0, 0], [0, -1, 0], [0, 0, 0]]), np.array([[0, 0, 0], [0, 1, 0], [0, 0, -1]]),
+          np.array([[0, 1, 0], [1, 0, 0], [0, 0, 0]]), np.array([[0, 0, 1], [0, 0, 0], [1, 0, 0]]),
+          np.array([[0, 0, 0], [0, 0, 1], [0, 1, 0]])]
+    E6 = [np.diag([1.0, 0, 0]), np.diag([0, 1.0, 0]), np.diag([0, 0, 1.0])] + Bs[2:]
+    for i in range(sc.N):
+        Yi, Gi = Y[3 * i:3 * i + 3], QY[3 * i:3 * i + 3]
+        basis = E6 if i == 0 else Bs
+        Amat = np.stack([(Bl @ Yi).ravel() for Bl in basis], axis=1)
+        y, *_ = np.linalg.lstsq(Amat, Gi.ravel(), rcond=None)
+        Lref = sum(c * Bl for c, Bl in zip(y, basis))
+        np.testing.assert_allclose(Lam[i], Lref, atol=1e-9 * np.abs(Lref).max() + 1e-12)
+
+
+def test_licq_rank(small_problem):
+    """App. A.4 / S:406: {A_i Uᵀ} has rank m = 5N+1 at feasible points (N ≤ 6)."""
+    N = 5
+    Y = random_factor(N, 4, 9)
+    n = 3 * N
+    Bs = [np.array([[1, 0, 0], [0, -1, 0], [0, 0, 0]]), np.array([[0, 0, 0], [0, 1, 0], [0, 0, -1]]),
+          np.array([[0, 1, 0], [1, 0, 0], [0, 0, 0]]), np.array([[0, 0, 1], [0, 0, 0], [1, 0, 0]]),
+          np.array([[0, 0, 0], [0, 0, 1], [0, 1, 0]])]
+    E6 = [np.diag([1.0, 0, 0]), np.diag([0, 1.0, 0]), np.diag([0, 0, 1.0])] + Bs[2:]
+    cols = []
+    for i in range(N):
+        for Bl in (E6 if i == 0 else Bs):
+            A = np.zeros((n, n))
+            A[3 * i:3 * i + 3, 3 * i:3 * i + 3] = Bl
+            cols.append((A @ Y).ravel())
+    assert np.linalg.matrix_rank(np.stack(cols, 1)) == 5 * N + 1
+
+
+def test_retraction_properties(small_problem):
+    """step 0 ⇒ identity; feasibility; ‖R(hV) − (Y+hV)‖ = O(h²)."""
+    sc, _ = small_problem
+    Y = random_factor(sc.N, 5, 4)
+    V = xo.project(Y, random_tangent_ambient(sc.N, 5, 5))
+    np.testing.assert_allclose(xo.retract(Y, 0 * V), Y, atol=1e-14)
+    errs = []
+    for h in (1e-3, 5e-4, 2.5e-4, 1.25e-4):
+        Yh = xo.retract(Y, h * V)
+        errs.append(np.linalg.norm(Yh - (Y + h * V)))
+        B = xo.blocks(Yh)
+        G = np.einsum("iar,ibr->iab", B, B)
+        np.testing.assert_allclose(G[0], np.eye(3), atol=1e-12)
+        a = np.trace(G, axis1=1, axis2=2) / 3
+        assert np.abs(G - a[:, None, None] * np.eye(3)).max() < 1e-12
+    ratios = [errs[j] / errs[j + 1] for j in range(3)]
+    assert all(3.6 < q < 4.4 for q in ratios), ratios
+
+
+@pytest.mark.parametrize("r", [3, 4, 5])
+def test_gradient_finite_differences(small_problem, r):
+    """S:241, acceptance 4: d/dh f(R(hV)) at 0 = ⟨grad f, V⟩."""
+    sc, dm = small_problem
+    Y = random_factor(sc.N, r, 20 + r)
+    V = xo.project(Y, random_tangent_ambient(sc.N, r, 30 + r))
+    g, _ = xo.rgrad(Y, dm.Q @ Y)
+    h = 1e-5
+    fd = (xo.cost(dm.Q, xo.retract(Y, h * V)) - xo.cost(dm.Q, xo.retract(Y, -h * V))) / (2 * h)
+    assert abs(fd - np.vdot(g, V)) <= 1e-6 * max(1.0, abs(fd))
+    # Euclidean gradient 2QY vs FD of the ambient cost
+    A = random_tangent_ambient(sc.N, r, 40 + r)
+    fdE = (xo.cost(dm.Q, Y + h * A) - xo.cost(dm.Q, Y - h * A)) / (2 * h)
+    assert abs(fdE - np.vdot(2 * dm.Q @ Y, A)) <= 1e-6 * max(1.0, abs(fdE))
+
+
+@pytest.mark.parametrize("r", [3, 4, 5])
+def test_hessian_finite_differences_and_symmetry(small_problem, r):
+    """S:258-259, acceptance 4: Hess[V] = P_Y(D grad[V]) (FD of the smoothly
+    extended gradient), self-adjoint."""
+    sc, dm = small_problem
+    Y = random_factor(sc.N, r, 50 + r)
+    V = xo.project(Y, random_tangent_ambient(sc.N, r, 60 + r))
+    W = xo.project(Y, random_tangent_ambient(sc.N, r, 70 + r))
+    _, Lam = xo.rgrad(Y, dm.Q @ Y)
+    HV = xo.hess(dm.Q, Y, Lam, V)
+    h = 1e-6
+    gp, _ = xo.rgrad(Y + h * V, dm.Q @ (Y + h * V))
+    gm, _ = xo.rgrad(Y - h * V, dm.Q @ (Y - h * V))
+    fd = xo.project(Y, (gp - gm) / (2 * h))
+    assert np.linalg.norm(fd - HV) <= 1e-5 * np.linalg.norm(HV)
+    HW = xo.hess(dm.Q, Y, Lam, W)
+    assert abs(np.vdot(HV, W) - np.vdot(V, HW)) <= 1e-10 * np.linalg.norm(HV) * np.linalg.norm(W)
+
+
+# ------------------------------------------------------------------ certificate
+def test_golden_min_eig_diag():
+    g = GOLD["min_eig_diag"]
+    Z = np.diag(g["Z_diag"])
+    lam, v = xo.dense_min_eig(Z)
+    assert lam == g["lambda_min"]
+    np.testing.assert_allclose(v, g["v"], atol=0)
+    lam2, v2, _, _ = xo.lanczos_min_eig(lambda x: Z @ x, 3, 1e-12)
+    assert abs(lam2 - g["lambda_min"]) < 1e-12
+    np.testing.assert_allclose(np.abs(v2), g["v"], atol=1e-10)
+
+
+def test_lanczos_matches_dense_eig(small_problem):
+    sc, dm = small_problem
+    Y = random_factor(sc.N, 4, 13)
+    _, Lam = xo.rgrad(Y, dm.Q @ Y)
+    Z = xo.z_matrix(dm.Q, Lam)
+    lam_d = np.linalg.eigvalsh(Z)[0]
+    lam_l, v, k, res = xo.lanczos_min_eig(lambda x: Z @ x, Z.shape[0], 1e-10 * dm.normF)
+    assert abs(lam_l - lam_d) <= 1e-9 * dm.normF
+    assert np.linalg.norm(Z @ v - lam_l * v) <= 1e-8 * dm.normF
+
+
+def test_golden_suboptimality_and_bound():
+    for c in GOLD["suboptimality"]["cases"]:
+        assert xo.suboptimality(c["rho_hat"], c["rho_lower"]) == c["eta"]
+    for c in GOLD["rigorous_lower_bound"]["cases"]:
+        cert = xo.Certificate(lambda_min=c["lambda_min"], v=None, rho_dual=c["rho_dual"], Lam=None,
+                              kkt_resid=0, grad_norm=0, lanczos_steps=0, trace_X=c["trace_X"])
+        rep = xo.report(cert, 0.0)
+        lowE = max(0.0, c["lambda_min"]) * c["trace_X"] + c["rho_dual"]
+        assert lowE == c["lower"]
+        assert abs(rep["eta_E"] - (0.0 - lowE) / (1 + abs(lowE))) < 1e-15
+
+
+# ------------------------------------------------------------------ staircase
+def test_noise_free_tight_certified_and_gt_recovered():
+    """Acceptance 2: noise-free ⇒ certified at
+    r=3, f≈0, λ_min ≥ −1e-6‖Q‖, η ≤ 1e-6, recovered poses = GT, no flips."""
+    sc = make_scene(20, 100, "unordered", seed=2, vis_prob=0.4)
+    dm, st, sol, rep = xo.solve(sc)
+    nQ = dm.normF
+    assert st.certified and st.r == 3
+    assert abs(st.f) <= 1e-10 * nQ
+    assert st.cert.lambda_min >= -1e-6 * nQ
+    assert rep["eta"] <= 1e-6
+    np.testing.assert_allclose(sol.s, sc.s, atol=1e-8)
+    np.testing.assert_allclose(sol.R, sc.R, atol=1e-8)
+    np.testing.assert_allclose(sol.t, sc.t, atol=1e-7)
+    np.testing.assert_allclose(sol.p, sc.p, atol=1e-7)
+    assert sol.n_flipped == 0
+    # KKT: ‖ZY‖ ≤ 1e-8‖Q‖; multipliers vanish; f = tr Λ₀ (F5)
+    assert st.cert.kkt_resid <= 1e-8 * nQ
+    assert np.abs(st.cert.Lam).max() <= 1e-8 * nQ
+    # Lanczos vs dense brute force on the same Z
+    lam_d, _ = xo.dense_min_eig(xo.z_matrix(dm.Q, st.cert.Lam))
+    assert abs(lam_d - st.cert.lambda_min) <= 1e-7 * nQ
+
+
+def test_noisy_kkt_identities():
+    """F5 / Thm 1: at a certified critical point f = tr Λ₀ = ρ_dual,
+    ⟨(QY)_i, Y_i⟩ ≈ 0 (i ≥ 1), ⟨V,HessV⟩ = 2⟨V,ZV⟩; edge objective (Eq. (3))
+    at the recovered solution = f(Ŷ) (Prop. 1)."""
+    sc = make_scene(8, 80, "unordered", seed=7, vis_prob=0.5, sigma_d=0.1, sigma_u=0.01, weights="uniform")
+    dm, st, sol, rep = xo.solve(sc)
+    nQ = dm.normF
+    assert st.certified
+    assert abs(st.f - st.cert.rho_dual) <= 1e-8 * max(1.0, abs(st.f))
+    B, G = xo.blocks(st.Y), xo.blocks(st.QY)
+    assert np.abs(np.einsum("iar,iar->i", B, G)[1:]).max() <= 1e-8 * nQ
+    V = xo.project(st.Y, random_tangent_ambient(sc.N, st.r, 3))
+    HV = xo.hess(dm.Q, st.Y, st.cert.Lam, V)
+    Z = xo.z_matrix(dm.Q, st.cert.Lam)
+    assert abs(np.vdot(V, HV) - 2 * np.vdot(V, Z @ V)) <= 1e-7 * abs(np.vdot(V, HV))
+    assert abs(sol.edge_objective - sol.rho_hat) <= 1e-8 * max(1.0, abs(sol.rho_hat))
+    assert rep["eta"] <= 1e-6
+
+
+def test_non_tight_instance_chain_inequality():
+    """Eq. (14): on a high-noise instance the relaxation is
+    not tight (rank 4 certified optimum, det flips); still ρ_lower ≤ ρ̂ and
+    η > 0, and the certified SDP value f ≤ ρ̂."""
+    sc = make_scene(8, 80, "unordered", seed=7, vis_prob=0.5, sigma_d=0.3, sigma_u=0.01, weights="uniform")
+    dm, st, sol, rep = xo.solve(sc)
+    assert st.certified and st.r == 4
+    assert rep["rho_lower"] <= sol.rho_hat + 1e-9 * (1 + abs(sol.rho_hat))
+    assert st.f <= sol.rho_hat and rep["eta"] > 1e-6
+
+
+def test_random_init_escalates_and_reaches_same_X():
+    """Thm 2/3, Fig. 8 behaviour, acceptance 7; F6: random
+    init at r=3 stalls at a spurious critical point, the escape along [0, v]
+    lifts to r=4 and the staircase certifies the same X as identity init."""
+    sc = make_scene(10, 500, "unordered", seed=0, vis_prob=0.6)
+    dm = xo.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+    st_id = xo.staircase(dm)
+    st_rd = xo.staircase(dm, Y0=random_factor(sc.N, 3, 1))
+    assert st_rd.ranks == [3, 4] and st_rd.certified
+    Xa = st_id.Y @ st_id.Y.T
+    Xb = st_rd.Y @ st_rd.Y.T
+    assert np.linalg.norm(Xa - Xb) <= 1e-8 * np.linalg.norm(Xa)
+
+
+def test_escape_direction_is_tangent_and_descends():
+    """Thm 2: D = [0, v] is tangent at [Y, 0]; line search lowers f."""
+    sc = make_scene(10, 500, "unordered", seed=0, vis_prob=0.6)
+    dm = xo.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+    opts = xo.Options(rank_cap=3)
+    st = xo.staircase(dm, opts, Y0=random_factor(sc.N, 3, 1))
+    assert st.cert.lambda_min < 0 and not st.certified
+    Yz = np.concatenate([st.Y, np.zeros((st.Y.shape[0], 1))], 1)
+    D = np.zeros_like(Yz)
+    D[:, 3] = st.cert.v
+    np.testing.assert_allclose(xo.project(Yz, D), D, atol=1e-12)
+    Yp, alpha, df = xo.escape(dm.Q, st.Y, st.QY, st.cert.v)
+    assert df < 0 and xo.cost(dm.Q, Yp) < st.f
+
+
+# -------------------------------------------------------------- N = 2 closed form
+def umeyama(x, y, c):
+    """Weighted similarity registration y ≈ sRx + t (Umeyama 1991)."""
+    cs = c / c.sum()
+    mx, my = cs @ x, cs @ y
+    xc, yc = x - mx, y - my
+    Sxy = (cs[:, None] * yc).T @ xc
+    U, D, Vt = np.linalg.svd(Sxy)
+    Sg = np.diag([1.0, 1.0, np.sign(np.linalg.det(U) * np.linalg.det(Vt))])
+    R = U @ Sg @ Vt
+    var = float(np.sum(cs * np.sum(xc * xc, 1)))
+    s = float(np.trace(np.diag(D) @ Sg)) / var
+    return s, R, my - s * R @ mx
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_two_frames_equal_umeyama(seed):
+    """Remark 1, acceptance 3: N = 2 SBA = scaled point cloud
+    registration; eliminating p_k gives weights c_k = w_0k w_1k/(w_0k + w_1k)."""
+    sc = make_scene(2, 40, "unordered", seed=seed, vis_prob=0.9, sigma_d=0.05, sigma_u=0.01,
+                    weights="uniform")
+    dm, st, sol, rep = xo.solve(sc)
+    assert st.certified
+    idx0 = {k: e for e, (i, k) in enumerate(zip(sc.frame, sc.landmark)) if i == 0}
+    idx1 = {k: e for e, (i, k) in enumerate(zip(sc.frame, sc.landmark)) if i == 1}
+    both = sorted(set(idx0) & set(idx1))
+    x = np.array([sc.pts[idx1[k]] for k in both])
+    y = np.array([sc.pts[idx0[k]] for k in both])
+    w0 = np.array([sc.w[idx0[k]] for k in both])
+    w1 = np.array([sc.w[idx1[k]] for k in both])
+    s, R, t = umeyama(x, y, w0 * w1 / (w0 + w1))
+    assert abs(sol.s[1] - s) <= 1e-8 * s
+    ang = math.atan2(np.linalg.norm(R.T @ sol.R[1] - sol.R[1].T @ R) / math.sqrt(2),
+                     np.trace(R.T @ sol.R[1]) - 1)
+    assert abs(ang) <= 1e-6
+    np.testing.assert_allclose(sol.t[1], t, atol=1e-7 * max(1.0, np.abs(t).max()))
+
+
+# ------------------------------------------------------------------ validation
+def test_validation_errors():
+    fr = np.array([0, 1, 0, 1])
+    lm = np.array([0, 0, 1, 1])
+    pts = np.array([[0.1, 0.1, 1.0]] * 4)
+    with pytest.raises(xo.OracleError) as e:
+        xo.validate(2, 2, np.array([0, 2, 0, 1]), lm, pts)
+    assert e.value.code == "EINVAL"
+    bad = pts.copy()
+    bad[2, 2] = -1.0
+    with pytest.raises(xo.OracleError):
+        xo.validate(2, 2, fr, lm, bad)
+    with pytest.raises(xo.OracleError):
+        xo.validate(2, 2, fr, lm, pts, np.array([1.0, 0.0, 1.0, 1.0]))
+    nan = pts.copy()
+    nan[0, 0] = np.nan
+    with pytest.raises(xo.OracleError):
+        xo.validate(2, 2, fr, lm, nan)
+    # disconnected: two frames, private landmarks
+    with pytest.raises(xo.OracleError) as e:
+        xo.validate(2, 2, np.array([0, 1]), np.array([0, 1]), pts[:2])
+    assert e.value.code == "EDISCONNECTED"
+    # duplicates: keep first
+    f2 = np.array([0, 1, 0, 1, 0])
+    l2 = np.array([0, 0, 1, 1, 0])
+    p2 = np.concatenate([pts, [[9.0, 9.0, 9.0]]])
+    out = xo.validate(2, 2, f2, l2, p2)
+    assert out[4] == 1 and len(out[0]) == 4 and not np.any(out[2][:, 0] == 9.0)
