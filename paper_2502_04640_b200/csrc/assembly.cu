@@ -1,0 +1,804 @@
+// assembly.cu — SURVEY §8(a) rows H1–H5 on the device.
+//
+//  H1 validate + de-duplicate (keep first duplicate)
+//  H2 sort edges by (landmark, frame) and (frame, landmark), track stats W_k
+//     (Q_3 = diag(W_k), App. A)
+//  H3 co-visibility pattern of S (BSR rowptr / colidx, bit-exact contract)
+//  H4 landmark elimination: row-owned clique scatter into dense S, C, K
+//       H_(i,j) = Σ_k [δ_ij w_e a_e a_eᵀ − (w_e w_f / W_k) a_e a_fᵀ],  a = [ũ; 1]
+//     (the expanded quadratic form of App. A P:1162-1189 with p eliminated)
+//  H5 translation elimination with t_0 = 0: K̄ = L Lᵀ, G = L⁻¹ C̄,
+//     Q = S − Gᵀ G  (Prop. 1 Q, P:1249 with the sign reading C1)
+//
+// Everything is deterministic: sorts are stable, every dense entry is owned by
+// one CTA that accumulates landmarks in ascending order.
+#include "xm_internal.cuh"
+
+#include <cmath>
+
+namespace xm {
+
+// =============================================================== H1 validate
+enum { ERR_RANGE = 1, ERR_WEIGHT = 2, ERR_POINT = 4 };
+
+__global__ void k_validate(int64_t E, int N, int M, const int32_t* __restrict__ fr,
+                           const int32_t* __restrict__ lm, const double* __restrict__ pts,
+                           const double* __restrict__ w, int* __restrict__ err,
+                           uint64_t* __restrict__ key, uint32_t* __restrict__ val) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  int f = fr[e], k = lm[e];
+  int bad = 0;
+  if (f < 0 || f >= N || k < 0 || k >= M) bad |= ERR_RANGE;
+  double we = w ? w[e] : 1.0;
+  if (!(we > 0.0) || !isfinite(we)) bad |= ERR_WEIGHT;
+  double x = pts[3 * e], y = pts[3 * e + 1], z = pts[3 * e + 2];
+  if (!isfinite(x) || !isfinite(y) || !isfinite(z) || !(z > 0.0)) bad |= ERR_POINT;
+  if (bad) atomicOr(err, bad);
+  key[e] = bad ? 0ull : (uint64_t)f * (uint64_t)M + (uint64_t)k;  // (frame, landmark) order
+  val[e] = (uint32_t)e;
+}
+
+__global__ void k_first_flags(const uint64_t* __restrict__ key, int64_t n, int32_t* __restrict__ flag) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  flag[j] = (j == 0 || key[j] != key[j - 1]) ? 1 : 0;
+}
+
+// kept frame-sorted items → (landmark, frame) keys for the second sort
+__global__ void k_compact_fs(const uint64_t* __restrict__ key, const uint32_t* __restrict__ val,
+                             const int32_t* __restrict__ flag, const int32_t* __restrict__ pos,
+                             int64_t n, int M, int N, int32_t* __restrict__ fs_in,
+                             int32_t* __restrict__ fs_fr, uint64_t* __restrict__ key2,
+                             uint32_t* __restrict__ val2) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n || !flag[j]) return;
+  int p = pos[j];
+  uint64_t k = key[j];
+  int f = (int)(k / (uint64_t)M), l = (int)(k % (uint64_t)M);
+  fs_in[p] = (int32_t)val[j];
+  fs_fr[p] = f;
+  key2[p] = (uint64_t)l * (uint64_t)N + (uint64_t)f;
+  val2[p] = (uint32_t)p;
+}
+
+// canonical (landmark-major) edge arrays + inverse map frame-sorted → canonical
+__global__ void k_gather_edges(int64_t E, const uint64_t* __restrict__ key2,
+                               const uint32_t* __restrict__ val2, const int32_t* __restrict__ fs_in,
+                               int N, const double* __restrict__ pts, const double* __restrict__ w,
+                               int32_t* __restrict__ e_fr, int32_t* __restrict__ e_lm,
+                               double* __restrict__ e_pts, double* __restrict__ e_w,
+                               int32_t* __restrict__ fr_edge) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= E) return;
+  uint64_t k = key2[c];
+  int j = (int)val2[c];
+  int ein = fs_in[j];
+  e_lm[c] = (int)(k / (uint64_t)N);
+  e_fr[c] = (int)(k % (uint64_t)N);
+  e_pts[3 * c] = pts[3 * (int64_t)ein];
+  e_pts[3 * c + 1] = pts[3 * (int64_t)ein + 1];
+  e_pts[3 * c + 2] = pts[3 * (int64_t)ein + 2];
+  e_w[c] = w ? w[ein] : 1.0;
+  fr_edge[j] = (int32_t)c;
+}
+
+__global__ void k_histogram(const int32_t* __restrict__ idx, int64_t n, int32_t* __restrict__ cnt) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < n) atomicAdd(&cnt[idx[j]], 1);
+}
+
+// W_k = Σ_{e ∈ track k} w_e, sequential per landmark (deterministic)
+__global__ void k_track_weight(int M, const int32_t* __restrict__ off, const double* __restrict__ w,
+                               double* __restrict__ W) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= M) return;
+  double s = 0.0;
+  for (int e = off[k]; e < off[k + 1]; ++e) s += w[e];
+  W[k] = s;
+}
+
+// ------------------------------------------------ connectivity (min-label + jumping)
+__global__ void k_cc_init(int n, int32_t* parent) {
+  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < n) parent[v] = v;
+}
+__global__ void k_cc_hook(int64_t E, int N, const int32_t* __restrict__ fr,
+                          const int32_t* __restrict__ lm, int32_t* parent, int* changed) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  int a = parent[fr[e]], b = parent[N + lm[e]];
+  if (a != b) {
+    int hi = a > b ? a : b, lo = a > b ? b : a;
+    atomicMin(&parent[hi], lo);
+    *changed = 1;
+  }
+}
+__global__ void k_cc_jump(int n, int32_t* parent) {
+  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  int p = parent[v];
+  while (p != parent[p]) p = parent[p];
+  parent[v] = p;
+}
+__global__ void k_cc_count(int N, int M, const int32_t* __restrict__ parent,
+                           const int32_t* __restrict__ lm_off, const int32_t* __restrict__ fr_cnt,
+                           int* out) {
+  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= N + M) return;
+  bool present = v < N ? (fr_cnt[v] > 0) : (lm_off[v - N + 1] > lm_off[v - N]);
+  if (v < N && fr_cnt[v] == 0) atomicAdd(&out[1], 1);  // unobserved frame
+  if (present && parent[v] == v) atomicAdd(&out[0], 1);
+}
+
+// ============================================================ H3 S pattern
+__global__ void k_pattern_bits(int N, int W32, const int32_t* __restrict__ fr_off,
+                               const int32_t* __restrict__ fr_edge, const int32_t* __restrict__ e_lm,
+                               const int32_t* __restrict__ lm_off, const int32_t* __restrict__ e_fr,
+                               unsigned* __restrict__ bits) {
+  int i = blockIdx.x;
+  unsigned* row = bits + (int64_t)i * W32;
+  if (threadIdx.x == 0) atomicOr(&row[i >> 5], 1u << (i & 31));
+  for (int j = fr_off[i]; j < fr_off[i + 1]; ++j) {
+    int k = e_lm[fr_edge[j]];
+    for (int f = lm_off[k] + threadIdx.x; f < lm_off[k + 1]; f += blockDim.x) {
+      int jf = e_fr[f];
+      atomicOr(&row[jf >> 5], 1u << (jf & 31));
+    }
+  }
+}
+__global__ void k_pattern_count(int N, int W32, const unsigned* __restrict__ bits,
+                                int32_t* __restrict__ cnt) {
+  int i = blockIdx.x;
+  int s = 0;
+  for (int w = threadIdx.x; w < W32; w += blockDim.x) s += __popc(bits[(int64_t)i * W32 + w]);
+  __shared__ int sh[256];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) cnt[i] = sh[0];
+}
+// one warp per row: enumerate set bits in ascending column order
+__global__ void k_pattern_cols(int N, int W32, const unsigned* __restrict__ bits,
+                               const int32_t* __restrict__ off32, int32_t* __restrict__ colidx,
+                               int64_t* __restrict__ rowptr) {
+  int i = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  int lane = threadIdx.x & 31;
+  if (i >= N) return;
+  int base = off32[i];
+  if (lane == 0) rowptr[i] = base;
+  for (int w0 = 0; w0 < W32; w0 += 32) {
+    int w = w0 + lane;
+    unsigned b = (w < W32) ? bits[(int64_t)i * W32 + w] : 0u;
+    int c = __popc(b);
+    int incl = c;
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    int pos = base + incl - c;
+    while (b) {
+      int bit = __ffs(b) - 1;
+      colidx[pos++] = w * 32 + bit;
+      b &= b - 1;
+    }
+    base += __shfl_sync(0xffffffffu, incl, 31);
+  }
+}
+
+// ============================================================ H4 clique scatter
+// CTA i owns: S rows 3i..3i+2 (if i is this rank's frame), C̄ row i−1 (t_i),
+// K̄ row i−1.  For each landmark k of frame i (ascending k) the threads update
+// H_(i, j_f) for every f in track(k); a __syncthreads between landmarks makes
+// the accumulation order fixed.
+__global__ void __launch_bounds__(128) k_clique_scatter(
+    int N, int f0, int f1, const int32_t* __restrict__ fr_off, const int32_t* __restrict__ fr_edge,
+    const int32_t* __restrict__ lm_off, const int32_t* __restrict__ e_fr,
+    const double* __restrict__ e_pts, const double* __restrict__ e_w, const double* __restrict__ W,
+    const int32_t* __restrict__ e_lm, double* __restrict__ S, int64_t ldq, int row0,
+    double* __restrict__ Cb, double* __restrict__ Kb, int64_t ldk) {
+  const int i = blockIdx.x;
+  const bool own = (i >= f0 && i < f1);
+  for (int j = fr_off[i]; j < fr_off[i + 1]; ++j) {
+    const int e = fr_edge[j];
+    const int k = e_lm[e];
+    const double ae0 = e_pts[3 * e], ae1 = e_pts[3 * e + 1], ae2 = e_pts[3 * e + 2];
+    const double we = e_w[e];
+    const double coef = we / W[k];
+    for (int f = lm_off[k] + threadIdx.x; f < lm_off[k + 1]; f += blockDim.x) {
+      const int jf = e_fr[f];
+      const double af[4] = {e_pts[3 * f], e_pts[3 * f + 1], e_pts[3 * f + 2], 1.0};
+      const double ae[4] = {ae0, ae1, ae2, 1.0};
+      const double cf = coef * e_w[f];
+      double h[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) h[a][b] = -cf * ae[a] * af[b];
+      if (f == e) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) h[a][b] += we * ae[a] * ae[b];
+      }
+      if (own) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          double* rowp = S + (int64_t)(3 * i + a - row0) * ldq + 3 * jf;
+#pragma unroll
+          for (int b = 0; b < 3; ++b) rowp[b] += h[a][b];
+        }
+      }
+      if (i >= 1) {
+        double* crow = Cb + (int64_t)(i - 1) * ldq + 3 * jf;
+#pragma unroll
+        for (int b = 0; b < 3; ++b) crow[b] += h[3][b];
+        if (jf >= 1) Kb[(int64_t)(i - 1) * ldk + (jf - 1)] += h[3][3];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ============================================================ dense fp64 kernels
+// GEMM:  C = beta·C + alpha·op(A)·op(B), op(A) M×K, op(B) K×N, row-major storage.
+//   TA: A stored K×M (op = transpose); TB: B stored N×K.
+//   LOWER: only tiles with tile_col ≤ tile_row (BM == BN) are computed.
+// 64×64 tile, BK = 16, 256 threads, each thread a 4×4 strided micro-tile
+// (rows ty + 16·a, cols tx + 16·b ⇒ conflict-free smem reads with broadcast).
+constexpr int GB = 64, GK = 16;
+
+template <bool TA, bool TB, bool LOWER>
+__global__ void __launch_bounds__(256) k_dgemm(int M, int N, int K, double alpha,
+                                               const double* __restrict__ A, int64_t lda,
+                                               const double* __restrict__ B, int64_t ldb,
+                                               double beta, double* __restrict__ C, int64_t ldc) {
+  const int bm = blockIdx.y, bn = blockIdx.x;
+  if (LOWER && bn > bm) return;
+  __shared__ double As[2][GK][GB + 2];
+  __shared__ double Bs[2][GK][GB + 2];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int m0 = bm * GB, n0 = bn * GB;
+  double acc[4][4] = {};
+  double ra[4], rb[4];
+  auto load_a = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int lin = tid + q * 256;  // 0..1023 over 64×16
+      int mm, kk;
+      if (TA) { mm = lin & 63; kk = lin >> 6; }   // A[k][m]: contiguous in m
+      else    { kk = lin & 15; mm = lin >> 4; }   // A[m][k]: contiguous in k
+      int gm = m0 + mm, gk = k0 + kk;
+      double v = 0.0;
+      if (gm < M && gk < K) v = TA ? A[(int64_t)gk * lda + gm] : A[(int64_t)gm * lda + gk];
+      ra[q] = v;
+    }
+  };
+  auto load_b = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int lin = tid + q * 256;
+      int nn, kk;
+      if (!TB) { nn = lin & 63; kk = lin >> 6; }  // B[k][n]: contiguous in n
+      else     { kk = lin & 15; nn = lin >> 4; }  // B[n][k]: contiguous in k
+      int gn = n0 + nn, gk = k0 + kk;
+      double v = 0.0;
+      if (gn < N && gk < K) v = TB ? B[(int64_t)gn * ldb + gk] : B[(int64_t)gk * ldb + gn];
+      rb[q] = v;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int lin = tid + q * 256;
+      int mm, kk;
+      if (TA) { mm = lin & 63; kk = lin >> 6; } else { kk = lin & 15; mm = lin >> 4; }
+      As[buf][kk][mm] = ra[q];
+      int nn, k2;
+      if (!TB) { nn = lin & 63; k2 = lin >> 6; } else { k2 = lin & 15; nn = lin >> 4; }
+      Bs[buf][k2][nn] = rb[q];
+    }
+  };
+  int nk = (K + GK - 1) / GK;
+  if (nk > 0) {
+    load_a(0);
+    load_b(0);
+    store(0);
+  }
+  __syncthreads();
+  for (int t = 0; t < nk; ++t) {
+    int cur = t & 1;
+    if (t + 1 < nk) {
+      load_a((t + 1) * GK);
+      load_b((t + 1) * GK);
+    }
+#pragma unroll
+    for (int kk = 0; kk < GK; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) a[q] = As[cur][kk][ty + 16 * q];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) b[q] = Bs[cur][kk][tx + 16 * q];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
+    }
+    if (t + 1 < nk) store(cur ^ 1);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    int gm = m0 + ty + 16 * x;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      int gn = n0 + tx + 16 * y;
+      if (gn >= N) continue;
+      double* cp = C + (int64_t)gm * ldc + gn;
+      *cp = (beta == 0.0 ? 0.0 : beta * *cp) + alpha * acc[x][y];
+    }
+  }
+}
+
+void dgemm(xm_ctx* c, bool ta, bool tb, bool lower, int M, int N, int K, double alpha,
+           const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+           int64_t ldc) {
+  if (M <= 0 || N <= 0) return;
+  dim3 grid(ceil_div(N, GB), ceil_div(M, GB));
+#define XM_GEMM_CASE(a_, b_, l_)                                                            \
+  if (ta == a_ && tb == b_ && lower == l_) {                                                \
+    k_dgemm<a_, b_, l_><<<grid, 256, 0, c->stream>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, \
+                                                     ldc);                                   \
+    XM_CHECK_LAUNCH();                                                                       \
+    count_launch(c);                                                                         \
+    return;                                                                                  \
+  }
+  XM_GEMM_CASE(false, false, false)
+  XM_GEMM_CASE(true, false, false)
+  XM_GEMM_CASE(true, false, true)
+  XM_GEMM_CASE(false, true, false)
+  XM_GEMM_CASE(false, true, true)
+#undef XM_GEMM_CASE
+  throw Error(XM_EINVAL, "dgemm variant not instantiated");
+}
+
+// ---------------------------------------------------------------- Cholesky
+constexpr int NB = 64;
+
+// Unblocked Cholesky of the nb×nb diagonal block (one CTA, block in smem).
+__global__ void __launch_bounds__(256) k_potf2(double* __restrict__ A, int64_t lda, int nb,
+                                               double rel_tol, const double* __restrict__ scale,
+                                               int* __restrict__ err) {
+  const double pivot_tol = rel_tol * (*scale);
+  __shared__ double a[NB][NB + 1];
+  for (int t = threadIdx.x; t < nb * nb; t += blockDim.x) {
+    int i = t / nb, j = t % nb;
+    a[i][j] = (j <= i) ? A[(int64_t)i * lda + j] : 0.0;
+  }
+  __syncthreads();
+  for (int j = 0; j < nb; ++j) {
+    if (threadIdx.x == 0) {
+      double d = a[j][j];
+      if (!(d > pivot_tol)) {
+        atomicOr(err, 1);
+        d = 1.0;
+      }
+      a[j][j] = sqrt(d);
+    }
+    __syncthreads();
+    double djj = a[j][j];
+    for (int i = j + 1 + threadIdx.x; i < nb; i += blockDim.x) a[i][j] /= djj;
+    __syncthreads();
+    int rem = nb - j - 1;
+    for (int t = threadIdx.x; t < rem * rem; t += blockDim.x) {
+      int ii = j + 1 + t / rem, ll = j + 1 + t % rem;
+      if (ll <= ii) a[ii][ll] -= a[ii][j] * a[ll][j];
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < nb * nb; t += blockDim.x) {
+    int i = t / nb, j = t % nb;
+    A[(int64_t)i * lda + j] = (j <= i) ? a[i][j] : 0.0;
+  }
+}
+
+// Panel: rows below the diagonal block, X·L11ᵀ = A21 (one thread per row).
+template <int NBT>
+__global__ void __launch_bounds__(128) k_trsm_panel(const double* __restrict__ L11, int64_t lda,
+                                                    double* __restrict__ A21, int rows, int nb) {
+  __shared__ double l[NBT][NBT + 1];
+  for (int t = threadIdx.x; t < nb * nb; t += blockDim.x) {
+    int i = t / nb, j = t % nb;
+    l[i][j] = (j <= i) ? L11[(int64_t)i * lda + j] : 0.0;
+  }
+  __syncthreads();
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  double* row = A21 + (int64_t)r * lda;
+  double x[NBT];
+#pragma unroll
+  for (int j = 0; j < NBT; ++j) {
+    if (j < nb) {
+      double s = row[j];
+#pragma unroll
+      for (int q = 0; q < j; ++q) s -= x[q] * l[j][q];
+      x[j] = s / l[j][j];
+    } else {
+      x[j] = 0.0;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NBT; ++j)
+    if (j < nb) row[j] = x[j];
+}
+
+__global__ void k_zero_upper(double* A, int m, int64_t lda) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)m * m) return;
+  int i = (int)(t / m), j = (int)(t % m);
+  if (j > i) A[(int64_t)i * lda + j] = 0.0;
+}
+
+// max_i A[i][i] (one block; used to make the Cholesky pivot test relative)
+__global__ void k_diag_max(const double* __restrict__ A, int m, int64_t lda, double* out) {
+  __shared__ double sh[256];
+  double v = 0.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) v = fmax(v, A[(int64_t)i * lda + i]);
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
+void dense_cholesky(xm_ctx* c, double* A, int m, int64_t lda, double rel_tol) {
+  if (m <= 0) return;
+  c->flags.alloc(16);
+  c->scal.alloc(64);
+  XM_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int), c->stream));
+  double* d_scale = c->scal.p + 63;
+  k_diag_max<<<1, 256, 0, c->stream>>>(A, m, lda, d_scale);
+  XM_CHECK_LAUNCH();
+  count_launch(c);
+  for (int kb = 0; kb < m; kb += NB) {
+    int nb = std::min(NB, m - kb);
+    double* Akk = A + (int64_t)kb * lda + kb;
+    k_potf2<<<1, 256, 0, c->stream>>>(Akk, lda, nb, rel_tol, d_scale, c->flags.p);
+    XM_CHECK_LAUNCH();
+    count_launch(c);
+    int rows = m - kb - nb;
+    if (rows > 0) {
+      double* A21 = A + (int64_t)(kb + nb) * lda + kb;
+      k_trsm_panel<NB><<<ceil_div(rows, 128), 128, 0, c->stream>>>(Akk, lda, A21, rows, nb);
+      XM_CHECK_LAUNCH();
+      count_launch(c);
+      double* A22 = A + (int64_t)(kb + nb) * lda + (kb + nb);
+      dgemm(c, false, true, true, rows, rows, nb, -1.0, A21, lda, A21, lda, 1.0, A22, lda);
+    }
+  }
+  k_zero_upper<<<ceil_div((int64_t)m * m, 256), 256, 0, c->stream>>>(A, m, lda);
+  XM_CHECK_LAUNCH();
+  count_launch(c);
+  int h_err = 0;
+  XM_CUDA(cudaMemcpyAsync(&h_err, c->flags.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  if (h_err) throw Error(XM_EDISCONNECTED, "graph numerically disconnected (Cholesky pivot)");
+}
+
+// Forward substitution of a diagonal block for many right-hand sides:
+// B[0:nb, :] ← L11⁻¹ B[0:nb, :] (one thread per column; L11 in smem).
+template <int NBT>
+__global__ void __launch_bounds__(128) k_trsm_block_cols(const double* __restrict__ L11,
+                                                         int64_t ldl, double* __restrict__ B,
+                                                         int64_t ldb, int nb, int ncols) {
+  __shared__ double l[NBT][NBT + 1];
+  for (int t = threadIdx.x; t < nb * nb; t += blockDim.x) {
+    int i = t / nb, j = t % nb;
+    l[i][j] = (j <= i) ? L11[(int64_t)i * ldl + j] : 0.0;
+  }
+  __syncthreads();
+  int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= ncols) return;
+  double x[NBT];
+#pragma unroll
+  for (int j = 0; j < NBT; ++j) {
+    if (j < nb) {
+      double s = B[(int64_t)j * ldb + col];
+#pragma unroll
+      for (int q = 0; q < j; ++q) s -= l[j][q] * x[q];
+      x[j] = s / l[j][j];
+    } else {
+      x[j] = 0.0;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NBT; ++j)
+    if (j < nb) B[(int64_t)j * ldb + col] = x[j];
+}
+
+void dense_trsm_lower_left(xm_ctx* c, const double* L, int m, int64_t ldl, double* B, int ncols,
+                           int64_t ldb) {
+  for (int kb = 0; kb < m; kb += NB) {
+    int nb = std::min(NB, m - kb);
+    const double* Lkk = L + (int64_t)kb * ldl + kb;
+    double* Bk = B + (int64_t)kb * ldb;
+    k_trsm_block_cols<NB><<<ceil_div(ncols, 128), 128, 0, c->stream>>>(Lkk, ldl, Bk, ldb, nb, ncols);
+    XM_CHECK_LAUNCH();
+    count_launch(c);
+    int rows = m - kb - nb;
+    if (rows > 0) {
+      const double* L21 = L + (int64_t)(kb + nb) * ldl + kb;
+      dgemm(c, false, false, false, rows, ncols, nb, -1.0, L21, ldl, Bk, ldb, 1.0,
+            B + (int64_t)(kb + nb) * ldb, ldb);
+    }
+  }
+}
+
+// Q[i][j] (j > i) ← Q[j][i]: exact symmetry after a lower-triangle SYRK.
+__global__ void k_mirror(double* Q, int n, int64_t ldq) {
+  __shared__ double tile[32][33];
+  int bi = blockIdx.y, bj = blockIdx.x;  // destination tile (bi row, bj col), bj > bi
+  if (bj < bi) return;
+  int tx = threadIdx.x, ty = threadIdx.y;
+  // read source tile (rows bj*32.., cols bi*32..) — lower part
+  for (int y = ty; y < 32; y += blockDim.y) {
+    int r = bj * 32 + y, cc = bi * 32 + tx;
+    tile[y][tx] = (r < n && cc < n) ? Q[(int64_t)r * ldq + cc] : 0.0;
+  }
+  __syncthreads();
+  for (int y = ty; y < 32; y += blockDim.y) {
+    int r = bi * 32 + y, cc = bj * 32 + tx;
+    if (r < n && cc < n && cc > r) Q[(int64_t)r * ldq + cc] = tile[tx][y];
+  }
+}
+
+void mirror_lower(xm_ctx* c, double* Q, int n, int64_t ldq) {
+  dim3 grid(ceil_div(n, 32), ceil_div(n, 32));
+  k_mirror<<<grid, dim3(32, 8), 0, c->stream>>>(Q, n, ldq);
+  XM_CHECK_LAUNCH();
+  count_launch(c);
+}
+
+__global__ void k_sumsq_rows(const double* __restrict__ Q, int rows, int n, int64_t ldq,
+                             double* __restrict__ partials) {
+  __shared__ double sh[256];
+  double acc = 0.0;
+  int64_t tot = (int64_t)rows * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int i = (int)(t / n), j = (int)(t % n);
+    double v = Q[(int64_t)i * ldq + j];
+    acc = fma(v, v, acc);
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partials[blockIdx.x] = sh[0];
+}
+
+// ============================================================ driver
+void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, const int32_t* lm_in,
+                    const double* pts_in, const double* w_in) {
+  if (N < 1 || M < 1 || E < 1) throw Error(XM_EINVAL, "empty view graph");
+  if (E >= (int64_t)INT32_MAX) throw Error(XM_EINVAL, "too many observations");
+  const int T = 256;
+  // stage inputs on the device
+  DBuf<int32_t> d_fr, d_lm;
+  DBuf<double> d_pts, d_w;
+  const int32_t* fr = fr_in;
+  const int32_t* lm = lm_in;
+  const double* pts = pts_in;
+  const double* w = w_in;
+  if (!is_device_ptr(fr_in)) { d_fr.alloc(E); copy_in(c, d_fr.p, fr_in, E * 4); fr = d_fr.p; }
+  if (!is_device_ptr(lm_in)) { d_lm.alloc(E); copy_in(c, d_lm.p, lm_in, E * 4); lm = d_lm.p; }
+  if (!is_device_ptr(pts_in)) { d_pts.alloc(3 * E); copy_in(c, d_pts.p, pts_in, E * 24); pts = d_pts.p; }
+  if (w_in && !is_device_ptr(w_in)) { d_w.alloc(E); copy_in(c, d_w.p, w_in, E * 8); w = d_w.p; }
+
+  c->flags.alloc(16);
+  XM_CUDA(cudaMemsetAsync(c->flags.p, 0, 16 * sizeof(int), c->stream));
+  // ---- H1: validate, key = (frame, landmark)
+  DBuf<uint64_t> key, key2, tk;
+  DBuf<uint32_t> val, val2, tv;
+  key.alloc(E);
+  val.alloc(E);
+  k_validate<<<ceil_div(E, T), T, 0, c->stream>>>(E, N, M, fr, lm, pts, w, c->flags.p, key.p, val.p);
+  XM_CHECK_LAUNCH();
+  count_launch(c);
+  int h_err = 0;
+  XM_CUDA(cudaMemcpyAsync(&h_err, c->flags.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  if (h_err & ERR_RANGE) throw Error(XM_EINVAL, "index out of range");
+  if (h_err & ERR_WEIGHT) throw Error(XM_EINVAL, "non-positive or non-finite weight");
+  if (h_err & ERR_POINT) throw Error(XM_EINVAL, "non-finite point or non-positive depth");
+  int bits_fl = 1;
+  while (bits_fl < 64 && ((uint64_t)N * (uint64_t)M) > (1ull << bits_fl)) ++bits_fl;
+  radix_sort_u64(c, key.p, val.p, E, bits_fl, tk, tv);
+  // ---- dedupe (stable sort ⇒ the first occurrence of a key is the earliest input)
+  DBuf<int32_t> flag, pos;
+  flag.alloc(E);
+  pos.alloc(E);
+  k_first_flags<<<ceil_div(E, T), T, 0, c->stream>>>(key.p, E, flag.p);
+  XM_CHECK_LAUNCH();
+  count_launch(c);
+  int32_t* d_total = c->flags.p + 4;
+  exclusive_scan_i32(c, flag.p, pos.p, E, d_total);
+  int32_t Ek = 0;
+  XM_CUDA(cudaMemcpyAsync(&Ek, d_total, 4, cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  c->stats.n_dup = E - Ek;
+  c->E = Ek;
+  DBuf<int32_t> fs_in, fs_fr;
+  fs_in.alloc(Ek);
+  fs_fr.alloc(Ek);
+  key2.alloc(Ek);
+  val2.alloc(Ek);
+  k_compact_fs<<<ceil_div(E, T), T, 0, c->stream>>>(key.p, val.p, flag.p, pos.p, E, M, N, fs_in.p,
+                                                   fs_fr.p, key2.p, val2.p);
+  XM_CHECK_LAUNCH();
+  count_launch(c);
+  // ---- H2: canonical (landmark, frame) order
+  radix_sort_u64(c, key2.p, val2.p, Ek, bits_fl, tk, tv);
+  c->e_fr.alloc(Ek);
+  c->e_lm.alloc(Ek);
+  c->e_pts.alloc(3 * Ek);
+  c->e_w.alloc(Ek);
+  c->fr_edge.alloc(Ek);
+  k_gather_edges<<<ceil_div(Ek, T), T, 0, c->stream>>>(Ek, key2.p, val2.p, fs_in.p, N, pts, w,
+                                                      c->e_fr.p, c->e_lm.p, c->e_pts.p, c->e_w.p,
+                                                      c->fr_edge.p);
+  XM_CHECK_LAUNCH();
+  count_launch(c);
+  DBuf<int32_t> cnt;
+  cnt.alloc((size_t)std::max(N, M) + 1);
+  c->lm_off.alloc(M + 1);
+  c->fr_off.alloc(N + 1);
+  XM_CUDA(cudaMemsetAsync(cnt.p, 0, (M + 1) * 4, c->stream));
+  k_histogram<<<ceil_div(Ek, T), T, 0, c->stream>>>(c->e_lm.p, Ek, cnt.p);
+  XM_CHECK_LAUNCH();
+  exclusive_scan_i32(c, cnt.p, c->lm_off.p, M + 1, nullptr);
+  DBuf<int32_t> fcnt;
+  fcnt.alloc(N + 1);
+  XM_CUDA(cudaMemsetAsync(fcnt.p, 0, (N + 1) * 4, c->stream));
+  k_histogram<<<ceil_div(Ek, T), T, 0, c->stream>>>(fs_fr.p, Ek, fcnt.p);
+  XM_CHECK_LAUNCH();
+  exclusive_scan_i32(c, fcnt.p, c->fr_off.p, N + 1, nullptr);
+  count_launch(c, 2);
+  c->W.alloc(M);
+  k_track_weight<<<ceil_div(M, T), T, 0, c->stream>>>(M, c->lm_off.p, c->e_w.p, c->W.p);
+  XM_CHECK_LAUNCH();
+  count_launch(c);
+
+  // ---- connectivity: frames ∪ observed landmarks must form one component
+  {
+    DBuf<int32_t> parent;
+    parent.alloc(N + M);
+    k_cc_init<<<ceil_div(N + M, T), T, 0, c->stream>>>(N + M, parent.p);
+    count_launch(c);
+    int* d_changed = c->flags.p + 8;
+    for (int it = 0; it < 100000; ++it) {
+      XM_CUDA(cudaMemsetAsync(d_changed, 0, 4, c->stream));
+      k_cc_hook<<<ceil_div(Ek, T), T, 0, c->stream>>>(Ek, N, c->e_fr.p, c->e_lm.p, parent.p, d_changed);
+      k_cc_jump<<<ceil_div(N + M, T), T, 0, c->stream>>>(N + M, parent.p);
+      XM_CHECK_LAUNCH();
+      count_launch(c, 2);
+      int ch = 0;
+      XM_CUDA(cudaMemcpyAsync(&ch, d_changed, 4, cudaMemcpyDeviceToHost, c->stream));
+      sync(c);
+      if (!ch) break;
+    }
+    int* d_cnt = c->flags.p + 12;
+    XM_CUDA(cudaMemsetAsync(d_cnt, 0, 8, c->stream));
+    k_cc_count<<<ceil_div(N + M, T), T, 0, c->stream>>>(N, M, parent.p, c->lm_off.p, fcnt.p, d_cnt);
+    XM_CHECK_LAUNCH();
+    count_launch(c);
+    int h_cc[2] = {0, 0};
+    XM_CUDA(cudaMemcpyAsync(h_cc, d_cnt, 8, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    if (h_cc[1] > 0) throw Error(XM_EDISCONNECTED, "a frame has no observation");
+    if (h_cc[0] != 1) throw Error(XM_EDISCONNECTED, "graph numerically disconnected");
+  }
+
+  // ---- H3: S pattern
+  {
+    int W32 = ceil_div(N, 32);
+    DBuf<unsigned> bits;
+    bits.alloc((size_t)N * W32);
+    XM_CUDA(cudaMemsetAsync(bits.p, 0, (size_t)N * W32 * 4, c->stream));
+    k_pattern_bits<<<N, 128, 0, c->stream>>>(N, W32, c->fr_off.p, c->fr_edge.p, c->e_lm.p,
+                                             c->lm_off.p, c->e_fr.p, bits.p);
+    XM_CHECK_LAUNCH();
+    DBuf<int32_t> rc, ro;
+    rc.alloc(N);
+    ro.alloc(N);
+    k_pattern_count<<<N, 256, 0, c->stream>>>(N, W32, bits.p, rc.p);
+    XM_CHECK_LAUNCH();
+    exclusive_scan_i32(c, rc.p, ro.p, N, c->flags.p + 6);
+    int32_t nnzb = 0;
+    XM_CUDA(cudaMemcpyAsync(&nnzb, c->flags.p + 6, 4, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    c->nnzb = nnzb;
+    c->stats.nnzb_S = nnzb;
+    c->s_rowptr.alloc(N + 1);
+    c->s_colidx.alloc(nnzb);
+    k_pattern_cols<<<ceil_div(N, 8), 256, 0, c->stream>>>(N, W32, bits.p, ro.p, c->s_colidx.p,
+                                                         c->s_rowptr.p);
+    XM_CHECK_LAUNCH();
+    int64_t last = nnzb;
+    XM_CUDA(cudaMemcpyAsync(c->s_rowptr.p + N, &last, 8, cudaMemcpyHostToDevice, c->stream));
+    count_launch(c, 3);
+    sync(c);
+  }
+
+  // ---- H4: dense S (own rows, in the Q buffer), C̄ (in the G buffer), K̄ (in L)
+  const int n = 3 * N;
+  c->N = N;
+  c->M = M;
+  c->n = n;
+  c->ldq = round_up(std::max(n, 1), 32);
+  c->ldk = round_up(std::max(N - 1, 1), 32);
+  c->nfpr = ceil_div(N, c->world);
+  c->f0 = std::min(N, c->rank * c->nfpr);
+  c->f1 = std::min(N, c->f0 + c->nfpr);
+  c->row0 = 3 * c->f0;
+  c->nrows = 3 * (c->f1 - c->f0);
+  c->Q.alloc((size_t)std::max(c->nrows, 1) * c->ldq);
+  XM_CUDA(cudaMemsetAsync(c->Q.p, 0, (size_t)std::max(c->nrows, 1) * c->ldq * 8, c->stream));
+  if (N > 1) {
+    c->G.alloc((size_t)(N - 1) * c->ldq);
+    c->L.alloc((size_t)(N - 1) * c->ldk);
+    XM_CUDA(cudaMemsetAsync(c->G.p, 0, (size_t)(N - 1) * c->ldq * 8, c->stream));
+    XM_CUDA(cudaMemsetAsync(c->L.p, 0, (size_t)(N - 1) * c->ldk * 8, c->stream));
+  } else {
+    c->G.alloc(1);
+    c->L.alloc(1);
+  }
+  k_clique_scatter<<<N, 128, 0, c->stream>>>(N, c->f0, c->f1, c->fr_off.p, c->fr_edge.p,
+                                             c->lm_off.p, c->e_fr.p, c->e_pts.p, c->e_w.p, c->W.p,
+                                             c->e_lm.p, c->Q.p, c->ldq, c->row0, c->G.p, c->L.p,
+                                             c->ldk);
+  XM_CHECK_LAUNCH();
+  count_launch(c);
+
+  // ---- H5: K̄ = LLᵀ, G = L⁻¹C̄, Q = S − GᵀG
+  if (N > 1) {
+    // pivot test relative to max diag(K̄); a disconnected graph gives a ~0 pivot
+    dense_cholesky(c, c->L.p, N - 1, c->ldk, 1e-12);
+    dense_trsm_lower_left(c, c->L.p, N - 1, c->ldk, c->G.p, n, c->ldq);
+    const double* Gown = c->G.p + c->row0;  // columns of this rank's rows
+    bool lower = (c->world == 1);
+    dgemm(c, true, false, lower, c->nrows, n, N - 1, -1.0, Gown, c->ldq, c->G.p, c->ldq, 1.0,
+          c->Q.p, c->ldq);
+    if (lower) mirror_lower(c, c->Q.p, n, c->ldq);
+  } else if (c->world == 1) {
+    mirror_lower(c, c->Q.p, n, c->ldq);
+  }
+  c->have_recovery = true;
+  // ‖Q‖_F (all-reduced over ranks)
+  {
+    DBuf<double> part;
+    part.alloc(kDotBlocks);
+    k_sumsq_rows<<<kDotBlocks, 256, 0, c->stream>>>(c->Q.p, c->nrows, n, c->ldq, part.p);
+    XM_CHECK_LAUNCH();
+    c->scal.alloc(64);
+    reduce_partials(c, part.p, kDotBlocks, 1, c->scal.p);
+    count_launch(c);
+    if (c->world > 1) nccl_allreduce_sum(c, c->scal.p, 1);
+    double s2 = 0.0;
+    XM_CUDA(cudaMemcpyAsync(&s2, c->scal.p, 8, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    c->normQ = std::sqrt(s2);
+  }
+  c->stats.E = c->E;
+  c->stats.q_bytes = (int64_t)c->nrows * n * 8;
+}
+
+}  // namespace xm

@@ -1,0 +1,103 @@
+// comm.cu — NCCL over NVLink 5 / NVSwitch for the row-sharded path.
+//
+// The only exchange of the solve is the all-gather of the Q·V row shards after
+// every product (one per HVP / Δf / Lanczos step); all O(N·r) per-camera work
+// and every dot product then run redundantly (and bitwise identically) on the
+// replicated full vectors, so no all-reduce is needed in the inner loop.
+// NCCL is loaded with dlopen only when world > 1 (single-GPU runs do not
+// depend on it); the communicator is bootstrapped from an ncclUniqueId that
+// the caller broadcasts (torch.distributed in the Python harness).
+#include "xm_internal.cuh"
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+namespace xm {
+
+namespace {
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+
+void load_nccl() {
+  if (g_nccl.h) return;
+  const char* names[] = {"libnccl.so.2", "libnccl.so"};
+  for (const char* nm : names) {
+    g_nccl.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+    if (g_nccl.h) break;
+  }
+  if (!g_nccl.h) throw Error(XM_ENCCL, "cannot dlopen libnccl.so.2");
+  auto sym = [](const char* s) {
+    void* p = dlsym(g_nccl.h, s);
+    if (!p) throw Error(XM_ENCCL, std::string("missing NCCL symbol ") + s);
+    return p;
+  };
+  g_nccl.GetUniqueId = (decltype(g_nccl.GetUniqueId))sym("ncclGetUniqueId");
+  g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))sym("ncclCommInitRank");
+  g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))sym("ncclCommDestroy");
+  g_nccl.AllGather = (decltype(g_nccl.AllGather))sym("ncclAllGather");
+  g_nccl.AllReduce = (decltype(g_nccl.AllReduce))sym("ncclAllReduce");
+  g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))sym("ncclGetErrorString");
+}
+
+void check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw Error(XM_ENCCL, std::string(what) + ": " + (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?"));
+}
+}  // namespace
+
+void nccl_unique_id(void* out128) {
+  load_nccl();
+  ncclUniqueId id;
+  check(g_nccl.GetUniqueId(&id), "ncclGetUniqueId");
+  memcpy(out128, &id, sizeof(id));
+}
+
+void nccl_init(xm_ctx* c, const void* id) {
+  if (c->world <= 1) return;
+  if (!id) throw Error(XM_EINVAL, "world > 1 requires an ncclUniqueId");
+  load_nccl();
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof(uid));
+  ncclComm_t comm;
+  check(g_nccl.CommInitRank(&comm, c->world, uid, c->rank), "ncclCommInitRank");
+  c->nccl_comm = comm;
+}
+
+void nccl_destroy(xm_ctx* c) {
+  if (c->nccl_comm && g_nccl.CommDestroy) g_nccl.CommDestroy((ncclComm_t)c->nccl_comm);
+  c->nccl_comm = nullptr;
+}
+
+void nccl_allgather(xm_ctx* c, const double* send, double* recv, size_t count_per_rank) {
+  check(g_nccl.AllGather(send, recv, count_per_rank, ncclFloat64, (ncclComm_t)c->nccl_comm,
+                         c->stream),
+        "ncclAllGather");
+}
+
+void nccl_allreduce_sum(xm_ctx* c, double* buf, size_t count) {
+  if (c->world <= 1) return;
+  check(g_nccl.AllReduce(buf, buf, count, ncclFloat64, ncclSum, (ncclComm_t)c->nccl_comm,
+                         c->stream),
+        "ncclAllReduce");
+}
+
+// Row shards are contiguous frame ranges of equal size nfpr (the last one
+// padded), so gathering the padded shards in rank order yields the natural
+// row-major n×r layout (vectors are allocated with world·3·nfpr rows).
+void allgather_rows(xm_ctx* c, double* full, int r) {
+  if (c->world <= 1) return;
+  size_t per = (size_t)3 * c->nfpr * r;
+  nccl_allgather(c, full + (size_t)c->rank * per, full, per);
+}
+
+}  // namespace xm

@@ -1,0 +1,664 @@
+// xm_api.cu — the C ABI (include/xm.h) and the host-side control of
+// Algorithm 1 (Riemannian staircase) with the Riemannian
+// trust-region / truncated-CG local optimiser.
+//
+// The host only holds O(1) scalars per iteration (TR radius, ρ) and the k
+// Lanczos coefficients; every O(n) and O(n²) operation is a device kernel.
+// The tCG inner loop runs from device-resident state (TcgState): kernels read
+// α, β, τ and the stop flag from device memory, so the host launches tCG
+// iterations in batches and synchronises once per batch.
+#include "xm_internal.cuh"
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+using namespace xm;
+
+namespace {
+
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+template <typename F>
+xm_status guard(xm_ctx* c, F&& f) {
+  try {
+    if (c) XM_CUDA(cudaSetDevice(c->device));
+    f();
+    return XM_OK;
+  } catch (const Error& e) {
+    if (c) c->last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    if (c) c->last_error = e.what();
+    return XM_ECUDA;
+  }
+}
+
+void require_stage(xm_ctx* c, int stage) {
+  if (c->stage < stage) throw Error(XM_ESTATE, "call order violated");
+}
+
+constexpr int kMaxCols = XM_MAX_R + 1;
+
+void alloc_vectors(xm_ctx* c) {
+  int64_t rows = std::max<int64_t>(c->n, (int64_t)c->world * 3 * c->nfpr);
+  rows = round_up(rows, 32);
+  if (c->n_alloc == rows && c->Y.p) return;
+  c->n_alloc = rows;
+  size_t sz = (size_t)rows * kMaxCols + 64;
+  for (DBuf<double>* b : {&c->Y, &c->QY, &c->grad, &c->eta, &c->Heta, &c->res, &c->dir, &c->Hdir,
+                          &c->Ynew, &c->Dv, &c->QD, &c->tmp, &c->tmp2, &c->hY, &c->hV, &c->hO,
+                          &c->hQY}) {
+    b->alloc(sz);
+    XM_CUDA(cudaMemsetAsync(b->p, 0, sz * 8, c->stream));
+  }
+  c->lam.alloc((size_t)c->N * 6 + 6);
+  c->scal.alloc(64);
+  c->tcg.alloc(1);
+  c->flags.alloc(16);
+  c->cert_v.alloc((size_t)rows + 64);
+  c->red.alloc((size_t)ceil_div(c->N, 128) * 4 + 1024);
+}
+
+void read_scal(xm_ctx* c, int first, int count, double* out) {
+  XM_CUDA(cudaMemcpyAsync(out, c->scal.p + first, count * 8, cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+}
+
+// fresh QY and gradient at c->Y; returns f, ‖g‖², α_min
+void eval_point(xm_ctx* c, double* f, double* g2, double* amin) {
+  spmm_full(c, c->Y.p, c->r, c->QY.p, nullptr);
+  grad_and_multipliers(c, c->r, c->Y.p, c->QY.p, c->grad.p, c->scal.p);
+  double h[3];
+  read_scal(c, 0, 3, h);
+  *f = h[0];
+  *g2 = h[1];
+  *amin = h[2];
+}
+
+// ⟨a_q, b_q⟩ for up to 4 pairs of flat arrays of length len → host
+void dots(xm_ctx* c, int64_t len, int npair, const double* const* a, const double* const* b,
+          double* out) {
+  c->lz_part.alloc((size_t)kDotBlocks * 4 + 64);
+  for (int q = 0; q < npair; ++q) {
+    dot_flat(c, a[q], b[q], len, c->lz_part.p, kDotBlocks);
+    reduce_partials(c, c->lz_part.p, kDotBlocks, 1, c->scal.p + 8 + q);
+  }
+  read_scal(c, 8, npair, out);
+}
+
+struct RtrOut {
+  bool converged = false;
+  int64_t outer = 0;
+  double f = 0, g2 = 0, amin = 0;
+};
+
+// Riemannian trust region with device-state tCG (O5).
+RtrOut rtr(xm_ctx* c, double tol_abs) {
+  const int r = c->r;
+  const int64_t len = (int64_t)c->n * r;
+  const xm_options& o = c->opt;
+  const double Delta0 = o.delta0_coef * std::sqrt(3.0 * c->N);
+  const double Dbar = o.delta_max_mult * Delta0;
+  double Delta = Delta0;
+  RtrOut out;
+  double f, g2, amin;
+  eval_point(c, &f, &g2, &amin);
+  int64_t accepts = 0;
+  int64_t it = 0;
+  const double eps = 2.220446049250313e-16;
+  for (it = 0;; ++it) {
+    if (std::sqrt(g2) <= tol_abs) {
+      out.converged = true;
+      break;
+    }
+    if (it >= o.max_outer) break;
+    // ---- tCG (device-resident state)
+    tcg_init(c, r, Delta);
+    int batch = c->tcg_batch;
+    TcgState hs{};
+    while (true) {
+      for (int b = 0; b < batch; ++b) {
+        spmm_full(c, c->dir.p, r, c->tmp.p, &c->tcg.p->stop);
+        hvp_epilogue(c, r, c->Y.p, c->dir.p, c->tmp.p, c->Hdir.p, nullptr, &c->tcg.p->stop);
+        tcg_ctrl_a(c);
+        tcg_update(c, r);
+        tcg_ctrl_b(c);
+        tcg_dir(c, r);
+      }
+      XM_CUDA(cudaMemcpyAsync(&hs, c->tcg.p, sizeof(TcgState), cudaMemcpyDeviceToHost, c->stream));
+      sync(c);
+      if (hs.stop) break;
+    }
+    c->info.hvps += hs.n_hvp;
+    // ---- retraction + cancellation-free Δf (reading C21)
+    XM_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int), c->stream));
+    retract(c, r, c->Y.p, c->eta.p, 1.0, c->Ynew.p, c->Dv.p, c->flags.p);
+    spmm_full(c, c->Dv.p, r, c->QD.p, nullptr);
+    const double* A[4] = {c->QY.p, c->Dv.p, c->grad.p, c->eta.p};
+    const double* B[4] = {c->Dv.p, c->QD.p, c->eta.p, c->Heta.p};
+    double d[4];
+    dots(c, len, 4, A, B, d);
+    int rerr = 0;
+    XM_CUDA(cudaMemcpyAsync(&rerr, c->flags.p, 4, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    if (rerr) throw Error(XM_ERETRACT, "retraction failure");
+    const double df = 2.0 * d[0] + d[1];
+    const double model_dec = -d[2] - 0.5 * d[3];
+    const double reg = std::max(1.0, std::fabs(f)) * eps * 1e3;
+    const double rho = (-df + reg) / (model_dec + reg);
+    const bool limited = (hs.stop == TCG_NEGCURV || hs.stop == TCG_EXCEEDED);
+    if (!(rho >= 0.25) || std::isnan(rho)) Delta /= 4.0;
+    else if (rho > 0.75 && limited) Delta = std::min(2.0 * Delta, Dbar);
+    if (rho > o.rho_prime) {
+      std::swap(c->Y.p, c->Ynew.p);
+      ++accepts;
+      if (o.refresh_every > 0 && accepts % o.refresh_every == 0) {
+        spmm_full(c, c->Y.p, r, c->QY.p, nullptr);
+      } else {
+        axpy(c, len, 1.0, c->QD.p, c->QY.p);
+      }
+      grad_and_multipliers(c, r, c->Y.p, c->QY.p, c->grad.p, c->scal.p);
+      double h[3];
+      read_scal(c, 0, 3, h);
+      f = h[0];
+      g2 = h[1];
+      amin = h[2];
+    }
+  }
+  // fresh Q·Y before any certificate (O4)
+  eval_point(c, &f, &g2, &amin);
+  out.outer = it;
+  out.f = f;
+  out.g2 = g2;
+  out.amin = amin;
+  c->info.outer_iters += it;
+  return out;
+}
+
+void certify_current(xm_ctx* c, double* lambda, int* steps) {
+  double tol = c->opt.eig_tol * std::max(1.0, c->normQ);
+  lanczos(c, tol, c->opt.lanczos_max, lambda, steps, c->cert_v.p);
+  c->cert_valid = true;
+  c->cert_lambda = *lambda;
+  c->cert_steps = *steps;
+  c->info.lanczos_steps += *steps;
+}
+
+// Escape along D = [0, v] from [Y, 0] (Thm 2, Alg. 1 l.14-22, reading C9)
+void escape(xm_ctx* c) {
+  const int r = c->r;
+  const int r1 = r + 1;
+  const int64_t len1 = (int64_t)c->n * r1;
+  pad_column(c, r, c->Y.p, c->Ynew.p, c->cert_v.p, c->dir.p);   // Yz, Dz
+  pad_column(c, r, c->QY.p, c->Heta.p, nullptr, nullptr);       // QYz
+  double alpha = 1.0;
+  for (int h = 0; h <= 60; ++h) {
+    XM_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int), c->stream));
+    retract(c, r1, c->Ynew.p, c->dir.p, alpha, c->eta.p, c->Dv.p, c->flags.p);
+    spmm_full(c, c->Dv.p, r1, c->QD.p, nullptr);
+    const double* A[2] = {c->Heta.p, c->Dv.p};
+    const double* B[2] = {c->Dv.p, c->QD.p};
+    double d[2];
+    dots(c, len1, 2, A, B, d);
+    double df = 2.0 * d[0] + d[1];
+    if (df < 0.0) {
+      XM_CUDA(cudaMemcpyAsync(c->Y.p, c->eta.p, len1 * 8, cudaMemcpyDeviceToDevice, c->stream));
+      c->r = r1;
+      c->info.escapes++;
+      return;
+    }
+    alpha *= 0.5;
+  }
+  throw Error(XM_EESCAPE, "escape failed");
+}
+
+__global__ void k_identity_init(int N, int r, double* Y) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)3 * N * r) return;
+  int64_t row = t / r;
+  int col = (int)(t % r);
+  Y[t] = (col == (int)(row % 3)) ? 1.0 : 0.0;
+}
+
+void reset_after_new_Q(xm_ctx* c) {
+  c->stage = 1;
+  c->factor_set = false;
+  c->cert_valid = false;
+  c->have_round = false;
+  c->r = 0;
+  alloc_vectors(c);
+}
+
+}  // namespace
+
+// =============================================================================
+extern "C" {
+
+void xm_default_options(xm_options* o) {
+  if (!o) return;
+  o->grad_tol = 1e-10;
+  o->delta0_coef = 0.1;
+  o->delta_max_mult = 10.0;
+  o->rho_prime = 0.1;
+  o->tcg_kappa = 0.1;
+  o->tcg_theta = 1.0;
+  o->eig_tol = 1e-8;
+  o->cert_tol = 1e-6;
+  o->scale_floor = 1e-3;
+  o->tcg_max_inner = 500;
+  o->max_outer = 5000;
+  o->rank_cap = 10;
+  o->lanczos_max = 3000;
+  o->refresh_every = 50;
+  o->profile = 0;
+  o->seed = 0;
+}
+
+const char* xm_strerror(xm_status s) {
+  switch (s) {
+    case XM_OK: return "ok (certified)";
+    case XM_UNCERTIFIED: return "uncertified: rank cap reached with lambda_min(Z) < -cert_tol";
+    case XM_NOT_CONVERGED: return "trust region did not converge";
+    case XM_EINVAL: return "invalid argument";
+    case XM_EDISCONNECTED: return "graph numerically disconnected";
+    case XM_ENOMEM: return "out of device memory";
+    case XM_ECUDA: return "CUDA error";
+    case XM_ENCCL: return "NCCL error";
+    case XM_ERETRACT: return "retraction failure";
+    case XM_EESCAPE: return "escape failed";
+    case XM_EINFEASIBLE: return "infeasible point";
+    case XM_EDEGENERATE: return "degenerate block";
+    case XM_ESTATE: return "call order violated";
+  }
+  return "unknown status";
+}
+
+xm_status xm_nccl_unique_id(void* out128) {
+  if (!out128) return XM_EINVAL;
+  try {
+    nccl_unique_id(out128);
+    return XM_OK;
+  } catch (const Error& e) {
+    return e.code;
+  }
+}
+
+xm_status xm_create(xm_ctx** out, int device, int rank, int world, const void* nccl_id,
+                    const xm_options* opts, void* cuda_stream) {
+  if (!out || world < 1 || rank < 0 || rank >= world) return XM_EINVAL;
+  *out = nullptr;
+  xm_ctx* c = new xm_ctx();
+  c->device = device;
+  c->rank = rank;
+  c->world = world;
+  if (opts) c->opt = *opts; else xm_default_options(&c->opt);
+  if (c->opt.rank_cap > XM_MAX_R) c->opt.rank_cap = XM_MAX_R;
+  xm_status st = guard(c, [&] {
+    if (cuda_stream) {
+      c->stream = (cudaStream_t)cuda_stream;
+    } else {
+      XM_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    nccl_init(c, nccl_id);
+  });
+  if (st != XM_OK) {
+    xm_destroy(c);
+    return st;
+  }
+  *out = c;
+  return XM_OK;
+}
+
+void xm_destroy(xm_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  nccl_destroy(c);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+xm_status xm_build_Q(xm_ctx* c, int32_t N, int32_t M, int64_t E, const int32_t* frame,
+                     const int32_t* landmark, const double* lifted_pts, const double* weights) {
+  if (!c) return XM_EINVAL;
+  if (!frame || !landmark || !lifted_pts) return XM_EINVAL;
+  return guard(c, [&] {
+    double t0 = now_ms();
+    c->stage = 0;
+    build_Q_device(c, N, M, E, frame, landmark, lifted_pts, weights);
+    reset_after_new_Q(c);
+    sync(c);
+    c->stats.ms_build += now_ms() - t0;
+  });
+}
+
+__global__ void k_copy_rows(int rows, int n, const double* __restrict__ src, int64_t lds,
+                            double* __restrict__ dst, int64_t ldd) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)rows * n) return;
+  int i = (int)(t / n), j = (int)(t % n);
+  dst[(int64_t)i * ldd + j] = src[(int64_t)i * lds + j];
+}
+
+xm_status xm_set_Q(xm_ctx* c, int32_t N, const double* Q_full) {
+  if (!c || N < 1 || !Q_full) return XM_EINVAL;
+  return guard(c, [&] {
+    c->N = N;
+    c->M = 0;
+    c->E = 0;
+    c->n = 3 * N;
+    c->ldq = round_up(c->n, 32);
+    c->ldk = round_up(std::max(N - 1, 1), 32);
+    c->nfpr = ceil_div(N, c->world);
+    c->f0 = std::min(N, c->rank * c->nfpr);
+    c->f1 = std::min(N, c->f0 + c->nfpr);
+    c->row0 = 3 * c->f0;
+    c->nrows = 3 * (c->f1 - c->f0);
+    c->Q.alloc((size_t)std::max(c->nrows, 1) * c->ldq);
+    const int64_t n = c->n;
+    if (c->nrows > 0) {
+      XM_CUDA(cudaMemcpy2DAsync(c->Q.p, c->ldq * 8, Q_full + (int64_t)c->row0 * n, n * 8, n * 8,
+                                c->nrows,
+                                is_device_ptr(Q_full) ? cudaMemcpyDeviceToDevice
+                                                      : cudaMemcpyHostToDevice,
+                                c->stream));
+    }
+    c->have_recovery = false;
+    c->nnzb = 0;
+    // ‖Q‖_F
+    DBuf<double> part;
+    part.alloc(kDotBlocks);
+    DBuf<double> tmp;
+    tmp.alloc((size_t)std::max(c->nrows, 1) * n);
+    k_copy_rows<<<ceil_div((int64_t)c->nrows * n, 256), 256, 0, c->stream>>>(c->nrows, (int)n, c->Q.p,
+                                                                           c->ldq, tmp.p, n);
+    dot_flat(c, tmp.p, tmp.p, (int64_t)c->nrows * n, part.p, kDotBlocks);
+    c->scal.alloc(64);
+    reduce_partials(c, part.p, kDotBlocks, 1, c->scal.p);
+    if (c->world > 1) nccl_allreduce_sum(c, c->scal.p, 1);
+    double s2 = 0;
+    XM_CUDA(cudaMemcpyAsync(&s2, c->scal.p, 8, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    c->normQ = std::sqrt(s2);
+    c->stats.q_bytes = (int64_t)c->nrows * n * 8;
+    reset_after_new_Q(c);
+  });
+}
+
+xm_status xm_solve(xm_ctx* c, int32_t r0, double tol, xm_solve_info* info) {
+  if (!c) return XM_EINVAL;
+  xm_status result = XM_OK;
+  xm_status st = guard(c, [&] {
+    require_stage(c, 1);
+    double t0 = now_ms();
+    c->info = xm_solve_info{};
+    if (!c->factor_set) {
+      if (r0 < 3 || r0 > XM_MAX_R) throw Error(XM_EINVAL, "r0 must be in [3, 12]");
+      c->r = r0;
+      int64_t len = (int64_t)c->n * r0;
+      k_identity_init<<<ceil_div(len, 256), 256, 0, c->stream>>>(c->N, r0, c->Y.p);
+      XM_CHECK_LAUNCH();
+      count_launch(c);
+    }
+    c->factor_set = false;
+    const double tol_abs = (tol > 0 ? tol : c->opt.grad_tol) * std::max(1.0, c->normQ);
+    const int64_t spmm0 = c->stats.spmm_calls;
+    bool certified = false;
+    RtrOut ro;
+    double lam = 0.0;
+    while (true) {
+      ro = rtr(c, tol_abs);
+      int steps = 0;
+      certify_current(c, &lam, &steps);
+      certified = ro.converged && lam >= -c->opt.cert_tol * std::max(1.0, c->normQ);
+      if (certified || !ro.converged || c->r >= c->opt.rank_cap) break;
+      escape(c);
+    }
+    c->info.f = ro.f;
+    c->info.grad_norm = std::sqrt(ro.g2);
+    c->info.lambda_min = lam;
+    c->info.normQ = c->normQ;
+    c->info.s_min = c->N > 1 ? std::sqrt(std::max(ro.amin, 0.0)) : 1.0;
+    c->info.r = c->r;
+    c->info.certified = certified;
+    c->info.converged = ro.converged;
+    c->info.spmms = c->stats.spmm_calls - spmm0;
+    c->stage = 2;
+    c->have_round = false;
+    c->stats.ms_solve += now_ms() - t0;
+    if (!ro.converged) result = XM_NOT_CONVERGED;
+    else if (!certified) result = XM_UNCERTIFIED;
+    if (c->N > 1 && c->info.s_min < 1e-8) throw Error(XM_EDEGENERATE, "scale collapse s_i < 1e-8");
+  });
+  if (info && c) *info = c->info;
+  return st != XM_OK ? st : result;
+}
+
+xm_status xm_certify(xm_ctx* c, xm_certificate* out, double* min_eigvec) {
+  if (!c) return XM_EINVAL;
+  return guard(c, [&] {
+    require_stage(c, 1);
+    if (c->r == 0) throw Error(XM_ESTATE, "no factor: call xm_solve or xm_set_factor first");
+    double t0 = now_ms();
+    double f, g2, amin;
+    eval_point(c, &f, &g2, &amin);
+    double lam;
+    int steps;
+    if (c->cert_valid) {
+      lam = c->cert_lambda;
+      steps = c->cert_steps;
+    } else {
+      certify_current(c, &lam, &steps);
+    }
+    round_recover_device(c);
+    // ρ̂ = f(Ŷ) at the rounded factor
+    spmm_full(c, c->Yr.p, 3, c->tmp.p, nullptr);
+    const double* A[2] = {c->Yr.p, c->Y.p};
+    const double* B[2] = {c->tmp.p, c->Y.p};
+    double d[2];
+    dots(c, (int64_t)c->n * 3, 1, A, B, d);
+    double trX;
+    {
+      const double* A2[1] = {c->Y.p};
+      const double* B2[1] = {c->Y.p};
+      dots(c, (int64_t)c->n * c->r, 1, A2, B2, &trX);
+    }
+    double l0[3];
+    XM_CUDA(cudaMemcpyAsync(l0, c->lam.p, 24, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    xm_certificate ce{};
+    ce.lambda_min = lam;
+    ce.rho_dual = l0[0] + l0[1] + l0[2];
+    ce.rho_hat = d[0];
+    ce.trace_X = trX;
+    ce.rho_lower = ce.rho_dual + std::min(0.0, lam) * trX;
+    ce.eta = (ce.rho_hat - ce.rho_lower) / (1.0 + std::fabs(ce.rho_hat) + std::fabs(ce.rho_lower));
+    double lowE = std::max(0.0, lam) * trX + ce.rho_dual;
+    ce.eta_E = (ce.rho_hat - lowE) / (1.0 + std::fabs(ce.rho_hat) + std::fabs(lowE));
+    ce.kkt_resid = 0.5 * std::sqrt(g2);  // grad = 2 Z Y
+    ce.grad_norm = std::sqrt(g2);
+    ce.normQ = c->normQ;
+    ce.lanczos_steps = steps;
+    ce.certified = (lam >= -c->opt.cert_tol * std::max(1.0, c->normQ)) &&
+                   std::sqrt(g2) <= c->opt.grad_tol * std::max(1.0, c->normQ) * 1.0001;
+    c->cert = ce;
+    c->have_cert = true;
+    if (out) *out = ce;
+    if (min_eigvec) copy_out(c, min_eigvec, c->cert_v.p, (size_t)c->n * 8);
+    c->stats.ms_certify += now_ms() - t0;
+  });
+}
+
+xm_status xm_round_recover(xm_ctx* c, double* R, double* s, double* t, double* p,
+                           int32_t* n_flipped) {
+  if (!c) return XM_EINVAL;
+  return guard(c, [&] {
+    require_stage(c, 1);
+    if (c->r == 0) throw Error(XM_ESTATE, "no factor");
+    double t0 = now_ms();
+    if (!c->have_round) round_recover_device(c);
+    copy_out(c, R, c->Rs.p, (size_t)c->N * 9 * 8);
+    copy_out(c, s, c->s_out.p, (size_t)c->N * 8);
+    copy_out(c, t, c->t_out.p, (size_t)c->N * 3 * 8);
+    if (p && c->M > 0) copy_out(c, p, c->p_out.p, (size_t)c->M * 3 * 8);
+    if (n_flipped) *n_flipped = c->n_flipped;
+    sync(c);
+    c->stats.ms_round += now_ms() - t0;
+  });
+}
+
+// ----------------------------------------------------------------- hooks
+xm_status xm_get_S_pattern(xm_ctx* c, int64_t* rowptr, int32_t* colidx, int64_t* nnzb) {
+  if (!c) return XM_EINVAL;
+  return guard(c, [&] {
+    require_stage(c, 1);
+    if (!c->have_recovery) throw Error(XM_ESTATE, "no view graph (Q was set directly)");
+    if (nnzb) *nnzb = c->nnzb;
+    if (rowptr) copy_out(c, rowptr, c->s_rowptr.p, (size_t)(c->N + 1) * 8);
+    if (colidx) copy_out(c, colidx, c->s_colidx.p, (size_t)c->nnzb * 4);
+    sync(c);
+  });
+}
+
+xm_status xm_get_Q_rows(xm_ctx* c, int32_t row0, int32_t nrows, double* out) {
+  if (!c || !out) return XM_EINVAL;
+  return guard(c, [&] {
+    require_stage(c, 1);
+    if (row0 < c->row0 || row0 + nrows > c->row0 + c->nrows || nrows < 0)
+      throw Error(XM_EINVAL, "rows not owned by this rank");
+    if (nrows == 0) return;
+    XM_CUDA(cudaMemcpy2DAsync(out, (size_t)c->n * 8, c->Q.p + (int64_t)(row0 - c->row0) * c->ldq,
+                              c->ldq * 8, (size_t)c->n * 8, nrows,
+                              is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                              c->stream));
+    sync(c);
+  });
+}
+
+xm_status xm_spmm(xm_ctx* c, const double* V, double* out, int32_t r) {
+  if (!c || !V || !out || r < 1 || r > XM_MAX_R) return XM_EINVAL;
+  return guard(c, [&] {
+    require_stage(c, 1);
+    int64_t len = (int64_t)c->n * r;
+    copy_in(c, c->hV.p, V, len * 8);
+    spmm_full(c, c->hV.p, r, c->hO.p, nullptr);
+    copy_out(c, out, c->hO.p, len * 8);
+    sync(c);
+  });
+}
+
+xm_status xm_grad(xm_ctx* c, const double* Y, double* grad, double* f, int32_t r) {
+  if (!c || !Y || r < 1 || r > XM_MAX_R) return XM_EINVAL;
+  return guard(c, [&] {
+    require_stage(c, 1);
+    int64_t len = (int64_t)c->n * r;
+    copy_in(c, c->hY.p, Y, len * 8);
+    spmm_full(c, c->hY.p, r, c->hQY.p, nullptr);
+    grad_and_multipliers(c, r, c->hY.p, c->hQY.p, c->hO.p, c->scal.p + 20);
+    if (grad) copy_out(c, grad, c->hO.p, len * 8);
+    if (f) read_scal(c, 20, 1, f);
+    sync(c);
+    c->cert_valid = false;  // Λ buffer now holds the hook's multipliers
+  });
+}
+
+xm_status xm_hvp(xm_ctx* c, const double* Y, const double* V, double* HV, int32_t r) {
+  if (!c || !Y || !V || !HV || r < 1 || r > XM_MAX_R) return XM_EINVAL;
+  return guard(c, [&] {
+    require_stage(c, 1);
+    int64_t len = (int64_t)c->n * r;
+    copy_in(c, c->hY.p, Y, len * 8);
+    copy_in(c, c->hV.p, V, len * 8);
+    spmm_full(c, c->hY.p, r, c->hQY.p, nullptr);
+    grad_and_multipliers(c, r, c->hY.p, c->hQY.p, c->hO.p, c->scal.p + 20);
+    spmm_full(c, c->hV.p, r, c->hQY.p, nullptr);
+    hvp_epilogue(c, r, c->hY.p, c->hV.p, c->hQY.p, c->hO.p, nullptr, nullptr);
+    copy_out(c, HV, c->hO.p, len * 8);
+    sync(c);
+    c->cert_valid = false;
+  });
+}
+
+xm_status xm_project(xm_ctx* c, const double* Y, const double* W, double* out, int32_t r) {
+  if (!c || !Y || !W || !out || r < 1 || r > XM_MAX_R) return XM_EINVAL;
+  return guard(c, [&] {
+    require_stage(c, 1);
+    int64_t len = (int64_t)c->n * r;
+    copy_in(c, c->hY.p, Y, len * 8);
+    copy_in(c, c->hV.p, W, len * 8);
+    project(c, r, c->hY.p, c->hV.p, c->hO.p);
+    copy_out(c, out, c->hO.p, len * 8);
+    sync(c);
+  });
+}
+
+xm_status xm_retract(xm_ctx* c, const double* Y, const double* V, double* out, int32_t r) {
+  if (!c || !Y || !V || !out || r < 1 || r > XM_MAX_R) return XM_EINVAL;
+  return guard(c, [&] {
+    require_stage(c, 1);
+    int64_t len = (int64_t)c->n * r;
+    copy_in(c, c->hY.p, Y, len * 8);
+    copy_in(c, c->hV.p, V, len * 8);
+    XM_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int), c->stream));
+    retract(c, r, c->hY.p, c->hV.p, 1.0, c->hO.p, nullptr, c->flags.p);
+    int err = 0;
+    XM_CUDA(cudaMemcpyAsync(&err, c->flags.p, 4, cudaMemcpyDeviceToHost, c->stream));
+    copy_out(c, out, c->hO.p, len * 8);
+    sync(c);
+    if (err) throw Error(XM_ERETRACT, "retraction failure");
+  });
+}
+
+xm_status xm_get_factor(xm_ctx* c, double* Y, int32_t* r) {
+  if (!c) return XM_EINVAL;
+  return guard(c, [&] {
+    if (r) *r = c->r;
+    if (Y && c->r > 0) copy_out(c, Y, c->Y.p, (size_t)c->n * c->r * 8);
+    sync(c);
+  });
+}
+
+xm_status xm_set_factor(xm_ctx* c, const double* Y, int32_t r) {
+  if (!c || !Y || r < 3 || r > XM_MAX_R) return XM_EINVAL;
+  return guard(c, [&] {
+    require_stage(c, 1);
+    c->r = r;
+    copy_in(c, c->Y.p, Y, (size_t)c->n * r * 8);
+    sync(c);
+    c->factor_set = true;
+    c->cert_valid = false;
+    c->have_round = false;
+  });
+}
+
+xm_status xm_get_stats(xm_ctx* c, xm_stats* out) {
+  if (!c || !out) return XM_EINVAL;
+  return guard(c, [&] {
+    harvest_events(c);
+    *out = c->stats;
+  });
+}
+
+xm_status xm_reset_stats(xm_ctx* c) {
+  if (!c) return XM_EINVAL;
+  return guard(c, [&] {
+    harvest_events(c);
+    int64_t E = c->stats.E, nd = c->stats.n_dup, nz = c->stats.nnzb_S, qb = c->stats.q_bytes;
+    c->stats = xm_stats{};
+    c->stats.E = E;
+    c->stats.n_dup = nd;
+    c->stats.nnzb_S = nz;
+    c->stats.q_bytes = qb;
+  });
+}
+
+const char* xm_last_error(xm_ctx* c) { return c ? c->last_error.c_str() : ""; }
+
+}  // extern "C"

@@ -1,0 +1,253 @@
+// xm_internal.cuh — shared declarations of libxm (B200 / sm_100a, fp64).
+//
+// Citations: P:n = PAPER.md line n; S:n = SPEC.md line n; SURVEY §8 rows H1..H13.
+// Nothing here is shared with oracle/ (the CPU oracle is independent).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/xm.h"
+
+#define XM_MAX_R 12
+
+namespace xm {
+
+// ---------------------------------------------------------------- errors
+struct Error : public std::runtime_error {
+  xm_status code;
+  Error(xm_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define XM_CUDA(call)                                                                \
+  do {                                                                               \
+    cudaError_t e__ = (call);                                                        \
+    if (e__ != cudaSuccess)                                                          \
+      throw ::xm::Error(XM_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e__)); \
+  } while (0)
+
+#define XM_CHECK_LAUNCH() XM_CUDA(cudaGetLastError())
+
+// ---------------------------------------------------------------- device buffers
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    if (count <= n && p) return;
+    release();
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+      throw Error(XM_ENOMEM, "cudaMalloc " + std::to_string(count * sizeof(T)) + " bytes");
+    }
+    n = count;
+  }
+  operator T*() const { return p; }
+  T* get() const { return p; }
+};
+
+// ---------------------------------------------------------------- tCG device state
+// All trust-region / tCG scalars live in device memory so that the inner loop
+// can run without host round trips (kernels read α, β, τ from here).
+struct TcgState {
+  double Delta;      // TR radius
+  double z, z_old, r0, e_Pe, e_Pd, d_Pd;
+  double alpha, beta, tau, d_Hd, e_Pe_new;
+  double kappa, theta;
+  int j;             // completed iterations
+  int max_inner;
+  int stop;          // 0 running, 1 negcurv, 2 exceeded, 3 converged, 4 maxinner
+  int boundary;      // this iteration steps to the TR boundary
+  int n_hvp;
+  int pad;
+};
+
+enum { TCG_RUNNING = 0, TCG_NEGCURV = 1, TCG_EXCEEDED = 2, TCG_CONVERGED = 3, TCG_MAXINNER = 4 };
+
+// ---------------------------------------------------------------- launch helpers
+struct Launcher;  // fwd
+
+}  // namespace xm
+
+// The context (opaque in the ABI).
+struct xm_ctx {
+  int device = 0, rank = 0, world = 1;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  xm_options opt{};
+  xm_stats stats{};
+  int stage = 0;  // 0 created, 1 Q built, 2 solved
+
+  // problem
+  int N = 0, M = 0;
+  int64_t E = 0;      // after de-duplication
+  int n = 0;          // 3N
+  int64_t ldq = 0;    // leading dimension of Q / G rows (padded to 32 doubles)
+  int64_t ldk = 0;    // leading dimension of K̄ / L
+  // sharding: frames [f0, f1) → rows [row0, row0 + nrows)
+  int nfpr = 0, f0 = 0, f1 = 0, row0 = 0, nrows = 0;
+  double normQ = 0.0, normQ2_local = 0.0;
+
+  // canonical edges (sorted by (landmark, frame))
+  xm::DBuf<int32_t> e_fr, e_lm;
+  xm::DBuf<double> e_pts, e_w;
+  xm::DBuf<int32_t> lm_off, fr_off, fr_edge;  // track / frame offsets, frame-sorted edge ids
+  xm::DBuf<double> W;                        // per-landmark weight Σ w_e (Q_3 diag)
+  // S pattern
+  xm::DBuf<int64_t> s_rowptr;
+  xm::DBuf<int32_t> s_colidx;
+  int64_t nnzb = 0;
+  // dense assembly products
+  xm::DBuf<double> Q;   // nrows × ldq (this rank's rows)
+  xm::DBuf<double> L;   // (N−1) × ldk  Cholesky of K̄
+  xm::DBuf<double> G;   // (N−1) × ldq  L⁻¹ C̄
+  bool have_recovery = false;  // L, G valid (false after xm_set_Q)
+
+  // solver state (all n_alloc × r row-major, replicated on every rank)
+  int r = 0;
+  int64_t n_alloc = 0;  // rows allocated for vectors (≥ world·3·nfpr)
+  xm::DBuf<double> Y, QY, grad, eta, Heta, res, dir, Hdir, Ynew, Dv, QD, tmp, tmp2;
+  xm::DBuf<double> alpha;  // N
+  xm::DBuf<double> lam;    // N × 6 (xx, yy, zz, xy, xz, yz)
+  xm::DBuf<double> part;   // SpMM split-K partials: nsplit × nrows × r
+  xm::DBuf<double> red;    // block partials for reductions
+  xm::DBuf<double> scal;   // reduced scalars (device)
+  xm::DBuf<xm::TcgState> tcg;
+  xm::DBuf<int> flags;     // error flags etc.
+  xm::DBuf<double> hostbuf_dummy;
+  double* h_scal = nullptr;  // pinned host mirror of scal
+  xm::TcgState* h_tcg = nullptr;
+  int* h_flags = nullptr;
+  bool factor_set = false;
+  // Lanczos
+  xm::DBuf<double> lz_V, lz_w, lz_c, lz_part, lz_x;
+  double last_lambda = 0.0;
+  int last_lanczos_steps = 0;
+  bool have_cert = false;
+  xm_certificate cert{};
+  xm_solve_info info{};
+  // rounding
+  xm::DBuf<double> Yr;  // n × 3 rounded factor
+  xm::DBuf<double> Rs;  // N × 9, s N, t N×3, p M×3
+  xm::DBuf<double> s_out, t_out, p_out, rhs;
+  int n_flipped = 0;
+  bool have_round = false;
+  // profiling
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  // NCCL
+  void* nccl_comm = nullptr;
+  xm::DBuf<double> gbuf;  // all-gather staging
+  // hooks (test / bench entry points) use their own scratch
+  xm::DBuf<double> hY, hV, hO, hQY;
+  // certificate cache (valid while the factor is unchanged)
+  bool cert_valid = false;
+  double cert_lambda = 0.0;
+  int cert_steps = 0;
+  xm::DBuf<double> cert_v;
+  int tcg_batch = 4;
+  std::string last_error;
+};
+
+namespace xm {
+
+inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+inline int64_t round_up(int64_t a, int64_t b) { return ((a + b - 1) / b) * b; }
+
+// Pointer helpers: copy between caller memory (host or device) and device.
+bool is_device_ptr(const void* p);
+void copy_in(xm_ctx* c, void* dst_dev, const void* src, size_t bytes);
+void copy_out(xm_ctx* c, void* dst, const void* src_dev, size_t bytes);
+void sync(xm_ctx* c);
+inline void count_launch(xm_ctx* c, int k = 1) { c->stats.kernel_launches += k; }
+
+// ------------------------------------------------------------ util kernels (util.cu)
+// Deterministic reductions: blocks write partials, one block reduces in fixed order.
+// min_mask: bit c set ⇒ component c is reduced with min instead of sum.
+void reduce_partials(xm_ctx* c, const double* partials, int nblk, int ncomp, double* out,
+                     unsigned min_mask = 0u);
+void exclusive_scan_i32(xm_ctx* c, const int32_t* in, int32_t* out, int64_t n, int32_t* total_dev);
+void radix_sort_u64(xm_ctx* c, uint64_t* keys, uint32_t* vals, int64_t n, int bits,
+                    DBuf<uint64_t>& tmp_k, DBuf<uint32_t>& tmp_v);
+void dot_flat(xm_ctx* c, const double* a, const double* b, int64_t len, double* partials, int nblk);
+constexpr int kDotBlocks = 296;  // 2 × 148 SMs; fixed ⇒ deterministic sums
+
+// ------------------------------------------------------------ assembly (assembly.cu)
+void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr, const int32_t* lm,
+                    const double* pts, const double* w);
+void dense_cholesky(xm_ctx* c, double* A, int m, int64_t lda, double pivot_tol);
+void dense_trsm_lower_left(xm_ctx* c, const double* L, int m, int64_t ldl, double* B, int ncols,
+                           int64_t ldb);
+void dgemm(xm_ctx* c, bool ta, bool tb, bool lower, int M, int N, int K, double alpha,
+           const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+           int64_t ldc);
+void mirror_lower(xm_ctx* c, double* Q, int n, int64_t ldq);
+
+// ------------------------------------------------------------ SpMM (spmm.cu)
+struct SpmmPlan {
+  int nsplit = 1, kc = 0, nrowblk = 1, rpw = 4;
+};
+SpmmPlan spmm_plan(xm_ctx* c, int r);
+// part[split][row][c] for this rank's rows; if stop != nullptr the kernel is a
+// no-op when *stop != 0 (speculative tCG batches).
+void spmm_partial(xm_ctx* c, const double* V, int r, double* part, const SpmmPlan& pl,
+                  const int* stop);
+// out (full vector layout, this rank's rows written then all-gathered) = Σ_split part.
+void spmm_reduce(xm_ctx* c, const double* part, int r, const SpmmPlan& pl, double* out_full,
+                 const int* stop);
+void harvest_events(xm_ctx* c);
+// Full product into out (n × r, replicated): partial + reduce + all-gather.
+void spmm_full(xm_ctx* c, const double* V, int r, double* out_full, const int* stop = nullptr);
+void allgather_rows(xm_ctx* c, double* full, int r);
+
+// ------------------------------------------------------------ manifold (manifold.cu)
+// grad = 2(QY − ΛY); α, Λ from (Y, QY); red ← [f, ‖g‖², s_min²] partials.
+void grad_and_multipliers(xm_ctx* c, int r, const double* Y, const double* QY, double* grad,
+                          double* scal_out /*3*/);
+void project(xm_ctx* c, int r, const double* Y, const double* W, double* out);
+void retract(xm_ctx* c, int r, const double* Y, const double* V, double step, double* Yout,
+             double* D, int* err);
+// HV = P(2·QV − 2ΛV), partial ⟨V, HV⟩ into red; QV given as a full n×r array.
+void hvp_epilogue(xm_ctx* c, int r, const double* Y, const double* V, const double* QV,
+                  double* HV, double* dot_out /*1*/, const int* stop);
+// tCG device-side steps
+void tcg_init(xm_ctx* c, int r, double Delta);
+void tcg_ctrl_a(xm_ctx* c);
+void tcg_update(xm_ctx* c, int r);
+void tcg_ctrl_b(xm_ctx* c);
+void tcg_dir(xm_ctx* c, int r);
+void axpy(xm_ctx* c, int64_t len, double a, const double* x, double* y);
+void pad_column(xm_ctx* c, int r, const double* Y, double* Yz, const double* v, double* Dz);
+void zmul(xm_ctx* c, const double* x, const double* Zx_q, double* out);  // Zx = Qx − Λx (r = 1)
+double min_scale(xm_ctx* c, int r, const double* Y);
+
+// ------------------------------------------------------------ Lanczos / rounding (cert.cu)
+void lanczos(xm_ctx* c, double tol_abs, int max_steps, double* lambda, int* steps,
+             double* vec_dev);
+void round_recover_device(xm_ctx* c);
+
+// ------------------------------------------------------------ NCCL (comm.cu)
+void nccl_unique_id(void* out128);
+void nccl_init(xm_ctx* c, const void* id);
+void nccl_destroy(xm_ctx* c);
+void nccl_allgather(xm_ctx* c, const double* send, double* recv, size_t count_per_rank);
+void nccl_allreduce_sum(xm_ctx* c, double* buf, size_t count);
+
+}  // namespace xm
