@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""Benchmark of the XM hot path on B200 (BASELINE.json metric:
+"solve-to-certificate seconds & HVP/s; SpMM HBM GB/s vs peak").
+
+One STEP = one pass of the whole hot path (SURVEY §8(a) H1–H13) over one
+synthetic view graph: xm_build_Q → xm_solve (staircase, every rank certified
+with Lanczos) → xm_certify → xm_round_recover.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config B] [--impl xm|reference]
+
+Multi-GPU (N > 1) is launched by torchrun; Q rows are sharded across ranks
+and the library all-gathers Q·V shards with NCCL (strong scaling: the total
+work is fixed).  Timing: CUDA events on the library's stream (torch's current
+stream is passed to xm_create), barrier + synchronize around the K timed steps,
+max over ranks.  Inputs (Q is 288 MB at config B, 7.4 GB at E) are larger than
+the 126 MB L2, so no explicit flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback ("of fallback")
+COUNTS_FILE = os.path.join(ROOT, "profiles", "workload_counts.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "spmm_traffic.json")
+METRIC = "solve_to_certificate_s"
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_FILE) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.gpu_idle,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.fh,
+                stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        try:
+            rows = [l.strip().split(", ") for l in open(self.path) if l.strip()]
+        except Exception:
+            rows = []
+        names = ["gpu_idle", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        sm, mx, reasons = [], 0.0, set()
+        for r in rows:
+            if len(r) < 7:
+                continue
+            try:
+                cur, m = float(r[0]), float(r[1])
+            except ValueError:
+                continue
+            mx = max(mx, m)
+            act = {nm for nm, v in zip(names, r[2:7]) if v.strip().lower() == "active"}
+            if "gpu_idle" not in act:
+                sm.append(cur)
+            reasons |= act - {"gpu_idle"}
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- oracle timing
+def load_counts(cfg):
+    try:
+        with open(COUNTS_FILE) as f:
+            return json.load(f).get(cfg)
+    except Exception:
+        return None
+
+
+def oracle_sample(scene, hvps: int, lanczos_steps: int, spmms: int, n_hvp_sample=12,
+                  n_lz_sample=24):
+    """Time the oracle as it stands on this host on a bounded sample of the
+    workload: the full oracle Q build (validate + Schur complement) plus
+    n_hvp_sample oracle Hessian-vector products and n_lz_sample oracle Lanczos
+    steps at the workload's size, scaled to the solve's counts."""
+    import numpy as np
+    from oracle import xm_oracle as xo
+    t0 = time.perf_counter()
+    dm = xo.build_Q(scene.N, scene.M, scene.frame, scene.landmark, scene.pts, scene.w)
+    t_build = time.perf_counter() - t0
+    n = dm.n
+    Y = np.zeros((n, 3))
+    for i in range(scene.N):
+        Y[3 * i:3 * i + 3, :] = np.eye(3)
+    g, Lam = xo.rgrad(Y, dm.Q @ Y)
+    t0 = time.perf_counter()
+    for _ in range(n_hvp_sample):
+        xo.hess(dm.Q, Y, Lam, g)
+    t_hvp = (time.perf_counter() - t0) / n_hvp_sample
+
+    def apply_Z(x):
+        X = x.reshape(-1, 1)
+        return (dm.Q @ X - xo.block_apply(Lam, X)).ravel()
+    t0 = time.perf_counter()
+    xo.lanczos_min_eig(apply_Z, n, 0.0, max_steps=n_lz_sample)
+    t_lz = (time.perf_counter() - t0) / n_lz_sample
+    est = t_build + t_hvp * max(spmms - lanczos_steps, hvps) + t_lz * lanczos_steps
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([p.get("num_threads", 1) for p in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count() or 1
+    sample = (f"oracle build_Q on the full workload ({t_build:.2f}s) + {n_hvp_sample} oracle HVPs "
+              f"({t_hvp*1e3:.1f} ms each) + {n_lz_sample} oracle Lanczos steps ({t_lz*1e3:.1f} ms "
+              f"each), scaled to {max(spmms - lanczos_steps, hvps)} products + {lanczos_steps} "
+              f"Lanczos steps of the solve")
+    return est, cores, sample
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from synth.scenes import CONFIG_DESCRIPTIONS, config_scene
+    sc = config_scene(args.config, seed=args.seed)
+    counts = load_counts(args.config) or {"hvps": 12000, "lanczos_steps": 1000, "spmms": 25000}
+    times = []
+    for i in range(args.warmup + args.steps):
+        est, cores, sample = oracle_sample(sc, counts["hvps"], counts["lanczos_steps"],
+                                           counts["spmms"], n_hvp_sample=4 if i < args.warmup else 12,
+                                           n_lz_sample=8 if i < args.warmup else 24)
+        if i >= args.warmup:
+            times.append(est)
+    v = sum(times) / len(times)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"config {args.config}: {CONFIG_DESCRIPTIONS[args.config]}",
+                       "N": sc.N, "M": sc.M, "E": sc.E, "seed": args.seed,
+                       "counts_source": "profiles/workload_counts.json (GPU solve of the same scene)"},
+            "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- xm arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="B", choices=list("ABCDE"))
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--impl", default="xm", choices=["xm", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    from paper_2502_04640_b200 import xm
+    from synth.scenes import CONFIG_DESCRIPTIONS, config_scene
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    nccl_id = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        obj = [xm.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    sc = config_scene(args.config, seed=args.seed)
+    dev = torch.device("cuda", local)
+    d_fr = torch.from_numpy(sc.frame).to(dev)
+    d_lm = torch.from_numpy(sc.landmark).to(dev)
+    d_pts = torch.from_numpy(sc.pts).to(dev)
+    d_w = torch.from_numpy(sc.w).to(dev)
+    out_dev = dict(R=torch.empty((sc.N, 3, 3), dtype=torch.float64, device=dev),
+                   s=torch.empty(sc.N, dtype=torch.float64, device=dev),
+                   t=torch.empty((sc.N, 3), dtype=torch.float64, device=dev),
+                   p=torch.empty((sc.M, 3), dtype=torch.float64, device=dev))
+    stream = torch.cuda.current_stream(dev)
+    ctx = xm.Context(device=local, rank=rank, world=world, nccl_id=nccl_id,
+                     stream=stream.cuda_stream, profile=1)
+
+    def step(inputs, outputs):
+        ctx.build_Q(sc.N, sc.M, *inputs)
+        st, info = ctx.solve(3)
+        cert = ctx.certify()
+        ctx.round_recover_into(**outputs)
+        return st, info, cert
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    dev_in = (d_fr, d_lm, d_pts, d_w)
+    for _ in range(args.warmup):
+        step(dev_in, out_dev)
+    torch.cuda.synchronize()
+    ctx.reset_stats()
+    infos = []
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            infos.append(step(dev_in, out_dev))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    stats = ctx.stats()
+    if dist is not None:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- end to end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        h_in = tuple(torch.from_numpy(a).pin_memory() for a in (sc.frame, sc.landmark, sc.pts, sc.w))
+        out_host = {k: torch.empty(v.shape, dtype=torch.float64).pin_memory() for k, v in out_dev.items()}
+        step(h_in, out_host)
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            step(h_in, out_host)
+        torch.cuda.synchronize()
+        barrier()
+        e2e_s = (time.perf_counter() - t0) / args.steps
+        if dist is not None:
+            t = torch.tensor([e2e_s], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": e2e_s, "unit": "s",
+               "h2d_bytes_per_step": int(sum(a.numel() * a.element_size() for a in h_in)),
+               "d2h_bytes_per_step": int(sum(v.numel() * 8 for v in out_host.values()))}
+
+    st, info, cert = infos[-1]
+    value = ms / 1e3
+    spmm_ms_per_launch = stats["spmm_ms"] / max(stats["spmm_timed"], 1)
+    bytes_per_launch = stats["spmm_alg_bytes"] / max(stats["spmm_timed"], 1)
+    achieved = bytes_per_launch / (spmm_ms_per_launch / 1e3) / 1e9 if stats["spmm_timed"] else None
+    peak, peak_kind = hbm_peak()
+    traffic = None
+    try:
+        with open(TRAFFIC_FILE) as f:
+            traffic = json.load(f).get(args.config, {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    spmm_share = stats["spmm_ms"] / (ms * args.steps) if ms > 0 else None
+    result = {
+        "metric": METRIC, "value": value, "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config {args.config}: {CONFIG_DESCRIPTIONS[args.config]}",
+                   "N": sc.N, "M": sc.M, "E": sc.E, "seed": args.seed,
+                   "parallelism": f"rows{world}", "l2": "inputs larger than L2 (Q > 126 MB)"},
+        "hvp_per_s": info["hvps"] / value if value > 0 else None,
+        "solve": {"hvps": info["hvps"], "spmms": info["spmms"], "lanczos_steps": info["lanczos_steps"],
+                  "outer_iters": info["outer_iters"], "r": info["r"], "escapes": info["escapes"],
+                  "certified": info["certified"], "f": info["f"], "s_min": info["s_min"],
+                  "lambda_min": cert["lambda_min"], "lambda_min_rel": cert["lambda_min"] / max(1.0, cert["normQ"]),
+                  "eta": cert["eta"], "rho_hat": cert["rho_hat"], "status": st},
+        "phases_ms": {k: stats[k] / args.steps for k in ("ms_build", "ms_solve", "ms_certify", "ms_round")},
+        "roofline": {"kernel": "k_spmm_partial (Q·V)", "bound": "hbm", "achieved": achieved,
+                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "alg_bytes_per_launch": bytes_per_launch, "launch_ms": spmm_ms_per_launch,
+                     "launches": stats["spmm_timed"], "share_of_step": spmm_share},
+        "gpu_launches": int(stats["kernel_launches"]),
+        "e2e": e2e,
+    }
+    if rank == 0:
+        os.makedirs(os.path.dirname(COUNTS_FILE), exist_ok=True)
+        try:
+            counts = json.load(open(COUNTS_FILE)) if os.path.exists(COUNTS_FILE) else {}
+        except Exception:
+            counts = {}
+        counts[args.config] = {"hvps": info["hvps"], "spmms": info["spmms"],
+                               "lanczos_steps": info["lanczos_steps"], "N": sc.N}
+        with open(COUNTS_FILE, "w") as f:
+            json.dump(counts, f, indent=1)
+    clocks = clk.summary()
+    result["clocks"] = clocks
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        est, cores, sample = oracle_sample(sc, info["hvps"], info["lanczos_steps"], info["spmms"])
+        result["cpu_baseline"] = {"value": est, "unit": "s", "cores": cores, "kind": "oracle",
+                                  "sample": sample}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    ctx.close()
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

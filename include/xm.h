@@ -130,6 +130,8 @@ typedef struct {
   int64_t spmm_rows;         /* Q rows streamed per call on this rank            */
   double spmm_ms;            /* Σ CUDA-event time of SpMM launches (profile=1)  */
   int64_t spmm_timed;        /* number of SpMM launches included in spmm_ms      */
+  double spmm_alg_bytes;     /* Σ algorithmic bytes of those launches:           */
+                             /*   8·(nrows·n + n·r + nrows·r) each               */
   double ms_build, ms_solve, ms_certify, ms_round;  /* host wall per phase        */
   int64_t n_dup;             /* duplicate observations dropped (keep first)     */
   int64_t E;                 /* observations after de-duplication                */

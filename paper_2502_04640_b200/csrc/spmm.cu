@@ -29,8 +29,10 @@ constexpr int kSpmmWarps = kSpmmThreads / 32;
 template <int R, int RPW>
 __global__ void __launch_bounds__(kSpmmThreads) k_spmm_partial(
     const double* __restrict__ Q, int64_t ldq, int nrows, int n, const double* __restrict__ V,
-    int kc, int nrowblk, double* __restrict__ part, const int* __restrict__ stop) {
+    int kc, int nrowblk, double* __restrict__ part, const int* __restrict__ stop,
+    int* __restrict__ exec_flag) {
   if (stop && *stop) return;
+  if (exec_flag && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *exec_flag = 1;
   extern __shared__ __align__(16) double vt[];  // [R][kc]
   const int rb = blockIdx.x, split = blockIdx.y;
   const int k0 = split * kc;
@@ -142,7 +144,7 @@ SpmmPlan spmm_plan(xm_ctx* c, int r) {
 
 template <int R>
 static void launch_partial_r(xm_ctx* c, const double* V, double* part, const SpmmPlan& pl,
-                             const int* stop) {
+                             const int* stop, int* exec) {
   dim3 grid(pl.nrowblk, pl.nsplit);
   size_t smem = (size_t)R * pl.kc * 8;
   auto run = [&](auto kern) {
@@ -152,7 +154,7 @@ static void launch_partial_r(xm_ctx* c, const double* V, double* part, const Spm
     }
     attr_set = true;
     kern<<<grid, kSpmmThreads, smem, c->stream>>>(c->Q.p, c->ldq, c->nrows, c->n, V, pl.kc,
-                                                  pl.nrowblk, part, stop);
+                                                  pl.nrowblk, part, stop, exec);
   };
   constexpr int RPW = (R == 1) ? 8 : (R <= 6 ? 4 : 2);  // = rpw_for(R)
   if (pl.rpw != RPW) throw Error(XM_EINVAL, "spmm plan / kernel mismatch");
@@ -162,9 +164,9 @@ static void launch_partial_r(xm_ctx* c, const double* V, double* part, const Spm
 }
 
 void spmm_partial(xm_ctx* c, const double* V, int r, double* part, const SpmmPlan& pl,
-                  const int* stop) {
+                  const int* stop, int* exec) {
   switch (r) {
-#define XM_R(RR) case RR: launch_partial_r<RR>(c, V, part, pl, stop); break;
+#define XM_R(RR) case RR: launch_partial_r<RR>(c, V, part, pl, stop, exec); break;
     XM_R(1) XM_R(2) XM_R(3) XM_R(4) XM_R(5) XM_R(6) XM_R(7) XM_R(8) XM_R(9) XM_R(10) XM_R(11)
     XM_R(12)
 #undef XM_R
@@ -194,13 +196,22 @@ void spmm_full(xm_ctx* c, const double* V, int r, double* out_full, const int* s
         XM_CUDA(cudaEventCreate(&e));
         c->ev_pool.push_back(e);
       }
+      c->ev_exec.alloc(512);
+      c->ev_bytes.assign(512, 0.0);
+      XM_CUDA(cudaMemsetAsync(c->ev_exec.p, 0, 512 * sizeof(int), c->stream));
     }
     if (c->ev_used + 2 > c->ev_pool.size()) harvest_events(c);
     e0 = c->ev_pool[c->ev_used++];
     e1 = c->ev_pool[c->ev_used++];
     XM_CUDA(cudaEventRecord(e0, c->stream));
   }
-  spmm_partial(c, V, r, c->part.p, pl, stop);
+  int* exec = nullptr;
+  if (timed) {
+    size_t pair = c->ev_used / 2 - 1;
+    exec = c->ev_exec.p + pair;
+    c->ev_bytes[pair] = 8.0 * ((double)c->nrows * c->n + (double)c->n * r + (double)c->nrows * r);
+  }
+  spmm_partial(c, V, r, c->part.p, pl, stop, exec);
   if (timed) XM_CUDA(cudaEventRecord(e1, c->stream));
   spmm_reduce(c, c->part.p, r, pl, out_full, stop);
   if (c->world > 1) allgather_rows(c, out_full, r);
@@ -213,12 +224,17 @@ void spmm_full(xm_ctx* c, const double* V, int r, double* out_full, const int* s
 void harvest_events(xm_ctx* c) {
   if (c->ev_used == 0) return;
   XM_CUDA(cudaEventSynchronize(c->ev_pool[c->ev_used - 1]));
+  std::vector<int> exec(c->ev_used / 2);
+  XM_CUDA(cudaMemcpy(exec.data(), c->ev_exec.p, exec.size() * sizeof(int), cudaMemcpyDeviceToHost));
   for (size_t q = 0; q + 1 < c->ev_used; q += 2) {
+    if (!exec[q / 2]) continue;  // speculative launch that early-exited (tCG already stopped)
     float ms = 0.f;
     XM_CUDA(cudaEventElapsedTime(&ms, c->ev_pool[q], c->ev_pool[q + 1]));
     c->stats.spmm_ms += ms;
     c->stats.spmm_timed++;
+    c->stats.spmm_alg_bytes += c->ev_bytes[q / 2];
   }
+  XM_CUDA(cudaMemsetAsync(c->ev_exec.p, 0, 512 * sizeof(int), c->stream));
   c->ev_used = 0;
 }
 

@@ -152,6 +152,8 @@ struct xm_ctx {
   // profiling
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
+  xm::DBuf<int> ev_exec;           // per event pair: 1 if the SpMM actually ran
+  std::vector<double> ev_bytes;    // per event pair: algorithmic bytes
   // NCCL
   void* nccl_comm = nullptr;
   xm::DBuf<double> gbuf;  // all-gather staging
@@ -208,7 +210,7 @@ SpmmPlan spmm_plan(xm_ctx* c, int r);
 // part[split][row][c] for this rank's rows; if stop != nullptr the kernel is a
 // no-op when *stop != 0 (speculative tCG batches).
 void spmm_partial(xm_ctx* c, const double* V, int r, double* part, const SpmmPlan& pl,
-                  const int* stop);
+                  const int* stop, int* exec = nullptr);
 // out (full vector layout, this rank's rows written then all-gathered) = Σ_split part.
 void spmm_reduce(xm_ctx* c, const double* part, int r, const SpmmPlan& pl, double* out_full,
                  const int* stop);

@@ -61,7 +61,7 @@ class Certificate(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [("kernel_launches", ctypes.c_int64), ("spmm_calls", ctypes.c_int64),
                 ("spmm_rows", ctypes.c_int64), ("spmm_ms", ctypes.c_double),
-                ("spmm_timed", ctypes.c_int64), ("ms_build", ctypes.c_double),
+                ("spmm_timed", ctypes.c_int64), ("spmm_alg_bytes", ctypes.c_double), ("ms_build", ctypes.c_double),
                 ("ms_solve", ctypes.c_double), ("ms_certify", ctypes.c_double),
                 ("ms_round", ctypes.c_double), ("n_dup", ctypes.c_int64), ("E", ctypes.c_int64),
                 ("nnzb_S", ctypes.c_int64), ("q_bytes", ctypes.c_int64)]
@@ -244,6 +244,16 @@ class Context:
                                        p.ctypes.data, ctypes.byref(nf))
         self._check(st, "xm_round_recover")
         return dict(R=R, s=s, t=t, p=p[: self.M], n_flipped=int(nf.value))
+
+    def round_recover_into(self, R, s, t, p):
+        """Same as round_recover, writing into caller buffers (torch tensors on
+        the device or pinned host, or numpy arrays)."""
+        def ptr(x):
+            return ctypes.c_void_p(x.data_ptr() if _is_torch(x) else x.ctypes.data)
+        nf = ctypes.c_int32()
+        st = self.lib.xm_round_recover(self.h, ptr(R), ptr(s), ptr(t), ptr(p), ctypes.byref(nf))
+        self._check(st, "xm_round_recover")
+        return int(nf.value)
 
     # ------------------------------------------------------------------ hooks
     def S_pattern(self):
