@@ -14,7 +14,9 @@
 // one CTA that accumulates landmarks in ascending order.
 #include "xm_internal.cuh"
 
+#include <chrono>
 #include <cmath>
+#include <cstdlib>
 
 namespace xm {
 
@@ -591,6 +593,17 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
   if (N < 1 || M < 1 || E < 1) throw Error(XM_EINVAL, "empty view graph");
   if (E >= (int64_t)INT32_MAX) throw Error(XM_EINVAL, "too many observations");
   const int T = 256;
+  const bool verbose = std::getenv("XM_VERBOSE") != nullptr;
+  double tph = 0.0;
+  auto phase = [&](const char* nm) {
+    if (!verbose) return;
+    sync(c);
+    double t = std::chrono::duration<double, std::milli>(
+                   std::chrono::steady_clock::now().time_since_epoch()).count();
+    if (tph > 0.0) fprintf(stderr, "[xm build] %-14s %9.3f ms\n", nm, t - tph);
+    tph = t;
+  };
+  phase("start");
   // stage inputs on the device
   DBuf<int32_t> d_fr, d_lm;
   DBuf<double> d_pts, d_w;
@@ -622,6 +635,7 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
   int bits_fl = 1;
   while (bits_fl < 64 && ((uint64_t)N * (uint64_t)M) > (1ull << bits_fl)) ++bits_fl;
   radix_sort_u64(c, key.p, val.p, E, bits_fl, tk, tv);
+  phase("validate+sort1");
   // ---- dedupe (stable sort ⇒ the first occurrence of a key is the earliest input)
   DBuf<int32_t> flag, pos;
   flag.alloc(E);
@@ -645,6 +659,7 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
                                                    fs_fr.p, key2.p, val2.p);
   XM_CHECK_LAUNCH();
   count_launch(c);
+  phase("dedupe");
   // ---- H2: canonical (landmark, frame) order
   radix_sort_u64(c, key2.p, val2.p, Ek, bits_fl, tk, tv);
   c->e_fr.alloc(Ek);
@@ -677,6 +692,7 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
   XM_CHECK_LAUNCH();
   count_launch(c);
 
+  phase("sort2+offsets");
   // ---- connectivity: frames ∪ observed landmarks must form one component
   {
     DBuf<int32_t> parent;
@@ -684,7 +700,9 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
     k_cc_init<<<ceil_div(N + M, T), T, 0, c->stream>>>(N + M, parent.p);
     count_launch(c);
     int* d_changed = c->flags.p + 8;
+    int cc_iters = 0;
     for (int it = 0; it < 100000; ++it) {
+      cc_iters = it + 1;
       XM_CUDA(cudaMemsetAsync(d_changed, 0, 4, c->stream));
       k_cc_hook<<<ceil_div(Ek, T), T, 0, c->stream>>>(Ek, N, c->e_fr.p, c->e_lm.p, parent.p, d_changed);
       k_cc_jump<<<ceil_div(N + M, T), T, 0, c->stream>>>(N + M, parent.p);
@@ -695,6 +713,7 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
       sync(c);
       if (!ch) break;
     }
+    if (verbose) fprintf(stderr, "[xm build] connectivity iterations: %d\n", cc_iters);
     int* d_cnt = c->flags.p + 12;
     XM_CUDA(cudaMemsetAsync(d_cnt, 0, 8, c->stream));
     k_cc_count<<<ceil_div(N + M, T), T, 0, c->stream>>>(N, M, parent.p, c->lm_off.p, fcnt.p, d_cnt);
@@ -707,6 +726,7 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
     if (h_cc[0] != 1) throw Error(XM_EDISCONNECTED, "graph numerically disconnected");
   }
 
+  phase("connectivity");
   // ---- H3: S pattern
   {
     int W32 = ceil_div(N, 32);
@@ -738,6 +758,7 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
     sync(c);
   }
 
+  phase("pattern");
   // ---- H4: dense S (own rows, in the Q buffer), C̄ (in the G buffer), K̄ (in L)
   const int n = 3 * N;
   c->N = N;
@@ -768,6 +789,7 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
   XM_CHECK_LAUNCH();
   count_launch(c);
 
+  phase("scatter");
   // ---- H5: K̄ = LLᵀ, G = L⁻¹C̄, Q = S − GᵀG
   if (N > 1) {
     // pivot test relative to max diag(K̄); a disconnected graph gives a ~0 pivot
@@ -781,6 +803,7 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
   } else if (c->world == 1) {
     mirror_lower(c, c->Q.p, n, c->ldq);
   }
+  phase("chol+trsm+syrk");
   c->have_recovery = true;
   // ‖Q‖_F (all-reduced over ranks)
   {
@@ -797,6 +820,7 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
     sync(c);
     c->normQ = std::sqrt(s2);
   }
+  phase("normQ");
   c->stats.E = c->E;
   c->stats.q_bytes = (int64_t)c->nrows * n * 8;
 }

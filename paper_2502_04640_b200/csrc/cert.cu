@@ -204,7 +204,7 @@ void lanczos(xm_ctx* c, double tol_abs, int max_steps, double* lambda, int* step
   c->lz_w.alloc(round_up(n, 32) * std::max(1, c->world) + 64);
   c->lz_c.alloc((size_t)2 * (kmax + 1) + 64);
   int nchunk_max = ceil_div(kmax + 1, kGemvChunk);
-  c->lz_part.alloc((size_t)nchunk_max * n + kDotBlocks * 4);
+  c->lz_part.alloc((size_t)nchunk_max * n + 4096);
   c->tmp.alloc((size_t)c->n_alloc * 4);
   double* alphas = c->lz_c.p;                    // device α_j
   double* betas = c->lz_c.p + (kmax + 1);        // device β_j
@@ -231,10 +231,19 @@ void lanczos(xm_ctx* c, double tol_abs, int max_steps, double* lambda, int* step
     for (; k < batch_end; ++k) {
       const double* vk = c->lz_V.p + (int64_t)k * ldv;
       // w = Z v_k = Q v_k − Λ v_k
-      spmm_full(c, vk, 1, c->tmp.p, nullptr);
-      zmul(c, vk, c->tmp.p, c->lz_w.p);
-      dot_flat(c, vk, c->lz_w.p, n, dots, kDotBlocks);
-      reduce_partials(c, dots, kDotBlocks, 1, alphas + k);
+      if (c->world == 1) {
+        SpmmEpiArgs ep{};
+        ep.out = c->lz_w.p;
+        ep.lam = c->lam.p;
+        ep.partials = dots;
+        spmm(c, vk, 1, EPI_ZMUL, ep);  // w = Qv − Λv, partials of ⟨v, w⟩
+        reduce_partials(c, dots, spmm_grid(c, 1), 1, alphas + k);
+      } else {
+        spmm_full(c, vk, 1, c->tmp.p, nullptr);
+        zmul(c, vk, c->tmp.p, c->lz_w.p);
+        dot_flat(c, vk, c->lz_w.p, n, dots, kDotBlocks);
+        reduce_partials(c, dots, kDotBlocks, 1, alphas + k);
+      }
       // full re-orthogonalisation against v_0..v_k, two passes
       for (int pass = 0; pass < 2; ++pass) {
         k_gemv_t<<<k + 1, 256, 0, c->stream>>>(c->lz_V.p, ldv, n, c->lz_w.p, cbuf.p);

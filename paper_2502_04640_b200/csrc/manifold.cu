@@ -1,10 +1,10 @@
-// manifold.cu — per-camera kernels of the BM Riemannian solve (H7–H10, H12).
+// manifold.cu — per-camera kernels of the BM Riemannian solve (H7–H10, H12)
+// and the device-resident truncated-CG iteration (H9).
 //
 // Manifold (Prop. 5): block 0 on St(r,3) (Y_0Y_0ᵀ = I), blocks
 // i ≥ 1 on ℝ₊ × St(r,3) (Y_iY_iᵀ = α_i I).  Tangent vectors are ambient 3×r
 // blocks with the Frobenius metric (reading C4).  One thread per camera: the
-// whole 3×r block (r ≤ 12) lives in registers; the r×r-free formulas below only
-// need the 3×3 matrix M = W Y_iᵀ.
+// whole 3×r block (r ≤ 12) lives in registers.
 //
 //   P_i(W)   = W − sym₀(W Y_iᵀ) Y_i / α_i        (i ≥ 1),   P_0(W) = W − sym(W Y_0ᵀ) Y_0
 //   Λ_i      = sym₀((QY)_i Y_iᵀ)/α_i, Λ_0 = sym((QY)_0 Y_0ᵀ)  (Thm 1 Eq. (18), App. A.4)
@@ -12,130 +12,19 @@
 //   Hess[V]  = P(2QV − 2ΛV)                                  (analytic HVP)
 //   Retr     : s′ = max(s + ⟨V_i,R̂⟩/3, c·s), R̂′ = MGS(R̂ + W/s)   (C6, C7)
 //
-// Sums (dots) are reduced deterministically: per-thread camera sums → fixed
-// block tree → per-block partials → one fixed-order final block.
-#include "xm_internal.cuh"
+// tCG (Steihaug–Toint in Manopt's form) runs as THREE kernels
+// per iteration with the scalar recurrences folded in: every block recomputes
+// the same scalar from the same partials in the same fixed order (so all blocks
+// agree bit for bit), and block 0 writes the next state into the other half of
+// a double-buffered TcgState — no host round trip, no separate control kernel:
+//   K1  Hδ = Hess[δ] (SpMM + fused epilogue), partials of ⟨δ, Hδ⟩
+//   K2  α, τ, boundary test; η += αδ, Hη += αHδ, r ← P(r + αHδ), partials ⟨r,r⟩
+//   K3  stop tests, β, e_Pd/d_Pd recurrences; δ ← −r + βδ
+#include "frame_ops.cuh"
 
 namespace xm {
 
 constexpr int kFT = 128;  // threads per block for per-frame kernels
-
-template <int R>
-struct Blk {
-  double v[3][R];
-};
-
-template <int R>
-__device__ __forceinline__ void load_blk(const double* __restrict__ X, int i, Blk<R>& b) {
-  const double* p = X + (int64_t)3 * i * R;
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int c = 0; c < R; ++c) b.v[a][c] = p[a * R + c];
-}
-template <int R>
-__device__ __forceinline__ void store_blk(double* __restrict__ X, int i, const Blk<R>& b) {
-  double* p = X + (int64_t)3 * i * R;
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int c = 0; c < R; ++c) p[a * R + c] = b.v[a][c];
-}
-// M = A Bᵀ (3×3)
-template <int R>
-__device__ __forceinline__ void mul_abt(const Blk<R>& A, const Blk<R>& B, double M[3][3]) {
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int b = 0; b < 3; ++b) {
-      double s = 0.0;
-#pragma unroll
-      for (int c = 0; c < R; ++c) s = fma(A.v[a][c], B.v[b][c], s);
-      M[a][b] = s;
-    }
-}
-template <int R>
-__device__ __forceinline__ double frob2(const Blk<R>& A) {
-  double s = 0.0;
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int c = 0; c < R; ++c) s = fma(A.v[a][c], A.v[a][c], s);
-  return s;
-}
-template <int R>
-__device__ __forceinline__ double dotb(const Blk<R>& A, const Blk<R>& B) {
-  double s = 0.0;
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int c = 0; c < R; ++c) s = fma(A.v[a][c], B.v[a][c], s);
-  return s;
-}
-// Λ = sym(M) (anchor) or sym₀(M)/α, stored as (xx, yy, zz, xy, xz, yz)
-__device__ __forceinline__ void sym_lambda(const double M[3][3], bool anchor, double alpha,
-                                           double L[6]) {
-  double xx = M[0][0], yy = M[1][1], zz = M[2][2];
-  double xy = 0.5 * (M[0][1] + M[1][0]);
-  double xz = 0.5 * (M[0][2] + M[2][0]);
-  double yz = 0.5 * (M[1][2] + M[2][1]);
-  if (anchor) {
-    L[0] = xx; L[1] = yy; L[2] = zz; L[3] = xy; L[4] = xz; L[5] = yz;
-  } else {
-    double tr3 = (xx + yy + zz) / 3.0;
-    double ia = 1.0 / alpha;
-    L[0] = (xx - tr3) * ia; L[1] = (yy - tr3) * ia; L[2] = (zz - tr3) * ia;
-    L[3] = xy * ia; L[4] = xz * ia; L[5] = yz * ia;
-  }
-}
-// out = A − Λ B   (Λ symmetric 3×3 in packed form)
-template <int R>
-__device__ __forceinline__ void sub_lam(const Blk<R>& A, const double L[6], const Blk<R>& B,
-                                        double scaleA, double scaleL, Blk<R>& out) {
-  const double Lm[3][3] = {{L[0], L[3], L[4]}, {L[3], L[1], L[5]}, {L[4], L[5], L[2]}};
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int c = 0; c < R; ++c) {
-      double s = Lm[a][0] * B.v[0][c] + Lm[a][1] * B.v[1][c] + Lm[a][2] * B.v[2][c];
-      out.v[a][c] = scaleA * A.v[a][c] - scaleL * s;
-    }
-}
-// in-place tangent projection of W at Y
-template <int R>
-__device__ __forceinline__ void project_blk(const Blk<R>& Y, bool anchor, Blk<R>& W) {
-  double M[3][3], L[6];
-  mul_abt<R>(W, Y, M);
-  double alpha = anchor ? 1.0 : frob2<R>(Y) / 3.0;
-  sym_lambda(M, anchor, alpha, L);
-  Blk<R> o;
-  sub_lam<R>(W, L, Y, 1.0, 1.0, o);
-  W = o;
-}
-
-// block reduce of NC components → partials[blockIdx.x * NC + c]
-template <int NC>
-__device__ __forceinline__ void block_reduce_store(double (&v)[NC], double* __restrict__ partials,
-                                                   const bool* is_min = nullptr) {
-  __shared__ double sh[NC][kFT];
-#pragma unroll
-  for (int c = 0; c < NC; ++c) sh[c][threadIdx.x] = v[c];
-  __syncthreads();
-  for (int s = kFT / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) {
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        double a = sh[c][threadIdx.x], b = sh[c][threadIdx.x + s];
-        sh[c][threadIdx.x] = (is_min && is_min[c]) ? fmin(a, b) : a + b;
-      }
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int c = 0; c < NC; ++c) partials[blockIdx.x * NC + c] = sh[c][0];
-  }
-}
 
 // ------------------------------------------------------------------ H7 gradient
 template <int R>
@@ -151,8 +40,7 @@ __global__ void __launch_bounds__(kFT) k_grad(int N, const double* __restrict__ 
     load_blk<R>(QY, i, g);
     double M[3][3], L[6];
     mul_abt<R>(g, y, M);
-    double a2 = frob2<R>(y);
-    double alpha = a2 / 3.0;
+    double alpha = frob2<R>(y) / 3.0;
     sym_lambda(M, i == 0, alpha, L);
 #pragma unroll
     for (int q = 0; q < 6; ++q) lam[6 * i + q] = L[q];
@@ -163,8 +51,7 @@ __global__ void __launch_bounds__(kFT) k_grad(int N, const double* __restrict__ 
     v[1] = frob2<R>(gr);
     if (i > 0) v[2] = alpha;
   }
-  const bool mins[3] = {false, false, true};
-  block_reduce_store<3>(v, partials, mins);
+  block_reduce_store<3, kFT>(v, partials, 4u);
 }
 
 // ------------------------------------------------------------------ projection
@@ -181,7 +68,7 @@ __global__ void __launch_bounds__(kFT) k_project(int N, const double* __restrict
   store_blk<R>(out, i, w);
 }
 
-// ------------------------------------------------------------------ H8 HVP epilogue
+// ------------------------------------------------------------------ H8 HVP epilogue (unfused)
 template <int R>
 __global__ void __launch_bounds__(kFT) k_hvp(int N, const double* __restrict__ Y,
                                              const double* __restrict__ lam,
@@ -200,12 +87,12 @@ __global__ void __launch_bounds__(kFT) k_hvp(int N, const double* __restrict__ Y
     double L[6];
 #pragma unroll
     for (int q = 0; q < 6; ++q) L[q] = lam[6 * i + q];
-    sub_lam<R>(qv, L, vv, 2.0, 2.0, w);  // 2QV − 2ΛV
+    sub_lam<R>(qv, L, vv, 2.0, 2.0, w);
     project_blk<R>(y, i == 0, w);
     store_blk<R>(HV, i, w);
     v[0] = dotb<R>(vv, w);
   }
-  block_reduce_store<1>(v, partials);
+  block_reduce_store<1, kFT>(v, partials);
 }
 
 // ------------------------------------------------------------------ H10 retraction
@@ -213,81 +100,94 @@ template <int R>
 __global__ void __launch_bounds__(kFT) k_retract(int N, const double* __restrict__ Y,
                                                  const double* __restrict__ V, double step,
                                                  double c_floor, double* __restrict__ Yout,
-                                                 double* __restrict__ D, int* __restrict__ err) {
+                                                 double* __restrict__ D, int* __restrict__ err,
+                                                 const double* __restrict__ g,
+                                                 const double* __restrict__ HV,
+                                                 double* __restrict__ dots2) {
   int i = blockIdx.x * kFT + threadIdx.x;
-  if (i >= N) return;
-  Blk<R> y, v, m;
-  load_blk<R>(Y, i, y);
-  load_blk<R>(V, i, v);
-  double s_new;
-  if (i == 0) {
+  double pd[2] = {0.0, 0.0};
+  if (i < N) {
+    Blk<R> y, v, m;
+    load_blk<R>(Y, i, y);
+    load_blk<R>(V, i, v);
+    if (dots2) {
+      Blk<R> gg, hv;
+      load_blk<R>(g, i, gg);
+      load_blk<R>(HV, i, hv);
+      pd[0] = dotb<R>(gg, v);
+      pd[1] = dotb<R>(v, hv);
+    }
+    double s_new;
+    if (i == 0) {
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
+      for (int a = 0; a < 3; ++a)
 #pragma unroll
-      for (int c = 0; c < R; ++c) m.v[a][c] = y.v[a][c] + step * v.v[a][c];
-    s_new = 1.0;
-  } else {
-    double s = sqrt(frob2<R>(y) / 3.0);
-    double is = 1.0 / s;
-    double ds = 0.0;
+        for (int c = 0; c < R; ++c) m.v[a][c] = y.v[a][c] + step * v.v[a][c];
+      s_new = 1.0;
+    } else {
+      double s = sqrt(frob2<R>(y) / 3.0);
+      double is = 1.0 / s;
+      double ds = 0.0;
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
+      for (int a = 0; a < 3; ++a)
 #pragma unroll
-      for (int c = 0; c < R; ++c) ds = fma(step * v.v[a][c], y.v[a][c] * is, ds);
-    ds /= 3.0;
+        for (int c = 0; c < R; ++c) ds = fma(step * v.v[a][c], y.v[a][c] * is, ds);
+      ds /= 3.0;
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
+      for (int a = 0; a < 3; ++a)
 #pragma unroll
-      for (int c = 0; c < R; ++c) {
-        double rh = y.v[a][c] * is;
-        double wt = step * v.v[a][c] - ds * rh;
-        m.v[a][c] = rh + wt * is;
+        for (int c = 0; c < R; ++c) {
+          double rh = y.v[a][c] * is;
+          double wt = step * v.v[a][c] - ds * rh;
+          m.v[a][c] = rh + wt * is;
+        }
+      s_new = fmax(s + ds, c_floor * s);
+    }
+    // modified Gram–Schmidt on the three rows, positive diagonal (C20)
+    double scale = sqrt(frob2<R>(m));
+    bool bad = false;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+#pragma unroll
+      for (int b = 0; b < a; ++b) {
+        double d = 0.0;
+#pragma unroll
+        for (int c = 0; c < R; ++c) d = fma(m.v[a][c], m.v[b][c], d);
+#pragma unroll
+        for (int c = 0; c < R; ++c) m.v[a][c] -= d * m.v[b][c];
       }
-    s_new = fmax(s + ds, c_floor * s);
-  }
-  // modified Gram–Schmidt on the three rows, positive diagonal (C20)
-  double scale = sqrt(frob2<R>(m));
-  bool bad = false;
+      double nv = 0.0;
 #pragma unroll
-  for (int a = 0; a < 3; ++a) {
+      for (int c = 0; c < R; ++c) nv = fma(m.v[a][c], m.v[a][c], nv);
+      nv = sqrt(nv);
+      if (!(nv > 1e-14 * scale)) {
+        bad = true;
+        nv = 1.0;
+      }
+      double inv = 1.0 / nv;
 #pragma unroll
-    for (int b = 0; b < a; ++b) {
-      double d = 0.0;
-#pragma unroll
-      for (int c = 0; c < R; ++c) d = fma(m.v[a][c], m.v[b][c], d);
-#pragma unroll
-      for (int c = 0; c < R; ++c) m.v[a][c] -= d * m.v[b][c];
+      for (int c = 0; c < R; ++c) m.v[a][c] *= inv;
     }
-    double nv = 0.0;
-#pragma unroll
-    for (int c = 0; c < R; ++c) nv = fma(m.v[a][c], m.v[a][c], nv);
-    nv = sqrt(nv);
-    if (!(nv > 1e-14 * scale)) {
-      bad = true;
-      nv = 1.0;
-    }
-    double inv = 1.0 / nv;
-#pragma unroll
-    for (int c = 0; c < R; ++c) m.v[a][c] *= inv;
-  }
-  if (bad) atomicOr(err, 1);
-  Blk<R> out;
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int c = 0; c < R; ++c) out.v[a][c] = s_new * m.v[a][c];
-  store_blk<R>(Yout, i, out);
-  if (D) {
+    if (bad) atomicOr(err, 1);
+    Blk<R> out;
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
-      for (int c = 0; c < R; ++c) out.v[a][c] -= y.v[a][c];
-    store_blk<R>(D, i, out);
+      for (int c = 0; c < R; ++c) out.v[a][c] = s_new * m.v[a][c];
+    store_blk<R>(Yout, i, out);
+    if (D) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int c = 0; c < R; ++c) out.v[a][c] -= y.v[a][c];
+      store_blk<R>(D, i, out);
+    }
   }
+  if (dots2) block_reduce_store<2, kFT>(pd, dots2);
 }
 
-// ------------------------------------------------------------------ H9 tCG (device state)
-// Initialise: η = Hη = 0, r = g, δ = −g, z = ⟨r, r⟩ (from the gradient pass).
+// ------------------------------------------------------------------ H9 tCG
+// Initialise: η = Hη = 0, r = g, δ = −g, state st[0] (z = ‖g‖² from the gradient pass).
 __global__ void k_tcg_init_vec(int64_t len, const double* __restrict__ g, double* __restrict__ eta,
                                double* __restrict__ Heta, double* __restrict__ res,
                                double* __restrict__ dir) {
@@ -305,65 +205,48 @@ __global__ void k_tcg_init_state(TcgState* st, const double* __restrict__ z0, do
   s.Delta = Delta;
   s.z = *z0;
   s.r0 = sqrt(s.z);
-  s.e_Pe = 0.0;
-  s.e_Pd = 0.0;
   s.d_Pd = s.z;
   s.kappa = kappa;
   s.theta = theta;
   s.max_inner = max_inner;
   s.stop = (max_inner <= 0) ? TCG_MAXINNER : TCG_RUNNING;
-  *st = s;
+  st[0] = s;
+  st[1] = s;
 }
 
-// fixed-order sum of block partials inside a single 256-thread block
-__device__ __forceinline__ double block_sum_partials(const double* __restrict__ part, int nblk) {
-  __shared__ double sh[256];
-  double a = 0.0;
-  for (int b = threadIdx.x; b < nblk; b += blockDim.x) a += part[b];
-  sh[threadIdx.x] = a;
-  __syncthreads();
-  for (int s = 128; s > 0; s >>= 1) {
-    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
-    __syncthreads();
-  }
-  return sh[0];
-}
-
-// after the HVP: d_Hd, α, boundary test (Manopt / Steihaug–Toint, O5)
-__global__ void __launch_bounds__(256) k_tcg_ctrl_a(TcgState* st, const double* __restrict__ part,
-                                                    int nblk) {
-  if (st->stop) return;
-  double dHd = block_sum_partials(part, nblk);
-  if (threadIdx.x != 0) return;
-  TcgState s = *st;
-  s.d_Hd = dHd;
-  s.n_hvp += 1;
-  double alpha = (dHd != 0.0) ? s.z / dHd : INFINITY;
-  double e_new = s.e_Pe + 2.0 * alpha * s.e_Pd + alpha * alpha * s.d_Pd;
-  s.alpha = alpha;
-  s.e_Pe_new = e_new;
-  double D2 = s.Delta * s.Delta;
-  if (dHd <= 0.0 || e_new >= D2) {
-    s.tau = (-s.e_Pd + sqrt(s.e_Pd * s.e_Pd + s.d_Pd * (D2 - s.e_Pe))) / s.d_Pd;
-    s.boundary = 1;
-  } else {
-    s.boundary = 0;
-  }
-  *st = s;
-}
-
+// K2: d_Hd from K1's partials; α, e_Pe′, boundary / τ; vector updates; ⟨r,r⟩ partials.
 template <int R>
-__global__ void __launch_bounds__(kFT) k_tcg_update(int N, const TcgState* __restrict__ st,
+__global__ void __launch_bounds__(kFT) k_tcg_update(int N, const TcgState* __restrict__ sin,
+                                                    TcgState* __restrict__ sout,
+                                                    const double* __restrict__ p1, int n1,
                                                     const double* __restrict__ Y,
                                                     const double* __restrict__ dir,
                                                     const double* __restrict__ Hdir,
                                                     double* __restrict__ eta,
                                                     double* __restrict__ Heta,
                                                     double* __restrict__ res,
-                                                    double* __restrict__ partials) {
-  if (st->stop) return;
-  const int boundary = st->boundary;
-  const double a = boundary ? st->tau : st->alpha;
+                                                    double* __restrict__ p2) {
+  TcgState s = *sin;
+  if (s.stop) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *sout = s;
+    return;
+  }
+  const double dHd = block_sum_all<kFT>(p1, n1);
+  s.d_Hd = dHd;
+  s.n_hvp += 1;
+  const double alpha = (dHd != 0.0) ? s.z / dHd : INFINITY;
+  const double e_new = s.e_Pe + 2.0 * alpha * s.e_Pd + alpha * alpha * s.d_Pd;
+  const double D2 = s.Delta * s.Delta;
+  s.alpha = alpha;
+  s.e_Pe_new = e_new;
+  if (dHd <= 0.0 || e_new >= D2) {
+    s.tau = (-s.e_Pd + sqrt(s.e_Pd * s.e_Pd + s.d_Pd * (D2 - s.e_Pe))) / s.d_Pd;
+    s.boundary = 1;
+    s.stop = (dHd <= 0.0) ? TCG_NEGCURV : TCG_EXCEEDED;
+  } else {
+    s.boundary = 0;
+  }
+  const double a = s.boundary ? s.tau : alpha;
   int i = blockIdx.x * kFT + threadIdx.x;
   double v[1] = {0.0};
   if (i < N) {
@@ -381,7 +264,7 @@ __global__ void __launch_bounds__(kFT) k_tcg_update(int N, const TcgState* __res
       }
     store_blk<R>(eta, i, e);
     store_blk<R>(Heta, i, he);
-    if (!boundary) {
+    if (!s.boundary) {
       Blk<R> y, rr;
       load_blk<R>(Y, i, y);
       load_blk<R>(res, i, rr);
@@ -394,27 +277,27 @@ __global__ void __launch_bounds__(kFT) k_tcg_update(int N, const TcgState* __res
       v[0] = frob2<R>(rr);
     }
   }
-  block_reduce_store<1>(v, partials);
+  block_reduce_store<1, kFT>(v, p2);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *sout = s;
 }
 
-// after the update: stop tests, β, e_Pd / d_Pd recurrences
-__global__ void __launch_bounds__(256) k_tcg_ctrl_b(TcgState* st, const double* __restrict__ part,
-                                                    int nblk) {
-  if (st->stop) return;
-  double z = block_sum_partials(part, nblk);
-  if (threadIdx.x != 0) return;
-  TcgState s = *st;
-  if (s.boundary) {
-    s.stop = (s.d_Hd <= 0.0) ? TCG_NEGCURV : TCG_EXCEEDED;
-    *st = s;
+// K3: stop tests, β, recurrences; δ ← −r + βδ.  Grid over n·r elements.
+__global__ void __launch_bounds__(256) k_tcg_dir(int64_t len, const TcgState* __restrict__ sin,
+                                                 TcgState* __restrict__ sout,
+                                                 const double* __restrict__ p2, int n2,
+                                                 const double* __restrict__ res,
+                                                 double* __restrict__ dir) {
+  TcgState s = *sin;
+  if (s.stop) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *sout = s;
     return;
   }
+  const double z = block_sum_all<256>(p2, n2);
   s.e_Pe = s.e_Pe_new;
   s.z_old = s.z;
   s.z = z;
   s.j += 1;
-  double rn = sqrt(z);
-  if (rn <= s.r0 * fmin(pow(s.r0, s.theta), s.kappa)) {
+  if (sqrt(z) <= s.r0 * fmin(pow(s.r0, s.theta), s.kappa)) {
     s.stop = TCG_CONVERGED;
   } else {
     s.beta = s.z / s.z_old;
@@ -422,15 +305,11 @@ __global__ void __launch_bounds__(256) k_tcg_ctrl_b(TcgState* st, const double* 
     s.d_Pd = s.z + s.beta * s.beta * s.d_Pd;
     if (s.j >= s.max_inner) s.stop = TCG_MAXINNER;
   }
-  *st = s;
-}
-
-__global__ void k_tcg_dir(int64_t len, const TcgState* __restrict__ st,
-                          const double* __restrict__ res, double* __restrict__ dir) {
-  if (st->stop) return;
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= len) return;
-  dir[t] = fma(st->beta, dir[t], -res[t]);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *sout = s;
+  if (s.stop) return;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < len;
+       t += (int64_t)gridDim.x * blockDim.x)
+    dir[t] = fma(s.beta, dir[t], -res[t]);
 }
 
 // ------------------------------------------------------------------ misc vector ops
@@ -466,20 +345,6 @@ __global__ void __launch_bounds__(kFT) k_zmul(int N, const double* __restrict__ 
   out[3 * i + 2] = qx[3 * i + 2] - (L[4] * x0 + L[5] * x1 + L[2] * x2);
 }
 
-template <int R>
-__global__ void __launch_bounds__(kFT) k_min_alpha(int N, const double* __restrict__ Y,
-                                                   double* __restrict__ partials) {
-  int i = blockIdx.x * kFT + threadIdx.x;
-  double v[1] = {1.0e300};
-  if (i > 0 && i < N) {
-    Blk<R> y;
-    load_blk<R>(Y, i, y);
-    v[0] = frob2<R>(y) / 3.0;
-  }
-  const bool mins[1] = {true};
-  block_reduce_store<1>(v, partials, mins);
-}
-
 // ================================================================== host wrappers
 #define XM_DISPATCH_R(r, CALL)                                                      \
   switch (r) {                                                                      \
@@ -498,11 +363,11 @@ __global__ void __launch_bounds__(kFT) k_min_alpha(int N, const double* __restri
     default: throw Error(XM_EINVAL, "rank r out of range (1..12)");                \
   }
 
-static inline int fblocks(int N) { return ceil_div(N, kFT); }
+int frame_blocks(xm_ctx* c) { return ceil_div(c->N, kFT); }
 
 void grad_and_multipliers(xm_ctx* c, int r, const double* Y, const double* QY, double* grad,
                           double* scal_out) {
-  int nb = fblocks(c->N);
+  int nb = frame_blocks(c);
   c->red.alloc((size_t)nb * 4 + 1024);
   XM_DISPATCH_R(r, (k_grad<R><<<nb, kFT, 0, c->stream>>>(c->N, Y, QY, c->lam.p, grad, c->red.p)));
   XM_CHECK_LAUNCH();
@@ -511,28 +376,42 @@ void grad_and_multipliers(xm_ctx* c, int r, const double* Y, const double* QY, d
 }
 
 void project(xm_ctx* c, int r, const double* Y, const double* W, double* out) {
-  XM_DISPATCH_R(r, (k_project<R><<<fblocks(c->N), kFT, 0, c->stream>>>(c->N, Y, W, out)));
+  XM_DISPATCH_R(r, (k_project<R><<<frame_blocks(c), kFT, 0, c->stream>>>(c->N, Y, W, out)));
   XM_CHECK_LAUNCH();
   count_launch(c);
 }
 
 void retract(xm_ctx* c, int r, const double* Y, const double* V, double step, double* Yout,
-             double* D, int* err) {
-  XM_DISPATCH_R(r, (k_retract<R><<<fblocks(c->N), kFT, 0, c->stream>>>(
-                       c->N, Y, V, step, c->opt.scale_floor, Yout, D, err)));
+             double* D, int* err, const double* g, const double* HV, double* dots2) {
+  XM_DISPATCH_R(r, (k_retract<R><<<frame_blocks(c), kFT, 0, c->stream>>>(
+                       c->N, Y, V, step, c->opt.scale_floor, Yout, D, err, g, HV, dots2)));
   XM_CHECK_LAUNCH();
   count_launch(c);
 }
 
 void hvp_epilogue(xm_ctx* c, int r, const double* Y, const double* V, const double* QV,
-                  double* HV, double* dot_out, const int* stop) {
-  int nb = fblocks(c->N);
-  c->red.alloc((size_t)nb * 4 + 1024);
-  XM_DISPATCH_R(r, (k_hvp<R><<<nb, kFT, 0, c->stream>>>(c->N, Y, c->lam.p, V, QV, HV, c->red.p,
-                                                        stop)));
+                  double* HV, double* partials, const int* stop) {
+  XM_DISPATCH_R(r, (k_hvp<R><<<frame_blocks(c), kFT, 0, c->stream>>>(c->N, Y, c->lam.p, V, QV, HV,
+                                                                     partials, stop)));
   XM_CHECK_LAUNCH();
   count_launch(c);
-  if (dot_out) reduce_partials(c, c->red.p, nb, 1, dot_out);
+}
+
+int hvp_product(xm_ctx* c, int r, const double* Y, const double* V, double* HV, double* partials,
+                const int* stop) {
+  if (c->world == 1) {
+    SpmmEpiArgs ep{};
+    ep.Y = Y;
+    ep.lam = c->lam.p;
+    ep.out2 = HV;
+    ep.partials = partials;
+    ep.stop = stop;
+    spmm(c, V, r, EPI_HVP, ep);
+    return spmm_grid(c, r);
+  }
+  spmm_full(c, V, r, c->tmp.p, stop);
+  hvp_epilogue(c, r, Y, V, c->tmp.p, HV, partials, stop);
+  return frame_blocks(c);
 }
 
 void tcg_init(xm_ctx* c, int r, double Delta) {
@@ -547,32 +426,22 @@ void tcg_init(xm_ctx* c, int r, double Delta) {
   count_launch(c, 2);
 }
 
-void tcg_ctrl_a(xm_ctx* c) {
-  k_tcg_ctrl_a<<<1, 256, 0, c->stream>>>(c->tcg.p, c->red.p, fblocks(c->N));
+// One tCG iteration = three kernels; state flows st[0] → st[1] → st[0].
+void tcg_iteration(xm_ctx* c, int r) {
+  const int nb = frame_blocks(c);
+  const int64_t len = (int64_t)c->n * r;
+  c->part1.alloc(2048);
+  c->part2.alloc((size_t)nb + 64);
+  int n1 = hvp_product(c, r, c->Y.p, c->dir.p, c->Hdir.p, c->part1.p, &c->tcg.p[0].stop);
+  XM_DISPATCH_R(r, (k_tcg_update<R><<<nb, kFT, 0, c->stream>>>(
+                       c->N, c->tcg.p, c->tcg.p + 1, c->part1.p, n1, c->Y.p, c->dir.p, c->Hdir.p,
+                       c->eta.p, c->Heta.p, c->res.p, c->part2.p)));
   XM_CHECK_LAUNCH();
-  count_launch(c);
-}
-
-void tcg_update(xm_ctx* c, int r) {
-  int nb = fblocks(c->N);
-  XM_DISPATCH_R(r, (k_tcg_update<R><<<nb, kFT, 0, c->stream>>>(c->N, c->tcg.p, c->Y.p, c->dir.p,
-                                                               c->Hdir.p, c->eta.p, c->Heta.p,
-                                                               c->res.p, c->red.p)));
+  int g3 = std::max(1, std::min(ceil_div(len, 256), 148));
+  k_tcg_dir<<<g3, 256, 0, c->stream>>>(len, c->tcg.p + 1, c->tcg.p, c->part2.p, nb, c->res.p,
+                                       c->dir.p);
   XM_CHECK_LAUNCH();
-  count_launch(c);
-}
-
-void tcg_ctrl_b(xm_ctx* c) {
-  k_tcg_ctrl_b<<<1, 256, 0, c->stream>>>(c->tcg.p, c->red.p, fblocks(c->N));
-  XM_CHECK_LAUNCH();
-  count_launch(c);
-}
-
-void tcg_dir(xm_ctx* c, int r) {
-  int64_t len = (int64_t)c->n * r;
-  k_tcg_dir<<<ceil_div(len, 256), 256, 0, c->stream>>>(len, c->tcg.p, c->res.p, c->dir.p);
-  XM_CHECK_LAUNCH();
-  count_launch(c);
+  count_launch(c, 2);
 }
 
 void axpy(xm_ctx* c, int64_t len, double a, const double* x, double* y) {
@@ -589,22 +458,9 @@ void pad_column(xm_ctx* c, int r, const double* Y, double* Yz, const double* v, 
 }
 
 void zmul(xm_ctx* c, const double* x, const double* Zx_q, double* out) {
-  k_zmul<<<fblocks(c->N), kFT, 0, c->stream>>>(c->N, c->lam.p, x, Zx_q, out);
+  k_zmul<<<frame_blocks(c), kFT, 0, c->stream>>>(c->N, c->lam.p, x, Zx_q, out);
   XM_CHECK_LAUNCH();
   count_launch(c);
-}
-
-double min_scale(xm_ctx* c, int r, const double* Y) {
-  int nb = fblocks(c->N);
-  c->red.alloc((size_t)nb * 4 + 1024);
-  XM_DISPATCH_R(r, (k_min_alpha<R><<<nb, kFT, 0, c->stream>>>(c->N, Y, c->red.p)));
-  XM_CHECK_LAUNCH();
-  count_launch(c);
-  reduce_partials(c, c->red.p, nb, 1, c->scal.p + 40, 1u);
-  double a = 0.0;
-  XM_CUDA(cudaMemcpyAsync(&a, c->scal.p + 40, 8, cudaMemcpyDeviceToHost, c->stream));
-  sync(c);
-  return c->N > 1 ? sqrt(a) : 1.0;
 }
 
 }  // namespace xm

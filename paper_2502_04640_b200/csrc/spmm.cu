@@ -1,172 +1,343 @@
-// spmm.cu — H6: out = Q·V for the tall-skinny BM factor V ∈ ℝ^{n×r}
-// (cost, gradient, every HVP of tCG, Δf, escapes, Lanczos with r = 1).
-// The paper applies its dense Q with cuBLAS matrix-vector products (P:520,
-// P:1075); here one streaming kernel reads each Q byte exactly once per product.
+// spmm.cu — H6: Q·V for the tall-skinny BM factor V ∈ ℝ^{n×r} (cost,
+// gradient, every HVP of tCG, Δf, escapes, Lanczos with r = 1), with the
+// per-camera epilogues H7/H8/H11 fused in.  The paper applies its dense Q with
+// cuBLAS matrix-vector products; here one streaming kernel
+// reads each Q byte exactly once per product.
 //
 // Roofline: HBM-bound.  Algorithmic bytes per product = 8·nrows·n (Q) +
-// 8·n·r (V) + 8·nrows·r (out); 2·nrows·n·r flop ⇒ 0.25·r flop/B, far below the
-// fp64 ridge (≈6 flop/B), so tensor cores are irrelevant.
+// 8·n·r (V) + 8·nrows·r (out); 2·nrows·n·r flop ⇒ 0.25·r flop/B ≪ the fp64
+// ridge (≈6 flop/B): tensor cores are irrelevant.
 //
-// Design (sm_100a):
-//  * grid = (row blocks) × (K splits); a CTA streams its row range of one K
-//    chunk.  The V chunk (kc × r) is staged once per CTA in shared memory,
-//    transposed (Vt[c][k]) so that every lane reads a conflict-free double2.
-//  * each warp owns a contiguous slice of the CTA's rows and processes RPW rows
-//    at a time: per 64-column step a lane issues RPW 128-bit streaming loads
-//    (ld.global.cs: evict-first, Q must not evict V / partials from L2) and
-//    r shared-memory double2 loads, 2·RPW·r FMAs.
-//  * per row group the lane partials are reduced with warp shuffles.
-//  * split-K partials are summed in a fixed order by spmm_reduce (deterministic;
-//    identical row results for any number of ranks).
-//  * grid sized to whole waves of 148 SMs × resident CTAs.
-#include "xm_internal.cuh"
+// Design (sm_100a), one persistent CTA per SM:
+//  * CTA c owns the frame-aligned row range of frames [c·N_own/G, (c+1)·N_own/G)
+//    over ALL columns ⇒ no split-K partials, every output row is final (and
+//    identical for any number of ranks), and the per-camera epilogue runs in
+//    the same kernel.  G = min(148, N_own) ⇒ balanced to within one camera.
+//  * warp-specialised TMA pipeline: one elected producer thread streams tiles
+//    of 8 Q rows × KC columns (one cp.async.bulk per row, L2 evict-first) plus
+//    the matching V chunk (KC × r, contiguous) into a ring of S stages guarded
+//    by full/empty mbarriers (transaction-count completion).  Bytes in flight =
+//    S × stage bytes (≥ 128 KB per SM) independent of register pressure.
+//  * 8 consumer warps: warp w owns columns [64w, 64w+64) of every tile and all 8
+//    rows; a lane reads its 2 V values per column pair once (r LDS.128) and
+//    reuses them for the 8 rows (8 LDS.128 of Q) ⇒ shared-memory traffic
+//    ≈ (1 + r/8)× the Q stream.  Per-row partials stay in registers across the
+//    K loop and are reduced once per row group (shuffles, then a fixed-order
+//    cross-warp sum) into a per-row accumulator in shared memory.
+//  * epilogues (one thread per camera of the CTA): STORE, HVP
+//    (Hv = P(2Qv − 2Λv), ⟨v, Hv⟩), ZMUL (Zv = Qv − Λv, ⟨v, Zv⟩), DF (QD,
+//    ⟨QY, D⟩, ⟨D, QD⟩), GRAD (QY, Λ, grad, f, ‖g‖², min α); scalar partials per
+//    CTA, reduced in a fixed order by the consumer ⇒ deterministic.
+#include "frame_ops.cuh"
 
 namespace xm {
 
-constexpr int kSpmmThreads = 256;
-constexpr int kSpmmWarps = kSpmmThreads / 32;
+constexpr int kConsumerWarps = 8;
+constexpr int kSpmmThreads = 32 * (kConsumerWarps + 1);  // + 1 producer warp
+constexpr int kTileRows = 8;
+constexpr int kTileCols = 64 * kConsumerWarps;  // 512 columns per tile
 
-template <int R, int RPW>
-__global__ void __launch_bounds__(kSpmmThreads) k_spmm_partial(
-    const double* __restrict__ Q, int64_t ldq, int nrows, int n, const double* __restrict__ V,
-    int kc, int nrowblk, double* __restrict__ part, const int* __restrict__ stop,
-    int* __restrict__ exec_flag) {
-  if (stop && *stop) return;
-  if (exec_flag && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *exec_flag = 1;
-  extern __shared__ __align__(16) double vt[];  // [R][kc]
-  const int rb = blockIdx.x, split = blockIdx.y;
-  const int k0 = split * kc;
-  const int klen = min(kc, n - k0);
-  // stage V chunk transposed
-  for (int idx = threadIdx.x; idx < klen * R; idx += kSpmmThreads) {
-    int k = idx / R, cc = idx - k * R;
-    vt[cc * kc + k] = V[(int64_t)(k0 + k) * R + cc];
-  }
-  __syncthreads();
-  const int r_lo = (int)((int64_t)rb * nrows / nrowblk);
-  const int r_hi = (int)((int64_t)(rb + 1) * nrows / nrowblk);
-  const int cnt = r_hi - r_lo;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int w_lo = r_lo + (int)((int64_t)warp * cnt / kSpmmWarps);
-  const int w_hi = r_lo + (int)((int64_t)(warp + 1) * cnt / kSpmmWarps);
-  const int kfull = klen & ~63;  // columns covered by full 64-wide steps
-  for (int row = w_lo; row < w_hi; row += RPW) {
-    double acc[RPW][R];
-#pragma unroll
-    for (int q = 0; q < RPW; ++q)
-#pragma unroll
-      for (int cc = 0; cc < R; ++cc) acc[q][cc] = 0.0;
-    const double* qrow[RPW];
-    bool live[RPW];
-#pragma unroll
-    for (int q = 0; q < RPW; ++q) {
-      live[q] = (row + q) < w_hi;
-      qrow[q] = Q + (int64_t)(live[q] ? row + q : row) * ldq + k0;
-    }
-    int k = 2 * lane;
-#pragma unroll 2
-    for (; k < kfull; k += 64) {
-      double2 qv[RPW];
-#pragma unroll
-      for (int q = 0; q < RPW; ++q)
-        qv[q] = live[q] ? __ldcs(reinterpret_cast<const double2*>(qrow[q] + k))
-                        : make_double2(0.0, 0.0);
-#pragma unroll
-      for (int cc = 0; cc < R; ++cc) {
-        double2 v = *reinterpret_cast<const double2*>(&vt[cc * kc + k]);
-#pragma unroll
-        for (int q = 0; q < RPW; ++q) acc[q][cc] = fma(qv[q].x, v.x, fma(qv[q].y, v.y, acc[q][cc]));
-      }
-    }
-    // ragged tail (< 64 columns), scalar loads
-    for (int kt = kfull + lane; kt < klen; kt += 32) {
-#pragma unroll
-      for (int q = 0; q < RPW; ++q) {
-        double qq = live[q] ? qrow[q][kt] : 0.0;
-#pragma unroll
-        for (int cc = 0; cc < R; ++cc) acc[q][cc] = fma(qq, vt[cc * kc + kt], acc[q][cc]);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < RPW; ++q)
-#pragma unroll
-      for (int cc = 0; cc < R; ++cc) {
-        double v = acc[q][cc];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        acc[q][cc] = v;
-      }
-    if (lane == 0) {
-#pragma unroll
-      for (int q = 0; q < RPW; ++q)
-        if (live[q]) {
-          double* o = part + ((int64_t)split * nrows + row + q) * R;
-#pragma unroll
-          for (int cc = 0; cc < R; ++cc) o[cc] = acc[q][cc];
-        }
-    }
-  }
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
 }
-
-// out_full[(row0 + row)·r + c] = Σ_split part[split][row][c]  (fixed order)
-__global__ void k_spmm_reduce(const double* __restrict__ part, int nsplit, int nrows, int r,
-                              double* __restrict__ out, const int* __restrict__ stop) {
-  if (stop && *stop) return;
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t tot = (int64_t)nrows * r;
-  if (t >= tot) return;
-  double s = 0.0;
-  for (int sp = 0; sp < nsplit; ++sp) s += part[sp * tot + t];
-  out[t] = s;
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
 }
-
-static int rpw_for(int r) { return r == 1 ? 8 : (r <= 6 ? 4 : 2); }
-static int kc_for(int r) { return r <= 2 ? 4096 : (r <= 6 ? 1024 : 512); }
-
-SpmmPlan spmm_plan(xm_ctx* c, int r) {
-  SpmmPlan p;
-  p.rpw = rpw_for(r);
-  p.kc = std::min<int>(kc_for(r), (int)round_up(std::max(c->n, 2), 64));
-  p.nsplit = ceil_div(c->n, p.kc);
-  int smem = r * p.kc * 8;
-  int occ = std::max(1, std::min(8, (int)((227 * 1024) / std::max(smem + 1024, 1))));
-  int slots = 148 * occ;
-  int rows = std::max(c->nrows, 1);
-  int maxblk = std::max(1, rows / 8);  // ≥ 1 row per warp
-  int waves = 1;
-  int nrb = std::max(1, slots * waves / p.nsplit);
-  while (nrb > maxblk && nrb > 1) nrb = std::max(1, nrb / 2);
-  // aim for ≥ 2 waves when each CTA would stream a lot of rows
-  if ((int64_t)rows / nrb > 512 && nrb * 2 <= maxblk) nrb *= 2;
-  p.nrowblk = std::min(nrb, maxblk);
-  return p;
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+// 1-D bulk copy global → shared, completion counted on `bar` (bytes % 16 == 0)
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes,
+                                            uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;\n" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
 }
 
 template <int R>
-static void launch_partial_r(xm_ctx* c, const double* V, double* part, const SpmmPlan& pl,
-                             const int* stop, int* exec) {
-  dim3 grid(pl.nrowblk, pl.nsplit);
-  size_t smem = (size_t)R * pl.kc * 8;
-  auto run = [&](auto kern) {
-    static bool attr_set = false;
-    if (!attr_set && smem > 48 * 1024) {
-      XM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+struct SpmmCfg {
+  static constexpr int kVBytes = kTileCols * R * 8;
+  static constexpr int kQBytes = kTileRows * kTileCols * 8;  // 32 KB
+  static constexpr int kStageBytes = kQBytes + kVBytes;
+  static constexpr int kStages = (kStageBytes * 4 <= 176 * 1024) ? 4 : (kStageBytes * 3 <= 192 * 1024 ? 3 : 2);
+};
+
+template <int R, int MODE>
+__global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(
+    const double* __restrict__ Q, int64_t ldq, int n, int f_lo_rank, int nframes_own,
+    const double* __restrict__ V, SpmmEpiArgs ep) {
+  using Cfg = SpmmCfg<R>;
+  constexpr int S = Cfg::kStages;
+  if (ep.stop && *ep.stop) return;
+  if (ep.exec && blockIdx.x == 0 && threadIdx.x == 0) *ep.exec = 1;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* stage_base = reinterpret_cast<double*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)S * Cfg::kStageBytes);
+  uint64_t* empty = full + S;
+  double* red = reinterpret_cast<double*>(empty + S);   // [warps][kTileRows][R]
+  double* acc = red + kConsumerWarps * kTileRows * R;   // [rows_cta][R]
+
+  const int G = gridDim.x;
+  const int fa = (int)((int64_t)blockIdx.x * nframes_own / G);
+  const int fb = (int)((int64_t)(blockIdx.x + 1) * nframes_own / G);
+  const int nrow = 3 * (fb - fa);
+  const int row_base = 3 * fa;  // local to this rank's Q rows
+  const int ngroups = (nrow + kTileRows - 1) / kTileRows;
+  const int nchunks = (n + kTileCols - 1) / kTileCols;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  for (int t = threadIdx.x; t < nrow * R; t += kSpmmThreads) acc[t] = 0.0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
     }
-    attr_set = true;
-    kern<<<grid, kSpmmThreads, smem, c->stream>>>(c->Q.p, c->ldq, c->nrows, c->n, V, pl.kc,
-                                                  pl.nrowblk, part, stop, exec);
-  };
-  constexpr int RPW = (R == 1) ? 8 : (R <= 6 ? 4 : 2);  // = rpw_for(R)
-  if (pl.rpw != RPW) throw Error(XM_EINVAL, "spmm plan / kernel mismatch");
-  run(k_spmm_partial<R, RPW>);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      const uint64_t pol_q = policy_evict_first();
+      const uint64_t pol_v = policy_evict_last();
+      int it = 0;
+      for (int g = 0; g < ngroups; ++g) {
+        const int r0 = g * kTileRows;
+        const int rows = min(kTileRows, nrow - r0);
+        for (int j = 0; j < nchunks; ++j, ++it) {
+          const int s = it % S;
+          const unsigned ph = (unsigned)((it / S) & 1);
+          mbar_wait(&empty[s], ph ^ 1u);
+          const int k0 = j * kTileCols;
+          const int klen = min(kTileCols, n - k0);
+          const unsigned qb = (unsigned)(((klen + 1) & ~1) * 8);  // 16-B multiple (pad ≤ 1 col)
+          const unsigned vb = (unsigned)(((klen * R + 1) & ~1) * 8);
+          mbar_expect_tx(&full[s], qb * rows + vb);
+          double* st = stage_base + (size_t)s * (Cfg::kStageBytes / 8);
+          for (int q = 0; q < rows; ++q)
+            tma_load_1d(st + q * kTileCols, Q + (int64_t)(row_base + r0 + q) * ldq + k0, qb,
+                        &full[s], pol_q);
+          tma_load_1d(st + kTileRows * kTileCols, V + (int64_t)k0 * R, vb, &full[s], pol_v);
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ consumers
+    int it = 0;
+    const int col = 64 * warp + 2 * lane;  // this lane's column pair within a tile
+    for (int g = 0; g < ngroups; ++g) {
+      const int r0 = g * kTileRows;
+      const int rows = min(kTileRows, nrow - r0);
+      double a[kTileRows][R];
+#pragma unroll
+      for (int q = 0; q < kTileRows; ++q)
+#pragma unroll
+        for (int cc = 0; cc < R; ++cc) a[q][cc] = 0.0;
+      for (int j = 0; j < nchunks; ++j, ++it) {
+        const int s = it % S;
+        const unsigned ph = (unsigned)((it / S) & 1);
+        mbar_wait(&full[s], ph);
+        const int klen = min(kTileCols, n - j * kTileCols);
+        const double* st = stage_base + (size_t)s * (Cfg::kStageBytes / 8);
+        const double* vs = st + kTileRows * kTileCols;
+        if (col + 1 < klen) {
+          double v0[R], v1[R];
+#pragma unroll
+          for (int cc = 0; cc < R; ++cc) {
+            v0[cc] = vs[col * R + cc];
+            v1[cc] = vs[(col + 1) * R + cc];
+          }
+#pragma unroll
+          for (int q = 0; q < kTileRows; ++q) {
+            if (q < rows) {
+              double2 qv = *reinterpret_cast<const double2*>(st + q * kTileCols + col);
+#pragma unroll
+              for (int cc = 0; cc < R; ++cc) a[q][cc] = fma(qv.x, v0[cc], fma(qv.y, v1[cc], a[q][cc]));
+            }
+          }
+        } else if (col < klen) {  // odd tail column
+#pragma unroll
+          for (int q = 0; q < kTileRows; ++q) {
+            if (q < rows) {
+              double qq = st[q * kTileCols + col];
+#pragma unroll
+              for (int cc = 0; cc < R; ++cc) a[q][cc] = fma(qq, vs[col * R + cc], a[q][cc]);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
+      // reduce the row group: lanes (shuffles) → warps (fixed order) → acc
+#pragma unroll
+      for (int q = 0; q < kTileRows; ++q)
+#pragma unroll
+        for (int cc = 0; cc < R; ++cc) {
+          double v = a[q][cc];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          a[q][cc] = v;
+        }
+      if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < kTileRows; ++q)
+#pragma unroll
+          for (int cc = 0; cc < R; ++cc) red[(warp * kTileRows + q) * R + cc] = a[q][cc];
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kConsumerWarps) : "memory");
+      for (int t = threadIdx.x; t < rows * R; t += 32 * kConsumerWarps) {
+        double sum = 0.0;
+        for (int w = 0; w < kConsumerWarps; ++w) sum += red[w * kTileRows * R + t];
+        acc[r0 * R + t] = sum;
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kConsumerWarps) : "memory");
+    }
+  }
+  __syncthreads();
+  // ------------------------------------------------------------ epilogue
+  const int f0g = f_lo_rank + fa;  // global frame index of the CTA's first frame
+  if (MODE == EPI_STORE) {
+    double* out = ep.out + (int64_t)(f_lo_rank * 3 + row_base) * R;
+    for (int t = threadIdx.x; t < nrow * R; t += kSpmmThreads) out[t] = acc[t];
+    return;
+  }
+  constexpr int NC = (MODE == EPI_GRAD) ? 3 : (MODE == EPI_DF ? 2 : 1);
+  double part[NC];
+#pragma unroll
+  for (int q = 0; q < NC; ++q) part[q] = (MODE == EPI_GRAD && q == 2) ? 1.0e300 : 0.0;
+  for (int lf = threadIdx.x; lf < fb - fa; lf += kSpmmThreads) {
+    const int i = f0g + lf;
+    Blk<R> qv;
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int cc = 0; cc < R; ++cc) qv.v[p][cc] = acc[(3 * lf + p) * R + cc];
+    if (MODE == EPI_HVP) {
+      Blk<R> y, vv, w;
+      load_blk<R>(ep.Y, i, y);
+      load_blk<R>(V, i, vv);
+      double L[6];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) L[q] = ep.lam[6 * i + q];
+      sub_lam<R>(qv, L, vv, 2.0, 2.0, w);  // 2Qv − 2Λv
+      project_blk<R>(y, i == 0, w);
+      store_blk<R>(ep.out2, i, w);
+      part[0] += dotb<R>(vv, w);
+    } else if (MODE == EPI_ZMUL) {
+      Blk<R> vv, w;
+      load_blk<R>(V, i, vv);
+      double L[6];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) L[q] = ep.lam[6 * i + q];
+      sub_lam<R>(qv, L, vv, 1.0, 1.0, w);  // Qv − Λv
+      store_blk<R>(ep.out, i, w);
+      part[0] += dotb<R>(vv, w);
+    } else if (MODE == EPI_DF) {
+      Blk<R> d, qy;
+      load_blk<R>(V, i, d);
+      load_blk<R>(ep.aux, i, qy);
+      store_blk<R>(ep.out, i, qv);
+      part[0] += dotb<R>(qy, d);
+      part[1] += dotb<R>(d, qv);
+    } else if (MODE == EPI_GRAD) {
+      Blk<R> y, gr;
+      load_blk<R>(V, i, y);  // V = Y
+      store_blk<R>(ep.out, i, qv);
+      double M[3][3], L[6];
+      mul_abt<R>(qv, y, M);
+      double alpha = frob2<R>(y) / 3.0;
+      sym_lambda(M, i == 0, alpha, L);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) ep.lam_out[6 * i + q] = L[q];
+      sub_lam<R>(qv, L, y, 2.0, 2.0, gr);
+      store_blk<R>(ep.out2, i, gr);
+      part[0] += dotb<R>(y, qv);
+      part[1] += frob2<R>(gr);
+      if (i > 0) part[2] = fmin(part[2], alpha);
+    }
+  }
+  // fixed-order reduction over the 9 warps: shuffles, then warp 0 in order
+  __shared__ double wsum[kConsumerWarps + 1][NC];
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    double v = part[q];
+    const bool is_min = (MODE == EPI_GRAD && q == 2);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double u = __shfl_xor_sync(0xffffffffu, v, o);
+      v = is_min ? fmin(v, u) : v + u;
+    }
+    if (lane == 0) wsum[warp][q] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < NC) {
+    const int q = threadIdx.x;
+    const bool is_min = (MODE == EPI_GRAD && q == 2);
+    double v = wsum[0][q];
+    for (int w = 1; w <= kConsumerWarps; ++w) v = is_min ? fmin(v, wsum[w][q]) : v + wsum[w][q];
+    ep.partials[blockIdx.x * NC + q] = v;
+  }
+}
+
+int spmm_grid(xm_ctx* c, int r) {
+  (void)r;
+  int nown = std::max(1, c->f1 - c->f0);
+  return std::max(1, std::min(148, nown));
+}
+
+template <int R, int MODE>
+static void launch_r(xm_ctx* c, const double* V, const SpmmEpiArgs& ep) {
+  using Cfg = SpmmCfg<R>;
+  const int G = spmm_grid(c, R);
+  const int nown = c->f1 - c->f0;
+  const int rows_max = 3 * ((nown + G - 1) / G);
+  size_t smem = (size_t)Cfg::kStages * Cfg::kStageBytes + 2 * Cfg::kStages * 8 +
+                (size_t)kConsumerWarps * kTileRows * R * 8 + (size_t)rows_max * R * 8;
+  if (smem > 227 * 1024) throw Error(XM_EINVAL, "SpMM shared memory plan exceeds 227 KB");
+  auto kern = k_spmm<R, MODE>;
+  static size_t attr = 0;
+  if (smem > attr) {
+    XM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  kern<<<G, kSpmmThreads, smem, c->stream>>>(c->Q.p, c->ldq, c->n, c->f0, nown, V, ep);
   XM_CHECK_LAUNCH();
   count_launch(c);
 }
 
-void spmm_partial(xm_ctx* c, const double* V, int r, double* part, const SpmmPlan& pl,
-                  const int* stop, int* exec) {
+template <int MODE>
+static void launch_mode(xm_ctx* c, const double* V, int r, const SpmmEpiArgs& ep) {
   switch (r) {
-#define XM_R(RR) case RR: launch_partial_r<RR>(c, V, part, pl, stop, exec); break;
+#define XM_R(RR) case RR: launch_r<RR, MODE>(c, V, ep); break;
     XM_R(1) XM_R(2) XM_R(3) XM_R(4) XM_R(5) XM_R(6) XM_R(7) XM_R(8) XM_R(9) XM_R(10) XM_R(11)
     XM_R(12)
 #undef XM_R
@@ -174,19 +345,11 @@ void spmm_partial(xm_ctx* c, const double* V, int r, double* part, const SpmmPla
   }
 }
 
-void spmm_reduce(xm_ctx* c, const double* part, int r, const SpmmPlan& pl, double* out_full,
-                 const int* stop) {
-  int64_t tot = (int64_t)c->nrows * r;
-  if (tot == 0) return;
-  k_spmm_reduce<<<ceil_div(tot, 256), 256, 0, c->stream>>>(part, pl.nsplit, c->nrows, r,
-                                                          out_full + (int64_t)c->row0 * r, stop);
-  XM_CHECK_LAUNCH();
-  count_launch(c);
-}
-
-void spmm_full(xm_ctx* c, const double* V, int r, double* out_full, const int* stop) {
-  SpmmPlan pl = spmm_plan(c, r);
-  c->part.alloc((size_t)pl.nsplit * std::max(c->nrows, 1) * r);
+// One (optionally profiled) SpMM launch with epilogue `mode` on this rank's rows.
+void spmm(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep_in) {
+  if (mode != EPI_STORE && c->world > 1)
+    throw Error(XM_EINVAL, "fused epilogues need world == 1 (use spmm_full + epilogue kernels)");
+  SpmmEpiArgs ep = ep_in;
   bool timed = c->opt.profile != 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (timed) {
@@ -203,31 +366,42 @@ void spmm_full(xm_ctx* c, const double* V, int r, double* out_full, const int* s
     if (c->ev_used + 2 > c->ev_pool.size()) harvest_events(c);
     e0 = c->ev_pool[c->ev_used++];
     e1 = c->ev_pool[c->ev_used++];
+    size_t pair = c->ev_used / 2 - 1;
+    ep.exec = c->ev_exec.p + pair;
+    c->ev_bytes[pair] = 8.0 * ((double)c->nrows * c->n + (double)c->n * r + (double)c->nrows * r);
     XM_CUDA(cudaEventRecord(e0, c->stream));
   }
-  int* exec = nullptr;
-  if (timed) {
-    size_t pair = c->ev_used / 2 - 1;
-    exec = c->ev_exec.p + pair;
-    c->ev_bytes[pair] = 8.0 * ((double)c->nrows * c->n + (double)c->n * r + (double)c->nrows * r);
+  switch (mode) {
+    case EPI_STORE: launch_mode<EPI_STORE>(c, V, r, ep); break;
+    case EPI_HVP: launch_mode<EPI_HVP>(c, V, r, ep); break;
+    case EPI_ZMUL: launch_mode<EPI_ZMUL>(c, V, r, ep); break;
+    case EPI_DF: launch_mode<EPI_DF>(c, V, r, ep); break;
+    case EPI_GRAD: launch_mode<EPI_GRAD>(c, V, r, ep); break;
+    default: throw Error(XM_EINVAL, "bad epilogue");
   }
-  spmm_partial(c, V, r, c->part.p, pl, stop, exec);
   if (timed) XM_CUDA(cudaEventRecord(e1, c->stream));
-  spmm_reduce(c, c->part.p, r, pl, out_full, stop);
-  if (c->world > 1) allgather_rows(c, out_full, r);
   c->stats.spmm_calls++;
   c->stats.spmm_rows = c->nrows;
 }
 
-// Accumulate the CUDA-event time of every profiled SpMM launch (pairs of events
-// recorded on the launching stream around k_spmm_partial) into stats.spmm_ms.
+// Full product into out (replicated n × r): this rank's rows, then all-gather.
+void spmm_full(xm_ctx* c, const double* V, int r, double* out_full, const int* stop) {
+  SpmmEpiArgs ep{};
+  ep.out = out_full;
+  ep.stop = stop;
+  spmm(c, V, r, EPI_STORE, ep);
+  if (c->world > 1) allgather_rows(c, out_full, r);
+}
+
+// Accumulate the CUDA-event time of every profiled SpMM launch that actually
+// ran (speculative launches that early-exited are skipped) into stats.
 void harvest_events(xm_ctx* c) {
   if (c->ev_used == 0) return;
   XM_CUDA(cudaEventSynchronize(c->ev_pool[c->ev_used - 1]));
   std::vector<int> exec(c->ev_used / 2);
   XM_CUDA(cudaMemcpy(exec.data(), c->ev_exec.p, exec.size() * sizeof(int), cudaMemcpyDeviceToHost));
   for (size_t q = 0; q + 1 < c->ev_used; q += 2) {
-    if (!exec[q / 2]) continue;  // speculative launch that early-exited (tCG already stopped)
+    if (!exec[q / 2]) continue;
     float ms = 0.f;
     XM_CUDA(cudaEventElapsedTime(&ms, c->ev_pool[q], c->ev_pool[q + 1]));
     c->stats.spmm_ms += ms;

@@ -58,7 +58,7 @@ void alloc_vectors(xm_ctx* c) {
   }
   c->lam.alloc((size_t)c->N * 6 + 6);
   c->scal.alloc(64);
-  c->tcg.alloc(1);
+  c->tcg.alloc(2);
   c->flags.alloc(16);
   c->cert_v.alloc((size_t)rows + 64);
   c->red.alloc((size_t)ceil_div(c->N, 128) * 4 + 1024);
@@ -69,15 +69,52 @@ void read_scal(xm_ctx* c, int first, int count, double* out) {
   sync(c);
 }
 
+// QY = Q·Y, Λ, grad, and scal_out[0..2] = f, ‖g‖², min α  (fused on one GPU)
+void grad_fused(xm_ctx* c, int r, const double* Y, double* QY, double* grad, double* scal_out) {
+  if (c->world == 1) {
+    c->part1.alloc(2048);
+    SpmmEpiArgs ep{};
+    ep.out = QY;
+    ep.out2 = grad;
+    ep.lam_out = c->lam.p;
+    ep.partials = c->part1.p;
+    spmm(c, Y, r, EPI_GRAD, ep);
+    reduce_partials(c, c->part1.p, spmm_grid(c, r), 3, scal_out, 4u);
+  } else {
+    spmm_full(c, Y, r, QY, nullptr);
+    grad_and_multipliers(c, r, Y, QY, grad, scal_out);
+  }
+}
+
 // fresh QY and gradient at c->Y; returns f, ‖g‖², α_min
 void eval_point(xm_ctx* c, double* f, double* g2, double* amin) {
-  spmm_full(c, c->Y.p, c->r, c->QY.p, nullptr);
-  grad_and_multipliers(c, c->r, c->Y.p, c->QY.p, c->grad.p, c->scal.p);
+  grad_fused(c, c->r, c->Y.p, c->QY.p, c->grad.p, c->scal.p);
   double h[3];
   read_scal(c, 0, 3, h);
   *f = h[0];
   *g2 = h[1];
   *amin = h[2];
+}
+
+// D ↦ (QD, ⟨QY, D⟩, ⟨D, QD⟩) → scal_out[0..1]
+void df_product(xm_ctx* c, int r, const double* D, const double* QY, double* QD, double* scal_out) {
+  const int64_t len = (int64_t)c->n * r;
+  if (c->world == 1) {
+    c->part2.alloc(4096);
+    SpmmEpiArgs ep{};
+    ep.out = QD;
+    ep.aux = QY;
+    ep.partials = c->part2.p;
+    spmm(c, D, r, EPI_DF, ep);
+    reduce_partials(c, c->part2.p, spmm_grid(c, r), 2, scal_out);
+  } else {
+    spmm_full(c, D, r, QD, nullptr);
+    c->lz_part.alloc((size_t)kDotBlocks * 4 + 64);
+    dot_flat(c, QY, D, len, c->lz_part.p, kDotBlocks);
+    reduce_partials(c, c->lz_part.p, kDotBlocks, 1, scal_out);
+    dot_flat(c, D, QD, len, c->lz_part.p, kDotBlocks);
+    reduce_partials(c, c->lz_part.p, kDotBlocks, 1, scal_out + 1);
+  }
 }
 
 // ⟨a_q, b_q⟩ for up to 4 pairs of flat arrays of length len → host
@@ -117,32 +154,27 @@ RtrOut rtr(xm_ctx* c, double tol_abs) {
       break;
     }
     if (it >= o.max_outer) break;
-    // ---- tCG (device-resident state)
+    // ---- tCG (device-resident, double-buffered state; 3 kernels / iteration)
     tcg_init(c, r, Delta);
     int batch = c->tcg_batch;
     TcgState hs{};
     while (true) {
-      for (int b = 0; b < batch; ++b) {
-        spmm_full(c, c->dir.p, r, c->tmp.p, &c->tcg.p->stop);
-        hvp_epilogue(c, r, c->Y.p, c->dir.p, c->tmp.p, c->Hdir.p, nullptr, &c->tcg.p->stop);
-        tcg_ctrl_a(c);
-        tcg_update(c, r);
-        tcg_ctrl_b(c);
-        tcg_dir(c, r);
-      }
+      for (int b = 0; b < batch; ++b) tcg_iteration(c, r);
       XM_CUDA(cudaMemcpyAsync(&hs, c->tcg.p, sizeof(TcgState), cudaMemcpyDeviceToHost, c->stream));
       sync(c);
       if (hs.stop) break;
     }
     c->info.hvps += hs.n_hvp;
-    // ---- retraction + cancellation-free Δf (reading C21)
+    // ---- retraction (+ ⟨g,η⟩, ⟨η,Hη⟩) and cancellation-free Δf (reading C21)
     XM_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int), c->stream));
-    retract(c, r, c->Y.p, c->eta.p, 1.0, c->Ynew.p, c->Dv.p, c->flags.p);
-    spmm_full(c, c->Dv.p, r, c->QD.p, nullptr);
-    const double* A[4] = {c->QY.p, c->Dv.p, c->grad.p, c->eta.p};
-    const double* B[4] = {c->Dv.p, c->QD.p, c->eta.p, c->Heta.p};
+    const int nb = frame_blocks(c);
+    c->red.alloc((size_t)nb * 4 + 1024);
+    retract(c, r, c->Y.p, c->eta.p, 1.0, c->Ynew.p, c->Dv.p, c->flags.p, c->grad.p, c->Heta.p,
+            c->red.p);
+    reduce_partials(c, c->red.p, nb, 2, c->scal.p + 10);
+    df_product(c, r, c->Dv.p, c->QY.p, c->QD.p, c->scal.p + 8);
     double d[4];
-    dots(c, len, 4, A, B, d);
+    read_scal(c, 8, 4, d);
     int rerr = 0;
     XM_CUDA(cudaMemcpyAsync(&rerr, c->flags.p, 4, cudaMemcpyDeviceToHost, c->stream));
     sync(c);
@@ -155,14 +187,14 @@ RtrOut rtr(xm_ctx* c, double tol_abs) {
     if (!(rho >= 0.25) || std::isnan(rho)) Delta /= 4.0;
     else if (rho > 0.75 && limited) Delta = std::min(2.0 * Delta, Dbar);
     if (rho > o.rho_prime) {
-      std::swap(c->Y.p, c->Ynew.p);
+      XM_CUDA(cudaMemcpyAsync(c->Y.p, c->Ynew.p, len * 8, cudaMemcpyDeviceToDevice, c->stream));
       ++accepts;
       if (o.refresh_every > 0 && accepts % o.refresh_every == 0) {
-        spmm_full(c, c->Y.p, r, c->QY.p, nullptr);
+        grad_fused(c, r, c->Y.p, c->QY.p, c->grad.p, c->scal.p);
       } else {
         axpy(c, len, 1.0, c->QD.p, c->QY.p);
+        grad_and_multipliers(c, r, c->Y.p, c->QY.p, c->grad.p, c->scal.p);
       }
-      grad_and_multipliers(c, r, c->Y.p, c->QY.p, c->grad.p, c->scal.p);
       double h[3];
       read_scal(c, 0, 3, h);
       f = h[0];
@@ -200,11 +232,9 @@ void escape(xm_ctx* c) {
   for (int h = 0; h <= 60; ++h) {
     XM_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int), c->stream));
     retract(c, r1, c->Ynew.p, c->dir.p, alpha, c->eta.p, c->Dv.p, c->flags.p);
-    spmm_full(c, c->Dv.p, r1, c->QD.p, nullptr);
-    const double* A[2] = {c->Heta.p, c->Dv.p};
-    const double* B[2] = {c->Dv.p, c->QD.p};
+    df_product(c, r1, c->Dv.p, c->Heta.p, c->QD.p, c->scal.p + 8);
     double d[2];
-    dots(c, len1, 2, A, B, d);
+    read_scal(c, 8, 2, d);
     double df = 2.0 * d[0] + d[1];
     if (df < 0.0) {
       XM_CUDA(cudaMemcpyAsync(c->Y.p, c->eta.p, len1 * 8, cudaMemcpyDeviceToDevice, c->stream));
@@ -560,8 +590,7 @@ xm_status xm_grad(xm_ctx* c, const double* Y, double* grad, double* f, int32_t r
     require_stage(c, 1);
     int64_t len = (int64_t)c->n * r;
     copy_in(c, c->hY.p, Y, len * 8);
-    spmm_full(c, c->hY.p, r, c->hQY.p, nullptr);
-    grad_and_multipliers(c, r, c->hY.p, c->hQY.p, c->hO.p, c->scal.p + 20);
+    grad_fused(c, r, c->hY.p, c->hQY.p, c->hO.p, c->scal.p + 20);
     if (grad) copy_out(c, grad, c->hO.p, len * 8);
     if (f) read_scal(c, 20, 1, f);
     sync(c);
@@ -576,10 +605,9 @@ xm_status xm_hvp(xm_ctx* c, const double* Y, const double* V, double* HV, int32_
     int64_t len = (int64_t)c->n * r;
     copy_in(c, c->hY.p, Y, len * 8);
     copy_in(c, c->hV.p, V, len * 8);
-    spmm_full(c, c->hY.p, r, c->hQY.p, nullptr);
-    grad_and_multipliers(c, r, c->hY.p, c->hQY.p, c->hO.p, c->scal.p + 20);
-    spmm_full(c, c->hV.p, r, c->hQY.p, nullptr);
-    hvp_epilogue(c, r, c->hY.p, c->hV.p, c->hQY.p, c->hO.p, nullptr, nullptr);
+    grad_fused(c, r, c->hY.p, c->hQY.p, c->hO.p, c->scal.p + 20);
+    c->part1.alloc(2048);
+    hvp_product(c, r, c->hY.p, c->hV.p, c->hO.p, c->part1.p, nullptr);
     copy_out(c, HV, c->hO.p, len * 8);
     sync(c);
     c->cert_valid = false;

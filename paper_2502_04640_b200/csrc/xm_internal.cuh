@@ -129,7 +129,8 @@ struct xm_ctx {
   xm::DBuf<double> part;   // SpMM split-K partials: nsplit × nrows × r
   xm::DBuf<double> red;    // block partials for reductions
   xm::DBuf<double> scal;   // reduced scalars (device)
-  xm::DBuf<xm::TcgState> tcg;
+  xm::DBuf<xm::TcgState> tcg;   // [2]: double-buffered tCG state
+  xm::DBuf<double> part1, part2; // scalar partials of the tCG kernels
   xm::DBuf<int> flags;     // error flags etc.
   xm::DBuf<double> hostbuf_dummy;
   double* h_scal = nullptr;  // pinned host mirror of scal
@@ -203,42 +204,48 @@ void dgemm(xm_ctx* c, bool ta, bool tb, bool lower, int M, int N, int K, double 
 void mirror_lower(xm_ctx* c, double* Q, int n, int64_t ldq);
 
 // ------------------------------------------------------------ SpMM (spmm.cu)
-struct SpmmPlan {
-  int nsplit = 1, kc = 0, nrowblk = 1, rpw = 4;
+enum { EPI_STORE = 0, EPI_HVP = 1, EPI_ZMUL = 2, EPI_DF = 3, EPI_GRAD = 4 };
+struct SpmmEpiArgs {
+  double* out = nullptr;         // STORE / ZMUL (Zv) / DF (QD) / GRAD (QY): full-layout rows
+  double* out2 = nullptr;        // HVP: Hv;  GRAD: grad
+  const double* Y = nullptr;     // HVP: current point
+  const double* lam = nullptr;   // HVP / ZMUL: Λ (N × 6)
+  const double* aux = nullptr;   // DF: QY
+  double* lam_out = nullptr;     // GRAD: Λ written here
+  double* partials = nullptr;    // per-CTA scalar partials [G][NC]
+  const int* stop = nullptr;     // no-op when *stop != 0
+  int* exec = nullptr;           // profiling: set to 1 when the kernel ran
 };
-SpmmPlan spmm_plan(xm_ctx* c, int r);
-// part[split][row][c] for this rank's rows; if stop != nullptr the kernel is a
-// no-op when *stop != 0 (speculative tCG batches).
-void spmm_partial(xm_ctx* c, const double* V, int r, double* part, const SpmmPlan& pl,
-                  const int* stop, int* exec = nullptr);
-// out (full vector layout, this rank's rows written then all-gathered) = Σ_split part.
-void spmm_reduce(xm_ctx* c, const double* part, int r, const SpmmPlan& pl, double* out_full,
-                 const int* stop);
-void harvest_events(xm_ctx* c);
-// Full product into out (n × r, replicated): partial + reduce + all-gather.
+int spmm_grid(xm_ctx* c, int r);  // number of CTAs = number of scalar partials
+void spmm(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep);
+// Full product into out (n × r, replicated): this rank's rows + all-gather.
 void spmm_full(xm_ctx* c, const double* V, int r, double* out_full, const int* stop = nullptr);
 void allgather_rows(xm_ctx* c, double* full, int r);
+void harvest_events(xm_ctx* c);
 
 // ------------------------------------------------------------ manifold (manifold.cu)
-// grad = 2(QY − ΛY); α, Λ from (Y, QY); red ← [f, ‖g‖², s_min²] partials.
+// grad = 2(QY − ΛY); Λ written to c->lam; scal_out[0..2] = f, ‖g‖², min α (i ≥ 1).
 void grad_and_multipliers(xm_ctx* c, int r, const double* Y, const double* QY, double* grad,
                           double* scal_out /*3*/);
 void project(xm_ctx* c, int r, const double* Y, const double* W, double* out);
+// Y_out = R_Y(step·V); D = Y_out − Y (nullable); optional partials of ⟨g, V⟩ and
+// ⟨V, HV⟩ (dots2 != nullptr) written as [nblk][2].
 void retract(xm_ctx* c, int r, const double* Y, const double* V, double step, double* Yout,
-             double* D, int* err);
-// HV = P(2·QV − 2ΛV), partial ⟨V, HV⟩ into red; QV given as a full n×r array.
+             double* D, int* err, const double* g = nullptr, const double* HV = nullptr,
+             double* dots2 = nullptr);
+// HV = P(2·QV − 2ΛV), partials of ⟨V, HV⟩ (one per block of 128 cameras).
 void hvp_epilogue(xm_ctx* c, int r, const double* Y, const double* V, const double* QV,
-                  double* HV, double* dot_out /*1*/, const int* stop);
-// tCG device-side steps
+                  double* HV, double* partials, const int* stop);
+int frame_blocks(xm_ctx* c);
+// Hessian-vector product V → HV with ⟨V,HV⟩ partials; returns the partial count.
+int hvp_product(xm_ctx* c, int r, const double* Y, const double* V, double* HV, double* partials,
+                const int* stop);
+// tCG with double-buffered device state st[0] / st[1] (TcgState)
 void tcg_init(xm_ctx* c, int r, double Delta);
-void tcg_ctrl_a(xm_ctx* c);
-void tcg_update(xm_ctx* c, int r);
-void tcg_ctrl_b(xm_ctx* c);
-void tcg_dir(xm_ctx* c, int r);
+void tcg_iteration(xm_ctx* c, int r);
 void axpy(xm_ctx* c, int64_t len, double a, const double* x, double* y);
 void pad_column(xm_ctx* c, int r, const double* Y, double* Yz, const double* v, double* Dz);
 void zmul(xm_ctx* c, const double* x, const double* Zx_q, double* out);  // Zx = Qx − Λx (r = 1)
-double min_scale(xm_ctx* c, int r, const double* Y);
 
 // ------------------------------------------------------------ Lanczos / rounding (cert.cu)
 void lanczos(xm_ctx* c, double tol_abs, int max_steps, double* lambda, int* steps,
