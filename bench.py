@@ -156,6 +156,8 @@ def run_reference(args):
     from synth.scenes import CONFIG_DESCRIPTIONS, config_scene
     sc = config_scene(args.config, seed=args.seed)
     counts = load_counts(args.config) or {"hvps": 12000, "lanczos_steps": 1000, "spmms": 25000}
+    if counts.get("lanczos_steps_full"):
+        counts = dict(counts, lanczos_steps=counts["lanczos_steps_full"])
     times = []
     for i in range(args.warmup + args.steps):
         est, cores, sample = oracle_sample(sc, counts["hvps"], counts["lanczos_steps"],
@@ -309,6 +311,8 @@ def main():
                   "outer_iters": info["outer_iters"], "r": info["r"], "escapes": info["escapes"],
                   "certified": info["certified"], "f": info["f"], "s_min": info["s_min"],
                   "lambda_min": cert["lambda_min"], "lambda_min_rel": cert["lambda_min"] / max(1.0, cert["normQ"]),
+                  "lambda_lower": cert["lambda_lower"],
+                  "cert_method": ["lanczos", "cholesky(Z+eps*I)"][cert["method"]],
                   "eta": cert["eta"], "rho_hat": cert["rho_hat"], "status": st},
         "phases_ms": {k: stats[k] / args.steps for k in ("ms_build", "ms_solve", "ms_certify", "ms_round")},
         "roofline": {"kernel": "k_spmm_partial (Q·V)", "bound": "hbm", "achieved": achieved,
@@ -325,14 +329,21 @@ def main():
             counts = json.load(open(COUNTS_FILE)) if os.path.exists(COUNTS_FILE) else {}
         except Exception:
             counts = {}
+        prev = counts.get(args.config, {})
+        full = info["lanczos_steps"] if cert["method"] == 0 else prev.get("lanczos_steps_full")
         counts[args.config] = {"hvps": info["hvps"], "spmms": info["spmms"],
-                               "lanczos_steps": info["lanczos_steps"], "N": sc.N}
+                               "lanczos_steps": info["lanczos_steps"],
+                               "lanczos_steps_full": full, "N": sc.N}
         with open(COUNTS_FILE, "w") as f:
             json.dump(counts, f, indent=1)
     clocks = clk.summary()
     result["clocks"] = clocks
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        est, cores, sample = oracle_sample(sc, info["hvps"], info["lanczos_steps"], info["spmms"])
+        # the oracle certifies with Lanczos to convergence (it has no Cholesky test)
+        lz = info["lanczos_steps"]
+        if cert["method"] != 0:
+            lz = (load_counts(args.config) or {}).get("lanczos_steps_full") or lz
+        est, cores, sample = oracle_sample(sc, info["hvps"], lz, info["spmms"])
         result["cpu_baseline"] = {"value": est, "unit": "s", "cores": cores, "kind": "oracle",
                                   "sample": sample}
     if rank == 0:

@@ -90,6 +90,9 @@ typedef struct {
   int32_t lanczos_max;    /* Lanczos step cap                              [3000] */
   int32_t refresh_every;  /* fresh Q·Y every k accepted TR steps (C21)       [50] */
   int32_t profile;        /* 1: time every SpMM with CUDA events (xm_stats)  [0]  */
+  int32_t cert_cholesky;  /* 1: if Lanczos has not converged within n/72 steps,  */
+                          /* test Z + εI ⪰ 0 by dense Cholesky (ε = cert_tol·   */
+                          /* max(1,‖Q‖_F); Alg. 1); single GPU     [1]  */
   uint64_t seed;          /* Lanczos start vector (splitmix64 stream)         [0]  */
 } xm_options;
 
@@ -110,10 +113,12 @@ typedef struct {
 } xm_solve_info;
 
 typedef struct {
-  double lambda_min;      /* λ_min(Z(y)), Z = Q − blkdiag(Λ) (Eq. (16))         */
+  double lambda_min;      /* λ_min(Z(y)), Z = Q − blkdiag(Λ) (Eq. (16)); if    */
+                          /* method == 1 the smallest Ritz value (upper bound)  */
+  double lambda_lower;    /* certified lower bound on λ_min (= λ_min, or −ε)    */
   double rho_dual;        /* b·y = tr Λ_0 (dual objective, Eq. (16))      */
   double rho_hat;         /* objective at the rounded, recovered solution        */
-  double rho_lower;       /* ρ_dual + min(0, λ_min)·tr X̂ (reading C10)          */
+  double rho_lower;       /* ρ_dual + min(0, λ_lower)·tr X̂ (reading C10)        */
   double eta;             /* (ρ̂ − ρ_lower)/(1 + |ρ̂| + |ρ_lower|)  (Eq. (13))    */
   double eta_E;           /* App. E formula as printed: max(0, λ_min)·tr X       */
   double kkt_resid;       /* ‖Z(y) Y‖_F (Thm 1 Eq. (18))                         */
@@ -122,6 +127,7 @@ typedef struct {
   double normQ;
   int32_t lanczos_steps;
   int32_t certified;
+  int32_t method;         /* 0: Lanczos converged; 1: Cholesky of Z + εI        */
 } xm_certificate;
 
 typedef struct {

@@ -459,8 +459,8 @@ __global__ void k_diag_max(const double* __restrict__ A, int m, int64_t lda, dou
   if (threadIdx.x == 0) *out = sh[0];
 }
 
-void dense_cholesky(xm_ctx* c, double* A, int m, int64_t lda, double rel_tol) {
-  if (m <= 0) return;
+bool dense_cholesky(xm_ctx* c, double* A, int m, int64_t lda, double rel_tol, bool throw_on_fail) {
+  if (m <= 0) return true;
   c->flags.alloc(16);
   c->scal.alloc(64);
   XM_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int), c->stream));
@@ -484,13 +484,48 @@ void dense_cholesky(xm_ctx* c, double* A, int m, int64_t lda, double rel_tol) {
       dgemm(c, false, true, true, rows, rows, nb, -1.0, A21, lda, A21, lda, 1.0, A22, lda);
     }
   }
-  k_zero_upper<<<ceil_div((int64_t)m * m, 256), 256, 0, c->stream>>>(A, m, lda);
-  XM_CHECK_LAUNCH();
-  count_launch(c);
+  if (throw_on_fail) {
+    k_zero_upper<<<ceil_div((int64_t)m * m, 256), 256, 0, c->stream>>>(A, m, lda);
+    XM_CHECK_LAUNCH();
+    count_launch(c);
+  }
   int h_err = 0;
   XM_CUDA(cudaMemcpyAsync(&h_err, c->flags.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   sync(c);
-  if (h_err) throw Error(XM_EDISCONNECTED, "graph numerically disconnected (Cholesky pivot)");
+  if (h_err && throw_on_fail)
+    throw Error(XM_EDISCONNECTED, "graph numerically disconnected (Cholesky pivot)");
+  return h_err == 0;
+}
+
+// Z + εI with Z = Q − blkdiag(Λ) (Eq. (16)); lower triangle incl. diagonal is all potrf reads.
+__global__ void k_form_z_shift(const double* __restrict__ Q, int64_t ldq, int n,
+                               const double* __restrict__ lam, double eps, double* __restrict__ Z) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n * n) return;
+  int i = (int)(t / n), j = (int)(t % n);
+  if (j > i) return;
+  double v = Q[(int64_t)i * ldq + j];
+  if (i / 3 == j / 3) {
+    const double* L = lam + 6 * (i / 3);
+    int a = i % 3, b = j % 3;
+    const int idx[3][3] = {{0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
+    v -= L[idx[a][b]];
+    if (i == j) v += eps;
+  }
+  Z[(int64_t)i * ldq + j] = v;
+}
+
+// PSD test of Z(y) (Alg. 1): Cholesky of Z + εI succeeds ⇔ λ_min(Z) > −ε
+// (up to the backward error of Cholesky, O(n·u·‖Z‖) ≪ ε).  Single-rank Q only.
+bool psd_test_cholesky(xm_ctx* c, double eps) {
+  if (c->world != 1) throw Error(XM_EINVAL, "Cholesky PSD test needs the full Q on one rank");
+  const int n = c->n;
+  c->Zw.alloc((size_t)n * c->ldq);
+  k_form_z_shift<<<ceil_div((int64_t)n * n, 256), 256, 0, c->stream>>>(c->Q.p, c->ldq, n,
+                                                                      c->lam.p, eps, c->Zw.p);
+  XM_CHECK_LAUNCH();
+  count_launch(c);
+  return dense_cholesky(c, c->Zw.p, n, c->ldq, 0.0, false);
 }
 
 // Forward substitution of a diagonal block for many right-hand sides:

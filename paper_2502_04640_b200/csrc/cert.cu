@@ -195,7 +195,7 @@ static void tridiag_min(const std::vector<double>& a, const std::vector<double>&
   s = x;
 }
 
-void lanczos(xm_ctx* c, double tol_abs, int max_steps, double* lambda, int* steps,
+bool lanczos(xm_ctx* c, double tol_abs, int max_steps, double* lambda, int* steps,
              double* vec_dev) {
   const int64_t n = c->n;
   const int kmax = (int)std::max<int64_t>(1, std::min<int64_t>(max_steps, n));
@@ -224,6 +224,7 @@ void lanczos(xm_ctx* c, double tol_abs, int max_steps, double* lambda, int* step
   std::vector<double> ha, hb, s;
   double lam = 0.0;
   int k = 0;
+  bool converged = false;
   const int check_every = 8;
   bool done = false;
   while (!done) {
@@ -272,7 +273,8 @@ void lanczos(xm_ctx* c, double tol_abs, int max_steps, double* lambda, int* step
     tridiag_min(ha, hb, kk, lam, s);
     double res = std::fabs(hb[kk - 1] * s[kk - 1]);
     bool breakdown = hb[kk - 1] <= 1e-14 * std::max(1.0, c->normQ);
-    if (res <= tol_abs || breakdown || kk >= kmax) done = true;
+    converged = res <= tol_abs || breakdown || kk >= (int)n;
+    if (converged || kk >= kmax) done = true;
   }
   *lambda = lam;
   *steps = k;
@@ -293,6 +295,7 @@ void lanczos(xm_ctx* c, double tol_abs, int max_steps, double* lambda, int* step
     count_launch(c, 5);
     sync(c);
   }
+  return converged;
 }
 
 // ================================================================== rounding

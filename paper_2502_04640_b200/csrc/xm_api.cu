@@ -212,9 +212,33 @@ RtrOut rtr(xm_ctx* c, double tol_abs) {
   return out;
 }
 
+// Certificate at the current point (Alg. 1 lines 9-12): Λ from the last gradient
+// pass; λ_min(Z) by Lanczos.  If Lanczos has not converged within ≈ the cost of
+// one dense factorisation (n/72 steps), Z ⪰ −εI is decided by Cholesky of Z + εI
+// (single GPU); only if that fails does Lanczos continue to convergence (the
+// escape direction v is needed then).
 void certify_current(xm_ctx* c, double* lambda, int* steps) {
-  double tol = c->opt.eig_tol * std::max(1.0, c->normQ);
-  lanczos(c, tol, c->opt.lanczos_max, lambda, steps, c->cert_v.p);
+  const double tol = c->opt.eig_tol * std::max(1.0, c->normQ);
+  const double eps = c->opt.cert_tol * std::max(1.0, c->normQ);
+  c->cert_method = 0;
+  if (c->world == 1 && c->opt.cert_cholesky) {
+    int budget = std::min(c->opt.lanczos_max, std::max(32, c->n / 72));
+    bool conv = lanczos(c, tol, budget, lambda, steps, c->cert_v.p);
+    if (conv) {
+      c->cert_lower = *lambda;
+    } else if (psd_test_cholesky(c, eps)) {
+      c->cert_method = 1;
+      c->cert_lower = -eps;
+    } else {
+      int s1 = *steps;
+      lanczos(c, tol, c->opt.lanczos_max, lambda, steps, c->cert_v.p);
+      *steps += s1;
+      c->cert_lower = *lambda;
+    }
+  } else {
+    lanczos(c, tol, c->opt.lanczos_max, lambda, steps, c->cert_v.p);
+    c->cert_lower = *lambda;
+  }
   c->cert_valid = true;
   c->cert_lambda = *lambda;
   c->cert_steps = *steps;
@@ -286,6 +310,7 @@ void xm_default_options(xm_options* o) {
   o->lanczos_max = 3000;
   o->refresh_every = 50;
   o->profile = 0;
+  o->cert_cholesky = 1;
   o->seed = 0;
 }
 
@@ -447,7 +472,7 @@ xm_status xm_solve(xm_ctx* c, int32_t r0, double tol, xm_solve_info* info) {
       ro = rtr(c, tol_abs);
       int steps = 0;
       certify_current(c, &lam, &steps);
-      certified = ro.converged && lam >= -c->opt.cert_tol * std::max(1.0, c->normQ);
+      certified = ro.converged && c->cert_lower >= -c->opt.cert_tol * std::max(1.0, c->normQ);
       if (certified || !ro.converged || c->r >= c->opt.rank_cap) break;
       escape(c);
     }
@@ -505,18 +530,20 @@ xm_status xm_certify(xm_ctx* c, xm_certificate* out, double* min_eigvec) {
     sync(c);
     xm_certificate ce{};
     ce.lambda_min = lam;
+    ce.lambda_lower = c->cert_lower;
+    ce.method = c->cert_method;
     ce.rho_dual = l0[0] + l0[1] + l0[2];
     ce.rho_hat = d[0];
     ce.trace_X = trX;
-    ce.rho_lower = ce.rho_dual + std::min(0.0, lam) * trX;
+    ce.rho_lower = ce.rho_dual + std::min(0.0, c->cert_lower) * trX;
     ce.eta = (ce.rho_hat - ce.rho_lower) / (1.0 + std::fabs(ce.rho_hat) + std::fabs(ce.rho_lower));
-    double lowE = std::max(0.0, lam) * trX + ce.rho_dual;
+    double lowE = std::max(0.0, c->cert_lower) * trX + ce.rho_dual;
     ce.eta_E = (ce.rho_hat - lowE) / (1.0 + std::fabs(ce.rho_hat) + std::fabs(lowE));
     ce.kkt_resid = 0.5 * std::sqrt(g2);  // grad = 2 Z Y
     ce.grad_norm = std::sqrt(g2);
     ce.normQ = c->normQ;
     ce.lanczos_steps = steps;
-    ce.certified = (lam >= -c->opt.cert_tol * std::max(1.0, c->normQ)) &&
+    ce.certified = (c->cert_lower >= -c->opt.cert_tol * std::max(1.0, c->normQ)) &&
                    std::sqrt(g2) <= c->opt.grad_tol * std::max(1.0, c->normQ) * 1.0001;
     c->cert = ce;
     c->have_cert = true;

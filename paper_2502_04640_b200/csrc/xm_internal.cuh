@@ -165,6 +165,9 @@ struct xm_ctx {
   double cert_lambda = 0.0;
   int cert_steps = 0;
   xm::DBuf<double> cert_v;
+  xm::DBuf<double> Zw;       // Z + εI work copy for the Cholesky PSD test
+  double cert_lower = 0.0;   // certified lower bound on λ_min(Z)
+  int cert_method = 0;       // 0 Lanczos converged, 1 Cholesky of Z + εI
   int tcg_batch = 4;
   std::string last_error;
 };
@@ -195,7 +198,9 @@ constexpr int kDotBlocks = 296;  // 2 × 148 SMs; fixed ⇒ deterministic sums
 // ------------------------------------------------------------ assembly (assembly.cu)
 void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr, const int32_t* lm,
                     const double* pts, const double* w);
-void dense_cholesky(xm_ctx* c, double* A, int m, int64_t lda, double pivot_tol);
+bool dense_cholesky(xm_ctx* c, double* A, int m, int64_t lda, double rel_tol,
+                    bool throw_on_fail = true);
+bool psd_test_cholesky(xm_ctx* c, double eps);
 void dense_trsm_lower_left(xm_ctx* c, const double* L, int m, int64_t ldl, double* B, int ncols,
                            int64_t ldb);
 void dgemm(xm_ctx* c, bool ta, bool tb, bool lower, int M, int N, int K, double alpha,
@@ -248,7 +253,8 @@ void pad_column(xm_ctx* c, int r, const double* Y, double* Yz, const double* v, 
 void zmul(xm_ctx* c, const double* x, const double* Zx_q, double* out);  // Zx = Qx − Λx (r = 1)
 
 // ------------------------------------------------------------ Lanczos / rounding (cert.cu)
-void lanczos(xm_ctx* c, double tol_abs, int max_steps, double* lambda, int* steps,
+// returns true if the smallest Ritz pair converged (|β_k s_k| ≤ tol_abs)
+bool lanczos(xm_ctx* c, double tol_abs, int max_steps, double* lambda, int* steps,
              double* vec_dev);
 void round_recover_device(xm_ctx* c);
 

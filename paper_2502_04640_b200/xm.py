@@ -37,7 +37,8 @@ class Options(ctypes.Structure):
                 ("scale_floor", ctypes.c_double), ("tcg_max_inner", ctypes.c_int32),
                 ("max_outer", ctypes.c_int32), ("rank_cap", ctypes.c_int32),
                 ("lanczos_max", ctypes.c_int32), ("refresh_every", ctypes.c_int32),
-                ("profile", ctypes.c_int32), ("seed", ctypes.c_uint64)]
+                ("profile", ctypes.c_int32), ("cert_cholesky", ctypes.c_int32),
+                ("seed", ctypes.c_uint64)]
 
 
 class SolveInfo(ctypes.Structure):
@@ -50,12 +51,14 @@ class SolveInfo(ctypes.Structure):
 
 
 class Certificate(ctypes.Structure):
-    _fields_ = [("lambda_min", ctypes.c_double), ("rho_dual", ctypes.c_double),
+    _fields_ = [("lambda_min", ctypes.c_double), ("lambda_lower", ctypes.c_double),
+                ("rho_dual", ctypes.c_double),
                 ("rho_hat", ctypes.c_double), ("rho_lower", ctypes.c_double),
                 ("eta", ctypes.c_double), ("eta_E", ctypes.c_double),
                 ("kkt_resid", ctypes.c_double), ("grad_norm", ctypes.c_double),
                 ("trace_X", ctypes.c_double), ("normQ", ctypes.c_double),
-                ("lanczos_steps", ctypes.c_int32), ("certified", ctypes.c_int32)]
+                ("lanczos_steps", ctypes.c_int32), ("certified", ctypes.c_int32),
+                ("method", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
