@@ -768,10 +768,16 @@ def suboptimality(rho_hat, rho_lower):
     return (rho_hat - rho_lower) / (1.0 + abs(rho_hat) + abs(rho_lower))
 
 
-def report(cert: Certificate, rho_hat: float):
-    """ρ_lower = ρ_dual + min(0, λ_min)·tr X̂ (reading C10); η per Eq. (13);
-    η_E per App. E as printed (max(0, λ_min))."""
-    rho_lower = cert.rho_dual + min(0.0, cert.lambda_min) * cert.trace_X
+def report(cert: Certificate, rho_hat: float, normQ: float = 1.0, cert_tol: float = 1e-6):
+    """η per Eq. (13) with ρ_SDP estimated by (reading C10):
+      * at a certified point (λ_min ≥ −cert_tol·max(1,‖Q‖_F)): the dual value
+        ρ_dual = b·y (strong duality; Thm 1) — η is the relative
+        duality gap between the rounded primal ρ̂ and the dual;
+      * otherwise ρ_lower = ρ_dual + min(0, λ_min)·tr X̂ (heuristic, C10).
+    η_E per App. E as printed (max(0, λ_min), P:1684)."""
+    certified = cert.lambda_min >= -cert_tol * max(1.0, normQ)
+    rho_lower = cert.rho_dual if certified else \
+        cert.rho_dual + min(0.0, cert.lambda_min) * cert.trace_X
     lowE = max(0.0, cert.lambda_min) * cert.trace_X + cert.rho_dual
     return dict(rho_lower=rho_lower, eta=suboptimality(rho_hat, rho_lower),
                 eta_E=(rho_hat - lowE) / (1.0 + abs(rho_hat) + abs(lowE)))
@@ -783,5 +789,5 @@ def solve(scene_or_arrays, opts: Options = None, Y0=None, dense_cert=False):
     dm = build_Q(s.N, s.M, s.frame, s.landmark, s.pts, s.w)
     st = staircase(dm, opts, Y0=Y0, dense_cert=dense_cert)
     sol = round_recover(dm, st.Y)
-    rep = report(st.cert, sol.rho_hat)
+    rep = report(st.cert, sol.rho_hat, dm.normF, (opts or Options()).cert_tol)
     return dm, st, sol, rep

@@ -352,7 +352,20 @@ void spmm(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep_in)
   SpmmEpiArgs ep = ep_in;
   bool timed = c->opt.profile != 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (timed) {
+  if (timed && c->cap_target) {
+    // capturing a graph: the event pair and exec flag belong to the graph
+    auto* g = c->cap_target;
+    size_t pair = g->bytes.size();
+    if ((pair + 1) * sizeof(int) > g->execf.n * sizeof(int))
+      throw Error(XM_EINVAL, "graph profiling slots exhausted");
+    XM_CUDA(cudaEventCreate(&e0));
+    XM_CUDA(cudaEventCreate(&e1));
+    g->ev.push_back(e0);
+    g->ev.push_back(e1);
+    g->bytes.push_back(8.0 * ((double)c->nrows * c->n + (double)c->n * r + (double)c->nrows * r));
+    ep.exec = g->execf.p + pair;
+    XM_CUDA(cudaEventRecord(e0, c->stream));
+  } else if (timed) {
     if (c->ev_pool.empty()) {
       for (int q = 0; q < 1024; ++q) {
         cudaEvent_t e;

@@ -62,6 +62,8 @@ void alloc_vectors(xm_ctx* c) {
   c->flags.alloc(16);
   c->cert_v.alloc((size_t)rows + 64);
   c->red.alloc((size_t)ceil_div(c->N, 128) * 4 + 1024);
+  c->part1.alloc(4096);   // fixed addresses: captured by the tCG graphs
+  c->part2.alloc((size_t)ceil_div(c->N, 128) + 4096);
 }
 
 void read_scal(xm_ctx* c, int first, int count, double* out) {
@@ -128,6 +130,63 @@ void dots(xm_ctx* c, int64_t len, int npair, const double* const* a, const doubl
   read_scal(c, 8, npair, out);
 }
 
+// Capture `tcg_batch` tCG iterations at rank r into a CUDA graph (once; all
+// buffers used by the iteration have fixed addresses).  Every kernel in it
+// early-exits once the device-side tCG state says stop, so a replay past the
+// end of tCG is a cheap no-op.  With profile=1 each SpMM is bracketed by event
+// nodes owned by the graph (harvested after every replay).
+xm_ctx::TcgGraph* tcg_graph(xm_ctx* c, int r) {
+  auto& g = c->tcg_graphs[r];
+  if (g.exec) return &g;
+  if (!c->cap_stream) XM_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  g.batch = c->tcg_batch;
+  g.execf.alloc((size_t)g.batch * 4 + 8);
+  XM_CUDA(cudaMemsetAsync(g.execf.p, 0, g.execf.n * sizeof(int), c->stream));
+  sync(c);
+  cudaStream_t orig = c->stream;
+  const int64_t l0 = c->stats.kernel_launches, s0 = c->stats.spmm_calls;
+  c->stream = c->cap_stream;
+  c->cap_target = &g;
+  cudaGraph_t graph = nullptr;
+  try {
+    XM_CUDA(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeRelaxed));
+    if (c->opt.profile)
+      XM_CUDA(cudaMemsetAsync(g.execf.p, 0, g.execf.n * sizeof(int), c->cap_stream));
+    for (int b = 0; b < g.batch; ++b) tcg_iteration(c, r);
+    XM_CUDA(cudaStreamEndCapture(c->cap_stream, &graph));
+  } catch (...) {
+    cudaStreamEndCapture(c->cap_stream, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    c->stream = orig;
+    c->cap_target = nullptr;
+    throw;
+  }
+  c->stream = orig;
+  c->cap_target = nullptr;
+  g.launches = c->stats.kernel_launches - l0;
+  g.spmms = c->stats.spmm_calls - s0;
+  c->stats.kernel_launches = l0;
+  c->stats.spmm_calls = s0;
+  XM_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
+  cudaGraphDestroy(graph);
+  return &g;
+}
+
+void harvest_graph(xm_ctx* c, xm_ctx::TcgGraph& g) {
+  const size_t np = g.bytes.size();
+  if (!np) return;
+  std::vector<int> ex(np);
+  XM_CUDA(cudaMemcpy(ex.data(), g.execf.p, np * sizeof(int), cudaMemcpyDeviceToHost));
+  for (size_t q = 0; q < np; ++q) {
+    if (!ex[q]) continue;
+    float ms = 0.f;
+    XM_CUDA(cudaEventElapsedTime(&ms, g.ev[2 * q], g.ev[2 * q + 1]));
+    c->stats.spmm_ms += ms;
+    c->stats.spmm_timed++;
+    c->stats.spmm_alg_bytes += g.bytes[q];
+  }
+}
+
 struct RtrOut {
   bool converged = false;
   int64_t outer = 0;
@@ -156,12 +215,19 @@ RtrOut rtr(xm_ctx* c, double tol_abs) {
     if (it >= o.max_outer) break;
     // ---- tCG (device-resident, double-buffered state; 3 kernels / iteration)
     tcg_init(c, r, Delta);
-    int batch = c->tcg_batch;
     TcgState hs{};
+    xm_ctx::TcgGraph* g = c->use_graphs && c->world == 1 ? tcg_graph(c, r) : nullptr;
     while (true) {
-      for (int b = 0; b < batch; ++b) tcg_iteration(c, r);
+      if (g) {
+        XM_CUDA(cudaGraphLaunch(g->exec, c->stream));
+        c->stats.kernel_launches += g->launches;
+        c->stats.spmm_calls += g->spmms;
+      } else {
+        for (int b = 0; b < c->tcg_batch; ++b) tcg_iteration(c, r);
+      }
       XM_CUDA(cudaMemcpyAsync(&hs, c->tcg.p, sizeof(TcgState), cudaMemcpyDeviceToHost, c->stream));
       sync(c);
+      if (g && c->opt.profile) harvest_graph(c, *g);
       if (hs.stop) break;
     }
     c->info.hvps += hs.n_hvp;
@@ -279,7 +345,19 @@ __global__ void k_identity_init(int N, int r, double* Y) {
   Y[t] = (col == (int)(row % 3)) ? 1.0 : 0.0;
 }
 
+void destroy_graphs(xm_ctx* c) {
+  for (auto& g : c->tcg_graphs) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    for (cudaEvent_t e : g.ev) cudaEventDestroy(e);
+    g.exec = nullptr;
+    g.ev.clear();
+    g.bytes.clear();
+    g.batch = 0;
+  }
+}
+
 void reset_after_new_Q(xm_ctx* c) {
+  destroy_graphs(c);
   c->stage = 1;
   c->factor_set = false;
   c->cert_valid = false;
@@ -375,6 +453,8 @@ void xm_destroy(xm_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  destroy_graphs(c);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   nccl_destroy(c);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -535,7 +615,10 @@ xm_status xm_certify(xm_ctx* c, xm_certificate* out, double* min_eigvec) {
     ce.rho_dual = l0[0] + l0[1] + l0[2];
     ce.rho_hat = d[0];
     ce.trace_X = trX;
-    ce.rho_lower = ce.rho_dual + std::min(0.0, c->cert_lower) * trX;
+    // η (Eq. (13)): ρ_SDP estimated by the dual value at a certified point,
+    // ρ_dual + min(0, λ_min)·tr X̂ otherwise (reading C10)
+    const bool psd_ok = c->cert_lower >= -c->opt.cert_tol * std::max(1.0, c->normQ);
+    ce.rho_lower = psd_ok ? ce.rho_dual : ce.rho_dual + std::min(0.0, lam) * trX;
     ce.eta = (ce.rho_hat - ce.rho_lower) / (1.0 + std::fabs(ce.rho_hat) + std::fabs(ce.rho_lower));
     double lowE = std::max(0.0, c->cert_lower) * trX + ce.rho_dual;
     ce.eta_E = (ce.rho_hat - lowE) / (1.0 + std::fabs(ce.rho_hat) + std::fabs(lowE));

@@ -168,7 +168,20 @@ struct xm_ctx {
   xm::DBuf<double> Zw;       // Z + εI work copy for the Cholesky PSD test
   double cert_lower = 0.0;   // certified lower bound on λ_min(Z)
   int cert_method = 0;       // 0 Lanczos converged, 1 Cholesky of Z + εI
-  int tcg_batch = 4;
+  int tcg_batch = 8;
+  // CUDA graph of `tcg_batch` tCG iterations per rank r (captured once, replayed)
+  struct TcgGraph {
+    cudaGraphExec_t exec = nullptr;
+    int batch = 0;
+    int64_t launches = 0, spmms = 0;              // kernels / SpMMs per replay
+    std::vector<cudaEvent_t> ev;                  // profiling event pairs (captured)
+    std::vector<double> bytes;                    // algorithmic bytes per pair
+    xm::DBuf<int> execf;                          // per pair: 1 if the SpMM ran
+  };
+  TcgGraph tcg_graphs[XM_MAX_R + 1];
+  TcgGraph* cap_target = nullptr;                 // non-null while capturing
+  cudaStream_t cap_stream = nullptr;
+  bool use_graphs = true;
   std::string last_error;
 };
 
