@@ -364,7 +364,8 @@ void spmm(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep_in)
     g->ev.push_back(e1);
     g->bytes.push_back(8.0 * ((double)c->nrows * c->n + (double)c->n * r + (double)c->nrows * r));
     ep.exec = g->execf.p + pair;
-    XM_CUDA(cudaEventRecord(e0, c->stream));
+    // External ⇒ captured as an event-record node (plain records are capture markers)
+    XM_CUDA(cudaEventRecordWithFlags(e0, c->stream, cudaEventRecordExternal));
   } else if (timed) {
     if (c->ev_pool.empty()) {
       for (int q = 0; q < 1024; ++q) {
@@ -392,7 +393,10 @@ void spmm(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep_in)
     case EPI_GRAD: launch_mode<EPI_GRAD>(c, V, r, ep); break;
     default: throw Error(XM_EINVAL, "bad epilogue");
   }
-  if (timed) XM_CUDA(cudaEventRecord(e1, c->stream));
+  if (timed) {
+    if (c->cap_target) XM_CUDA(cudaEventRecordWithFlags(e1, c->stream, cudaEventRecordExternal));
+    else XM_CUDA(cudaEventRecord(e1, c->stream));
+  }
   c->stats.spmm_calls++;
   c->stats.spmm_rows = c->nrows;
 }
