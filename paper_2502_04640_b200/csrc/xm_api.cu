@@ -135,9 +135,29 @@ void dots(xm_ctx* c, int64_t len, int npair, const double* const* a, const doubl
 // early-exits once the device-side tCG state says stop, so a replay past the
 // end of tCG is a cheap no-op.  With profile=1 each SpMM is bracketed by event
 // nodes owned by the graph (harvested after every replay).
+std::vector<uintptr_t> graph_signature(xm_ctx* c) {
+  return {(uintptr_t)c->N, (uintptr_t)c->n, (uintptr_t)c->ldq, (uintptr_t)c->Q.p,
+          (uintptr_t)c->Y.p, (uintptr_t)c->dir.p, (uintptr_t)c->lam.p, (uintptr_t)c->tcg.p,
+          (uintptr_t)c->part1.p, (uintptr_t)c->part2.p, (uintptr_t)c->opt.profile,
+          (uintptr_t)c->f0, (uintptr_t)c->f1};
+}
+
+void destroy_graph(xm_ctx::TcgGraph& g) {
+  if (g.exec) cudaGraphExecDestroy(g.exec);
+  for (cudaEvent_t e : g.ev) cudaEventDestroy(e);
+  g.exec = nullptr;
+  g.ev.clear();
+  g.bytes.clear();
+  g.sig.clear();
+  g.batch = 0;
+}
+
 xm_ctx::TcgGraph* tcg_graph(xm_ctx* c, int r) {
   auto& g = c->tcg_graphs[r];
-  if (g.exec) return &g;
+  auto sig = graph_signature(c);
+  if (g.exec && g.sig == sig) return &g;
+  destroy_graph(g);
+  g.sig = sig;
   if (!c->cap_stream) XM_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
   g.batch = c->tcg_batch;
   g.execf.alloc((size_t)g.batch * 4 + 8);
@@ -346,18 +366,10 @@ __global__ void k_identity_init(int N, int r, double* Y) {
 }
 
 void destroy_graphs(xm_ctx* c) {
-  for (auto& g : c->tcg_graphs) {
-    if (g.exec) cudaGraphExecDestroy(g.exec);
-    for (cudaEvent_t e : g.ev) cudaEventDestroy(e);
-    g.exec = nullptr;
-    g.ev.clear();
-    g.bytes.clear();
-    g.batch = 0;
-  }
+  for (auto& g : c->tcg_graphs) destroy_graph(g);
 }
 
 void reset_after_new_Q(xm_ctx* c) {
-  destroy_graphs(c);
   c->stage = 1;
   c->factor_set = false;
   c->cert_valid = false;

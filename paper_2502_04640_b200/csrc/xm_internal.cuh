@@ -177,6 +177,7 @@ struct xm_ctx {
     std::vector<cudaEvent_t> ev;                  // profiling event pairs (captured)
     std::vector<double> bytes;                    // algorithmic bytes per pair
     xm::DBuf<int> execf;                          // per pair: 1 if the SpMM ran
+    std::vector<uintptr_t> sig;                   // buffers / sizes the capture baked in
   };
   TcgGraph tcg_graphs[XM_MAX_R + 1];
   TcgGraph* cap_target = nullptr;                 // non-null while capturing
