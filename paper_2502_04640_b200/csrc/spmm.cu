@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(
 }
 
 int spmm_grid(xm_ctx* c, int r) {
-  (void)r;
+  if (spmm_sym_supported(c, r)) return ceil_div(c->N, 128);  // k_sym_finish blocks
   int nown = std::max(1, c->f1 - c->f0);
   return std::max(1, std::min(148, nown));
 }
@@ -345,6 +345,14 @@ static void launch_mode(xm_ctx* c, const double* V, int r, const SpmmEpiArgs& ep
   }
 }
 
+// Algorithmic bytes of one product: Q (full rows, or the lower triangle when
+// the symmetric kernel runs) + V in + result out.
+static double alg_bytes(xm_ctx* c, int r) {
+  const double n = c->n;
+  const double qb = spmm_sym_supported(c, r) ? 8.0 * n * (n + 1) / 2 : 8.0 * (double)c->nrows * n;
+  return qb + 8.0 * n * r + 8.0 * (double)c->nrows * r;
+}
+
 // One (optionally profiled) SpMM launch with epilogue `mode` on this rank's rows.
 void spmm(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep_in) {
   if (mode != EPI_STORE && c->world > 1)
@@ -362,7 +370,7 @@ void spmm(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep_in)
     XM_CUDA(cudaEventCreate(&e1));
     g->ev.push_back(e0);
     g->ev.push_back(e1);
-    g->bytes.push_back(8.0 * ((double)c->nrows * c->n + (double)c->n * r + (double)c->nrows * r));
+    g->bytes.push_back(alg_bytes(c, r));
     ep.exec = g->execf.p + pair;
     // External ⇒ captured as an event-record node (plain records are capture markers)
     XM_CUDA(cudaEventRecordWithFlags(e0, c->stream, cudaEventRecordExternal));
@@ -382,10 +390,12 @@ void spmm(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep_in)
     e1 = c->ev_pool[c->ev_used++];
     size_t pair = c->ev_used / 2 - 1;
     ep.exec = c->ev_exec.p + pair;
-    c->ev_bytes[pair] = 8.0 * ((double)c->nrows * c->n + (double)c->n * r + (double)c->nrows * r);
+    c->ev_bytes[pair] = alg_bytes(c, r);
     XM_CUDA(cudaEventRecord(e0, c->stream));
   }
-  switch (mode) {
+  if (spmm_sym_supported(c, r)) {
+    spmm_sym_launch(c, V, r, mode, ep);
+  } else switch (mode) {
     case EPI_STORE: launch_mode<EPI_STORE>(c, V, r, ep); break;
     case EPI_HVP: launch_mode<EPI_HVP>(c, V, r, ep); break;
     case EPI_ZMUL: launch_mode<EPI_ZMUL>(c, V, r, ep); break;

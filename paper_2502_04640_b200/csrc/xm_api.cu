@@ -442,6 +442,9 @@ xm_status xm_create(xm_ctx** out, int device, int rank, int world, const void* n
   c->rank = rank;
   c->world = world;
   if (opts) c->opt = *opts; else xm_default_options(&c->opt);
+  // A/B switches for measurements (the defaults are the production path)
+  if (std::getenv("XM_NO_SYM")) c->use_sym = false;
+  if (std::getenv("XM_NO_GRAPHS")) c->use_graphs = false;
   if (c->opt.rank_cap > XM_MAX_R) c->opt.rank_cap = XM_MAX_R;
   xm_status st = guard(c, [&] {
     if (cuda_stream) {

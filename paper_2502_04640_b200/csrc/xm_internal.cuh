@@ -183,6 +183,8 @@ struct xm_ctx {
   TcgGraph* cap_target = nullptr;                 // non-null while capturing
   cudaStream_t cap_stream = nullptr;
   bool use_graphs = true;
+  bool use_sym = true;             // symmetric (lower-triangle) SpMM on one GPU, r ≤ 6
+  xm::DBuf<double> sym_part;       // per-unit row / column partials of the symmetric SpMM
   std::string last_error;
 };
 
@@ -235,7 +237,9 @@ struct SpmmEpiArgs {
   const int* stop = nullptr;     // no-op when *stop != 0
   int* exec = nullptr;           // profiling: set to 1 when the kernel ran
 };
-int spmm_grid(xm_ctx* c, int r);  // number of CTAs = number of scalar partials
+int spmm_grid(xm_ctx* c, int r);  // number of scalar partials written by spmm()
+bool spmm_sym_supported(xm_ctx* c, int r);
+void spmm_sym_launch(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep);
 void spmm(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep);
 // Full product into out (n × r, replicated): this rank's rows + all-gather.
 void spmm_full(xm_ctx* c, const double* V, int r, double* out_full, const int* stop = nullptr);
