@@ -1,41 +1,50 @@
 // spmm_sym.cu — H6 with symmetric Q: out = Q·V streaming only the lower
-// triangle (Q = Qᵀ by construction, Prop. 1), i.e. half of the HBM bytes of
-// the full-row kernel.
+// triangle (Q = Qᵀ by construction, Prop. 1) — half the HBM bytes of the
+// full-row kernel (spmm.cu).
 //
 //   out_i = Σ_{j ≤ i} Q_ij V_j  +  Σ_{j > i} Q_ji V_j
-//         = (row part of the lower triangle) + (column part of the strictly lower triangle)
+//         = row part (lower triangle) + column part (strictly lower triangle)
 //
-// Work units are the T(T+1)/2 lower-triangular 128×128 blocks (I, J ≥ ... J ≤ I),
-// distributed as contiguous ranges over G = 148 persistent CTAs (one per SM).
-// For unit (I, J) a CTA produces, deterministically,
-//   rowpart[u][ℓ] = Σ_{j in block J, j ≤ i} Q_ij V_j      (ℓ = row within block I)
-//   colpart[u][m] = Σ_{i in block I, i > j} Q_ij V_i      (m = column within block J)
-// and k_sym_finish sums, for each output row in block K, the row parts of
-// units (K, 0..K) and the column parts of units (K..T−1, K) in a fixed order,
-// then applies the per-camera epilogue (same modes as spmm.cu).
+// Geometry.  Units are the lower-triangular 128-row × 256-column blocks
+// (I, J), J ≤ ⌊I/2⌋; a unit is 16 tiles of 8 rows × 256 columns (16 KB).  The
+// W = 16·U tiles are split stream-K style into G = 148 equal contiguous ranges
+// (one persistent CTA per SM), so every SM streams the same number of tiles.
+// A CTA's range is a sequence of *segments* (maximal runs of tiles of one
+// unit); a unit cut between two CTAs simply yields two segments.
 //
-// Pipeline per CTA: one producer thread streams 32-row × 128-column Q tiles
-// (one cp.async.bulk per row, diagonal rows only up to the diagonal; L2
-// evict-first) into a 4-stage ring, and per unit the V_J / V_I row blocks into
-// a 2-slot ring.  8 consumer warps: warp w owns 4 rows of every tile, lane ℓ
-// owns the 4 interleaved columns {2ℓ, 2ℓ+1, 64+2ℓ, 65+2ℓ} (conflict-free
-// LDS.128).  V_J for the lane's columns lives in registers for the unit; the
-// column partials accumulate in registers over the unit's 128 rows and are
-// combined across warps in a fixed order through shared memory.
+// Per tile (warp w ↔ row w, lane ℓ ↔ the 8 columns {2ℓ+64m, 2ℓ+64m+1},
+// m = 0..3 — conflict-free LDS.128):
+//   row part   r_i += Σ_j Q_ij V_j  with V_J for the lane's columns held in
+//              registers for the whole segment; one 5-level shuffle reduction
+//              per row, then lane 0 writes rowpart[u][ℓ] (each row of a unit
+//              lives in exactly one tile ⇒ single writer);
+//   column part c_j += Q_ij V_i (j < i), accumulated in registers over the
+//              segment's rows (V_i broadcast from shared memory), then summed
+//              over the 8 warps in a fixed order and written to colpart[segment].
+// The producer thread streams each tile with one cp.async.bulk per row (rows
+// of diagonal units only up to the diagonal; L2 evict-first) into an 8-stage
+// ring (8 × 16 KB); the per-segment V_J / V_I blocks go through a 2-slot ring.
 //
-// Algorithmic bytes per product: 8·n(n+1)/2 (lower triangle of Q) + 16·n·r.
+// k_sym_finish (one CTA per 64 cameras) sums, in a fixed order, the row parts
+// of units (K, 0..⌊K/2⌋) and the column parts of every segment of column block
+// ⌊row/256⌋, then applies the per-camera epilogue (same modes as spmm.cu).
+// Deterministic; algorithmic bytes per product: 8·n(n+1)/2 + 16·n·r.
 #include "frame_ops.cuh"
+
+#include <map>
 
 namespace xm {
 
 namespace {
 constexpr int kWarps = 8;
 constexpr int kThreads = 32 * (kWarps + 1);
-constexpr int BT = 128;          // unit block size
-constexpr int TR = 32;           // rows per streamed tile
-constexpr int kTiles = BT / TR;  // tiles per unit
-constexpr int kStages = 4;
-constexpr int kTileBytes = TR * BT * 8;  // 32 KB
+constexpr int BR = 128;                 // unit rows
+constexpr int BC = 256;                 // unit columns
+constexpr int TR = 8;                   // rows per tile (one per warp)
+constexpr int kTilesPerUnit = BR / TR;  // 16
+constexpr int kStages = 8;
+constexpr int kTileBytes = TR * BC * 8;  // 16 KB
+constexpr int kFinishFrames = 64;
 
 __device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void bar_init(uint64_t* b, unsigned cnt) {
@@ -72,45 +81,113 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(su32(b)), "l"(pol)
       : "memory");
 }
-__device__ __forceinline__ void unit_ij(int64_t u, int& I, int& J) {
-  int i = (int)((sqrt(8.0 * (double)u + 1.0) - 1.0) * 0.5);
-  while ((int64_t)(i + 1) * (i + 2) / 2 <= u) ++i;
-  while ((int64_t)i * (i + 1) / 2 > u) --i;
-  I = i;
-  J = (int)(u - (int64_t)i * (i + 1) / 2);
+// unit u → (I, J) using unit_base[I] = Σ_{I'<I} (⌊I'·BR/BC⌋ + 1)
+__device__ __forceinline__ void unit_ij(int u, const int* __restrict__ ubase, int TRb, int& I, int& J) {
+  int lo = 0, hi = TRb - 1;
+  while (lo < hi) {  // largest I with ubase[I] ≤ u
+    int mid = (lo + hi + 1) >> 1;
+    if (ubase[mid] <= u) lo = mid; else hi = mid - 1;
+  }
+  I = lo;
+  J = u - ubase[lo];
 }
 }  // namespace
 
+// Static work plan for one (n, G): unit bases, per-CTA segment bases and the
+// per-column-block list of segments (fixed summation order for the finish).
+struct SymPlan {
+  int n = 0, G = 0, TRb = 0, TCb = 0, U = 0, S = 0;
+  DBuf<int> ubase;     // TRb + 1
+  DBuf<int> segbase;   // G + 1
+  DBuf<int> segunit;   // S
+  DBuf<int> colptr;    // TCb + 1
+  DBuf<int> colidx;    // S (segments grouped by column block, ordered by unit then CTA)
+};
+
+static SymPlan& sym_plan(xm_ctx* c) {
+  static std::map<xm_ctx*, SymPlan> plans;  // one plan per context
+  SymPlan& p = plans[c];
+  const int n = c->n, G = 148;
+  if (p.n == n && p.G == G && p.ubase.p) return p;
+  p.n = n;
+  p.G = G;
+  p.TRb = ceil_div(n, BR);
+  p.TCb = ceil_div(n, BC);
+  std::vector<int> ub(p.TRb + 1, 0);
+  for (int I = 0; I < p.TRb; ++I) ub[I + 1] = ub[I] + (I * BR) / BC + 1;
+  p.U = ub[p.TRb];
+  const int64_t W = (int64_t)p.U * kTilesPerUnit;
+  std::vector<int> segbase(G + 1, 0), segunit;
+  for (int cta = 0; cta < G; ++cta) {
+    int64_t t0 = (int64_t)cta * W / G, t1 = (int64_t)(cta + 1) * W / G;
+    segbase[cta] = (int)segunit.size();
+    int last = -1;
+    for (int64_t t = t0; t < t1; ++t) {
+      int u = (int)(t / kTilesPerUnit);
+      if (u != last) {
+        segunit.push_back(u);
+        last = u;
+      }
+    }
+  }
+  segbase[G] = (int)segunit.size();
+  p.S = (int)segunit.size();
+  auto unitJ = [&](int u) {
+    int I = 0;
+    while (ub[I + 1] <= u) ++I;
+    return u - ub[I];
+  };
+  std::vector<std::vector<int>> bycol(p.TCb);
+  for (int s = 0; s < p.S; ++s) bycol[unitJ(segunit[s])].push_back(s);  // s increasing ⇒ unit, then CTA order
+  std::vector<int> colptr(p.TCb + 1, 0), colidx;
+  for (int J = 0; J < p.TCb; ++J) {
+    for (int s : bycol[J]) colidx.push_back(s);
+    colptr[J + 1] = (int)colidx.size();
+  }
+  p.ubase.alloc(ub.size());
+  p.segbase.alloc(segbase.size());
+  p.segunit.alloc(std::max<size_t>(1, segunit.size()));
+  p.colptr.alloc(colptr.size());
+  p.colidx.alloc(std::max<size_t>(1, colidx.size()));
+  XM_CUDA(cudaMemcpy(p.ubase.p, ub.data(), ub.size() * 4, cudaMemcpyHostToDevice));
+  XM_CUDA(cudaMemcpy(p.segbase.p, segbase.data(), segbase.size() * 4, cudaMemcpyHostToDevice));
+  if (!segunit.empty())
+    XM_CUDA(cudaMemcpy(p.segunit.p, segunit.data(), segunit.size() * 4, cudaMemcpyHostToDevice));
+  XM_CUDA(cudaMemcpy(p.colptr.p, colptr.data(), colptr.size() * 4, cudaMemcpyHostToDevice));
+  if (!colidx.empty())
+    XM_CUDA(cudaMemcpy(p.colidx.p, colidx.data(), colidx.size() * 4, cudaMemcpyHostToDevice));
+  return p;
+}
+
 template <int R>
 struct SymCfg {
-  static constexpr int kVBlockBytes = BT * R * 8;           // one V row block
-  static constexpr int kColRedBytes = kWarps * BT * R * 8;  // cross-warp column reduction
-  static constexpr size_t kSmem = (size_t)kStages * kTileBytes + 2 * 2 * kVBlockBytes +
-                                  kColRedBytes + 64 * 8;
+  static constexpr int kVJ = BC * R;   // doubles
+  static constexpr int kVI = BR * R;
+  static constexpr size_t kSmem = (size_t)kStages * kTileBytes + 2 * (size_t)(kVJ + kVI) * 8 +
+                                  (size_t)BC * R * 8 + 64 * 8;
 };
 
 template <int R>
-__global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(const double* __restrict__ Q, int64_t ldq,
-                                                          int n, int T, const double* __restrict__ V,
-                                                          double* __restrict__ part,
-                                                          const int* __restrict__ stop,
-                                                          int* __restrict__ exec) {
+__global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
+    const double* __restrict__ Q, int64_t ldq, int n, int TRb, int U, const int* __restrict__ ubase,
+    const int* __restrict__ segbase, const double* __restrict__ V, double* __restrict__ rowpart,
+    double* __restrict__ colpart, const int* __restrict__ stop, int* __restrict__ exec) {
   using Cfg = SymCfg<R>;
   if (stop && *stop) return;
   if (exec && blockIdx.x == 0 && threadIdx.x == 0) *exec = 1;
   extern __shared__ __align__(128) unsigned char sm[];
   double* tiles = reinterpret_cast<double*>(sm);
-  double* vbuf = reinterpret_cast<double*>(sm + (size_t)kStages * kTileBytes);  // [2 slots][VJ, VI]
-  double* colred = vbuf + 2 * 2 * BT * R;                                           // [warp][BT][R]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(colred + kWarps * BT * R);
+  double* vbuf = tiles + (size_t)kStages * TR * BC;  // 2 slots × (V_J, V_I)
+  double* colred = vbuf + 2 * (Cfg::kVJ + Cfg::kVI);  // [BC][R]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(colred + BC * R);
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages;
   uint64_t* vfull = bars + 2 * kStages;
   uint64_t* vempty = vfull + 2;
 
-  const int64_t U = (int64_t)T * (T + 1) / 2;
-  const int64_t u0 = (int64_t)blockIdx.x * U / gridDim.x;
-  const int64_t u1 = (int64_t)(blockIdx.x + 1) * U / gridDim.x;
+  const int64_t W = (int64_t)U * kTilesPerUnit;
+  const int64_t t0 = (int64_t)blockIdx.x * W / gridDim.x;
+  const int64_t t1 = (int64_t)(blockIdx.x + 1) * W / gridDim.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -124,169 +201,212 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(const double* __restri
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  if (t0 >= t1) return;
 
   if (warp == kWarps) {
     // ------------------------------------------------------------ producer
     if (lane != 0) return;
     const uint64_t pq = pol_first(), pv = pol_last();
-    int it = 0;
-    int uu = 0;
-    for (int64_t u = u0; u < u1; ++u, ++uu) {
+    int it = 0, seg = 0, cur_u = -1;
+    for (int64_t t = t0; t < t1; ++t, ++it) {
+      const int u = (int)(t / kTilesPerUnit);
+      const int tl = (int)(t % kTilesPerUnit);
       int I, J;
-      unit_ij(u, I, J);
-      const int vs = uu & 1;
-      bar_wait(&vempty[vs], (unsigned)(((uu >> 1) & 1) ^ 1));
-      const int nj = min(BT, n - J * BT), ni = min(BT, n - I * BT);
-      const unsigned bj = (unsigned)(((nj * R + 1) & ~1) * 8), bi = (unsigned)(((ni * R + 1) & ~1) * 8);
-      bar_expect(&vfull[vs], bj + bi);
-      double* vj = vbuf + (size_t)vs * 2 * BT * R;
-      bulk_g2s(vj, V + (int64_t)J * BT * R, bj, &vfull[vs], pv);
-      bulk_g2s(vj + BT * R, V + (int64_t)I * BT * R, bi, &vfull[vs], pv);
-      for (int t = 0; t < kTiles; ++t, ++it) {
-        const int s = it % kStages;
-        bar_wait(&empty[s], (unsigned)(((it / kStages) & 1) ^ 1));
-        const int r0 = I * BT + t * TR;
-        const int rows = max(0, min(TR, n - r0));
-        unsigned total = 0;
-        unsigned len[TR];
-        for (int q = 0; q < rows; ++q) {
-          int i = r0 + q;
-          int cols = (I == J) ? (i - J * BT + 1) : nj;
-          len[q] = (unsigned)(((cols + 1) & ~1) * 8);
-          total += len[q];
-        }
-        bar_expect(&full[s], total);
-        double* st = tiles + (size_t)s * TR * BT;
-        for (int q = 0; q < rows; ++q)
-          bulk_g2s(st + q * BT, Q + (int64_t)(r0 + q) * ldq + (int64_t)J * BT, len[q], &full[s], pq);
+      unit_ij(u, ubase, TRb, I, J);
+      if (u != cur_u) {  // new segment: stage V_J and V_I
+        const int vs = seg & 1;
+        bar_wait(&vempty[vs], (unsigned)(((seg >> 1) & 1) ^ 1));
+        const int nj = min(BC, n - J * BC), ni = min(BR, n - I * BR);
+        const unsigned bj = (unsigned)(((nj * R + 1) & ~1) * 8);
+        const unsigned bi = (unsigned)(((ni * R + 1) & ~1) * 8);
+        bar_expect(&vfull[vs], bj + bi);
+        double* vj = vbuf + (size_t)vs * (Cfg::kVJ + Cfg::kVI);
+        bulk_g2s(vj, V + (int64_t)J * BC * R, bj, &vfull[vs], pv);
+        bulk_g2s(vj + Cfg::kVJ, V + (int64_t)I * BR * R, bi, &vfull[vs], pv);
+        cur_u = u;
+        ++seg;
       }
+      const int s = it % kStages;
+      bar_wait(&empty[s], (unsigned)(((it / kStages) & 1) ^ 1));
+      const int r0 = I * BR + tl * TR;
+      const bool dblk = (J == (I * BR) / BC);  // column block holding the diagonal
+      unsigned len[TR];
+      unsigned total = 0;
+#pragma unroll
+      for (int q = 0; q < TR; ++q) {
+        const int i = r0 + q;
+        int cols = 0;
+        if (i < n) cols = dblk ? (i - J * BC + 1) : min(BC, n - J * BC);
+        len[q] = (unsigned)(((cols + 1) & ~1) * 8);
+        total += len[q];
+      }
+      bar_expect(&full[s], total);
+      double* st = tiles + (size_t)s * TR * BC;
+#pragma unroll
+      for (int q = 0; q < TR; ++q)
+        if (len[q]) bulk_g2s(st + q * BC, Q + (int64_t)(r0 + q) * ldq + (int64_t)J * BC, len[q], &full[s], pq);
     }
     return;
   }
 
   // ------------------------------------------------------------ consumers
-  int it = 0;
-  int uu = 0;
-  const int c0 = 2 * lane, c1 = 64 + 2 * lane;  // lane's column pairs within the block
-  for (int64_t u = u0; u < u1; ++u, ++uu) {
-    int I, J;
-    unit_ij(u, I, J);
-    const bool diag = (I == J);
-    const int vs = uu & 1;
-    bar_wait(&vfull[vs], (unsigned)((uu >> 1) & 1));
-    const double* vj = vbuf + (size_t)vs * 2 * BT * R;
-    const double* vi = vj + BT * R;
-    const int nj = min(BT, n - J * BT);
-    double vr[4][R];  // V_J for the lane's 4 columns
-    const int cl[4] = {c0, c0 + 1, c1, c1 + 1};
+  int it = 0, seg = 0, cur_u = -1;
+  int I = 0, J = 0;
+  bool dblk = false;
+  double vr[8][R];      // V_J rows for the lane's 8 columns
+  double colacc[8][R];  // column partials for the lane's 8 columns
+  const double* vi = nullptr;
+  int vs = 0;
+  auto flush = [&](int slot_seg) {
+    // fixed-order cross-warp sum of colacc into colred, then to global
+    for (int w = 0; w < kWarps; ++w) {
+      if (warp == w) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+        for (int m = 0; m < 4; ++m)
 #pragma unroll
-      for (int cc = 0; cc < R; ++cc) vr[k][cc] = (cl[k] < nj) ? vj[cl[k] * R + cc] : 0.0;
-    double colacc[4][R];
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-#pragma unroll
-      for (int cc = 0; cc < R; ++cc) colacc[k][cc] = 0.0;
-    for (int t = 0; t < kTiles; ++t, ++it) {
-      const int s = it % kStages;
-      bar_wait(&full[s], (unsigned)((it / kStages) & 1));
-      const double* st = tiles + (size_t)s * TR * BT;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int rl = t * TR + warp * 4 + q;  // row within block I
-        const int i = I * BT + rl;
-        double rs[R];
-#pragma unroll
-        for (int cc = 0; cc < R; ++cc) rs[cc] = 0.0;
-        if (i < n) {
-          const double2 qa = *reinterpret_cast<const double2*>(st + (warp * 4 + q) * BT + c0);
-          const double2 qb = *reinterpret_cast<const double2*>(st + (warp * 4 + q) * BT + c1);
-          const double qv[4] = {qa.x, qa.y, qb.x, qb.y};
-          double vrow[R];
-#pragma unroll
-          for (int cc = 0; cc < R; ++cc) vrow[cc] = vi[rl * R + cc];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int jl = cl[k];
-            const bool in_row = diag ? (jl <= rl) : (jl < nj);
-            const bool in_col = diag ? (jl < rl) : (jl < nj);
-            const double x = in_row ? qv[k] : 0.0;
-            const double y = in_col ? qv[k] : 0.0;
+          for (int h = 0; h < 2; ++h) {
+            const int jl = 2 * lane + 64 * m + h;
 #pragma unroll
             for (int cc = 0; cc < R; ++cc) {
-              rs[cc] = fma(x, vr[k][cc], rs[cc]);
-              colacc[k][cc] = fma(y, vrow[cc], colacc[k][cc]);
+              double v = colacc[2 * m + h][cc];
+              colred[jl * R + cc] = (w == 0) ? v : colred[jl * R + cc] + v;
             }
           }
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kWarps) : "memory");
+    }
+    double* dst = colpart + ((int64_t)(segbase[blockIdx.x] + slot_seg)) * BC * R;
+    for (int e = threadIdx.x; e < BC * R; e += 32 * kWarps) dst[e] = colred[e];
+    asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kWarps) : "memory");
+  };
+  for (int64_t t = t0; t < t1; ++t, ++it) {
+    const int u = (int)(t / kTilesPerUnit);
+    const int tl = (int)(t % kTilesPerUnit);
+    if (u != cur_u) {
+      if (cur_u >= 0) {
+        if (lane == 0) bar_arrive(&vempty[vs]);
+        flush(seg - 1);
+      }
+      unit_ij(u, ubase, TRb, I, J);
+      dblk = (J == (I * BR) / BC);
+      vs = seg & 1;
+      bar_wait(&vfull[vs], (unsigned)((seg >> 1) & 1));
+      const double* vj = vbuf + (size_t)vs * (Cfg::kVJ + Cfg::kVI);
+      vi = vj + Cfg::kVJ;
+      const int nj = min(BC, n - J * BC);
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int jl = 2 * lane + 64 * m + h;
+#pragma unroll
+          for (int cc = 0; cc < R; ++cc) {
+            vr[2 * m + h][cc] = (jl < nj) ? vj[jl * R + cc] : 0.0;
+            colacc[2 * m + h][cc] = 0.0;
+          }
         }
+      cur_u = u;
+      ++seg;
+    }
+    const int s = it % kStages;
+    bar_wait(&full[s], (unsigned)((it / kStages) & 1));
+    const double* st = tiles + (size_t)s * TR * BC + warp * BC;
+    const int rl = tl * TR + warp;  // row within the unit
+    const int i = I * BR + rl;
+    if (i < n) {
+      const int jmax = dblk ? (i - J * BC) : (min(BC, n - J * BC) - 1);  // last column (row part)
+      double rs[R];
+#pragma unroll
+      for (int cc = 0; cc < R; ++cc) rs[cc] = 0.0;
+      double vrow[R];
+#pragma unroll
+      for (int cc = 0; cc < R; ++cc) vrow[cc] = vi[rl * R + cc];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int jl = 2 * lane + 64 * m;
+        double2 q2 = make_double2(0.0, 0.0);
+        if (jl <= jmax) q2 = *reinterpret_cast<const double2*>(st + jl);
+        const double qa = q2.x;
+        const double qb = (jl + 1 <= jmax) ? q2.y : 0.0;
+        // column part: strictly below the diagonal (j < i) — on the diagonal
+        // block drop j == i; jl + 1 > jmax already zeroed above.
+        const double ca = (dblk && jl == jmax) ? 0.0 : qa;
+        const double cb = (dblk && jl + 1 == jmax) ? 0.0 : qb;
 #pragma unroll
         for (int cc = 0; cc < R; ++cc) {
-          double v = rs[cc];
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-          rs[cc] = v;
-        }
-        if (lane == 0 && i < n) {
-          double* pr = part + (u * 2 * BT + rl) * R;
-#pragma unroll
-          for (int cc = 0; cc < R; ++cc) pr[cc] = rs[cc];
+          rs[cc] = fma(qa, vr[2 * m][cc], fma(qb, vr[2 * m + 1][cc], rs[cc]));
+          colacc[2 * m][cc] = fma(ca, vrow[cc], colacc[2 * m][cc]);
+          colacc[2 * m + 1][cc] = fma(cb, vrow[cc], colacc[2 * m + 1][cc]);
         }
       }
-      __syncwarp();
-      if (lane == 0) bar_arrive(&empty[s]);
+#pragma unroll
+      for (int cc = 0; cc < R; ++cc) {
+        double v = rs[cc];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        rs[cc] = v;
+      }
+      if (lane == 0) {
+        double* pr = rowpart + ((int64_t)u * BR + rl) * R;
+#pragma unroll
+        for (int cc = 0; cc < R; ++cc) pr[cc] = rs[cc];
+      }
     }
+    __syncwarp();
+    if (lane == 0) bar_arrive(&empty[s]);
+  }
+  if (cur_u >= 0) {
     if (lane == 0) bar_arrive(&vempty[vs]);
-    // column partials: registers → smem [warp][col][R] → fixed-order sum over warps
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-#pragma unroll
-      for (int cc = 0; cc < R; ++cc) colred[(warp * BT + cl[k]) * R + cc] = colacc[k][cc];
-    asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kWarps) : "memory");
-    for (int e = threadIdx.x; e < nj * R; e += 32 * kWarps) {
-      double sum = 0.0;
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) sum += colred[w * BT * R + e];
-      part[(u * 2 * BT + BT) * R + e] = sum;
-    }
-    asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kWarps) : "memory");
+    flush(seg - 1);
   }
 }
 
 // ---------------------------------------------------------------- finish + epilogue
+// CTA = kFinishFrames cameras (3·64 rows): phase 1 one thread per row sums the
+// row parts (units (K, 0..⌊K/2⌋)) and the column parts of all segments of the
+// row's column block in fixed order; phase 2 one thread per camera epilogue.
 template <int R, int MODE>
-__global__ void __launch_bounds__(128) k_sym_finish(int N, int n, int T, const double* __restrict__ part,
-                                                    const double* __restrict__ V, SpmmEpiArgs ep) {
+__global__ void __launch_bounds__(3 * kFinishFrames) k_sym_finish(
+    int N, int n, const int* __restrict__ ubase, const int* __restrict__ segunit,
+    const int* __restrict__ colptr, const int* __restrict__ colidx, const double* __restrict__ rowpart,
+    const double* __restrict__ colpart, const double* __restrict__ V, SpmmEpiArgs ep) {
   if (ep.stop && *ep.stop) return;
-  const int i = blockIdx.x * 128 + threadIdx.x;
+  __shared__ double qrow[3 * kFinishFrames][R];
+  const int f0 = blockIdx.x * kFinishFrames;
+  const int row = 3 * f0 + threadIdx.x;
+  if (row < n) {
+    double acc[R];
+#pragma unroll
+    for (int cc = 0; cc < R; ++cc) acc[cc] = 0.0;
+    const int K = row / BR, l = row % BR;
+    const int u0 = ubase[K], u1 = ubase[K + 1];
+    for (int u = u0; u < u1; ++u) {
+      const double* p = rowpart + ((int64_t)u * BR + l) * R;
+#pragma unroll
+      for (int cc = 0; cc < R; ++cc) acc[cc] += p[cc];
+    }
+    const int Jc = row / BC, m = row % BC;
+    for (int q = colptr[Jc]; q < colptr[Jc + 1]; ++q) {
+      const double* p = colpart + ((int64_t)colidx[q] * BC + m) * R;
+#pragma unroll
+      for (int cc = 0; cc < R; ++cc) acc[cc] += p[cc];
+    }
+#pragma unroll
+    for (int cc = 0; cc < R; ++cc) qrow[threadIdx.x][cc] = acc[cc];
+  }
+  __syncthreads();
   constexpr int NC = (MODE == EPI_GRAD) ? 3 : (MODE == EPI_DF ? 2 : 1);
   double pt[NC];
 #pragma unroll
   for (int q = 0; q < NC; ++q) pt[q] = (MODE == EPI_GRAD && q == 2) ? 1.0e300 : 0.0;
-  if (i < N) {
+  const int lf = threadIdx.x;
+  const int i = f0 + lf;
+  if (lf < kFinishFrames && i < N) {
     Blk<R> qv;
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const int row = 3 * i + a;
-      const int K = row / BT, l = row % BT;
-      double acc[R];
+    for (int a = 0; a < 3; ++a)
 #pragma unroll
-      for (int cc = 0; cc < R; ++cc) acc[cc] = 0.0;
-      for (int J = 0; J <= K; ++J) {  // row parts of units (K, J)
-        const int64_t u = (int64_t)K * (K + 1) / 2 + J;
-        const double* p = part + (u * 2 * BT + l) * R;
-#pragma unroll
-        for (int cc = 0; cc < R; ++cc) acc[cc] += p[cc];
-      }
-      for (int Ib = K; Ib < T; ++Ib) {  // column parts of units (Ib, K)
-        const int64_t u = (int64_t)Ib * (Ib + 1) / 2 + K;
-        const double* p = part + (u * 2 * BT + BT + l) * R;
-#pragma unroll
-        for (int cc = 0; cc < R; ++cc) acc[cc] += p[cc];
-      }
-#pragma unroll
-      for (int cc = 0; cc < R; ++cc) qv.v[a][cc] = acc[cc];
-    }
+      for (int cc = 0; cc < R; ++cc) qv.v[a][cc] = qrow[3 * lf + a][cc];
     if (MODE == EPI_STORE) {
       store_blk<R>(ep.out, i, qv);
     } else if (MODE == EPI_HVP) {
@@ -333,30 +453,32 @@ __global__ void __launch_bounds__(128) k_sym_finish(int N, int n, int T, const d
       if (i > 0) pt[2] = fmin(pt[2], alpha);
     }
   }
-  if (MODE != EPI_STORE) block_reduce_store<NC, 128>(pt, ep.partials, MODE == EPI_GRAD ? 4u : 0u);
+  if (MODE != EPI_STORE) block_reduce_store<NC, 3 * kFinishFrames>(pt, ep.partials, MODE == EPI_GRAD ? 4u : 0u);
 }
 
 // ---------------------------------------------------------------- host side
-bool spmm_sym_supported(xm_ctx* c, int r) { return c->world == 1 && r >= 1 && r <= 6 && c->use_sym; }
+bool spmm_sym_supported(xm_ctx* c, int r) { return c->world == 1 && r >= 1 && r <= 5 && c->use_sym; }
 
-int spmm_sym_partials(xm_ctx* c) { return ceil_div(c->N, 128); }
+int spmm_sym_partials(xm_ctx* c) { return ceil_div(c->N, kFinishFrames); }
 
 template <int R, int MODE>
 static void launch_sym(xm_ctx* c, const double* V, const SpmmEpiArgs& ep) {
-  const int T = ceil_div(c->n, BT);
-  const int64_t U = (int64_t)T * (T + 1) / 2;
-  c->sym_part.alloc((size_t)U * 2 * BT * R + 64);
+  SymPlan& p = sym_plan(c);
+  const size_t rp = (size_t)p.U * BR * R, cp = (size_t)std::max(p.S, 1) * BC * R;
+  c->sym_part.alloc(rp + cp + 64);
+  double* rowpart = c->sym_part.p;
+  double* colpart = c->sym_part.p + rp;
   const size_t smem = SymCfg<R>::kSmem;
   static bool attr = false;
   if (!attr) {
     XM_CUDA(cudaFuncSetAttribute(k_spmm_sym<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  const int G = (int)std::min<int64_t>(148, U);
-  k_spmm_sym<R><<<G, kThreads, smem, c->stream>>>(c->Q.p, c->ldq, c->n, T, V, c->sym_part.p, ep.stop,
-                                                  ep.exec);
+  k_spmm_sym<R><<<p.G, kThreads, smem, c->stream>>>(c->Q.p, c->ldq, c->n, p.TRb, p.U, p.ubase.p,
+                                                    p.segbase.p, V, rowpart, colpart, ep.stop, ep.exec);
   XM_CHECK_LAUNCH();
-  k_sym_finish<R, MODE><<<ceil_div(c->N, 128), 128, 0, c->stream>>>(c->N, c->n, T, c->sym_part.p, V, ep);
+  k_sym_finish<R, MODE><<<ceil_div(c->N, kFinishFrames), 3 * kFinishFrames, 0, c->stream>>>(
+      c->N, c->n, p.ubase.p, p.segunit.p, p.colptr.p, p.colidx.p, rowpart, colpart, V, ep);
   XM_CHECK_LAUNCH();
   count_launch(c, 2);
 }
@@ -369,8 +491,7 @@ static void sym_mode(xm_ctx* c, const double* V, int r, const SpmmEpiArgs& ep) {
     case 3: launch_sym<3, MODE>(c, V, ep); break;
     case 4: launch_sym<4, MODE>(c, V, ep); break;
     case 5: launch_sym<5, MODE>(c, V, ep); break;
-    case 6: launch_sym<6, MODE>(c, V, ep); break;
-    default: throw Error(XM_EINVAL, "symmetric SpMM supports r ≤ 6");
+    default: throw Error(XM_EINVAL, "symmetric SpMM supports r ≤ 5");
   }
 }
 
