@@ -99,6 +99,12 @@ __device__ __forceinline__ void project_blk(const Blk<R>& Y, bool anchor, Blk<R>
   W = o;
 }
 
+__host__ __device__ constexpr int pow2_floor(int x) {
+  int p = 1;
+  while (p * 2 <= x) p *= 2;
+  return p;
+}
+
 // Fixed-order block reduction of NC components over a block of NT threads →
 // partials[blockIdx.x·NC + c].  min_mask bit c ⇒ component c uses min.
 template <int NC, int NT>
@@ -108,7 +114,18 @@ __device__ __forceinline__ void block_reduce_store(double (&v)[NC], double* __re
 #pragma unroll
   for (int c = 0; c < NC; ++c) sh[c][threadIdx.x] = v[c];
   __syncthreads();
-  for (int s = NT / 2; s > 0; s >>= 1) {
+  constexpr int P = pow2_floor(NT);  // largest power of two ≤ NT
+  if (P != NT) {  // fold the tail [P, NT) onto [0, NT − P)
+    if (threadIdx.x < NT - P) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        double a = sh[c][threadIdx.x], b = sh[c][threadIdx.x + P];
+        sh[c][threadIdx.x] = ((min_mask >> c) & 1u) ? fmin(a, b) : a + b;
+      }
+    }
+    __syncthreads();
+  }
+  for (int s = P / 2; s > 0; s >>= 1) {
     if (threadIdx.x < s) {
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
