@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(
 }
 
 int spmm_grid(xm_ctx* c, int r) {
-  if (spmm_sym_supported(c, r)) return ceil_div(c->N, 128);  // k_sym_finish blocks
+  if (spmm_sym_supported(c, r)) return spmm_sym_partials(c);  // k_sym_finish blocks
   int nown = std::max(1, c->f1 - c->f0);
   return std::max(1, std::min(148, nown));
 }

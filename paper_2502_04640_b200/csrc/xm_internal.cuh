@@ -239,6 +239,7 @@ struct SpmmEpiArgs {
 };
 int spmm_grid(xm_ctx* c, int r);  // number of scalar partials written by spmm()
 bool spmm_sym_supported(xm_ctx* c, int r);
+int spmm_sym_partials(xm_ctx* c);
 void spmm_sym_launch(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep);
 void spmm(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep);
 // Full product into out (n × r, replicated): this rank's rows + all-gather.
