@@ -6,13 +6,13 @@
 //         = row part (lower triangle) + column part (strictly lower triangle)
 //
 // Geometry.  Units are the lower-triangular 128-row × 256-column blocks
-// (I, J), J ≤ ⌊I/2⌋; a unit is 16 tiles of 8 rows × 256 columns (16 KB).  The
+// (I, J), J ≤ ⌊I/2⌋; a unit is 8 tiles of 16 rows × 256 columns (32 KB).  The
 // W = 16·U tiles are split stream-K style into G = 148 equal contiguous ranges
 // (one persistent CTA per SM), so every SM streams the same number of tiles.
 // A CTA's range is a sequence of *segments* (maximal runs of tiles of one
 // unit); a unit cut between two CTAs simply yields two segments.
 //
-// Per tile (warp w ↔ row w, lane ℓ ↔ the 8 columns {2ℓ+64m, 2ℓ+64m+1},
+// Per tile (warp w ↔ rows w, w+8; lane ℓ ↔ the 8 columns {2ℓ+64m, 2ℓ+64m+1},
 // m = 0..3 — conflict-free LDS.128):
 //   row part   r_i += Σ_j Q_ij V_j  with V_J for the lane's columns held in
 //              registers for the whole segment; one 5-level shuffle reduction
@@ -21,14 +21,18 @@
 //   column part c_j += Q_ij V_i (j < i), accumulated in registers over the
 //              segment's rows (V_i broadcast from shared memory), then summed
 //              over the 8 warps in a fixed order and written to colpart[segment].
-// The producer thread streams each tile with one cp.async.bulk per row (rows
-// of diagonal units only up to the diagonal; L2 evict-first) into an 8-stage
-// ring (8 × 16 KB); the per-segment V_J / V_I blocks go through a 2-slot ring.
+// The producer thread streams each tile with ONE 2-D tensor TMA copy
+// (cp.async.bulk.tensor.2d, L2 evict-first; rows / columns past n zero-filled)
+// into a 5-stage ring (5 × 32 KB); the per-segment V_J / V_I blocks go through
+// a 2-slot ring (1-D bulk copies).
 //
 // k_sym_finish (one CTA per 64 cameras) sums, in a fixed order, the row parts
 // of units (K, 0..⌊K/2⌋) and the column parts of every segment of column block
 // ⌊row/256⌋, then applies the per-camera epilogue (same modes as spmm.cu).
 // Deterministic; algorithmic bytes per product: 8·n(n+1)/2 + 16·n·r.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "frame_ops.cuh"
 
 #include <map>
@@ -40,10 +44,10 @@ constexpr int kWarps = 8;
 constexpr int kThreads = 32 * (kWarps + 1);
 constexpr int BR = 128;                 // unit rows
 constexpr int BC = 256;                 // unit columns
-constexpr int TR = 8;                   // rows per tile (one per warp)
-constexpr int kTilesPerUnit = BR / TR;  // 16
-constexpr int kStages = 8;
-constexpr int kTileBytes = TR * BC * 8;  // 16 KB
+constexpr int TR = 16;                  // rows per tile (two per warp)
+constexpr int kTilesPerUnit = BR / TR;  // 8
+constexpr int kStages = 5;
+constexpr int kTileBytes = TR * BC * 8;  // 32 KB
 constexpr int kFinishFrames = 64;
 
 __device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -81,6 +85,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(su32(b)), "l"(pol)
       : "memory");
 }
+// 2-D tensor copy of one TR × BC tile of Q (OOB rows / columns zero-filled)
+__device__ __forceinline__ void tma_tile(void* dst, const CUtensorMap* tm, int x, int y, uint64_t* b,
+                                         uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(su32(b)), "l"(pol)
+      : "memory");
+}
 // unit u → (I, J) using unit_base[I] = Σ_{I'<I} (⌊I'·BR/BC⌋ + 1)
 __device__ __forceinline__ void unit_ij(int u, const int* __restrict__ ubase, int TRb, int& I, int& J) {
   int lo = 0, hi = TRb - 1;
@@ -97,6 +110,9 @@ __device__ __forceinline__ void unit_ij(int u, const int* __restrict__ ubase, in
 // per-column-block list of segments (fixed summation order for the finish).
 struct SymPlan {
   int n = 0, G = 0, TRb = 0, TCb = 0, U = 0, S = 0;
+  const void* qptr = nullptr;  // Q the tensor map was encoded for
+  int64_t ldq = 0;
+  CUtensorMap tmq;
   DBuf<int> ubase;     // TRb + 1
   DBuf<int> segbase;   // G + 1
   DBuf<int> segunit;   // S
@@ -108,6 +124,29 @@ static SymPlan& sym_plan(xm_ctx* c) {
   static std::map<xm_ctx*, SymPlan> plans;  // one plan per context
   SymPlan& p = plans[c];
   const int n = c->n, G = 148;
+  if (p.n == n && p.G == G && p.ubase.p && p.qptr == c->Q.p && p.ldq == c->ldq) return p;
+  // Q tensor map: dims {n columns, n rows}, row pitch ldq·8 B, box TR × BC,
+  // OOB → zero fill (rows / columns ≥ n read as 0)
+  {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+      cudaDriverEntryPointQueryResult q;
+      XM_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode),
+                                      cudaEnableDefault, &q));
+      if (!encode || q != cudaDriverEntryPointSuccess)
+        throw Error(XM_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    }
+    cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)n};
+    cuuint64_t strides[1] = {(cuuint64_t)c->ldq * 8};
+    cuuint32_t box[2] = {(cuuint32_t)BC, (cuuint32_t)TR};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(&p.tmq, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, c->Q.p, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(XM_ECUDA, "cuTensorMapEncodeTiled failed");
+    p.qptr = c->Q.p;
+    p.ldq = c->ldq;
+  }
   if (p.n == n && p.G == G && p.ubase.p) return p;
   p.n = n;
   p.G = G;
@@ -169,7 +208,7 @@ struct SymCfg {
 
 template <int R>
 __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
-    const double* __restrict__ Q, int64_t ldq, int n, int TRb, int U, const int* __restrict__ ubase,
+    const __grid_constant__ CUtensorMap tmq, int n, int TRb, int U, const int* __restrict__ ubase,
     const int* __restrict__ segbase, const double* __restrict__ V, double* __restrict__ rowpart,
     double* __restrict__ colpart, const int* __restrict__ stop, int* __restrict__ exec) {
   using Cfg = SymCfg<R>;
@@ -207,13 +246,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
     // ------------------------------------------------------------ producer
     if (lane != 0) return;
     const uint64_t pq = pol_first(), pv = pol_last();
-    int it = 0, seg = 0, cur_u = -1;
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmq)) : "memory");
+    int it = 0, seg = 0, cur_u = -1, I = 0, J = 0;
     for (int64_t t = t0; t < t1; ++t, ++it) {
       const int u = (int)(t / kTilesPerUnit);
       const int tl = (int)(t % kTilesPerUnit);
-      int I, J;
-      unit_ij(u, ubase, TRb, I, J);
-      if (u != cur_u) {  // new segment: stage V_J and V_I
+      if (u != cur_u) {  // new segment: locate the unit, stage V_J and V_I
+        unit_ij(u, ubase, TRb, I, J);
         const int vs = seg & 1;
         bar_wait(&vempty[vs], (unsigned)(((seg >> 1) & 1) ^ 1));
         const int nj = min(BC, n - J * BC), ni = min(BR, n - I * BR);
@@ -228,23 +267,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
       }
       const int s = it % kStages;
       bar_wait(&empty[s], (unsigned)(((it / kStages) & 1) ^ 1));
-      const int r0 = I * BR + tl * TR;
-      const bool dblk = (J == (I * BR) / BC);  // column block holding the diagonal
-      unsigned len[TR];
-      unsigned total = 0;
-#pragma unroll
-      for (int q = 0; q < TR; ++q) {
-        const int i = r0 + q;
-        int cols = 0;
-        if (i < n) cols = dblk ? (i - J * BC + 1) : min(BC, n - J * BC);
-        len[q] = (unsigned)(((cols + 1) & ~1) * 8);
-        total += len[q];
-      }
-      bar_expect(&full[s], total);
-      double* st = tiles + (size_t)s * TR * BC;
-#pragma unroll
-      for (int q = 0; q < TR; ++q)
-        if (len[q]) bulk_g2s(st + q * BC, Q + (int64_t)(r0 + q) * ldq + (int64_t)J * BC, len[q], &full[s], pq);
+      bar_expect(&full[s], (unsigned)kTileBytes);
+      tma_tile(tiles + (size_t)s * TR * BC, &tmq, J * BC, I * BR + tl * TR, &full[s], pq);
     }
     return;
   }
@@ -310,46 +334,48 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
     }
     const int s = it % kStages;
     bar_wait(&full[s], (unsigned)((it / kStages) & 1));
-    const double* st = tiles + (size_t)s * TR * BC + warp * BC;
-    const int rl = tl * TR + warp;  // row within the unit
-    const int i = I * BR + rl;
-    if (i < n) {
-      const int jmax = dblk ? (i - J * BC) : (min(BC, n - J * BC) - 1);  // last column (row part)
-      double rs[R];
 #pragma unroll
-      for (int cc = 0; cc < R; ++cc) rs[cc] = 0.0;
-      double vrow[R];
+    for (int half = 0; half < 2; ++half) {
+      const double* st = tiles + (size_t)s * TR * BC + (warp + 8 * half) * BC;
+      const int rl = tl * TR + warp + 8 * half;  // row within the unit
+      const int i = I * BR + rl;
+      if (i < n) {
+        // row part covers j ≤ i (diagonal block) / the whole block; OOB columns are zero
+        const int jmax = dblk ? (i - J * BC) : (BC - 1);
+        double rs[R];
 #pragma unroll
-      for (int cc = 0; cc < R; ++cc) vrow[cc] = vi[rl * R + cc];
+        for (int cc = 0; cc < R; ++cc) rs[cc] = 0.0;
+        double vrow[R];
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int jl = 2 * lane + 64 * m;
-        double2 q2 = make_double2(0.0, 0.0);
-        if (jl <= jmax) q2 = *reinterpret_cast<const double2*>(st + jl);
-        const double qa = q2.x;
-        const double qb = (jl + 1 <= jmax) ? q2.y : 0.0;
-        // column part: strictly below the diagonal (j < i) — on the diagonal
-        // block drop j == i; jl + 1 > jmax already zeroed above.
-        const double ca = (dblk && jl == jmax) ? 0.0 : qa;
-        const double cb = (dblk && jl + 1 == jmax) ? 0.0 : qb;
+        for (int cc = 0; cc < R; ++cc) vrow[cc] = vi[rl * R + cc];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const int jl = 2 * lane + 64 * m;
+          const double2 q2 = *reinterpret_cast<const double2*>(st + jl);
+          const double qa = (jl <= jmax) ? q2.x : 0.0;
+          const double qb = (jl + 1 <= jmax) ? q2.y : 0.0;
+          // column part: strictly below the diagonal (j < i)
+          const double ca = (dblk && jl == jmax) ? 0.0 : qa;
+          const double cb = (dblk && jl + 1 == jmax) ? 0.0 : qb;
+#pragma unroll
+          for (int cc = 0; cc < R; ++cc) {
+            rs[cc] = fma(qa, vr[2 * m][cc], fma(qb, vr[2 * m + 1][cc], rs[cc]));
+            colacc[2 * m][cc] = fma(ca, vrow[cc], colacc[2 * m][cc]);
+            colacc[2 * m + 1][cc] = fma(cb, vrow[cc], colacc[2 * m + 1][cc]);
+          }
+        }
 #pragma unroll
         for (int cc = 0; cc < R; ++cc) {
-          rs[cc] = fma(qa, vr[2 * m][cc], fma(qb, vr[2 * m + 1][cc], rs[cc]));
-          colacc[2 * m][cc] = fma(ca, vrow[cc], colacc[2 * m][cc]);
-          colacc[2 * m + 1][cc] = fma(cb, vrow[cc], colacc[2 * m + 1][cc]);
+          double v = rs[cc];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          rs[cc] = v;
         }
-      }
+        if (lane == 0) {
+          double* pr = rowpart + ((int64_t)u * BR + rl) * R;
 #pragma unroll
-      for (int cc = 0; cc < R; ++cc) {
-        double v = rs[cc];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        rs[cc] = v;
-      }
-      if (lane == 0) {
-        double* pr = rowpart + ((int64_t)u * BR + rl) * R;
-#pragma unroll
-        for (int cc = 0; cc < R; ++cc) pr[cc] = rs[cc];
+          for (int cc = 0; cc < R; ++cc) pr[cc] = rs[cc];
+        }
       }
     }
     __syncwarp();
@@ -474,7 +500,7 @@ static void launch_sym(xm_ctx* c, const double* V, const SpmmEpiArgs& ep) {
     XM_CUDA(cudaFuncSetAttribute(k_spmm_sym<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  k_spmm_sym<R><<<p.G, kThreads, smem, c->stream>>>(c->Q.p, c->ldq, c->n, p.TRb, p.U, p.ubase.p,
+  k_spmm_sym<R><<<p.G, kThreads, smem, c->stream>>>(p.tmq, c->n, p.TRb, p.U, p.ubase.p,
                                                     p.segbase.p, V, rowpart, colpart, ep.stop, ep.exec);
   XM_CHECK_LAUNCH();
   k_sym_finish<R, MODE><<<ceil_div(c->N, kFinishFrames), 3 * kFinishFrames, 0, c->stream>>>(
