@@ -26,7 +26,7 @@
 // into a 5-stage ring (5 × 32 KB); the per-segment V_J / V_I blocks go through
 // a 2-slot ring (1-D bulk copies).
 //
-// k_sym_finish (one CTA per 64 cameras) sums, in a fixed order, the row parts
+// k_sym_finish (one CTA per 8 cameras, a warp per row) sums, in a fixed order, the row parts
 // of units (K, 0..⌊K/2⌋) and the column parts of every segment of column block
 // ⌊row/256⌋, then applies the per-camera epilogue (same modes as spmm.cu).
 // Deterministic; algorithmic bytes per product: 8·n(n+1)/2 + 16·n·r.
@@ -46,9 +46,8 @@ constexpr int BR = 128;                 // unit rows
 constexpr int BC = 256;                 // unit columns
 constexpr int TR = 16;                  // rows per tile (two per warp)
 constexpr int kTilesPerUnit = BR / TR;  // 8
-constexpr int kStages = 5;
 constexpr int kTileBytes = TR * BC * 8;  // 32 KB
-constexpr int kFinishFrames = 64;
+constexpr int kFinishFrames = 8;  // cameras per finish CTA (24 warps = 24 rows)
 
 __device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void bar_init(uint64_t* b, unsigned cnt) {
@@ -202,8 +201,9 @@ template <int R>
 struct SymCfg {
   static constexpr int kVJ = BC * R;   // doubles
   static constexpr int kVI = BR * R;
+  static constexpr int kStages = (R <= 3) ? 5 : 4;
   static constexpr size_t kSmem = (size_t)kStages * kTileBytes + 2 * (size_t)(kVJ + kVI) * 8 +
-                                  (size_t)BC * R * 8 + 64 * 8;
+                                  4 * (size_t)BC * R * 8 + 64 * 8;
 };
 
 template <int R>
@@ -212,13 +212,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
     const int* __restrict__ segbase, const double* __restrict__ V, double* __restrict__ rowpart,
     double* __restrict__ colpart, const int* __restrict__ stop, int* __restrict__ exec) {
   using Cfg = SymCfg<R>;
+  constexpr int kStages = Cfg::kStages;
   if (stop && *stop) return;
   if (exec && blockIdx.x == 0 && threadIdx.x == 0) *exec = 1;
   extern __shared__ __align__(128) unsigned char sm[];
   double* tiles = reinterpret_cast<double*>(sm);
   double* vbuf = tiles + (size_t)kStages * TR * BC;  // 2 slots × (V_J, V_I)
-  double* colred = vbuf + 2 * (Cfg::kVJ + Cfg::kVI);  // [BC][R]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(colred + BC * R);
+  double* colred = vbuf + 2 * (Cfg::kVJ + Cfg::kVI);  // [4 slots][BC][R]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(colred + 4 * BC * R);
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages;
   uint64_t* vfull = bars + 2 * kStages;
@@ -282,25 +283,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
   const double* vi = nullptr;
   int vs = 0;
   auto flush = [&](int slot_seg) {
-    // fixed-order cross-warp sum of colacc into colred, then to global
-    for (int w = 0; w < kWarps; ++w) {
-      if (warp == w) {
+    // fixed-order cross-warp sum of colacc: warps w and w+4 share slot w
+    // (w stores, w+4 adds), then slots 0..3 are summed left to right
+    double* cr = colred + (warp & 3) * BC * R;
+    if (warp < 4) {
 #pragma unroll
-        for (int m = 0; m < 4; ++m)
+      for (int m = 0; m < 4; ++m)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int jl = 2 * lane + 64 * m + h;
+        for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int cc = 0; cc < R; ++cc) {
-              double v = colacc[2 * m + h][cc];
-              colred[jl * R + cc] = (w == 0) ? v : colred[jl * R + cc] + v;
-            }
-          }
-      }
-      asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kWarps) : "memory");
+          for (int cc = 0; cc < R; ++cc) cr[(2 * lane + 64 * m + h) * R + cc] = colacc[2 * m + h][cc];
     }
+    asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kWarps) : "memory");
+    if (warp >= 4) {
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int cc = 0; cc < R; ++cc) cr[(2 * lane + 64 * m + h) * R + cc] += colacc[2 * m + h][cc];
+    }
+    asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kWarps) : "memory");
     double* dst = colpart + ((int64_t)(segbase[blockIdx.x] + slot_seg)) * BC * R;
-    for (int e = threadIdx.x; e < BC * R; e += 32 * kWarps) dst[e] = colred[e];
+    for (int e = threadIdx.x; e < BC * R; e += 32 * kWarps)
+      dst[e] = ((colred[e] + colred[BC * R + e]) + colred[2 * BC * R + e]) + colred[3 * BC * R + e];
     asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kWarps) : "memory");
   };
   for (int64_t t = t0; t < t1; ++t, ++it) {
@@ -388,37 +394,42 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
 }
 
 // ---------------------------------------------------------------- finish + epilogue
-// CTA = kFinishFrames cameras (3·64 rows): phase 1 one thread per row sums the
-// row parts (units (K, 0..⌊K/2⌋)) and the column parts of all segments of the
-// row's column block in fixed order; phase 2 one thread per camera epilogue.
+// CTA = kFinishFrames cameras.  Phase 1: warp w owns row 3·f0 + w; its lanes
+// split the row's contribution list (row parts of units (K, 0..⌊K/2⌋), then
+// the column parts of the segments of column block ⌊row/256⌋) and the lane sums
+// are combined by a fixed xor-shuffle tree.  Phase 2: one thread per camera
+// applies the epilogue.
 template <int R, int MODE>
-__global__ void __launch_bounds__(3 * kFinishFrames) k_sym_finish(
+__global__ void __launch_bounds__(96 * kFinishFrames) k_sym_finish(
     int N, int n, const int* __restrict__ ubase, const int* __restrict__ segunit,
     const int* __restrict__ colptr, const int* __restrict__ colidx, const double* __restrict__ rowpart,
     const double* __restrict__ colpart, const double* __restrict__ V, SpmmEpiArgs ep) {
   if (ep.stop && *ep.stop) return;
   __shared__ double qrow[3 * kFinishFrames][R];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int f0 = blockIdx.x * kFinishFrames;
-  const int row = 3 * f0 + threadIdx.x;
+  const int row = 3 * f0 + warp;
   if (row < n) {
+    const int K = row / BR, l = row % BR;
+    const int u0 = ubase[K], nu = ubase[K + 1] - u0;
+    const int Jc = row / BC, m = row % BC;
+    const int c0 = colptr[Jc], nc = colptr[Jc + 1] - c0;
     double acc[R];
 #pragma unroll
     for (int cc = 0; cc < R; ++cc) acc[cc] = 0.0;
-    const int K = row / BR, l = row % BR;
-    const int u0 = ubase[K], u1 = ubase[K + 1];
-    for (int u = u0; u < u1; ++u) {
-      const double* p = rowpart + ((int64_t)u * BR + l) * R;
-#pragma unroll
-      for (int cc = 0; cc < R; ++cc) acc[cc] += p[cc];
-    }
-    const int Jc = row / BC, m = row % BC;
-    for (int q = colptr[Jc]; q < colptr[Jc + 1]; ++q) {
-      const double* p = colpart + ((int64_t)colidx[q] * BC + m) * R;
+    for (int q = lane; q < nu + nc; q += 32) {
+      const double* p = (q < nu) ? rowpart + ((int64_t)(u0 + q) * BR + l) * R
+                                 : colpart + ((int64_t)colidx[c0 + q - nu] * BC + m) * R;
 #pragma unroll
       for (int cc = 0; cc < R; ++cc) acc[cc] += p[cc];
     }
 #pragma unroll
-    for (int cc = 0; cc < R; ++cc) qrow[threadIdx.x][cc] = acc[cc];
+    for (int cc = 0; cc < R; ++cc) {
+      double v = acc[cc];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) qrow[warp][cc] = v;
+    }
   }
   __syncthreads();
   constexpr int NC = (MODE == EPI_GRAD) ? 3 : (MODE == EPI_DF ? 2 : 1);
@@ -479,7 +490,7 @@ __global__ void __launch_bounds__(3 * kFinishFrames) k_sym_finish(
       if (i > 0) pt[2] = fmin(pt[2], alpha);
     }
   }
-  if (MODE != EPI_STORE) block_reduce_store<NC, 3 * kFinishFrames>(pt, ep.partials, MODE == EPI_GRAD ? 4u : 0u);
+  if (MODE != EPI_STORE) block_reduce_store<NC, 96 * kFinishFrames>(pt, ep.partials, MODE == EPI_GRAD ? 4u : 0u);
 }
 
 // ---------------------------------------------------------------- host side
@@ -503,7 +514,7 @@ static void launch_sym(xm_ctx* c, const double* V, const SpmmEpiArgs& ep) {
   k_spmm_sym<R><<<p.G, kThreads, smem, c->stream>>>(p.tmq, c->n, p.TRb, p.U, p.ubase.p,
                                                     p.segbase.p, V, rowpart, colpart, ep.stop, ep.exec);
   XM_CHECK_LAUNCH();
-  k_sym_finish<R, MODE><<<ceil_div(c->N, kFinishFrames), 3 * kFinishFrames, 0, c->stream>>>(
+  k_sym_finish<R, MODE><<<ceil_div(c->N, kFinishFrames), 96 * kFinishFrames, 0, c->stream>>>(
       c->N, c->n, p.ubase.p, p.segunit.p, p.colptr.p, p.colidx.p, rowpart, colpart, V, ep);
   XM_CHECK_LAUNCH();
   count_launch(c, 2);
