@@ -640,8 +640,10 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
   };
   phase("start");
   // stage inputs on the device
-  DBuf<int32_t> d_fr, d_lm;
-  DBuf<double> d_pts, d_w;
+  DBuf<int32_t>& d_fr = scratch_i32(c, "in_fr");
+  DBuf<int32_t>& d_lm = scratch_i32(c, "in_lm");
+  DBuf<double>& d_pts = scratch_f64(c, "in_pts");
+  DBuf<double>& d_w = scratch_f64(c, "in_w");
   const int32_t* fr = fr_in;
   const int32_t* lm = lm_in;
   const double* pts = pts_in;
@@ -654,8 +656,12 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
   c->flags.alloc(16);
   XM_CUDA(cudaMemsetAsync(c->flags.p, 0, 16 * sizeof(int), c->stream));
   // ---- H1: validate, key = (frame, landmark)
-  DBuf<uint64_t> key, key2, tk;
-  DBuf<uint32_t> val, val2, tv;
+  DBuf<uint64_t>& key = scratch_u64(c, "key");
+  DBuf<uint64_t>& key2 = scratch_u64(c, "key2");
+  DBuf<uint64_t>& tk = scratch_u64(c, "sort_tk");
+  DBuf<uint32_t>& val = scratch_u32(c, "val");
+  DBuf<uint32_t>& val2 = scratch_u32(c, "val2");
+  DBuf<uint32_t>& tv = scratch_u32(c, "sort_tv");
   key.alloc(E);
   val.alloc(E);
   k_validate<<<ceil_div(E, T), T, 0, c->stream>>>(E, N, M, fr, lm, pts, w, c->flags.p, key.p, val.p);
@@ -672,7 +678,8 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
   radix_sort_u64(c, key.p, val.p, E, bits_fl, tk, tv);
   phase("validate+sort1");
   // ---- dedupe (stable sort ⇒ the first occurrence of a key is the earliest input)
-  DBuf<int32_t> flag, pos;
+  DBuf<int32_t>& flag = scratch_i32(c, "flag");
+  DBuf<int32_t>& pos = scratch_i32(c, "pos");
   flag.alloc(E);
   pos.alloc(E);
   k_first_flags<<<ceil_div(E, T), T, 0, c->stream>>>(key.p, E, flag.p);
@@ -685,7 +692,8 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
   sync(c);
   c->stats.n_dup = E - Ek;
   c->E = Ek;
-  DBuf<int32_t> fs_in, fs_fr;
+  DBuf<int32_t>& fs_in = scratch_i32(c, "fs_in");
+  DBuf<int32_t>& fs_fr = scratch_i32(c, "fs_fr");
   fs_in.alloc(Ek);
   fs_fr.alloc(Ek);
   key2.alloc(Ek);
@@ -707,7 +715,7 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
                                                       c->fr_edge.p);
   XM_CHECK_LAUNCH();
   count_launch(c);
-  DBuf<int32_t> cnt;
+  DBuf<int32_t>& cnt = scratch_i32(c, "cnt");
   cnt.alloc((size_t)std::max(N, M) + 1);
   c->lm_off.alloc(M + 1);
   c->fr_off.alloc(N + 1);
@@ -715,7 +723,7 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
   k_histogram<<<ceil_div(Ek, T), T, 0, c->stream>>>(c->e_lm.p, Ek, cnt.p);
   XM_CHECK_LAUNCH();
   exclusive_scan_i32(c, cnt.p, c->lm_off.p, M + 1, nullptr);
-  DBuf<int32_t> fcnt;
+  DBuf<int32_t>& fcnt = scratch_i32(c, "fcnt");
   fcnt.alloc(N + 1);
   XM_CUDA(cudaMemsetAsync(fcnt.p, 0, (N + 1) * 4, c->stream));
   k_histogram<<<ceil_div(Ek, T), T, 0, c->stream>>>(fs_fr.p, Ek, fcnt.p);
@@ -730,7 +738,7 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
   phase("sort2+offsets");
   // ---- connectivity: frames ∪ observed landmarks must form one component
   {
-    DBuf<int32_t> parent;
+    DBuf<int32_t>& parent = scratch_i32(c, "cc_parent");
     parent.alloc(N + M);
     k_cc_init<<<ceil_div(N + M, T), T, 0, c->stream>>>(N + M, parent.p);
     count_launch(c);
@@ -765,13 +773,14 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
   // ---- H3: S pattern
   {
     int W32 = ceil_div(N, 32);
-    DBuf<unsigned> bits;
+    DBuf<uint32_t>& bits = scratch_u32(c, "pattern_bits");
     bits.alloc((size_t)N * W32);
     XM_CUDA(cudaMemsetAsync(bits.p, 0, (size_t)N * W32 * 4, c->stream));
     k_pattern_bits<<<N, 128, 0, c->stream>>>(N, W32, c->fr_off.p, c->fr_edge.p, c->e_lm.p,
                                              c->lm_off.p, c->e_fr.p, bits.p);
     XM_CHECK_LAUNCH();
-    DBuf<int32_t> rc, ro;
+    DBuf<int32_t>& rc = scratch_i32(c, "pattern_rc");
+    DBuf<int32_t>& ro = scratch_i32(c, "pattern_ro");
     rc.alloc(N);
     ro.alloc(N);
     k_pattern_count<<<N, 256, 0, c->stream>>>(N, W32, bits.p, rc.p);
@@ -842,7 +851,7 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
   c->have_recovery = true;
   // ‖Q‖_F (all-reduced over ranks)
   {
-    DBuf<double> part;
+    DBuf<double>& part = scratch_f64(c, "normq_part");
     part.alloc(kDotBlocks);
     k_sumsq_rows<<<kDotBlocks, 256, 0, c->stream>>>(c->Q.p, c->nrows, n, c->ldq, part.p);
     XM_CHECK_LAUNCH();

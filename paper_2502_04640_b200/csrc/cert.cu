@@ -208,7 +208,7 @@ bool lanczos(xm_ctx* c, double tol_abs, int max_steps, double* lambda, int* step
   c->tmp.alloc((size_t)c->n_alloc * 4);
   double* alphas = c->lz_c.p;                    // device α_j
   double* betas = c->lz_c.p + (kmax + 1);        // device β_j
-  DBuf<double> cbuf;
+  DBuf<double>& cbuf = scratch_f64(c, "lz_cbuf");
   cbuf.alloc(kmax + 64);
   double* dots = c->lz_part.p + (size_t)nchunk_max * n;  // kDotBlocks partials
   double* scal = c->scal.p + 48;
@@ -632,7 +632,9 @@ void round_recover_device(xm_ctx* c) {
   c->t_out.alloc((size_t)N * 3);
   c->p_out.alloc((size_t)M * 3);
   c->rhs.alloc((size_t)std::max(N, 1) * 3 + 64);
-  DBuf<double> gram, Y3, g;
+  DBuf<double>& gram = scratch_f64(c, "rnd_gram");
+  DBuf<double>& Y3 = scratch_f64(c, "rnd_Y3");
+  DBuf<double>& g = scratch_f64(c, "rnd_g");
   gram.alloc((size_t)r * r);
   Y3.alloc((size_t)n * 3);
   g.alloc(16);
@@ -647,7 +649,7 @@ void round_recover_device(xm_ctx* c) {
   std::vector<double> W3(r * 3);
   for (int p = 0; p < r; ++p)
     for (int q = 0; q < 3; ++q) W3[p * 3 + q] = V[p * r + q];
-  DBuf<double> dW3;
+  DBuf<double>& dW3 = scratch_f64(c, "rnd_W3");
   dW3.alloc(r * 3);
   XM_CUDA(cudaMemcpyAsync(dW3.p, W3.data(), r * 3 * 8, cudaMemcpyHostToDevice, c->stream));
   k_y_times_w3<<<ceil_div(n, 256), 256, 0, c->stream>>>(n, r, c->Y.p, dW3.p, Y3.p);

@@ -133,7 +133,7 @@ __global__ void k_scan_total(const int32_t* in, const int32_t* out, int64_t n, i
   if (threadIdx.x == 0 && blockIdx.x == 0) *total = (n > 0) ? out[n - 1] + in[n - 1] : 0;
 }
 
-static void scan_rec(xm_ctx* c, const int32_t* in, int32_t* out, int64_t n) {
+static void scan_rec(xm_ctx* c, const int32_t* in, int32_t* out, int64_t n, int level = 0) {
   int nb = ceil_div(n, kScanTile);
   if (nb <= 1) {
     k_scan_tile<<<1, kScanThreads, 0, c->stream>>>(in, out, n, nullptr);
@@ -141,22 +141,22 @@ static void scan_rec(xm_ctx* c, const int32_t* in, int32_t* out, int64_t n) {
     count_launch(c);
     return;
   }
-  DBuf<int32_t> sums, offs;
+  DBuf<int32_t>& sums = scratch_i32(c, "scan_sums" + std::to_string(level));
+  DBuf<int32_t>& offs = scratch_i32(c, "scan_offs" + std::to_string(level));
   sums.alloc(nb);
   offs.alloc(nb);
   k_scan_tile<<<nb, kScanThreads, 0, c->stream>>>(in, out, n, sums.p);
   XM_CHECK_LAUNCH();
-  scan_rec(c, sums.p, offs.p, nb);
+  scan_rec(c, sums.p, offs.p, nb, level + 1);
   k_scan_add<<<nb, kScanThreads, 0, c->stream>>>(out, n, offs.p);
   XM_CHECK_LAUNCH();
   count_launch(c, 2);
-  XM_CUDA(cudaStreamSynchronize(c->stream));  // temporaries freed on return
 }
 
 void exclusive_scan_i32(xm_ctx* c, const int32_t* in, int32_t* out, int64_t n, int32_t* total_dev) {
   if (n <= 0) return;
   if (in == out) {
-    DBuf<int32_t> tmp;
+    DBuf<int32_t>& tmp = scratch_i32(c, "scan_inplace");
     tmp.alloc(n);
     XM_CUDA(cudaMemcpyAsync(tmp.p, in, n * 4, cudaMemcpyDeviceToDevice, c->stream));
     scan_rec(c, tmp.p, out, n);
@@ -243,7 +243,8 @@ void radix_sort_u64(xm_ctx* c, uint64_t* keys, uint32_t* vals, int64_t n, int bi
   int ntiles = ceil_div(n, kSortTile);
   tmp_k.alloc(n);
   tmp_v.alloc(n);
-  DBuf<int32_t> hist, offs;
+  DBuf<int32_t>& hist = scratch_i32(c, "radix_hist");
+  DBuf<int32_t>& offs = scratch_i32(c, "radix_offs");
   hist.alloc((size_t)256 * ntiles);
   offs.alloc((size_t)256 * ntiles);
   uint64_t *ka = keys, *kb = tmp_k.p;

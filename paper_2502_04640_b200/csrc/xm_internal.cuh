@@ -8,6 +8,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <map>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -185,6 +186,12 @@ struct xm_ctx {
   bool use_graphs = true;
   bool use_sym = true;             // symmetric (lower-triangle) SpMM on one GPU, r ≤ 6
   xm::DBuf<double> sym_part;       // per-unit row / column partials of the symmetric SpMM
+  // named scratch buffers that persist across calls (grow-only): no cudaMalloc /
+  // cudaFree churn (each cudaFree synchronises the device) inside build / solve
+  std::map<std::string, xm::DBuf<int32_t>> s_i32;
+  std::map<std::string, xm::DBuf<uint32_t>> s_u32;
+  std::map<std::string, xm::DBuf<uint64_t>> s_u64;
+  std::map<std::string, xm::DBuf<double>> s_f64;
   std::string last_error;
 };
 
@@ -199,6 +206,12 @@ void copy_in(xm_ctx* c, void* dst_dev, const void* src, size_t bytes);
 void copy_out(xm_ctx* c, void* dst, const void* src_dev, size_t bytes);
 void sync(xm_ctx* c);
 inline void count_launch(xm_ctx* c, int k = 1) { c->stats.kernel_launches += k; }
+
+// Persistent named scratch (see xm_ctx::s_*).
+inline DBuf<int32_t>& scratch_i32(xm_ctx* c, const std::string& k) { return c->s_i32[k]; }
+inline DBuf<uint32_t>& scratch_u32(xm_ctx* c, const std::string& k) { return c->s_u32[k]; }
+inline DBuf<uint64_t>& scratch_u64(xm_ctx* c, const std::string& k) { return c->s_u64[k]; }
+inline DBuf<double>& scratch_f64(xm_ctx* c, const std::string& k) { return c->s_f64[k]; }
 
 // ------------------------------------------------------------ util kernels (util.cu)
 // Deterministic reductions: blocks write partials, one block reduces in fixed order.
