@@ -26,9 +26,9 @@
 // into a 5-stage ring (5 × 32 KB); the per-segment V_J / V_I blocks go through
 // a 2-slot ring (1-D bulk copies).
 //
-// k_sym_finish (one CTA per 8 cameras, a warp per row) sums, in a fixed order, the row parts
-// of units (K, 0..⌊K/2⌋) and the column parts of every segment of column block
-// ⌊row/256⌋, then applies the per-camera epilogue (same modes as spmm.cu).
+// After a software grid barrier the same CTAs sum, in a fixed order, the row
+// parts of units (K, 0..⌊K/2⌋) and the column parts of every segment of column
+// block ⌊row/256⌋, and apply the per-camera epilogue (same modes as spmm.cu).
 // Deterministic; algorithmic bytes per product: 8·n(n+1)/2 + 16·n·r.
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -36,6 +36,7 @@
 #include "frame_ops.cuh"
 
 #include <map>
+#include <type_traits>
 
 namespace xm {
 
@@ -47,7 +48,6 @@ constexpr int BC = 256;                 // unit columns
 constexpr int TR = 16;                  // rows per tile (two per warp)
 constexpr int kTilesPerUnit = BR / TR;  // 8
 constexpr int kTileBytes = TR * BC * 8;  // 32 KB
-constexpr int kFinishFrames = 8;  // cameras per finish CTA (24 warps = 24 rows)
 
 __device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void bar_init(uint64_t* b, unsigned cnt) {
@@ -122,7 +122,9 @@ struct SymPlan {
 static SymPlan& sym_plan(xm_ctx* c) {
   static std::map<xm_ctx*, SymPlan> plans;  // one plan per context
   SymPlan& p = plans[c];
-  const int n = c->n, G = 148;
+  int sms = 148;
+  XM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+  const int n = c->n, G = std::min(148, sms);
   if (p.n == n && p.G == G && p.ubase.p && p.qptr == c->Q.p && p.ldq == c->ldq) return p;
   // Q tensor map: dims {n columns, n rows}, row pitch ldq·8 B, box TR × BC,
   // OOB → zero fill (rows / columns ≥ n read as 0)
@@ -206,15 +208,41 @@ struct SymCfg {
                                   4 * (size_t)BC * R * 8 + 64 * 8;
 };
 
-template <int R>
+// Sense-reversing software grid barrier.  Valid because the G CTAs of
+// k_spmm_sym are all co-resident (one per SM, G ≤ #SMs, checked on the host)
+// and the library issues its kernels on a single stream.
+struct GridBar {
+  int count;
+  int sense;
+};
+__device__ __forceinline__ void grid_barrier(GridBar* gb, int G) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile int* vs = &gb->sense;
+    const int s = *vs;
+    __threadfence();
+    if (atomicAdd(&gb->count, 1) == G - 1) {
+      gb->count = 0;
+      __threadfence();
+      atomicExch(&gb->sense, s ^ 1);
+    } else {
+      while (*vs == s) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <int R, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
-    const __grid_constant__ CUtensorMap tmq, int n, int TRb, int U, const int* __restrict__ ubase,
-    const int* __restrict__ segbase, const double* __restrict__ V, double* __restrict__ rowpart,
-    double* __restrict__ colpart, const int* __restrict__ stop, int* __restrict__ exec) {
+    const __grid_constant__ CUtensorMap tmq, int N, int n, int TRb, int U,
+    const int* __restrict__ ubase, const int* __restrict__ segbase, const int* __restrict__ colptr,
+    const int* __restrict__ colidx, const double* __restrict__ V, double* __restrict__ rowpart,
+    double* __restrict__ colpart, GridBar* __restrict__ gbar, SpmmEpiArgs ep) {
   using Cfg = SymCfg<R>;
   constexpr int kStages = Cfg::kStages;
-  if (stop && *stop) return;
-  if (exec && blockIdx.x == 0 && threadIdx.x == 0) *exec = 1;
+  if (ep.stop && *ep.stop) return;
+  if (ep.exec && blockIdx.x == 0 && threadIdx.x == 0) *ep.exec = 1;
   extern __shared__ __align__(128) unsigned char sm[];
   double* tiles = reinterpret_cast<double*>(sm);
   double* vbuf = tiles + (size_t)kStages * TR * BC;  // 2 slots × (V_J, V_I)
@@ -225,9 +253,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
   uint64_t* vfull = bars + 2 * kStages;
   uint64_t* vempty = vfull + 2;
 
+  const int G = gridDim.x;
   const int64_t W = (int64_t)U * kTilesPerUnit;
-  const int64_t t0 = (int64_t)blockIdx.x * W / gridDim.x;
-  const int64_t t1 = (int64_t)(blockIdx.x + 1) * W / gridDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * W / G;
+  const int64_t t1 = (int64_t)(blockIdx.x + 1) * W / G;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -241,175 +270,172 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  if (t0 >= t1) return;
 
   if (warp == kWarps) {
     // ------------------------------------------------------------ producer
-    if (lane != 0) return;
-    const uint64_t pq = pol_first(), pv = pol_last();
-    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmq)) : "memory");
-    int it = 0, seg = 0, cur_u = -1, I = 0, J = 0;
+    if (lane == 0 && t0 < t1) {
+      const uint64_t pq = pol_first(), pv = pol_last();
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmq)) : "memory");
+      int it = 0, seg = 0, cur_u = -1, I = 0, J = 0;
+      for (int64_t t = t0; t < t1; ++t, ++it) {
+        const int u = (int)(t / kTilesPerUnit);
+        const int tl = (int)(t % kTilesPerUnit);
+        if (u != cur_u) {  // new segment: locate the unit, stage V_J and V_I
+          unit_ij(u, ubase, TRb, I, J);
+          const int vs = seg & 1;
+          bar_wait(&vempty[vs], (unsigned)(((seg >> 1) & 1) ^ 1));
+          const int nj = min(BC, n - J * BC), ni = min(BR, n - I * BR);
+          const unsigned bj = (unsigned)(((nj * R + 1) & ~1) * 8);
+          const unsigned bi = (unsigned)(((ni * R + 1) & ~1) * 8);
+          bar_expect(&vfull[vs], bj + bi);
+          double* vj = vbuf + (size_t)vs * (Cfg::kVJ + Cfg::kVI);
+          bulk_g2s(vj, V + (int64_t)J * BC * R, bj, &vfull[vs], pv);
+          bulk_g2s(vj + Cfg::kVJ, V + (int64_t)I * BR * R, bi, &vfull[vs], pv);
+          cur_u = u;
+          ++seg;
+        }
+        const int s = it % kStages;
+        bar_wait(&empty[s], (unsigned)(((it / kStages) & 1) ^ 1));
+        bar_expect(&full[s], (unsigned)kTileBytes);
+        tma_tile(tiles + (size_t)s * TR * BC, &tmq, J * BC, I * BR + tl * TR, &full[s], pq);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ consumers
+    int it = 0, seg = 0, cur_u = -1;
+    int I = 0, J = 0;
+    bool dblk = false;
+    double vr[8][R];      // V_J rows for the lane's 8 columns
+    double colacc[8][R];  // column partials for the lane's 8 columns
+    const double* vi = nullptr;
+    int vs = 0;
+    auto flush = [&](int slot_seg) {
+      // fixed-order cross-warp sum of colacc: warps w and w+4 share slot w
+      // (w stores, w+4 adds), then slots 0..3 are summed left to right
+      double* cr = colred + (warp & 3) * BC * R;
+      if (warp < 4) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int cc = 0; cc < R; ++cc) cr[(2 * lane + 64 * m + h) * R + cc] = colacc[2 * m + h][cc];
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kWarps) : "memory");
+      if (warp >= 4) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int cc = 0; cc < R; ++cc) cr[(2 * lane + 64 * m + h) * R + cc] += colacc[2 * m + h][cc];
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kWarps) : "memory");
+      double* dst = colpart + ((int64_t)(segbase[blockIdx.x] + slot_seg)) * BC * R;
+      for (int e = threadIdx.x; e < BC * R; e += 32 * kWarps)
+        dst[e] = ((colred[e] + colred[BC * R + e]) + colred[2 * BC * R + e]) + colred[3 * BC * R + e];
+      asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kWarps) : "memory");
+    };
+    // one row of a tile: row part (j ≤ jmax) and column part (j < i)
+    auto do_row = [&](auto diag_tag, const double* st, int rl, int i, int64_t u) {
+      constexpr bool DIAG = decltype(diag_tag)::value;
+      double rs[R];
+#pragma unroll
+      for (int cc = 0; cc < R; ++cc) rs[cc] = 0.0;
+      double vrow[R];
+#pragma unroll
+      for (int cc = 0; cc < R; ++cc) vrow[cc] = vi[rl * R + cc];
+      const int jmax = i - J * BC;  // diagonal column (DIAG only)
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int jl = 2 * lane + 64 * m;
+        const double2 q2 = *reinterpret_cast<const double2*>(st + jl);
+        double qa = q2.x, qb = q2.y, ca = qa, cb = qb;
+        if (DIAG) {  // row part j ≤ i, column part j < i; beyond: zero
+          qa = (jl <= jmax) ? qa : 0.0;
+          qb = (jl + 1 <= jmax) ? qb : 0.0;
+          ca = (jl < jmax) ? q2.x : 0.0;
+          cb = (jl + 1 < jmax) ? q2.y : 0.0;
+        }
+#pragma unroll
+        for (int cc = 0; cc < R; ++cc) {
+          rs[cc] = fma(qa, vr[2 * m][cc], fma(qb, vr[2 * m + 1][cc], rs[cc]));
+          colacc[2 * m][cc] = fma(ca, vrow[cc], colacc[2 * m][cc]);
+          colacc[2 * m + 1][cc] = fma(cb, vrow[cc], colacc[2 * m + 1][cc]);
+        }
+      }
+#pragma unroll
+      for (int cc = 0; cc < R; ++cc) {
+        double v = rs[cc];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        rs[cc] = v;
+      }
+      if (lane == 0) {
+        double* pr = rowpart + (u * BR + rl) * R;
+#pragma unroll
+        for (int cc = 0; cc < R; ++cc) pr[cc] = rs[cc];
+      }
+    };
     for (int64_t t = t0; t < t1; ++t, ++it) {
       const int u = (int)(t / kTilesPerUnit);
       const int tl = (int)(t % kTilesPerUnit);
-      if (u != cur_u) {  // new segment: locate the unit, stage V_J and V_I
+      if (u != cur_u) {
+        if (cur_u >= 0) {
+          if (lane == 0) bar_arrive(&vempty[vs]);
+          flush(seg - 1);
+        }
         unit_ij(u, ubase, TRb, I, J);
-        const int vs = seg & 1;
-        bar_wait(&vempty[vs], (unsigned)(((seg >> 1) & 1) ^ 1));
-        const int nj = min(BC, n - J * BC), ni = min(BR, n - I * BR);
-        const unsigned bj = (unsigned)(((nj * R + 1) & ~1) * 8);
-        const unsigned bi = (unsigned)(((ni * R + 1) & ~1) * 8);
-        bar_expect(&vfull[vs], bj + bi);
-        double* vj = vbuf + (size_t)vs * (Cfg::kVJ + Cfg::kVI);
-        bulk_g2s(vj, V + (int64_t)J * BC * R, bj, &vfull[vs], pv);
-        bulk_g2s(vj + Cfg::kVJ, V + (int64_t)I * BR * R, bi, &vfull[vs], pv);
+        dblk = (J == (I * BR) / BC);
+        vs = seg & 1;
+        bar_wait(&vfull[vs], (unsigned)((seg >> 1) & 1));
+        const double* vj = vbuf + (size_t)vs * (Cfg::kVJ + Cfg::kVI);
+        vi = vj + Cfg::kVJ;
+        const int nj = min(BC, n - J * BC);
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int jl = 2 * lane + 64 * m + h;
+#pragma unroll
+            for (int cc = 0; cc < R; ++cc) {
+              vr[2 * m + h][cc] = (jl < nj) ? vj[jl * R + cc] : 0.0;
+              colacc[2 * m + h][cc] = 0.0;
+            }
+          }
         cur_u = u;
         ++seg;
       }
       const int s = it % kStages;
-      bar_wait(&empty[s], (unsigned)(((it / kStages) & 1) ^ 1));
-      bar_expect(&full[s], (unsigned)kTileBytes);
-      tma_tile(tiles + (size_t)s * TR * BC, &tmq, J * BC, I * BR + tl * TR, &full[s], pq);
-    }
-    return;
-  }
-
-  // ------------------------------------------------------------ consumers
-  int it = 0, seg = 0, cur_u = -1;
-  int I = 0, J = 0;
-  bool dblk = false;
-  double vr[8][R];      // V_J rows for the lane's 8 columns
-  double colacc[8][R];  // column partials for the lane's 8 columns
-  const double* vi = nullptr;
-  int vs = 0;
-  auto flush = [&](int slot_seg) {
-    // fixed-order cross-warp sum of colacc: warps w and w+4 share slot w
-    // (w stores, w+4 adds), then slots 0..3 are summed left to right
-    double* cr = colred + (warp & 3) * BC * R;
-    if (warp < 4) {
+      bar_wait(&full[s], (unsigned)((it / kStages) & 1));
 #pragma unroll
-      for (int m = 0; m < 4; ++m)
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int cc = 0; cc < R; ++cc) cr[(2 * lane + 64 * m + h) * R + cc] = colacc[2 * m + h][cc];
-    }
-    asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kWarps) : "memory");
-    if (warp >= 4) {
-#pragma unroll
-      for (int m = 0; m < 4; ++m)
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int cc = 0; cc < R; ++cc) cr[(2 * lane + 64 * m + h) * R + cc] += colacc[2 * m + h][cc];
-    }
-    asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kWarps) : "memory");
-    double* dst = colpart + ((int64_t)(segbase[blockIdx.x] + slot_seg)) * BC * R;
-    for (int e = threadIdx.x; e < BC * R; e += 32 * kWarps)
-      dst[e] = ((colred[e] + colred[BC * R + e]) + colred[2 * BC * R + e]) + colred[3 * BC * R + e];
-    asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kWarps) : "memory");
-  };
-  for (int64_t t = t0; t < t1; ++t, ++it) {
-    const int u = (int)(t / kTilesPerUnit);
-    const int tl = (int)(t % kTilesPerUnit);
-    if (u != cur_u) {
-      if (cur_u >= 0) {
-        if (lane == 0) bar_arrive(&vempty[vs]);
-        flush(seg - 1);
-      }
-      unit_ij(u, ubase, TRb, I, J);
-      dblk = (J == (I * BR) / BC);
-      vs = seg & 1;
-      bar_wait(&vfull[vs], (unsigned)((seg >> 1) & 1));
-      const double* vj = vbuf + (size_t)vs * (Cfg::kVJ + Cfg::kVI);
-      vi = vj + Cfg::kVJ;
-      const int nj = min(BC, n - J * BC);
-#pragma unroll
-      for (int m = 0; m < 4; ++m)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int jl = 2 * lane + 64 * m + h;
-#pragma unroll
-          for (int cc = 0; cc < R; ++cc) {
-            vr[2 * m + h][cc] = (jl < nj) ? vj[jl * R + cc] : 0.0;
-            colacc[2 * m + h][cc] = 0.0;
-          }
-        }
-      cur_u = u;
-      ++seg;
-    }
-    const int s = it % kStages;
-    bar_wait(&full[s], (unsigned)((it / kStages) & 1));
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      const double* st = tiles + (size_t)s * TR * BC + (warp + 8 * half) * BC;
-      const int rl = tl * TR + warp + 8 * half;  // row within the unit
-      const int i = I * BR + rl;
-      if (i < n) {
-        // row part covers j ≤ i (diagonal block) / the whole block; OOB columns are zero
-        const int jmax = dblk ? (i - J * BC) : (BC - 1);
-        double rs[R];
-#pragma unroll
-        for (int cc = 0; cc < R; ++cc) rs[cc] = 0.0;
-        double vrow[R];
-#pragma unroll
-        for (int cc = 0; cc < R; ++cc) vrow[cc] = vi[rl * R + cc];
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          const int jl = 2 * lane + 64 * m;
-          const double2 q2 = *reinterpret_cast<const double2*>(st + jl);
-          const double qa = (jl <= jmax) ? q2.x : 0.0;
-          const double qb = (jl + 1 <= jmax) ? q2.y : 0.0;
-          // column part: strictly below the diagonal (j < i)
-          const double ca = (dblk && jl == jmax) ? 0.0 : qa;
-          const double cb = (dblk && jl + 1 == jmax) ? 0.0 : qb;
-#pragma unroll
-          for (int cc = 0; cc < R; ++cc) {
-            rs[cc] = fma(qa, vr[2 * m][cc], fma(qb, vr[2 * m + 1][cc], rs[cc]));
-            colacc[2 * m][cc] = fma(ca, vrow[cc], colacc[2 * m][cc]);
-            colacc[2 * m + 1][cc] = fma(cb, vrow[cc], colacc[2 * m + 1][cc]);
-          }
-        }
-#pragma unroll
-        for (int cc = 0; cc < R; ++cc) {
-          double v = rs[cc];
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-          rs[cc] = v;
-        }
-        if (lane == 0) {
-          double* pr = rowpart + ((int64_t)u * BR + rl) * R;
-#pragma unroll
-          for (int cc = 0; cc < R; ++cc) pr[cc] = rs[cc];
+      for (int half = 0; half < 2; ++half) {
+        const double* st = tiles + (size_t)s * TR * BC + (warp + 8 * half) * BC;
+        const int rl = tl * TR + warp + 8 * half;  // row within the unit
+        const int i = I * BR + rl;
+        if (i < n) {
+          if (dblk) do_row(std::true_type{}, st, rl, i, (int64_t)u);
+          else do_row(std::false_type{}, st, rl, i, (int64_t)u);
         }
       }
+      __syncwarp();
+      if (lane == 0) bar_arrive(&empty[s]);
     }
-    __syncwarp();
-    if (lane == 0) bar_arrive(&empty[s]);
+    if (cur_u >= 0) {
+      if (lane == 0) bar_arrive(&vempty[vs]);
+      flush(seg - 1);
+    }
   }
-  if (cur_u >= 0) {
-    if (lane == 0) bar_arrive(&vempty[vs]);
-    flush(seg - 1);
-  }
-}
 
-// ---------------------------------------------------------------- finish + epilogue
-// CTA = kFinishFrames cameras.  Phase 1: warp w owns row 3·f0 + w; its lanes
-// split the row's contribution list (row parts of units (K, 0..⌊K/2⌋), then
-// the column parts of the segments of column block ⌊row/256⌋) and the lane sums
-// are combined by a fixed xor-shuffle tree.  Phase 2: one thread per camera
-// applies the epilogue.
-template <int R, int MODE>
-__global__ void __launch_bounds__(96 * kFinishFrames) k_sym_finish(
-    int N, int n, const int* __restrict__ ubase, const int* __restrict__ segunit,
-    const int* __restrict__ colptr, const int* __restrict__ colidx, const double* __restrict__ rowpart,
-    const double* __restrict__ colpart, const double* __restrict__ V, SpmmEpiArgs ep) {
-  if (ep.stop && *ep.stop) return;
-  __shared__ double qrow[3 * kFinishFrames][R];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int f0 = blockIdx.x * kFinishFrames;
-  const int row = 3 * f0 + warp;
-  if (row < n) {
+  // ------------------------------------------------------------ finish (fused)
+  // All row / column partials are published; CTA c now sums the partial lists
+  // of the rows of frames [c·N/G, (c+1)·N/G) (warp per row, lanes split the
+  // list, fixed xor-shuffle tree) and applies the per-camera epilogue.
+  grid_barrier(gbar, G);
+  const int fa = (int)((int64_t)blockIdx.x * N / G), fb = (int)((int64_t)(blockIdx.x + 1) * N / G);
+  double* qrow = tiles;  // pipeline smem is free now: [rows][R]
+  for (int rr = warp; rr < 3 * (fb - fa); rr += kWarps + 1) {
+    const int row = 3 * fa + rr;
     const int K = row / BR, l = row % BR;
     const int u0 = ubase[K], nu = ubase[K + 1] - u0;
     const int Jc = row / BC, m = row % BC;
@@ -428,7 +454,7 @@ __global__ void __launch_bounds__(96 * kFinishFrames) k_sym_finish(
       double v = acc[cc];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) qrow[warp][cc] = v;
+      if (lane == 0) qrow[rr * R + cc] = v;
     }
   }
   __syncthreads();
@@ -436,14 +462,13 @@ __global__ void __launch_bounds__(96 * kFinishFrames) k_sym_finish(
   double pt[NC];
 #pragma unroll
   for (int q = 0; q < NC; ++q) pt[q] = (MODE == EPI_GRAD && q == 2) ? 1.0e300 : 0.0;
-  const int lf = threadIdx.x;
-  const int i = f0 + lf;
-  if (lf < kFinishFrames && i < N) {
+  for (int lf = threadIdx.x; lf < fb - fa; lf += kThreads) {
+    const int i = fa + lf;
     Blk<R> qv;
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
-      for (int cc = 0; cc < R; ++cc) qv.v[a][cc] = qrow[3 * lf + a][cc];
+      for (int cc = 0; cc < R; ++cc) qv.v[a][cc] = qrow[(3 * lf + a) * R + cc];
     if (MODE == EPI_STORE) {
       store_blk<R>(ep.out, i, qv);
     } else if (MODE == EPI_HVP) {
@@ -490,13 +515,13 @@ __global__ void __launch_bounds__(96 * kFinishFrames) k_sym_finish(
       if (i > 0) pt[2] = fmin(pt[2], alpha);
     }
   }
-  if (MODE != EPI_STORE) block_reduce_store<NC, 96 * kFinishFrames>(pt, ep.partials, MODE == EPI_GRAD ? 4u : 0u);
+  if (MODE != EPI_STORE) block_reduce_store<NC, kThreads>(pt, ep.partials, MODE == EPI_GRAD ? 4u : 0u);
 }
 
 // ---------------------------------------------------------------- host side
 bool spmm_sym_supported(xm_ctx* c, int r) { return c->world == 1 && r >= 1 && r <= 5 && c->use_sym; }
 
-int spmm_sym_partials(xm_ctx* c) { return ceil_div(c->N, kFinishFrames); }
+int spmm_sym_partials(xm_ctx* c) { return sym_plan(c).G; }
 
 template <int R, int MODE>
 static void launch_sym(xm_ctx* c, const double* V, const SpmmEpiArgs& ep) {
@@ -505,19 +530,25 @@ static void launch_sym(xm_ctx* c, const double* V, const SpmmEpiArgs& ep) {
   c->sym_part.alloc(rp + cp + 64);
   double* rowpart = c->sym_part.p;
   double* colpart = c->sym_part.p + rp;
+  if (!c->gbar.p) {
+    c->gbar.alloc(4);
+    XM_CUDA(cudaMemset(c->gbar.p, 0, 4 * sizeof(int)));
+  }
   const size_t smem = SymCfg<R>::kSmem;
   static bool attr = false;
   if (!attr) {
-    XM_CUDA(cudaFuncSetAttribute(k_spmm_sym<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    XM_CUDA(cudaFuncSetAttribute(k_spmm_sym<R, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    int nb = 0;
+    XM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_spmm_sym<R, MODE>, kThreads, smem));
+    if (nb < 1) throw Error(XM_ECUDA, "symmetric SpMM does not fit on an SM");
     attr = true;
   }
-  k_spmm_sym<R><<<p.G, kThreads, smem, c->stream>>>(p.tmq, c->n, p.TRb, p.U, p.ubase.p,
-                                                    p.segbase.p, V, rowpart, colpart, ep.stop, ep.exec);
+  k_spmm_sym<R, MODE><<<p.G, kThreads, smem, c->stream>>>(
+      p.tmq, c->N, c->n, p.TRb, p.U, p.ubase.p, p.segbase.p, p.colptr.p, p.colidx.p, V, rowpart,
+      colpart, reinterpret_cast<GridBar*>(c->gbar.p), ep);
   XM_CHECK_LAUNCH();
-  k_sym_finish<R, MODE><<<ceil_div(c->N, kFinishFrames), 96 * kFinishFrames, 0, c->stream>>>(
-      c->N, c->n, p.ubase.p, p.segunit.p, p.colptr.p, p.colidx.p, rowpart, colpart, V, ep);
-  XM_CHECK_LAUNCH();
-  count_launch(c, 2);
+  count_launch(c, 1);
 }
 
 template <int MODE>

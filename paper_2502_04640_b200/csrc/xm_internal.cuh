@@ -186,6 +186,7 @@ struct xm_ctx {
   bool use_graphs = true;
   bool use_sym = true;             // symmetric (lower-triangle) SpMM on one GPU, r ≤ 6
   xm::DBuf<double> sym_part;       // per-unit row / column partials of the symmetric SpMM
+  xm::DBuf<int> gbar;              // software grid-barrier state of the symmetric SpMM
   // named scratch buffers that persist across calls (grow-only): no cudaMalloc /
   // cudaFree churn (each cudaFree synchronises the device) inside build / solve
   std::map<std::string, xm::DBuf<int32_t>> s_i32;
