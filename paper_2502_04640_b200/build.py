@@ -19,6 +19,8 @@ SOURCES = ["util.cu", "assembly.cu", "spmm.cu", "spmm_sym.cu", "manifold.cu", "c
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include")]
+# experiments only (kernel A/B switches such as -DXM_EXP_NOCOMPUTE); empty by default
+FLAGS += os.environ.get("XM_NVCC_EXTRA", "").split()
 
 
 def nvcc() -> str:

@@ -413,10 +413,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
         const double* st = tiles + (size_t)s * TR * BC + (warp + 8 * half) * BC;
         const int rl = tl * TR + warp + 8 * half;  // row within the unit
         const int i = I * BR + rl;
+#ifndef XM_EXP_NOCOMPUTE
         if (i < n) {
           if (dblk) do_row(std::true_type{}, st, rl, i, (int64_t)u);
           else do_row(std::false_type{}, st, rl, i, (int64_t)u);
         }
+#else
+        (void)st; (void)i;
+#endif
       }
       __syncwarp();
       if (lane == 0) bar_arrive(&empty[s]);
@@ -431,6 +435,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
   // All row / column partials are published; CTA c now sums the partial lists
   // of the rows of frames [c·N/G, (c+1)·N/G) (warp per row, lanes split the
   // list, fixed xor-shuffle tree) and applies the per-camera epilogue.
+#ifdef XM_EXP_NOFINISH
+  return;
+#endif
   grid_barrier(gbar, G);
   const int fa = (int)((int64_t)blockIdx.x * N / G), fb = (int)((int64_t)(blockIdx.x + 1) * N / G);
   double* qrow = tiles;  // pipeline smem is free now: [rows][R]
