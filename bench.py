@@ -150,7 +150,7 @@ def oracle_sample(scene, hvps: int, lanczos_steps: int, spmms: int, n_hvp_sample
 
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
+    _, rank, _ = dist_env()
     if rank != 0:
         return 0
     from synth.scenes import CONFIG_DESCRIPTIONS, config_scene
@@ -180,6 +180,30 @@ def run_reference(args):
     return 0
 
 
+# ----------------------------------------------------------------------------- multi-rank plumbing
+def dist_env():
+    """(world, rank, local_rank) from the torchrun environment."""
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def share_id(dist, rank: int, make):
+    """Rank 0 calls make() (the 128-byte ncclUniqueId); every rank returns it."""
+    obj = [make() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def max_over_ranks(dist, x: float, device) -> float:
+    """Device-timed numbers are reported as the max over ranks."""
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 # ----------------------------------------------------------------------------- xm arm
 def main():
     ap = argparse.ArgumentParser()
@@ -202,18 +226,14 @@ def main():
     from paper_2502_04640_b200 import xm
     from synth.scenes import CONFIG_DESCRIPTIONS, config_scene
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    world, rank, local = dist_env()
     torch.cuda.set_device(local)
     dist = None
     nccl_id = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        obj = [xm.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        nccl_id = share_id(dist, rank, xm.nccl_unique_id)
 
     sc = config_scene(args.config, seed=args.seed)
     dev = torch.device("cuda", local)
@@ -257,12 +277,8 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
-    ms = e0.elapsed_time(e1) / args.steps
+    ms = max_over_ranks(dist, e0.elapsed_time(e1) / args.steps, dev)
     stats = ctx.stats()
-    if dist is not None:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
 
     # ---- end to end through the public API with pinned host buffers
     e2e = None
@@ -277,11 +293,7 @@ def main():
             step(h_in, out_host)
         torch.cuda.synchronize()
         barrier()
-        e2e_s = (time.perf_counter() - t0) / args.steps
-        if dist is not None:
-            t = torch.tensor([e2e_s], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t.item())
+        e2e_s = max_over_ranks(dist, (time.perf_counter() - t0) / args.steps, dev)
         e2e = {"value": e2e_s, "unit": "s",
                "h2d_bytes_per_step": int(sum(a.numel() * a.element_size() for a in h_in)),
                "d2h_bytes_per_step": int(sum(v.numel() * 8 for v in out_host.values()))}

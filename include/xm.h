@@ -93,6 +93,9 @@ typedef struct {
   int32_t cert_cholesky;  /* 1: if Lanczos has not converged within n/72 steps,  */
                           /* test Z + εI ⪰ 0 by dense Cholesky (ε = cert_tol·   */
                           /* max(1,‖Q‖_F); Alg. 1); single GPU     [1]  */
+  int32_t spmm_kernel;    /* Q·V kernel: 0 auto by (N, r); 1 full-row stream;  */
+                          /* 2 lower-triangle (symmetric) stream — one GPU and */
+                          /* r ≤ 5 only, else falls back to 1 [0] */
   uint64_t seed;          /* Lanczos start vector (splitmix64 stream)         [0]  */
 } xm_options;
 
@@ -153,11 +156,26 @@ const char* xm_strerror(xm_status s);
  * row sharding (world = 1: single GPU).  nccl_id: 128-byte ncclUniqueId from
  * xm_nccl_unique_id on rank 0, broadcast by the caller (NULL if world == 1).
  * opts: NULL ⇒ defaults.  cuda_stream: a cudaStream_t to run on (NULL ⇒ the
- * context creates its own non-blocking stream). */
+ * context creates its own non-blocking stream).
+ * Testing world > 1 on one GPU: an nccl_id whose first bytes are
+ * XM_LOOPBACK_MAGIC joins an in-process loopback group instead of NCCL — the
+ * `world` contexts (one host thread each, same 128-byte id) then exchange
+ * shards by device copies with the NCCL collectives' semantics. */
+#define XM_LOOPBACK_MAGIC "XM-LOOPBACK"
 xm_status xm_create(xm_ctx** out, int device, int rank, int world, const void* nccl_id,
                     const xm_options* opts, void* cuda_stream);
 void xm_destroy(xm_ctx* ctx);
 xm_status xm_nccl_unique_id(void* out128);
+
+/* Row shard of `rank` among `world` ranks.  Host-only: no
+ * device work, callable without a GPU.  Rank q owns frames [*f0, *f1) ⇒ Q rows
+ * [3·f0, 3·f1): contiguous ranges of nfpr = ⌈N/world⌉ frames
+ * (*frames_per_rank, may be NULL); trailing ranks may be short or empty.
+ * Replicated n×r vectors are all-gathered in a padded layout of world·3·nfpr
+ * rows (rank q's shard at row 3·q·nfpr), whose first n rows are the natural
+ * row-major order.  XM_EINVAL on N < 1, world < 1 or rank ∉ [0, world). */
+xm_status xm_shard_rows(int32_t N, int32_t world, int32_t rank, int32_t* f0, int32_t* f1,
+                        int32_t* frames_per_rank);
 
 /* H1–H5.  Build Q from E observations (frame[e], landmark[e], ũ_e =
  * lifted_pts[3e..3e+2], w_e = weights[e] or 1 if weights == NULL).

@@ -254,6 +254,76 @@ def build_Q(N: int, M: int, frame, landmark, pts, w=None, validate_input=True) -
                       pts=pts, w=w, N=N, M=M)
 
 
+def q_rows(N: int, M: int, frame, landmark, pts, w=None, rows=()) -> np.ndarray:
+    """Rows I of the same Q as build_Q, without forming any n×n matrix — the
+    full-size sampled parity oracle (configs too large for a dense n×n Q).
+
+    Same definition (Schur complement of Eq. (3)'s quadratic form, landmarks
+    then translations eliminated, t_0 = 0; App. A, reading C1):
+      * landmark elimination (H_pp = diag(W_k)): for a z-block
+        Z (z = [Y-rows; t]),  H_z Z = Σ_e w_e b_e (b_eᵀZ − m_k(e)),
+        m_k = Σ_{e∈k} w_e b_eᵀZ / W_k  (the weighted landmark mean);
+      * S[I,:] = (H_z E_I)[:n]ᵀ,  C̄[:,I] = (H_z E_I)[n+1:]  (H_z symmetric);
+      * K̄ = H_z[t₁.., t₁..] = diag(Σ_{e∈i} w_e) − F diag(1/W) Fᵀ,
+        F_ik = Σ_{e: i,k} w_e  (the t-block of the same formula);
+      * Q[I,:] = S[I,:] − (K̄⁻¹ C̄[:,I])ᵀ C̄,  with C̄ᵀX = (H_z [0; 0; X])[:n].
+    Cost O(E·|I|) plus one dense Cholesky of K̄ ((N−1)×(N−1))."""
+    frame, landmark, pts, w, _ = validate(N, M, frame, landmark, pts, w)
+    n = 3 * N
+    rows = np.asarray(rows, dtype=np.int64).ravel()
+    W = np.bincount(landmark, weights=w, minlength=M)
+    Winv = np.zeros(M)
+    Winv[W > 0] = 1.0 / W[W > 0]
+
+    def hz_apply(Z):                      # Z: (n+N)×c  →  H_z Z
+        c = Z.shape[1]
+        Yb = Z[:n].reshape(N, 3, c)
+        be = np.einsum("ea,eac->ec", pts, Yb[frame]) + Z[n + frame]        # b_eᵀZ
+        m = np.zeros((M, c))
+        np.add.at(m, landmark, w[:, None] * be)
+        res = w[:, None] * (be - Winv[landmark, None] * m[landmark])     # w_e(b_eᵀZ − m_k)
+        out = np.zeros((n + N, c))
+        outY = out[:n].reshape(N, 3, c)
+        np.add.at(outY, frame, pts[:, :, None] * res[:, None, :])
+        np.add.at(out[n:], frame, res)
+        return out
+
+    def hz_cols(Z, chunk=8):
+        return np.concatenate([hz_apply(Z[:, j:j + chunk]) for j in range(0, Z.shape[1], chunk)],
+                              axis=1) if Z.shape[1] else np.zeros((n + N, 0))
+
+    EI = np.zeros((n + N, rows.size))
+    EI[rows, np.arange(rows.size)] = 1.0
+    HI = hz_cols(EI)
+    S_I = HI[:n].T.copy()                 # S[I, :]
+    if N == 1:
+        return S_I
+    F = sp.csr_matrix((w, (frame, landmark)), shape=(N, M))
+    K = -(F @ sp.diags(Winv) @ F.T).toarray()
+    K[np.arange(N), np.arange(N)] += np.bincount(frame, weights=w, minlength=N)
+    Kb = K[1:, 1:]
+    try:
+        L = np.linalg.cholesky(Kb)
+    except np.linalg.LinAlgError:
+        raise OracleError("EDISCONNECTED", "graph numerically disconnected")
+    X = sla.cho_solve((L, True), HI[n + 1:])          # K̄⁻¹ C̄[:, I]
+    Z = np.zeros((n + N, rows.size))
+    Z[n + 1:] = X
+    CtX = hz_cols(Z)[:n]                               # C̄ᵀ X
+    return S_I - CtX.T
+
+
+def edge_objective(frame, landmark, pts, w, s, R, t, p) -> float:
+    """Eq. (3) evaluated directly: Σ_e w_e ‖s_i R_i ũ_e + t_i − p_k‖²."""
+    frame = np.asarray(frame, np.int64)
+    landmark = np.asarray(landmark, np.int64)
+    pts = np.asarray(pts, np.float64).reshape(-1, 3)
+    w = np.ones(len(frame)) if w is None else np.asarray(w, np.float64)
+    x_e = s[frame, None] * np.einsum("eab,eb->ea", R[frame], pts) + t[frame]
+    resid = x_e - p[landmark]
+    return float(np.sum(w * np.sum(resid * resid, axis=1)))
+
+
 # =============================================================================
 # Manifold calculus  (Prop. 4/5 P:360-374, P:487-508; S:191-279; C4, C5)
 # =============================================================================
@@ -753,8 +823,7 @@ def round_recover(dm: DataMatrix, Y) -> Solution:
     np.add.at(acc, dm.landmark, dm.w[:, None] * x_e)
     obs = dm.W > 0
     p[obs] = acc[obs] / dm.W[obs, None]
-    resid = x_e - p[dm.landmark]
-    edge_obj = float(np.sum(dm.w * np.sum(resid * resid, axis=1)))
+    edge_obj = edge_objective(dm.frame, dm.landmark, dm.pts, dm.w, s, R, t, p)
     return Solution(R=R, s=s, t=t, p=p, n_flipped=flips, Yr=Yr,
                     rho_hat=float(np.vdot(Yr, dm.Q @ Yr)), edge_objective=edge_obj)
 

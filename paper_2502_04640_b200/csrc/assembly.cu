@@ -810,11 +810,7 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
   c->n = n;
   c->ldq = round_up(std::max(n, 1), 32);
   c->ldk = round_up(std::max(N - 1, 1), 32);
-  c->nfpr = ceil_div(N, c->world);
-  c->f0 = std::min(N, c->rank * c->nfpr);
-  c->f1 = std::min(N, c->f0 + c->nfpr);
-  c->row0 = 3 * c->f0;
-  c->nrows = 3 * (c->f1 - c->f0);
+  set_shard(c, N);
   c->Q.alloc((size_t)std::max(c->nrows, 1) * c->ldq);
   XM_CUDA(cudaMemsetAsync(c->Q.p, 0, (size_t)std::max(c->nrows, 1) * c->ldq * 8, c->stream));
   if (N > 1) {

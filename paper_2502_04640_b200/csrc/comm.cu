@@ -12,6 +12,11 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <condition_variable>
+#include <map>
+#include <mutex>
+#include <vector>
+
 namespace xm {
 
 namespace {
@@ -62,9 +67,57 @@ void nccl_unique_id(void* out128) {
   memcpy(out128, &id, sizeof(id));
 }
 
+// ---------------------------------------------------------------------------
+// Loopback group: `world` contexts of ONE process (one thread each, any device)
+// exchanging through device-to-device copies with host barriers.  Selected by
+// an id that starts with XM_LOOPBACK_MAGIC (include/xm.h); it exists so the
+// world > 1 path (sharded assembly, partial SpMM rows, padded all-gather,
+// all-reduce) runs and is checked on a single-GPU box.  Same semantics as the
+// NCCL calls it replaces; the all-reduce sums in rank order on every rank.
+struct LoopGroup {
+  int world = 0, refs = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  std::vector<const void*> ptr;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    const uint64_t g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+static std::mutex g_loop_m;
+static std::map<std::string, LoopGroup*> g_loops;
+
+static bool is_loopback_id(const void* id) {
+  return id && memcmp(id, XM_LOOPBACK_MAGIC, sizeof(XM_LOOPBACK_MAGIC) - 1) == 0;
+}
+
 void nccl_init(xm_ctx* c, const void* id) {
   if (c->world <= 1) return;
   if (!id) throw Error(XM_EINVAL, "world > 1 requires an ncclUniqueId");
+  if (is_loopback_id(id)) {
+    std::string key((const char*)id, 128);
+    std::lock_guard<std::mutex> lk(g_loop_m);
+    LoopGroup*& g = g_loops[key];
+    if (!g) {
+      g = new LoopGroup();
+      g->world = c->world;
+      g->ptr.assign(c->world, nullptr);
+    }
+    if (g->world != c->world) throw Error(XM_EINVAL, "loopback group: world mismatch");
+    ++g->refs;
+    c->loop = g;
+    c->loop_key = key;
+    return;
+  }
   load_nccl();
   ncclUniqueId uid;
   memcpy(&uid, id, sizeof(uid));
@@ -74,11 +127,34 @@ void nccl_init(xm_ctx* c, const void* id) {
 }
 
 void nccl_destroy(xm_ctx* c) {
+  if (c->loop) {
+    std::lock_guard<std::mutex> lk(g_loop_m);
+    LoopGroup* g = static_cast<LoopGroup*>(c->loop);
+    if (--g->refs == 0) {
+      g_loops.erase(c->loop_key);
+      delete g;
+    }
+    c->loop = nullptr;
+  }
   if (c->nccl_comm && g_nccl.CommDestroy) g_nccl.CommDestroy((ncclComm_t)c->nccl_comm);
   c->nccl_comm = nullptr;
 }
 
 void nccl_allgather(xm_ctx* c, const double* send, double* recv, size_t count_per_rank) {
+  if (c->loop) {
+    LoopGroup* g = static_cast<LoopGroup*>(c->loop);
+    XM_CUDA(cudaStreamSynchronize(c->stream));  // our shard is complete
+    g->ptr[c->rank] = send;
+    g->barrier();                               // every shard is complete
+    for (int q = 0; q < c->world; ++q) {
+      double* dst = recv + (size_t)q * count_per_rank;
+      if (g->ptr[q] != dst)
+        XM_CUDA(cudaMemcpyAsync(dst, g->ptr[q], count_per_rank * 8, cudaMemcpyDefault, c->stream));
+    }
+    XM_CUDA(cudaStreamSynchronize(c->stream));
+    g->barrier();                               // nobody overwrites a shard still being read
+    return;
+  }
   check(g_nccl.AllGather(send, recv, count_per_rank, ncclFloat64, (ncclComm_t)c->nccl_comm,
                          c->stream),
         "ncclAllGather");
@@ -86,6 +162,20 @@ void nccl_allgather(xm_ctx* c, const double* send, double* recv, size_t count_pe
 
 void nccl_allreduce_sum(xm_ctx* c, double* buf, size_t count) {
   if (c->world <= 1) return;
+  if (c->loop) {
+    LoopGroup* g = static_cast<LoopGroup*>(c->loop);
+    std::vector<double> all((size_t)c->world * count), sum(count, 0.0);
+    XM_CUDA(cudaStreamSynchronize(c->stream));
+    g->ptr[c->rank] = buf;
+    g->barrier();
+    for (int q = 0; q < c->world; ++q)
+      XM_CUDA(cudaMemcpy(all.data() + (size_t)q * count, g->ptr[q], count * 8, cudaMemcpyDefault));
+    g->barrier();
+    for (int q = 0; q < c->world; ++q)
+      for (size_t k = 0; k < count; ++k) sum[k] += all[(size_t)q * count + k];
+    XM_CUDA(cudaMemcpy(buf, sum.data(), count * 8, cudaMemcpyDefault));
+    return;
+  }
   check(g_nccl.AllReduce(buf, buf, count, ncclFloat64, ncclSum, (ncclComm_t)c->nccl_comm,
                          c->stream),
         "ncclAllReduce");

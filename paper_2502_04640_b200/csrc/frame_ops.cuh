@@ -115,7 +115,7 @@ __device__ __forceinline__ void block_reduce_store(double (&v)[NC], double* __re
   for (int c = 0; c < NC; ++c) sh[c][threadIdx.x] = v[c];
   __syncthreads();
   constexpr int P = pow2_floor(NT);  // largest power of two ≤ NT
-  if (P != NT) {  // fold the tail [P, NT) onto [0, NT − P)
+  if constexpr (P != NT) {  // fold the tail [P, NT) onto [0, NT − P)
     if (threadIdx.x < NT - P) {
 #pragma unroll
       for (int c = 0; c < NC; ++c) {

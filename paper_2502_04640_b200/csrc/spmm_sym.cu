@@ -120,8 +120,8 @@ struct SymPlan {
 };
 
 static SymPlan& sym_plan(xm_ctx* c) {
-  static std::map<xm_ctx*, SymPlan> plans;  // one plan per context
-  SymPlan& p = plans[c];
+  if (!c->sym_plan) c->sym_plan = new SymPlan();
+  SymPlan& p = *static_cast<SymPlan*>(c->sym_plan);
   int sms = 148;
   XM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
   const int n = c->n, G = std::min(148, sms);
@@ -129,14 +129,16 @@ static SymPlan& sym_plan(xm_ctx* c) {
   // Q tensor map: dims {n columns, n rows}, row pitch ldq·8 B, box TR × BC,
   // OOB → zero fill (rows / columns ≥ n read as 0)
   {
-    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-    if (!encode) {
+    static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+      PFN_cuTensorMapEncodeTiled_v12000 f = nullptr;
       cudaDriverEntryPointQueryResult q;
-      XM_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode),
-                                      cudaEnableDefault, &q));
-      if (!encode || q != cudaDriverEntryPointSuccess)
-        throw Error(XM_ECUDA, "cuTensorMapEncodeTiled unavailable");
-    }
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&f),
+                                  cudaEnableDefault, &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess)
+        f = nullptr;
+      return f;
+    }();
+    if (!encode) throw Error(XM_ECUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)n};
     cuuint64_t strides[1] = {(cuuint64_t)c->ldq * 8};
     cuuint32_t box[2] = {(cuuint32_t)BC, (cuuint32_t)TR};
@@ -526,7 +528,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
 }
 
 // ---------------------------------------------------------------- host side
-bool spmm_sym_supported(xm_ctx* c, int r) { return c->world == 1 && r >= 1 && r <= 5 && c->use_sym; }
+// Kernel choice per (N, r), from tools/exp_sym.sh on B200:
+//   B (N=2000): sym 41.4 µs vs full-row 51.1 µs at r=1, 57.9 vs 55.3 at r=3;
+//   E (N=10155): sym 988 µs vs full-row 1033 µs at r=3.
+// The fused finish + per-tile 2-sided update cost ~25 µs at N=2000, so the
+// half-traffic kernel only pays for r = 1 (Lanczos) or once Q is large.
+void sym_plan_destroy(xm_ctx* c) {
+  delete static_cast<SymPlan*>(c->sym_plan);
+  c->sym_plan = nullptr;
+}
+
+bool spmm_sym_supported(xm_ctx* c, int r) {
+  if (c->world != 1 || r < 1 || r > 5 || c->opt.spmm_kernel == 1) return false;
+  return c->opt.spmm_kernel == 2 || r == 1 || c->N >= 4000;
+}
 
 int spmm_sym_partials(xm_ctx* c) { return sym_plan(c).G; }
 

@@ -401,6 +401,7 @@ void xm_default_options(xm_options* o) {
   o->refresh_every = 50;
   o->profile = 0;
   o->cert_cholesky = 1;
+  o->spmm_kernel = 0;
   o->seed = 0;
 }
 
@@ -423,6 +424,17 @@ const char* xm_strerror(xm_status s) {
   return "unknown status";
 }
 
+xm_status xm_shard_rows(int32_t N, int32_t world, int32_t rank, int32_t* f0, int32_t* f1,
+                        int32_t* frames_per_rank) {
+  if (N < 1 || world < 1 || rank < 0 || rank >= world || !f0 || !f1) return XM_EINVAL;
+  int a, b, nfpr;
+  shard_of(N, world, rank, &a, &b, &nfpr);
+  *f0 = a;
+  *f1 = b;
+  if (frames_per_rank) *frames_per_rank = nfpr;
+  return XM_OK;
+}
+
 xm_status xm_nccl_unique_id(void* out128) {
   if (!out128) return XM_EINVAL;
   try {
@@ -443,7 +455,8 @@ xm_status xm_create(xm_ctx** out, int device, int rank, int world, const void* n
   c->world = world;
   if (opts) c->opt = *opts; else xm_default_options(&c->opt);
   // A/B switches for measurements (the defaults are the production path)
-  if (std::getenv("XM_NO_SYM")) c->use_sym = false;
+  if (std::getenv("XM_NO_SYM")) c->opt.spmm_kernel = 1;
+  if (std::getenv("XM_FORCE_SYM")) c->opt.spmm_kernel = 2;
   if (std::getenv("XM_NO_GRAPHS")) c->use_graphs = false;
   if (c->opt.rank_cap > XM_MAX_R) c->opt.rank_cap = XM_MAX_R;
   xm_status st = guard(c, [&] {
@@ -471,6 +484,7 @@ void xm_destroy(xm_ctx* c) {
   destroy_graphs(c);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   nccl_destroy(c);
+  sym_plan_destroy(c);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -506,11 +520,7 @@ xm_status xm_set_Q(xm_ctx* c, int32_t N, const double* Q_full) {
     c->n = 3 * N;
     c->ldq = round_up(c->n, 32);
     c->ldk = round_up(std::max(N - 1, 1), 32);
-    c->nfpr = ceil_div(N, c->world);
-    c->f0 = std::min(N, c->rank * c->nfpr);
-    c->f1 = std::min(N, c->f0 + c->nfpr);
-    c->row0 = 3 * c->f0;
-    c->nrows = 3 * (c->f1 - c->f0);
+    set_shard(c, N);
     c->Q.alloc((size_t)std::max(c->nrows, 1) * c->ldq);
     const int64_t n = c->n;
     if (c->nrows > 0) {

@@ -6,6 +6,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <map>
@@ -156,8 +157,12 @@ struct xm_ctx {
   size_t ev_used = 0;
   xm::DBuf<int> ev_exec;           // per event pair: 1 if the SpMM actually ran
   std::vector<double> ev_bytes;    // per event pair: algorithmic bytes
-  // NCCL
+  // NCCL (or the in-process loopback group used to test world > 1 on one GPU)
   void* nccl_comm = nullptr;
+  void* loop = nullptr;
+  std::string loop_key;
+  // lower-triangle SpMM work plan + tensor map (spmm_sym.cu)
+  void* sym_plan = nullptr;
   xm::DBuf<double> gbuf;  // all-gather staging
   // hooks (test / bench entry points) use their own scratch
   xm::DBuf<double> hY, hV, hO, hQY;
@@ -184,7 +189,6 @@ struct xm_ctx {
   TcgGraph* cap_target = nullptr;                 // non-null while capturing
   cudaStream_t cap_stream = nullptr;
   bool use_graphs = true;
-  bool use_sym = true;             // symmetric (lower-triangle) SpMM on one GPU, r ≤ 6
   xm::DBuf<double> sym_part;       // per-unit row / column partials of the symmetric SpMM
   xm::DBuf<int> gbar;              // software grid-barrier state of the symmetric SpMM
   // named scratch buffers that persist across calls (grow-only): no cudaMalloc /
@@ -297,5 +301,19 @@ void nccl_init(xm_ctx* c, const void* id);
 void nccl_destroy(xm_ctx* c);
 void nccl_allgather(xm_ctx* c, const double* send, double* recv, size_t count_per_rank);
 void nccl_allreduce_sum(xm_ctx* c, double* buf, size_t count);
+void sym_plan_destroy(xm_ctx* c);
+
+// Row sharding: rank q owns frames [q·nfpr, min(N, (q+1)·nfpr)),
+// nfpr = ⌈N/world⌉; vectors exchanged by the all-gather hold world·3·nfpr rows.
+inline void shard_of(int N, int world, int rank, int* f0, int* f1, int* nfpr) {
+  *nfpr = (N + world - 1) / world;
+  *f0 = std::min(N, rank * *nfpr);
+  *f1 = std::min(N, *f0 + *nfpr);
+}
+inline void set_shard(xm_ctx* c, int N) {
+  shard_of(N, c->world, c->rank, &c->f0, &c->f1, &c->nfpr);
+  c->row0 = 3 * c->f0;
+  c->nrows = 3 * (c->f1 - c->f0);
+}
 
 }  // namespace xm

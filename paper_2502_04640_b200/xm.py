@@ -38,7 +38,7 @@ class Options(ctypes.Structure):
                 ("max_outer", ctypes.c_int32), ("rank_cap", ctypes.c_int32),
                 ("lanczos_max", ctypes.c_int32), ("refresh_every", ctypes.c_int32),
                 ("profile", ctypes.c_int32), ("cert_cholesky", ctypes.c_int32),
-                ("seed", ctypes.c_uint64)]
+                ("spmm_kernel", ctypes.c_int32), ("seed", ctypes.c_uint64)]
 
 
 class SolveInfo(ctypes.Structure):
@@ -82,6 +82,7 @@ _SIGS = {
     "xm_create": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, _P, _P]),
     "xm_destroy": (None, [_P]),
     "xm_nccl_unique_id": (ctypes.c_int, [_P]),
+    "xm_shard_rows": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P, _P, _P]),
     "xm_build_Q": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, _P, _P, _P, _P]),
     "xm_solve": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_double, _P]),
     "xm_certify": (ctypes.c_int, [_P, _P, _P]),
@@ -128,12 +129,36 @@ def default_options(**overrides) -> Options:
     return o
 
 
+def shard_rows(N: int, world: int, rank: int):
+    """(f0, f1, nfpr): frames [f0, f1) of `rank`, nfpr = ⌈N/world⌉ (xm_shard_rows;
+    host-only, no GPU needed)."""
+    f0, f1, nf = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    st = load_library().xm_shard_rows(int(N), int(world), int(rank), ctypes.byref(f0),
+                                      ctypes.byref(f1), ctypes.byref(nf))
+    if st != 0:
+        raise XMError(st, "xm_shard_rows")
+    return f0.value, f1.value, nf.value
+
+
 def nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     st = load_library().xm_nccl_unique_id(buf)
     if st != 0:
         raise XMError(st, "ncclGetUniqueId")
     return buf.raw
+
+
+LOOPBACK_MAGIC = b"XM-LOOPBACK"
+
+
+def loopback_id(token: str) -> bytes:
+    """128-byte id selecting the in-process loopback group (include/xm.h
+    XM_LOOPBACK_MAGIC): `world` Contexts created with it, one host thread each,
+    run the world > 1 path on one GPU without NCCL."""
+    raw = LOOPBACK_MAGIC + b"\0" + token.encode()
+    if len(raw) > 128:
+        raise ValueError("token too long")
+    return raw.ljust(128, b"\0")
 
 
 # --------------------------------------------------------------- marshalling

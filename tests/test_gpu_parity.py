@@ -87,11 +87,14 @@ def test_duplicates_keep_first_and_errors(xm):
         assert e.value.name == "ESTATE"
 
 
-@pytest.fixture(scope="module")
-def identical_Q(xm):
+KERNELS = {1: "fullrow", 2: "lowertri"}   # xm_options.spmm_kernel (r > 5 ⇒ full-row)
+
+
+@pytest.fixture(scope="module", params=sorted(KERNELS), ids=lambda k: KERNELS[k])
+def identical_Q(xm, request):
     sc = make_scene(67, 1500, "unordered", seed=5, track_mean=9.0, sigma_d=0.1, sigma_u=0.01)
     dm = xo.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
-    ctx = xm.Context()
+    ctx = xm.Context(spmm_kernel=request.param)
     ctx.set_Q(dm.Q)
     yield sc, dm, ctx
     ctx.close()
@@ -124,9 +127,9 @@ def test_grad_hvp_project_retract_identical_Q(identical_Q, r):
     assert rel(Yr, xo.retract(Y, 0.3 * V)) <= 1e-13
 
 
-def _e2e(xm, sc, Y0=None, **opts):
+def _e2e(xm, sc, Y0=None, ctx_opts=None, **opts):
     dm, st, sol, rep = xo.solve(sc, Y0=Y0, opts=xo.Options(**opts) if opts else None)
-    with xm.Context(**opts) as ctx:
+    with xm.Context(**opts, **(ctx_opts or {})) as ctx:
         ctx.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
         if Y0 is not None:
             ctx.set_factor(Y0)
@@ -137,10 +140,11 @@ def _e2e(xm, sc, Y0=None, **opts):
     return dm, st, sol, rep, status, info, cert, gsol, Yg
 
 
+@pytest.mark.parametrize("kernel", [0, 2], ids=["auto", "lowertri"])
 @pytest.mark.parametrize("cfg", SCENES[:3], ids=lambda c: f"{c['kind']}{c['N']}")
-def test_end_to_end_solve_parity(xm, cfg):
+def test_end_to_end_solve_parity(xm, cfg, kernel):
     sc = make_scene(seed=3, **cfg)
-    dm, st, sol, rep, status, info, cert, gsol, Yg = _e2e(xm, sc)
+    dm, st, sol, rep, status, info, cert, gsol, Yg = _e2e(xm, sc, ctx_opts=dict(spmm_kernel=kernel))
     assert status == 0 and info["certified"] == 1 and st.certified
     assert abs(info["f"] - st.f) <= 1e-8 * (1.0 + abs(st.f))
     assert x_rel_err(Yg, st.Y) <= 1e-6

@@ -95,6 +95,57 @@ def test_prop1_equivalence_brute_force(seed):
         assert abs(f_q - f_b) <= 1e-9 * max(1.0, abs(f_b)), (r, f_q, f_b)
 
 
+@pytest.mark.parametrize("cfg", [
+    dict(N=9, M=120, kind="unordered", vis_prob=0.5, sigma_d=0.1, sigma_u=0.01),
+    dict(N=30, M=400, kind="loop", window=5, sigma_d=0.05),
+    dict(N=25, M=500, kind="road", track_mean=5.0, sigma_u=1e-3, sigma_d=0.01, weights="uniform"),
+    dict(N=1, M=6, kind="unordered", vis_prob=1.0),
+], ids=lambda c: f"{c['kind']}{c['N']}")
+def test_q_rows_matches_dense_Q(cfg):
+    """Sampled-row Schur complement (q_rows) = rows of the dense build_Q — the
+    latter pinned above by Prop. 1 brute force; incl. the first / last row,
+    duplicate observations and N = 1 (Q = 0)."""
+    sc = make_scene(seed=4, **cfg)
+    dm = xo.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+    n = 3 * sc.N
+    rows = np.unique(np.concatenate([[0, n - 1], np.random.default_rng(1).integers(0, n, 7)]))
+    fr = np.concatenate([sc.frame, sc.frame[:3]])         # duplicates: keep first (S:92)
+    lm = np.concatenate([sc.landmark, sc.landmark[:3]])
+    pts = np.concatenate([sc.pts, 2.0 * sc.pts[:3]])
+    w = np.concatenate([sc.w, sc.w[:3]])
+    QI = xo.q_rows(sc.N, sc.M, fr, lm, pts, w, rows)
+    assert QI.shape == (rows.size, n)
+    assert np.linalg.norm(QI - dm.Q[rows]) <= 1e-12 * max(1.0, dm.normF)
+
+
+def test_q_rows_noise_free_annihilates_ground_truth():
+    """F1: Q[I,:] Y_gt = 0 on a noise-free scene, every row."""
+    sc = make_scene(15, 300, "unordered", seed=2, vis_prob=0.4)
+    QI = xo.q_rows(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w, np.arange(3 * sc.N))
+    assert np.linalg.norm(QI @ gt_factor(sc)) <= 1e-10 * np.linalg.norm(QI)
+    assert np.linalg.norm(QI - QI.T) <= 1e-12 * np.linalg.norm(QI)
+
+
+def test_edge_objective_brute_force_and_ground_truth():
+    """Eq. (3): zero at the noise-free ground truth, and equal to a
+    per-observation loop at arbitrary (s, R, t, p)."""
+    sc = make_scene(6, 40, "unordered", seed=3, vis_prob=0.6)
+    assert xo.edge_objective(sc.frame, sc.landmark, sc.pts, sc.w, sc.s, sc.R, sc.t, sc.p) \
+        <= 1e-20 * len(sc.frame) + 1e-24
+    rng = np.random.default_rng(0)
+    s = rng.uniform(0.5, 2.0, sc.N)
+    R = np.stack([np.linalg.qr(rng.standard_normal((3, 3)))[0] for _ in range(sc.N)])
+    t = rng.standard_normal((sc.N, 3))
+    p = rng.standard_normal((sc.M, 3))
+    tot = 0.0
+    for e in range(len(sc.frame)):
+        i, k = int(sc.frame[e]), int(sc.landmark[e])
+        d = s[i] * (R[i] @ sc.pts[e]) + t[i] - p[k]
+        tot += sc.w[e] * float(d @ d)
+    assert abs(xo.edge_objective(sc.frame, sc.landmark, sc.pts, sc.w, s, R, t, p) - tot) \
+        <= 1e-12 * tot
+
+
 def test_N1_gives_zero_Q():
     """S:148: N = 1 ⇒ Q = 0."""
     sc = make_scene(1, 7, "unordered", seed=0, vis_prob=1.0)
