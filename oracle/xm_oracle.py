@@ -254,7 +254,8 @@ def build_Q(N: int, M: int, frame, landmark, pts, w=None, validate_input=True) -
                       pts=pts, w=w, N=N, M=M)
 
 
-def q_rows(N: int, M: int, frame, landmark, pts, w=None, rows=()) -> np.ndarray:
+def q_rows(N: int, M: int, frame, landmark, pts, w=None, rows=(), info: Optional[dict] = None
+           ) -> np.ndarray:
     """Rows I of the same Q as build_Q, without forming any n×n matrix — the
     full-size sampled parity oracle (configs too large for a dense n×n Q).
 
@@ -267,7 +268,10 @@ def q_rows(N: int, M: int, frame, landmark, pts, w=None, rows=()) -> np.ndarray:
       * K̄ = H_z[t₁.., t₁..] = diag(Σ_{e∈i} w_e) − F diag(1/W) Fᵀ,
         F_ik = Σ_{e: i,k} w_e  (the t-block of the same formula);
       * Q[I,:] = S[I,:] − (K̄⁻¹ C̄[:,I])ᵀ C̄,  with C̄ᵀX = (H_z [0; 0; X])[:n].
-    Cost O(E·|I|) plus one dense Cholesky of K̄ ((N−1)×(N−1))."""
+    Cost O(E·|I|) plus one dense Cholesky of K̄ ((N−1)×(N−1)).
+    If `info` is a dict it receives the rounding-error scale of the
+    elimination (reading C13): kappa_K (LAPACK dpocon 1-norm estimate of
+    κ(K̄)) and S_I_norm = ‖S[I,:]‖_F (the magnitude Q[I,:] cancels from)."""
     frame, landmark, pts, w, _ = validate(N, M, frame, landmark, pts, w)
     n = 3 * N
     rows = np.asarray(rows, dtype=np.int64).ravel()
@@ -296,6 +300,8 @@ def q_rows(N: int, M: int, frame, landmark, pts, w=None, rows=()) -> np.ndarray:
     EI[rows, np.arange(rows.size)] = 1.0
     HI = hz_cols(EI)
     S_I = HI[:n].T.copy()                 # S[I, :]
+    if info is not None:
+        info.update(S_I_norm=float(np.linalg.norm(S_I)), kappa_K=1.0)
     if N == 1:
         return S_I
     F = sp.csr_matrix((w, (frame, landmark)), shape=(N, M))
@@ -306,6 +312,9 @@ def q_rows(N: int, M: int, frame, landmark, pts, w=None, rows=()) -> np.ndarray:
         L = np.linalg.cholesky(Kb)
     except np.linalg.LinAlgError:
         raise OracleError("EDISCONNECTED", "graph numerically disconnected")
+    if info is not None:
+        rcond, _ = sla.lapack.dpocon(L.T, np.abs(Kb).sum(axis=0).max())
+        info["kappa_K"] = 1.0 / max(float(rcond), 1e-300)
     X = sla.cho_solve((L, True), HI[n + 1:])          # K̄⁻¹ C̄[:, I]
     Z = np.zeros((n + N, rows.size))
     Z[n + 1:] = X

@@ -109,7 +109,13 @@ def E_noisy():
 def test_E_sampled_Q_rows_and_spmm(xm, E_noisy):
     sc = E_noisy
     rows = _sample_rows(sc.N, 12, 3)
-    QI = xo.q_rows(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w, rows)
+    info = {}
+    QI = xo.q_rows(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w, rows, info=info)
+    # reading C13: both sides solve with K̄ by backward-stable Cholesky, so
+    # ‖ΔQ_I‖ ≲ c·u·κ(K̄)·‖S_I‖ (Q_I is S_I minus a term of S_I's size); c = 8
+    # covers both sides' errors.  Config E: κ₁(K̄) ≈ 2.3e4, ‖S_I‖/‖Q_I‖ ≈ 71.
+    tol = max(1e-10, 8 * np.finfo(float).eps * info["kappa_K"] * info["S_I_norm"]
+              / np.linalg.norm(QI))
     Vs = {r: random_tangent_ambient(sc.N, r, 21 + r) for r in (1, 3)}
     outs = {}
     for kernel in (0, 1, 2):
@@ -117,13 +123,13 @@ def test_E_sampled_Q_rows_and_spmm(xm, E_noisy):
             ctx.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
             if kernel == 0:
                 Qg = np.concatenate([ctx.Q_rows(int(a), 3) for a in rows[::3]])
-                assert rel(Qg, QI) <= 1e-10, rel(Qg, QI)
+                assert rel(Qg, QI) <= tol, (rel(Qg, QI), tol)
             for r, V in Vs.items():
                 outs[kernel, r] = ctx.spmm(V)
     for r, V in Vs.items():
         ref = QI @ V
         for kernel in (0, 1, 2):
-            assert rel(outs[kernel, r][rows], ref) <= 1e-10, (kernel, r)
+            assert rel(outs[kernel, r][rows], ref) <= tol, (kernel, r, tol)
         # the two streaming kernels on the same GPU-built Q: fp64 rounding apart
         assert rel(outs[1, r], outs[2, r]) <= 1e-12
 
@@ -158,13 +164,15 @@ def test_E_noisy_certified_and_recovery_optimal(xm, E_noisy):
     # rounded rotations are in SO(3), the anchor is the identity
     assert np.abs(np.einsum("iab,icb->iac", R, R) - np.eye(3)).max() <= 1e-12
     assert np.all(np.linalg.det(R) > 0) and s[0] == 1.0 and np.abs(R[0] - np.eye(3)).max() == 0
+    # (a property of the GPU's outputs, evaluated here — not an oracle call)
     # ρ̂ = tr(Q Ūᵀ Ū) equals Eq. (3) at the recovered (s, R, t, p)
-    rho_edge = xo.edge_objective(sc.frame, sc.landmark, sc.pts, sc.w, s, R, t, p)
-    assert abs(rho_edge - cert["rho_hat"]) <= 1e-8 * (1.0 + abs(rho_edge))
-    # Eq. (4): p_k, t_i (i ≥ 1) minimise Eq. (3) at fixed Ū — zero gradients
     fr, lm, w = sc.frame.astype(np.int64), sc.landmark.astype(np.int64), sc.w
     x = s[fr, None] * np.einsum("eab,eb->ea", R[fr], sc.pts) + t[fr]
-    res = w[:, None] * (x - p[lm])
+    d = x - p[lm]
+    rho_edge = float(np.sum(w * np.sum(d * d, axis=1)))
+    assert abs(rho_edge - cert["rho_hat"]) <= 1e-8 * (1.0 + abs(rho_edge))
+    # Eq. (4): p_k, t_i (i ≥ 1) minimise Eq. (3) at fixed Ū — zero gradients
+    res = w[:, None] * d
     gp = np.zeros((sc.M, 3))
     np.add.at(gp, lm, res)
     gt = np.zeros((sc.N, 3))
