@@ -1,0 +1,19 @@
+#!/bin/bash
+# One GPU call that produces a round's measurement evidence under gpurun_out/:
+# bench lines (xm arm B with cpu_baseline + e2e, reference arm B, xm arm E),
+# the ncu launch list of the bench command, and one `ncu --set full` capture of
+# the dominant kernel (k_spmm, non-speculative launches picked by --launch-skip).
+set -x
+OUT=gpurun_out/${TAG:-r1}
+mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu --format=csv > $OUT/gpu.txt
+timeout 900 python bench.py > $OUT/bench_B.json 2> $OUT/bench_B.err
+timeout 900 python bench.py --impl reference > $OUT/bench_ref_B.json 2> $OUT/bench_ref_B.err
+timeout 900 python bench.py --config E --no-cpu-baseline > $OUT/bench_E.json 2> $OUT/bench_E.err
+timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file $OUT/launches_B.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e \
+  > $OUT/ncu_launch.log 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_spmm \
+  --launch-skip ${SKIP:-3000} --launch-count ${COUNT:-6} -o $OUT/ncu_full_B -f \
+  python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/ncu_full.log 2>&1
+ls -la $OUT
