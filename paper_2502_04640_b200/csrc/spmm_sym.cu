@@ -548,8 +548,11 @@ int spmm_sym_partials(xm_ctx* c) { return sym_plan(c).G; }
 template <int R, int MODE>
 static void launch_sym(xm_ctx* c, const double* V, const SpmmEpiArgs& ep) {
   SymPlan& p = sym_plan(c);
-  const size_t rp = (size_t)p.U * BR * R, cp = (size_t)std::max(p.S, 1) * BC * R;
-  c->sym_part.alloc(rp + cp + 64);
+  // sized for the largest supported r once, so the address never changes when
+  // the staircase climbs (the tCG graphs of lower ranks captured it)
+  constexpr int kRmax = 5;
+  const size_t rp = (size_t)p.U * BR * R;
+  c->sym_part.alloc((size_t)p.U * BR * kRmax + (size_t)std::max(p.S, 1) * BC * kRmax + 64);
   double* rowpart = c->sym_part.p;
   double* colpart = c->sym_part.p + rp;
   if (!c->gbar.p) {

@@ -139,7 +139,8 @@ std::vector<uintptr_t> graph_signature(xm_ctx* c) {
   return {(uintptr_t)c->N, (uintptr_t)c->n, (uintptr_t)c->ldq, (uintptr_t)c->Q.p,
           (uintptr_t)c->Y.p, (uintptr_t)c->dir.p, (uintptr_t)c->lam.p, (uintptr_t)c->tcg.p,
           (uintptr_t)c->part1.p, (uintptr_t)c->part2.p, (uintptr_t)c->opt.profile,
-          (uintptr_t)c->f0, (uintptr_t)c->f1};
+          (uintptr_t)c->f0, (uintptr_t)c->f1, (uintptr_t)c->sym_part.p, (uintptr_t)c->gbar.p,
+          (uintptr_t)c->sym_plan};
 }
 
 void destroy_graph(xm_ctx::TcgGraph& g) {

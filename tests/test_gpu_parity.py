@@ -191,3 +191,23 @@ def test_lanczos_min_eig_matches_dense(xm):
         cert = ctx.certify(want_vector=True)
     assert abs(cert["lambda_min"] - lam_d) <= 1e-8 * dm.normF
     assert abs(abs(float(cert["v"] @ v_d)) - 1.0) <= 1e-6
+
+
+@pytest.mark.parametrize("kernel", [1, 2], ids=["fullrow", "lowertri"])
+def test_repeated_solves_reuse_graphs_across_rank_climb(xm, kernel):
+    """One context, build → solve twice (as bench.py's steps do) where the
+    staircase climbs 3 → 4: the tCG graphs captured at r = 3 in the first solve
+    are replayed in the second after the r = 4 products ran, and the results
+    are bitwise identical (buffers captured by a graph never move)."""
+    sc = make_scene(10, 500, "unordered", seed=0, vis_prob=0.6)
+    Y0 = random_factor(sc.N, 3, 1)
+    runs = []
+    with xm.Context(spmm_kernel=kernel, profile=1) as ctx:
+        for _ in range(3):
+            ctx.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+            ctx.set_factor(Y0)
+            status, info = ctx.solve()
+            runs.append((status, info, ctx.get_factor()))
+    for status, info, Y in runs:
+        assert status == 0 and info["r"] == 4 and info["escapes"] == 1
+        assert info["f"] == runs[0][1]["f"] and np.array_equal(Y, runs[0][2])
