@@ -163,4 +163,51 @@ __device__ __forceinline__ double block_sum_all(const double* __restrict__ part,
   return r;
 }
 
+// Sense-reversing software grid barrier.  Valid only for kernels whose G
+// CTAs are all co-resident (one per SM, G ≤ #SMs; launched cooperatively or
+// checked on the host) and issued on the library's single stream.
+__device__ __forceinline__ void grid_barrier(GridBar* gb, int G) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile int* vs = &gb->sense;
+    const int s = *vs;
+    __threadfence();
+    if (atomicAdd(&gb->count, 1) == G - 1) {
+      gb->count = 0;
+      __threadfence();
+      atomicExch(&gb->sense, s ^ 1);
+    } else {
+      while (*vs == s) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Fixed-order block sum for any block size NT (multiple of 32): xor-shuffle
+// tree per warp, then warp sums in warp order.  Every thread returns the same
+// value, and every block running it on the same inputs gets the same bits.
+template <int NT>
+__device__ __forceinline__ double block_sum_fixed(double v) {
+  static_assert(NT % 32 == 0, "whole warps");
+  __shared__ double ws[NT / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = ws[0];
+#pragma unroll
+  for (int w = 1; w < NT / 32; ++w) t += ws[w];
+  __syncthreads();
+  return t;
+}
+// Σ part[0..n) in a fixed order, identical in every block.  L1-bypassing
+// loads: the partials were written by other SMs before a grid barrier.
+template <int NT>
+__device__ __forceinline__ double block_sum_partials(const double* part, int n) {
+  double a = 0.0;
+  for (int b = threadIdx.x; b < n; b += NT) a += __ldcg(part + b);
+  return block_sum_fixed<NT>(a);
+}
+
 }  // namespace xm

@@ -416,6 +416,10 @@ int hvp_product(xm_ctx* c, int r, const double* Y, const double* V, double* HV, 
 
 void tcg_init(xm_ctx* c, int r, double Delta) {
   int64_t len = (int64_t)c->n * r;
+  if (!c->gbar.p) {  // grid-barrier state of the fused kernels (never inside a capture)
+    c->gbar.alloc(4);
+    XM_CUDA(cudaMemsetAsync(c->gbar.p, 0, 4 * sizeof(int), c->stream));
+  }
   k_tcg_init_vec<<<ceil_div(len, 256), 256, 0, c->stream>>>(len, c->grad.p, c->eta.p, c->Heta.p,
                                                            c->res.p, c->dir.p);
   XM_CHECK_LAUNCH();
@@ -426,12 +430,30 @@ void tcg_init(xm_ctx* c, int r, double Delta) {
   count_launch(c, 2);
 }
 
-// One tCG iteration = three kernels; state flows st[0] → st[1] → st[0].
+// One tCG iteration.  One GPU, full-row SpMM: ONE cooperative launch
+// (Q·δ → Hδ → grid barrier → α, η, Hη, r → grid barrier → β, δ; spmm.cu
+// EPI_TCG), state st[0] → st[0].  Otherwise three kernels, st[0] → st[1] → st[0].
 void tcg_iteration(xm_ctx* c, int r) {
   const int nb = frame_blocks(c);
   const int64_t len = (int64_t)c->n * r;
   c->part1.alloc(2048);
-  c->part2.alloc((size_t)nb + 64);
+  c->part2.alloc((size_t)nb + 4096);
+  if (tcg_fused_supported(c, r)) {
+    SpmmEpiArgs ep{};
+    ep.out = c->dir.p;
+    ep.Y = c->Y.p;
+    ep.lam = c->lam.p;
+    ep.partials = c->part1.p;
+    ep.stop = &c->tcg.p[0].stop;
+    ep.st = c->tcg.p;
+    ep.eta = c->eta.p;
+    ep.Heta = c->Heta.p;
+    ep.res = c->res.p;
+    ep.p2 = c->part2.p;
+    ep.gbar = reinterpret_cast<GridBar*>(c->gbar.p);
+    spmm(c, c->dir.p, r, EPI_TCG, ep);
+    return;
+  }
   int n1 = hvp_product(c, r, c->Y.p, c->dir.p, c->Hdir.p, c->part1.p, &c->tcg.p[0].stop);
   XM_DISPATCH_R(r, (k_tcg_update<R><<<nb, kFT, 0, c->stream>>>(
                        c->N, c->tcg.p, c->tcg.p + 1, c->part1.p, n1, c->Y.p, c->dir.p, c->Hdir.p,

@@ -90,6 +90,113 @@ struct SpmmCfg {
   static constexpr int kStages = (kStageBytes * 4 <= 176 * 1024) ? 4 : (kStageBytes * 3 <= 192 * 1024 ? 3 : 2);
 };
 
+// EPI_TCG: the rest of one Steihaug–Toint iteration after Hδ's Q·δ rows
+// (H8 + H9, the same arithmetic as k_tcg_update + k_tcg_dir in manifold.cu),
+// with two software grid barriers instead of two more launches.  Thread t
+// owns camera f0g + t of this CTA (≤ kSpmmThreads cameras per CTA, checked on
+// the host), so δ, Hδ, η, Hη, r and Y stay in registers across the barriers.
+// Every CTA re-derives α, τ, β and the stop tests from the same partials in
+// the same order ⇒ identical decisions everywhere; CTA 0 writes the state.
+template <int R>
+__device__ __forceinline__ void tcg_tail(const double* __restrict__ acc, int nf, int f0g,
+                                         const SpmmEpiArgs& ep, const TcgState& s0) {
+  constexpr int NT = kSpmmThreads;
+  const int t = threadIdx.x;
+  const bool has = t < nf;
+  const int i = f0g + t;
+  double* __restrict__ dir = ep.out;
+  Blk<R> y, dv, hd, e, he, rr;
+  double part = 0.0;
+  if (has) {
+    Blk<R> qv;
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int cc = 0; cc < R; ++cc) qv.v[p][cc] = acc[(3 * t + p) * R + cc];
+    load_blk<R>(ep.Y, i, y);
+    load_blk<R>(dir, i, dv);
+    double L[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) L[q] = ep.lam[6 * i + q];
+    sub_lam<R>(qv, L, dv, 2.0, 2.0, hd);  // Hδ = P(2Qδ − 2Λδ)
+    project_blk<R>(y, i == 0, hd);
+    part = dotb<R>(dv, hd);
+    load_blk<R>(ep.eta, i, e);
+    load_blk<R>(ep.Heta, i, he);
+    load_blk<R>(ep.res, i, rr);
+  }
+  const double pc = block_sum_fixed<NT>(part);
+  if (t == 0) ep.partials[blockIdx.x] = pc;
+  grid_barrier(ep.gbar, gridDim.x);
+  // ---- α, e_Pe′, boundary / τ  (k_tcg_update)
+  TcgState s = s0;
+  const double dHd = block_sum_partials<NT>(ep.partials, gridDim.x);
+  s.d_Hd = dHd;
+  s.n_hvp += 1;
+  const double alpha = (dHd != 0.0) ? s.z / dHd : INFINITY;
+  const double e_new = s.e_Pe + 2.0 * alpha * s.e_Pd + alpha * alpha * s.d_Pd;
+  const double D2 = s.Delta * s.Delta;
+  s.alpha = alpha;
+  s.e_Pe_new = e_new;
+  if (dHd <= 0.0 || e_new >= D2) {
+    s.tau = (-s.e_Pd + sqrt(s.e_Pd * s.e_Pd + s.d_Pd * (D2 - s.e_Pe))) / s.d_Pd;
+    s.boundary = 1;
+    s.stop = (dHd <= 0.0) ? TCG_NEGCURV : TCG_EXCEEDED;
+  } else {
+    s.boundary = 0;
+  }
+  const double a = s.boundary ? s.tau : alpha;
+  double rn2 = 0.0;
+  if (has) {
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int cc = 0; cc < R; ++cc) {
+        e.v[p][cc] = fma(a, dv.v[p][cc], e.v[p][cc]);
+        he.v[p][cc] = fma(a, hd.v[p][cc], he.v[p][cc]);
+      }
+    store_blk<R>(ep.eta, i, e);
+    store_blk<R>(ep.Heta, i, he);
+    if (!s.boundary) {
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int cc = 0; cc < R; ++cc) rr.v[p][cc] = fma(a, hd.v[p][cc], rr.v[p][cc]);
+      project_blk<R>(y, i == 0, rr);
+      store_blk<R>(ep.res, i, rr);
+      rn2 = frob2<R>(rr);
+    }
+  }
+  if (s.boundary) {
+    if (blockIdx.x == 0 && t == 0) *ep.st = s;
+    return;
+  }
+  const double pr = block_sum_fixed<NT>(rn2);
+  if (t == 0) ep.p2[blockIdx.x] = pr;
+  grid_barrier(ep.gbar, gridDim.x);
+  // ---- stop tests, β, recurrences  (k_tcg_dir)
+  const double z = block_sum_partials<NT>(ep.p2, gridDim.x);
+  s.e_Pe = s.e_Pe_new;
+  s.z_old = s.z;
+  s.z = z;
+  s.j += 1;
+  if (sqrt(z) <= s.r0 * fmin(pow(s.r0, s.theta), s.kappa)) {
+    s.stop = TCG_CONVERGED;
+  } else {
+    s.beta = s.z / s.z_old;
+    s.e_Pd = s.beta * (s.e_Pd + s.alpha * s.d_Pd);
+    s.d_Pd = s.z + s.beta * s.beta * s.d_Pd;
+    if (s.j >= s.max_inner) s.stop = TCG_MAXINNER;
+  }
+  if (blockIdx.x == 0 && t == 0) *ep.st = s;
+  if (s.stop || !has) return;
+#pragma unroll
+  for (int p = 0; p < 3; ++p)
+#pragma unroll
+    for (int cc = 0; cc < R; ++cc) dv.v[p][cc] = fma(s.beta, dv.v[p][cc], -rr.v[p][cc]);
+  store_blk<R>(dir, i, dv);  // δ ← −r + βδ (own cameras; every CTA is past its Q·δ)
+}
+
 template <int R, int MODE>
 __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(
     const double* __restrict__ Q, int64_t ldq, int n, int f_lo_rank, int nframes_own,
@@ -115,6 +222,8 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   for (int t = threadIdx.x; t < nrow * R; t += kSpmmThreads) acc[t] = 0.0;
+  __shared__ TcgState ts0;  // EPI_TCG: the iteration's starting state (read before any write)
+  if (MODE == EPI_TCG && threadIdx.x == 0) ts0 = *ep.st;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
@@ -230,6 +339,10 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(
     for (int t = threadIdx.x; t < nrow * R; t += kSpmmThreads) out[t] = acc[t];
     return;
   }
+  if constexpr (MODE == EPI_TCG) {
+    tcg_tail<R>(acc, fb - fa, f0g, ep, ts0);
+    return;
+  }
   constexpr int NC = (MODE == EPI_GRAD) ? 3 : (MODE == EPI_DF ? 2 : 1);
   double part[NC];
 #pragma unroll
@@ -329,7 +442,23 @@ static void launch_r(xm_ctx* c, const double* V, const SpmmEpiArgs& ep) {
     XM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
-  kern<<<G, kSpmmThreads, smem, c->stream>>>(c->Q.p, c->ldq, c->n, c->f0, nown, V, ep);
+  if (MODE == EPI_TCG) {
+    // grid barriers inside: cooperative launch guarantees the G CTAs are co-resident
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(kSpmmThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    XM_CUDA(cudaLaunchKernelEx(&cfg, kern, (const double*)c->Q.p, (int64_t)c->ldq, c->n, c->f0,
+                               nown, V, ep));
+  } else {
+    kern<<<G, kSpmmThreads, smem, c->stream>>>(c->Q.p, c->ldq, c->n, c->f0, nown, V, ep);
+  }
   XM_CHECK_LAUNCH();
   count_launch(c);
 }
@@ -345,11 +474,29 @@ static void launch_mode(xm_ctx* c, const double* V, int r, const SpmmEpiArgs& ep
   }
 }
 
+static void launch_tcg(xm_ctx* c, const double* V, int r, const SpmmEpiArgs& ep) {
+  switch (r) {
+#define XM_R(RR) case RR: launch_r<RR, EPI_TCG>(c, V, ep); break;
+    XM_R(1) XM_R(2) XM_R(3) XM_R(4) XM_R(5) XM_R(6)
+#undef XM_R
+    default: throw Error(XM_EINVAL, "fused tCG supports r ≤ 6");
+  }
+}
+
+bool tcg_fused_supported(xm_ctx* c, int r) {
+  if (c->world != 1 || r < 1 || r > 6 || spmm_sym_supported(c, r) || c->N < 1) return false;
+  const int G = spmm_grid(c, r);
+  return ceil_div(c->N, G) <= kSpmmThreads;
+}
+
 // Algorithmic bytes of one product: Q (full rows, or the lower triangle when
-// the symmetric kernel runs) + V in + result out.
-static double alg_bytes(xm_ctx* c, int r) {
+// the symmetric kernel runs) + V in + result out.  The fused tCG iteration
+// (EPI_TCG) instead moves Q + δ, then per camera reads Y, η, Hη, r, δ and
+// writes η, Hη, r, δ (+ Λ): 8·n·n + 9·8·n·r + 48·N.
+static double alg_bytes(xm_ctx* c, int r, int mode) {
   const double n = c->n;
   const double qb = spmm_sym_supported(c, r) ? 8.0 * n * (n + 1) / 2 : 8.0 * (double)c->nrows * n;
+  if (mode == EPI_TCG) return qb + 9.0 * 8.0 * n * r + 48.0 * c->N;
   return qb + 8.0 * n * r + 8.0 * (double)c->nrows * r;
 }
 
@@ -370,7 +517,7 @@ void spmm(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep_in)
     XM_CUDA(cudaEventCreate(&e1));
     g->ev.push_back(e0);
     g->ev.push_back(e1);
-    g->bytes.push_back(alg_bytes(c, r));
+    g->bytes.push_back(alg_bytes(c, r, mode));
     ep.exec = g->execf.p + pair;
     // External ⇒ captured as an event-record node (plain records are capture markers)
     XM_CUDA(cudaEventRecordWithFlags(e0, c->stream, cudaEventRecordExternal));
@@ -390,7 +537,7 @@ void spmm(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep_in)
     e1 = c->ev_pool[c->ev_used++];
     size_t pair = c->ev_used / 2 - 1;
     ep.exec = c->ev_exec.p + pair;
-    c->ev_bytes[pair] = alg_bytes(c, r);
+    c->ev_bytes[pair] = alg_bytes(c, r, mode);
     XM_CUDA(cudaEventRecord(e0, c->stream));
   }
   if (spmm_sym_supported(c, r)) {
@@ -401,6 +548,7 @@ void spmm(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep_in)
     case EPI_ZMUL: launch_mode<EPI_ZMUL>(c, V, r, ep); break;
     case EPI_DF: launch_mode<EPI_DF>(c, V, r, ep); break;
     case EPI_GRAD: launch_mode<EPI_GRAD>(c, V, r, ep); break;
+    case EPI_TCG: launch_tcg(c, V, r, ep); break;
     default: throw Error(XM_EINVAL, "bad epilogue");
   }
   if (timed) {

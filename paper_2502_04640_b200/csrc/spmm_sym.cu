@@ -210,31 +210,6 @@ struct SymCfg {
                                   4 * (size_t)BC * R * 8 + 64 * 8;
 };
 
-// Sense-reversing software grid barrier.  Valid because the G CTAs of
-// k_spmm_sym are all co-resident (one per SM, G ≤ #SMs, checked on the host)
-// and the library issues its kernels on a single stream.
-struct GridBar {
-  int count;
-  int sense;
-};
-__device__ __forceinline__ void grid_barrier(GridBar* gb, int G) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile int* vs = &gb->sense;
-    const int s = *vs;
-    __threadfence();
-    if (atomicAdd(&gb->count, 1) == G - 1) {
-      gb->count = 0;
-      __threadfence();
-      atomicExch(&gb->sense, s ^ 1);
-    } else {
-      while (*vs == s) __nanosleep(32);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
 template <int R, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
     const __grid_constant__ CUtensorMap tmq, int N, int n, int TRb, int U,

@@ -243,7 +243,11 @@ void dgemm(xm_ctx* c, bool ta, bool tb, bool lower, int M, int N, int K, double 
 void mirror_lower(xm_ctx* c, double* Q, int n, int64_t ldq);
 
 // ------------------------------------------------------------ SpMM (spmm.cu)
-enum { EPI_STORE = 0, EPI_HVP = 1, EPI_ZMUL = 2, EPI_DF = 3, EPI_GRAD = 4 };
+enum { EPI_STORE = 0, EPI_HVP = 1, EPI_ZMUL = 2, EPI_DF = 3, EPI_GRAD = 4, EPI_TCG = 5 };
+struct GridBar {  // sense-reversing software grid barrier state (frame_ops.cuh)
+  int count;
+  int sense;
+};
 struct SpmmEpiArgs {
   double* out = nullptr;         // STORE / ZMUL (Zv) / DF (QD) / GRAD (QY): full-layout rows
   double* out2 = nullptr;        // HVP: Hv;  GRAD: grad
@@ -254,9 +258,18 @@ struct SpmmEpiArgs {
   double* partials = nullptr;    // per-CTA scalar partials [G][NC]
   const int* stop = nullptr;     // no-op when *stop != 0
   int* exec = nullptr;           // profiling: set to 1 when the kernel ran
+  // EPI_TCG (one fused Steihaug–Toint iteration, world == 1): V = δ (updated
+  // in place), partials = ⟨δ,Hδ⟩ per CTA, p2 = ‖r‖² per CTA, st = state
+  TcgState* st = nullptr;
+  double* eta = nullptr;
+  double* Heta = nullptr;
+  double* res = nullptr;
+  double* p2 = nullptr;
+  GridBar* gbar = nullptr;
 };
 int spmm_grid(xm_ctx* c, int r);  // number of scalar partials written by spmm()
 bool spmm_sym_supported(xm_ctx* c, int r);
+bool tcg_fused_supported(xm_ctx* c, int r);  // one-launch tCG iteration (EPI_TCG)
 int spmm_sym_partials(xm_ctx* c);
 void spmm_sym_launch(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep);
 void spmm(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep);
