@@ -484,7 +484,8 @@ static void launch_tcg(xm_ctx* c, const double* V, int r, const SpmmEpiArgs& ep)
 }
 
 bool tcg_fused_supported(xm_ctx* c, int r) {
-  if (c->world != 1 || r < 1 || r > 6 || spmm_sym_supported(c, r) || c->N < 1) return false;
+  if (!c->fused_tcg || c->world != 1 || r < 1 || r > 6 || spmm_sym_supported(c, r) || c->N < 1)
+    return false;
   const int G = spmm_grid(c, r);
   return ceil_div(c->N, G) <= kSpmmThreads;
 }

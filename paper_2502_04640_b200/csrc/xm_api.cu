@@ -208,6 +208,28 @@ void harvest_graph(xm_ctx* c, xm_ctx::TcgGraph& g) {
   }
 }
 
+// XM_PHASES diagnostics: lap(k) adds the time since the previous lap to slot k.
+struct PhaseClock {
+  xm_ctx* c;
+  double t = 0.0;
+  explicit PhaseClock(xm_ctx* cc) : c(cc) {
+    if (c->phases_on) {
+      sync(c);
+      t = now_ms();
+    }
+  }
+  void lap(int k) {
+    if (!c->phases_on) return;
+    sync(c);
+    const double n = now_ms();
+    c->phase_ms[k] += n - t;
+    c->phase_n[k]++;
+    t = n;
+  }
+};
+static const char* kPhaseNames[8] = {"tcg", "retract+df", "accept+grad", "eval_point",
+                                     "certify", "escape", "init", "other"};
+
 struct RtrOut {
   bool converged = false;
   int64_t outer = 0;
@@ -224,7 +246,9 @@ RtrOut rtr(xm_ctx* c, double tol_abs) {
   double Delta = Delta0;
   RtrOut out;
   double f, g2, amin;
+  PhaseClock pc(c);
   eval_point(c, &f, &g2, &amin);
+  pc.lap(3);
   int64_t accepts = 0;
   int64_t it = 0;
   const double eps = 2.220446049250313e-16;
@@ -252,6 +276,7 @@ RtrOut rtr(xm_ctx* c, double tol_abs) {
       if (hs.stop) break;
     }
     c->info.hvps += hs.n_hvp;
+    pc.lap(0);
     // ---- retraction (+ ⟨g,η⟩, ⟨η,Hη⟩) and cancellation-free Δf (reading C21)
     XM_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int), c->stream));
     const int nb = frame_blocks(c);
@@ -266,6 +291,7 @@ RtrOut rtr(xm_ctx* c, double tol_abs) {
     XM_CUDA(cudaMemcpyAsync(&rerr, c->flags.p, 4, cudaMemcpyDeviceToHost, c->stream));
     sync(c);
     if (rerr) throw Error(XM_ERETRACT, "retraction failure");
+    pc.lap(1);
     const double df = 2.0 * d[0] + d[1];
     const double model_dec = -d[2] - 0.5 * d[3];
     const double reg = std::max(1.0, std::fabs(f)) * eps * 1e3;
@@ -288,9 +314,11 @@ RtrOut rtr(xm_ctx* c, double tol_abs) {
       g2 = h[1];
       amin = h[2];
     }
+    pc.lap(2);
   }
   // fresh Q·Y before any certificate (O4)
   eval_point(c, &f, &g2, &amin);
+  pc.lap(3);
   out.outer = it;
   out.f = f;
   out.g2 = g2;
@@ -458,6 +486,8 @@ xm_status xm_create(xm_ctx** out, int device, int rank, int world, const void* n
   // A/B switches for measurements (the defaults are the production path)
   if (std::getenv("XM_NO_SYM")) c->opt.spmm_kernel = 1;
   if (std::getenv("XM_FORCE_SYM")) c->opt.spmm_kernel = 2;
+  if (std::getenv("XM_PHASES")) c->phases_on = true;
+  if (std::getenv("XM_NO_FUSED_TCG")) c->fused_tcg = false;
   if (std::getenv("XM_NO_GRAPHS")) c->use_graphs = false;
   if (c->opt.rank_cap > XM_MAX_R) c->opt.rank_cap = XM_MAX_R;
   xm_status st = guard(c, [&] {
@@ -577,10 +607,20 @@ xm_status xm_solve(xm_ctx* c, int32_t r0, double tol, xm_solve_info* info) {
     while (true) {
       ro = rtr(c, tol_abs);
       int steps = 0;
+      PhaseClock pc(c);
       certify_current(c, &lam, &steps);
+      pc.lap(4);
       certified = ro.converged && c->cert_lower >= -c->opt.cert_tol * std::max(1.0, c->normQ);
       if (certified || !ro.converged || c->r >= c->opt.rank_cap) break;
       escape(c);
+      pc.lap(5);
+    }
+    if (c->phases_on) {
+      for (int k = 0; k < 8; ++k)
+        if (c->phase_n[k])
+          fprintf(stderr, "[xm phases] %-12s %9.3f ms  (%lld laps)\n", kPhaseNames[k], c->phase_ms[k],
+                  c->phase_n[k]);
+      for (int k = 0; k < 8; ++k) c->phase_ms[k] = 0.0, c->phase_n[k] = 0;
     }
     c->info.f = ro.f;
     c->info.grad_norm = std::sqrt(ro.g2);

@@ -190,6 +190,11 @@ struct xm_ctx {
   cudaStream_t cap_stream = nullptr;
   bool use_graphs = true;
   xm::DBuf<double> sym_part;       // per-unit row / column partials of the symmetric SpMM
+  // XM_PHASES=1: host wall-clock breakdown of xm_solve (synchronises; diagnostics only)
+  bool phases_on = false;
+  bool fused_tcg = true;  // XM_NO_FUSED_TCG=1: three-kernel tCG iteration (A/B measurement)
+  double phase_ms[8] = {0};
+  long long phase_n[8] = {0};
   xm::DBuf<int> gbar;              // software grid-barrier state of the symmetric SpMM
   // named scratch buffers that persist across calls (grow-only): no cudaMalloc /
   // cudaFree churn (each cudaFree synchronises the device) inside build / solve
