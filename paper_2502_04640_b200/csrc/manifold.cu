@@ -451,6 +451,13 @@ void tcg_iteration(xm_ctx* c, int r) {
     ep.res = c->res.p;
     ep.p2 = c->part2.p;
     ep.gbar = reinterpret_cast<GridBar*>(c->gbar.p);
+    if (c->phases_on) {
+      if (!c->tdbg.p) {
+        c->tdbg.alloc(148 * 8);
+        XM_CUDA(cudaMemsetAsync(c->tdbg.p, 0, 148 * 8 * 8, c->stream));
+      }
+      ep.dbg = c->tdbg.p;
+    }
     spmm(c, c->dir.p, r, EPI_TCG, ep);
     return;
   }

@@ -37,6 +37,14 @@ constexpr int kSpmmThreads = 32 * (kConsumerWarps + 1);  // + 1 producer warp
 constexpr int kTileRows = 8;
 constexpr int kTileCols = 64 * kConsumerWarps;  // 512 columns per tile
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define XM_STAMP(k) \
+  if (ep.dbg && threadIdx.x == 0) ep.dbg[blockIdx.x * 8 + (k)] = gtimer();
+
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
 }
@@ -127,7 +135,9 @@ __device__ __forceinline__ void tcg_tail(const double* __restrict__ acc, int nf,
   }
   const double pc = block_sum_fixed<NT>(part);
   if (t == 0) ep.partials[blockIdx.x] = pc;
+  XM_STAMP(2);
   grid_barrier(ep.gbar, gridDim.x);
+  XM_STAMP(3);
   // ---- α, e_Pe′, boundary / τ  (k_tcg_update)
   TcgState s = s0;
   const double dHd = block_sum_partials<NT>(ep.partials, gridDim.x);
@@ -173,7 +183,9 @@ __device__ __forceinline__ void tcg_tail(const double* __restrict__ acc, int nf,
   }
   const double pr = block_sum_fixed<NT>(rn2);
   if (t == 0) ep.p2[blockIdx.x] = pr;
+  XM_STAMP(4);
   grid_barrier(ep.gbar, gridDim.x);
+  XM_STAMP(5);
   // ---- stop tests, β, recurrences  (k_tcg_dir)
   const double z = block_sum_partials<NT>(ep.p2, gridDim.x);
   s.e_Pe = s.e_Pe_new;
@@ -195,6 +207,7 @@ __device__ __forceinline__ void tcg_tail(const double* __restrict__ acc, int nf,
 #pragma unroll
     for (int cc = 0; cc < R; ++cc) dv.v[p][cc] = fma(s.beta, dv.v[p][cc], -rr.v[p][cc]);
   store_blk<R>(dir, i, dv);  // δ ← −r + βδ (own cameras; every CTA is past its Q·δ)
+  XM_STAMP(6);
 }
 
 template <int R, int MODE>
@@ -224,6 +237,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(
   for (int t = threadIdx.x; t < nrow * R; t += kSpmmThreads) acc[t] = 0.0;
   __shared__ TcgState ts0;  // EPI_TCG: the iteration's starting state (read before any write)
   if (MODE == EPI_TCG && threadIdx.x == 0) ts0 = *ep.st;
+  if (MODE == EPI_TCG) XM_STAMP(0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
@@ -340,6 +354,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(
     return;
   }
   if constexpr (MODE == EPI_TCG) {
+    XM_STAMP(1);
     tcg_tail<R>(acc, fb - fa, f0g, ep, ts0);
     return;
   }

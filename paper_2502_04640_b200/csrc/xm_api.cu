@@ -9,6 +9,8 @@
 // iterations in batches and synchronises once per batch.
 #include "xm_internal.cuh"
 
+#include <algorithm>
+
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -621,6 +623,24 @@ xm_status xm_solve(xm_ctx* c, int32_t r0, double tol, xm_solve_info* info) {
           fprintf(stderr, "[xm phases] %-12s %9.3f ms  (%lld laps)\n", kPhaseNames[k], c->phase_ms[k],
                   c->phase_n[k]);
       for (int k = 0; k < 8; ++k) c->phase_ms[k] = 0.0, c->phase_n[k] = 0;
+      if (c->tdbg.p) {  // stamps of the last fused tCG iteration that ran to its end
+        std::vector<unsigned long long> h(148 * 8);
+        XM_CUDA(cudaMemcpy(h.data(), c->tdbg.p, h.size() * 8, cudaMemcpyDeviceToHost));
+        const int G = std::min(148, c->N);
+        unsigned long long t0 = ~0ull;
+        for (int b = 0; b < G; ++b) t0 = std::min(t0, h[b * 8]);
+        const char* nm[7] = {"start", "loop end", "pre-bar1", "post-bar1", "pre-bar2", "post-bar2",
+                             "end"};
+        for (int k = 0; k < 7; ++k) {
+          std::vector<double> v;
+          for (int b = 0; b < G; ++b)
+            if (h[b * 8 + k]) v.push_back((h[b * 8 + k] - t0) * 1e-3);
+          if (v.empty()) continue;
+          std::sort(v.begin(), v.end());
+          fprintf(stderr, "[xm fused tCG] %-9s min %7.2f  med %7.2f  max %7.2f us\n", nm[k], v.front(),
+                  v[v.size() / 2], v.back());
+        }
+      }
     }
     c->info.f = ro.f;
     c->info.grad_norm = std::sqrt(ro.g2);

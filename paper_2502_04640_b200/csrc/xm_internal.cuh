@@ -192,7 +192,8 @@ struct xm_ctx {
   xm::DBuf<double> sym_part;       // per-unit row / column partials of the symmetric SpMM
   // XM_PHASES=1: host wall-clock breakdown of xm_solve (synchronises; diagnostics only)
   bool phases_on = false;
-  bool fused_tcg = true;  // XM_NO_FUSED_TCG=1: three-kernel tCG iteration (A/B measurement)
+  bool fused_tcg = true;
+  xm::DBuf<unsigned long long> tdbg;  // XM_PHASES: fused-tCG phase stamps  // XM_NO_FUSED_TCG=1: three-kernel tCG iteration (A/B measurement)
   double phase_ms[8] = {0};
   long long phase_n[8] = {0};
   xm::DBuf<int> gbar;              // software grid-barrier state of the symmetric SpMM
@@ -271,6 +272,7 @@ struct SpmmEpiArgs {
   double* res = nullptr;
   double* p2 = nullptr;
   GridBar* gbar = nullptr;
+  unsigned long long* dbg = nullptr;  // XM_PHASES: per-CTA %globaltimer stamps [G][8]
 };
 int spmm_grid(xm_ctx* c, int r);  // number of scalar partials written by spmm()
 bool spmm_sym_supported(xm_ctx* c, int r);
