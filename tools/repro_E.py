@@ -12,7 +12,7 @@ for kv in sys.argv[3:]:
     ov[k] = float(v) if "." in v or "e" in v else int(v)
 sc = config_scene(cfg, **ov)
 print(cfg, sc.N, sc.M, sc.E, flush=True)
-with xm.Context(profile=1) as ctx:
+with xm.Context(profile=int(os.environ.get("XM_PROFILE", "1"))) as ctx:
     for k, op in enumerate(seq):
         t = time.time()
         try:
