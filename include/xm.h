@@ -224,6 +224,11 @@ xm_status xm_get_factor(xm_ctx* ctx, double* Y, int32_t* r);
 xm_status xm_set_factor(xm_ctx* ctx, const double* Y, int32_t r);
 xm_status xm_get_stats(xm_ctx* ctx, xm_stats* out);
 xm_status xm_reset_stats(xm_ctx* ctx);
+/* Switch per-launch CUDA-event timing of the Q·V kernels (xm_options.profile)
+ * on or off for subsequent calls.  Event records inside the CUDA graphs cost
+ * a few µs per launch, so timed runs that report the solve time keep it off
+ * and a separate profiled run supplies the kernel timings. */
+xm_status xm_set_profile(xm_ctx* ctx, int32_t on);
 /* Human-readable detail of the last failed call on this context ("" if none;
  * the pointer stays valid until the next call). */
 const char* xm_last_error(xm_ctx* ctx);

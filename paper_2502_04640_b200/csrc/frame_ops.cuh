@@ -184,6 +184,23 @@ __device__ __forceinline__ void grid_barrier(GridBar* gb, int G) {
   __syncthreads();
 }
 
+// Grid barrier on a monotonically increasing 64-bit arrival counter (reset
+// to 0 before a launch sequence; every barrier adds G): the last arrival
+// itself releases the others — one release-add per CTA and acquire polling of
+// one L2 line, no reset / flip round trip.  Same co-residency requirement.
+__device__ __forceinline__ void grid_sync(unsigned long long* cnt, unsigned G) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long v, cur;
+    asm volatile("atom.add.release.gpu.u64 %0, [%1], 1;" : "=l"(v) : "l"(cnt) : "memory");
+    const unsigned long long target = (v / G + 1) * G;
+    do {
+      asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(cur) : "l"(cnt) : "memory");
+    } while (cur < target);
+  }
+  __syncthreads();
+}
+
 // Fixed-order block sum for any block size NT (multiple of 32): xor-shuffle
 // tree per warp, then warp sums in warp order.  Every thread returns the same
 // value, and every block running it on the same inputs gets the same bits.

@@ -420,6 +420,8 @@ void tcg_init(xm_ctx* c, int r, double Delta) {
     c->gbar.alloc(4);
     XM_CUDA(cudaMemsetAsync(c->gbar.p, 0, 4 * sizeof(int), c->stream));
   }
+  c->gsync.alloc(4);
+  XM_CUDA(cudaMemsetAsync(c->gsync.p, 0, 4 * sizeof(unsigned long long), c->stream));
   k_tcg_init_vec<<<ceil_div(len, 256), 256, 0, c->stream>>>(len, c->grad.p, c->eta.p, c->Heta.p,
                                                            c->res.p, c->dir.p);
   XM_CHECK_LAUNCH();
@@ -451,6 +453,8 @@ void tcg_iteration(xm_ctx* c, int r) {
     ep.res = c->res.p;
     ep.p2 = c->part2.p;
     ep.gbar = reinterpret_cast<GridBar*>(c->gbar.p);
+    ep.gsync = c->gsync.p;
+    ep.out2 = c->Hdir.p;  // Q·δ rows (row-balanced producers → camera-owned consumers)
     if (c->phases_on) {
       if (!c->tdbg.p) {
         c->tdbg.alloc(148 * 8);

@@ -106,29 +106,24 @@ struct SpmmCfg {
 // Every CTA re-derives α, τ, β and the stop tests from the same partials in
 // the same order ⇒ identical decisions everywhere; CTA 0 writes the state.
 template <int R>
-__device__ __forceinline__ void tcg_tail(const double* __restrict__ acc, int nf, int f0g,
-                                         const SpmmEpiArgs& ep, const TcgState& s0) {
+__device__ __forceinline__ void tcg_tail(int nf, int f0g, const SpmmEpiArgs& ep,
+                                         const TcgState& s0, double part) {
   constexpr int NT = kSpmmThreads;
   const int t = threadIdx.x;
   const bool has = t < nf;
   const int i = f0g + t;
   double* __restrict__ dir = ep.out;
-  Blk<R> y, dv, hd, e, he, rr;
-  double part = 0.0;
+  Blk<R> y, dv, e, he, rr;
+  double L[6];
   if (has) {
-    Blk<R> qv;
-#pragma unroll
-    for (int p = 0; p < 3; ++p)
-#pragma unroll
-      for (int cc = 0; cc < R; ++cc) qv.v[p][cc] = acc[(3 * t + p) * R + cc];
     load_blk<R>(ep.Y, i, y);
     load_blk<R>(dir, i, dv);
-    double L[6];
 #pragma unroll
     for (int q = 0; q < 6; ++q) L[q] = ep.lam[6 * i + q];
-    sub_lam<R>(qv, L, dv, 2.0, 2.0, hd);  // Hδ = P(2Qδ − 2Λδ)
-    project_blk<R>(y, i == 0, hd);
-    part = dotb<R>(dv, hd);
+    // ⟨δ, Hδ⟩ = ⟨δ, 2Qδ − 2Λδ⟩ (δ tangent, P self-adjoint): camera part −2⟨δ_i, Λ_iδ_i⟩
+    Blk<R> zero{}, lamd;
+    sub_lam<R>(zero, L, dv, 0.0, 1.0, lamd);  // −Λ_iδ_i
+    part = fma(2.0, dotb<R>(dv, lamd), part);
     load_blk<R>(ep.eta, i, e);
     load_blk<R>(ep.Heta, i, he);
     load_blk<R>(ep.res, i, rr);
@@ -136,7 +131,7 @@ __device__ __forceinline__ void tcg_tail(const double* __restrict__ acc, int nf,
   const double pc = block_sum_fixed<NT>(part);
   if (t == 0) ep.partials[blockIdx.x] = pc;
   XM_STAMP(2);
-  grid_barrier(ep.gbar, gridDim.x);
+  grid_sync(ep.gsync, gridDim.x);
   XM_STAMP(3);
   // ---- α, e_Pe′, boundary / τ  (k_tcg_update)
   TcgState s = s0;
@@ -157,7 +152,16 @@ __device__ __forceinline__ void tcg_tail(const double* __restrict__ acc, int nf,
   }
   const double a = s.boundary ? s.tau : alpha;
   double rn2 = 0.0;
+  Blk<R> hd;
   if (has) {
+    Blk<R> qv;  // this camera's Q·δ rows, written by whichever CTA streamed them
+    const double* qp = ep.out2 + (int64_t)3 * i * R;
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int cc = 0; cc < R; ++cc) qv.v[p][cc] = __ldcg(qp + p * R + cc);
+    sub_lam<R>(qv, L, dv, 2.0, 2.0, hd);  // Hδ = P(2Qδ − 2Λδ)
+    project_blk<R>(y, i == 0, hd);
 #pragma unroll
     for (int p = 0; p < 3; ++p)
 #pragma unroll
@@ -184,7 +188,7 @@ __device__ __forceinline__ void tcg_tail(const double* __restrict__ acc, int nf,
   const double pr = block_sum_fixed<NT>(rn2);
   if (t == 0) ep.p2[blockIdx.x] = pr;
   XM_STAMP(4);
-  grid_barrier(ep.gbar, gridDim.x);
+  grid_sync(ep.gsync, gridDim.x);
   XM_STAMP(5);
   // ---- stop tests, β, recurrences  (k_tcg_dir)
   const double z = block_sum_partials<NT>(ep.p2, gridDim.x);
@@ -226,10 +230,15 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(
   double* acc = red + kConsumerWarps * kTileRows * R;   // [rows_cta][R]
 
   const int G = gridDim.x;
+  // cameras [fa, fb) of this CTA (epilogues); Q rows [row_base, row_base + nrow):
+  // the cameras' rows, or for EPI_TCG an even split of all rows (the camera
+  // work runs after a grid barrier, so the stream need not be frame-aligned)
   const int fa = (int)((int64_t)blockIdx.x * nframes_own / G);
   const int fb = (int)((int64_t)(blockIdx.x + 1) * nframes_own / G);
-  const int nrow = 3 * (fb - fa);
-  const int row_base = 3 * fa;  // local to this rank's Q rows
+  const int row_base = (MODE == EPI_TCG) ? (int)((int64_t)blockIdx.x * 3 * nframes_own / G) : 3 * fa;
+  const int nrow = (MODE == EPI_TCG)
+                       ? (int)((int64_t)(blockIdx.x + 1) * 3 * nframes_own / G) - row_base
+                       : 3 * (fb - fa);
   const int ngroups = (nrow + kTileRows - 1) / kTileRows;
   const int nchunks = (n + kTileCols - 1) / kTileCols;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -355,7 +364,16 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(
   }
   if constexpr (MODE == EPI_TCG) {
     XM_STAMP(1);
-    tcg_tail<R>(acc, fb - fa, f0g, ep, ts0);
+    // Q·δ rows → ep.out2 (read back by the owning cameras after the barrier),
+    // and this CTA's rows' share of ⟨δ, 2Qδ⟩
+    double part = 0.0;
+    for (int t = threadIdx.x; t < nrow * R; t += kSpmmThreads) {
+      const int64_t g = (int64_t)(f_lo_rank * 3 + row_base) * R + t;
+      const double q = acc[t];
+      ep.out2[g] = q;
+      part = fma(2.0 * q, V[g], part);
+    }
+    tcg_tail<R>(fb - fa, f0g, ep, ts0, part);
     return;
   }
   constexpr int NC = (MODE == EPI_GRAD) ? 3 : (MODE == EPI_DF ? 2 : 1);

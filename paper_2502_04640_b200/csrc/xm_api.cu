@@ -142,7 +142,7 @@ std::vector<uintptr_t> graph_signature(xm_ctx* c) {
           (uintptr_t)c->Y.p, (uintptr_t)c->dir.p, (uintptr_t)c->lam.p, (uintptr_t)c->tcg.p,
           (uintptr_t)c->part1.p, (uintptr_t)c->part2.p, (uintptr_t)c->opt.profile,
           (uintptr_t)c->f0, (uintptr_t)c->f1, (uintptr_t)c->sym_part.p, (uintptr_t)c->gbar.p,
-          (uintptr_t)c->sym_plan};
+          (uintptr_t)c->sym_plan, (uintptr_t)c->gsync.p};
 }
 
 void destroy_graph(xm_ctx::TcgGraph& g) {
@@ -867,6 +867,14 @@ xm_status xm_get_stats(xm_ctx* c, xm_stats* out) {
   return guard(c, [&] {
     harvest_events(c);
     *out = c->stats;
+  });
+}
+
+xm_status xm_set_profile(xm_ctx* c, int32_t on) {
+  if (!c) return XM_EINVAL;
+  return guard(c, [&] {
+    harvest_events(c);
+    c->opt.profile = on ? 1 : 0;  // part of the graph signature ⇒ graphs are recaptured
   });
 }
 

@@ -196,7 +196,8 @@ struct xm_ctx {
   xm::DBuf<unsigned long long> tdbg;  // XM_PHASES: fused-tCG phase stamps  // XM_NO_FUSED_TCG=1: three-kernel tCG iteration (A/B measurement)
   double phase_ms[8] = {0};
   long long phase_n[8] = {0};
-  xm::DBuf<int> gbar;              // software grid-barrier state of the symmetric SpMM
+  xm::DBuf<int> gbar;                  // software grid-barrier state of the symmetric SpMM
+  xm::DBuf<unsigned long long> gsync;  // fused tCG grid_sync counter (reset by tcg_init)
   // named scratch buffers that persist across calls (grow-only): no cudaMalloc /
   // cudaFree churn (each cudaFree synchronises the device) inside build / solve
   std::map<std::string, xm::DBuf<int32_t>> s_i32;
@@ -273,6 +274,7 @@ struct SpmmEpiArgs {
   double* p2 = nullptr;
   GridBar* gbar = nullptr;
   unsigned long long* dbg = nullptr;  // XM_PHASES: per-CTA %globaltimer stamps [G][8]
+  unsigned long long* gsync = nullptr;  // EPI_TCG: grid_sync arrival counter
 };
 int spmm_grid(xm_ctx* c, int r);  // number of scalar partials written by spmm()
 bool spmm_sym_supported(xm_ctx* c, int r);

@@ -99,6 +99,7 @@ _SIGS = {
     "xm_set_factor": (ctypes.c_int, [_P, _P, ctypes.c_int32]),
     "xm_get_stats": (ctypes.c_int, [_P, _P]),
     "xm_reset_stats": (ctypes.c_int, [_P]),
+    "xm_set_profile": (ctypes.c_int, [_P, ctypes.c_int32]),
 }
 
 _lib = None
@@ -356,6 +357,9 @@ class Context:
 
     def reset_stats(self):
         self._check(self.lib.xm_reset_stats(self.h), "xm_reset_stats")
+
+    def set_profile(self, on: bool):
+        self._check(self.lib.xm_set_profile(self.h, int(bool(on))), "xm_set_profile")
 
 
 def solve_scene(scene, device: int = 0, r0: int = 3, tol: float = 0.0, **opts):
