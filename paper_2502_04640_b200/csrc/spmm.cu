@@ -28,7 +28,7 @@
 //    (Hv = P(2Qv − 2Λv), ⟨v, Hv⟩), ZMUL (Zv = Qv − Λv, ⟨v, Zv⟩), DF (QD,
 //    ⟨QY, D⟩, ⟨D, QD⟩), GRAD (QY, Λ, grad, f, ‖g‖², min α); scalar partials per
 //    CTA, reduced in a fixed order by the consumer ⇒ deterministic.
-#include "frame_ops.cuh"
+#include "pipeline.cuh"
 
 namespace xm {
 
@@ -36,59 +36,6 @@ constexpr int kConsumerWarps = 8;
 constexpr int kSpmmThreads = 32 * (kConsumerWarps + 1);  // + 1 producer warp
 constexpr int kTileRows = 8;
 constexpr int kTileCols = 64 * kConsumerWarps;  // 512 columns per tile
-
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#define XM_STAMP(k) \
-  if (ep.dbg && threadIdx.x == 0) ep.dbg[blockIdx.x * 8 + (k)] = gtimer();
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
-  return pol;
-}
-// 1-D bulk copy global → shared, completion counted on `bar` (bytes % 16 == 0)
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes,
-                                            uint64_t* bar, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-      "[%0], [%1], %2, [%3], %4;\n" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
-}
 
 template <int R>
 struct SpmmCfg {

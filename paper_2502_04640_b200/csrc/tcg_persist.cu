@@ -1,0 +1,515 @@
+// tcg_persist.cu — H8 + H9: the whole Steihaug–Toint truncated-CG solve of
+// one trust-region step (Manopt's tCG) in ONE
+// persistent cooperative kernel, on one GPU with the full-row Q stream.
+//
+// Per iteration k (same arithmetic as k_tcg_update / k_tcg_dir, manifold.cu):
+//   stream  Qδ_k for this CTA's rows (Q tiles by TMA, δ_k built on the fly)
+//   ── grid barrier A ──  d_Hd = ⟨δ_k, Hδ_k⟩ → α, boundary / τ
+//   cameras: Hδ = P(2Qδ − 2Λδ), η += αδ, Hη += αHδ, r += αHδ (projected)
+//   ── grid barrier B ──  ‖r‖² → stop tests, β, δ_{k+1} = −r_{k+1} + βδ_k
+//
+// What the persistent form buys over one launch per iteration:
+//  * no launch, no pipeline drain / fill between iterations — the producer
+//    warp keeps prefetching the next iteration's Q tiles (Q never changes)
+//    while the consumers are in the barrier / camera phases;
+//  * no third barrier for δ: the next stream needs δ_{k+1} for ALL columns,
+//    which consumers form on the fly from r_{k+1} and δ_k tiles (TMA-loaded
+//    next to the Q tile) as −r + βδ with the same fma the owners use, so every
+//    CTA sees bitwise the same δ; owners write δ_{k+1} into the other half of
+//    a ping-pong pair for the stream after next;
+//  * camera state (Y_i, Λ_i, δ_i, r_i) stays in the owner thread's registers
+//    for the whole solve.
+// Rows are split evenly over the CTAs (the camera work follows barrier A and
+// reads Qδ rows back from L2), cameras by ⌊N·c/G⌋ (≤ 256 per CTA).
+// Determinism: fixed-order partial sums, identical decisions in every CTA.
+#include "pipeline.cuh"
+
+namespace xm {
+
+namespace {
+constexpr int kPW = 8;                  // consumer warps
+constexpr int kPC = 32 * kPW;           // consumer threads
+constexpr int kPThreads = kPC + 32;     // + one producer warp
+constexpr int kPRows = 8;               // Q rows per tile
+constexpr int kPCols = 64 * kPW;        // 512 columns per tile
+
+template <int R>
+struct PCfg {
+  static constexpr int kQBytes = kPRows * kPCols * 8;  // 32 KB
+  static constexpr int kVBytes = kPCols * R * 8;       // one chunk of r or δ
+  static constexpr int kStageBytes = kQBytes + 2 * kVBytes;
+  static constexpr int kStages = (R == 1) ? 5 : (R == 2 ? 4 : 3);
+};
+
+__device__ __forceinline__ void cbar() {  // consumers only (the producer keeps streaming)
+  asm volatile("bar.sync 1, %0;\n" ::"n"(kPC) : "memory");
+}
+// fixed-order sum over the 256 consumer threads; every consumer gets the value
+__device__ __forceinline__ double csum(double v, double* ws) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+  cbar();
+  double t = ws[0];
+#pragma unroll
+  for (int w = 1; w < kPW; ++w) t += ws[w];
+  cbar();
+  return t;
+}
+__device__ __forceinline__ double csum_partials(const double* part, int n, double* ws) {
+  double a = 0.0;
+  for (int b = threadIdx.x; b < n; b += kPC) a += __ldcg(part + b);
+  return csum(a, ws);
+}
+// grid barrier among the consumer groups of all CTAs (see grid_sync)
+__device__ __forceinline__ void cgrid_sync(unsigned long long* cnt, unsigned G) {
+  cbar();
+  if (threadIdx.x == 0) {
+    unsigned long long v, cur;
+    asm volatile("atom.add.release.gpu.u64 %0, [%1], 1;" : "=l"(v) : "l"(cnt) : "memory");
+    const unsigned long long target = (v / G + 1) * G;
+    do {
+      asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(cur) : "l"(cnt) : "memory");
+    } while (cur < target);
+  }
+  cbar();
+}
+}  // namespace
+
+__device__ __forceinline__ void tcg_final(const TcgState& s, int t, volatile int* sh_stop,
+                                          TcgState* st) {
+  if (t == 0) {
+    *sh_stop = 1;
+    if (blockIdx.x == 0) *st = s;
+  }
+}
+
+struct TcgPersistArgs {
+  const double* Q;
+  int64_t ldq;
+  int n, N;
+  TcgState* st;
+  const double* Y;
+  const double* lam;
+  double* res;                 // r_k (all rows; read by every CTA's stream)
+  double* D0;                  // δ ping-pong: δ_k in D[k & 1]; D1 = 0 on entry (δ_{−1})
+  double* D1;
+  double* eta;
+  double* Heta;
+  double* QD;                  // Qδ rows (row producers → camera owners)
+  double* pA;                  // per-CTA partials ⟨δ, Hδ⟩
+  double* pB;                  // per-CTA partials ‖r‖²
+  unsigned long long* gsync;   // grid barrier counter (0 on entry)
+};
+
+template <int R>
+__global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(TcgPersistArgs a) {
+  using Cfg = PCfg<R>;
+  constexpr int S = Cfg::kStages;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* stage_base = reinterpret_cast<double*>(smem_raw);
+  uint64_t* fullQ = reinterpret_cast<uint64_t*>(smem_raw + (size_t)S * Cfg::kStageBytes);
+  uint64_t* fullV = fullQ + S;
+  uint64_t* empty = fullV + S;
+  double* red = reinterpret_cast<double*>(empty + S);  // [warps][kPRows][R]
+  double* acc = red + kPW * kPRows * R;                // [rows of this CTA][R]
+  __shared__ TcgState ts;
+  __shared__ volatile int sh_vgen;  // streams ≤ sh_vgen may load their r / δ tiles
+  __shared__ volatile int sh_stop;
+  __shared__ double ws[kPW];
+
+  const int G = gridDim.x;
+  const int n = a.n;
+  const int row_base = (int)((int64_t)blockIdx.x * n / G);
+  const int nrow = (int)((int64_t)(blockIdx.x + 1) * n / G) - row_base;
+  const int fa = (int)((int64_t)blockIdx.x * a.N / G);
+  const int nf = (int)((int64_t)(blockIdx.x + 1) * a.N / G) - fa;
+  const int ngroups = (nrow + kPRows - 1) / kPRows;
+  const int nchunks = (n + kPCols - 1) / kPCols;
+  const int tiles = ngroups * nchunks;  // per iteration
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&fullQ[s], 1);
+      mbar_init(&fullV[s], 1);
+      mbar_init(&empty[s], kPW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    ts = *a.st;
+    sh_vgen = 0;
+    sh_stop = ts.stop != 0;
+  }
+  __syncthreads();
+  if (sh_stop) return;
+
+  if (warp == kPW) {
+    // ================================================================ producer
+    if (lane != 0) return;
+    const uint64_t pol_q = policy_evict_first();
+    const uint64_t pol_v = policy_evict_last();
+    long long iq = 0, iv = 0;  // tiles whose Q / (r, δ) copies have been issued
+    int fenced = -1;
+    while (true) {
+      bool moved = false;
+      if (iv < iq) {
+        const int kv = (int)(iv / tiles);
+        if (kv <= sh_vgen) {
+          if (kv > fenced) {
+            fence_proxy_async();  // r_k, δ_{k−1} were written by generic stores
+            fenced = kv;
+          }
+          const int s = (int)(iv % S);
+          const int j = (int)(iv % tiles) % nchunks;
+          const int k0 = j * kPCols;
+          const int klen = min(kPCols, n - k0);
+          const unsigned vb = (unsigned)(((klen * R + 1) & ~1) * 8);
+          double* st = stage_base + (size_t)s * (Cfg::kStageBytes / 8) + kPRows * kPCols;
+          const double* dprev = (kv & 1) ? a.D0 : a.D1;  // δ_{k−1} = D[(k−1) & 1]
+          mbar_expect_tx(&fullV[s], 2 * vb);
+          tma_load_1d(st, a.res + (int64_t)k0 * R, vb, &fullV[s], pol_v);
+          tma_load_1d(st + kPCols * R, dprev + (int64_t)k0 * R, vb, &fullV[s], pol_v);
+          ++iv;
+          moved = true;
+        }
+      }
+      if (sh_stop) break;
+      {
+        const int s = (int)(iq % S);
+        const unsigned ph = (unsigned)((iq / S) & 1);
+        if (iq - iv < S && mbar_test(&empty[s], ph ^ 1u)) {
+          const int t = (int)(iq % tiles);
+          const int g = t / nchunks, j = t % nchunks;
+          const int r0 = g * kPRows;
+          const int rows = min(kPRows, nrow - r0);
+          const int k0 = j * kPCols;
+          const int klen = min(kPCols, n - k0);
+          const unsigned qb = (unsigned)(((klen + 1) & ~1) * 8);
+          mbar_expect_tx(&fullQ[s], qb * rows);
+          double* st = stage_base + (size_t)s * (Cfg::kStageBytes / 8);
+          for (int q = 0; q < rows; ++q)
+            tma_load_1d(st + q * kPCols, a.Q + (int64_t)(row_base + r0 + q) * a.ldq + k0, qb,
+                        &fullQ[s], pol_q);
+          ++iq;
+          moved = true;
+        }
+      }
+      if (!moved) __nanosleep(32);
+    }
+    // in-flight Q copies of never-consumed tiles must land before the CTA exits
+    for (long long t = iv; t < iq; ++t) mbar_wait(&fullQ[t % S], (unsigned)((t / S) & 1));
+    return;
+  }
+
+  // ================================================================== consumers
+  // Camera state is (re)loaded after each stream — own rows of δ_k, r_k were
+  // written by this same thread — so no registers are held across the stream.
+  const int t = threadIdx.x;
+  const bool has = t < nf;
+  const int i = fa + t;
+  if (has) {  // δ_0 = −r_0 (= fma(0, 0, −r): the same bits the streams form)
+    Blk<R> r0b, d0b;
+    load_blk<R>(a.res, i, r0b);
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int cc = 0; cc < R; ++cc) d0b.v[p][cc] = fma(0.0, 0.0, -r0b.v[p][cc]);
+    store_blk<R>(a.D0, i, d0b);
+  }
+  double beta_prev = 0.0;  // β_{k−1}: stream k uses δ_k = −r_k + β_{k−1}δ_{k−1}
+  const int col = 64 * warp + 2 * lane;
+  long long it = 0;
+  for (int k = 0;; ++k) {
+    // ---------------------------------------------------------------- stream
+    const double* dprev_g = (k & 1) ? a.D0 : a.D1;
+    for (int g = 0; g < ngroups; ++g) {
+      const int r0 = g * kPRows;
+      const int rows = min(kPRows, nrow - r0);
+      double acc8[kPRows][R];
+#pragma unroll
+      for (int q = 0; q < kPRows; ++q)
+#pragma unroll
+        for (int cc = 0; cc < R; ++cc) acc8[q][cc] = 0.0;
+      for (int j = 0; j < nchunks; ++j, ++it) {
+        const int sidx = (int)(it % S);
+        const unsigned ph = (unsigned)((it / S) & 1);
+        mbar_wait(&fullQ[sidx], ph);
+        mbar_wait(&fullV[sidx], ph);
+        const int klen = min(kPCols, n - j * kPCols);
+        const double* stg = stage_base + (size_t)sidx * (Cfg::kStageBytes / 8);
+        const double* rs = stg + kPRows * kPCols;
+        const double* ds = rs + kPCols * R;
+        if (col + 1 < klen) {
+          double v0[R], v1[R];
+#pragma unroll
+          for (int cc = 0; cc < R; ++cc) {
+            v0[cc] = fma(beta_prev, ds[col * R + cc], -rs[col * R + cc]);
+            v1[cc] = fma(beta_prev, ds[(col + 1) * R + cc], -rs[(col + 1) * R + cc]);
+          }
+#pragma unroll
+          for (int q = 0; q < kPRows; ++q) {
+            if (q < rows) {
+              double2 qv = *reinterpret_cast<const double2*>(stg + q * kPCols + col);
+#pragma unroll
+              for (int cc = 0; cc < R; ++cc)
+                acc8[q][cc] = fma(qv.x, v0[cc], fma(qv.y, v1[cc], acc8[q][cc]));
+            }
+          }
+        } else if (col < klen) {
+          double v0[R];
+#pragma unroll
+          for (int cc = 0; cc < R; ++cc) v0[cc] = fma(beta_prev, ds[col * R + cc], -rs[col * R + cc]);
+#pragma unroll
+          for (int q = 0; q < kPRows; ++q) {
+            if (q < rows) {
+              const double qq = stg[q * kPCols + col];
+#pragma unroll
+              for (int cc = 0; cc < R; ++cc) acc8[q][cc] = fma(qq, v0[cc], acc8[q][cc]);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[sidx]);
+      }
+#pragma unroll
+      for (int q = 0; q < kPRows; ++q)
+#pragma unroll
+        for (int cc = 0; cc < R; ++cc) {
+          double v = acc8[q][cc];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          acc8[q][cc] = v;
+        }
+      if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < kPRows; ++q)
+#pragma unroll
+          for (int cc = 0; cc < R; ++cc) red[(warp * kPRows + q) * R + cc] = acc8[q][cc];
+      }
+      cbar();
+      for (int u = t; u < rows * R; u += kPC) {
+        double sum = 0.0;
+        for (int w = 0; w < kPW; ++w) sum += red[w * kPRows * R + u];
+        acc[r0 * R + u] = sum;
+      }
+      cbar();
+    }
+    // ------------------------------------------- rows → QD, ⟨δ_k, 2Qδ_k⟩ rows part
+    double part = 0.0;
+    for (int u = t; u < nrow * R; u += kPC) {
+      const int64_t gidx = (int64_t)row_base * R + u;
+      const double q = acc[u];
+      a.QD[gidx] = q;
+      const double d = fma(beta_prev, __ldcg(dprev_g + gidx), -__ldcg(a.res + gidx));  // δ_k
+      part = fma(2.0 * q, d, part);
+    }
+    TcgState s = ts;
+    Blk<R> y, dcur, rcur;
+    double L[6];
+    if (has) {  // camera part −2⟨δ_i, Λ_iδ_i⟩ (δ tangent, P self-adjoint)
+      load_blk<R>(a.Y, i, y);
+      load_blk<R>((k & 1) ? a.D1 : a.D0, i, dcur);  // δ_k = D[k & 1] (own rows)
+      load_blk<R>(a.res, i, rcur);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) L[q] = a.lam[6 * i + q];
+      Blk<R> zero{}, lamd;
+      sub_lam<R>(zero, L, dcur, 0.0, 1.0, lamd);
+      part = fma(2.0, dotb<R>(dcur, lamd), part);
+    }
+    {
+      const double pc = csum(part, ws);
+      if (t == 0) a.pA[blockIdx.x] = pc;
+    }
+    cgrid_sync(a.gsync, G);
+    // -------------------------------------------------- α, boundary / τ, update
+    const double dHd = csum_partials(a.pA, G, ws);
+    s.d_Hd = dHd;
+    s.n_hvp += 1;
+    const double alpha = (dHd != 0.0) ? s.z / dHd : INFINITY;
+    const double e_new = s.e_Pe + 2.0 * alpha * s.e_Pd + alpha * alpha * s.d_Pd;
+    const double D2 = s.Delta * s.Delta;
+    s.alpha = alpha;
+    s.e_Pe_new = e_new;
+    if (dHd <= 0.0 || e_new >= D2) {
+      s.tau = (-s.e_Pd + sqrt(s.e_Pd * s.e_Pd + s.d_Pd * (D2 - s.e_Pe))) / s.d_Pd;
+      s.boundary = 1;
+      s.stop = (dHd <= 0.0) ? TCG_NEGCURV : TCG_EXCEEDED;
+    } else {
+      s.boundary = 0;
+    }
+    const double step = s.boundary ? s.tau : alpha;
+    double rn2 = 0.0;
+    if (has) {
+      Blk<R> qv, hd, e, he;
+      const double* qp = a.QD + (int64_t)3 * i * R;
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int cc = 0; cc < R; ++cc) qv.v[p][cc] = __ldcg(qp + p * R + cc);
+      sub_lam<R>(qv, L, dcur, 2.0, 2.0, hd);  // Hδ = P(2Qδ − 2Λδ)
+      project_blk<R>(y, i == 0, hd);
+      load_blk<R>(a.eta, i, e);
+      load_blk<R>(a.Heta, i, he);
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int cc = 0; cc < R; ++cc) {
+          e.v[p][cc] = fma(step, dcur.v[p][cc], e.v[p][cc]);
+          he.v[p][cc] = fma(step, hd.v[p][cc], he.v[p][cc]);
+        }
+      store_blk<R>(a.eta, i, e);
+      store_blk<R>(a.Heta, i, he);
+      if (!s.boundary) {
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+#pragma unroll
+          for (int cc = 0; cc < R; ++cc) rcur.v[p][cc] = fma(step, hd.v[p][cc], rcur.v[p][cc]);
+        project_blk<R>(y, i == 0, rcur);
+        store_blk<R>(a.res, i, rcur);
+        rn2 = frob2<R>(rcur);
+      }
+    }
+    if (s.boundary) {
+      tcg_final(s, t, &sh_stop, a.st);
+      break;
+    }
+    {
+      const double pr = csum(rn2, ws);
+      if (t == 0) a.pB[blockIdx.x] = pr;
+    }
+    cgrid_sync(a.gsync, G);
+    // ------------------------------------------------ stop tests, β, δ_{k+1}
+    const double z = csum_partials(a.pB, G, ws);
+    s.e_Pe = s.e_Pe_new;
+    s.z_old = s.z;
+    s.z = z;
+    s.j += 1;
+    if (sqrt(z) <= s.r0 * fmin(pow(s.r0, s.theta), s.kappa)) {
+      s.stop = TCG_CONVERGED;
+    } else {
+      s.beta = s.z / s.z_old;
+      s.e_Pd = s.beta * (s.e_Pd + s.alpha * s.d_Pd);
+      s.d_Pd = s.z + s.beta * s.beta * s.d_Pd;
+      if (s.j >= s.max_inner) s.stop = TCG_MAXINNER;
+    }
+    if (s.stop) {
+      tcg_final(s, t, &sh_stop, a.st);
+      break;
+    }
+    if (has) {
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int cc = 0; cc < R; ++cc) dcur.v[p][cc] = fma(s.beta, dcur.v[p][cc], -rcur.v[p][cc]);
+      store_blk<R>((k & 1) ? a.D0 : a.D1, i, dcur);  // δ_{k+1} → D[(k+1) & 1]
+    }
+    beta_prev = s.beta;
+    cbar();  // every consumer has read ts for this iteration
+    if (t == 0) {
+      ts = s;
+      __threadfence_block();
+      sh_vgen = k + 1;  // r_{k+1} and δ_k are final everywhere (barrier B)
+    }
+  }
+  // (the break paths leave `s` in the loop scope: CTA 0 re-derives nothing —
+  // it stored the final state before breaking, see tcg_final)
+}
+
+// ---------------------------------------------------------------------- host
+namespace {
+template <int R>
+size_t persist_smem(int n, int G) {
+  using Cfg = PCfg<R>;
+  const int rows_max = ceil_div(n, G) + 1;
+  return (size_t)Cfg::kStages * Cfg::kStageBytes + 3 * Cfg::kStages * 8 +
+         (size_t)kPW * kPRows * R * 8 + (size_t)rows_max * R * 8;
+}
+size_t persist_smem_r(int r, int n, int G) {
+  switch (r) {
+    case 1: return persist_smem<1>(n, G);
+    case 2: return persist_smem<2>(n, G);
+    case 3: return persist_smem<3>(n, G);
+    case 4: return persist_smem<4>(n, G);
+    case 5: return persist_smem<5>(n, G);
+    default: return ~(size_t)0;
+  }
+}
+constexpr size_t kSmemCap = 227 * 1024 - 1024;  // dynamic budget (static smem ≈ 0.3 KB)
+}  // namespace
+
+bool tcg_persist_supported(xm_ctx* c, int r) {
+  if (!c->fused_tcg || !c->persist_tcg || c->world != 1 || r < 1 || r > 5 ||
+      spmm_sym_supported(c, r) || c->N < 1)
+    return false;
+  const int G = std::min(148, c->N);
+  return ceil_div(c->N, G) <= kPC && persist_smem_r(r, c->n, G) <= kSmemCap;
+}
+
+template <int R>
+static void launch_persist(xm_ctx* c) {
+  const int G = std::min(148, c->N);
+  const size_t smem = persist_smem<R>(c->n, G);
+  if (smem > kSmemCap) throw Error(XM_EINVAL, "persistent tCG shared memory plan exceeds 227 KB");
+  static size_t attr = 0;
+  if (smem > attr) {
+    XM_CUDA(cudaFuncSetAttribute(k_tcg_persist<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    attr = smem;
+  }
+  TcgPersistArgs a{};
+  a.Q = c->Q.p;
+  a.ldq = c->ldq;
+  a.n = c->n;
+  a.N = c->N;
+  a.st = c->tcg.p;
+  a.Y = c->Y.p;
+  a.lam = c->lam.p;
+  a.res = c->res.p;
+  a.D0 = c->dir.p;
+  a.D1 = c->dir2.p;
+  a.eta = c->eta.p;
+  a.Heta = c->Heta.p;
+  a.QD = c->Hdir.p;
+  a.pA = c->part1.p;
+  a.pB = c->part2.p;
+  a.gsync = c->gsync.p;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(kPThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  XM_CUDA(cudaLaunchKernelEx(&cfg, k_tcg_persist<R>, a));
+  XM_CHECK_LAUNCH();
+  count_launch(c);
+}
+
+// Whole tCG solve (state already initialised by tcg_init); returns after the
+// kernel is enqueued.  Algorithmic bytes per iteration for the roofline:
+// Q (8·n·n) + the r and δ tiles every CTA streams (2·8·n·r per CTA row group,
+// from L2) are not HBM-unique; we count Q + one pass over r, δ, QD, η, Hη, Y
+// (8·n·r each, ≈ 9·8·n·r with reads + writes) + Λ (48·N).
+double tcg_persist_bytes_per_iter(xm_ctx* c, int r) {
+  const double n = c->n;
+  return 8.0 * n * n + 9.0 * 8.0 * n * r + 48.0 * c->N;
+}
+
+void tcg_persist_launch(xm_ctx* c, int r) {
+  const int64_t len = (int64_t)c->n * r;
+  c->dir2.alloc((size_t)len + 64);
+  XM_CUDA(cudaMemsetAsync(c->dir2.p, 0, len * 8, c->stream));  // δ_{−1} = 0
+  switch (r) {
+    case 1: launch_persist<1>(c); break;
+    case 2: launch_persist<2>(c); break;
+    case 3: launch_persist<3>(c); break;
+    case 4: launch_persist<4>(c); break;
+    case 5: launch_persist<5>(c); break;
+    default: throw Error(XM_EINVAL, "persistent tCG supports r ≤ 5");
+  }
+}
+
+}  // namespace xm

@@ -263,8 +263,29 @@ RtrOut rtr(xm_ctx* c, double tol_abs) {
     // ---- tCG (device-resident, double-buffered state; 3 kernels / iteration)
     tcg_init(c, r, Delta);
     TcgState hs{};
-    xm_ctx::TcgGraph* g = c->use_graphs && c->world == 1 ? tcg_graph(c, r) : nullptr;
-    while (true) {
+    const bool persist = tcg_persist_supported(c, r);
+    xm_ctx::TcgGraph* g = !persist && c->use_graphs && c->world == 1 ? tcg_graph(c, r) : nullptr;
+    if (persist) {  // the whole tCG loop in one cooperative launch (tcg_persist.cu)
+      const bool timed = c->opt.profile != 0;
+      if (timed && !c->ev_persist[0]) {
+        XM_CUDA(cudaEventCreate(&c->ev_persist[0]));
+        XM_CUDA(cudaEventCreate(&c->ev_persist[1]));
+      }
+      if (timed) XM_CUDA(cudaEventRecord(c->ev_persist[0], c->stream));
+      tcg_persist_launch(c, r);
+      if (timed) XM_CUDA(cudaEventRecord(c->ev_persist[1], c->stream));
+      XM_CUDA(cudaMemcpyAsync(&hs, c->tcg.p, sizeof(TcgState), cudaMemcpyDeviceToHost, c->stream));
+      sync(c);
+      c->stats.spmm_calls += hs.n_hvp;
+      if (timed && hs.n_hvp > 0) {  // per-iteration figures: one Q stream per iteration
+        float ms = 0.f;
+        XM_CUDA(cudaEventElapsedTime(&ms, c->ev_persist[0], c->ev_persist[1]));
+        c->stats.spmm_ms += ms;
+        c->stats.spmm_timed += hs.n_hvp;
+        c->stats.spmm_alg_bytes += hs.n_hvp * tcg_persist_bytes_per_iter(c, r);
+      }
+    }
+    while (!persist) {
       if (g) {
         XM_CUDA(cudaGraphLaunch(g->exec, c->stream));
         c->stats.kernel_launches += g->launches;
@@ -490,6 +511,7 @@ xm_status xm_create(xm_ctx** out, int device, int rank, int world, const void* n
   if (std::getenv("XM_FORCE_SYM")) c->opt.spmm_kernel = 2;
   if (std::getenv("XM_PHASES")) c->phases_on = true;
   if (std::getenv("XM_NO_FUSED_TCG")) c->fused_tcg = false;
+  if (std::getenv("XM_NO_PERSIST_TCG")) c->persist_tcg = false;
   if (std::getenv("XM_NO_GRAPHS")) c->use_graphs = false;
   if (c->opt.rank_cap > XM_MAX_R) c->opt.rank_cap = XM_MAX_R;
   xm_status st = guard(c, [&] {
@@ -514,6 +536,8 @@ void xm_destroy(xm_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->ev_persist)
+    if (e) cudaEventDestroy(e);
   destroy_graphs(c);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   nccl_destroy(c);

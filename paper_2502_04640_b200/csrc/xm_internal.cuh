@@ -192,8 +192,11 @@ struct xm_ctx {
   xm::DBuf<double> sym_part;       // per-unit row / column partials of the symmetric SpMM
   // XM_PHASES=1: host wall-clock breakdown of xm_solve (synchronises; diagnostics only)
   bool phases_on = false;
-  bool fused_tcg = true;
-  xm::DBuf<unsigned long long> tdbg;  // XM_PHASES: fused-tCG phase stamps  // XM_NO_FUSED_TCG=1: three-kernel tCG iteration (A/B measurement)
+  bool fused_tcg = true;    // XM_NO_FUSED_TCG=1: three-kernel tCG iteration (A/B measurement)
+  bool persist_tcg = true;  // XM_NO_PERSIST_TCG=1: one launch per tCG iteration instead
+  xm::DBuf<double> dir2;    // δ ping-pong partner of dir (persistent tCG)
+  cudaEvent_t ev_persist[2] = {nullptr, nullptr};
+  xm::DBuf<unsigned long long> tdbg;  // XM_PHASES: fused-tCG phase stamps
   double phase_ms[8] = {0};
   long long phase_n[8] = {0};
   xm::DBuf<int> gbar;                  // software grid-barrier state of the symmetric SpMM
@@ -279,6 +282,9 @@ struct SpmmEpiArgs {
 int spmm_grid(xm_ctx* c, int r);  // number of scalar partials written by spmm()
 bool spmm_sym_supported(xm_ctx* c, int r);
 bool tcg_fused_supported(xm_ctx* c, int r);  // one-launch tCG iteration (EPI_TCG)
+bool tcg_persist_supported(xm_ctx* c, int r);  // whole tCG solve in one launch
+void tcg_persist_launch(xm_ctx* c, int r);
+double tcg_persist_bytes_per_iter(xm_ctx* c, int r);
 int spmm_sym_partials(xm_ctx* c);
 void spmm_sym_launch(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep);
 void spmm(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep);
