@@ -36,6 +36,10 @@ constexpr int kConsumerWarps = 8;
 constexpr int kSpmmThreads = 32 * (kConsumerWarps + 1);  // + 1 producer warp
 constexpr int kTileRows = 8;
 constexpr int kTileCols = 64 * kConsumerWarps;  // 512 columns per tile
+#ifndef XM_SPMM_PREFETCH
+#define XM_SPMM_PREFETCH 4
+#endif
+constexpr int kSpmmPrefetch = XM_SPMM_PREFETCH;  // L2 prefetch distance (tiles)
 
 template <int R>
 struct SpmmCfg {
@@ -208,6 +212,18 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(
     if (lane == 0) {
       const uint64_t pol_q = policy_evict_first();
       const uint64_t pol_v = policy_evict_last();
+      // L2 prefetch kSpmmPrefetch tiles ahead of the smem ring: more HBM
+      // requests in flight than the ring's S × 32 KB
+      auto prefetch_tile = [&](int tp) {
+        if (tp >= ngroups * nchunks) return;
+        const int gp = tp / nchunks, jp = tp % nchunks;
+        const int rp0 = gp * kTileRows, rowsp = min(kTileRows, nrow - rp0);
+        const int kp0 = jp * kTileCols, klenp = min(kTileCols, n - kp0);
+        for (int q = 0; q < rowsp; ++q)
+          prefetch_l2(Q + (int64_t)(row_base + rp0 + q) * ldq + kp0,
+                      (unsigned)(((klenp + 1) & ~1) * 8));
+      };
+      for (int tp = 0; tp < kSpmmPrefetch; ++tp) prefetch_tile(tp);
       int it = 0;
       for (int g = 0; g < ngroups; ++g) {
         const int r0 = g * kTileRows;
@@ -226,6 +242,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(
             tma_load_1d(st + q * kTileCols, Q + (int64_t)(row_base + r0 + q) * ldq + k0, qb,
                         &full[s], pol_q);
           tma_load_1d(st + kTileRows * kTileCols, V + (int64_t)k0 * R, vb, &full[s], pol_v);
+          prefetch_tile(it + kSpmmPrefetch);
         }
       }
     }

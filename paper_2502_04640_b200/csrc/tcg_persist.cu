@@ -32,6 +32,7 @@ constexpr int kPC = 32 * kPW;           // consumer threads
 constexpr int kPThreads = kPC + 32;     // + one producer warp
 constexpr int kPRows = 8;               // Q rows per tile
 constexpr int kPCols = 64 * kPW;        // 512 columns per tile
+constexpr int kPrefetch = 6;            // L2 prefetch distance in tiles (≈ 6 × 32 KB per SM)
 
 template <int R>
 struct PCfg {
@@ -150,6 +151,14 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(TcgPersistArgs a) 
     const uint64_t pol_v = policy_evict_last();
     long long iq = 0, iv = 0;  // tiles whose Q / (r, δ) copies have been issued
     int fenced = -1;
+    for (int tp = 0; tp < min(kPrefetch, tiles); ++tp) {  // warm L2 for the first tiles
+      const int gp = tp / nchunks, jp = tp % nchunks;
+      const int rp0 = gp * kPRows, rowsp = min(kPRows, nrow - rp0);
+      const int kp0 = jp * kPCols, klenp = min(kPCols, n - kp0);
+      for (int q = 0; q < rowsp; ++q)
+        prefetch_l2(a.Q + (int64_t)(row_base + rp0 + q) * a.ldq + kp0,
+                    (unsigned)(((klenp + 1) & ~1) * 8));
+    }
     while (true) {
       bool moved = false;
       if (iv < iq) {
@@ -190,6 +199,15 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(TcgPersistArgs a) 
           for (int q = 0; q < rows; ++q)
             tma_load_1d(st + q * kPCols, a.Q + (int64_t)(row_base + r0 + q) * a.ldq + k0, qb,
                         &fullQ[s], pol_q);
+          {  // L2 prefetch kPrefetch tiles ahead (wrapping into the next iteration's Q)
+            const int tp = (int)((iq + kPrefetch) % tiles);
+            const int gp = tp / nchunks, jp = tp % nchunks;
+            const int rp0 = gp * kPRows, rowsp = min(kPRows, nrow - rp0);
+            const int kp0 = jp * kPCols, klenp = min(kPCols, n - kp0);
+            const unsigned qbp = (unsigned)(((klenp + 1) & ~1) * 8);
+            for (int q = 0; q < rowsp; ++q)
+              prefetch_l2(a.Q + (int64_t)(row_base + rp0 + q) * a.ldq + kp0, qbp);
+          }
           ++iq;
           moved = true;
         }
