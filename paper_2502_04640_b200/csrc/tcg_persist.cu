@@ -100,6 +100,7 @@ struct TcgPersistArgs {
   double* pA;                  // per-CTA partials ⟨δ, Hδ⟩
   double* pB;                  // per-CTA partials ‖r‖²
   unsigned long long* gsync;   // grid barrier counter (0 on entry)
+  unsigned long long* dbg;     // XM_PHASES: %globaltimer stamps [G][8] of iteration 1
 };
 
 template <int R>
@@ -235,7 +236,10 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(TcgPersistArgs a) 
   double beta_prev = 0.0;  // β_{k−1}: stream k uses δ_k = −r_k + β_{k−1}δ_{k−1}
   const int col = 64 * warp + 2 * lane;
   long long it = 0;
+#define XM_PSTAMP(q) \
+  if (a.dbg && k == 1 && t == 0) a.dbg[blockIdx.x * 8 + (q)] = gtimer();
   for (int k = 0;; ++k) {
+    XM_PSTAMP(0);
     // ---------------------------------------------------------------- stream
     const double* dprev_g = (k & 1) ? a.D0 : a.D1;
     for (int g = 0; g < ngroups; ++g) {
@@ -310,6 +314,7 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(TcgPersistArgs a) 
       }
       cbar();
     }
+    XM_PSTAMP(1);
     // ------------------------------------------- rows → QD, ⟨δ_k, 2Qδ_k⟩ rows part
     double part = 0.0;
     for (int u = t; u < nrow * R; u += kPC) {
@@ -336,7 +341,9 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(TcgPersistArgs a) 
       const double pc = csum(part, ws);
       if (t == 0) a.pA[blockIdx.x] = pc;
     }
+    XM_PSTAMP(2);
     cgrid_sync(a.gsync, G);
+    XM_PSTAMP(3);
     // -------------------------------------------------- α, boundary / τ, update
     const double dHd = csum_partials(a.pA, G, ws);
     s.d_Hd = dHd;
@@ -393,7 +400,9 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(TcgPersistArgs a) 
       const double pr = csum(rn2, ws);
       if (t == 0) a.pB[blockIdx.x] = pr;
     }
+    XM_PSTAMP(4);
     cgrid_sync(a.gsync, G);
+    XM_PSTAMP(5);
     // ------------------------------------------------ stop tests, β, δ_{k+1}
     const double z = csum_partials(a.pB, G, ws);
     s.e_Pe = s.e_Pe_new;
@@ -420,6 +429,7 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(TcgPersistArgs a) 
       store_blk<R>((k & 1) ? a.D0 : a.D1, i, dcur);  // δ_{k+1} → D[(k+1) & 1]
     }
     beta_prev = s.beta;
+    XM_PSTAMP(6);
     cbar();  // every consumer has read ts for this iteration
     if (t == 0) {
       ts = s;
@@ -489,6 +499,13 @@ static void launch_persist(xm_ctx* c) {
   a.pA = c->part1.p;
   a.pB = c->part2.p;
   a.gsync = c->gsync.p;
+  if (c->phases_on) {
+    if (!c->tdbg.p) {
+      c->tdbg.alloc(148 * 8);
+      XM_CUDA(cudaMemsetAsync(c->tdbg.p, 0, 148 * 8 * 8, c->stream));
+    }
+    a.dbg = c->tdbg.p;
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(G);
   cfg.blockDim = dim3(kPThreads);

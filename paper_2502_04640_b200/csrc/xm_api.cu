@@ -654,7 +654,7 @@ xm_status xm_solve(xm_ctx* c, int32_t r0, double tol, xm_solve_info* info) {
         unsigned long long t0 = ~0ull;
         for (int b = 0; b < G; ++b) t0 = std::min(t0, h[b * 8]);
         const char* nm[7] = {"start", "loop end", "pre-bar1", "post-bar1", "pre-bar2", "post-bar2",
-                             "end"};
+                             "end"};  // persistent kernel: stamps of iteration 1 ("start" = stream start)
         for (int k = 0; k < 7; ++k) {
           std::vector<double> v;
           for (int b = 0; b < G; ++b)
