@@ -9,19 +9,25 @@
 //   ── grid barrier B ──  ‖r‖² → stop tests, β, δ_{k+1} = −r_{k+1} + βδ_k
 //
 // What the persistent form buys over one launch per iteration:
-//  * no launch, no pipeline drain / fill between iterations — the producer
+//  * no launch, no pipeline drain / fill between iterations — the Q producer
 //    warp keeps prefetching the next iteration's Q tiles (Q never changes)
 //    while the consumers are in the barrier / camera phases;
 //  * no third barrier for δ: the next stream needs δ_{k+1} for ALL columns,
 //    which consumers form on the fly from r_{k+1} and δ_k tiles (TMA-loaded
 //    next to the Q tile) as −r + βδ with the same fma the owners use, so every
 //    CTA sees bitwise the same δ; owners write δ_{k+1} into the other half of
-//    a ping-pong pair for the stream after next;
-//  * camera state (Y_i, Λ_i, δ_i, r_i) stays in the owner thread's registers
-//    for the whole solve.
-// Rows are split evenly over the CTAs (the camera work follows barrier A and
-// reads Qδ rows back from L2), cameras by ⌊N·c/G⌋ (≤ 256 per CTA).
-// Determinism: fixed-order partial sums, identical decisions in every CTA.
+//    a ping-pong pair for the stream after next.
+//
+// Tiling.  The L2 slices, not HBM, cap the stream when vector tiles are
+// re-read per small row group (B200: ≈ 8.8 TB/s through L2 for Q + V traffic,
+// measured).  So a tile is a whole ROW BLOCK of the CTA (≤ 48
+// rows, one 1-D bulk copy per row) × 128 columns: each r / δ element is read
+// from L2 once per row block instead of once per 8 rows.  8 consumer warps =
+// 4 row quarters × 2 column halves; a lane owns 2 columns and ≤ 12 rows and
+// reduces once per row block.  Rows are split evenly over the CTAs (the
+// camera work follows barrier A and reads Qδ rows back from L2); cameras by
+// ⌊N·c/G⌋ (≤ 256 per CTA).  Determinism: fixed-order partial sums, identical
+// decisions in every CTA.
 #include "pipeline.cuh"
 
 namespace xm {
@@ -30,18 +36,19 @@ namespace {
 constexpr int kPW = 8;                  // consumer warps
 constexpr int kPC = 32 * kPW;           // consumer threads
 constexpr int kPThreads = kPC + 64;     // + two producer warps (Q tiles; r / δ tiles)
-constexpr int kPRows = 8;               // Q rows per tile
-constexpr int kPCols = 64 * kPW;        // 512 columns per tile
+constexpr int kBlockRows = 48;          // rows per row block (4 quarters × ≤ 12)
+constexpr int kQuarterRows = kBlockRows / 4;
+constexpr int kPCols = 128;             // columns per tile (2 halves × 32 lanes × 2)
 
 template <int R>
 struct PCfg {
-  static constexpr int kQBytes = kPRows * kPCols * 8;  // 32 KB
-  static constexpr int kVBytes = kPCols * R * 8;       // one chunk of r or δ
+  static constexpr int kQBytes = kBlockRows * kPCols * 8;  // 48 KB
+  static constexpr int kVBytes = kPCols * R * 8;           // one chunk of r or δ
   static constexpr int kStageBytes = kQBytes + 2 * kVBytes;
-  static constexpr int kStages = (R == 1) ? 5 : (R == 2 ? 4 : 3);
+  static constexpr int kStages = (kStageBytes * 4 <= 212 * 1024) ? 4 : 3;
 };
 
-__device__ __forceinline__ void cbar() {  // consumers only (the producer keeps streaming)
+__device__ __forceinline__ void cbar() {  // consumers only (the producers keep streaming)
   asm volatile("bar.sync 1, %0;\n" ::"n"(kPC) : "memory");
 }
 // fixed-order sum over the 256 consumer threads; every consumer gets the value
@@ -112,8 +119,8 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(TcgPersistArgs a) 
   uint64_t* fullQ = reinterpret_cast<uint64_t*>(smem_raw + (size_t)S * Cfg::kStageBytes);
   uint64_t* fullV = fullQ + S;
   uint64_t* empty = fullV + S;
-  double* red = reinterpret_cast<double*>(empty + S);  // [warps][kPRows][R]
-  double* acc = red + kPW * kPRows * R;                // [rows of this CTA][R]
+  double* red = reinterpret_cast<double*>(empty + S);  // [2 halves][kBlockRows][R]
+  double* acc = red + 2 * kBlockRows * R;              // [rows of this CTA][R]
   __shared__ TcgState ts;
   __shared__ volatile int sh_vgen;  // streams ≤ sh_vgen may load their r / δ tiles
   __shared__ volatile int sh_stop;
@@ -127,9 +134,9 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(TcgPersistArgs a) 
   const int nrow = (int)((int64_t)(blockIdx.x + 1) * n / G) - row_base;
   const int fa = (int)((int64_t)blockIdx.x * a.N / G);
   const int nf = (int)((int64_t)(blockIdx.x + 1) * a.N / G) - fa;
-  const int ngroups = (nrow + kPRows - 1) / kPRows;
+  const int nblocks = (nrow + kBlockRows - 1) / kBlockRows;
   const int nchunks = (n + kPCols - 1) / kPCols;
-  const int tiles = ngroups * nchunks;  // per iteration
+  const int tiles = nblocks * nchunks;  // per iteration
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -148,43 +155,49 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(TcgPersistArgs a) 
   __syncthreads();
   if (sh_stop) return;
 
-  if (warp >= kPW) {
-    // ============================================================== producers
-    // warp kPW: Q tiles (blocking waits on the ring's empty barriers, runs
-    // ahead into the next iteration); warp kPW+1: the r / δ tiles of each
-    // stage, gated on the iteration's barrier B.  Both leave on sh_stop.
-    if (lane != 0) return;
-    if (warp == kPW) {
-      const uint64_t pol_q = policy_evict_first();
-      long long iq = 0;
-      for (;; ++iq) {
-        const int s = (int)(iq % S);
-        const unsigned ph = (unsigned)((iq / S) & 1);
-        bool got = false;
-        while (!(got = mbar_try_wait(&empty[s], ph ^ 1u)))
+  if (warp == kPW) {
+    // ============================================================ Q producer
+    // whole warp: lane 0 acquires the slot, every lane issues rows ℓ, ℓ + 32
+    const uint64_t pol_q = policy_evict_first();
+    long long iq = 0;
+    for (;; ++iq) {
+      const int s = (int)(iq % S);
+      const unsigned ph = (unsigned)((iq / S) & 1);
+      int go = 0;
+      if (lane == 0) {
+        while (!(go = mbar_try_wait(&empty[s], ph ^ 1u)))
           if (sh_stop) break;
-        if (!got) break;
-        if (sh_stop) break;
-        const int t = (int)(iq % tiles);
-        const int g = t / nchunks, j = t % nchunks;
-        const int r0 = g * kPRows;
-        const int rows = min(kPRows, nrow - r0);
-        const int k0 = j * kPCols;
-        const int klen = min(kPCols, n - k0);
-        const unsigned qb = (unsigned)(((klen + 1) & ~1) * 8);
-        mbar_expect_tx(&fullQ[s], qb * rows);
-        double* st = stage_base + (size_t)s * (Cfg::kStageBytes / 8);
-        for (int q = 0; q < rows; ++q)
-          tma_load_1d(st + q * kPCols, a.Q + (int64_t)(row_base + r0 + q) * a.ldq + k0, qb,
-                      &fullQ[s], pol_q);
-        sh_iq = iq + 1;
+        if (sh_stop) go = 0;
       }
-      // Q copies issued for tiles the consumers never took must land before exit
+      go = __shfl_sync(0xffffffffu, go, 0);
+      if (!go) break;
+      const int tt = (int)(iq % tiles);
+      const int b = tt / nchunks, j = tt % nchunks;
+      const int r0 = b * kBlockRows;
+      const int rows = min(kBlockRows, nrow - r0);
+      const int k0 = j * kPCols;
+      const int klen = min(kPCols, n - k0);
+      const unsigned qb = (unsigned)(((klen + 1) & ~1) * 8);
+      if (lane == 0) mbar_expect_tx(&fullQ[s], qb * rows);
+      __syncwarp();
+      double* st = stage_base + (size_t)s * (Cfg::kStageBytes / 8);
+      for (int q = lane; q < rows; q += 32)
+        tma_load_1d(st + q * kPCols, a.Q + (int64_t)(row_base + r0 + q) * a.ldq + k0, qb,
+                    &fullQ[s], pol_q);
+      __syncwarp();
+      if (lane == 0) sh_iq = iq + 1;
+    }
+    if (lane == 0) {  // Q copies issued for tiles nobody will consume must land first
       while (sh_ivdone < 0) {
       }
-      for (long long t = sh_ivdone; t < iq; ++t) mbar_wait(&fullQ[t % S], (unsigned)((t / S) & 1));
-      return;
+      for (long long tq = sh_ivdone; tq < iq; ++tq)
+        mbar_wait(&fullQ[tq % S], (unsigned)((tq / S) & 1));
     }
+    return;
+  }
+  if (warp == kPW + 1) {
+    // ======================================================= r / δ producer
+    if (lane != 0) return;
     const uint64_t pol_v = policy_evict_last();
     long long iv = 0;
     int fenced = -1;
@@ -208,7 +221,7 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(TcgPersistArgs a) 
       const int k0 = j * kPCols;
       const int klen = min(kPCols, n - k0);
       const unsigned vb = (unsigned)(((klen * R + 1) & ~1) * 8);
-      double* st = stage_base + (size_t)s * (Cfg::kStageBytes / 8) + kPRows * kPCols;
+      double* st = stage_base + (size_t)s * (Cfg::kStageBytes / 8) + kBlockRows * kPCols;
       const double* dprev = (kv & 1) ? a.D0 : a.D1;  // δ_{k−1} = D[(k−1) & 1]
       mbar_expect_tx(&fullV[s], 2 * vb);
       tma_load_1d(st, a.res + (int64_t)k0 * R, vb, &fullV[s], pol_v);
@@ -234,7 +247,8 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(TcgPersistArgs a) 
     store_blk<R>(a.D0, i, d0b);
   }
   double beta_prev = 0.0;  // β_{k−1}: stream k uses δ_k = −r_k + β_{k−1}δ_{k−1}
-  const int col = 64 * warp + 2 * lane;
+  const int quarter = warp >> 1, half = warp & 1;
+  const int col = 64 * half + 2 * lane;  // this lane's column pair within a tile
   long long it = 0;
 #define XM_PSTAMP(q) \
   if (a.dbg && k == 1 && t == 0) a.dbg[blockIdx.x * 8 + (q)] = gtimer();
@@ -242,14 +256,16 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(TcgPersistArgs a) 
     XM_PSTAMP(0);
     // ---------------------------------------------------------------- stream
     const double* dprev_g = (k & 1) ? a.D0 : a.D1;
-    for (int g = 0; g < ngroups; ++g) {
-      const int r0 = g * kPRows;
-      const int rows = min(kPRows, nrow - r0);
-      double acc8[kPRows][R];
+    for (int b = 0; b < nblocks; ++b) {
+      const int rb = min(kBlockRows, nrow - b * kBlockRows);
+      const int rq = (rb + 3) >> 2;                 // rows per quarter (≤ 12)
+      const int q0 = quarter * rq;                  // this warp's first row in the block
+      const int nq = max(0, min(rq, rb - q0));      // this warp's row count
+      double acc12[kQuarterRows][R];
 #pragma unroll
-      for (int q = 0; q < kPRows; ++q)
+      for (int q = 0; q < kQuarterRows; ++q)
 #pragma unroll
-        for (int cc = 0; cc < R; ++cc) acc8[q][cc] = 0.0;
+        for (int cc = 0; cc < R; ++cc) acc12[q][cc] = 0.0;
       for (int j = 0; j < nchunks; ++j, ++it) {
         const int sidx = (int)(it % S);
         const unsigned ph = (unsigned)((it / S) & 1);
@@ -257,8 +273,9 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(TcgPersistArgs a) 
         mbar_wait(&fullV[sidx], ph);
         const int klen = min(kPCols, n - j * kPCols);
         const double* stg = stage_base + (size_t)sidx * (Cfg::kStageBytes / 8);
-        const double* rs = stg + kPRows * kPCols;
+        const double* rs = stg + kBlockRows * kPCols;
         const double* ds = rs + kPCols * R;
+        const double* qrow = stg + (size_t)q0 * kPCols + col;
         if (col + 1 < klen) {
           double v0[R], v1[R];
 #pragma unroll
@@ -267,12 +284,12 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(TcgPersistArgs a) 
             v1[cc] = fma(beta_prev, ds[(col + 1) * R + cc], -rs[(col + 1) * R + cc]);
           }
 #pragma unroll
-          for (int q = 0; q < kPRows; ++q) {
-            if (q < rows) {
-              double2 qv = *reinterpret_cast<const double2*>(stg + q * kPCols + col);
+          for (int q = 0; q < kQuarterRows; ++q) {
+            if (q < nq) {
+              const double2 qv = *reinterpret_cast<const double2*>(qrow + q * kPCols);
 #pragma unroll
               for (int cc = 0; cc < R; ++cc)
-                acc8[q][cc] = fma(qv.x, v0[cc], fma(qv.y, v1[cc], acc8[q][cc]));
+                acc12[q][cc] = fma(qv.x, v0[cc], fma(qv.y, v1[cc], acc12[q][cc]));
             }
           }
         } else if (col < klen) {
@@ -280,38 +297,37 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(TcgPersistArgs a) 
 #pragma unroll
           for (int cc = 0; cc < R; ++cc) v0[cc] = fma(beta_prev, ds[col * R + cc], -rs[col * R + cc]);
 #pragma unroll
-          for (int q = 0; q < kPRows; ++q) {
-            if (q < rows) {
-              const double qq = stg[q * kPCols + col];
+          for (int q = 0; q < kQuarterRows; ++q) {
+            if (q < nq) {
+              const double qq = qrow[q * kPCols];
 #pragma unroll
-              for (int cc = 0; cc < R; ++cc) acc8[q][cc] = fma(qq, v0[cc], acc8[q][cc]);
+              for (int cc = 0; cc < R; ++cc) acc12[q][cc] = fma(qq, v0[cc], acc12[q][cc]);
             }
           }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[sidx]);
       }
+      // reduce the row block: lanes (xor tree) → the two column halves (fixed order)
 #pragma unroll
-      for (int q = 0; q < kPRows; ++q)
+      for (int q = 0; q < kQuarterRows; ++q)
 #pragma unroll
         for (int cc = 0; cc < R; ++cc) {
-          double v = acc8[q][cc];
+          double v = acc12[q][cc];
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-          acc8[q][cc] = v;
+          acc12[q][cc] = v;
         }
       if (lane == 0) {
 #pragma unroll
-        for (int q = 0; q < kPRows; ++q)
+        for (int q = 0; q < kQuarterRows; ++q)
+          if (q < nq)
 #pragma unroll
-          for (int cc = 0; cc < R; ++cc) red[(warp * kPRows + q) * R + cc] = acc8[q][cc];
+            for (int cc = 0; cc < R; ++cc) red[(half * kBlockRows + q0 + q) * R + cc] = acc12[q][cc];
       }
       cbar();
-      for (int u = t; u < rows * R; u += kPC) {
-        double sum = 0.0;
-        for (int w = 0; w < kPW; ++w) sum += red[w * kPRows * R + u];
-        acc[r0 * R + u] = sum;
-      }
+      for (int u = t; u < rb * R; u += kPC)
+        acc[b * kBlockRows * R + u] = red[u] + red[kBlockRows * R + u];
       cbar();
     }
     XM_PSTAMP(1);
@@ -448,7 +464,7 @@ size_t persist_smem(int n, int G) {
   using Cfg = PCfg<R>;
   const int rows_max = ceil_div(n, G) + 1;
   return (size_t)Cfg::kStages * Cfg::kStageBytes + 3 * Cfg::kStages * 8 +
-         (size_t)kPW * kPRows * R * 8 + (size_t)rows_max * R * 8;
+         (size_t)2 * kBlockRows * R * 8 + (size_t)rows_max * R * 8;
 }
 size_t persist_smem_r(int r, int n, int G) {
   switch (r) {
