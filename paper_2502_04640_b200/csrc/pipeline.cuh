@@ -1,6 +1,8 @@
 // pipeline.cuh — sm_100a building blocks of the streaming kernels: mbarrier
 // ring primitives, 1-D TMA bulk copies with L2 cache policies, %globaltimer.
 #pragma once
+#include <cuda.h>
+
 #include "frame_ops.cuh"
 
 namespace xm {
@@ -62,6 +64,16 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
 // requests in flight beyond what the shared-memory ring can hold
 __device__ __forceinline__ void prefetch_l2(const void* src, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
+
+// 2-D tensor TMA: box at element coordinates (x = column, y = row) → smem
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int x, int y,
+                                            uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
 }
 
 // one (potentially suspending) probe of an mbarrier phase; false on timeout

@@ -28,6 +28,8 @@
 // camera work follows barrier A and reads Qδ rows back from L2); cameras by
 // ⌊N·c/G⌋ (≤ 256 per CTA).  Determinism: fixed-order partial sums, identical
 // decisions in every CTA.
+#include <cudaTypedefs.h>
+
 #include "pipeline.cuh"
 
 namespace xm {
@@ -108,10 +110,12 @@ struct TcgPersistArgs {
   double* pB;                  // per-CTA partials ‖r‖²
   unsigned long long* gsync;   // grid barrier counter (0 on entry)
   unsigned long long* dbg;     // XM_PHASES: %globaltimer stamps [G][8] of iteration 1
+  int bh;                      // rows per row block = the tensor map's box height
 };
 
 template <int R>
-__global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(TcgPersistArgs a) {
+__global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(const __grid_constant__ CUtensorMap tmq,
+                                                              TcgPersistArgs a) {
   using Cfg = PCfg<R>;
   constexpr int S = Cfg::kStages;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -134,7 +138,8 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(TcgPersistArgs a) 
   const int nrow = (int)((int64_t)(blockIdx.x + 1) * n / G) - row_base;
   const int fa = (int)((int64_t)blockIdx.x * a.N / G);
   const int nf = (int)((int64_t)(blockIdx.x + 1) * a.N / G) - fa;
-  const int nblocks = (nrow + kBlockRows - 1) / kBlockRows;
+  const int bh = a.bh;                       // ≤ kBlockRows, same in every CTA
+  const int nblocks = (nrow + bh - 1) / bh;
   const int nchunks = (n + kPCols - 1) / kPCols;
   const int tiles = nblocks * nchunks;  // per iteration
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -157,42 +162,31 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(TcgPersistArgs a) 
 
   if (warp == kPW) {
     // ============================================================ Q producer
-    // whole warp: lane 0 acquires the slot, every lane issues rows ℓ, ℓ + 32
+    // one 2-D tensor copy per stage: the row block (bh rows from the CTA's
+    // block start; rows past the CTA's range are loaded and ignored, rows ≥ n
+    // are zero-filled) × 128 columns
+    if (lane != 0) return;
     const uint64_t pol_q = policy_evict_first();
+    const unsigned qbytes = (unsigned)(kPCols * bh * 8);
     long long iq = 0;
     for (;; ++iq) {
       const int s = (int)(iq % S);
       const unsigned ph = (unsigned)((iq / S) & 1);
-      int go = 0;
-      if (lane == 0) {
-        while (!(go = mbar_try_wait(&empty[s], ph ^ 1u)))
-          if (sh_stop) break;
-        if (sh_stop) go = 0;
-      }
-      go = __shfl_sync(0xffffffffu, go, 0);
-      if (!go) break;
+      bool go;
+      while (!(go = mbar_try_wait(&empty[s], ph ^ 1u)))
+        if (sh_stop) break;
+      if (!go || sh_stop) break;
       const int tt = (int)(iq % tiles);
       const int b = tt / nchunks, j = tt % nchunks;
-      const int r0 = b * kBlockRows;
-      const int rows = min(kBlockRows, nrow - r0);
-      const int k0 = j * kPCols;
-      const int klen = min(kPCols, n - k0);
-      const unsigned qb = (unsigned)(((klen + 1) & ~1) * 8);
-      if (lane == 0) mbar_expect_tx(&fullQ[s], qb * rows);
-      __syncwarp();
-      double* st = stage_base + (size_t)s * (Cfg::kStageBytes / 8);
-      for (int q = lane; q < rows; q += 32)
-        tma_load_1d(st + q * kPCols, a.Q + (int64_t)(row_base + r0 + q) * a.ldq + k0, qb,
-                    &fullQ[s], pol_q);
-      __syncwarp();
-      if (lane == 0) sh_iq = iq + 1;
+      mbar_expect_tx(&fullQ[s], qbytes);
+      tma_load_2d(stage_base + (size_t)s * (Cfg::kStageBytes / 8), &tmq, j * kPCols,
+                  row_base + b * bh, &fullQ[s], pol_q);
+      sh_iq = iq + 1;
     }
-    if (lane == 0) {  // Q copies issued for tiles nobody will consume must land first
-      while (sh_ivdone < 0) {
-      }
-      for (long long tq = sh_ivdone; tq < iq; ++tq)
-        mbar_wait(&fullQ[tq % S], (unsigned)((tq / S) & 1));
+    // Q copies issued for tiles nobody will consume must land first
+    while (sh_ivdone < 0) {
     }
+    for (long long tq = sh_ivdone; tq < iq; ++tq) mbar_wait(&fullQ[tq % S], (unsigned)((tq / S) & 1));
     return;
   }
   if (warp == kPW + 1) {
@@ -257,7 +251,7 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(TcgPersistArgs a) 
     // ---------------------------------------------------------------- stream
     const double* dprev_g = (k & 1) ? a.D0 : a.D1;
     for (int b = 0; b < nblocks; ++b) {
-      const int rb = min(kBlockRows, nrow - b * kBlockRows);
+      const int rb = min(bh, nrow - b * bh);       // valid rows of this block
       const int rq = (rb + 3) >> 2;                 // rows per quarter (≤ 12)
       const int q0 = quarter * rq;                  // this warp's first row in the block
       const int nq = max(0, min(rq, rb - q0));      // this warp's row count
@@ -327,7 +321,7 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(TcgPersistArgs a) 
       }
       cbar();
       for (int u = t; u < rb * R; u += kPC)
-        acc[b * kBlockRows * R + u] = red[u] + red[kBlockRows * R + u];
+        acc[b * bh * R + u] = red[u] + red[kBlockRows * R + u];
       cbar();
     }
     XM_PSTAMP(1);
@@ -487,9 +481,45 @@ bool tcg_persist_supported(xm_ctx* c, int r) {
   return ceil_div(c->N, G) <= kPC && persist_smem_r(r, c->n, G) <= kSmemCap;
 }
 
+// rows per block: the CTA row count (⌈n/G⌉) split into ⌈·/48⌉ equal blocks
+static int persist_bh(int n, int G) {
+  const int rows_max = ceil_div(n, G);
+  return ceil_div(rows_max, ceil_div(rows_max, kBlockRows));
+}
+
+static const CUtensorMap* persist_tmap(xm_ctx* c, int G) {
+  const int bh = persist_bh(c->n, G);
+  if (c->persist_tmap_q == c->Q.p && c->persist_tmap_bh == bh && c->persist_tmap_n == c->n)
+    return reinterpret_cast<const CUtensorMap*>(c->persist_tmap);
+  static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    PFN_cuTensorMapEncodeTiled_v12000 f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&f),
+                                cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return f;
+  }();
+  if (!encode) throw Error(XM_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)c->n, (cuuint64_t)c->n};
+  cuuint64_t strides[1] = {(cuuint64_t)c->ldq * 8};
+  cuuint32_t box[2] = {(cuuint32_t)kPCols, (cuuint32_t)bh};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(reinterpret_cast<CUtensorMap*>(c->persist_tmap), CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                      2, c->Q.p, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(XM_ECUDA, "cuTensorMapEncodeTiled failed (persistent tCG)");
+  c->persist_tmap_q = c->Q.p;
+  c->persist_tmap_bh = bh;
+  c->persist_tmap_n = c->n;
+  return reinterpret_cast<const CUtensorMap*>(c->persist_tmap);
+}
+
 template <int R>
 static void launch_persist(xm_ctx* c) {
   const int G = std::min(148, c->N);
+  const CUtensorMap* tm = persist_tmap(c, G);
   const size_t smem = persist_smem<R>(c->n, G);
   if (smem > kSmemCap) throw Error(XM_EINVAL, "persistent tCG shared memory plan exceeds 227 KB");
   static size_t attr = 0;
@@ -515,6 +545,7 @@ static void launch_persist(xm_ctx* c) {
   a.pA = c->part1.p;
   a.pB = c->part2.p;
   a.gsync = c->gsync.p;
+  a.bh = c->persist_tmap_bh;
   if (c->phases_on) {
     if (!c->tdbg.p) {
       c->tdbg.alloc(148 * 8);
@@ -532,7 +563,7 @@ static void launch_persist(xm_ctx* c) {
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  XM_CUDA(cudaLaunchKernelEx(&cfg, k_tcg_persist<R>, a));
+  XM_CUDA(cudaLaunchKernelEx(&cfg, k_tcg_persist<R>, *tm, a));
   XM_CHECK_LAUNCH();
   count_launch(c);
 }

@@ -196,6 +196,10 @@ struct xm_ctx {
   bool persist_tcg = true;  // XM_NO_PERSIST_TCG=1: one launch per tCG iteration instead
   xm::DBuf<double> dir2;    // δ ping-pong partner of dir (persistent tCG)
   cudaEvent_t ev_persist[2] = {nullptr, nullptr};
+  // persistent tCG: 2-D tensor map of Q (box 128 columns × bh rows), raw CUtensorMap bytes
+  alignas(64) unsigned char persist_tmap[128] = {0};
+  const void* persist_tmap_q = nullptr;
+  int persist_tmap_bh = 0, persist_tmap_n = 0;
   xm::DBuf<unsigned long long> tdbg;  // XM_PHASES: fused-tCG phase stamps
   double phase_ms[8] = {0};
   long long phase_n[8] = {0};
