@@ -21,10 +21,10 @@
 // Tiling.  The L2 slices, not HBM, cap the stream when vector tiles are
 // re-read per small row group (B200: ≈ 8.8 TB/s through L2 for Q + V traffic,
 // measured).  So a tile is a whole ROW BLOCK of the CTA (≤ 48
-// rows) × 128 columns, one 2-D tensor copy: each r / δ element is read from
-// L2 once per row block instead of once per 8 rows.  Warp w owns ≤ 6 rows of
-// the block, lane ℓ columns 4ℓ..4ℓ+3 (V reused across the rows, 32-B Q reads
-// per lane), one xor reduction per row block.  Rows are split evenly over the CTAs (the
+// rows, one 1-D bulk copy per row) × 128 columns: each r / δ element is read
+// from L2 once per row block instead of once per 8 rows.  8 consumer warps =
+// 4 row quarters × 2 column halves; a lane owns 2 columns and ≤ 12 rows and
+// reduces once per row block.  Rows are split evenly over the CTAs (the
 // camera work follows barrier A and reads Qδ rows back from L2); cameras by
 // ⌊N·c/G⌋ (≤ 256 per CTA).  Determinism: fixed-order partial sums, identical
 // decisions in every CTA.
@@ -38,9 +38,9 @@ namespace {
 constexpr int kPW = 8;                  // consumer warps
 constexpr int kPC = 32 * kPW;           // consumer threads
 constexpr int kPThreads = kPC + 64;     // + two producer warps (Q tiles; r / δ tiles)
-constexpr int kBlockRows = 48;          // rows per row block (8 warps × ≤ 6)
-constexpr int kWarpRows = kBlockRows / kPW;
-constexpr int kPCols = 128;             // columns per tile (32 lanes × 4)
+constexpr int kBlockRows = 48;          // rows per row block (4 quarters × ≤ 12)
+constexpr int kQuarterRows = kBlockRows / 4;
+constexpr int kPCols = 128;             // columns per tile (2 halves × 32 lanes × 2)
 
 template <int R>
 struct PCfg {
@@ -123,7 +123,8 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(const __grid_const
   uint64_t* fullQ = reinterpret_cast<uint64_t*>(smem_raw + (size_t)S * Cfg::kStageBytes);
   uint64_t* fullV = fullQ + S;
   uint64_t* empty = fullV + S;
-  double* acc = reinterpret_cast<double*>(empty + S);  // [rows of this CTA][R]
+  double* red = reinterpret_cast<double*>(empty + S);  // [2 halves][kBlockRows][R]
+  double* acc = red + 2 * kBlockRows * R;              // [rows of this CTA][R]
   __shared__ TcgState ts;
   __shared__ volatile int sh_vgen;  // streams ≤ sh_vgen may load their r / δ tiles
   __shared__ volatile int sh_stop;
@@ -240,7 +241,8 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(const __grid_const
     store_blk<R>(a.D0, i, d0b);
   }
   double beta_prev = 0.0;  // β_{k−1}: stream k uses δ_k = −r_k + β_{k−1}δ_{k−1}
-  const int col = 4 * lane;  // this lane's 4 columns within a tile
+  const int quarter = warp >> 1, half = warp & 1;
+  const int col = 64 * half + 2 * lane;  // this lane's column pair within a tile
   long long it = 0;
 #define XM_PSTAMP(q) \
   if (a.dbg && k == 1 && t == 0) a.dbg[blockIdx.x * 8 + (q)] = gtimer();
@@ -257,14 +259,14 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(const __grid_const
     }
     for (int b = 0; b < nblocks; ++b) {
       const int rb = min(bh, nrow - b * bh);       // valid rows of this block
-      const int rpw = (rb + kPW - 1) / kPW;         // rows per warp (≤ kWarpRows)
-      const int q0 = warp * rpw;                    // this warp's first row in the block
-      const int nq = max(0, min(rpw, rb - q0));     // this warp's row count
-      double accw[kWarpRows][R];
+      const int rq = (rb + 3) >> 2;                 // rows per quarter (≤ 12)
+      const int q0 = quarter * rq;                  // this warp's first row in the block
+      const int nq = max(0, min(rq, rb - q0));      // this warp's row count
+      double acc12[kQuarterRows][R];
 #pragma unroll
-      for (int q = 0; q < kWarpRows; ++q)
+      for (int q = 0; q < kQuarterRows; ++q)
 #pragma unroll
-        for (int cc = 0; cc < R; ++cc) accw[q][cc] = 0.0;
+        for (int cc = 0; cc < R; ++cc) acc12[q][cc] = 0.0;
       for (int j = 0; j < nchunks; ++j, ++it) {
         const int sidx = (int)(it % S);
         const unsigned ph = (unsigned)((it / S) & 1);
@@ -274,50 +276,61 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(const __grid_const
         const double* stg = stage_base + (size_t)sidx * (Cfg::kStageBytes / 8);
         const double* rs = stg + kBlockRows * kPCols;
         const double* ds = rs + kPCols * R;
-        // columns ≥ klen (last chunk): the Q tile is zero-filled there (OOB)
-        // and the stage's r / δ slots are stale, so those V entries are set to 0
-        double v[4][R];
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          const bool ok = col + m < klen;
-#pragma unroll
-          for (int cc = 0; cc < R; ++cc)
-            v[m][cc] = ok ? fma(beta_prev, ds[(col + m) * R + cc], -rs[(col + m) * R + cc]) : 0.0;
-        }
         const double* qrow = stg + (size_t)q0 * kPCols + col;
+        if (col + 1 < klen) {
+          double v0[R], v1[R];
 #pragma unroll
-        for (int q = 0; q < kWarpRows; ++q) {
-          if (q < nq) {
-            const double2 qa = *reinterpret_cast<const double2*>(qrow + q * kPCols);
-            const double2 qb = *reinterpret_cast<const double2*>(qrow + q * kPCols + 2);
+          for (int cc = 0; cc < R; ++cc) {
+            v0[cc] = fma(beta_prev, ds[col * R + cc], -rs[col * R + cc]);
+            v1[cc] = fma(beta_prev, ds[(col + 1) * R + cc], -rs[(col + 1) * R + cc]);
+          }
 #pragma unroll
-            for (int cc = 0; cc < R; ++cc)
-              accw[q][cc] = fma(qa.x, v[0][cc], fma(qa.y, v[1][cc],
-                             fma(qb.x, v[2][cc], fma(qb.y, v[3][cc], accw[q][cc]))));
+          for (int q = 0; q < kQuarterRows; ++q) {
+            if (q < nq) {
+              const double2 qv = *reinterpret_cast<const double2*>(qrow + q * kPCols);
+#pragma unroll
+              for (int cc = 0; cc < R; ++cc)
+                acc12[q][cc] = fma(qv.x, v0[cc], fma(qv.y, v1[cc], acc12[q][cc]));
+            }
+          }
+        } else if (col < klen) {
+          double v0[R];
+#pragma unroll
+          for (int cc = 0; cc < R; ++cc) v0[cc] = fma(beta_prev, ds[col * R + cc], -rs[col * R + cc]);
+#pragma unroll
+          for (int q = 0; q < kQuarterRows; ++q) {
+            if (q < nq) {
+              const double qq = qrow[q * kPCols];
+#pragma unroll
+              for (int cc = 0; cc < R; ++cc) acc12[q][cc] = fma(qq, v0[cc], acc12[q][cc]);
+            }
           }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[sidx]);
       }
-      // reduce the warp's rows over its 32 lanes (xor tree, fixed order)
+      // reduce the row block: lanes (xor tree) → the two column halves (fixed order)
 #pragma unroll
-      for (int q = 0; q < kWarpRows; ++q)
+      for (int q = 0; q < kQuarterRows; ++q)
 #pragma unroll
         for (int cc = 0; cc < R; ++cc) {
-          double x = accw[q][cc];
+          double v = acc12[q][cc];
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-          accw[q][cc] = x;
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          acc12[q][cc] = v;
         }
       if (lane == 0) {
 #pragma unroll
-        for (int q = 0; q < kWarpRows; ++q)
+        for (int q = 0; q < kQuarterRows; ++q)
           if (q < nq)
 #pragma unroll
-            for (int cc = 0; cc < R; ++cc) acc[(b * bh + q0 + q) * R + cc] = accw[q][cc];
+            for (int cc = 0; cc < R; ++cc) red[(half * kBlockRows + q0 + q) * R + cc] = acc12[q][cc];
       }
+      cbar();
+      for (int u = t; u < rb * R; u += kPC)
+        acc[b * bh * R + u] = red[u] + red[kBlockRows * R + u];
+      cbar();
     }
-    cbar();
     XM_PSTAMP(1);
     // ------------------------------------------- rows → QD, ⟨δ_k, 2Qδ_k⟩ rows part
     double part = 0.0;
@@ -330,9 +343,11 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(const __grid_const
       part = fma(2.0 * q, d, part);
     }
     TcgState s = ts;
-    Blk<R> y, dcur, rcur;
+    Blk<R> y, dcur, rcur, e, he;
     double L[6];
     if (has) {  // camera part −2⟨δ_i, Λ_iδ_i⟩ (δ tangent, P self-adjoint)
+      load_blk<R>(a.eta, i, e);  // own rows: issued before the barrier
+      load_blk<R>(a.Heta, i, he);
       load_blk<R>(a.Y, i, y);
       load_blk<R>((k & 1) ? a.D1 : a.D0, i, dcur);  // δ_k = D[k & 1] (own rows)
       load_blk<R>(a.res, i, rcur);
@@ -368,9 +383,7 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(const __grid_const
     const double step = s.boundary ? s.tau : alpha;
     double rn2 = 0.0;
     if (has) {
-      Blk<R> qv, hd, e, he;
-      load_blk<R>(a.eta, i, e);
-      load_blk<R>(a.Heta, i, he);
+      Blk<R> qv, hd;
       const double* qp = a.QD + (int64_t)3 * i * R;
 #pragma unroll
       for (int p = 0; p < 3; ++p)
@@ -453,7 +466,7 @@ size_t persist_smem(int n, int G) {
   using Cfg = PCfg<R>;
   const int rows_max = ceil_div(n, G) + 1;
   return (size_t)Cfg::kStages * Cfg::kStageBytes + 3 * Cfg::kStages * 8 +
-         (size_t)rows_max * R * 8;
+         (size_t)2 * kBlockRows * R * 8 + (size_t)rows_max * R * 8;
 }
 size_t persist_smem_r(int r, int n, int G) {
   switch (r) {
