@@ -250,13 +250,6 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(const __grid_const
     XM_PSTAMP(0);
     // ---------------------------------------------------------------- stream
     const double* dprev_g = (k & 1) ? a.D0 : a.D1;
-    // δ_k at this CTA's own rows (for the rows part of ⟨δ,Hδ⟩), loaded now so
-    // the latency hides under the stream (r_k, δ_{k−1} are final since barrier B)
-    double dk_own = 0.0;
-    if (t < nrow * R) {
-      const int64_t gidx = (int64_t)row_base * R + t;
-      dk_own = fma(beta_prev, __ldcg(dprev_g + gidx), -__ldcg(a.res + gidx));
-    }
     for (int b = 0; b < nblocks; ++b) {
       const int rb = min(bh, nrow - b * bh);       // valid rows of this block
       const int rq = (rb + 3) >> 2;                 // rows per quarter (≤ 12)
@@ -338,16 +331,13 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(const __grid_const
       const int64_t gidx = (int64_t)row_base * R + u;
       const double q = acc[u];
       a.QD[gidx] = q;
-      const double d =
-          (u == t) ? dk_own : fma(beta_prev, __ldcg(dprev_g + gidx), -__ldcg(a.res + gidx));  // δ_k
+      const double d = fma(beta_prev, __ldcg(dprev_g + gidx), -__ldcg(a.res + gidx));  // δ_k
       part = fma(2.0 * q, d, part);
     }
     TcgState s = ts;
-    Blk<R> y, dcur, rcur, e, he;
+    Blk<R> y, dcur, rcur;
     double L[6];
     if (has) {  // camera part −2⟨δ_i, Λ_iδ_i⟩ (δ tangent, P self-adjoint)
-      load_blk<R>(a.eta, i, e);  // own rows: issued before the barrier
-      load_blk<R>(a.Heta, i, he);
       load_blk<R>(a.Y, i, y);
       load_blk<R>((k & 1) ? a.D1 : a.D0, i, dcur);  // δ_k = D[k & 1] (own rows)
       load_blk<R>(a.res, i, rcur);
@@ -383,7 +373,7 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(const __grid_const
     const double step = s.boundary ? s.tau : alpha;
     double rn2 = 0.0;
     if (has) {
-      Blk<R> qv, hd;
+      Blk<R> qv, hd, e, he;
       const double* qp = a.QD + (int64_t)3 * i * R;
 #pragma unroll
       for (int p = 0; p < 3; ++p)
@@ -391,6 +381,8 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(const __grid_const
         for (int cc = 0; cc < R; ++cc) qv.v[p][cc] = __ldcg(qp + p * R + cc);
       sub_lam<R>(qv, L, dcur, 2.0, 2.0, hd);  // Hδ = P(2Qδ − 2Λδ)
       project_blk<R>(y, i == 0, hd);
+      load_blk<R>(a.eta, i, e);
+      load_blk<R>(a.Heta, i, he);
 #pragma unroll
       for (int p = 0; p < 3; ++p)
 #pragma unroll
