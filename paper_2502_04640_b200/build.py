@@ -15,7 +15,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libxm.so")
 OBJ = os.path.join(HERE, "build")
-SOURCES = ["util.cu", "assembly.cu", "spmm.cu", "spmm_sym.cu", "tcg_persist.cu", "manifold.cu", "cert.cu", "comm.cu", "xm_api.cu"]
+SOURCES = ["util.cu", "assembly.cu", "spmm.cu", "spmm_sym.cu", "tcg_persist.cu", "manifold.cu", "cert.cu", "comm.cu", "blas.cu", "xm_api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include")]
@@ -39,7 +39,8 @@ def _stale(obj: str, deps) -> bool:
 
 def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
-    headers = [os.path.join(CSRC, "xm_internal.cuh"), os.path.join(ROOT, "include", "xm.h")]
+    headers = [os.path.join(CSRC, h) for h in sorted(os.listdir(CSRC)) if h.endswith(".cuh")]
+    headers.append(os.path.join(ROOT, "include", "xm.h"))
     cc = nvcc()
     objs = []
     jobs = []

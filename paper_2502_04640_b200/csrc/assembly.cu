@@ -350,6 +350,14 @@ void dgemm(xm_ctx* c, bool ta, bool tb, bool lower, int M, int N, int K, double 
            const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
            int64_t ldc) {
   if (M <= 0 || N <= 0) return;
+  if (c->use_blas) {
+    if (!lower) {
+      if (blas_dgemm(c, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc)) return;
+    } else if (A == B && lda == ldb && M == N && ta != tb) {
+      // SYRK: op(A)·op(B) = X·Xᵀ (tb) or Xᵀ·X (ta) with X = A
+      if (blas_dsyrk_lower(c, ta, M, K, alpha, A, lda, beta, C, ldc)) return;
+    }
+  }
   dim3 grid(ceil_div(N, GB), ceil_div(M, GB));
 #define XM_GEMM_CASE(a_, b_, l_)                                                            \
   if (ta == a_ && tb == b_ && lower == l_) {                                                \

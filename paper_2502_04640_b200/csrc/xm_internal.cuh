@@ -161,6 +161,7 @@ struct xm_ctx {
   void* nccl_comm = nullptr;
   void* loop = nullptr;
   std::string loop_key;
+  void* cublas = nullptr;  // cublasHandle_t (blas.cu), created on first use
   // lower-triangle SpMM work plan + tensor map (spmm_sym.cu)
   void* sym_plan = nullptr;
   xm::DBuf<double> gbuf;  // all-gather staging
@@ -194,6 +195,7 @@ struct xm_ctx {
   bool phases_on = false;
   bool fused_tcg = true;    // XM_NO_FUSED_TCG=1: three-kernel tCG iteration (A/B measurement)
   bool persist_tcg = true;  // XM_NO_PERSIST_TCG=1: one launch per tCG iteration instead
+  bool use_blas = true;     // XM_NO_CUBLAS=1: the library's own k_dgemm for the dense updates
   xm::DBuf<double> dir2;    // δ ping-pong partner of dir (persistent tCG)
   cudaEvent_t ev_persist[2] = {nullptr, nullptr};
   // persistent tCG: 2-D tensor map of Q (box 128 columns × bh rows), raw CUtensorMap bytes
@@ -334,6 +336,12 @@ void nccl_destroy(xm_ctx* c);
 void nccl_allgather(xm_ctx* c, const double* send, double* recv, size_t count_per_rank);
 void nccl_allreduce_sum(xm_ctx* c, double* buf, size_t count);
 void sym_plan_destroy(xm_ctx* c);
+// cuBLAS (blas.cu) for plain dense GEMM / SYRK; false ⇒ not available
+bool blas_dgemm(xm_ctx* c, bool ta, bool tb, int M, int N, int K, double alpha, const double* A,
+                int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc);
+bool blas_dsyrk_lower(xm_ctx* c, bool trans_x, int n, int k, double alpha, const double* X,
+                      int64_t ldx, double beta, double* C, int64_t ldc);
+void blas_destroy(xm_ctx* c);
 
 // Row sharding: rank q owns frames [q·nfpr, min(N, (q+1)·nfpr)),
 // nfpr = ⌈N/world⌉; vectors exchanged by the all-gather hold world·3·nfpr rows.
