@@ -379,73 +379,6 @@ void dgemm(xm_ctx* c, bool ta, bool tb, bool lower, int M, int N, int K, double 
 // ---------------------------------------------------------------- Cholesky
 constexpr int NB = 64;
 
-// Unblocked Cholesky of the nb×nb diagonal block (one CTA, block in smem).
-__global__ void __launch_bounds__(256) k_potf2(double* __restrict__ A, int64_t lda, int nb,
-                                               double rel_tol, const double* __restrict__ scale,
-                                               int* __restrict__ err) {
-  const double pivot_tol = rel_tol * (*scale);
-  __shared__ double a[NB][NB + 1];
-  for (int t = threadIdx.x; t < nb * nb; t += blockDim.x) {
-    int i = t / nb, j = t % nb;
-    a[i][j] = (j <= i) ? A[(int64_t)i * lda + j] : 0.0;
-  }
-  __syncthreads();
-  for (int j = 0; j < nb; ++j) {
-    if (threadIdx.x == 0) {
-      double d = a[j][j];
-      if (!(d > pivot_tol)) {
-        atomicOr(err, 1);
-        d = 1.0;
-      }
-      a[j][j] = sqrt(d);
-    }
-    __syncthreads();
-    double djj = a[j][j];
-    for (int i = j + 1 + threadIdx.x; i < nb; i += blockDim.x) a[i][j] /= djj;
-    __syncthreads();
-    int rem = nb - j - 1;
-    for (int t = threadIdx.x; t < rem * rem; t += blockDim.x) {
-      int ii = j + 1 + t / rem, ll = j + 1 + t % rem;
-      if (ll <= ii) a[ii][ll] -= a[ii][j] * a[ll][j];
-    }
-    __syncthreads();
-  }
-  for (int t = threadIdx.x; t < nb * nb; t += blockDim.x) {
-    int i = t / nb, j = t % nb;
-    A[(int64_t)i * lda + j] = (j <= i) ? a[i][j] : 0.0;
-  }
-}
-
-// Panel: rows below the diagonal block, X·L11ᵀ = A21 (one thread per row).
-template <int NBT>
-__global__ void __launch_bounds__(128) k_trsm_panel(const double* __restrict__ L11, int64_t lda,
-                                                    double* __restrict__ A21, int rows, int nb) {
-  __shared__ double l[NBT][NBT + 1];
-  for (int t = threadIdx.x; t < nb * nb; t += blockDim.x) {
-    int i = t / nb, j = t % nb;
-    l[i][j] = (j <= i) ? L11[(int64_t)i * lda + j] : 0.0;
-  }
-  __syncthreads();
-  int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= rows) return;
-  double* row = A21 + (int64_t)r * lda;
-  double x[NBT];
-#pragma unroll
-  for (int j = 0; j < NBT; ++j) {
-    if (j < nb) {
-      double s = row[j];
-#pragma unroll
-      for (int q = 0; q < j; ++q) s -= x[q] * l[j][q];
-      x[j] = s / l[j][j];
-    } else {
-      x[j] = 0.0;
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < NBT; ++j)
-    if (j < nb) row[j] = x[j];
-}
-
 __global__ void k_zero_upper(double* A, int m, int64_t lda) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= (int64_t)m * m) return;
@@ -467,6 +400,89 @@ __global__ void k_diag_max(const double* __restrict__ A, int m, int64_t lda, dou
   if (threadIdx.x == 0) *out = sh[0];
 }
 
+// One panel step of the blocked Cholesky, fused: every CTA factors the
+// nb×nb diagonal block in shared memory (redundantly — it is ≈ 3 µs of work
+// and saves a dependent launch; CTA 0 stores it in a side slot that
+// k_chol_diag_back copies into place after the last step), then each thread
+// solves one row of the panel below, x·L11ᵀ = a  (row in registers).
+// Diagonal-block factorisation: 16×16 threads, thread (ti, tl) owns the 4×4
+// sub-block rows 4ti.., columns 4tl.. of the trailing update (no index
+// division in the inner loop).
+template <int NBT>
+__global__ void __launch_bounds__(256) k_chol_panel(double* __restrict__ Akk, int64_t lda, int nb,
+                                                    int rows, double rel_tol,
+                                                    const double* __restrict__ scale,
+                                                    int* __restrict__ err,
+                                                    double* __restrict__ L11_out) {
+  static_assert(NBT == 64, "16 x 16 threads x 4 x 4");
+  __shared__ double a[NBT][NBT + 1];
+  const double pivot_tol = rel_tol * (*scale);
+  const int tid = threadIdx.x, ti = tid >> 4, tl = tid & 15;
+  for (int t = tid; t < NBT * NBT; t += 256) {
+    const int i = t >> 6, j = t & 63;
+    a[i][j] = (i < nb && j < nb && j <= i) ? Akk[(int64_t)i * lda + j] : (i == j ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  for (int j = 0; j < nb; ++j) {
+    if (tid == 0) {
+      double d = a[j][j];
+      if (!(d > pivot_tol)) {
+        if (blockIdx.x == 0) atomicOr(err, 1);
+        d = 1.0;
+      }
+      a[j][j] = sqrt(d);
+    }
+    __syncthreads();
+    if (tid > j && tid < nb) a[tid][j] /= a[j][j];
+    __syncthreads();
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int i = 4 * ti + x;
+      if (i > j && i < nb) {
+        const double aij = a[i][j];
+#pragma unroll
+        for (int y = 0; y < 4; ++y) {
+          const int l = 4 * tl + y;
+          if (l > j && l <= i) a[i][l] = fma(-aij, a[l][j], a[i][l]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == 0)  // into a side slot: other CTAs may still be reading Akk
+    for (int t = tid; t < NBT * NBT; t += 256) L11_out[t] = a[t >> 6][t & 63];
+  // panel rows: X·L11ᵀ = A21
+  const int r = blockIdx.x * 256 + tid;
+  if (r >= rows) return;
+  double* row = Akk + (int64_t)(nb + r) * lda;
+  double x[NBT];
+#pragma unroll
+  for (int j = 0; j < NBT; ++j) {
+    if (j < nb) {
+      double s2 = row[j];
+#pragma unroll
+      for (int q = 0; q < j; ++q) s2 = fma(-x[q], a[j][q], s2);
+      x[j] = s2 / a[j][j];
+    } else {
+      x[j] = 0.0;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NBT; ++j)
+    if (j < nb) row[j] = x[j];
+}
+
+// L11 slots → diagonal blocks (strict upper part of each block zeroed)
+__global__ void k_chol_diag_back(const double* __restrict__ slots, double* __restrict__ A,
+                                 int64_t lda, int m) {
+  const int blk = blockIdx.x, kb = blk * NB, nb = min(NB, m - kb);
+  const double* sl = slots + (size_t)blk * NB * NB;
+  for (int t = threadIdx.x; t < NB * NB; t += blockDim.x) {
+    const int i = t / NB, j = t % NB;
+    if (i < nb && j < nb) A[(int64_t)(kb + i) * lda + kb + j] = (j <= i) ? sl[t] : 0.0;
+  }
+}
+
 bool dense_cholesky(xm_ctx* c, double* A, int m, int64_t lda, double rel_tol, bool throw_on_fail) {
   if (m <= 0) return true;
   c->flags.alloc(16);
@@ -476,22 +492,25 @@ bool dense_cholesky(xm_ctx* c, double* A, int m, int64_t lda, double rel_tol, bo
   k_diag_max<<<1, 256, 0, c->stream>>>(A, m, lda, d_scale);
   XM_CHECK_LAUNCH();
   count_launch(c);
+  DBuf<double>& slots = scratch_f64(c, "chol_l11");
+  slots.alloc((size_t)ceil_div(m, NB) * NB * NB);
   for (int kb = 0; kb < m; kb += NB) {
     int nb = std::min(NB, m - kb);
     double* Akk = A + (int64_t)kb * lda + kb;
-    k_potf2<<<1, 256, 0, c->stream>>>(Akk, lda, nb, rel_tol, d_scale, c->flags.p);
+    int rows = m - kb - nb;
+    k_chol_panel<NB><<<std::max(1, ceil_div(rows, 256)), 256, 0, c->stream>>>(
+        Akk, lda, nb, rows, rel_tol, d_scale, c->flags.p, slots.p + (size_t)(kb / NB) * NB * NB);
     XM_CHECK_LAUNCH();
     count_launch(c);
-    int rows = m - kb - nb;
     if (rows > 0) {
       double* A21 = A + (int64_t)(kb + nb) * lda + kb;
-      k_trsm_panel<NB><<<ceil_div(rows, 128), 128, 0, c->stream>>>(Akk, lda, A21, rows, nb);
-      XM_CHECK_LAUNCH();
-      count_launch(c);
       double* A22 = A + (int64_t)(kb + nb) * lda + (kb + nb);
       dgemm(c, false, true, true, rows, rows, nb, -1.0, A21, lda, A21, lda, 1.0, A22, lda);
     }
   }
+  k_chol_diag_back<<<ceil_div(m, NB), 256, 0, c->stream>>>(slots.p, A, lda, m);
+  XM_CHECK_LAUNCH();
+  count_launch(c);
   if (throw_on_fail) {
     k_zero_upper<<<ceil_div((int64_t)m * m, 256), 256, 0, c->stream>>>(A, m, lda);
     XM_CHECK_LAUNCH();
