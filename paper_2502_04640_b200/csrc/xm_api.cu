@@ -230,7 +230,7 @@ struct PhaseClock {
   }
 };
 static const char* kPhaseNames[8] = {"tcg", "retract+df", "accept+grad", "eval_point",
-                                     "certify", "escape", "init", "other"};
+                                     "certify", "escape", "lanczos", "cholesky"};
 
 struct RtrOut {
   bool converged = false;
@@ -361,10 +361,12 @@ void certify_current(xm_ctx* c, double* lambda, int* steps) {
   c->cert_method = 0;
   if (c->world == 1 && c->opt.cert_cholesky) {
     int budget = std::min(c->opt.lanczos_max, std::max(32, c->n / 72));
+    PhaseClock pc(c);
     bool conv = lanczos(c, tol, budget, lambda, steps, c->cert_v.p);
+    pc.lap(6);
     if (conv) {
       c->cert_lower = *lambda;
-    } else if (psd_test_cholesky(c, eps)) {
+    } else if (psd_test_cholesky(c, eps) && (pc.lap(7), true)) {
       c->cert_method = 1;
       c->cert_lower = -eps;
     } else {
