@@ -451,6 +451,457 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(const __grid_const
   // it stored the final state before breaking, see tcg_final)
 }
 
+// ======================================================================
+// Symmetric variant: the stream reads only the LOWER triangle of Q (half the
+// bytes).  Work units = (48-row block I, 128-column chunk J) with J·128 ≤ the
+// block's last row, ordered column-major and split evenly over the CTAs.  A
+// unit adds Q_IJ δ_J to its rows (row partial, one per unit) and Q_IJᵀ δ_I to
+// its columns (column partial, accumulated across the CTA's consecutive units
+// of the same chunk = a segment).  Diagonal-straddling units mask j ≥ i (the
+// diagonal counts once, in the row part).  ⟨δ, Qδ⟩ comes out of the same
+// partials before barrier A (δ_I·row + δ_J·column), so no extra barrier; after
+// barrier A each CTA assembles the Qδ rows of its own cameras from the
+// partials in a fixed order (deterministic).
+constexpr int kSB = 48;         // rows per unit
+constexpr int kSC = 128;        // columns per unit (lane ℓ: columns ℓ + 32m, m < 4)
+constexpr int kSWR = kSB / kPW; // 6 rows per warp
+
+template <int R>
+struct SCfg {
+  static constexpr int kQBytes = kSB * kSC * 8;            // 48 KB
+  static constexpr int kVBytes = 2 * (kSC + kSB) * R * 8;  // r, δ at the chunk's columns and block's rows
+  static constexpr int kStageBytes = kQBytes + kVBytes;
+  static constexpr int kStages = (kStageBytes * 4 <= 200 * 1024) ? 4 : 3;
+};
+
+struct SymTcgArgs {
+  TcgPersistArgs b;
+  const int* ubase;   // nJ + 1: first unit of chunk J
+  const int* uimin;   // nJ: first row block of chunk J
+  const int* segbase; // G + 1: first column-partial slot of CTA c
+  const int* colptr;  // nJ + 1
+  const int* colidx;  // column-partial slots of chunk J, CTA order
+  double* RP;         // [U][kSB][R] row partials
+  double* CP;         // [slots][kSC][R] column partials
+  int U, nJ, nI;
+};
+
+__device__ __forceinline__ int sym_chunk_of(const int* __restrict__ ubase, int nJ, int u) {
+  int lo = 0, hi = nJ - 1;  // largest J with ubase[J] ≤ u
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(ubase + mid) <= u) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+template <int R>
+__global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist_sym(const __grid_constant__ CUtensorMap tmq,
+                                                                  SymTcgArgs sa) {
+  using Cfg = SCfg<R>;
+  constexpr int S = Cfg::kStages;
+  const TcgPersistArgs& a = sa.b;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* stage_base = reinterpret_cast<double*>(smem_raw);
+  uint64_t* fullQ = reinterpret_cast<uint64_t*>(smem_raw + (size_t)S * Cfg::kStageBytes);
+  uint64_t* fullV = fullQ + S;
+  uint64_t* empty = fullV + S;
+  double* colred = reinterpret_cast<double*>(empty + S);  // [4][kSC][R]
+  double* yown = colred + 4 * kSC * R;                      // [3·cameras of this CTA][R]
+  __shared__ TcgState ts;
+  __shared__ volatile int sh_vgen;
+  __shared__ volatile int sh_stop;
+  __shared__ volatile long long sh_iq;
+  __shared__ volatile long long sh_ivdone;
+  __shared__ double ws[kPW];
+
+  const int G = gridDim.x;
+  const int n = a.n;
+  const int u0 = (int)((int64_t)blockIdx.x * sa.U / G);
+  const int u1 = (int)((int64_t)(blockIdx.x + 1) * sa.U / G);
+  const int tiles = u1 - u0;  // units per iteration
+  const int fa = (int)((int64_t)blockIdx.x * a.N / G);
+  const int nf = (int)((int64_t)(blockIdx.x + 1) * a.N / G) - fa;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int J0 = (tiles > 0) ? sym_chunk_of(sa.ubase, sa.nJ, u0) : 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&fullQ[s], 1);
+      mbar_init(&fullV[s], 1);
+      mbar_init(&empty[s], kPW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    ts = *a.st;
+    sh_vgen = 0;
+    sh_stop = ts.stop != 0;
+    sh_iq = 0;
+    sh_ivdone = -1;
+  }
+  __syncthreads();
+  if (sh_stop) return;
+
+  // unit cursor → (I, J): walk the column-major order from (I of u0, J0)
+  auto unit_ij = [&](int uu, int& I, int& J) {
+    J = J0;
+    while (J + 1 < sa.nJ && __ldg(sa.ubase + J + 1) <= uu) ++J;
+    I = __ldg(sa.uimin + J) + (uu - __ldg(sa.ubase + J));
+  };
+
+  if (warp == kPW) {
+    // ============================================================ Q producer
+    if (lane != 0) return;
+    const uint64_t pol_q = policy_evict_first();
+    const unsigned qbytes = (unsigned)(kSC * kSB * 8);
+    long long iq = 0;
+    int I = 0, J = J0, ucur = -1;
+    for (;; ++iq) {
+      const int s = (int)(iq % S);
+      const unsigned ph = (unsigned)((iq / S) & 1);
+      bool go;
+      while (!(go = mbar_try_wait(&empty[s], ph ^ 1u)))
+        if (sh_stop) break;
+      if (!go || sh_stop || tiles == 0) break;
+      const int uu = u0 + (int)(iq % tiles);
+      if (uu == u0 || uu != ucur + 1) {
+        unit_ij(uu, I, J);
+      } else {  // next unit: down the chunk, or the top of the next chunk
+        if (uu >= __ldg(sa.ubase + J + 1)) {
+          ++J;
+          I = __ldg(sa.uimin + J);
+        } else {
+          ++I;
+        }
+      }
+      ucur = uu;
+      mbar_expect_tx(&fullQ[s], qbytes);
+      tma_load_2d(stage_base + (size_t)s * (Cfg::kStageBytes / 8), &tmq, J * kSC, I * kSB, &fullQ[s],
+                  pol_q);
+      sh_iq = iq + 1;
+    }
+    while (sh_ivdone < 0) {
+    }
+    for (long long tq = sh_ivdone; tq < iq; ++tq) mbar_wait(&fullQ[tq % S], (unsigned)((tq / S) & 1));
+    return;
+  }
+  if (warp == kPW + 1) {
+    // ======================================================= r / δ producer
+    if (lane != 0) return;
+    const uint64_t pol_v = policy_evict_last();
+    long long iv = 0;
+    int fenced = -1;
+    for (;; ++iv) {
+      const int kv = tiles > 0 ? (int)(iv / tiles) : 0;
+      bool stop = false;
+      while (!(iv < sh_iq && kv <= sh_vgen)) {
+        if (sh_stop) {
+          stop = true;
+          break;
+        }
+        __nanosleep(20);
+      }
+      if (stop) break;
+      if (kv > fenced) {
+        fence_proxy_async();
+        fenced = kv;
+      }
+      const int s = (int)(iv % S);
+      int I, J;
+      unit_ij(u0 + (int)(iv % tiles), I, J);
+      const int c0 = J * kSC, klen = min(kSC, n - c0);
+      const int r0 = I * kSB, rlen = min(kSB, n - r0);
+      const unsigned vbc = (unsigned)(((klen * R + 1) & ~1) * 8);
+      const unsigned vbr = (unsigned)(((rlen * R + 1) & ~1) * 8);
+      double* st = stage_base + (size_t)s * (Cfg::kStageBytes / 8) + kSB * kSC;
+      const double* dprev = (kv & 1) ? a.D0 : a.D1;  // δ_{k−1}
+      mbar_expect_tx(&fullV[s], 2 * vbc + 2 * vbr);
+      tma_load_1d(st, a.res + (int64_t)c0 * R, vbc, &fullV[s], pol_v);
+      tma_load_1d(st + kSC * R, dprev + (int64_t)c0 * R, vbc, &fullV[s], pol_v);
+      tma_load_1d(st + 2 * kSC * R, a.res + (int64_t)r0 * R, vbr, &fullV[s], pol_v);
+      tma_load_1d(st + 2 * kSC * R + kSB * R, dprev + (int64_t)r0 * R, vbr, &fullV[s], pol_v);
+    }
+    sh_ivdone = iv;
+    return;
+  }
+
+  // ================================================================== consumers
+  const int t = threadIdx.x;
+  const bool has = t < nf;
+  const int i = fa + t;
+  if (has) {  // δ_0 = −r_0
+    Blk<R> r0b, d0b;
+    load_blk<R>(a.res, i, r0b);
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int cc = 0; cc < R; ++cc) d0b.v[p][cc] = fma(0.0, 0.0, -r0b.v[p][cc]);
+    store_blk<R>(a.D0, i, d0b);
+  }
+  double beta_prev = 0.0;
+  long long it = 0;
+  for (int k = 0;; ++k) {
+    const double* dprev_g = (k & 1) ? a.D0 : a.D1;
+    double part = 0.0;  // this thread's share of ⟨δ_k, Qδ_k⟩
+    double accc[4][R];  // column partial of the current segment (lane's 4 columns, warp's rows)
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int cc = 0; cc < R; ++cc) accc[m][cc] = 0.0;
+    int I = 0, J = J0;
+    for (int uu = u0; uu < u1; ++uu, ++it) {
+      if (uu == u0) {
+        unit_ij(uu, I, J);
+      } else if (uu >= __ldg(sa.ubase + J + 1)) {
+        ++J;
+        I = __ldg(sa.uimin + J);
+      } else {
+        ++I;
+      }
+      const int sidx = (int)(it % S);
+      const unsigned ph = (unsigned)((it / S) & 1);
+      mbar_wait(&fullQ[sidx], ph);
+      mbar_wait(&fullV[sidx], ph);
+      const double* stg = stage_base + (size_t)sidx * (Cfg::kStageBytes / 8);
+      const double* rJ = stg + kSB * kSC;
+      const double* dJ = rJ + kSC * R;
+      const double* rI = dJ + kSC * R;
+      const double* dI = rI + kSB * R;
+      const int c0 = J * kSC, rb0 = I * kSB;
+      double vj[4][R];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int cl = lane + 32 * m;
+        const bool ok = c0 + cl < n;
+#pragma unroll
+        for (int cc = 0; cc < R; ++cc)
+          vj[m][cc] = ok ? fma(beta_prev, dJ[cl * R + cc], -rJ[cl * R + cc]) : 0.0;
+      }
+      double accr[kSWR][R];
+#pragma unroll
+      for (int q = 0; q < kSWR; ++q)
+#pragma unroll
+        for (int cc = 0; cc < R; ++cc) accr[q][cc] = 0.0;
+      const bool straddle = c0 + kSC - 1 >= rb0;  // some element on / above the diagonal
+#pragma unroll
+      for (int q = 0; q < kSWR; ++q) {
+        const int rl = kSWR * warp + q;
+        const int rg = rb0 + rl;
+        double vi[R];
+#pragma unroll
+        for (int cc = 0; cc < R; ++cc)
+          vi[cc] = (rg < n) ? fma(beta_prev, dI[rl * R + cc], -rI[rl * R + cc]) : 0.0;
+        const double* qrow = stg + (size_t)rl * kSC + lane;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const double qv = qrow[32 * m];
+          const int cg = c0 + lane + 32 * m;
+          const bool lower = !straddle || cg < rg;
+          const bool rowp = lower || cg == rg;
+          if (rowp) {
+#pragma unroll
+            for (int cc = 0; cc < R; ++cc) accr[q][cc] = fma(qv, vj[m][cc], accr[q][cc]);
+          }
+          if (lower) {
+#pragma unroll
+            for (int cc = 0; cc < R; ++cc) accc[m][cc] = fma(qv, vi[cc], accc[m][cc]);
+          }
+        }
+      }
+      // row partial of this unit: lanes (xor tree) → RP, and δ_I · row partial
+#pragma unroll
+      for (int q = 0; q < kSWR; ++q)
+#pragma unroll
+        for (int cc = 0; cc < R; ++cc) {
+          double x = accr[q][cc];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+          accr[q][cc] = x;
+        }
+      if (lane == 0) {
+        double* rp = sa.RP + ((int64_t)uu * kSB + kSWR * warp) * R;
+#pragma unroll
+        for (int q = 0; q < kSWR; ++q) {
+          const int rl = kSWR * warp + q;
+          const bool okr = rb0 + rl < n;
+#pragma unroll
+          for (int cc = 0; cc < R; ++cc) {
+            rp[q * R + cc] = accr[q][cc];
+            const double di = okr ? fma(beta_prev, dI[rl * R + cc], -rI[rl * R + cc]) : 0.0;
+            part = fma(di, accr[q][cc], part);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[sidx]);
+      // segment end (chunk changes or last unit): column partial across the 8 warps
+      const bool seg_end = (uu + 1 == u1) || (uu + 1 >= __ldg(sa.ubase + J + 1));
+      if (seg_end) {
+        if (warp >= 4) {
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+#pragma unroll
+            for (int cc = 0; cc < R; ++cc)
+              colred[((warp - 4) * kSC + lane + 32 * m) * R + cc] = accc[m][cc];
+        }
+        cbar();
+        if (warp < 4) {
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+#pragma unroll
+            for (int cc = 0; cc < R; ++cc) {
+              double* p = colred + (warp * kSC + lane + 32 * m) * R + cc;
+              *p = accc[m][cc] + *p;  // warp w + warp w+4
+            }
+        }
+        cbar();
+        const int slot = __ldg(sa.segbase + blockIdx.x) + (J - J0);
+        for (int u2 = t; u2 < kSC * R; u2 += kPC) {
+          const double sum = (colred[u2] + colred[kSC * R + u2]) +
+                             (colred[2 * kSC * R + u2] + colred[3 * kSC * R + u2]);
+          sa.CP[(int64_t)slot * kSC * R + u2] = sum;
+          const int64_t g = (int64_t)c0 * R + u2;
+          if (c0 + u2 / R < n)
+            part = fma(fma(beta_prev, __ldcg(dprev_g + g), -__ldcg(a.res + g)), sum, part);
+        }
+        cbar();
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+          for (int cc = 0; cc < R; ++cc) accc[m][cc] = 0.0;
+      }
+    }
+    XM_PSTAMP(1);
+    TcgState s = ts;
+    Blk<R> y, dcur, rcur;
+    double L[6];
+    if (has) {  // camera part −2⟨δ_i, Λ_iδ_i⟩; rows part is 2⟨δ, Qδ⟩ = 2·part (summed below)
+      load_blk<R>(a.Y, i, y);
+      load_blk<R>((k & 1) ? a.D1 : a.D0, i, dcur);
+      load_blk<R>(a.res, i, rcur);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) L[q] = a.lam[6 * i + q];
+    }
+    {
+      double cam = 0.0;
+      if (has) {
+        Blk<R> zero{}, lamd;
+        sub_lam<R>(zero, L, dcur, 0.0, 1.0, lamd);
+        cam = dotb<R>(dcur, lamd);
+      }
+      const double pc = csum(fma(2.0, part, 2.0 * cam), ws);
+      if (t == 0) a.pA[blockIdx.x] = pc;
+    }
+    XM_PSTAMP(2);
+    cgrid_sync(a.gsync, G);
+    XM_PSTAMP(3);
+    // ---------------------- assemble Qδ at this CTA's camera rows (fixed order)
+    for (int o = t; o < 3 * nf * R; o += kPC) {
+      const int g = 3 * fa + o / R, cc = o % R;
+      const int Ib = g / kSB, l = g % kSB, Jg = g / kSC, mcol = g % kSC;
+      const int Jmax = min(sa.nJ - 1, (Ib * kSB + kSB - 1) / kSC);
+      double y2 = 0.0;
+      for (int Jp = 0; Jp <= Jmax; ++Jp) {
+        const int uu = __ldg(sa.ubase + Jp) + (Ib - __ldg(sa.uimin + Jp));
+        y2 += __ldcg(sa.RP + ((int64_t)uu * kSB + l) * R + cc);
+      }
+      for (int p = __ldg(sa.colptr + Jg); p < __ldg(sa.colptr + Jg + 1); ++p)
+        y2 += __ldcg(sa.CP + ((int64_t)__ldg(sa.colidx + p) * kSC + mcol) * R + cc);
+      yown[o] = y2;
+    }
+    cbar();
+    // -------------------------------------------------- α, boundary / τ, update
+    const double dHd = csum_partials(a.pA, G, ws);
+    s.d_Hd = dHd;
+    s.n_hvp += 1;
+    const double alpha = (dHd != 0.0) ? s.z / dHd : INFINITY;
+    const double e_new = s.e_Pe + 2.0 * alpha * s.e_Pd + alpha * alpha * s.d_Pd;
+    const double D2 = s.Delta * s.Delta;
+    s.alpha = alpha;
+    s.e_Pe_new = e_new;
+    if (dHd <= 0.0 || e_new >= D2) {
+      s.tau = (-s.e_Pd + sqrt(s.e_Pd * s.e_Pd + s.d_Pd * (D2 - s.e_Pe))) / s.d_Pd;
+      s.boundary = 1;
+      s.stop = (dHd <= 0.0) ? TCG_NEGCURV : TCG_EXCEEDED;
+    } else {
+      s.boundary = 0;
+    }
+    const double step = s.boundary ? s.tau : alpha;
+    double rn2 = 0.0;
+    if (has) {
+      Blk<R> qv, hd, e, he;
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int cc = 0; cc < R; ++cc) qv.v[p][cc] = yown[(3 * t + p) * R + cc];
+      sub_lam<R>(qv, L, dcur, 2.0, 2.0, hd);  // Hδ = P(2Qδ − 2Λδ)
+      project_blk<R>(y, i == 0, hd);
+      load_blk<R>(a.eta, i, e);
+      load_blk<R>(a.Heta, i, he);
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int cc = 0; cc < R; ++cc) {
+          e.v[p][cc] = fma(step, dcur.v[p][cc], e.v[p][cc]);
+          he.v[p][cc] = fma(step, hd.v[p][cc], he.v[p][cc]);
+        }
+      store_blk<R>(a.eta, i, e);
+      store_blk<R>(a.Heta, i, he);
+      if (!s.boundary) {
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+#pragma unroll
+          for (int cc = 0; cc < R; ++cc) rcur.v[p][cc] = fma(step, hd.v[p][cc], rcur.v[p][cc]);
+        project_blk<R>(y, i == 0, rcur);
+        store_blk<R>(a.res, i, rcur);
+        rn2 = frob2<R>(rcur);
+      }
+    }
+    if (s.boundary) {
+      tcg_final(s, t, &sh_stop, a.st);
+      break;
+    }
+    {
+      const double pr = csum(rn2, ws);
+      if (t == 0) a.pB[blockIdx.x] = pr;
+    }
+    XM_PSTAMP(4);
+    cgrid_sync(a.gsync, G);
+    XM_PSTAMP(5);
+    const double z = csum_partials(a.pB, G, ws);
+    s.e_Pe = s.e_Pe_new;
+    s.z_old = s.z;
+    s.z = z;
+    s.j += 1;
+    if (sqrt(z) <= s.r0 * fmin(pow(s.r0, s.theta), s.kappa)) {
+      s.stop = TCG_CONVERGED;
+    } else {
+      s.beta = s.z / s.z_old;
+      s.e_Pd = s.beta * (s.e_Pd + s.alpha * s.d_Pd);
+      s.d_Pd = s.z + s.beta * s.beta * s.d_Pd;
+      if (s.j >= s.max_inner) s.stop = TCG_MAXINNER;
+    }
+    if (s.stop) {
+      tcg_final(s, t, &sh_stop, a.st);
+      break;
+    }
+    if (has) {
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int cc = 0; cc < R; ++cc) dcur.v[p][cc] = fma(s.beta, dcur.v[p][cc], -rcur.v[p][cc]);
+      store_blk<R>((k & 1) ? a.D0 : a.D1, i, dcur);
+    }
+    beta_prev = s.beta;
+    XM_PSTAMP(6);
+    cbar();
+    if (t == 0) {
+      ts = s;
+      __threadfence_block();
+      sh_vgen = k + 1;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------- host
 namespace {
 template <int R>
@@ -473,7 +924,10 @@ size_t persist_smem_r(int r, int n, int G) {
 constexpr size_t kSmemCap = 227 * 1024 - 1024;  // dynamic budget (static smem ≈ 0.3 KB)
 }  // namespace
 
+bool tcg_persist_sym_supported(xm_ctx* c, int r);
+
 bool tcg_persist_supported(xm_ctx* c, int r) {
+  if (tcg_persist_sym_supported(c, r)) return true;
   if (!c->fused_tcg || !c->persist_tcg || c->world != 1 || r < 1 || r > 5 ||
       spmm_sym_supported(c, r) || c->N < 1)
     return false;
@@ -487,10 +941,7 @@ static int persist_bh(int n, int G) {
   return ceil_div(rows_max, ceil_div(rows_max, kBlockRows));
 }
 
-static const CUtensorMap* persist_tmap(xm_ctx* c, int G) {
-  const int bh = persist_bh(c->n, G);
-  if (c->persist_tmap_q == c->Q.p && c->persist_tmap_bh == bh && c->persist_tmap_n == c->n)
-    return reinterpret_cast<const CUtensorMap*>(c->persist_tmap);
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
     PFN_cuTensorMapEncodeTiled_v12000 f = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -501,19 +952,33 @@ static const CUtensorMap* persist_tmap(xm_ctx* c, int G) {
     return f;
   }();
   if (!encode) throw Error(XM_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  return encode;
+}
+
+// Q as a 2-D tensor (n columns × n rows, row pitch ldq·8), box kPCols × bh,
+// rows / columns ≥ n zero-filled.  Cached in `raw` (128 B) per (Q, bh, n).
+static const CUtensorMap* q_tmap(xm_ctx* c, int bh, unsigned char* raw, const void** q_cached,
+                                 int* bh_cached, int* n_cached) {
+  if (*q_cached == c->Q.p && *bh_cached == bh && *n_cached == c->n)
+    return reinterpret_cast<const CUtensorMap*>(raw);
   cuuint64_t dims[2] = {(cuuint64_t)c->n, (cuuint64_t)c->n};
   cuuint64_t strides[1] = {(cuuint64_t)c->ldq * 8};
   cuuint32_t box[2] = {(cuuint32_t)kPCols, (cuuint32_t)bh};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode(reinterpret_cast<CUtensorMap*>(c->persist_tmap), CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
-                      2, c->Q.p, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = tmap_encoder()(reinterpret_cast<CUtensorMap*>(raw), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                              c->Q.p, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(XM_ECUDA, "cuTensorMapEncodeTiled failed (persistent tCG)");
-  c->persist_tmap_q = c->Q.p;
-  c->persist_tmap_bh = bh;
-  c->persist_tmap_n = c->n;
-  return reinterpret_cast<const CUtensorMap*>(c->persist_tmap);
+  *q_cached = c->Q.p;
+  *bh_cached = bh;
+  *n_cached = c->n;
+  return reinterpret_cast<const CUtensorMap*>(raw);
+}
+
+static const CUtensorMap* persist_tmap(xm_ctx* c, int G) {
+  return q_tmap(c, persist_bh(c->n, G), c->persist_tmap, &c->persist_tmap_q, &c->persist_tmap_bh,
+                &c->persist_tmap_n);
 }
 
 template <int R>
@@ -575,10 +1040,185 @@ static void launch_persist(xm_ctx* c) {
 // (8·n·r each, ≈ 9·8·n·r with reads + writes) + Λ (48·N).
 double tcg_persist_bytes_per_iter(xm_ctx* c, int r) {
   const double n = c->n;
-  return 8.0 * n * n + 9.0 * 8.0 * n * r + 48.0 * c->N;
+  const double qb = tcg_persist_sym_supported(c, r) ? 8.0 * n * (n + 1) / 2 : 8.0 * n * n;
+  return qb + 9.0 * 8.0 * n * r + 48.0 * c->N;
+}
+
+// ------------------------------------------------------------- symmetric host
+struct SymTcgPlan {
+  int n = 0, G = 0, nI = 0, nJ = 0, U = 0, slots = 0, R = 0;
+  DBuf<int> ubase, uimin, segbase, colptr, colidx;
+  DBuf<double> RP, CP;
+  alignas(64) unsigned char tmap[128] = {0};
+  const void* tmap_q = nullptr;
+  int tmap_bh = 0, tmap_n = 0;
+};
+
+static SymTcgPlan& sym_tcg_plan(xm_ctx* c, int r) {
+  if (!c->persist_sym_plan) c->persist_sym_plan = new SymTcgPlan();
+  SymTcgPlan& p = *static_cast<SymTcgPlan*>(c->persist_sym_plan);
+  const int n = c->n, G = std::min(148, c->N);
+  if (p.n != n || p.G != G) {
+    p.n = n;
+    p.G = G;
+    p.nI = ceil_div(n, kSB);
+    p.nJ = ceil_div(n, kSC);
+    std::vector<int> ub(p.nJ + 1, 0), im(p.nJ, 0);
+    for (int J = 0; J < p.nJ; ++J) {
+      im[J] = std::max(0, ceil_div(J * kSC - (kSB - 1), kSB));  // first block reaching column J·kSC
+      ub[J + 1] = ub[J] + (p.nI - im[J]);
+    }
+    p.U = ub[p.nJ];
+    auto chunk_of = [&](int u) {
+      int J = 0;
+      while (J + 1 < p.nJ && ub[J + 1] <= u) ++J;
+      return J;
+    };
+    std::vector<int> sb(G + 1, 0);
+    std::vector<std::vector<int>> bycol(p.nJ);
+    for (int cta = 0; cta < G; ++cta) {
+      const int u0 = (int)((int64_t)cta * p.U / G), u1 = (int)((int64_t)(cta + 1) * p.U / G);
+      sb[cta + 1] = sb[cta];
+      if (u1 > u0) {
+        const int Ja = chunk_of(u0), Jb = chunk_of(u1 - 1);
+        for (int J = Ja; J <= Jb; ++J) bycol[J].push_back(sb[cta] + (J - Ja));
+        sb[cta + 1] += Jb - Ja + 1;
+      }
+    }
+    p.slots = sb[G];
+    std::vector<int> cp(p.nJ + 1, 0), ci;
+    for (int J = 0; J < p.nJ; ++J) {
+      for (int sl : bycol[J]) ci.push_back(sl);
+      cp[J + 1] = (int)ci.size();
+    }
+    p.ubase.alloc(ub.size());
+    p.uimin.alloc(im.size());
+    p.segbase.alloc(sb.size());
+    p.colptr.alloc(cp.size());
+    p.colidx.alloc(std::max<size_t>(1, ci.size()));
+    XM_CUDA(cudaMemcpy(p.ubase.p, ub.data(), ub.size() * 4, cudaMemcpyHostToDevice));
+    XM_CUDA(cudaMemcpy(p.uimin.p, im.data(), im.size() * 4, cudaMemcpyHostToDevice));
+    XM_CUDA(cudaMemcpy(p.segbase.p, sb.data(), sb.size() * 4, cudaMemcpyHostToDevice));
+    XM_CUDA(cudaMemcpy(p.colptr.p, cp.data(), cp.size() * 4, cudaMemcpyHostToDevice));
+    if (!ci.empty())
+      XM_CUDA(cudaMemcpy(p.colidx.p, ci.data(), ci.size() * 4, cudaMemcpyHostToDevice));
+  }
+  p.RP.alloc((size_t)p.U * kSB * 5 + 64);      // sized for r ≤ 5 (fixed addresses)
+  p.CP.alloc((size_t)p.slots * kSC * 5 + 64);
+  return p;
+}
+
+void sym_tcg_plan_destroy(xm_ctx* c) {
+  delete static_cast<SymTcgPlan*>(c->persist_sym_plan);
+  c->persist_sym_plan = nullptr;
+}
+
+namespace {
+template <int R>
+size_t persist_sym_smem(int N, int G) {
+  using Cfg = SCfg<R>;
+  const int nf_max = ceil_div(N, G);
+  return (size_t)Cfg::kStages * Cfg::kStageBytes + 3 * Cfg::kStages * 8 + 4 * (size_t)kSC * R * 8 +
+         (size_t)3 * nf_max * R * 8;
+}
+size_t persist_sym_smem_r(int r, int N, int G) {
+  switch (r) {
+    case 1: return persist_sym_smem<1>(N, G);
+    case 2: return persist_sym_smem<2>(N, G);
+    case 3: return persist_sym_smem<3>(N, G);
+    case 4: return persist_sym_smem<4>(N, G);
+    case 5: return persist_sym_smem<5>(N, G);
+    default: return ~(size_t)0;
+  }
+}
+}  // namespace
+
+// Lower-triangle persistent tCG: opt-in (XM_SYM_TCG=1) until it wins on the bench.
+bool tcg_persist_sym_supported(xm_ctx* c, int r) {
+  if (!c->persist_sym || !c->fused_tcg || !c->persist_tcg || c->world != 1 || r < 1 || r > 5 ||
+      c->N < 1)
+    return false;
+  const int G = std::min(148, c->N);
+  return ceil_div(c->N, G) <= kPC && persist_sym_smem_r(r, c->N, G) <= kSmemCap;
+}
+
+template <int R>
+static void launch_persist_sym(xm_ctx* c) {
+  const int G = std::min(148, c->N);
+  SymTcgPlan& p = sym_tcg_plan(c, R);
+  const CUtensorMap* tm = q_tmap(c, kSB, p.tmap, &p.tmap_q, &p.tmap_bh, &p.tmap_n);
+  const size_t smem = persist_sym_smem<R>(c->N, G);
+  if (smem > kSmemCap) throw Error(XM_EINVAL, "symmetric persistent tCG smem plan exceeds 227 KB");
+  static size_t attr = 0;
+  if (smem > attr) {
+    XM_CUDA(cudaFuncSetAttribute(k_tcg_persist_sym<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    attr = smem;
+  }
+  SymTcgArgs sa{};
+  TcgPersistArgs& a = sa.b;
+  a.Q = c->Q.p;
+  a.ldq = c->ldq;
+  a.n = c->n;
+  a.N = c->N;
+  a.st = c->tcg.p;
+  a.Y = c->Y.p;
+  a.lam = c->lam.p;
+  a.res = c->res.p;
+  a.D0 = c->dir.p;
+  a.D1 = c->dir2.p;
+  a.eta = c->eta.p;
+  a.Heta = c->Heta.p;
+  a.QD = c->Hdir.p;
+  a.pA = c->part1.p;
+  a.pB = c->part2.p;
+  a.gsync = c->gsync.p;
+  a.bh = kSB;
+  if (c->phases_on) {
+    if (!c->tdbg.p) {
+      c->tdbg.alloc(148 * 8);
+      XM_CUDA(cudaMemsetAsync(c->tdbg.p, 0, 148 * 8 * 8, c->stream));
+    }
+    a.dbg = c->tdbg.p;
+  }
+  sa.ubase = p.ubase.p;
+  sa.uimin = p.uimin.p;
+  sa.segbase = p.segbase.p;
+  sa.colptr = p.colptr.p;
+  sa.colidx = p.colidx.p;
+  sa.RP = p.RP.p;
+  sa.CP = p.CP.p;
+  sa.U = p.U;
+  sa.nJ = p.nJ;
+  sa.nI = p.nI;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(kPThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  XM_CUDA(cudaLaunchKernelEx(&cfg, k_tcg_persist_sym<R>, *tm, sa));
+  XM_CHECK_LAUNCH();
+  count_launch(c);
 }
 
 void tcg_persist_launch(xm_ctx* c, int r) {
+  if (tcg_persist_sym_supported(c, r)) {
+    const int64_t len = (int64_t)c->n * r;
+    c->dir2.alloc((size_t)len + 64);
+    XM_CUDA(cudaMemsetAsync(c->dir2.p, 0, len * 8, c->stream));  // δ_{−1} = 0
+    switch (r) {
+      case 1: launch_persist_sym<1>(c); return;
+      case 2: launch_persist_sym<2>(c); return;
+      case 3: launch_persist_sym<3>(c); return;
+      case 4: launch_persist_sym<4>(c); return;
+      case 5: launch_persist_sym<5>(c); return;
+    }
+  }
   const int64_t len = (int64_t)c->n * r;
   c->dir2.alloc((size_t)len + 64);
   XM_CUDA(cudaMemsetAsync(c->dir2.p, 0, len * 8, c->stream));  // δ_{−1} = 0

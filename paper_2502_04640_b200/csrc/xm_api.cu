@@ -515,6 +515,7 @@ xm_status xm_create(xm_ctx** out, int device, int rank, int world, const void* n
   if (std::getenv("XM_NO_FUSED_TCG")) c->fused_tcg = false;
   if (std::getenv("XM_NO_PERSIST_TCG")) c->persist_tcg = false;
   if (std::getenv("XM_NO_CUBLAS")) c->use_blas = false;
+  if (std::getenv("XM_SYM_TCG")) c->persist_sym = true;
   if (std::getenv("XM_NO_GRAPHS")) c->use_graphs = false;
   if (c->opt.rank_cap > XM_MAX_R) c->opt.rank_cap = XM_MAX_R;
   xm_status st = guard(c, [&] {
@@ -545,6 +546,7 @@ void xm_destroy(xm_ctx* c) {
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   nccl_destroy(c);
   sym_plan_destroy(c);
+  sym_tcg_plan_destroy(c);
   blas_destroy(c);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;

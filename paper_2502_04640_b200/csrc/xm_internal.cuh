@@ -196,6 +196,8 @@ struct xm_ctx {
   bool fused_tcg = true;    // XM_NO_FUSED_TCG=1: three-kernel tCG iteration (A/B measurement)
   bool persist_tcg = true;  // XM_NO_PERSIST_TCG=1: one launch per tCG iteration instead
   bool use_blas = true;     // XM_NO_CUBLAS=1: the library's own k_dgemm for the dense updates
+  bool persist_sym = false; // XM_SYM_TCG=1: lower-triangle persistent tCG (tcg_persist.cu)
+  void* persist_sym_plan = nullptr;
   xm::DBuf<double> dir2;    // δ ping-pong partner of dir (persistent tCG)
   cudaEvent_t ev_persist[2] = {nullptr, nullptr};
   // persistent tCG: 2-D tensor map of Q (box 128 columns × bh rows), raw CUtensorMap bytes
@@ -336,6 +338,7 @@ void nccl_destroy(xm_ctx* c);
 void nccl_allgather(xm_ctx* c, const double* send, double* recv, size_t count_per_rank);
 void nccl_allreduce_sum(xm_ctx* c, double* buf, size_t count);
 void sym_plan_destroy(xm_ctx* c);
+void sym_tcg_plan_destroy(xm_ctx* c);
 // cuBLAS (blas.cu) for plain dense GEMM / SYRK; false ⇒ not available
 bool blas_dgemm(xm_ctx* c, bool ta, bool tb, int M, int N, int K, double alpha, const double* A,
                 int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc);
