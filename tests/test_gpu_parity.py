@@ -129,7 +129,7 @@ def test_grad_hvp_project_retract_identical_Q(identical_Q, r):
 
 def _e2e(xm, sc, Y0=None, ctx_opts=None, **opts):
     dm, st, sol, rep = xo.solve(sc, Y0=Y0, opts=xo.Options(**opts) if opts else None)
-    with xm.Context(**opts, **(ctx_opts or {})) as ctx:
+    with xm.Context(**opts, **(ctx_opts or {})) as ctx:  # env switches are read here
         ctx.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
         if Y0 is not None:
             ctx.set_factor(Y0)
@@ -140,9 +140,19 @@ def _e2e(xm, sc, Y0=None, ctx_opts=None, **opts):
     return dm, st, sol, rep, status, info, cert, gsol, Yg
 
 
+# tCG code paths on one GPU (xm_create reads these switches): the persistent
+# full-row kernel (default), the persistent lower-triangle kernel, one fused
+# launch per iteration, and three kernels per iteration in CUDA graphs
+TCG_PATHS = {"persist": {}, "persist_sym": {"XM_SYM_TCG": "1"},
+             "fused": {"XM_NO_PERSIST_TCG": "1"}, "3kernel": {"XM_NO_FUSED_TCG": "1"}}
+
+
+@pytest.mark.parametrize("path", sorted(TCG_PATHS))
 @pytest.mark.parametrize("kernel", [0, 2], ids=["auto", "lowertri"])
 @pytest.mark.parametrize("cfg", SCENES[:3], ids=lambda c: f"{c['kind']}{c['N']}")
-def test_end_to_end_solve_parity(xm, cfg, kernel):
+def test_end_to_end_solve_parity(xm, cfg, kernel, path, monkeypatch):
+    for k, v in TCG_PATHS[path].items():
+        monkeypatch.setenv(k, v)
     sc = make_scene(seed=3, **cfg)
     dm, st, sol, rep, status, info, cert, gsol, Yg = _e2e(xm, sc, ctx_opts=dict(spmm_kernel=kernel))
     assert status == 0 and info["certified"] == 1 and st.certified
@@ -167,8 +177,11 @@ def test_end_to_end_solve_parity(xm, cfg, kernel):
         np.testing.assert_allclose(gsol["R"], sc.R, atol=1e-7)
 
 
-def test_random_init_staircase_parity(xm):
+@pytest.mark.parametrize("path", sorted(TCG_PATHS))
+def test_random_init_staircase_parity(xm, path, monkeypatch):
     """Thm 2/3: random init at r=3 escalates to r=4 on both sides, same X."""
+    for k, v in TCG_PATHS[path].items():
+        monkeypatch.setenv(k, v)
     sc = make_scene(10, 500, "unordered", seed=0, vis_prob=0.6)
     Y0 = random_factor(sc.N, 3, 1)
     dm, st, sol, rep, status, info, cert, gsol, Yg = _e2e(xm, sc, Y0=Y0)
@@ -193,12 +206,15 @@ def test_lanczos_min_eig_matches_dense(xm):
     assert abs(abs(float(cert["v"] @ v_d)) - 1.0) <= 1e-6
 
 
+@pytest.mark.parametrize("path", sorted(TCG_PATHS))
 @pytest.mark.parametrize("kernel", [1, 2], ids=["fullrow", "lowertri"])
-def test_repeated_solves_reuse_graphs_across_rank_climb(xm, kernel):
+def test_repeated_solves_reuse_graphs_across_rank_climb(xm, kernel, path, monkeypatch):
     """One context, build → solve twice (as bench.py's steps do) where the
     staircase climbs 3 → 4: the tCG graphs captured at r = 3 in the first solve
     are replayed in the second after the r = 4 products ran, and the results
     are bitwise identical (buffers captured by a graph never move)."""
+    for k, v in TCG_PATHS[path].items():
+        monkeypatch.setenv(k, v)
     sc = make_scene(10, 500, "unordered", seed=0, vis_prob=0.6)
     Y0 = random_factor(sc.N, 3, 1)
     runs = []
