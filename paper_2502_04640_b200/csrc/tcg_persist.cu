@@ -111,16 +111,18 @@ struct TcgPersistArgs {
   unsigned long long* gsync;   // grid barrier counter (0 on entry)
   unsigned long long* dbg;     // XM_PHASES: %globaltimer stamps [G][8] of iteration 1
   int bh;                      // rows per row block = the tensor map's box height
+  int stages;                  // ring depth (full-row kernel; host-sized to the smem budget)
 };
 
 template <int R>
 __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(const __grid_constant__ CUtensorMap tmq,
                                                               TcgPersistArgs a) {
-  using Cfg = PCfg<R>;
-  constexpr int S = Cfg::kStages;
+  // ring of S stages (runtime: as many as fit), stage = Q box (bh × 128) + r, δ chunks
+  const int S = a.stages;
+  const int stage_dbl = a.bh * kPCols + 2 * kPCols * R;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* stage_base = reinterpret_cast<double*>(smem_raw);
-  uint64_t* fullQ = reinterpret_cast<uint64_t*>(smem_raw + (size_t)S * Cfg::kStageBytes);
+  uint64_t* fullQ = reinterpret_cast<uint64_t*>(stage_base + (size_t)S * stage_dbl);
   uint64_t* fullV = fullQ + S;
   uint64_t* empty = fullV + S;
   double* red = reinterpret_cast<double*>(empty + S);  // [2 halves][kBlockRows][R]
@@ -179,8 +181,8 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(const __grid_const
       const int tt = (int)(iq % tiles);
       const int b = tt / nchunks, j = tt % nchunks;
       mbar_expect_tx(&fullQ[s], qbytes);
-      tma_load_2d(stage_base + (size_t)s * (Cfg::kStageBytes / 8), &tmq, j * kPCols,
-                  row_base + b * bh, &fullQ[s], pol_q);
+      tma_load_2d(stage_base + (size_t)s * stage_dbl, &tmq, j * kPCols, row_base + b * bh,
+                  &fullQ[s], pol_q);
       sh_iq = iq + 1;
     }
     // Q copies issued for tiles nobody will consume must land first
@@ -215,7 +217,7 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(const __grid_const
       const int k0 = j * kPCols;
       const int klen = min(kPCols, n - k0);
       const unsigned vb = (unsigned)(((klen * R + 1) & ~1) * 8);
-      double* st = stage_base + (size_t)s * (Cfg::kStageBytes / 8) + kBlockRows * kPCols;
+      double* st = stage_base + (size_t)s * stage_dbl + bh * kPCols;
       const double* dprev = (kv & 1) ? a.D0 : a.D1;  // δ_{k−1} = D[(k−1) & 1]
       mbar_expect_tx(&fullV[s], 2 * vb);
       tma_load_1d(st, a.res + (int64_t)k0 * R, vb, &fullV[s], pol_v);
@@ -266,8 +268,8 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(const __grid_const
         mbar_wait(&fullQ[sidx], ph);
         mbar_wait(&fullV[sidx], ph);
         const int klen = min(kPCols, n - j * kPCols);
-        const double* stg = stage_base + (size_t)sidx * (Cfg::kStageBytes / 8);
-        const double* rs = stg + kBlockRows * kPCols;
+        const double* stg = stage_base + (size_t)sidx * stage_dbl;
+        const double* rs = stg + bh * kPCols;
         const double* ds = rs + kPCols * R;
         const double* qrow = stg + (size_t)q0 * kPCols + col;
         if (col + 1 < klen) {
@@ -904,12 +906,26 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist_sym(const __grid_c
 
 // ---------------------------------------------------------------------- host
 namespace {
+constexpr size_t kSmemCap = 227 * 1024 - 1024;  // dynamic budget (static smem ≈ 0.3 KB)
+int persist_bh_(int n, int G) {
+  const int rows_max = ceil_div(n, G);
+  return ceil_div(rows_max, ceil_div(rows_max, kBlockRows));
+}
+// ring depth: as many stages (≤ 6) as fit next to the reduction scratch
+template <int R>
+int persist_stages(int n, int G) {
+  const size_t stage = (size_t)8 * (persist_bh_(n, G) * kPCols + 2 * kPCols * R);
+  const size_t other = (size_t)2 * kBlockRows * R * 8 + (size_t)(ceil_div(n, G) + 1) * R * 8;
+  const long long s = ((long long)kSmemCap - (long long)other) / (long long)(stage + 24);
+  return (int)std::max(0ll, std::min(6ll, s));
+}
 template <int R>
 size_t persist_smem(int n, int G) {
-  using Cfg = PCfg<R>;
-  const int rows_max = ceil_div(n, G) + 1;
-  return (size_t)Cfg::kStages * Cfg::kStageBytes + 3 * Cfg::kStages * 8 +
-         (size_t)2 * kBlockRows * R * 8 + (size_t)rows_max * R * 8;
+  const int S = persist_stages<R>(n, G);
+  if (S < 2) return ~(size_t)0;
+  const size_t stage = (size_t)8 * (persist_bh_(n, G) * kPCols + 2 * kPCols * R);
+  return (size_t)S * stage + 3 * (size_t)S * 8 + (size_t)2 * kBlockRows * R * 8 +
+         (size_t)(ceil_div(n, G) + 1) * R * 8;
 }
 size_t persist_smem_r(int r, int n, int G) {
   switch (r) {
@@ -921,7 +937,6 @@ size_t persist_smem_r(int r, int n, int G) {
     default: return ~(size_t)0;
   }
 }
-constexpr size_t kSmemCap = 227 * 1024 - 1024;  // dynamic budget (static smem ≈ 0.3 KB)
 }  // namespace
 
 bool tcg_persist_sym_supported(xm_ctx* c, int r);
@@ -1011,6 +1026,7 @@ static void launch_persist(xm_ctx* c) {
   a.pB = c->part2.p;
   a.gsync = c->gsync.p;
   a.bh = c->persist_tmap_bh;
+  a.stages = persist_stages<R>(c->n, G);
   if (c->phases_on) {
     if (!c->tdbg.p) {
       c->tdbg.alloc(148 * 8);
