@@ -917,7 +917,11 @@ int persist_stages(int n, int G) {
   const size_t stage = (size_t)8 * (persist_bh_(n, G) * kPCols + 2 * kPCols * R);
   const size_t other = (size_t)2 * kBlockRows * R * 8 + (size_t)(ceil_div(n, G) + 1) * R * 8;
   const long long s = ((long long)kSmemCap - (long long)other) / (long long)(stage + 24);
-  return (int)std::max(0ll, std::min(6ll, s));
+  static const long long cap = [] {  // XM_PERSIST_STAGES: A/B switch for measurements
+    const char* e = std::getenv("XM_PERSIST_STAGES");
+    return e ? std::max(2ll, std::atoll(e)) : 3ll;
+  }();
+  return (int)std::max(0ll, std::min(cap, s));
 }
 template <int R>
 size_t persist_smem(int n, int G) {
