@@ -42,13 +42,6 @@ constexpr int kBlockRows = 48;          // rows per row block (4 quarters × ≤
 constexpr int kQuarterRows = kBlockRows / 4;
 constexpr int kPCols = 128;             // columns per tile (2 halves × 32 lanes × 2)
 
-template <int R>
-struct PCfg {
-  static constexpr int kQBytes = kBlockRows * kPCols * 8;  // 48 KB
-  static constexpr int kVBytes = kPCols * R * 8;           // one chunk of r or δ
-  static constexpr int kStageBytes = kQBytes + 2 * kVBytes;
-  static constexpr int kStages = (kStageBytes * 4 <= 212 * 1024) ? 4 : 3;
-};
 
 __device__ __forceinline__ void cbar() {  // consumers only (the producers keep streaming)
   asm volatile("bar.sync 1, %0;\n" ::"n"(kPC) : "memory");
@@ -919,7 +912,7 @@ int persist_stages(int n, int G) {
   const long long s = ((long long)kSmemCap - (long long)other) / (long long)(stage + 24);
   static const long long cap = [] {  // XM_PERSIST_STAGES: A/B switch for measurements
     const char* e = std::getenv("XM_PERSIST_STAGES");
-    return e ? std::max(2ll, std::atoll(e)) : 3ll;
+    return e ? std::max(2ll, std::atoll(e)) : 4ll;
   }();
   return (int)std::max(0ll, std::min(cap, s));
 }
