@@ -457,14 +457,14 @@ __global__ void __launch_bounds__(256) k_chol_panel(double* __restrict__ Akk, in
   double* row = Akk + (int64_t)(nb + r) * lda;
   double x[NBT];
 #pragma unroll
+  for (int j = 0; j < NBT; ++j) x[j] = (j < nb) ? row[j] : 0.0;  // all loads in flight at once
+#pragma unroll
   for (int j = 0; j < NBT; ++j) {
     if (j < nb) {
-      double s2 = row[j];
+      double s2 = x[j];
 #pragma unroll
       for (int q = 0; q < j; ++q) s2 = fma(-x[q], a[j][q], s2);
       x[j] = s2 / a[j][j];
-    } else {
-      x[j] = 0.0;
     }
   }
 #pragma unroll
@@ -571,14 +571,14 @@ __global__ void __launch_bounds__(128) k_trsm_block_cols(const double* __restric
   if (col >= ncols) return;
   double x[NBT];
 #pragma unroll
+  for (int j = 0; j < NBT; ++j) x[j] = (j < nb) ? B[(int64_t)j * ldb + col] : 0.0;
+#pragma unroll
   for (int j = 0; j < NBT; ++j) {
     if (j < nb) {
-      double s = B[(int64_t)j * ldb + col];
+      double s = x[j];
 #pragma unroll
       for (int q = 0; q < j; ++q) s -= l[j][q] * x[q];
       x[j] = s / l[j][j];
-    } else {
-      x[j] = 0.0;
     }
   }
 #pragma unroll

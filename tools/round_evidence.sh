@@ -13,7 +13,7 @@ timeout 900 python bench.py --config E --no-cpu-baseline > $OUT/bench_E.json 2> 
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $OUT/launches_B.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e \
   > $OUT/ncu_launch.log 2>&1
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_spmm \
-  --launch-skip ${SKIP:-3000} --launch-count ${COUNT:-6} -o $OUT/ncu_full_B -f \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_tcg_persist \
+  --launch-skip ${SKIP:-30} --launch-count ${COUNT:-2} -o $OUT/ncu_full_B -f \
   python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/ncu_full.log 2>&1
 ls -la $OUT
