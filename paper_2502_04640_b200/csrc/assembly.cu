@@ -423,32 +423,47 @@ __global__ void __launch_bounds__(256) k_chol_panel(double* __restrict__ Akk, in
     a[i][j] = (i < nb && j < nb && j <= i) ? Akk[(int64_t)i * lda + j] : (i == j ? 1.0 : 0.0);
   }
   __syncthreads();
+  // Right-looking factorisation with ONE barrier per column: every thread
+  // derives 1/√d_j itself, updates its 4×4 sub-block with the unscaled column
+  // (a_il −= (a_ij·s)(a_lj·s), s = 1/√d_j), and scales its part of column j
+  // one step later (column j is no longer read by then).
+  double inv_prev = 1.0, sq_prev = 1.0;
   for (int j = 0; j < nb; ++j) {
-    if (tid == 0) {
-      double d = a[j][j];
-      if (!(d > pivot_tol)) {
-        if (blockIdx.x == 0) atomicOr(err, 1);
-        d = 1.0;
+    if (j > 0 && tl == (j - 1) >> 2) {  // finish column j−1 (and its diagonal)
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        const int i = 4 * ti + x;
+        if (i > j - 1 && i < nb) a[i][j - 1] *= inv_prev;
       }
-      a[j][j] = sqrt(d);
+      if (ti == (j - 1) >> 2) a[j - 1][j - 1] = sq_prev;
     }
-    __syncthreads();
-    if (tid > j && tid < nb) a[tid][j] /= a[j][j];
-    __syncthreads();
+    double d = a[j][j];
+    if (!(d > pivot_tol)) {
+      if (tid == 0 && blockIdx.x == 0) atomicOr(err, 1);
+      d = 1.0;
+    }
+    const double sq = sqrt(d);
+    const double inv = 1.0 / sq;
 #pragma unroll
     for (int x = 0; x < 4; ++x) {
       const int i = 4 * ti + x;
       if (i > j && i < nb) {
-        const double aij = a[i][j];
+        const double lij = a[i][j] * inv;
 #pragma unroll
         for (int y = 0; y < 4; ++y) {
           const int l = 4 * tl + y;
-          if (l > j && l <= i) a[i][l] = fma(-aij, a[l][j], a[i][l]);
+          if (l > j && l <= i) a[i][l] = fma(-lij, a[l][j] * inv, a[i][l]);
         }
       }
     }
+    inv_prev = inv;
+    sq_prev = sq;
     __syncthreads();
   }
+  if (nb > 0 && tl == (nb - 1) >> 2) {  // last column: only its diagonal
+    if (ti == (nb - 1) >> 2) a[nb - 1][nb - 1] = sq_prev;
+  }
+  __syncthreads();
   if (blockIdx.x == 0)  // into a side slot: other CTAs may still be reading Akk
     for (int t = tid; t < NBT * NBT; t += 256) L11_out[t] = a[t >> 6][t & 63];
   // panel rows: X·L11ᵀ = A21
