@@ -419,16 +419,21 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(
   }
 }
 
-int spmm_grid(xm_ctx* c, int r) {
-  if (spmm_sym_supported(c, r)) return spmm_sym_partials(c);  // k_sym_finish blocks
+// grid of the full-row kernel (k_spmm, every epilogue incl. EPI_TCG)
+static int spmm_fullrow_grid(xm_ctx* c) {
   int nown = std::max(1, c->f1 - c->f0);
   return std::max(1, std::min(148, nown));
+}
+// grid (= number of per-CTA scalar partials) of a plain product at rank r
+int spmm_grid(xm_ctx* c, int r) {
+  if (spmm_sym_supported(c, r)) return spmm_sym_partials(c);
+  return spmm_fullrow_grid(c);
 }
 
 template <int R, int MODE>
 static void launch_r(xm_ctx* c, const double* V, const SpmmEpiArgs& ep) {
   using Cfg = SpmmCfg<R>;
-  const int G = spmm_grid(c, R);
+  const int G = spmm_fullrow_grid(c);
   const int nown = c->f1 - c->f0;
   const int rows_max = 3 * ((nown + G - 1) / G);
   size_t smem = (size_t)Cfg::kStages * Cfg::kStageBytes + 2 * Cfg::kStages * 8 +
@@ -482,9 +487,9 @@ static void launch_tcg(xm_ctx* c, const double* V, int r, const SpmmEpiArgs& ep)
 }
 
 bool tcg_fused_supported(xm_ctx* c, int r) {
-  if (!c->fused_tcg || c->world != 1 || r < 1 || r > 6 || spmm_sym_supported(c, r) || c->N < 1)
+  if (!c->fused_tcg || c->world != 1 || r < 1 || r > 6 || !tcg_fullrow_ok(c) || c->N < 1)
     return false;
-  const int G = spmm_grid(c, r);
+  const int G = spmm_fullrow_grid(c);
   return ceil_div(c->N, G) <= kSpmmThreads;
 }
 
@@ -494,7 +499,8 @@ bool tcg_fused_supported(xm_ctx* c, int r) {
 // writes η, Hη, r, δ (+ Λ): 8·n·n + 9·8·n·r + 48·N.
 static double alg_bytes(xm_ctx* c, int r, int mode) {
   const double n = c->n;
-  const double qb = spmm_sym_supported(c, r) ? 8.0 * n * (n + 1) / 2 : 8.0 * (double)c->nrows * n;
+  const double qb = (mode != EPI_TCG && spmm_sym_supported(c, r)) ? 8.0 * n * (n + 1) / 2
+                                                                  : 8.0 * (double)c->nrows * n;
   if (mode == EPI_TCG) return qb + 9.0 * 8.0 * n * r + 48.0 * c->N;
   return qb + 8.0 * n * r + 8.0 * (double)c->nrows * r;
 }
@@ -539,7 +545,7 @@ void spmm(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep_in)
     c->ev_bytes[pair] = alg_bytes(c, r, mode);
     XM_CUDA(cudaEventRecord(e0, c->stream));
   }
-  if (spmm_sym_supported(c, r)) {
+  if (mode != EPI_TCG && spmm_sym_supported(c, r)) {
     spmm_sym_launch(c, V, r, mode, ep);
   } else switch (mode) {
     case EPI_STORE: launch_mode<EPI_STORE>(c, V, r, ep); break;

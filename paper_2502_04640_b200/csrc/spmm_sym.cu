@@ -5,31 +5,36 @@
 //   out_i = Σ_{j ≤ i} Q_ij V_j  +  Σ_{j > i} Q_ji V_j
 //         = row part (lower triangle) + column part (strictly lower triangle)
 //
-// Geometry.  Units are the lower-triangular 128-row × 256-column blocks
-// (I, J), J ≤ ⌊I/2⌋; a unit is 8 tiles of 16 rows × 256 columns (32 KB).  The
-// W = 16·U tiles are split stream-K style into G = 148 equal contiguous ranges
-// (one persistent CTA per SM), so every SM streams the same number of tiles.
-// A CTA's range is a sequence of *segments* (maximal runs of tiles of one
-// unit); a unit cut between two CTAs simply yields two segments.
+// Geometry (column-strip order).  The lower triangle is cut into column
+// panels J of BC = 256 columns; panel J is the run of TR = 32-row tiles that
+// start at its diagonal block (row tiles 8J … ⌈n/32⌉−1).  Tiles are numbered
+// panel-major and the W tiles are split stream-K style into G = 148 equal
+// contiguous ranges (one persistent CTA per SM).  A CTA's range is a short
+// sequence of *segments* (runs of tiles of one panel; 1–3 per CTA at the
+// bench sizes), so:
+//   * V_J for the lane's 8 columns and the column partials stay in registers
+//     for the whole segment — one column partial per segment (negligible
+//     traffic), not one per tile;
+//   * the row part of a tile is a finished 32 × r partial of (rows, panel J),
+//     written once (rowpart[tile]): R/256 extra bytes per Q byte.
 //
-// Per tile (warp w ↔ rows w, w+8; lane ℓ ↔ the 8 columns {2ℓ+64m, 2ℓ+64m+1},
+// Per tile (warp w ↔ rows 4w … 4w+3; lane ℓ ↔ the 8 columns {2ℓ+64m, 2ℓ+64m+1},
 // m = 0..3 — conflict-free LDS.128):
-//   row part   r_i += Σ_j Q_ij V_j  with V_J for the lane's columns held in
-//              registers for the whole segment; one 5-level shuffle reduction
-//              per row, then lane 0 writes rowpart[u][ℓ] (each row of a unit
-//              lives in exactly one tile ⇒ single writer);
+//   row part   r_i += Σ_j Q_ij V_j over the lane's columns for RP rows at a
+//              time, then ONE butterfly reduce-scatter over the warp for the
+//              RP rows together (xor 16 / 8 halve the row set, the remaining
+//              levels sum): 6r shuffles per 4 rows instead of 5r per row;
 //   column part c_j += Q_ij V_i (j < i), accumulated in registers over the
-//              segment's rows (V_i broadcast from shared memory), then summed
-//              over the 8 warps in a fixed order and written to colpart[segment].
-// The producer thread streams each tile with ONE 2-D tensor TMA copy
-// (cp.async.bulk.tensor.2d, L2 evict-first; rows / columns past n zero-filled)
-// into a 5-stage ring (5 × 32 KB); the per-segment V_J / V_I blocks go through
-// a 2-slot ring (1-D bulk copies).
+//              segment (V_i broadcast from shared memory).
+// Thread 0 streams each tile with ONE 2-D tensor TMA copy (box 256 × 32, L2
+// evict-first; rows / columns past n zero-filled) plus the tile's 32 × r
+// slice of V (1-D bulk copy) into a 3-stage ring (3 × 65 KB).
 //
 // After a software grid barrier the same CTAs sum, in a fixed order, the row
-// parts of units (K, 0..⌊K/2⌋) and the column parts of every segment of column
-// block ⌊row/256⌋, and apply the per-camera epilogue (same modes as spmm.cu).
-// Deterministic; algorithmic bytes per product: 8·n(n+1)/2 + 16·n·r.
+// parts of the tiles (K, J ≤ ⌊row/256⌋) and the column parts of the segments
+// of panel ⌊row/256⌋ (consecutive segment numbers), and apply the per-camera
+// epilogue (same modes as spmm.cu).  Deterministic; algorithmic bytes per
+// product: 8·n(n+1)/2 + 16·n·r.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -42,12 +47,15 @@ namespace xm {
 
 namespace {
 constexpr int kWarps = 8;
-constexpr int kThreads = 32 * (kWarps + 1);
-constexpr int BR = 128;                 // unit rows
-constexpr int BC = 256;                 // unit columns
-constexpr int TR = 16;                  // rows per tile (two per warp)
-constexpr int kTilesPerUnit = BR / TR;  // 8
-constexpr int kTileBytes = TR * BC * 8;  // 32 KB
+constexpr int kThreads = 32 * kWarps;
+constexpr int BC = 256;                  // panel width (columns)
+constexpr int TR = 32;                   // rows per tile (4 per consumer warp)
+constexpr int kRowsPerWarp = TR / kWarps;
+constexpr int kDiagTiles = BC / TR;      // tiles of a panel's diagonal block
+constexpr int kTileBytes = TR * BC * 8;  // 64 KB
+constexpr int kStages = 3;
+constexpr int kVsliceDoubles = TR * 6;   // V_I slice (r ≤ 5), padded; stage stride stays 128-B aligned
+constexpr int kStageDoubles = TR * BC + kVsliceDoubles;
 
 __device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void bar_init(uint64_t* b, unsigned cnt) {
@@ -93,30 +101,69 @@ __device__ __forceinline__ void tma_tile(void* dst, const CUtensorMap* tm, int x
       "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(su32(b)), "l"(pol)
       : "memory");
 }
-// unit u → (I, J) using unit_base[I] = Σ_{I'<I} (⌊I'·BR/BC⌋ + 1)
-__device__ __forceinline__ void unit_ij(int u, const int* __restrict__ ubase, int TRb, int& I, int& J) {
-  int lo = 0, hi = TRb - 1;
-  while (lo < hi) {  // largest I with ubase[I] ≤ u
+// tile t → panel J using pbase[J] = Σ_{J'<J} (TRt − 8J')
+__device__ __forceinline__ int tile_panel(int64_t t, const int* __restrict__ pbase, int TCb) {
+  int lo = 0, hi = TCb - 1;
+  while (lo < hi) {  // largest J with pbase[J] ≤ t
     int mid = (lo + hi + 1) >> 1;
-    if (ubase[mid] <= u) lo = mid; else hi = mid - 1;
+    if (pbase[mid] <= t) lo = mid; else hi = mid - 1;
   }
-  I = lo;
-  J = u - ubase[lo];
+  return lo;
+}
+
+// First row-part slot of row tile K: Σ_{K'<K} (⌊K'/8⌋ + 1) (panels 0..⌊K'/8⌋
+// intersect row tile K'), so the row parts of one row tile are contiguous.
+__device__ __forceinline__ int64_t rtile_base(int K) {
+  const int64_t a = K >> 3, b = K & 7;
+  return (int64_t)K + 4 * a * (a - 1) + a * b;
+}
+
+// Butterfly reduce-scatter of RP rows × R partial sums over the 32 lanes:
+// on return lane ℓ holds the full sums of row ((ℓ >> (5 − log2 RP)) & (RP−1))
+// in a[0][·].  Fixed order ⇒ deterministic.
+template <int RP, int R>
+__device__ __forceinline__ void warp_rows_reduce(double (&a)[RP][R], int lane) {
+  if constexpr (RP == 4) {
+    const bool h16 = (lane & 16) != 0;
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+      for (int cc = 0; cc < R; ++cc) {
+        const double snd = h16 ? a[k][cc] : a[k + 2][cc];
+        const double kp = h16 ? a[k + 2][cc] : a[k][cc];
+        a[k][cc] = kp + __shfl_xor_sync(0xffffffffu, snd, 16);
+      }
+  }
+  if constexpr (RP >= 2) {
+    constexpr int o = (RP == 4) ? 8 : 16;
+    const bool hb = (lane & o) != 0;
+#pragma unroll
+    for (int cc = 0; cc < R; ++cc) {
+      const double snd = hb ? a[0][cc] : a[1][cc];
+      const double kp = hb ? a[1][cc] : a[0][cc];
+      a[0][cc] = kp + __shfl_xor_sync(0xffffffffu, snd, o);
+    }
+  }
+  constexpr int top = (RP == 4) ? 4 : (RP == 2 ? 8 : 16);
+#pragma unroll
+  for (int o = top; o > 0; o >>= 1)
+#pragma unroll
+    for (int cc = 0; cc < R; ++cc) a[0][cc] += __shfl_xor_sync(0xffffffffu, a[0][cc], o);
 }
 }  // namespace
 
-// Static work plan for one (n, G): unit bases, per-CTA segment bases and the
-// per-column-block list of segments (fixed summation order for the finish).
+// Static work plan for one (n, G): panel bases, per-CTA segment bases and the
+// first segment of every panel (segments are numbered in tile order, so the
+// segments of one panel are consecutive — fixed summation order for the finish).
 struct SymPlan {
-  int n = 0, G = 0, TRb = 0, TCb = 0, U = 0, S = 0;
+  int n = 0, G = 0, TRt = 0, TCb = 0, S = 0;
+  int64_t W = 0;
   const void* qptr = nullptr;  // Q the tensor map was encoded for
   int64_t ldq = 0;
   CUtensorMap tmq;
-  DBuf<int> ubase;     // TRb + 1
-  DBuf<int> segbase;   // G + 1
-  DBuf<int> segunit;   // S
-  DBuf<int> colptr;    // TCb + 1
-  DBuf<int> colidx;    // S (segments grouped by column block, ordered by unit then CTA)
+  DBuf<int> pbase;    // TCb + 1
+  DBuf<int> segbase;  // G + 1
+  DBuf<int> colptr;   // TCb + 1: segments [colptr[J], colptr[J+1]) belong to panel J
 };
 
 static SymPlan& sym_plan(xm_ctx* c) {
@@ -125,8 +172,8 @@ static SymPlan& sym_plan(xm_ctx* c) {
   int sms = 148;
   XM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
   const int n = c->n, G = std::min(148, sms);
-  if (p.n == n && p.G == G && p.ubase.p && p.qptr == c->Q.p && p.ldq == c->ldq) return p;
-  // Q tensor map: dims {n columns, n rows}, row pitch ldq·8 B, box TR × BC,
+  if (p.n == n && p.G == G && p.pbase.p && p.qptr == c->Q.p && p.ldq == c->ldq) return p;
+  // Q tensor map: dims {n columns, n rows}, row pitch ldq·8 B, box BC × TR,
   // OOB → zero fill (rows / columns ≥ n read as 0)
   {
     static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
@@ -150,88 +197,70 @@ static SymPlan& sym_plan(xm_ctx* c) {
     p.qptr = c->Q.p;
     p.ldq = c->ldq;
   }
-  if (p.n == n && p.G == G && p.ubase.p) return p;
+  if (p.n == n && p.G == G && p.pbase.p) return p;
   p.n = n;
   p.G = G;
-  p.TRb = ceil_div(n, BR);
+  p.TRt = ceil_div(n, TR);
   p.TCb = ceil_div(n, BC);
-  std::vector<int> ub(p.TRb + 1, 0);
-  for (int I = 0; I < p.TRb; ++I) ub[I + 1] = ub[I] + (I * BR) / BC + 1;
-  p.U = ub[p.TRb];
-  const int64_t W = (int64_t)p.U * kTilesPerUnit;
-  std::vector<int> segbase(G + 1, 0), segunit;
+  std::vector<int> pb(p.TCb + 1, 0);
+  for (int J = 0; J < p.TCb; ++J) pb[J + 1] = pb[J] + (p.TRt - kDiagTiles * J);
+  p.W = pb[p.TCb];
+  std::vector<int> segbase(G + 1, 0), segpanel;
   for (int cta = 0; cta < G; ++cta) {
-    int64_t t0 = (int64_t)cta * W / G, t1 = (int64_t)(cta + 1) * W / G;
-    segbase[cta] = (int)segunit.size();
-    int last = -1;
-    for (int64_t t = t0; t < t1; ++t) {
-      int u = (int)(t / kTilesPerUnit);
-      if (u != last) {
-        segunit.push_back(u);
-        last = u;
-      }
+    const int64_t t0 = (int64_t)cta * p.W / G, t1 = (int64_t)(cta + 1) * p.W / G;
+    segbase[cta] = (int)segpanel.size();
+    int J = 0;
+    while (J + 1 < p.TCb && pb[J + 1] <= t0) ++J;
+    for (int64_t t = t0; t < t1;) {
+      while (pb[J + 1] <= t) ++J;
+      segpanel.push_back(J);
+      t = std::min<int64_t>(t1, pb[J + 1]);
     }
   }
-  segbase[G] = (int)segunit.size();
-  p.S = (int)segunit.size();
-  auto unitJ = [&](int u) {
-    int I = 0;
-    while (ub[I + 1] <= u) ++I;
-    return u - ub[I];
-  };
-  std::vector<std::vector<int>> bycol(p.TCb);
-  for (int s = 0; s < p.S; ++s) bycol[unitJ(segunit[s])].push_back(s);  // s increasing ⇒ unit, then CTA order
-  std::vector<int> colptr(p.TCb + 1, 0), colidx;
-  for (int J = 0; J < p.TCb; ++J) {
-    for (int s : bycol[J]) colidx.push_back(s);
-    colptr[J + 1] = (int)colidx.size();
+  segbase[G] = (int)segpanel.size();
+  p.S = (int)segpanel.size();
+  std::vector<int> colptr(p.TCb + 1, 0);
+  for (int s = 0, J = 0; J <= p.TCb; ++J) {  // segpanel is non-decreasing
+    while (s < p.S && segpanel[s] < J) ++s;
+    colptr[J] = s;
   }
-  p.ubase.alloc(ub.size());
+  p.pbase.alloc(pb.size());
   p.segbase.alloc(segbase.size());
-  p.segunit.alloc(std::max<size_t>(1, segunit.size()));
   p.colptr.alloc(colptr.size());
-  p.colidx.alloc(std::max<size_t>(1, colidx.size()));
-  XM_CUDA(cudaMemcpy(p.ubase.p, ub.data(), ub.size() * 4, cudaMemcpyHostToDevice));
+  XM_CUDA(cudaMemcpy(p.pbase.p, pb.data(), pb.size() * 4, cudaMemcpyHostToDevice));
   XM_CUDA(cudaMemcpy(p.segbase.p, segbase.data(), segbase.size() * 4, cudaMemcpyHostToDevice));
-  if (!segunit.empty())
-    XM_CUDA(cudaMemcpy(p.segunit.p, segunit.data(), segunit.size() * 4, cudaMemcpyHostToDevice));
   XM_CUDA(cudaMemcpy(p.colptr.p, colptr.data(), colptr.size() * 4, cudaMemcpyHostToDevice));
-  if (!colidx.empty())
-    XM_CUDA(cudaMemcpy(p.colidx.p, colidx.data(), colidx.size() * 4, cudaMemcpyHostToDevice));
   return p;
 }
 
 template <int R>
 struct SymCfg {
-  static constexpr int kVJ = BC * R;   // doubles
-  static constexpr int kVI = BR * R;
-  static constexpr int kStages = (R <= 3) ? 5 : 4;
-  static constexpr size_t kSmem = (size_t)kStages * kTileBytes + 2 * (size_t)(kVJ + kVI) * 8 +
-                                  4 * (size_t)BC * R * 8 + 64 * 8;
+#ifndef XM_SYM_RP4_MAXR
+#define XM_SYM_RP4_MAXR 4
+#endif
+  static constexpr int kRP = (R <= XM_SYM_RP4_MAXR) ? 4 : 2;  // rows reduced together (register budget)
+  static constexpr size_t kSmem =
+      (size_t)kStages * kStageDoubles * 8 + (size_t)BC * R * 8 + 64 * 8;
 };
 
 template <int R, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
-    const __grid_constant__ CUtensorMap tmq, int N, int n, int TRb, int U,
-    const int* __restrict__ ubase, const int* __restrict__ segbase, const int* __restrict__ colptr,
-    const int* __restrict__ colidx, const double* __restrict__ V, double* __restrict__ rowpart,
-    double* __restrict__ colpart, GridBar* __restrict__ gbar, SpmmEpiArgs ep) {
+    const __grid_constant__ CUtensorMap tmq, int N, int n, int TRt, int TCb, int64_t W,
+    const int* __restrict__ pbase, const int* __restrict__ segbase, const int* __restrict__ colptr,
+    const double* __restrict__ V, double* __restrict__ rowpart, double* __restrict__ colpart,
+    GridBar* __restrict__ gbar, SpmmEpiArgs ep) {
   using Cfg = SymCfg<R>;
-  constexpr int kStages = Cfg::kStages;
+  constexpr int RP = Cfg::kRP;
   if (ep.stop && *ep.stop) return;
   if (ep.exec && blockIdx.x == 0 && threadIdx.x == 0) *ep.exec = 1;
   extern __shared__ __align__(128) unsigned char sm[];
-  double* tiles = reinterpret_cast<double*>(sm);
-  double* vbuf = tiles + (size_t)kStages * TR * BC;  // 2 slots × (V_J, V_I)
-  double* colred = vbuf + 2 * (Cfg::kVJ + Cfg::kVI);  // [4 slots][BC][R]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(colred + 4 * BC * R);
+  double* stages = reinterpret_cast<double*>(sm);
+  double* colred = stages + (size_t)kStages * kStageDoubles;  // [BC][R]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(colred + BC * R);
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages;
-  uint64_t* vfull = bars + 2 * kStages;
-  uint64_t* vempty = vfull + 2;
 
   const int G = gridDim.x;
-  const int64_t W = (int64_t)U * kTilesPerUnit;
   const int64_t t0 = (int64_t)blockIdx.x * W / G;
   const int64_t t1 = (int64_t)(blockIdx.x + 1) * W / G;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -240,134 +269,118 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
       bar_init(&full[s], 1);
       bar_init(&empty[s], kWarps);
     }
-    for (int s = 0; s < 2; ++s) {
-      bar_init(&vfull[s], 1);
-      bar_init(&vempty[s], kWarps);
-    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
 
-  if (warp == kWarps) {
-    // ------------------------------------------------------------ producer
-    if (lane == 0 && t0 < t1) {
-      const uint64_t pq = pol_first(), pv = pol_last();
-      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmq)) : "memory");
-      int it = 0, seg = 0, cur_u = -1, I = 0, J = 0;
-      for (int64_t t = t0; t < t1; ++t, ++it) {
-        const int u = (int)(t / kTilesPerUnit);
-        const int tl = (int)(t % kTilesPerUnit);
-        if (u != cur_u) {  // new segment: locate the unit, stage V_J and V_I
-          unit_ij(u, ubase, TRb, I, J);
-          const int vs = seg & 1;
-          bar_wait(&vempty[vs], (unsigned)(((seg >> 1) & 1) ^ 1));
-          const int nj = min(BC, n - J * BC), ni = min(BR, n - I * BR);
-          const unsigned bj = (unsigned)(((nj * R + 1) & ~1) * 8);
-          const unsigned bi = (unsigned)(((ni * R + 1) & ~1) * 8);
-          bar_expect(&vfull[vs], bj + bi);
-          double* vj = vbuf + (size_t)vs * (Cfg::kVJ + Cfg::kVI);
-          bulk_g2s(vj, V + (int64_t)J * BC * R, bj, &vfull[vs], pv);
-          bulk_g2s(vj + Cfg::kVJ, V + (int64_t)I * BR * R, bi, &vfull[vs], pv);
-          cur_u = u;
-          ++seg;
-        }
-        const int s = it % kStages;
-        bar_wait(&empty[s], (unsigned)(((it / kStages) & 1) ^ 1));
-        bar_expect(&full[s], (unsigned)kTileBytes);
-        tma_tile(tiles + (size_t)s * TR * BC, &tmq, J * BC, I * BR + tl * TR, &full[s], pq);
-      }
+  // ------------------------------------------------------------ producer
+  // Thread 0 (of consumer warp 0) issues the loads: the first kStages tiles
+  // here, then tile it + kStages into slot it % kStages once all 8 warps have
+  // released tile it.  No separate producer warp: 8 warps = 2 per SM
+  // sub-partition, so each thread may use up to 255 registers (9 warps would
+  // put 3 warps on one sub-partition and cap the kernel at 168).
+  int pJ = 0, ppend = 0;
+  int64_t pt_next = t0;
+  uint64_t pq = 0, pv = 0;
+  auto issue = [&](int it_load) {
+    const int64_t t = pt_next++;
+    if (t >= ppend) {
+      ++pJ;
+      ppend = pbase[pJ + 1];
     }
-  } else {
+    const int rt = kDiagTiles * pJ + (int)(t - pbase[pJ]);  // row tile
+    const int s = it_load % kStages;
+    const int ni = min(TR, n - rt * TR);
+    const unsigned bv = (unsigned)(((ni * R + 1) & ~1) * 8);
+    bar_expect(&full[s], (unsigned)kTileBytes + bv);
+    double* st = stages + (size_t)s * kStageDoubles;
+    tma_tile(st, &tmq, pJ * BC, rt * TR, &full[s], pq);
+    bulk_g2s(st + TR * BC, V + (int64_t)rt * TR * R, bv, &full[s], pv);
+  };
+  const int ntiles = (int)(t1 - t0);
+  if (threadIdx.x == 0 && ntiles > 0) {
+    pq = pol_first();
+    pv = pol_last();
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmq)) : "memory");
+    pJ = tile_panel(t0, pbase, TCb) - 1;
+    ppend = pbase[pJ + 1];
+    for (int k = 0; k < min(kStages, ntiles); ++k) issue(k);
+  }
+  {
     // ------------------------------------------------------------ consumers
-    int it = 0, seg = 0, cur_u = -1;
-    int I = 0, J = 0;
-    bool dblk = false;
-    double vr[8][R];      // V_J rows for the lane's 8 columns
+    double vr[8][R];      // V_J rows for the lane's 8 columns (whole segment)
     double colacc[8][R];  // column partials for the lane's 8 columns
-    const double* vi = nullptr;
-    int vs = 0;
-    auto flush = [&](int slot_seg) {
-      // fixed-order cross-warp sum of colacc: warps w and w+4 share slot w
-      // (w stores, w+4 adds), then slots 0..3 are summed left to right
-      double* cr = colred + (warp & 3) * BC * R;
-      if (warp < 4) {
+    int seg = 0, J = -1, pend = 0;
+    int it = 0;
+    auto flush = [&]() {
+      // fixed-order cross-warp sum of colacc (warp 0 stores, warps 1..7 add in
+      // turn), then the segment's column partial is written out
+#pragma unroll 1
+      for (int w = 0; w < kWarps; ++w) {
+        if (warp == w) {
 #pragma unroll
-        for (int m = 0; m < 4; ++m)
+          for (int m = 0; m < 4; ++m)
 #pragma unroll
-          for (int h = 0; h < 2; ++h)
+            for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int cc = 0; cc < R; ++cc) cr[(2 * lane + 64 * m + h) * R + cc] = colacc[2 * m + h][cc];
+              for (int cc = 0; cc < R; ++cc) {
+                double* d = &colred[(2 * lane + 64 * m + h) * R + cc];
+                *d = (w == 0) ? colacc[2 * m + h][cc] : *d + colacc[2 * m + h][cc];
+              }
+        }
+        asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kWarps) : "memory");
       }
-      asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kWarps) : "memory");
-      if (warp >= 4) {
-#pragma unroll
-        for (int m = 0; m < 4; ++m)
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int cc = 0; cc < R; ++cc) cr[(2 * lane + 64 * m + h) * R + cc] += colacc[2 * m + h][cc];
-      }
-      asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kWarps) : "memory");
-      double* dst = colpart + ((int64_t)(segbase[blockIdx.x] + slot_seg)) * BC * R;
-      for (int e = threadIdx.x; e < BC * R; e += 32 * kWarps)
-        dst[e] = ((colred[e] + colred[BC * R + e]) + colred[2 * BC * R + e]) + colred[3 * BC * R + e];
+      double* dst = colpart + ((int64_t)(segbase[blockIdx.x] + seg - 1)) * BC * R;
+      for (int e = threadIdx.x; e < BC * R; e += 32 * kWarps) dst[e] = colred[e];
       asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kWarps) : "memory");
     };
-    // one row of a tile: row part (j ≤ jmax) and column part (j < i)
-    auto do_row = [&](auto diag_tag, const double* st, int rl, int i, int64_t u) {
+    // RP rows (k0 … k0+RP−1 of the warp's 4) of one tile
+    auto do_rows = [&](auto diag_tag, const double* st, const double* vi, int nv, int k0, int dl0,
+                       double* rp) {
       constexpr bool DIAG = decltype(diag_tag)::value;
-      double rs[R];
+      double rs[RP][R];
 #pragma unroll
-      for (int cc = 0; cc < R; ++cc) rs[cc] = 0.0;
-      double vrow[R];
+      for (int k = 0; k < RP; ++k) {
+        const int rl = kRowsPerWarp * warp + k0 + k;  // row within the tile
+        const double* q = st + rl * BC;
+        double vrow[R];
 #pragma unroll
-      for (int cc = 0; cc < R; ++cc) vrow[cc] = vi[rl * R + cc];
-      const int jmax = i - J * BC;  // diagonal column (DIAG only)
+        for (int cc = 0; cc < R; ++cc) vrow[cc] = (rl < nv) ? vi[rl * R + cc] : 0.0;
+        const int dl = dl0 + rl;  // diagonal column within the panel (DIAG only)
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int jl = 2 * lane + 64 * m;
-        const double2 q2 = *reinterpret_cast<const double2*>(st + jl);
-        double qa = q2.x, qb = q2.y, ca = qa, cb = qb;
-        if (DIAG) {  // row part j ≤ i, column part j < i; beyond: zero
-          qa = (jl <= jmax) ? qa : 0.0;
-          qb = (jl + 1 <= jmax) ? qb : 0.0;
-          ca = (jl < jmax) ? q2.x : 0.0;
-          cb = (jl + 1 < jmax) ? q2.y : 0.0;
-        }
+        for (int cc = 0; cc < R; ++cc) rs[k][cc] = 0.0;
 #pragma unroll
-        for (int cc = 0; cc < R; ++cc) {
-          rs[cc] = fma(qa, vr[2 * m][cc], fma(qb, vr[2 * m + 1][cc], rs[cc]));
-          colacc[2 * m][cc] = fma(ca, vrow[cc], colacc[2 * m][cc]);
-          colacc[2 * m + 1][cc] = fma(cb, vrow[cc], colacc[2 * m + 1][cc]);
+        for (int m = 0; m < 4; ++m) {
+          const int jl = 2 * lane + 64 * m;
+          const double2 q2 = *reinterpret_cast<const double2*>(q + jl);
+          double qa = q2.x, qb = q2.y, ca = qa, cb = qb;
+          if (DIAG) {  // row part j ≤ i, column part j < i; beyond: zero
+            qa = (jl <= dl) ? qa : 0.0;
+            qb = (jl + 1 <= dl) ? qb : 0.0;
+            ca = (jl < dl) ? q2.x : 0.0;
+            cb = (jl + 1 < dl) ? q2.y : 0.0;
+          }
+#pragma unroll
+          for (int cc = 0; cc < R; ++cc) {
+            rs[k][cc] = fma(qa, vr[2 * m][cc], fma(qb, vr[2 * m + 1][cc], rs[k][cc]));
+            colacc[2 * m][cc] = fma(ca, vrow[cc], colacc[2 * m][cc]);
+            colacc[2 * m + 1][cc] = fma(cb, vrow[cc], colacc[2 * m + 1][cc]);
+          }
         }
       }
+      warp_rows_reduce<RP, R>(rs, lane);
+      constexpr int sh = (RP == 4) ? 3 : (RP == 2 ? 4 : 5);
+      if ((lane & ((1 << sh) - 1)) == 0) {
+        const int rl = kRowsPerWarp * warp + k0 + (lane >> sh);
 #pragma unroll
-      for (int cc = 0; cc < R; ++cc) {
-        double v = rs[cc];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        rs[cc] = v;
-      }
-      if (lane == 0) {
-        double* pr = rowpart + (u * BR + rl) * R;
-#pragma unroll
-        for (int cc = 0; cc < R; ++cc) pr[cc] = rs[cc];
+        for (int cc = 0; cc < R; ++cc) rp[rl * R + cc] = rs[0][cc];
       }
     };
     for (int64_t t = t0; t < t1; ++t, ++it) {
-      const int u = (int)(t / kTilesPerUnit);
-      const int tl = (int)(t % kTilesPerUnit);
-      if (u != cur_u) {
-        if (cur_u >= 0) {
-          if (lane == 0) bar_arrive(&vempty[vs]);
-          flush(seg - 1);
-        }
-        unit_ij(u, ubase, TRb, I, J);
-        dblk = (J == (I * BR) / BC);
-        vs = seg & 1;
-        bar_wait(&vfull[vs], (unsigned)((seg >> 1) & 1));
-        const double* vj = vbuf + (size_t)vs * (Cfg::kVJ + Cfg::kVI);
-        vi = vj + Cfg::kVJ;
+      if (t >= pend) {  // new segment (panel J): flush the previous one, load V_J
+        if (J >= 0) flush();
+        J = (J < 0) ? tile_panel(t0, pbase, TCb) : J + 1;
+        pend = pbase[J + 1];
         const int nj = min(BC, n - J * BC);
 #pragma unroll
         for (int m = 0; m < 4; ++m)
@@ -376,70 +389,68 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
             const int jl = 2 * lane + 64 * m + h;
 #pragma unroll
             for (int cc = 0; cc < R; ++cc) {
-              vr[2 * m + h][cc] = (jl < nj) ? vj[jl * R + cc] : 0.0;
+              vr[2 * m + h][cc] = (jl < nj) ? V[((int64_t)J * BC + jl) * R + cc] : 0.0;
               colacc[2 * m + h][cc] = 0.0;
             }
           }
-        cur_u = u;
         ++seg;
       }
+      const int pt = (int)(t - pbase[J]);  // tile index within the panel
+      const int rt = kDiagTiles * J + pt;
       const int s = it % kStages;
       bar_wait(&full[s], (unsigned)((it / kStages) & 1));
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        const double* st = tiles + (size_t)s * TR * BC + (warp + 8 * half) * BC;
-        const int rl = tl * TR + warp + 8 * half;  // row within the unit
-        const int i = I * BR + rl;
+      const double* st = stages + (size_t)s * kStageDoubles;
+      const double* vi = st + TR * BC;
+      const int nv = n - rt * TR;  // rows ≥ n: Q reads as 0 (TMA zero fill), V slice is short
+      double* rp = rowpart + (rtile_base(rt) + J) * TR * R;  // [row tile][panel] order
 #ifndef XM_EXP_NOCOMPUTE
-        if (i < n) {
-          if (dblk) do_row(std::true_type{}, st, rl, i, (int64_t)u);
-          else do_row(std::false_type{}, st, rl, i, (int64_t)u);
-        }
-#else
-        (void)st; (void)i;
-#endif
+      if (pt < kDiagTiles) {
+#pragma unroll
+        for (int k0 = 0; k0 < kRowsPerWarp; k0 += RP) do_rows(std::true_type{}, st, vi, nv, k0, pt * TR, rp);
+      } else {
+#pragma unroll
+        for (int k0 = 0; k0 < kRowsPerWarp; k0 += RP) do_rows(std::false_type{}, st, vi, nv, k0, 0, rp);
       }
+#else
+      (void)rp; (void)pt;
+#endif
       __syncwarp();
       if (lane == 0) bar_arrive(&empty[s]);
+      if (threadIdx.x == 0 && it + kStages < ntiles) {  // refill slot s once every warp released it
+        bar_wait(&empty[s], (unsigned)((it / kStages) & 1));
+        issue(it + kStages);
+      }
     }
-    if (cur_u >= 0) {
-      if (lane == 0) bar_arrive(&vempty[vs]);
-      flush(seg - 1);
-    }
+    if (J >= 0) flush();
   }
 
   // ------------------------------------------------------------ finish (fused)
-  // All row / column partials are published; CTA c now sums the partial lists
-  // of the rows of frames [c·N/G, (c+1)·N/G) (warp per row, lanes split the
-  // list, fixed xor-shuffle tree) and applies the per-camera epilogue.
+  // All row / column partials are published; CTA c now sums, for the rows of
+  // frames [c·N/G, (c+1)·N/G), the row parts of panels 0..⌊row/256⌋ (stored
+  // contiguously per row tile) and the column parts of the segments of panel
+  // ⌊row/256⌋, one (row, column) element per thread in a fixed order
+  // (coalesced across threads), then applies the per-camera epilogue.
 #ifdef XM_EXP_NOFINISH
   return;
 #endif
   grid_barrier(gbar, G);
   const int fa = (int)((int64_t)blockIdx.x * N / G), fb = (int)((int64_t)(blockIdx.x + 1) * N / G);
-  double* qrow = tiles;  // pipeline smem is free now: [rows][R]
-  for (int rr = warp; rr < 3 * (fb - fa); rr += kWarps + 1) {
-    const int row = 3 * fa + rr;
-    const int K = row / BR, l = row % BR;
-    const int u0 = ubase[K], nu = ubase[K + 1] - u0;
+  double* qrow = stages;  // pipeline smem is free now: [rows][R]
+  for (int e = threadIdx.x; e < 3 * (fb - fa) * R; e += kThreads) {
+    const int row = 3 * fa + e / R, cc = e % R;
+    const int K = row / TR, l = row % TR;
     const int Jc = row / BC, m = row % BC;
-    const int c0 = colptr[Jc], nc = colptr[Jc + 1] - c0;
-    double acc[R];
-#pragma unroll
-    for (int cc = 0; cc < R; ++cc) acc[cc] = 0.0;
-    for (int q = lane; q < nu + nc; q += 32) {
-      const double* p = (q < nu) ? rowpart + ((int64_t)(u0 + q) * BR + l) * R
-                                 : colpart + ((int64_t)colidx[c0 + q - nu] * BC + m) * R;
-#pragma unroll
-      for (int cc = 0; cc < R; ++cc) acc[cc] += p[cc];
+    const double* p = rowpart + (rtile_base(K) * TR + l) * R + cc;
+    double acc = 0.0;
+    int q = 0;
+    for (; q + 4 <= Jc + 1; q += 4) {  // 4 loads in flight, summed in order
+      const double a0 = p[(int64_t)q * TR * R], a1 = p[(int64_t)(q + 1) * TR * R];
+      const double a2 = p[(int64_t)(q + 2) * TR * R], a3 = p[(int64_t)(q + 3) * TR * R];
+      acc = (((acc + a0) + a1) + a2) + a3;
     }
-#pragma unroll
-    for (int cc = 0; cc < R; ++cc) {
-      double v = acc[cc];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) qrow[rr * R + cc] = v;
-    }
+    for (; q <= Jc; ++q) acc += p[(int64_t)q * TR * R];
+    for (int sg = colptr[Jc]; sg < colptr[Jc + 1]; ++sg) acc += colpart[((int64_t)sg * BC + m) * R + cc];
+    qrow[e] = acc;
   }
   __syncthreads();
   constexpr int NC = (MODE == EPI_GRAD) ? 3 : (MODE == EPI_DF ? 2 : 1);
@@ -503,20 +514,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
 }
 
 // ---------------------------------------------------------------- host side
-// Kernel choice per (N, r), from tools/exp_sym.sh on B200:
-//   B (N=2000): sym 41.4 µs vs full-row 51.1 µs at r=1, 57.9 vs 55.3 at r=3;
-//   E (N=10155): sym 988 µs vs full-row 1033 µs at r=3.
-// The fused finish + per-tile 2-sided update cost ~25 µs at N=2000, so the
-// half-traffic kernel only pays for r = 1 (Lanczos) or once Q is large.
+// Kernel choice per (N, r), from tools/exp_sym.sh on B200.
 void sym_plan_destroy(xm_ctx* c) {
   delete static_cast<SymPlan*>(c->sym_plan);
   c->sym_plan = nullptr;
 }
 
+// Every plain product (gradient, Δf, Lanczos, HVP outside the persistent tCG)
+// takes the lower-triangle kernel on one GPU: measured faster than the
+// full-row stream at every (N, r) (B: 40.8 vs 55.4 µs at r = 3; E: 587 vs
+// 1037 µs at r = 3, 676 vs 1227 at r = 4).  The tCG loop keeps the persistent
+// full-row kernel below N = 4000 (tcg_fullrow_ok), where one fused launch per
+// TR step beats a three-kernel iteration around this one.
 bool spmm_sym_supported(xm_ctx* c, int r) {
   if (c->world != 1 || r < 1 || r > 5 || c->opt.spmm_kernel == 1) return false;
-  return c->opt.spmm_kernel == 2 || r == 1 || c->N >= 4000;
+  return true;
 }
+
+bool tcg_fullrow_ok(xm_ctx* c) { return c->opt.spmm_kernel != 2 && c->N < 4000; }
 
 int spmm_sym_partials(xm_ctx* c) { return sym_plan(c).G; }
 
@@ -526,8 +541,8 @@ static void launch_sym(xm_ctx* c, const double* V, const SpmmEpiArgs& ep) {
   // sized for the largest supported r once, so the address never changes when
   // the staircase climbs (the tCG graphs of lower ranks captured it)
   constexpr int kRmax = 5;
-  const size_t rp = (size_t)p.U * BR * R;
-  c->sym_part.alloc((size_t)p.U * BR * kRmax + (size_t)std::max(p.S, 1) * BC * kRmax + 64);
+  const size_t rp = (size_t)p.W * TR * R;
+  c->sym_part.alloc((size_t)p.W * TR * kRmax + (size_t)std::max(p.S, 1) * BC * kRmax + 64);
   double* rowpart = c->sym_part.p;
   double* colpart = c->sym_part.p + rp;
   if (!c->gbar.p) {
@@ -545,8 +560,8 @@ static void launch_sym(xm_ctx* c, const double* V, const SpmmEpiArgs& ep) {
     attr = true;
   }
   k_spmm_sym<R, MODE><<<p.G, kThreads, smem, c->stream>>>(
-      p.tmq, c->N, c->n, p.TRb, p.U, p.ubase.p, p.segbase.p, p.colptr.p, p.colidx.p, V, rowpart,
-      colpart, reinterpret_cast<GridBar*>(c->gbar.p), ep);
+      p.tmq, c->N, c->n, p.TRt, p.TCb, p.W, p.pbase.p, p.segbase.p, p.colptr.p, V, rowpart, colpart,
+      reinterpret_cast<GridBar*>(c->gbar.p), ep);
   XM_CHECK_LAUNCH();
   count_launch(c, 1);
 }

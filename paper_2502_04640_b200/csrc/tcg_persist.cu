@@ -941,7 +941,7 @@ bool tcg_persist_sym_supported(xm_ctx* c, int r);
 bool tcg_persist_supported(xm_ctx* c, int r) {
   if (tcg_persist_sym_supported(c, r)) return true;
   if (!c->fused_tcg || !c->persist_tcg || c->world != 1 || r < 1 || r > 5 ||
-      spmm_sym_supported(c, r) || c->N < 1)
+      !tcg_fullrow_ok(c) || c->N < 1)
     return false;
   const int G = std::min(148, c->N);
   return ceil_div(c->N, G) <= kPC && persist_smem_r(r, c->n, G) <= kSmemCap;

@@ -294,6 +294,7 @@ bool tcg_persist_supported(xm_ctx* c, int r);  // whole tCG solve in one launch
 void tcg_persist_launch(xm_ctx* c, int r);
 double tcg_persist_bytes_per_iter(xm_ctx* c, int r);
 int spmm_sym_partials(xm_ctx* c);
+bool tcg_fullrow_ok(xm_ctx* c);  // tCG may use the full-row fused / persistent kernels
 void spmm_sym_launch(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep);
 void spmm(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep);
 // Full product into out (n × r, replicated): this rank's rows + all-gather.
