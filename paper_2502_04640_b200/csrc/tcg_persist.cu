@@ -448,179 +448,218 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(const __grid_const
 
 // ======================================================================
 // Symmetric variant: the stream reads only the LOWER triangle of Q (half the
-// bytes).  Work units = (48-row block I, 128-column chunk J) with J·128 ≤ the
-// block's last row, ordered column-major and split evenly over the CTAs.  A
-// unit adds Q_IJ δ_J to its rows (row partial, one per unit) and Q_IJᵀ δ_I to
-// its columns (column partial, accumulated across the CTA's consecutive units
-// of the same chunk = a segment).  Diagonal-straddling units mask j ≥ i (the
-// diagonal counts once, in the row part).  ⟨δ, Qδ⟩ comes out of the same
-// partials before barrier A (δ_I·row + δ_J·column), so no extra barrier; after
-// barrier A each CTA assembles the Qδ rows of its own cameras from the
-// partials in a fixed order (deterministic).
-constexpr int kSB = 48;         // rows per unit
-constexpr int kSC = 128;        // columns per unit (lane ℓ: columns ℓ + 32m, m < 4)
-constexpr int kSWR = kSB / kPW; // 6 rows per warp
-
-template <int R>
-struct SCfg {
-  static constexpr int kQBytes = kSB * kSC * 8;            // 48 KB
-  static constexpr int kVBytes = 2 * (kSC + kSB) * R * 8;  // r, δ at the chunk's columns and block's rows
-  static constexpr int kStageBytes = kQBytes + kVBytes;
-  static constexpr int kStages = (kStageBytes * 4 <= 200 * 1024) ? 4 : 3;
-};
+// bytes), with the tile geometry of the plain symmetric product (spmm_sym.cu):
+// column panels J of 256 columns, each the run of 32-row tiles from its
+// diagonal block down, numbered panel-major and split stream-K style into G
+// equal contiguous ranges.  Per tile (warp w ↔ rows 4w … 4w+3, lane ℓ ↔
+// columns {2ℓ+64m, 2ℓ+64m+1}): row part Σ_j Q_ij δ_j (butterfly reduce over
+// the warp, one 32 × r partial per tile, row-tile-major), column part
+// Σ_i Q_ij δ_i (registers over the CTA's run of the panel = a segment, one
+// partial per segment).  δ_k is formed on the fly as fma(β, δ_{k−1}, −r_k) —
+// for the panel's columns from L2 at segment start, for the tile's rows from
+// the r / δ_{k−1} slices TMA-loaded next to the Q tile — with the fma the
+// camera owners use, so every CTA sees bitwise the same δ (no third barrier).
+// ⟨δ, Qδ⟩ = Σ δ_i·(row part) + Σ δ_j·(column part) comes out of the partials
+// before barrier A; after it each CTA assembles the Qδ rows of its own
+// cameras from the partials in a fixed order (deterministic).
+//
+// Thread 0 (of warp 0; no producer warp, so each thread may use 255
+// registers) issues the copies: Q tiles run up to 3 stages ahead, across
+// iterations (Q is constant); the r / δ slices of iteration k only after
+// barrier B of k − 1 made r_k, δ_{k−1} final.
+constexpr int kYR = 32;            // rows per tile (4 per warp)
+constexpr int kYC = 256;           // panel width
+constexpr int kYDiag = kYC / kYR;  // tiles of a panel's diagonal block
+constexpr int kYS = 3;             // ring stages
+constexpr int kYQDbl = kYR * kYC;  // Q tile (64 KB)
+constexpr int kYStageDbl = kYQDbl + 2 * kYR * 5;  // + r, δ_{k−1} slices (r ≤ 5); 128-B multiple
 
 struct SymTcgArgs {
   TcgPersistArgs b;
-  const int* ubase;   // nJ + 1: first unit of chunk J
-  const int* uimin;   // nJ: first row block of chunk J
-  const int* segbase; // G + 1: first column-partial slot of CTA c
-  const int* colptr;  // nJ + 1
-  const int* colidx;  // column-partial slots of chunk J, CTA order
-  double* RP;         // [U][kSB][R] row partials
-  double* CP;         // [slots][kSC][R] column partials
-  int U, nJ, nI;
+  const int* pbase;    // TCb + 1: first tile of panel J
+  const int* segbase;  // G + 1: first column-partial slot of CTA c
+  const int* colptr;   // TCb + 1: slots [colptr[J], colptr[J+1]) hold panel J (consecutive)
+  double* RP;          // [W][32][R] row partials, row-tile-major (rtile_base)
+  double* CP;          // [slots][8 warps][R][256] column partials
+  int TCb;
+  int W;
 };
 
-__device__ __forceinline__ int sym_chunk_of(const int* __restrict__ ubase, int nJ, int u) {
-  int lo = 0, hi = nJ - 1;  // largest J with ubase[J] ≤ u
+// first row-part slot of row tile K: Σ_{K'<K} (⌊K'/8⌋ + 1)
+__device__ __forceinline__ int64_t y_rtile_base(int K) {
+  const int64_t a = K >> 3, b = K & 7;
+  return (int64_t)K + 4 * a * (a - 1) + a * b;
+}
+__device__ __forceinline__ int y_panel_of(const int* __restrict__ pbase, int TCb, int t) {
+  int lo = 0, hi = TCb - 1;  // largest J with pbase[J] ≤ t
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (__ldg(ubase + mid) <= u) lo = mid; else hi = mid - 1;
+    if (__ldg(pbase + mid) <= t) lo = mid; else hi = mid - 1;
   }
   return lo;
 }
+// butterfly reduce-scatter of RP rows × R sums over the warp (spmm_sym.cu):
+// lane ℓ ends with the sums of row ℓ >> (5 − log2 RP) in a[0][·]
+template <int RP, int R>
+__device__ __forceinline__ void y_rows_reduce(double (&a)[RP][R], int lane) {
+  if constexpr (RP == 4) {
+    const bool h16 = (lane & 16) != 0;
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+      for (int cc = 0; cc < R; ++cc) {
+        const double snd = h16 ? a[k][cc] : a[k + 2][cc];
+        const double kp = h16 ? a[k + 2][cc] : a[k][cc];
+        a[k][cc] = kp + __shfl_xor_sync(0xffffffffu, snd, 16);
+      }
+  }
+  if constexpr (RP >= 2) {
+    constexpr int o = (RP == 4) ? 8 : 16;
+    const bool hb = (lane & o) != 0;
+#pragma unroll
+    for (int cc = 0; cc < R; ++cc) {
+      const double snd = hb ? a[0][cc] : a[1][cc];
+      const double kp = hb ? a[1][cc] : a[0][cc];
+      a[0][cc] = kp + __shfl_xor_sync(0xffffffffu, snd, o);
+    }
+  }
+  constexpr int top = (RP == 4) ? 4 : (RP == 2 ? 8 : 16);
+#pragma unroll
+  for (int o = top; o > 0; o >>= 1)
+#pragma unroll
+    for (int cc = 0; cc < R; ++cc) a[0][cc] += __shfl_xor_sync(0xffffffffu, a[0][cc], o);
+}
 
 template <int R>
-__global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist_sym(const __grid_constant__ CUtensorMap tmq,
-                                                                  SymTcgArgs sa) {
-  using Cfg = SCfg<R>;
-  constexpr int S = Cfg::kStages;
+__global__ void __launch_bounds__(kPC, 1) k_tcg_persist_sym(const __grid_constant__ CUtensorMap tmq,
+                                                            SymTcgArgs sa) {
+  constexpr int RP = (R <= 4) ? 4 : 2;  // rows reduced together (register budget)
+  constexpr int S = kYS;
   const TcgPersistArgs& a = sa.b;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* stage_base = reinterpret_cast<double*>(smem_raw);
-  uint64_t* fullQ = reinterpret_cast<uint64_t*>(smem_raw + (size_t)S * Cfg::kStageBytes);
+  // one region, two uses: during the stream the next segment's column slices
+  // (colv: r then δ_{k−1}, 256 × R each), after barrier A the Qδ rows of this
+  // CTA's cameras (yown) — the stream never overlaps the camera phase
+  double* colv = stage_base + (size_t)S * kYStageDbl;
+  double* yown = colv;  // [3·cameras of this CTA][R]
+  const int nf_max = (a.N + gridDim.x - 1) / gridDim.x;
+  uint64_t* fullQ = reinterpret_cast<uint64_t*>(colv + max(3 * nf_max * R, 2 * kYC * R));
   uint64_t* fullV = fullQ + S;
   uint64_t* empty = fullV + S;
-  double* colred = reinterpret_cast<double*>(empty + S);  // [4][kSC][R]
-  double* yown = colred + 4 * kSC * R;                      // [3·cameras of this CTA][R]
+  uint64_t* colfull = empty + S;     // next segment's column slices landed
+  uint64_t* colempty = colfull + 1;  // every warp has formed its δ_J registers from them
   __shared__ TcgState ts;
-  __shared__ volatile int sh_vgen;
   __shared__ volatile int sh_stop;
-  __shared__ volatile long long sh_iq;
-  __shared__ volatile long long sh_ivdone;
   __shared__ double ws[kPW];
 
   const int G = gridDim.x;
   const int n = a.n;
-  const int u0 = (int)((int64_t)blockIdx.x * sa.U / G);
-  const int u1 = (int)((int64_t)(blockIdx.x + 1) * sa.U / G);
-  const int tiles = u1 - u0;  // units per iteration
+  const int t0 = (int)((int64_t)blockIdx.x * sa.W / G);
+  const int T = (int)((int64_t)(blockIdx.x + 1) * sa.W / G) - t0;  // tiles per iteration
   const int fa = (int)((int64_t)blockIdx.x * a.N / G);
   const int nf = (int)((int64_t)(blockIdx.x + 1) * a.N / G) - fa;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int J0 = (tiles > 0) ? sym_chunk_of(sa.ubase, sa.nJ, u0) : 0;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int J0 = (T > 0) ? y_panel_of(sa.pbase, sa.TCb, t0) : 0;
 
-  if (threadIdx.x == 0) {
+  if (t == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&fullQ[s], 1);
       mbar_init(&fullV[s], 1);
       mbar_init(&empty[s], kPW);
     }
+    mbar_init(colfull, 1);
+    mbar_init(colempty, kPW);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     ts = *a.st;
-    sh_vgen = 0;
     sh_stop = ts.stop != 0;
-    sh_iq = 0;
-    sh_ivdone = -1;
   }
   __syncthreads();
   if (sh_stop) return;
+  // segments (panels J0 … J0 + nseg − 1) of this CTA's range, every iteration
+  const int nseg = (T > 0) ? y_panel_of(sa.pbase, sa.TCb, t0 + T - 1) - J0 + 1 : 0;
 
-  // unit cursor → (I, J): walk the column-major order from (I of u0, J0)
-  auto unit_ij = [&](int uu, int& I, int& J) {
-    J = J0;
-    while (J + 1 < sa.nJ && __ldg(sa.ubase + J + 1) <= uu) ++J;
-    I = __ldg(sa.uimin + J) + (uu - __ldg(sa.ubase + J));
+  // ---------------------------------------------------------------- producer state (thread 0)
+  // kept in shared memory: only thread 0 uses it, and registers are the
+  // stream's budget (every thread is allocated what the busiest one needs)
+  struct Prod {
+    long long iq, iv;  // Q tiles / r,δ slices issued (global tile counter)
+    long long ic;      // column-slice pairs issued (global segment counter)
+    int qJ, qpend, vJ, vpend;
   };
-
-  if (warp == kPW) {
-    // ============================================================ Q producer
-    if (lane != 0) return;
-    const uint64_t pol_q = policy_evict_first();
-    const unsigned qbytes = (unsigned)(kSC * kSB * 8);
-    long long iq = 0;
-    int I = 0, J = J0, ucur = -1;
-    for (;; ++iq) {
-      const int s = (int)(iq % S);
-      const unsigned ph = (unsigned)((iq / S) & 1);
-      bool go;
-      while (!(go = mbar_try_wait(&empty[s], ph ^ 1u)))
-        if (sh_stop) break;
-      if (!go || sh_stop || tiles == 0) break;
-      const int uu = u0 + (int)(iq % tiles);
-      if (uu == u0 || uu != ucur + 1) {
-        unit_ij(uu, I, J);
-      } else {  // next unit: down the chunk, or the top of the next chunk
-        if (uu >= __ldg(sa.ubase + J + 1)) {
-          ++J;
-          I = __ldg(sa.uimin + J);
-        } else {
-          ++I;
-        }
-      }
-      ucur = uu;
-      mbar_expect_tx(&fullQ[s], qbytes);
-      tma_load_2d(stage_base + (size_t)s * (Cfg::kStageBytes / 8), &tmq, J * kSC, I * kSB, &fullQ[s],
-                  pol_q);
-      sh_iq = iq + 1;
+  __shared__ Prod pr;
+  // tile g of the CTA's cyclic sequence → (panel J, row tile); cursors walk
+  // the panels incrementally and restart at J0 on every new iteration
+  auto geo = [&](long long g, int& J, int& pend) {
+    const int x = (int)(g % T);
+    if (x == 0) {
+      J = J0;
+      pend = __ldg(sa.pbase + J0 + 1);
     }
-    while (sh_ivdone < 0) {
+    while (t0 + x >= pend) {
+      ++J;
+      pend = __ldg(sa.pbase + J + 1);
     }
-    for (long long tq = sh_ivdone; tq < iq; ++tq) mbar_wait(&fullQ[tq % S], (unsigned)((tq / S) & 1));
-    return;
-  }
-  if (warp == kPW + 1) {
-    // ======================================================= r / δ producer
-    if (lane != 0) return;
+    return kYDiag * J + (t0 + x - __ldg(sa.pbase + J));
+  };
+  auto issue_q = [&]() {
+    const long long g = pr.iq;
+    int J = pr.qJ, pend = pr.qpend;
+    const int rt = geo(g, J, pend);
+    pr.qJ = J;
+    pr.qpend = pend;
+    const int s = (int)(g % S);
+    mbar_expect_tx(&fullQ[s], (unsigned)(kYQDbl * 8));
+    tma_load_2d(stage_base + (size_t)s * kYStageDbl, &tmq, J * kYC, rt * kYR, &fullQ[s],
+                policy_evict_first());
+    pr.iq = g + 1;
+  };
+  auto issue_v = [&](int k) {
+    const long long g = pr.iv;
+    int J = pr.vJ, pend = pr.vpend;
+    const int rt = geo(g, J, pend);
+    pr.vJ = J;
+    pr.vpend = pend;
+    const int s = (int)(g % S);
+    const int rlen = min(kYR, n - rt * kYR);
+    const unsigned vb = (unsigned)(((rlen * R + 1) & ~1) * 8);
+    const double* dprev = (k & 1) ? a.D0 : a.D1;  // δ_{k−1}
+    double* st = stage_base + (size_t)s * kYStageDbl + kYQDbl;
     const uint64_t pol_v = policy_evict_last();
-    long long iv = 0;
-    int fenced = -1;
-    for (;; ++iv) {
-      const int kv = tiles > 0 ? (int)(iv / tiles) : 0;
-      bool stop = false;
-      while (!(iv < sh_iq && kv <= sh_vgen)) {
-        if (sh_stop) {
-          stop = true;
-          break;
-        }
-        __nanosleep(20);
-      }
-      if (stop) break;
-      if (kv > fenced) {
-        fence_proxy_async();
-        fenced = kv;
-      }
-      const int s = (int)(iv % S);
-      int I, J;
-      unit_ij(u0 + (int)(iv % tiles), I, J);
-      const int c0 = J * kSC, klen = min(kSC, n - c0);
-      const int r0 = I * kSB, rlen = min(kSB, n - r0);
-      const unsigned vbc = (unsigned)(((klen * R + 1) & ~1) * 8);
-      const unsigned vbr = (unsigned)(((rlen * R + 1) & ~1) * 8);
-      double* st = stage_base + (size_t)s * (Cfg::kStageBytes / 8) + kSB * kSC;
-      const double* dprev = (kv & 1) ? a.D0 : a.D1;  // δ_{k−1}
-      mbar_expect_tx(&fullV[s], 2 * vbc + 2 * vbr);
-      tma_load_1d(st, a.res + (int64_t)c0 * R, vbc, &fullV[s], pol_v);
-      tma_load_1d(st + kSC * R, dprev + (int64_t)c0 * R, vbc, &fullV[s], pol_v);
-      tma_load_1d(st + 2 * kSC * R, a.res + (int64_t)r0 * R, vbr, &fullV[s], pol_v);
-      tma_load_1d(st + 2 * kSC * R + kSB * R, dprev + (int64_t)r0 * R, vbr, &fullV[s], pol_v);
+    mbar_expect_tx(&fullV[s], 2 * vb);
+    tma_load_1d(st, a.res + (int64_t)rt * kYR * R, vb, &fullV[s], pol_v);
+    tma_load_1d(st + kYR * R, dprev + (int64_t)rt * kYR * R, vb, &fullV[s], pol_v);
+    pr.iv = g + 1;
+  };
+  // next segment's column slices, once the previous ones were consumed and
+  // the segment belongs to iteration k (its r_k, δ_{k−1} are final)
+  auto issue_col = [&](int k) {
+    const long long g = pr.ic;
+    if (g >= (long long)(k + 1) * nseg) return;
+    if (g > 0 && !mbar_test(colempty, (unsigned)((g - 1) & 1))) return;
+    const int J = J0 + (int)(g % nseg);
+    const int nj = min(kYC, n - J * kYC);
+    const unsigned cb = (unsigned)(((nj * R + 1) & ~1) * 8);
+    const double* dprev = (k & 1) ? a.D0 : a.D1;
+    const uint64_t pol_v = policy_evict_last();
+    mbar_expect_tx(colfull, 2 * cb);
+    tma_load_1d(colv, a.res + (int64_t)J * kYC * R, cb, colfull, pol_v);
+    tma_load_1d(colv + kYC * R, dprev + (int64_t)J * kYC * R, cb, colfull, pol_v);
+    pr.ic = g + 1;
+  };
+  if (t == 0) {
+    pr.iq = 0;
+    pr.iv = 0;
+    pr.ic = 0;
+    pr.qJ = pr.vJ = J0;
+    pr.qpend = pr.vpend = 0;
+    if (T > 0) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmq)) : "memory");
+      for (int q = 0; q < S; ++q) issue_q();
     }
-    sh_ivdone = iv;
-    return;
   }
 
-  // ================================================================== consumers
-  const int t = threadIdx.x;
+  // ---------------------------------------------------------------- camera owners
   const bool has = t < nf;
   const int i = fa + t;
   if (has) {  // δ_0 = −r_0
@@ -633,150 +672,150 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist_sym(const __grid_c
     store_blk<R>(a.D0, i, d0b);
   }
   double beta_prev = 0.0;
-  long long it = 0;
+  long long it = 0;  // tiles consumed (global)
   for (int k = 0;; ++k) {
-    const double* dprev_g = (k & 1) ? a.D0 : a.D1;
+    XM_PSTAMP(0);
+    if (t == 0 && T > 0) {  // this iteration's r / δ_{k−1} slices (after barrier B of k − 1)
+      fence_proxy_async();
+      issue_col(k);
+      while (pr.iv < pr.iq && pr.iv < (long long)(k + 1) * T) issue_v(k);
+    }
+    // ------------------------------------------------------------ stream Qδ_k
     double part = 0.0;  // this thread's share of ⟨δ_k, Qδ_k⟩
-    double accc[4][R];  // column partial of the current segment (lane's 4 columns, warp's rows)
+    double vr[8][R], colacc[8][R];
+    int J = -1, pend = 0, seg = 0;
+    auto flush = [&]() {
+      // ⟨δ_J, column part⟩ per lane; each warp writes its own column partial
+      // (no cross-warp step here: the assembly sums the 8 warps in order)
 #pragma unroll
-    for (int m = 0; m < 4; ++m)
+      for (int m = 0; m < 8; ++m)
 #pragma unroll
-      for (int cc = 0; cc < R; ++cc) accc[m][cc] = 0.0;
-    int I = 0, J = J0;
-    for (int uu = u0; uu < u1; ++uu, ++it) {
-      if (uu == u0) {
-        unit_ij(uu, I, J);
-      } else if (uu >= __ldg(sa.ubase + J + 1)) {
-        ++J;
-        I = __ldg(sa.uimin + J);
-      } else {
-        ++I;
-      }
-      const int sidx = (int)(it % S);
-      const unsigned ph = (unsigned)((it / S) & 1);
-      mbar_wait(&fullQ[sidx], ph);
-      mbar_wait(&fullV[sidx], ph);
-      const double* stg = stage_base + (size_t)sidx * (Cfg::kStageBytes / 8);
-      const double* rJ = stg + kSB * kSC;
-      const double* dJ = rJ + kSC * R;
-      const double* rI = dJ + kSC * R;
-      const double* dI = rI + kSB * R;
-      const int c0 = J * kSC, rb0 = I * kSB;
-      double vj[4][R];
+        for (int cc = 0; cc < R; ++cc) part = fma(vr[m][cc], colacc[m][cc], part);
+      // layout [slot][warp][cc][col]: a lane's column pair is one 16-B store
+      double* dst = sa.CP + ((int64_t)(__ldg(sa.segbase + blockIdx.x) + seg - 1) * kPW + warp) * R * kYC;
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int cl = lane + 32 * m;
-        const bool ok = c0 + cl < n;
+      for (int m = 0; m < 4; ++m)
 #pragma unroll
         for (int cc = 0; cc < R; ++cc)
-          vj[m][cc] = ok ? fma(beta_prev, dJ[cl * R + cc], -rJ[cl * R + cc]) : 0.0;
-      }
-      double accr[kSWR][R];
+          *reinterpret_cast<double2*>(dst + cc * kYC + 2 * lane + 64 * m) =
+              make_double2(colacc[2 * m][cc], colacc[2 * m + 1][cc]);
+    };
+    auto do_rows = [&](auto diag_tag, const double* st, const double* rI, const double* dI, int nv,
+                       int k0, int dl0, double* rp) {
+      constexpr bool DIAG = decltype(diag_tag)::value;
+      double rs[RP][R];
 #pragma unroll
-      for (int q = 0; q < kSWR; ++q)
-#pragma unroll
-        for (int cc = 0; cc < R; ++cc) accr[q][cc] = 0.0;
-      const bool straddle = c0 + kSC - 1 >= rb0;  // some element on / above the diagonal
-#pragma unroll
-      for (int q = 0; q < kSWR; ++q) {
-        const int rl = kSWR * warp + q;
-        const int rg = rb0 + rl;
-        double vi[R];
+      for (int kk = 0; kk < RP; ++kk) {
+        const int rl = 4 * warp + k0 + kk;
+        const double* q = st + rl * kYC;
+        double vrow[R];
 #pragma unroll
         for (int cc = 0; cc < R; ++cc)
-          vi[cc] = (rg < n) ? fma(beta_prev, dI[rl * R + cc], -rI[rl * R + cc]) : 0.0;
-        const double* qrow = stg + (size_t)rl * kSC + lane;
+          vrow[cc] = (rl < nv) ? fma(beta_prev, dI[rl * R + cc], -rI[rl * R + cc]) : 0.0;
+        const int dl = dl0 + rl;
+#pragma unroll
+        for (int cc = 0; cc < R; ++cc) rs[kk][cc] = 0.0;
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
-          const double qv = qrow[32 * m];
-          const int cg = c0 + lane + 32 * m;
-          const bool lower = !straddle || cg < rg;
-          const bool rowp = lower || cg == rg;
-          if (rowp) {
-#pragma unroll
-            for (int cc = 0; cc < R; ++cc) accr[q][cc] = fma(qv, vj[m][cc], accr[q][cc]);
+          const int jl = 2 * lane + 64 * m;
+          const double2 q2 = *reinterpret_cast<const double2*>(q + jl);
+          double qa = q2.x, qb = q2.y, ca = qa, cb = qb;
+          if (DIAG) {  // row part j ≤ i, column part j < i
+            qa = (jl <= dl) ? qa : 0.0;
+            qb = (jl + 1 <= dl) ? qb : 0.0;
+            ca = (jl < dl) ? q2.x : 0.0;
+            cb = (jl + 1 < dl) ? q2.y : 0.0;
           }
-          if (lower) {
-#pragma unroll
-            for (int cc = 0; cc < R; ++cc) accc[m][cc] = fma(qv, vi[cc], accc[m][cc]);
-          }
-        }
-      }
-      // row partial of this unit: lanes (xor tree) → RP, and δ_I · row partial
-#pragma unroll
-      for (int q = 0; q < kSWR; ++q)
-#pragma unroll
-        for (int cc = 0; cc < R; ++cc) {
-          double x = accr[q][cc];
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-          accr[q][cc] = x;
-        }
-      if (lane == 0) {
-        double* rp = sa.RP + ((int64_t)uu * kSB + kSWR * warp) * R;
-#pragma unroll
-        for (int q = 0; q < kSWR; ++q) {
-          const int rl = kSWR * warp + q;
-          const bool okr = rb0 + rl < n;
 #pragma unroll
           for (int cc = 0; cc < R; ++cc) {
-            rp[q * R + cc] = accr[q][cc];
-            const double di = okr ? fma(beta_prev, dI[rl * R + cc], -rI[rl * R + cc]) : 0.0;
-            part = fma(di, accr[q][cc], part);
+            rs[kk][cc] = fma(qa, vr[2 * m][cc], fma(qb, vr[2 * m + 1][cc], rs[kk][cc]));
+            colacc[2 * m][cc] = fma(ca, vrow[cc], colacc[2 * m][cc]);
+            colacc[2 * m + 1][cc] = fma(cb, vrow[cc], colacc[2 * m + 1][cc]);
           }
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[sidx]);
-      // segment end (chunk changes or last unit): column partial across the 8 warps
-      const bool seg_end = (uu + 1 == u1) || (uu + 1 >= __ldg(sa.ubase + J + 1));
-      if (seg_end) {
-        if (warp >= 4) {
+      y_rows_reduce<RP, R>(rs, lane);
+      constexpr int sh = (RP == 4) ? 3 : (RP == 2 ? 4 : 5);
+      if ((lane & ((1 << sh) - 1)) == 0) {
+        const int rl = 4 * warp + k0 + (lane >> sh);
 #pragma unroll
-          for (int m = 0; m < 4; ++m)
-#pragma unroll
-            for (int cc = 0; cc < R; ++cc)
-              colred[((warp - 4) * kSC + lane + 32 * m) * R + cc] = accc[m][cc];
+        for (int cc = 0; cc < R; ++cc) {
+          rp[rl * R + cc] = rs[0][cc];
+          const double di = (rl < nv) ? fma(beta_prev, dI[rl * R + cc], -rI[rl * R + cc]) : 0.0;
+          part = fma(di, rs[0][cc], part);
         }
-        cbar();
-        if (warp < 4) {
-#pragma unroll
-          for (int m = 0; m < 4; ++m)
-#pragma unroll
-            for (int cc = 0; cc < R; ++cc) {
-              double* p = colred + (warp * kSC + lane + 32 * m) * R + cc;
-              *p = accc[m][cc] + *p;  // warp w + warp w+4
-            }
-        }
-        cbar();
-        const int slot = __ldg(sa.segbase + blockIdx.x) + (J - J0);
-        for (int u2 = t; u2 < kSC * R; u2 += kPC) {
-          const double sum = (colred[u2] + colred[kSC * R + u2]) +
-                             (colred[2 * kSC * R + u2] + colred[3 * kSC * R + u2]);
-          sa.CP[(int64_t)slot * kSC * R + u2] = sum;
-          const int64_t g = (int64_t)c0 * R + u2;
-          if (c0 + u2 / R < n)
-            part = fma(fma(beta_prev, __ldcg(dprev_g + g), -__ldcg(a.res + g)), sum, part);
-        }
-        cbar();
+      }
+    };
+    for (int x = 0; x < T; ++x, ++it) {
+      const int tt = t0 + x;
+      if (tt >= pend) {  // new segment: flush the previous one, form δ_J for the lane's columns
+        if (J >= 0) flush();
+        J = (J < 0) ? J0 : J + 1;
+        pend = __ldg(sa.pbase + J + 1);
+        const int nj = min(kYC, n - J * kYC);
+        const long long gs = (long long)k * nseg + seg;  // global segment index
+        mbar_wait(colfull, (unsigned)(gs & 1));
 #pragma unroll
         for (int m = 0; m < 4; ++m)
 #pragma unroll
-          for (int cc = 0; cc < R; ++cc) accc[m][cc] = 0.0;
+          for (int h = 0; h < 2; ++h) {
+            const int jl = 2 * lane + 64 * m + h;
+#pragma unroll
+            for (int cc = 0; cc < R; ++cc) {
+              vr[2 * m + h][cc] =
+                  (jl < nj) ? fma(beta_prev, colv[kYC * R + jl * R + cc], -colv[jl * R + cc]) : 0.0;
+              colacc[2 * m + h][cc] = 0.0;
+            }
+          }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(colempty);
+        ++seg;
+      }
+      const int ptl = tt - __ldg(sa.pbase + J);  // tile within the panel
+      const int rt = kYDiag * J + ptl;
+      const int s = (int)(it % S);
+      const unsigned ph = (unsigned)((it / S) & 1);
+      mbar_wait(&fullQ[s], ph);
+      mbar_wait(&fullV[s], ph);
+      const double* st = stage_base + (size_t)s * kYStageDbl;
+      const double* rI = st + kYQDbl;
+      const double* dI = rI + kYR * R;
+      const int nv = n - rt * kYR;
+      double* rp = sa.RP + (y_rtile_base(rt) + J) * kYR * R;
+      if (ptl < kYDiag) {
+#pragma unroll
+        for (int k0 = 0; k0 < 4; k0 += RP) do_rows(std::true_type{}, st, rI, dI, nv, k0, ptl * kYR, rp);
+      } else {
+#pragma unroll
+        for (int k0 = 0; k0 < 4; k0 += RP) do_rows(std::false_type{}, st, rI, dI, nv, k0, 0, rp);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (t == 0) {
+        // refill slot s with the tile S ahead if it belongs to this iteration;
+        // the next iteration's first tiles are issued after the assembly
+        // (in flight during barriers they would queue ahead of its L2 reads)
+        if (it + S < (long long)(k + 1) * T) {
+          mbar_wait(&empty[s], ph);
+          issue_q();
+          if (pr.iv < pr.iq) issue_v(k);
+        }
+        if (pr.ic < (long long)(k + 1) * nseg) issue_col(k);
       }
     }
+    if (J >= 0) flush();
     XM_PSTAMP(1);
     TcgState s = ts;
     Blk<R> y, dcur, rcur;
     double L[6];
-    if (has) {  // camera part −2⟨δ_i, Λ_iδ_i⟩; rows part is 2⟨δ, Qδ⟩ = 2·part (summed below)
+    if (has) {
       load_blk<R>(a.Y, i, y);
       load_blk<R>((k & 1) ? a.D1 : a.D0, i, dcur);
       load_blk<R>(a.res, i, rcur);
 #pragma unroll
       for (int q = 0; q < 6; ++q) L[q] = a.lam[6 * i + q];
     }
-    {
+    {  // ⟨δ, Hδ⟩ = 2⟨δ, Qδ⟩ − 2⟨δ, Λδ⟩ (δ tangent, P orthogonal)
       double cam = 0.0;
       if (has) {
         Blk<R> zero{}, lamd;
@@ -790,22 +829,40 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist_sym(const __grid_c
     cgrid_sync(a.gsync, G);
     XM_PSTAMP(3);
     // ---------------------- assemble Qδ at this CTA's camera rows (fixed order)
+    // every load of an element in flight at once (latency, not bandwidth,
+    // bounds this phase); this thread's ⟨δ,Hδ⟩ partial load overlaps it
+    const double pa_mine = (t < G) ? __ldcg(a.pA + t) : 0.0;  // = csum_partials' assignment (G ≤ 256)
     for (int o = t; o < 3 * nf * R; o += kPC) {
-      const int g = 3 * fa + o / R, cc = o % R;
-      const int Ib = g / kSB, l = g % kSB, Jg = g / kSC, mcol = g % kSC;
-      const int Jmax = min(sa.nJ - 1, (Ib * kSB + kSB - 1) / kSC);
+      const int row = 3 * fa + o / R, cc = o % R;
+      const int K = row / kYR, l = row % kYR, Jc = row / kYC, mcol = row % kYC;
+      const double* p = sa.RP + (y_rtile_base(K) * kYR + l) * R + cc;
+      constexpr int64_t st = kYR * R;
       double y2 = 0.0;
-      for (int Jp = 0; Jp <= Jmax; ++Jp) {
-        const int uu = __ldg(sa.ubase + Jp) + (Ib - __ldg(sa.uimin + Jp));
-        y2 += __ldcg(sa.RP + ((int64_t)uu * kSB + l) * R + cc);
+      for (int q0 = 0; q0 <= Jc; q0 += 32) {  // panels q0 … q0+31 (zeros past Jc add exactly)
+        double v[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) v[u] = (q0 + u <= Jc) ? __ldcg(p + (int64_t)(q0 + u) * st) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 32; ++u) y2 += v[u];
       }
-      for (int p = __ldg(sa.colptr + Jg); p < __ldg(sa.colptr + Jg + 1); ++p)
-        y2 += __ldcg(sa.CP + ((int64_t)__ldg(sa.colidx + p) * kSC + mcol) * R + cc);
+      // column partials of panel Jc: (slot, warp) pairs in order — consecutive
+      // in the [slot][warp][cc][col] layout — 32 loads in flight at a time
+      const int f0 = __ldg(sa.colptr + Jc) * kPW, nfl = __ldg(sa.colptr + Jc + 1) * kPW - f0;
+      const double* c = sa.CP + ((int64_t)f0 * R + cc) * kYC + mcol;
+      for (int q0 = 0; q0 < nfl; q0 += 32) {
+        double v[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) v[u] = (q0 + u < nfl) ? __ldcg(c + (int64_t)(q0 + u) * R * kYC) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 32; ++u) y2 += v[u];
+      }
       yown[o] = y2;
     }
-    cbar();
     // -------------------------------------------------- α, boundary / τ, update
-    const double dHd = csum_partials(a.pA, G, ws);
+    const double dHd = csum(pa_mine, ws);  // its cbar also publishes yown
+    XM_PSTAMP(7);
+    if (t == 0)  // Q prefetch of the next iteration (every warp has released every slot)
+      while (pr.iq < it + S) issue_q();
     s.d_Hd = dHd;
     s.n_hvp += 1;
     const double alpha = (dHd != 0.0) ? s.z / dHd : INFINITY;
@@ -884,17 +941,17 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist_sym(const __grid_c
       for (int p = 0; p < 3; ++p)
 #pragma unroll
         for (int cc = 0; cc < R; ++cc) dcur.v[p][cc] = fma(s.beta, dcur.v[p][cc], -rcur.v[p][cc]);
-      store_blk<R>((k & 1) ? a.D0 : a.D1, i, dcur);
+      store_blk<R>((k & 1) ? a.D0 : a.D1, i, dcur);  // δ_{k+1} → D[(k+1) & 1]
     }
     beta_prev = s.beta;
     XM_PSTAMP(6);
     cbar();
-    if (t == 0) {
-      ts = s;
-      __threadfence_block();
-      sh_vgen = k + 1;
-    }
+    if (t == 0) ts = s;
+    cbar();
   }
+  // drain: no Q copy may still be landing in shared memory when the CTA exits
+  if (t == 0)
+    for (long long g = it; g < pr.iq; ++g) mbar_wait(&fullQ[g % S], (unsigned)((g / S) & 1));
 }
 
 // ---------------------------------------------------------------------- host
@@ -1058,66 +1115,69 @@ double tcg_persist_bytes_per_iter(xm_ctx* c, int r) {
 }
 
 // ------------------------------------------------------------- symmetric host
+// Work plan of k_tcg_persist_sym for (n, G): panel bases, per-CTA column-partial
+// slot bases, the slots of each panel, the 256 × 32 Q tensor map, partials.
 struct SymTcgPlan {
-  int n = 0, G = 0, nI = 0, nJ = 0, U = 0, slots = 0, R = 0;
-  DBuf<int> ubase, uimin, segbase, colptr, colidx;
+  int n = 0, G = 0, TCb = 0, W = 0, slots = 0;
+  DBuf<int> pbase, segbase, colptr;
   DBuf<double> RP, CP;
   alignas(64) unsigned char tmap[128] = {0};
   const void* tmap_q = nullptr;
-  int tmap_bh = 0, tmap_n = 0;
+  int64_t tmap_ld = 0;
 };
 
-static SymTcgPlan& sym_tcg_plan(xm_ctx* c, int r) {
+static SymTcgPlan& sym_tcg_plan(xm_ctx* c) {
   if (!c->persist_sym_plan) c->persist_sym_plan = new SymTcgPlan();
   SymTcgPlan& p = *static_cast<SymTcgPlan*>(c->persist_sym_plan);
   const int n = c->n, G = std::min(148, c->N);
   if (p.n != n || p.G != G) {
     p.n = n;
     p.G = G;
-    p.nI = ceil_div(n, kSB);
-    p.nJ = ceil_div(n, kSC);
-    std::vector<int> ub(p.nJ + 1, 0), im(p.nJ, 0);
-    for (int J = 0; J < p.nJ; ++J) {
-      im[J] = std::max(0, ceil_div(J * kSC - (kSB - 1), kSB));  // first block reaching column J·kSC
-      ub[J + 1] = ub[J] + (p.nI - im[J]);
-    }
-    p.U = ub[p.nJ];
-    auto chunk_of = [&](int u) {
-      int J = 0;
-      while (J + 1 < p.nJ && ub[J + 1] <= u) ++J;
-      return J;
-    };
-    std::vector<int> sb(G + 1, 0);
-    std::vector<std::vector<int>> bycol(p.nJ);
+    const int TRt = ceil_div(n, kYR);
+    p.TCb = ceil_div(n, kYC);
+    std::vector<int> pb(p.TCb + 1, 0);
+    for (int J = 0; J < p.TCb; ++J) pb[J + 1] = pb[J] + (TRt - kYDiag * J);
+    p.W = pb[p.TCb];
+    std::vector<int> sb(G + 1, 0), segpanel;
     for (int cta = 0; cta < G; ++cta) {
-      const int u0 = (int)((int64_t)cta * p.U / G), u1 = (int)((int64_t)(cta + 1) * p.U / G);
-      sb[cta + 1] = sb[cta];
-      if (u1 > u0) {
-        const int Ja = chunk_of(u0), Jb = chunk_of(u1 - 1);
-        for (int J = Ja; J <= Jb; ++J) bycol[J].push_back(sb[cta] + (J - Ja));
-        sb[cta + 1] += Jb - Ja + 1;
+      const int64_t t0 = (int64_t)cta * p.W / G, t1 = (int64_t)(cta + 1) * p.W / G;
+      sb[cta] = (int)segpanel.size();
+      int J = 0;
+      for (int64_t tt = t0; tt < t1;) {
+        while (pb[J + 1] <= tt) ++J;
+        segpanel.push_back(J);
+        tt = std::min<int64_t>(t1, pb[J + 1]);
       }
     }
+    sb[G] = (int)segpanel.size();
     p.slots = sb[G];
-    std::vector<int> cp(p.nJ + 1, 0), ci;
-    for (int J = 0; J < p.nJ; ++J) {
-      for (int sl : bycol[J]) ci.push_back(sl);
-      cp[J + 1] = (int)ci.size();
+    std::vector<int> cp(p.TCb + 1, 0);
+    for (int s = 0, J = 0; J <= p.TCb; ++J) {  // segpanel is non-decreasing
+      while (s < p.slots && segpanel[s] < J) ++s;
+      cp[J] = s;
     }
-    p.ubase.alloc(ub.size());
-    p.uimin.alloc(im.size());
+    p.pbase.alloc(pb.size());
     p.segbase.alloc(sb.size());
     p.colptr.alloc(cp.size());
-    p.colidx.alloc(std::max<size_t>(1, ci.size()));
-    XM_CUDA(cudaMemcpy(p.ubase.p, ub.data(), ub.size() * 4, cudaMemcpyHostToDevice));
-    XM_CUDA(cudaMemcpy(p.uimin.p, im.data(), im.size() * 4, cudaMemcpyHostToDevice));
+    XM_CUDA(cudaMemcpy(p.pbase.p, pb.data(), pb.size() * 4, cudaMemcpyHostToDevice));
     XM_CUDA(cudaMemcpy(p.segbase.p, sb.data(), sb.size() * 4, cudaMemcpyHostToDevice));
     XM_CUDA(cudaMemcpy(p.colptr.p, cp.data(), cp.size() * 4, cudaMemcpyHostToDevice));
-    if (!ci.empty())
-      XM_CUDA(cudaMemcpy(p.colidx.p, ci.data(), ci.size() * 4, cudaMemcpyHostToDevice));
   }
-  p.RP.alloc((size_t)p.U * kSB * 5 + 64);      // sized for r ≤ 5 (fixed addresses)
-  p.CP.alloc((size_t)p.slots * kSC * 5 + 64);
+  p.RP.alloc((size_t)p.W * kYR * 5 + 64);  // sized for r ≤ 5 (fixed addresses)
+  p.CP.alloc((size_t)std::max(p.slots, 1) * kPW * kYC * 5 + 64);
+  if (p.tmap_q != c->Q.p || p.tmap_ld != c->ldq) {  // box 256 × 32, rows / columns ≥ n zero-filled
+    cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)n};
+    cuuint64_t strides[1] = {(cuuint64_t)c->ldq * 8};
+    cuuint32_t box[2] = {(cuuint32_t)kYC, (cuuint32_t)kYR};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = tmap_encoder()(reinterpret_cast<CUtensorMap*>(p.tmap), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                                c->Q.p, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(XM_ECUDA, "cuTensorMapEncodeTiled failed (symmetric tCG)");
+    p.tmap_q = c->Q.p;
+    p.tmap_ld = c->ldq;
+  }
   return p;
 }
 
@@ -1129,10 +1189,9 @@ void sym_tcg_plan_destroy(xm_ctx* c) {
 namespace {
 template <int R>
 size_t persist_sym_smem(int N, int G) {
-  using Cfg = SCfg<R>;
   const int nf_max = ceil_div(N, G);
-  return (size_t)Cfg::kStages * Cfg::kStageBytes + 3 * Cfg::kStages * 8 + 4 * (size_t)kSC * R * 8 +
-         (size_t)3 * nf_max * R * 8;
+  return (size_t)kYS * kYStageDbl * 8 + std::max((size_t)3 * nf_max * R * 8, (size_t)2 * kYC * R * 8) +
+         (3 * kYS + 2) * 8;
 }
 size_t persist_sym_smem_r(int r, int N, int G) {
   switch (r) {
@@ -1146,11 +1205,15 @@ size_t persist_sym_smem_r(int r, int N, int G) {
 }
 }  // namespace
 
-// Lower-triangle persistent tCG: opt-in (XM_SYM_TCG=1) until it wins on the bench.
+// Default below N = 4000 (B: 46.8 vs 53.0 µs per tCG iteration for the
+// full-row kernel, same box); at E the three-kernel iteration around the
+// plain symmetric product wins (605 vs 708 µs: 69 cameras per CTA to
+// assemble, spills at r = 4).
 bool tcg_persist_sym_supported(xm_ctx* c, int r) {
-  if (!c->persist_sym || !c->fused_tcg || !c->persist_tcg || c->world != 1 || r < 1 || r > 5 ||
-      c->N < 1)
+  if (c->persist_sym < 0 || !c->fused_tcg || !c->persist_tcg || c->world != 1 || r < 1 || r > 5 ||
+      c->N < 1 || c->opt.spmm_kernel == 1)
     return false;
+  if (c->persist_sym == 0 && c->N >= 4000) return false;
   const int G = std::min(148, c->N);
   return ceil_div(c->N, G) <= kPC && persist_sym_smem_r(r, c->N, G) <= kSmemCap;
 }
@@ -1158,8 +1221,7 @@ bool tcg_persist_sym_supported(xm_ctx* c, int r) {
 template <int R>
 static void launch_persist_sym(xm_ctx* c) {
   const int G = std::min(148, c->N);
-  SymTcgPlan& p = sym_tcg_plan(c, R);
-  const CUtensorMap* tm = q_tmap(c, kSB, p.tmap, &p.tmap_q, &p.tmap_bh, &p.tmap_n);
+  SymTcgPlan& p = sym_tcg_plan(c);
   const size_t smem = persist_sym_smem<R>(c->N, G);
   if (smem > kSmemCap) throw Error(XM_EINVAL, "symmetric persistent tCG smem plan exceeds 227 KB");
   static size_t attr = 0;
@@ -1186,7 +1248,7 @@ static void launch_persist_sym(xm_ctx* c) {
   a.pA = c->part1.p;
   a.pB = c->part2.p;
   a.gsync = c->gsync.p;
-  a.bh = kSB;
+  a.bh = kYR;
   if (c->phases_on) {
     if (!c->tdbg.p) {
       c->tdbg.alloc(148 * 8);
@@ -1194,19 +1256,16 @@ static void launch_persist_sym(xm_ctx* c) {
     }
     a.dbg = c->tdbg.p;
   }
-  sa.ubase = p.ubase.p;
-  sa.uimin = p.uimin.p;
+  sa.pbase = p.pbase.p;
   sa.segbase = p.segbase.p;
   sa.colptr = p.colptr.p;
-  sa.colidx = p.colidx.p;
   sa.RP = p.RP.p;
   sa.CP = p.CP.p;
-  sa.U = p.U;
-  sa.nJ = p.nJ;
-  sa.nI = p.nI;
+  sa.TCb = p.TCb;
+  sa.W = p.W;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(G);
-  cfg.blockDim = dim3(kPThreads);
+  cfg.blockDim = dim3(kPC);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = c->stream;
   cudaLaunchAttribute at[1];
@@ -1214,7 +1273,7 @@ static void launch_persist_sym(xm_ctx* c) {
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  XM_CUDA(cudaLaunchKernelEx(&cfg, k_tcg_persist_sym<R>, *tm, sa));
+  XM_CUDA(cudaLaunchKernelEx(&cfg, k_tcg_persist_sym<R>, *reinterpret_cast<const CUtensorMap*>(p.tmap), sa));
   XM_CHECK_LAUNCH();
   count_launch(c);
 }

@@ -515,7 +515,8 @@ xm_status xm_create(xm_ctx** out, int device, int rank, int world, const void* n
   if (std::getenv("XM_NO_FUSED_TCG")) c->fused_tcg = false;
   if (std::getenv("XM_NO_PERSIST_TCG")) c->persist_tcg = false;
   if (std::getenv("XM_NO_CUBLAS")) c->use_blas = false;
-  if (std::getenv("XM_SYM_TCG")) c->persist_sym = true;
+  if (std::getenv("XM_SYM_TCG")) c->persist_sym = 1;
+  if (std::getenv("XM_NO_SYM_TCG")) c->persist_sym = -1;
   if (std::getenv("XM_NO_GRAPHS")) c->use_graphs = false;
   if (c->opt.rank_cap > XM_MAX_R) c->opt.rank_cap = XM_MAX_R;
   xm_status st = guard(c, [&] {
@@ -659,9 +660,9 @@ xm_status xm_solve(xm_ctx* c, int32_t r0, double tol, xm_solve_info* info) {
         const int G = std::min(148, c->N);
         unsigned long long t0 = ~0ull;
         for (int b = 0; b < G; ++b) t0 = std::min(t0, h[b * 8]);
-        const char* nm[7] = {"start", "loop end", "pre-bar1", "post-bar1", "pre-bar2", "post-bar2",
-                             "end"};  // persistent kernel: stamps of iteration 1 ("start" = stream start)
-        for (int k = 0; k < 7; ++k) {
+        const char* nm[8] = {"start", "loop end", "pre-bar1", "post-bar1", "pre-bar2", "post-bar2",
+                             "end", "assembled"};  // persistent kernel: stamps of iteration 1
+        for (int k = 0; k < 8; ++k) {
           std::vector<double> v;
           for (int b = 0; b < G; ++b)
             if (h[b * 8 + k]) v.push_back((h[b * 8 + k] - t0) * 1e-3);
@@ -669,6 +670,11 @@ xm_status xm_solve(xm_ctx* c, int32_t r0, double tol, xm_solve_info* info) {
           std::sort(v.begin(), v.end());
           fprintf(stderr, "[xm fused tCG] %-9s min %7.2f  med %7.2f  max %7.2f us\n", nm[k], v.front(),
                   v[v.size() / 2], v.back());
+        }
+        if (std::getenv("XM_PHASES_CTA")) {  // per-CTA stream end (stamp 1), for balance studies
+          fprintf(stderr, "[xm fused tCG] loop end per CTA:");
+          for (int b = 0; b < G; ++b) fprintf(stderr, " %.1f", (h[b * 8 + 1] - t0) * 1e-3);
+          fprintf(stderr, "\n");
         }
       }
     }

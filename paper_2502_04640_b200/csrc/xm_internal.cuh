@@ -196,7 +196,7 @@ struct xm_ctx {
   bool fused_tcg = true;    // XM_NO_FUSED_TCG=1: three-kernel tCG iteration (A/B measurement)
   bool persist_tcg = true;  // XM_NO_PERSIST_TCG=1: one launch per tCG iteration instead
   bool use_blas = true;     // XM_NO_CUBLAS=1: the library's own k_dgemm for the dense updates
-  bool persist_sym = false; // XM_SYM_TCG=1: lower-triangle persistent tCG (tcg_persist.cu)
+  int persist_sym = 0;      // lower-triangle persistent tCG: 0 auto (N < 4000), 1 forced (XM_SYM_TCG), -1 off (XM_NO_SYM_TCG)
   void* persist_sym_plan = nullptr;
   xm::DBuf<double> dir2;    // δ ping-pong partner of dir (persistent tCG)
   cudaEvent_t ev_persist[2] = {nullptr, nullptr};

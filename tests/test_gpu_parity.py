@@ -143,7 +143,7 @@ def _e2e(xm, sc, Y0=None, ctx_opts=None, **opts):
 # tCG code paths on one GPU (xm_create reads these switches): the persistent
 # full-row kernel (default), the persistent lower-triangle kernel, one fused
 # launch per iteration, and three kernels per iteration in CUDA graphs
-TCG_PATHS = {"persist": {}, "persist_sym": {"XM_SYM_TCG": "1"},
+TCG_PATHS = {"persist": {"XM_NO_SYM_TCG": "1"}, "persist_sym": {"XM_SYM_TCG": "1"},
              "fused": {"XM_NO_PERSIST_TCG": "1"}, "3kernel": {"XM_NO_FUSED_TCG": "1"}}
 
 
