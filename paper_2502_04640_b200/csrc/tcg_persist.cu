@@ -477,12 +477,14 @@ constexpr int kYStageDbl = kYQDbl + 2 * kYR * 5;  // + r, Œ¥_{k‚àí1} slices (r ‚
 struct SymTcgArgs {
   TcgPersistArgs b;
   const int* pbase;    // TCb + 1: first tile of panel J
+  const int* tbase;    // G + 1: CTA c streams tiles [tbase[c], tbase[c+1]) (cost-balanced)
   const int* segbase;  // G + 1: first column-partial slot of CTA c
   const int* colptr;   // TCb + 1: slots [colptr[J], colptr[J+1]) hold panel J (consecutive)
   double* RP;          // [W][32][R] row partials, row-tile-major (rtile_base)
   double* CP;          // [slots][8 warps][R][256] column partials
   int TCb;
   int W;
+  int pmax;            // assembly lanes per element, at most (1, 2, 4, ‚Ä¶, 32)
 };
 
 // first row-part slot of row tile K: Œ£_{K'<K} (‚åäK'/8‚åã + 1)
@@ -555,8 +557,8 @@ __global__ void __launch_bounds__(kPC, 1) k_tcg_persist_sym(const __grid_constan
 
   const int G = gridDim.x;
   const int n = a.n;
-  const int t0 = (int)((int64_t)blockIdx.x * sa.W / G);
-  const int T = (int)((int64_t)(blockIdx.x + 1) * sa.W / G) - t0;  // tiles per iteration
+  const int t0 = __ldg(sa.tbase + blockIdx.x);
+  const int T = __ldg(sa.tbase + blockIdx.x + 1) - t0;  // tiles per iteration
   const int fa = (int)((int64_t)blockIdx.x * a.N / G);
   const int nf = (int)((int64_t)(blockIdx.x + 1) * a.N / G) - fa;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
@@ -832,31 +834,44 @@ __global__ void __launch_bounds__(kPC, 1) k_tcg_persist_sym(const __grid_constan
     // every load of an element in flight at once (latency, not bandwidth,
     // bounds this phase); this thread's ‚ü®Œ¥,HŒ¥‚ü© partial load overlaps it
     const double pa_mine = (t < G) ? __ldcg(a.pA + t) : 0.0;  // = csum_partials' assignment (G ‚â§ 256)
-    for (int o = t; o < 3 * nf * R; o += kPC) {
-      const int row = 3 * fa + o / R, cc = o % R;
+    // P consecutive lanes per element (P¬∑elements ‚â§ 256, P ‚â§ sa.pmax): lane
+    // j of a group sums list items j, j+P, ‚Ä¶ (batches of 32 loads in flight),
+    // then a fixed xor tree over the group.  The loop trip count is
+    // warp-uniform (the shuffles need every lane).
+    const int ne = 3 * nf * R;
+    int P = 1;
+    while (P < sa.pmax && 2 * P * ne <= kPC) P *= 2;
+    for (int ob = (t >> 5) * (32 / P); ob < ne; ob += kPC / P) {
+      const int o = ob + lane / P, j = lane % P;
+      const bool ok = o < ne;
+      const int oo = ok ? o : 0;
+      const int row = 3 * fa + oo / R, cc = oo % R;
       const int K = row / kYR, l = row % kYR, Jc = row / kYC, mcol = row % kYC;
       const double* p = sa.RP + (y_rtile_base(K) * kYR + l) * R + cc;
       constexpr int64_t st = kYR * R;
+      const int nrp = ok ? Jc + 1 : 0;
       double y2 = 0.0;
-      for (int q0 = 0; q0 <= Jc; q0 += 32) {  // panels q0 ‚Ä¶ q0+31 (zeros past Jc add exactly)
+      for (int q0 = j; q0 < nrp; q0 += 32 * P) {  // panels (zeros past Jc add exactly)
         double v[32];
 #pragma unroll
-        for (int u = 0; u < 32; ++u) v[u] = (q0 + u <= Jc) ? __ldcg(p + (int64_t)(q0 + u) * st) : 0.0;
+        for (int u = 0; u < 32; ++u) v[u] = (q0 + u * P < nrp) ? __ldcg(p + (int64_t)(q0 + u * P) * st) : 0.0;
 #pragma unroll
         for (int u = 0; u < 32; ++u) y2 += v[u];
       }
       // column partials of panel Jc: (slot, warp) pairs in order ‚Äî consecutive
-      // in the [slot][warp][cc][col] layout ‚Äî 32 loads in flight at a time
-      const int f0 = __ldg(sa.colptr + Jc) * kPW, nfl = __ldg(sa.colptr + Jc + 1) * kPW - f0;
+      // in the [slot][warp][cc][col] layout
+      const int f0 = __ldg(sa.colptr + Jc) * kPW, nfl = ok ? __ldg(sa.colptr + Jc + 1) * kPW - f0 : 0;
       const double* c = sa.CP + ((int64_t)f0 * R + cc) * kYC + mcol;
-      for (int q0 = 0; q0 < nfl; q0 += 32) {
+      for (int q0 = j; q0 < nfl; q0 += 32 * P) {
         double v[32];
 #pragma unroll
-        for (int u = 0; u < 32; ++u) v[u] = (q0 + u < nfl) ? __ldcg(c + (int64_t)(q0 + u) * R * kYC) : 0.0;
+        for (int u = 0; u < 32; ++u)
+          v[u] = (q0 + u * P < nfl) ? __ldcg(c + (int64_t)(q0 + u * P) * R * kYC) : 0.0;
 #pragma unroll
         for (int u = 0; u < 32; ++u) y2 += v[u];
       }
-      yown[o] = y2;
+      for (int o2 = 1; o2 < P; o2 <<= 1) y2 += __shfl_xor_sync(0xffffffffu, y2, o2);
+      if (ok && j == 0) yown[o] = y2;
     }
     // -------------------------------------------------- Œ±, boundary / œÑ, update
     const double dHd = csum(pa_mine, ws);  // its cbar also publishes yown
@@ -1119,7 +1134,7 @@ double tcg_persist_bytes_per_iter(xm_ctx* c, int r) {
 // slot bases, the slots of each panel, the 256 √ó 32 Q tensor map, partials.
 struct SymTcgPlan {
   int n = 0, G = 0, TCb = 0, W = 0, slots = 0;
-  DBuf<int> pbase, segbase, colptr;
+  DBuf<int> pbase, tbase, segbase, colptr;
   DBuf<double> RP, CP;
   alignas(64) unsigned char tmap[128] = {0};
   const void* tmap_q = nullptr;
@@ -1138,9 +1153,28 @@ static SymTcgPlan& sym_tcg_plan(xm_ctx* c) {
     std::vector<int> pb(p.TCb + 1, 0);
     for (int J = 0; J < p.TCb; ++J) pb[J + 1] = pb[J] + (TRt - kYDiag * J);
     p.W = pb[p.TCb];
+    // cost-balanced split: a tile costs 1, a diagonal-block tile 1 + c_d
+    // (masks), the first tile of a panel 1 + c_s (a CTA crossing into a new
+    // panel flushes a column partial and starts a segment); measured at B
+    // with XM_PHASES_CTA: a second segment ‚âà +1.5 tiles of stream time
+    double cs = 1.5, cd = 0.1;
+    if (const char* e = std::getenv("XM_PSYM_CSEG")) cs = atof(e);
+    if (const char* e = std::getenv("XM_PSYM_CDIAG")) cd = atof(e);
+    std::vector<double> cum(p.W + 1, 0.0);
+    for (int J = 0, tt = 0; J < p.TCb; ++J)
+      for (int x = 0; x < pb[J + 1] - pb[J]; ++x, ++tt)
+        cum[tt + 1] = cum[tt] + 1.0 + (x < kYDiag ? cd : 0.0) + (x == 0 ? cs : 0.0);
+    std::vector<int> tb(G + 1, 0);
+    for (int cta = 1; cta < G; ++cta) {
+      const double target = cum[p.W] * cta / G;
+      int tt = tb[cta - 1];
+      while (tt < p.W && cum[tt] < target) ++tt;
+      tb[cta] = tt;
+    }
+    tb[G] = p.W;
     std::vector<int> sb(G + 1, 0), segpanel;
     for (int cta = 0; cta < G; ++cta) {
-      const int64_t t0 = (int64_t)cta * p.W / G, t1 = (int64_t)(cta + 1) * p.W / G;
+      const int64_t t0 = tb[cta], t1 = tb[cta + 1];
       sb[cta] = (int)segpanel.size();
       int J = 0;
       for (int64_t tt = t0; tt < t1;) {
@@ -1157,6 +1191,8 @@ static SymTcgPlan& sym_tcg_plan(xm_ctx* c) {
       cp[J] = s;
     }
     p.pbase.alloc(pb.size());
+    p.tbase.alloc(tb.size());
+    XM_CUDA(cudaMemcpy(p.tbase.p, tb.data(), tb.size() * 4, cudaMemcpyHostToDevice));
     p.segbase.alloc(sb.size());
     p.colptr.alloc(cp.size());
     XM_CUDA(cudaMemcpy(p.pbase.p, pb.data(), pb.size() * 4, cudaMemcpyHostToDevice));
@@ -1257,12 +1293,15 @@ static void launch_persist_sym(xm_ctx* c) {
     a.dbg = c->tdbg.p;
   }
   sa.pbase = p.pbase.p;
+  sa.tbase = p.tbase.p;
   sa.segbase = p.segbase.p;
   sa.colptr = p.colptr.p;
   sa.RP = p.RP.p;
   sa.CP = p.CP.p;
   sa.TCb = p.TCb;
   sa.W = p.W;
+  sa.pmax = 32;
+  if (const char* e = std::getenv("XM_PSYM_PMAX")) sa.pmax = std::max(1, std::min(32, atoi(e)));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(G);
   cfg.blockDim = dim3(kPC);

@@ -674,6 +674,10 @@ xm_status xm_solve(xm_ctx* c, int32_t r0, double tol, xm_solve_info* info) {
         if (std::getenv("XM_PHASES_CTA")) {  // per-CTA stream end (stamp 1), for balance studies
           fprintf(stderr, "[xm fused tCG] loop end per CTA:");
           for (int b = 0; b < G; ++b) fprintf(stderr, " %.1f", (h[b * 8 + 1] - t0) * 1e-3);
+          fprintf(stderr, "\n[xm fused tCG] assembly per CTA:");
+          for (int b = 0; b < G; ++b) fprintf(stderr, " %.1f", (h[b * 8 + 7] - h[b * 8 + 3]) * 1e-3);
+          fprintf(stderr, "\n[xm fused tCG] camera per CTA:");
+          for (int b = 0; b < G; ++b) fprintf(stderr, " %.1f", (h[b * 8 + 4] - h[b * 8 + 7]) * 1e-3);
           fprintf(stderr, "\n");
         }
       }
