@@ -342,14 +342,18 @@ def main():
                   "cert_method": ["lanczos", "cholesky(Z+eps*I)"][cert["method"]],
                   "eta": cert["eta"], "rho_hat": cert["rho_hat"], "status": st},
         "phases_ms": {k: stats[k] / args.steps for k in ("ms_build", "ms_solve", "ms_certify", "ms_round")},
-        "roofline": {"kernel": "k_spmm (Q·V stream; one launch per tCG iteration incl. its "
-                               "fused update)", "bound": "hbm", "achieved": achieved,
+        "roofline": {"kernel": ("k_tcg_persist_sym (lower-triangle Q stream, timed per tCG iteration "
+                                "incl. its barriers and camera update) + k_spmm_sym (other products)"
+                                if sc.N < 4000 else
+                                "k_spmm_sym (lower-triangle Q stream, every product incl. the tCG HVP)"),
+                     "bound": "hbm", "achieved": achieved,
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "alg_bytes_per_launch": bytes_per_launch, "launch_ms": spmm_ms_per_launch,
                      "launches": pstats["spmm_timed"], "share_of_step": spmm_share,
-                     "timing": "CUDA events around every k_spmm launch, on the library's stream, "
-                               "over a second run of the same K steps"},
+                     "timing": "CUDA events around every Q-streaming launch (persistent tCG: per launch "
+                               "÷ its iterations), on the library's stream, over a second run of the "
+                               "same K steps"},
         "gpu_launches": int(stats["kernel_launches"]),
         "e2e": e2e,
     }
