@@ -841,7 +841,6 @@ __global__ void __launch_bounds__(kPC, 1) k_tcg_persist_sym(const __grid_constan
     const int ne = 3 * nf * R;
     int P = 1;
     while (P < sa.pmax && 2 * P * ne <= kPC) P *= 2;
-#ifndef XM_EXP_NOASM
     for (int ob = (t >> 5) * (32 / P); ob < ne; ob += kPC / P) {
       const int o = ob + lane / P, j = lane % P;
       const bool ok = o < ne;
@@ -874,7 +873,6 @@ __global__ void __launch_bounds__(kPC, 1) k_tcg_persist_sym(const __grid_constan
       for (int o2 = 1; o2 < P; o2 <<= 1) y2 += __shfl_xor_sync(0xffffffffu, y2, o2);
       if (ok && j == 0) yown[o] = y2;
     }
-#endif
     // -------------------------------------------------- α, boundary / τ, update
     const double dHd = csum(pa_mine, ws);  // its cbar also publishes yown
     XM_PSTAMP(7);
@@ -896,11 +894,7 @@ __global__ void __launch_bounds__(kPC, 1) k_tcg_persist_sym(const __grid_constan
     }
     const double step = s.boundary ? s.tau : alpha;
     double rn2 = 0.0;
-#ifndef XM_EXP_NOCAM
     if (has) {
-#else
-    if (false) {
-#endif
       Blk<R> qv, hd, e, he;
 #pragma unroll
       for (int p = 0; p < 3; ++p)
