@@ -869,3 +869,93 @@ def solve(scene_or_arrays, opts: Options = None, Y0=None, dense_cert=False):
     sol = round_recover(dm, st.Y)
     rep = report(st.cert, sol.rho_hat, dm.normF, (opts or Options()).cert_tol)
     return dm, st, sol, rep
+
+
+# =============================================================================
+# XM² — drop the largest-residual measurements and solve again
+# ("delete the 10% measurements with the largest residuals and re-run the
+# XM solver … XM² (running twice)"; S:472-476 edge_residuals
+# xm_squared; reading C22 in DESIGN.md)
+# =============================================================================
+
+def edge_residuals(frame, landmark, pts, w, sol: Solution) -> np.ndarray:
+    """The summands of Eq. (3):
+    res_e = w_e ‖s_i R_i ũ_e + t_i − p_k‖² at a recovered solution.
+    Their sum is `edge_objective`."""
+    frame = np.asarray(frame, np.int64)
+    landmark = np.asarray(landmark, np.int64)
+    pts = np.asarray(pts, np.float64).reshape(-1, 3)
+    w = np.ones(len(frame)) if w is None else np.asarray(w, np.float64)
+    res = np.empty(len(frame))
+    for e in range(len(frame)):                      # one observation at a time
+        i, k = frame[e], landmark[e]
+        d = sol.s[i] * (sol.R[i] @ pts[e]) + sol.t[i] - sol.p[k]
+        res[e] = w[e] * float(d @ d)
+    return res
+
+
+def xm2_select(N: int, M: int, frame, landmark, res, drop_fraction: float = 0.1) -> np.ndarray:
+    """Which measurements XM² keeps (reading C22).
+
+    1. Order the E measurements by residual, largest first; equal residuals
+       by (landmark, frame) ascending.  Drop the first ⌊drop_fraction·E⌋.
+    2. Never disconnect: if some frame is no longer in the
+       component of the others (bipartite frame–landmark graph of the kept
+       measurements), restore dropped measurements in the reverse of the drop
+       order (smallest residual first), each one only if it joins two
+       components, until all frames are in one component (S:518's "restore
+       minimal edges by ascending residual until connected").
+    Returns a boolean keep mask over the E measurements."""
+    frame = np.asarray(frame, np.int64)
+    landmark = np.asarray(landmark, np.int64)
+    E = len(frame)
+    nd = int(math.floor(drop_fraction * E))
+    order = sorted(range(E), key=lambda e: (-res[e], int(landmark[e]), int(frame[e])))
+    dropped = order[:nd]
+    keep = np.ones(E, dtype=bool)
+    keep[dropped] = False
+    parent = list(range(N + M))                      # frames 0..N-1, landmarks N..N+M-1
+
+    def find(x):
+        while parent[x] != x:
+            x = parent[x]
+        return x
+
+    for e in np.nonzero(keep)[0]:
+        a, b = find(int(frame[e])), find(N + int(landmark[e]))
+        if a != b:
+            parent[b] = a
+    has_frame = {}
+    for i in range(N):
+        has_frame[find(i)] = True
+    n_frame_comps = len(has_frame)
+    for e in reversed(dropped):                      # smallest residual first
+        if n_frame_comps == 1:
+            break
+        a, b = find(int(frame[e])), find(N + int(landmark[e]))
+        if a == b:
+            continue
+        fa, fb = has_frame.get(a, False), has_frame.get(b, False)
+        parent[b] = a
+        has_frame[a] = fa or fb
+        keep[e] = True
+        if fa and fb:
+            n_frame_comps -= 1
+    return keep
+
+
+def xm2(scene, opts: Options = None, drop_fraction: float = 0.1, dense_cert=False):
+    """XM²: solve, rank the (de-duplicated) measurements by
+    `edge_residuals` at the recovered solution, keep `xm2_select`'s set,
+    rebuild Q and solve again.  Returns (first, keep, residuals, second) with
+    first / second = solve()'s (dm, staircase, solution, report)."""
+    s = scene
+    first = solve(s, opts, dense_cert=dense_cert)
+    fr, lm, pts, w, _ = validate(s.N, s.M, s.frame, s.landmark, s.pts, s.w)
+    res = edge_residuals(fr, lm, pts, w, first[2])
+    keep = xm2_select(s.N, s.M, fr, lm, res, drop_fraction)
+    s2 = dataclasses.replace(s, frame=fr[keep].astype(np.int32), landmark=lm[keep].astype(np.int32),
+                             pts=pts[keep], w=w[keep]) if dataclasses.is_dataclass(s) else \
+        type("Scene2", (), dict(N=s.N, M=s.M, frame=fr[keep], landmark=lm[keep], pts=pts[keep], w=w[keep]))
+    second = solve(s2, opts, dense_cert=dense_cert)
+    return first, keep, res, second

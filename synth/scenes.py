@@ -509,3 +509,22 @@ def splitmix64_uniform(seed: int, n: int) -> np.ndarray:
         z = z ^ (z >> 31)
         out[j] = 2.0 * ((z >> 11) * (1.0 / 9007199254740992.0)) - 1.0
     return out
+
+
+def corrupt(sc: Scene, frac: float, seed: int = 0, bearing: float = 0.3, log_depth: float = 0.3):
+    """Outlier measurements for XM² tests: a seeded fraction of the
+    lifted keypoints gets its normalized image coordinates shifted by
+    U(−bearing, bearing) and its depth scaled by exp(U(−log_depth, log_depth))
+    (gross but not scale-collapsing; larger corruptions drive the SDP optimum
+    to collapsed scales).  Returns (new Scene, sorted indices of
+    the corrupted measurements)."""
+    rng = np.random.default_rng(np.random.SeedSequence([int(seed), sc.E, 0x4F55]))
+    m = int(round(frac * sc.E))
+    idx = np.sort(rng.choice(sc.E, size=m, replace=False))
+    pts = sc.pts.copy()
+    d = pts[idx, 2].copy()
+    u = pts[idx, :2] / d[:, None] + rng.uniform(-bearing, bearing, (m, 2))
+    d = d * np.exp(rng.uniform(-log_depth, log_depth, m))
+    pts[idx, :2] = u * d[:, None]
+    pts[idx, 2] = d
+    return dataclasses.replace(sc, pts=pts, noise_free=False, name=sc.name + f"-out{frac:g}"), idx

@@ -524,3 +524,104 @@ def test_validation_errors():
     p2 = np.concatenate([pts, [[9.0, 9.0, 9.0]]])
     out = xo.validate(2, 2, f2, l2, p2)
     assert out[4] == 1 and len(out[0]) == 4 and not np.any(out[2][:, 0] == 9.0)
+
+
+# ---------------------------------------------------------------------------
+# XM² (S:472-476 edge_residuals, S:533-537 xm_squared; reading C22)
+# ---------------------------------------------------------------------------
+
+def _rot_err(R, Rg):
+    """Geodesic angle via atan2 (F12 practical note)."""
+    M = R.transpose(0, 2, 1) @ Rg
+    sk = M - M.transpose(0, 2, 1)
+    sn = np.linalg.norm(sk, axis=(1, 2)) / math.sqrt(2)
+    return np.arctan2(sn, np.trace(M, axis1=1, axis2=2) - 1.0)
+
+
+def test_edge_residuals_sum_to_eq3_and_are_linear_in_w():
+    """Σ residuals = Eq. (3) at the solution, here evaluated by the
+    brute-force marginal least squares (independent of the oracle's recovery);
+    S:478: doubling one weight doubles that residual only."""
+    sc = make_scene(8, 120, "unordered", seed=5, vis_prob=0.6, sigma_u=1e-2, sigma_d=0.05)
+    dm, st, sol, rep = xo.solve(sc)
+    res = xo.edge_residuals(sc.frame, sc.landmark, sc.pts, sc.w, sol)
+    assert np.all(res >= 0)
+    brute = brute_marginal_objective(sc, sol.Yr)     # min over (t, p) at the rounded U
+    assert abs(res.sum() - brute) <= 1e-9 * (1 + brute)
+    w2 = sc.w.copy()
+    w2[7] *= 2.0
+    res2 = xo.edge_residuals(sc.frame, sc.landmark, sc.pts, w2, sol)
+    assert res2[7] == pytest.approx(2 * res[7], rel=1e-14)
+    assert np.array_equal(np.delete(res2, 7), np.delete(res, 7))
+
+
+def test_xm2_select_count_and_order():
+    """S:538: 10 edges → exactly ⌊0.1·10⌋ = 1 dropped, the largest residual;
+    ties broken by (landmark, frame) ascending (C22)."""
+    N, M = 2, 5
+    fr = np.array([0, 1] * 5)
+    lm = np.repeat(np.arange(5), 2)
+    res = np.array([1.0, 2, 3, 4, 5, 6, 7, 9, 8, 0.5])
+    keep = xo.xm2_select(N, M, fr, lm, res, 0.1)
+    assert (~keep).sum() == 1 and not keep[7]
+    res_tie = np.array([9.0, 1, 1, 1, 9, 1, 1, 1, 1, 1])  # edges 0 (lm 0) and 4 (lm 2) tie
+    keep = xo.xm2_select(N, M, fr, lm, res_tie, 0.1)
+    assert not keep[0] and keep[4]
+    E = 37
+    rng = np.random.default_rng(0)
+    fr = np.concatenate([np.zeros(20, int), np.ones(17, int)])
+    lm = np.concatenate([np.arange(20), np.arange(17)])   # landmarks 0..16 seen by both frames
+    keep = xo.xm2_select(2, 20, fr, lm, rng.uniform(size=E), 0.1)
+    assert (~keep).sum() == math.floor(0.1 * E)
+
+
+def test_xm2_select_restores_minimal_bridges():
+    """S:536/S:562 never disconnect: in a chain of 4 frames joined by single
+    landmarks, dropping the top residuals would cut bridges; exactly the
+    bridges needed to reconnect are restored, smallest residual first."""
+    # frames 0-1 share landmark 0; 1-2 share landmark 1; 2-3 share landmark 2;
+    # each frame also sees 4 private landmarks (3..18)
+    fr, lm = [], []
+    for i, k in [(0, 0), (1, 0), (1, 1), (2, 1), (2, 2), (3, 2)]:
+        fr.append(i), lm.append(k)
+    for i in range(4):
+        for q in range(4):
+            fr.append(i), lm.append(3 + 4 * i + q)
+    fr, lm = np.array(fr), np.array(lm)
+    E = len(fr)                                      # 22 → ⌊2.2⌋ = 2 dropped
+    res = np.ones(E)
+    res[1], res[3] = 10.0, 20.0                      # (1,0) and (2,1): both bridge edges
+    keep = xo.xm2_select(4, 19, fr, lm, res, 0.1)
+    assert keep[1] and keep[3]                       # both had to come back
+    assert xo.connected_components(4, 19, fr[keep], lm[keep]) == 1
+    res[5] = 15.0                                    # a third candidate: (3,2), also a bridge
+    keep = xo.xm2_select(4, 19, fr, lm, res, 0.1)    # drops (2,1) and (3,2); both restored
+    assert keep.all()
+
+
+def test_xm2_noise_free_keeps_the_optimum():
+    """S:537 example: noise-free scene → both solves reach the known optimum
+    (f = 0, GT poses); the dropped 10% do not change the solution."""
+    sc = make_scene(10, 300, "unordered", seed=2, vis_prob=0.6)
+    first, keep, res, second = xo.xm2(sc)
+    assert (~keep).sum() == math.floor(0.1 * sc.E)
+    for (dm, st, sol, rep) in (first, second):
+        assert st.certified
+        assert abs(st.f) <= 1e-8 * (1 + dm.normF)
+        assert np.max(np.abs(sol.s - sc.s)) <= 1e-6
+        assert np.max(_rot_err(sol.R, sc.R)) <= 1e-6
+
+
+def test_xm2_removes_outliers():
+    """P:569 (greedy outlier removal): with 4% outliers (bearing ±0.3,
+    depth ×e^±0.3) the dropped 10% hold most corrupted measurements and the
+    second solve's rotations are much closer to the ground truth."""
+    from synth.scenes import corrupt
+    sc0 = make_scene(12, 400, "unordered", seed=4, vis_prob=0.5, sigma_u=1e-3, sigma_d=0.01)
+    sc, bad = corrupt(sc0, 0.04, seed=4)
+    first, keep, res, second = xo.xm2(sc)
+    assert keep[bad].mean() < 0.2                    # ≥ 80% of the outliers dropped
+    assert keep[np.setdiff1d(np.arange(sc.E), bad)].mean() > 0.9
+    e1 = np.max(_rot_err(first[2].R, sc.R))
+    e2 = np.max(_rot_err(second[2].R, sc.R))
+    assert e2 < 0.5 * e1
