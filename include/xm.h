@@ -201,6 +201,32 @@ xm_status xm_certify(xm_ctx* ctx, xm_certificate* out, double* min_eigvec);
 xm_status xm_round_recover(xm_ctx* ctx, double* R, double* s, double* t, double* p,
                            int32_t* n_flipped);
 
+/* ---------------------------------------------------------------- XM²
+ * "delete the 10% measurements with the largest
+ * residuals and re-run the XM solver … XM² (running twice)", with
+ * SPEC's residual and never-disconnect rule;
+ * selection / restoration order = reading C22.
+ *
+ * xm_edge_residuals: res[e] = w_e‖s_i R_i ũ_e + t_i − p_k‖² (the Eq. (3)
+ *   summand) at the recovered solution of the last solve (rounds
+ *   first if xm_round_recover was not called), for every measurement e of the
+ *   caller's last xm_build_Q input, in that order (E doubles, host or device);
+ *   NaN for duplicates and for measurements an XM² step dropped.  Requires a
+ *   solve on a view graph (XM_ESTATE otherwise, or after xm_set_Q).
+ * xm_xm2: rank the measurements in use by that residual (largest first,
+ *   equal residuals by (landmark, frame) ascending), drop ⌊drop_fraction·E⌋,
+ *   restore dropped ones smallest-residual-first where needed to keep the
+ *   frames connected, and rebuild Q from the rest on the device.  The context
+ *   returns to "Q built": call xm_solve / xm_certify / xm_round_recover again.
+ *   keep (E bytes, caller's input order, host or device, or NULL): 1 for the
+ *   measurements the rebuilt Q uses.  n_dropped / n_restored (or NULL): net
+ *   drops and restorations.  drop_fraction ∉ [0, 1) ⇒ XM_EINVAL; a graph that
+ *   no restoration reconnects ⇒ XM_EDISCONNECTED.  Repeated calls compose
+ *   (indices always refer to the caller's original input). */
+xm_status xm_edge_residuals(xm_ctx* ctx, double* res);
+xm_status xm_xm2(xm_ctx* ctx, double drop_fraction, uint8_t* keep, int64_t* n_dropped,
+                 int64_t* n_restored);
+
 /* ----------------------------------------------------- test / bench hooks */
 /* S's co-visibility BSR pattern (H3): rowptr N+1 (int64), colidx nnzb (int32,
  * sorted per row).  Call with colidx == NULL to query *nnzb. */

@@ -70,7 +70,7 @@ __global__ void k_gather_edges(int64_t E, const uint64_t* __restrict__ key2,
                                int N, const double* __restrict__ pts, const double* __restrict__ w,
                                int32_t* __restrict__ e_fr, int32_t* __restrict__ e_lm,
                                double* __restrict__ e_pts, double* __restrict__ e_w,
-                               int32_t* __restrict__ fr_edge) {
+                               int32_t* __restrict__ fr_edge, int32_t* __restrict__ e_in) {
   int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= E) return;
   uint64_t k = key2[c];
@@ -82,6 +82,7 @@ __global__ void k_gather_edges(int64_t E, const uint64_t* __restrict__ key2,
   e_pts[3 * c + 1] = pts[3 * (int64_t)ein + 1];
   e_pts[3 * c + 2] = pts[3 * (int64_t)ein + 2];
   e_w[c] = w ? w[ein] : 1.0;
+  e_in[c] = ein;
   fr_edge[j] = (int32_t)c;
 }
 
@@ -752,9 +753,10 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
   c->e_pts.alloc(3 * Ek);
   c->e_w.alloc(Ek);
   c->fr_edge.alloc(Ek);
+  c->e_in.alloc(Ek);
   k_gather_edges<<<ceil_div(Ek, T), T, 0, c->stream>>>(Ek, key2.p, val2.p, fs_in.p, N, pts, w,
                                                       c->e_fr.p, c->e_lm.p, c->e_pts.p, c->e_w.p,
-                                                      c->fr_edge.p);
+                                                      c->fr_edge.p, c->e_in.p);
   XM_CHECK_LAUNCH();
   count_launch(c);
   DBuf<int32_t>& cnt = scratch_i32(c, "cnt");

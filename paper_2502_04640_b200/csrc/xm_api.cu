@@ -560,7 +560,9 @@ xm_status xm_build_Q(xm_ctx* c, int32_t N, int32_t M, int64_t E, const int32_t* 
   return guard(c, [&] {
     double t0 = now_ms();
     c->stage = 0;
+    c->orig_in.release();  // the caller's input order
     build_Q_device(c, N, M, E, frame, landmark, lifted_pts, weights);
+    c->E_user = E;
     reset_after_new_Q(c);
     sync(c);
     c->stats.ms_build += now_ms() - t0;
@@ -777,6 +779,44 @@ xm_status xm_round_recover(xm_ctx* c, double* R, double* s, double* t, double* p
     if (n_flipped) *n_flipped = c->n_flipped;
     sync(c);
     c->stats.ms_round += now_ms() - t0;
+  });
+}
+
+// ----------------------------------------------------------------- XM²
+// SURVEY §8(f) NEXT-2 (reading C22): residuals
+// of the measurements at the recovered solution, and the drop-10%-and-rebuild
+// step (the caller then solves / certifies / rounds again).
+xm_status xm_edge_residuals(xm_ctx* c, double* res) {
+  if (!c || !res) return XM_EINVAL;
+  return guard(c, [&] {
+    require_stage(c, 1);
+    if (c->r == 0) throw Error(XM_ESTATE, "no factor");
+    if (!c->have_recovery) throw Error(XM_ESTATE, "no view graph (Q was set directly)");
+    if (!c->have_round) round_recover_device(c);
+    DBuf<double>& out = scratch_f64(c, "xm2_user_res");
+    out.alloc(std::max<int64_t>(c->E_user, 1));
+    edge_residuals_user(c, out.p);
+    copy_out(c, res, out.p, (size_t)c->E_user * 8);
+    sync(c);
+  });
+}
+
+xm_status xm_xm2(xm_ctx* c, double drop_fraction, uint8_t* keep, int64_t* n_dropped, int64_t* n_restored) {
+  if (!c || !(drop_fraction >= 0.0 && drop_fraction < 1.0)) return XM_EINVAL;
+  return guard(c, [&] {
+    require_stage(c, 1);
+    if (c->r == 0) throw Error(XM_ESTATE, "no factor");
+    if (!c->have_recovery) throw Error(XM_ESTATE, "no view graph (Q was set directly)");
+    const double t0 = now_ms();
+    if (!c->have_round) round_recover_device(c);
+    DBuf<uint32_t>& kb = scratch_u32(c, "xm2_user_keep");
+    kb.alloc((size_t)c->E_user / 4 + 2);
+    uint8_t* kd = reinterpret_cast<uint8_t*>(kb.p);
+    xm2_device(c, drop_fraction, kd, n_dropped, n_restored);
+    reset_after_new_Q(c);
+    if (keep) copy_out(c, keep, kd, (size_t)c->E_user);
+    sync(c);
+    c->stats.ms_build += now_ms() - t0;
   });
 }
 

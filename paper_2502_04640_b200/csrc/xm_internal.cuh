@@ -100,6 +100,7 @@ struct xm_ctx {
   // problem
   int N = 0, M = 0;
   int64_t E = 0;      // after de-duplication
+  int64_t E_user = 0; // measurements in the caller's last xm_build_Q input (XM² maps back to it)
   int n = 0;          // 3N
   int64_t ldq = 0;    // leading dimension of Q / G rows (padded to 32 doubles)
   int64_t ldk = 0;    // leading dimension of K̄ / L
@@ -109,6 +110,8 @@ struct xm_ctx {
 
   // canonical edges (sorted by (landmark, frame))
   xm::DBuf<int32_t> e_fr, e_lm;
+  xm::DBuf<int32_t> e_in;     // canonical measurement → index in the last build's input
+  xm::DBuf<int32_t> orig_in;  // XM² rebuilds: build-input index → caller's index (empty: identity)
   xm::DBuf<double> e_pts, e_w;
   xm::DBuf<int32_t> lm_off, fr_off, fr_edge;  // track / frame offsets, frame-sorted edge ids
   xm::DBuf<double> W;                        // per-landmark weight Σ w_e (Q_3 diag)
@@ -331,6 +334,9 @@ void zmul(xm_ctx* c, const double* x, const double* Zx_q, double* out);  // Zx =
 bool lanczos(xm_ctx* c, double tol_abs, int max_steps, double* lambda, int* steps,
              double* vec_dev);
 void round_recover_device(xm_ctx* c);
+// xm2.cu
+void edge_residuals_user(xm_ctx* c, double* out_dev);
+void xm2_device(xm_ctx* c, double frac, uint8_t* keep_user_dev, int64_t* n_dropped, int64_t* n_restored);
 
 // ------------------------------------------------------------ NCCL (comm.cu)
 void nccl_unique_id(void* out128);

@@ -87,6 +87,8 @@ _SIGS = {
     "xm_solve": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_double, _P]),
     "xm_certify": (ctypes.c_int, [_P, _P, _P]),
     "xm_round_recover": (ctypes.c_int, [_P, _P, _P, _P, _P, _P]),
+    "xm_edge_residuals": (ctypes.c_int, [_P, _P]),
+    "xm_xm2": (ctypes.c_int, [_P, ctypes.c_double, _P, _P, _P]),
     "xm_get_S_pattern": (ctypes.c_int, [_P, _P, _P, _P]),
     "xm_get_Q_rows": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int32, _P]),
     "xm_set_Q": (ctypes.c_int, [_P, ctypes.c_int32, _P]),
@@ -205,6 +207,7 @@ class Context:
         self._check(st, "xm_create")
         self.options = opts
         self.N = self.M = self.n = 0
+        self.E_user = 0
         self.r = 0
 
     # ------------------------------------------------------------------
@@ -243,6 +246,7 @@ class Context:
                                  _in_ptr(w, np.float64, keep))
         self._check(st, "xm_build_Q")
         self.N, self.M, self.n = int(N), int(M), 3 * int(N)
+        self.E_user = E
 
     def solve(self, r0: int = 3, tol: float = 0.0):
         info = SolveInfo()
@@ -273,6 +277,21 @@ class Context:
                                        p.ctypes.data, ctypes.byref(nf))
         self._check(st, "xm_round_recover")
         return dict(R=R, s=s, t=t, p=p[: self.M], n_flipped=int(nf.value))
+
+    def edge_residuals(self):
+        """Eq. (3) summand per measurement of the last build input (xm.h)."""
+        res = np.empty(max(self.E_user, 1))
+        self._check(self.lib.xm_edge_residuals(self.h, res.ctypes.data), "xm_edge_residuals")
+        return res[: self.E_user]
+
+    def xm2(self, drop_fraction: float = 0.1):
+        """XM² step (xm.h): drop, restore, rebuild Q.  Returns (keep mask over
+        the original input, n_dropped, n_restored); solve / certify / round again."""
+        keep = np.zeros(max(self.E_user, 1), dtype=np.uint8)
+        nd, nr = ctypes.c_int64(), ctypes.c_int64()
+        self._check(self.lib.xm_xm2(self.h, float(drop_fraction), keep.ctypes.data, ctypes.byref(nd),
+                                    ctypes.byref(nr)), "xm_xm2")
+        return keep[: self.E_user].astype(bool), int(nd.value), int(nr.value)
 
     def round_recover_into(self, R, s, t, p):
         """Same as round_recover, writing into caller buffers (torch tensors on

@@ -1,0 +1,115 @@
+"""GPU parity for XM² (
+reading C22), through the C ABI (xm_edge_residuals, xm_xm2) against the
+oracle (oracle.xm_oracle.edge_residuals / xm2_select / xm2)."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import xm_oracle as xo
+from synth.scenes import corrupt, make_scene
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def xm():
+    from paper_2502_04640_b200 import xm as _xm
+    _xm.load_library()
+    return _xm
+
+
+def x_rel_err(Yg, Yo):
+    Xg, Xo = Yg @ Yg.T, Yo @ Yo.T
+    return np.linalg.norm(Xg - Xo) / np.linalg.norm(Xo)
+
+
+def _gpu_first(xm, sc):
+    ctx = xm.Context(device=0)
+    ctx.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+    st, info = ctx.solve(r0=3)
+    sol = ctx.round_recover()
+    return ctx, st, info, sol
+
+
+def test_edge_residuals_kernel_matches_formula(xm):
+    """The device residuals equal the Eq. (3) summand (oracle formula) at the
+    GPU's own recovered solution, element by element; duplicates are NaN."""
+    sc = make_scene(14, 500, "unordered", seed=8, vis_prob=0.5, sigma_u=1e-3, sigma_d=0.02,
+                    weights="uniform")
+    # one duplicate measurement appended: ignored by the build, NaN residual
+    fr = np.concatenate([sc.frame, sc.frame[:1]])
+    lm = np.concatenate([sc.landmark, sc.landmark[:1]])
+    pts = np.concatenate([sc.pts, sc.pts[:1] * 1.1])
+    w = np.concatenate([sc.w, sc.w[:1]])
+    with xm.Context(device=0) as ctx:
+        ctx.build_Q(sc.N, sc.M, fr, lm, pts, w)
+        st, info = ctx.solve(r0=3)
+        sol = ctx.round_recover()
+        res = ctx.edge_residuals()
+    assert st == 0 and res.shape == (sc.E + 1,)
+    assert np.isnan(res[-1]) and np.all(np.isfinite(res[:-1]))
+    osol = xo.Solution(R=sol["R"], s=sol["s"], t=sol["t"], p=sol["p"], n_flipped=0, Yr=None,
+                       rho_hat=0.0, edge_objective=0.0)
+    ref = xo.edge_residuals(sc.frame, sc.landmark, sc.pts, sc.w, osol)
+    assert np.max(np.abs(res[:-1] - ref) / (np.abs(ref) + 1e-12 * np.max(ref))) <= 1e-10
+    # the sum is Eq. (3) at the solution = ρ̂ (F13)
+    eq3 = xo.edge_objective(sc.frame, sc.landmark, sc.pts, sc.w, sol["s"], sol["R"], sol["t"], sol["p"])
+    assert abs(res[:-1].sum() - eq3) <= 1e-10 * (1 + eq3)
+
+
+@pytest.mark.parametrize("case", ["outliers", "restoration"])
+def test_xm2_parity(xm, case):
+    """Same measurements dropped as the oracle: the masks agree except inside
+    groups of equal residuals (e.g. the two measurements of a two-view
+    landmark have exactly equal residuals, so the two sides' last-bit
+    differences may order them either way); the oracle's residuals of the
+    dropped sets then agree value by value.  The second solve agrees with the
+    oracle's solve of the same kept set: f ≤ 1e-8(1+|f|), X = YYᵀ ≤ 1e-6
+    relative, rotations / scales ≤ 1e-6."""
+    if case == "outliers":
+        sc0 = make_scene(12, 400, "unordered", seed=4, vis_prob=0.5, sigma_u=1e-3, sigma_d=0.01)
+        sc, bad = corrupt(sc0, 0.04, seed=4)
+        frac = 0.1
+    else:  # sparse road scene where dropping half the measurements splits the graph
+        sc = make_scene(12, 60, "road", seed=3, sigma_u=1e-3, sigma_d=0.01, track_mean=3.0)
+        frac = 0.5
+    first, okeep, ores, second = xo.xm2(sc, drop_fraction=frac)
+    ctx, st, info, sol = _gpu_first(xm, sc)
+    with ctx:
+        assert st == 0
+        keep, n_drop, n_rest = ctx.xm2(frac)
+        nd = math.floor(frac * sc.E)
+        assert n_drop + n_rest == nd and (~keep).sum() == n_drop
+        assert (n_rest > 0) == (case == "restoration")
+        assert (~keep).sum() == (~okeep).sum()
+        a, b = np.sort(ores[~keep]), np.sort(ores[~okeep])
+        assert np.all(np.abs(a - b) <= 1e-9 * np.maximum(np.abs(b), 1e-12)), (a, b)
+        if case == "outliers":
+            assert np.array_equal(keep, okeep)       # no ties near the cut here
+        assert xo.connected_components(sc.N, sc.M, sc.frame[keep], sc.landmark[keep]) == 1
+        # the rebuilt Q is the data matrix of exactly the kept measurements
+        dmk = xo.build_Q(sc.N, sc.M, sc.frame[keep], sc.landmark[keep], sc.pts[keep], sc.w[keep])
+        Qg = ctx.Q_rows(0, 3 * sc.N)
+        assert np.linalg.norm(Qg - dmk.Q) <= 1e-10 * dmk.normF
+        if case == "restoration":
+            return  # half the measurements gone: the second SDP optimum collapses scales (C18)
+        st2, info2 = ctx.solve(r0=3)
+        cert2 = ctx.certify()
+        sol2 = ctx.round_recover()
+        Yg = ctx.get_factor()
+        res2 = ctx.edge_residuals()
+    if np.array_equal(keep, okeep):
+        dm2, st_o, osol2, rep2 = second
+    else:  # the oracle's solve of the GPU's kept set
+        import dataclasses
+        sc2 = dataclasses.replace(sc, frame=sc.frame[keep], landmark=sc.landmark[keep], pts=sc.pts[keep],
+                                  w=sc.w[keep])
+        dm2, st_o, osol2, rep2 = xo.solve(sc2)
+    assert st2 == 0 and info2["certified"] == 1 and st_o.certified
+    assert abs(info2["f"] - st_o.f) <= 1e-8 * (1.0 + abs(st_o.f))
+    assert x_rel_err(Yg, st_o.Y) <= 1e-6
+    assert np.max(np.abs(sol2["s"] - osol2.s)) <= 1e-6
+    assert np.max(np.abs(sol2["R"] - osol2.R)) <= 1e-6
+    assert np.all(np.isnan(res2[~keep])) and np.all(np.isfinite(res2[keep]))
+    assert cert2["eta"] <= 1e-6
