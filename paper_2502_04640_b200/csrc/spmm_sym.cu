@@ -162,7 +162,7 @@ struct SymPlan {
   int64_t ldq = 0;
   CUtensorMap tmq;
   DBuf<int> pbase;    // TCb + 1
-  DBuf<int> segbase;  // 2(G + 1): first segment of CTA c, then first tile of CTA c
+  DBuf<int> segbase;  // G + 1
   DBuf<int> colptr;   // TCb + 1: segments [colptr[J], colptr[J+1]) belong to panel J
 };
 
@@ -205,25 +205,9 @@ static SymPlan& sym_plan(xm_ctx* c) {
   std::vector<int> pb(p.TCb + 1, 0);
   for (int J = 0; J < p.TCb; ++J) pb[J + 1] = pb[J] + (p.TRt - kDiagTiles * J);
   p.W = pb[p.TCb];
-  // cost-balanced split (as the persistent tCG, tcg_persist.cu): a tile costs
-  // 1, a diagonal-block tile 1.1 (masks), the first tile of a panel 2.5 (a
-  // CTA crossing into a new panel flushes a column partial, loads V_J)
-  std::vector<double> cum(p.W + 1, 0.0);
-  for (int J = 0, tt = 0; J < p.TCb; ++J)
-    for (int x = 0; x < pb[J + 1] - pb[J]; ++x, ++tt)
-      cum[tt + 1] = cum[tt] + 1.0 + (x < kDiagTiles ? 0.1 : 0.0) + (x == 0 ? 1.5 : 0.0);
-  std::vector<int> tb(G + 1, 0);
-  for (int cta = 1; cta < G; ++cta) {
-    const double target = cum[p.W] * cta / G;
-    int tt = tb[cta - 1];
-    while (tt < p.W && cum[tt] < target) ++tt;
-    tb[cta] = tt;
-  }
-  tb[G] = (int)p.W;
-  std::vector<int> segbase(2 * (G + 1), 0), segpanel;  // [segment bases | tile bases]
-  for (int cta = 0; cta <= G; ++cta) segbase[G + 1 + cta] = tb[cta];
+  std::vector<int> segbase(G + 1, 0), segpanel;
   for (int cta = 0; cta < G; ++cta) {
-    const int64_t t0 = tb[cta], t1 = tb[cta + 1];
+    const int64_t t0 = (int64_t)cta * p.W / G, t1 = (int64_t)(cta + 1) * p.W / G;
     segbase[cta] = (int)segpanel.size();
     int J = 0;
     while (J + 1 < p.TCb && pb[J + 1] <= t0) ++J;
@@ -277,8 +261,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
   uint64_t* empty = bars + kStages;
 
   const int G = gridDim.x;
-  const int64_t t0 = segbase[G + 1 + blockIdx.x];  // cost-balanced tile range (sym_plan)
-  const int64_t t1 = segbase[G + 1 + blockIdx.x + 1];
+  const int64_t t0 = (int64_t)blockIdx.x * W / G;
+  const int64_t t1 = (int64_t)(blockIdx.x + 1) * W / G;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
