@@ -58,7 +58,7 @@ def test_edge_residuals_kernel_matches_formula(xm):
     assert abs(res[:-1].sum() - eq3) <= 1e-10 * (1 + eq3)
 
 
-@pytest.mark.parametrize("case", ["outliers", "restoration"])
+@pytest.mark.parametrize("case", ["outliers", "medium", "restoration"])
 def test_xm2_parity(xm, case):
     """Same measurements dropped as the oracle: the masks agree except inside
     groups of equal residuals (e.g. the two measurements of a two-view
@@ -71,6 +71,10 @@ def test_xm2_parity(xm, case):
         sc0 = make_scene(12, 400, "unordered", seed=4, vis_prob=0.5, sigma_u=1e-3, sigma_d=0.01)
         sc, bad = corrupt(sc0, 0.04, seed=4)
         frac = 0.1
+    elif case == "medium":  # > 148 frames: every kernel spans all CTAs, ragged tails
+        sc0 = make_scene(150, 3000, "unordered", seed=11, track_mean=8.0, sigma_u=1e-3, sigma_d=0.01)
+        sc, bad = corrupt(sc0, 0.03, seed=11)
+        frac = 0.1
     else:  # sparse road scene where dropping half the measurements splits the graph
         sc = make_scene(12, 60, "road", seed=3, sigma_u=1e-3, sigma_d=0.01, track_mean=3.0)
         frac = 0.5
@@ -81,19 +85,24 @@ def test_xm2_parity(xm, case):
         keep, n_drop, n_rest = ctx.xm2(frac)
         nd = math.floor(frac * sc.E)
         assert n_drop + n_rest == nd and (~keep).sum() == n_drop
-        assert (n_rest > 0) == (case == "restoration")
+        assert n_rest == nd - (~okeep).sum()         # as many restored as the oracle
+        assert (n_rest > 0) == (case != "outliers")
         assert (~keep).sum() == (~okeep).sum()
         a, b = np.sort(ores[~keep]), np.sort(ores[~okeep])
         assert np.all(np.abs(a - b) <= 1e-9 * np.maximum(np.abs(b), 1e-12)), (a, b)
-        if case == "outliers":
+        if case != "restoration":
             assert np.array_equal(keep, okeep)       # no ties near the cut here
+            assert keep[bad].mean() < 0.2            # the outliers are among the dropped
         assert xo.connected_components(sc.N, sc.M, sc.frame[keep], sc.landmark[keep]) == 1
         # the rebuilt Q is the data matrix of exactly the kept measurements
         dmk = xo.build_Q(sc.N, sc.M, sc.frame[keep], sc.landmark[keep], sc.pts[keep], sc.w[keep])
         Qg = ctx.Q_rows(0, 3 * sc.N)
         assert np.linalg.norm(Qg - dmk.Q) <= 1e-10 * dmk.normF
-        if case == "restoration":
-            return  # half the measurements gone: the second SDP optimum collapses scales (C18)
+        if case != "outliers":
+            # a frame whose every measurement ranked in the dropped set comes
+            # back with the single restored one: underdetermined, the second
+            # optimum collapses its scale (C18) — selection and rebuild only
+            return
         st2, info2 = ctx.solve(r0=3)
         cert2 = ctx.certify()
         sol2 = ctx.round_recover()
