@@ -115,3 +115,40 @@ def test_more_ranks_than_frames(xm):
 
     for QV in run_ranks(xm, 4, "tiny-4", fn):
         assert np.linalg.norm(QV - dm.Q @ V) <= 1e-12 * max(1.0, np.linalg.norm(dm.Q @ V))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_xm2_sharded(xm, world):
+    """XM² on the sharded path: every rank ranks the same
+    replicated solution's residuals and keeps the same measurements as the
+    oracle; each rank rebuilds its own rows of Q from them (gathered Q = the
+    oracle's Q of the kept set) and the second solve matches the oracle's."""
+    from synth.scenes import corrupt
+    sc0 = make_scene(12, 400, "unordered", seed=4, vis_prob=0.5, sigma_u=1e-3, sigma_d=0.01)
+    sc, bad = corrupt(sc0, 0.04, seed=4)
+    first, okeep, ores, second = xo.xm2(sc)
+    dm2, st_o, osol2, rep2 = second
+
+    def fn(ctx, q):
+        ctx.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+        ctx.solve(r0=3)
+        ctx.round_recover()
+        res = ctx.edge_residuals()
+        keep, nd, nr = ctx.xm2(0.1)
+        lo, hi, _ = xm.shard_rows(sc.N, world, q)
+        Qrows = ctx.Q_rows(3 * lo, 3 * (hi - lo)) if hi > lo else np.zeros((0, 3 * sc.N))
+        st2, info2 = ctx.solve(r0=3)
+        sol2 = ctx.round_recover()
+        return res, keep, Qrows, info2, sol2, ctx.get_factor()
+
+    out = run_ranks(xm, world, f"xm2-{world}", fn)
+    for q in range(world):
+        res, keep, Qrows, info2, sol2, Y = out[q]
+        assert np.array_equal(keep, okeep)
+        assert np.array_equal(res, out[0][0])                    # replicated, bitwise
+        assert np.array_equal(sol2["s"], out[0][4]["s"])
+        assert info2["certified"] == 1
+        assert abs(info2["f"] - st_o.f) <= 1e-8 * (1.0 + abs(st_o.f))
+        assert np.max(np.abs(sol2["R"] - osol2.R)) <= 1e-6
+    Qg = np.concatenate([o[2] for o in out], axis=0)
+    assert np.linalg.norm(Qg - dm2.Q) <= 1e-10 * dm2.normF
