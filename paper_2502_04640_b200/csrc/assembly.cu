@@ -866,6 +866,7 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
     c->G.alloc(1);
     c->L.alloc(1);
   }
+  phase("zero S,C,K");
   k_clique_scatter<<<N, 128, 0, c->stream>>>(N, c->f0, c->f1, c->fr_off.p, c->fr_edge.p,
                                              c->lm_off.p, c->e_fr.p, c->e_pts.p, c->e_w.p, c->W.p,
                                              c->e_lm.p, c->Q.p, c->ldq, c->row0, c->G.p, c->L.p,
