@@ -227,3 +227,20 @@ def test_repeated_solves_reuse_graphs_across_rank_climb(xm, kernel, path, monkey
     for status, info, Y in runs:
         assert status == 0 and info["r"] == 4 and info["escapes"] == 1
         assert info["f"] == runs[0][1]["f"] and np.array_equal(Y, runs[0][2])
+
+
+@pytest.mark.parametrize("path", ["persist", "persist_sym"])
+@pytest.mark.parametrize("r0", [4, 5])
+def test_higher_rank_start_parity(xm, path, r0, monkeypatch):
+    """Random initial factor at r = 4, 5 (Thm 3: any rank ≥ the optimum's
+    certifies): the persistent tCG kernels at R = 4, 5 over > 148 frames
+    (every CTA busy, ragged camera split) reach the oracle's X and f."""
+    for k, v in TCG_PATHS[path].items():
+        monkeypatch.setenv(k, v)
+    sc = make_scene(160, 3000, "unordered", seed=5, track_mean=8.0, sigma_u=1e-3, sigma_d=0.02)
+    Y0 = random_factor(sc.N, r0, 2)
+    dm, st, sol, rep, status, info, cert, gsol, Yg = _e2e(xm, sc, Y0=Y0)
+    assert st.certified and status == 0 and info["certified"] == 1 and info["r"] == r0
+    assert abs(info["f"] - st.f) <= 1e-8 * (1.0 + abs(st.f))
+    assert x_rel_err(Yg, st.Y) <= 1e-6
+    assert np.max(np.abs(gsol["s"] - sol.s)) <= 1e-6
