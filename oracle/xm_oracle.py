@@ -456,11 +456,14 @@ def retract(Y, V, c_floor=1e-3):
 # O5  truncated CG (Steihaug–Toint)   (C8)
 # =============================================================================
 
-def tcg(hvp, Y, g, Delta, kappa=0.1, theta=1.0, max_inner=500):
+def tcg(hvp, Y, g, Delta, kappa=0.1, theta=1.0, max_inner=500, trace=None):
     """Steihaug–Toint tCG in Manopt's form (no preconditioner).
 
     Returns (eta, Heta, n_hvp, stop) with stop ∈ {'negcurv', 'exceeded',
-    'converged', 'maxinner'}."""
+    'converged', 'maxinner'}.  If `trace` is a list, the state after every
+    completed inner iteration (η, δ, and the scalar recurrences e_Pe = ⟨η,η⟩,
+    e_Pd = ⟨η,δ⟩, d_Pd = ⟨δ,δ⟩ that the boundary test uses) is appended to it —
+    test instrumentation only, no effect on the arithmetic."""
     eta = np.zeros_like(g)
     Heta = np.zeros_like(g)
     r = g.copy()
@@ -497,6 +500,8 @@ def tcg(hvp, Y, g, Delta, kappa=0.1, theta=1.0, max_inner=500):
         delta = -r + beta * delta
         e_Pd = beta * (e_Pd + alpha * d_Pd)
         d_Pd = z + beta * beta * d_Pd
+        if trace is not None:
+            trace.append(dict(eta=eta.copy(), delta=delta.copy(), e_Pe=e_Pe, e_Pd=e_Pd, d_Pd=d_Pd))
     return eta, Heta, n_hvp, stop
 
 

@@ -625,3 +625,114 @@ def test_xm2_removes_outliers():
     e1 = np.max(_rot_err(first[2].R, sc.R))
     e2 = np.max(_rot_err(second[2].R, sc.R))
     assert e2 < 0.5 * e1
+
+
+# ----------------------------------------------------------------------------- tCG (O5)
+# Steihaug–Toint truncated CG ("Riemannian trust-region with truncated
+# conjugate gradient").  Pins independent of the
+# oracle's recurrences: (i) with an unbounded radius and a tiny tolerance the
+# returned η solves the projected Newton system H η = −g on the tangent space,
+# compared with a dense solve in an explicit orthonormal tangent basis;
+# (ii) the scalar recurrences e_Pe, e_Pd, d_Pd equal ⟨η,η⟩, ⟨η,δ⟩, ⟨δ,δ⟩
+# recomputed directly; (iii) a boundary / negative-curvature stop puts η on
+# the sphere ‖η‖ = Δ; (iv) Hη equals the operator applied to η (linearity).
+
+def _tangent_basis(Y):
+    """Orthonormal basis of the tangent space at Y: eigenvectors of the
+    (dense) projector matrix with eigenvalue 1."""
+    nr = Y.size
+    P = np.empty((nr, nr))
+    for j in range(nr):
+        e = np.zeros(nr)
+        e[j] = 1.0
+        P[:, j] = xo.project(Y, e.reshape(Y.shape)).ravel()
+    P = 0.5 * (P + P.T)
+    w, U = np.linalg.eigh(P)
+    return U[:, w > 0.5]
+
+
+def _spd_tangent_operator(Y, seed, cond=50.0, shift=0.0):
+    """V ↦ P(A P(V)) for a random symmetric A with spectrum in [1, cond] − shift."""
+    rng = np.random.default_rng(seed)
+    nr = Y.size
+    Qm, _ = np.linalg.qr(rng.standard_normal((nr, nr)))
+    A = (Qm * (np.geomspace(1.0, cond, nr) - shift)) @ Qm.T
+    A = 0.5 * (A + A.T)
+
+    def hvp(V):
+        return xo.project(Y, (A @ xo.project(Y, V).ravel()).reshape(Y.shape))
+    return hvp, A
+
+
+@pytest.mark.parametrize("r", [3, 4])
+def test_tcg_unbounded_solves_projected_newton_system(r):
+    """Δ = ∞, κ → 0: η = −(TᵀAT)⁻¹Tᵀg expressed in the tangent basis T."""
+    Y = random_factor(7, r, 21)
+    g = xo.project(Y, random_tangent_ambient(7, r, 22))
+    hvp, A = _spd_tangent_operator(Y, 5)
+    T = _tangent_basis(Y)
+    eta_star = -(T @ np.linalg.solve(T.T @ A @ T, T.T @ g.ravel())).reshape(Y.shape)
+    eta, Heta, nh, stop = xo.tcg(hvp, Y, g, 1e12, kappa=1e-13, theta=1.0, max_inner=10 * Y.size)
+    assert stop == "converged"
+    assert np.linalg.norm(eta - eta_star) <= 1e-9 * np.linalg.norm(eta_star)
+    np.testing.assert_allclose(Heta, hvp(eta), atol=1e-9 * np.linalg.norm(Heta))
+    # the Newton residual itself (no reference to the recurrences)
+    assert np.linalg.norm(hvp(eta) + g) <= 1e-10 * np.linalg.norm(g)
+
+
+def test_tcg_recurrences_equal_direct_inner_products(small_problem):
+    """e_Pe = ⟨η,η⟩, e_Pd = ⟨η,δ⟩, d_Pd = ⟨δ,δ⟩ along the iteration (the boundary
+    test ‖η + αδ‖² ≥ Δ² relies on them; Manopt's tCG form)."""
+    sc, dm = small_problem
+    Y = random_factor(sc.N, 3, 31)
+    cases = []
+    hvp, _ = _spd_tangent_operator(Y, 6, cond=30.0)
+    cases.append((hvp, xo.project(Y, random_tangent_ambient(sc.N, 3, 32))))
+    QY = dm.Q @ Y
+    g, Lam = xo.rgrad(Y, QY)
+    cases.append((lambda V: xo.hess(dm.Q, Y, Lam, V), g))
+    for hvp, gg in cases:
+        tr = []
+        xo.tcg(hvp, Y, gg, 1e12, kappa=1e-10, max_inner=40, trace=tr)
+        assert len(tr) >= 3
+        g0 = np.linalg.norm(gg)
+        for st in tr:
+            # absolute scale: ‖η‖·‖δ₀‖ (δ₀ = −g); late δ are at roundoff level
+            e, d = st["eta"], st["delta"]
+            sc_ = np.linalg.norm(e) * g0
+            assert abs(st["e_Pe"] - np.vdot(e, e)) <= 1e-8 * np.vdot(e, e)
+            assert abs(st["e_Pd"] - np.vdot(e, d)) <= 1e-8 * sc_
+            assert abs(st["d_Pd"] - np.vdot(d, d)) <= 1e-8 * max(np.vdot(d, d), 1e-6 * g0 * g0)
+
+
+@pytest.mark.parametrize("kind", ["exceeded", "negcurv"])
+def test_tcg_truncated_step_lands_on_the_trust_region_boundary(kind):
+    """A boundary or negative-curvature stop returns η with ‖η‖ = Δ exactly
+    (the positive root τ of ‖η + τδ‖ = Δ)."""
+    Y = random_factor(9, 4, 41)
+    g = xo.project(Y, random_tangent_ambient(9, 4, 42))
+    if kind == "exceeded":
+        hvp, A = _spd_tangent_operator(Y, 7, cond=200.0)
+        T = _tangent_basis(Y)
+        full = np.linalg.norm(T @ np.linalg.solve(T.T @ A @ T, T.T @ g.ravel()))
+        Delta = 0.6 * full                         # inside the unbounded solution's norm
+    else:
+        hvp, A = _spd_tangent_operator(Y, 8, cond=10.0, shift=5.0)   # indefinite
+        Delta = 1e6
+    eta, Heta, nh, stop = xo.tcg(hvp, Y, g, Delta, kappa=1e-12, max_inner=500)
+    assert stop == kind
+    assert abs(np.linalg.norm(eta) - Delta) <= 1e-12 * Delta
+    np.testing.assert_allclose(Heta, hvp(eta), atol=1e-9 * np.linalg.norm(Heta))
+    if kind == "exceeded":
+        assert nh >= 2                              # crossed after some CG steps
+    # the model decreases along the returned step (Steihaug: m(η) < m(0))
+    assert np.vdot(g, eta) + 0.5 * np.vdot(eta, hvp(eta)) < 0.0
+
+
+def test_tcg_negative_curvature_first_step_is_steepest_descent_to_boundary():
+    """H = −I on the tangent space: the first curvature is negative, so η = −Δ g/‖g‖."""
+    Y = random_factor(5, 3, 51)
+    g = xo.project(Y, random_tangent_ambient(5, 3, 52))
+    eta, Heta, nh, stop = xo.tcg(lambda V: -V, Y, g, 0.37)
+    assert stop == "negcurv" and nh == 1
+    np.testing.assert_allclose(eta, -0.37 * g / np.linalg.norm(g), rtol=0, atol=1e-14)
