@@ -247,135 +247,7 @@ __global__ void __launch_bounds__(128) k_clique_scatter(
 }
 
 // ============================================================ dense fp64 kernels
-// GEMM:  C = beta·C + alpha·op(A)·op(B), op(A) M×K, op(B) K×N, row-major storage.
-//   TA: A stored K×M (op = transpose); TB: B stored N×K.
-//   LOWER: only tiles with tile_col ≤ tile_row (BM == BN) are computed.
-// 64×64 tile, BK = 16, 256 threads, each thread a 4×4 strided micro-tile
-// (rows ty + 16·a, cols tx + 16·b ⇒ conflict-free smem reads with broadcast).
-constexpr int GB = 64, GK = 16;
-
-template <bool TA, bool TB, bool LOWER>
-__global__ void __launch_bounds__(256) k_dgemm(int M, int N, int K, double alpha,
-                                               const double* __restrict__ A, int64_t lda,
-                                               const double* __restrict__ B, int64_t ldb,
-                                               double beta, double* __restrict__ C, int64_t ldc) {
-  const int bm = blockIdx.y, bn = blockIdx.x;
-  if (LOWER && bn > bm) return;
-  __shared__ double As[2][GK][GB + 2];
-  __shared__ double Bs[2][GK][GB + 2];
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const int m0 = bm * GB, n0 = bn * GB;
-  double acc[4][4] = {};
-  double ra[4], rb[4];
-  auto load_a = [&](int k0) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      int lin = tid + q * 256;  // 0..1023 over 64×16
-      int mm, kk;
-      if (TA) { mm = lin & 63; kk = lin >> 6; }   // A[k][m]: contiguous in m
-      else    { kk = lin & 15; mm = lin >> 4; }   // A[m][k]: contiguous in k
-      int gm = m0 + mm, gk = k0 + kk;
-      double v = 0.0;
-      if (gm < M && gk < K) v = TA ? A[(int64_t)gk * lda + gm] : A[(int64_t)gm * lda + gk];
-      ra[q] = v;
-    }
-  };
-  auto load_b = [&](int k0) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      int lin = tid + q * 256;
-      int nn, kk;
-      if (!TB) { nn = lin & 63; kk = lin >> 6; }  // B[k][n]: contiguous in n
-      else     { kk = lin & 15; nn = lin >> 4; }  // B[n][k]: contiguous in k
-      int gn = n0 + nn, gk = k0 + kk;
-      double v = 0.0;
-      if (gn < N && gk < K) v = TB ? B[(int64_t)gn * ldb + gk] : B[(int64_t)gk * ldb + gn];
-      rb[q] = v;
-    }
-  };
-  auto store = [&](int buf) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      int lin = tid + q * 256;
-      int mm, kk;
-      if (TA) { mm = lin & 63; kk = lin >> 6; } else { kk = lin & 15; mm = lin >> 4; }
-      As[buf][kk][mm] = ra[q];
-      int nn, k2;
-      if (!TB) { nn = lin & 63; k2 = lin >> 6; } else { k2 = lin & 15; nn = lin >> 4; }
-      Bs[buf][k2][nn] = rb[q];
-    }
-  };
-  int nk = (K + GK - 1) / GK;
-  if (nk > 0) {
-    load_a(0);
-    load_b(0);
-    store(0);
-  }
-  __syncthreads();
-  for (int t = 0; t < nk; ++t) {
-    int cur = t & 1;
-    if (t + 1 < nk) {
-      load_a((t + 1) * GK);
-      load_b((t + 1) * GK);
-    }
-#pragma unroll
-    for (int kk = 0; kk < GK; ++kk) {
-      double a[4], b[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) a[q] = As[cur][kk][ty + 16 * q];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) b[q] = Bs[cur][kk][tx + 16 * q];
-#pragma unroll
-      for (int x = 0; x < 4; ++x)
-#pragma unroll
-        for (int y = 0; y < 4; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
-    }
-    if (t + 1 < nk) store(cur ^ 1);
-    __syncthreads();
-  }
-#pragma unroll
-  for (int x = 0; x < 4; ++x) {
-    int gm = m0 + ty + 16 * x;
-    if (gm >= M) continue;
-#pragma unroll
-    for (int y = 0; y < 4; ++y) {
-      int gn = n0 + tx + 16 * y;
-      if (gn >= N) continue;
-      double* cp = C + (int64_t)gm * ldc + gn;
-      *cp = (beta == 0.0 ? 0.0 : beta * *cp) + alpha * acc[x][y];
-    }
-  }
-}
-
-void dgemm(xm_ctx* c, bool ta, bool tb, bool lower, int M, int N, int K, double alpha,
-           const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
-           int64_t ldc) {
-  if (M <= 0 || N <= 0) return;
-  if (c->use_blas) {
-    if (!lower) {
-      if (blas_dgemm(c, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc)) return;
-    } else if (A == B && lda == ldb && M == N && ta != tb) {
-      // SYRK: op(A)·op(B) = X·Xᵀ (tb) or Xᵀ·X (ta) with X = A
-      if (blas_dsyrk_lower(c, ta, M, K, alpha, A, lda, beta, C, ldc)) return;
-    }
-  }
-  dim3 grid(ceil_div(N, GB), ceil_div(M, GB));
-#define XM_GEMM_CASE(a_, b_, l_)                                                            \
-  if (ta == a_ && tb == b_ && lower == l_) {                                                \
-    k_dgemm<a_, b_, l_><<<grid, 256, 0, c->stream>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, \
-                                                     ldc);                                   \
-    XM_CHECK_LAUNCH();                                                                       \
-    count_launch(c);                                                                         \
-    return;                                                                                  \
-  }
-  XM_GEMM_CASE(false, false, false)
-  XM_GEMM_CASE(true, false, false)
-  XM_GEMM_CASE(true, false, true)
-  XM_GEMM_CASE(false, true, false)
-  XM_GEMM_CASE(false, true, true)
-#undef XM_GEMM_CASE
-  throw Error(XM_EINVAL, "dgemm variant not instantiated");
-}
+// The O(N³) updates are the DMMA kernel of dgemm_tn.cu (TN shape, see there).
 
 // ---------------------------------------------------------------- Cholesky
 constexpr int NB = 64;
@@ -414,7 +286,8 @@ __global__ void __launch_bounds__(256) k_chol_panel(double* __restrict__ Akk, in
                                                     int rows, double rel_tol,
                                                     const double* __restrict__ scale,
                                                     int* __restrict__ err,
-                                                    double* __restrict__ L11_out) {
+                                                    double* __restrict__ L11_out,
+                                                    double* __restrict__ Ut, int64_t ldu) {
   static_assert(NBT == 64, "16 x 16 threads x 4 x 4");
   __shared__ double a[NBT][NBT + 1];
   const double pivot_tol = rel_tol * (*scale);
@@ -467,6 +340,9 @@ __global__ void __launch_bounds__(256) k_chol_panel(double* __restrict__ Akk, in
   __syncthreads();
   if (blockIdx.x == 0)  // into a side slot: other CTAs may still be reading Akk
     for (int t = tid; t < NBT * NBT; t += 256) L11_out[t] = a[t >> 6][t & 63];
+  __shared__ double rdiag[NBT];  // 1/L_jj: the row solve multiplies (no fp64 division chain)
+  if (tid < NBT) rdiag[tid] = 1.0 / a[tid][tid];
+  __syncthreads();
   // panel rows: X·L11ᵀ = A21
   const int r = blockIdx.x * 256 + tid;
   if (r >= rows) return;
@@ -480,12 +356,15 @@ __global__ void __launch_bounds__(256) k_chol_panel(double* __restrict__ Akk, in
       double s2 = x[j];
 #pragma unroll
       for (int q = 0; q < j; ++q) s2 = fma(-x[q], a[j][q], s2);
-      x[j] = s2 / a[j][j];
+      x[j] = s2 * rdiag[j];
     }
   }
 #pragma unroll
   for (int j = 0; j < NBT; ++j)
-    if (j < nb) row[j] = x[j];
+    if (j < nb) {
+      row[j] = x[j];
+      Ut[(int64_t)j * ldu + r] = x[j];  // the same panel transposed (U = Lᵀ rows), coalesced in r
+    }
 }
 
 // L11 slots → diagonal blocks (strict upper part of each block zeroed)
@@ -499,7 +378,13 @@ __global__ void k_chol_diag_back(const double* __restrict__ slots, double* __res
   }
 }
 
-bool dense_cholesky(xm_ctx* c, double* A, int m, int64_t lda, double rel_tol, bool throw_on_fail) {
+// Blocked right-looking Cholesky A = LLᵀ (lower, row-major, in place).  Each
+// panel step also writes the panel transposed — the rows kb..kb+nb of U = Lᵀ
+// right of the diagonal block — into U (if given; else into a one-panel
+// scratch), so the trailing update A₂₂ −= L₂₁L₂₁ᵀ is the TN DMMA kernel on
+// lower tiles, and a later TRSM can use U as its TN operand too.
+bool dense_cholesky(xm_ctx* c, double* A, int m, int64_t lda, double rel_tol, bool throw_on_fail,
+                    double* U, int64_t ldu) {
   if (m <= 0) return true;
   c->flags.alloc(16);
   c->scal.alloc(64);
@@ -510,18 +395,25 @@ bool dense_cholesky(xm_ctx* c, double* A, int m, int64_t lda, double rel_tol, bo
   count_launch(c);
   DBuf<double>& slots = scratch_f64(c, "chol_l11");
   slots.alloc((size_t)ceil_div(m, NB) * NB * NB);
+  DBuf<double>& panel = scratch_f64(c, "chol_panel");
+  if (!U) {
+    ldu = round_up(std::max(m, 1), 32);
+    panel.alloc((size_t)NB * ldu);
+  }
   for (int kb = 0; kb < m; kb += NB) {
     int nb = std::min(NB, m - kb);
     double* Akk = A + (int64_t)kb * lda + kb;
     int rows = m - kb - nb;
+    // U panel: rows kb.., columns kb+nb.. (scratch: rows 0.., columns 0..)
+    double* Up = U ? U + (int64_t)kb * ldu + (kb + nb) : panel.p;
     k_chol_panel<NB><<<std::max(1, ceil_div(rows, 256)), 256, 0, c->stream>>>(
-        Akk, lda, nb, rows, rel_tol, d_scale, c->flags.p, slots.p + (size_t)(kb / NB) * NB * NB);
+        Akk, lda, nb, rows, rel_tol, d_scale, c->flags.p, slots.p + (size_t)(kb / NB) * NB * NB,
+        Up, ldu);
     XM_CHECK_LAUNCH();
     count_launch(c);
     if (rows > 0) {
-      double* A21 = A + (int64_t)(kb + nb) * lda + kb;
       double* A22 = A + (int64_t)(kb + nb) * lda + (kb + nb);
-      dgemm(c, false, true, true, rows, rows, nb, -1.0, A21, lda, A21, lda, 1.0, A22, lda);
+      dgemm_tn(c, true, rows, rows, nb, -1.0, Up, ldu, Up, ldu, 1.0, A22, lda);
     }
   }
   k_chol_diag_back<<<ceil_div(m, NB), 256, 0, c->stream>>>(slots.p, A, lda, m);
@@ -602,21 +494,77 @@ __global__ void __launch_bounds__(128) k_trsm_block_cols(const double* __restric
     if (j < nb) B[(int64_t)j * ldb + col] = x[j];
 }
 
-void dense_trsm_lower_left(xm_ctx* c, const double* L, int m, int64_t ldl, double* B, int ncols,
-                           int64_t ldb) {
-  for (int kb = 0; kb < m; kb += NB) {
-    int nb = std::min(NB, m - kb);
+__global__ void k_eye(double* T, int m, int64_t ld) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m * m) return;
+  const int i = t / m, j = t % m;
+  T[(int64_t)i * ld + j] = (i == j) ? 1.0 : 0.0;
+}
+
+__global__ void k_transpose(const double* __restrict__ S, int64_t lds, double* __restrict__ D,
+                            int64_t ldd, int rows, int cols) {
+  __shared__ double tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int r = by + y, cc = bx + threadIdx.x;
+    tile[y][threadIdx.x] = (r < rows && cc < cols) ? S[(int64_t)r * lds + cc] : 0.0;
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int r = bx + y, cc = by + threadIdx.x;  // D[cc_src][r_src]
+    if (r < cols && cc < rows) D[(int64_t)r * ldd + cc] = tile[threadIdx.x][y];
+  }
+}
+
+// Rows [k0, k1) of B ← L⁻¹ B restricted to the diagonal block L[k0:k1, k0:k1]
+// (64-row diagonal solves with their short TN updates inside the block).
+static void trsm_block_inner(xm_ctx* c, const double* L, int64_t ldl, const double* U, int64_t ldu,
+                             int k0, int k1, double* B, int ncols, int64_t ldb) {
+  for (int kb = k0; kb < k1; kb += NB) {
+    int nb = std::min(NB, k1 - kb);
     const double* Lkk = L + (int64_t)kb * ldl + kb;
-    double* Bk = B + (int64_t)kb * ldb;
+    double* Bk = B + (int64_t)(kb - k0) * ldb;
     k_trsm_block_cols<NB><<<ceil_div(ncols, 128), 128, 0, c->stream>>>(Lkk, ldl, Bk, ldb, nb, ncols);
     XM_CHECK_LAUNCH();
     count_launch(c);
-    int rows = m - kb - nb;
-    if (rows > 0) {
-      const double* L21 = L + (int64_t)(kb + nb) * ldl + kb;
-      dgemm(c, false, false, false, rows, ncols, nb, -1.0, L21, ldl, Bk, ldb, 1.0,
-            B + (int64_t)(kb + nb) * ldb, ldb);
-    }
+    int rows = k1 - kb - nb;
+    if (rows > 0)
+      dgemm_tn(c, false, rows, ncols, nb, -1.0, U + (int64_t)kb * ldu + (kb + nb), ldu, Bk, ldb, 1.0,
+               B + (int64_t)(kb + nb - k0) * ldb, ldb);
+  }
+}
+
+// B ← L⁻¹B (L lower m×m).  Super-blocks of SB = 512 rows: the diagonal block's
+// inverse L_ss⁻¹ (SB × SB, from the 64-row solves on an identity) is applied
+// as ONE TN DMMA product (B_s ← L_ss⁻¹ B_s, via a scratch row block), then the
+// rows below get ONE TN DMMA update with K = SB (U = Lᵀ from the
+// factorisation is the A operand: L₂₁[i][k] = U[k][i]).  The serial 64-row
+// solves only ever touch SB columns.
+void dense_trsm_lower_left(xm_ctx* c, const double* L, int m, int64_t ldl, const double* U,
+                           int64_t ldu, double* B, int ncols, int64_t ldb) {
+  const int SB = c->trsm_sb;
+  DBuf<double>& T = scratch_f64(c, "trsm_inv");
+  DBuf<double>& Tt = scratch_f64(c, "trsm_invT");
+  DBuf<double>& X = scratch_f64(c, "trsm_rows");
+  T.alloc((size_t)SB * SB);
+  Tt.alloc((size_t)SB * SB);
+  X.alloc((size_t)SB * ldb);
+  for (int sb = 0; sb < m; sb += SB) {
+    const int se = std::min(m, sb + SB), s = se - sb;
+    k_eye<<<ceil_div(s * s, 256), 256, 0, c->stream>>>(T.p, s, SB);
+    XM_CHECK_LAUNCH();
+    trsm_block_inner(c, L, ldl, U, ldu, sb, se, T.p, s, SB);       // T = L_ss⁻¹
+    k_transpose<<<dim3(ceil_div(s, 32), ceil_div(s, 32)), dim3(32, 8), 0, c->stream>>>(T.p, SB, Tt.p,
+                                                                                       SB, s, s);
+    XM_CHECK_LAUNCH();
+    count_launch(c, 2);
+    // X = L_ss⁻¹ B_s :  X[i][j] = Σ_k Tt[k][i] B[sb + k][j]
+    dgemm_tn(c, false, s, ncols, s, 1.0, Tt.p, SB, B + (int64_t)sb * ldb, ldb, 0.0, X.p, ldb);
+    XM_CUDA(cudaMemcpyAsync(B + (int64_t)sb * ldb, X.p, (size_t)s * ldb * sizeof(double),
+                            cudaMemcpyDeviceToDevice, c->stream));
+    if (se < m)
+      dgemm_tn(c, false, m - se, ncols, s, -1.0, U + (int64_t)sb * ldu + se, ldu,
+               B + (int64_t)sb * ldb, ldb, 1.0, B + (int64_t)se * ldb, ldb);
   }
 }
 
@@ -878,17 +826,22 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
   // ---- H5: K̄ = LLᵀ, G = L⁻¹C̄, Q = S − GᵀG
   if (N > 1) {
     // pivot test relative to max diag(K̄); a disconnected graph gives a ~0 pivot
-    dense_cholesky(c, c->L.p, N - 1, c->ldk, 1e-12);
-    dense_trsm_lower_left(c, c->L.p, N - 1, c->ldk, c->G.p, n, c->ldq);
+    DBuf<double>& U = scratch_f64(c, "chol_U");
+    U.alloc((size_t)(N - 1) * c->ldk);
+    dense_cholesky(c, c->L.p, N - 1, c->ldk, 1e-12, true, U.p, c->ldk);
+    phase("cholesky");
+    dense_trsm_lower_left(c, c->L.p, N - 1, c->ldk, U.p, c->ldk, c->G.p, n, c->ldq);
+    phase("trsm");
     const double* Gown = c->G.p + c->row0;  // columns of this rank's rows
     bool lower = (c->world == 1);
-    dgemm(c, true, false, lower, c->nrows, n, N - 1, -1.0, Gown, c->ldq, c->G.p, c->ldq, 1.0,
-          c->Q.p, c->ldq);
+    // Q = S − GᵀG: Q[i][j] −= Σ_k G[k][i] G[k][j]
+    dgemm_tn(c, lower, c->nrows, n, N - 1, -1.0, Gown, c->ldq, c->G.p, c->ldq, 1.0, c->Q.p,
+             c->ldq);
     if (lower) mirror_lower(c, c->Q.p, n, c->ldq);
   } else if (c->world == 1) {
     mirror_lower(c, c->Q.p, n, c->ldq);
   }
-  phase("chol+trsm+syrk");
+  phase("syrk+mirror");
   c->have_recovery = true;
   // ‖Q‖_F (all-reduced over ranks)
   {

@@ -440,11 +440,7 @@ static void launch_r(xm_ctx* c, const double* V, const SpmmEpiArgs& ep) {
                 (size_t)kConsumerWarps * kTileRows * R * 8 + (size_t)rows_max * R * 8;
   if (smem > 227 * 1024) throw Error(XM_EINVAL, "SpMM shared memory plan exceeds 227 KB");
   auto kern = k_spmm<R, MODE>;
-  static size_t attr = 0;
-  if (smem > attr) {
-    XM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  ensure_smem_attr((const void*)kern, smem);
   if (MODE == EPI_TCG) {
     // grid barriers inside: cooperative launch guarantees the G CTAs are co-resident
     cudaLaunchConfig_t cfg{};

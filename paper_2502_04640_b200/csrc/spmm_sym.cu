@@ -550,18 +550,22 @@ static void launch_sym(xm_ctx* c, const double* V, const SpmmEpiArgs& ep) {
     XM_CUDA(cudaMemset(c->gbar.p, 0, 4 * sizeof(int)));
   }
   const size_t smem = SymCfg<R>::kSmem;
-  static bool attr = false;
-  if (!attr) {
-    XM_CUDA(cudaFuncSetAttribute(k_spmm_sym<R, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    int nb = 0;
-    XM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_spmm_sym<R, MODE>, kThreads, smem));
-    if (nb < 1) throw Error(XM_ECUDA, "symmetric SpMM does not fit on an SM");
-    attr = true;
-  }
-  k_spmm_sym<R, MODE><<<p.G, kThreads, smem, c->stream>>>(
-      p.tmq, c->N, c->n, p.TRt, p.TCb, p.W, p.pbase.p, p.segbase.p, p.colptr.p, V, rowpart, colpart,
-      reinterpret_cast<GridBar*>(c->gbar.p), ep);
+  ensure_smem_attr((const void*)k_spmm_sym<R, MODE>, smem);
+  // grid barrier inside: a cooperative launch guarantees (or cleanly refuses)
+  // the co-residency of the p.G CTAs
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(p.G);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  XM_CUDA(cudaLaunchKernelEx(&cfg, k_spmm_sym<R, MODE>, p.tmq, (int)c->N, (int)c->n, p.TRt, p.TCb,
+                             p.W, p.pbase.p, p.segbase.p, p.colptr.p, V, rowpart, colpart,
+                             reinterpret_cast<GridBar*>(c->gbar.p), ep));
   XM_CHECK_LAUNCH();
   count_launch(c, 1);
 }

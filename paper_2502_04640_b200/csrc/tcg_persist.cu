@@ -1071,12 +1071,7 @@ static void launch_persist(xm_ctx* c) {
   const CUtensorMap* tm = persist_tmap(c, G);
   const size_t smem = persist_smem<R>(c->n, G);
   if (smem > kSmemCap) throw Error(XM_EINVAL, "persistent tCG shared memory plan exceeds 227 KB");
-  static size_t attr = 0;
-  if (smem > attr) {
-    XM_CUDA(cudaFuncSetAttribute(k_tcg_persist<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    attr = smem;
-  }
+  ensure_smem_attr((const void*)k_tcg_persist<R>, smem);
   TcgPersistArgs a{};
   a.Q = c->Q.p;
   a.ldq = c->ldq;
@@ -1260,12 +1255,7 @@ static void launch_persist_sym(xm_ctx* c) {
   SymTcgPlan& p = sym_tcg_plan(c);
   const size_t smem = persist_sym_smem<R>(c->N, G);
   if (smem > kSmemCap) throw Error(XM_EINVAL, "symmetric persistent tCG smem plan exceeds 227 KB");
-  static size_t attr = 0;
-  if (smem > attr) {
-    XM_CUDA(cudaFuncSetAttribute(k_tcg_persist_sym<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    attr = smem;
-  }
+  ensure_smem_attr((const void*)k_tcg_persist_sym<R>, smem);
   SymTcgArgs sa{};
   TcgPersistArgs& a = sa.b;
   a.Q = c->Q.p;

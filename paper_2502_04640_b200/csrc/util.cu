@@ -5,6 +5,17 @@
 
 namespace xm {
 
+void ensure_smem_attr(const void* kern, size_t smem) {
+  thread_local std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  XM_CUDA(cudaGetDevice(&dev));
+  size_t& cur = done[{kern, dev}];
+  if (smem > cur) {
+    XM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cur = smem;
+  }
+}
+
 bool is_device_ptr(const void* p) {
   if (!p) return false;
   cudaPointerAttributes a;

@@ -514,7 +514,9 @@ xm_status xm_create(xm_ctx** out, int device, int rank, int world, const void* n
   if (std::getenv("XM_PHASES")) c->phases_on = true;
   if (std::getenv("XM_NO_FUSED_TCG")) c->fused_tcg = false;
   if (std::getenv("XM_NO_PERSIST_TCG")) c->persist_tcg = false;
-  if (std::getenv("XM_NO_CUBLAS")) c->use_blas = false;
+  if (const char* e = std::getenv("XM_GEMM_TILE"))
+    c->gemm_tile = std::string(e) == "bk16" ? 1 : std::string(e) == "mid" ? 2 : 0;
+  if (const char* e = std::getenv("XM_TRSM_SB")) c->trsm_sb = std::max(64, atoi(e) / 64 * 64);
   if (std::getenv("XM_SYM_TCG")) c->persist_sym = 1;
   if (std::getenv("XM_NO_SYM_TCG")) c->persist_sym = -1;
   if (std::getenv("XM_NO_GRAPHS")) c->use_graphs = false;
@@ -548,7 +550,6 @@ void xm_destroy(xm_ctx* c) {
   nccl_destroy(c);
   sym_plan_destroy(c);
   sym_tcg_plan_destroy(c);
-  blas_destroy(c);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }

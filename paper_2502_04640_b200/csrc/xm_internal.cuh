@@ -164,7 +164,6 @@ struct xm_ctx {
   void* nccl_comm = nullptr;
   void* loop = nullptr;
   std::string loop_key;
-  void* cublas = nullptr;  // cublasHandle_t (blas.cu), created on first use
   // lower-triangle SpMM work plan + tensor map (spmm_sym.cu)
   void* sym_plan = nullptr;
   xm::DBuf<double> gbuf;  // all-gather staging
@@ -197,8 +196,9 @@ struct xm_ctx {
   // XM_PHASES=1: host wall-clock breakdown of xm_solve (synchronises; diagnostics only)
   bool phases_on = false;
   bool fused_tcg = true;    // XM_NO_FUSED_TCG=1: three-kernel tCG iteration (A/B measurement)
-  bool persist_tcg = true;  // XM_NO_PERSIST_TCG=1: one launch per tCG iteration instead
-  bool use_blas = true;     // XM_NO_CUBLAS=1: the library's own k_dgemm for the dense updates
+  bool persist_tcg = true;
+  int gemm_tile = 0;        // XM_GEMM_TILE=bk16|mid: A/B variants of the DMMA tile for K > 64
+  int trsm_sb = 512;        // XM_TRSM_SB: TRSM super-block rows (multiple of 64)  // XM_NO_PERSIST_TCG=1: one launch per tCG iteration instead
   int persist_sym = 0;      // lower-triangle persistent tCG: 0 auto (N < 4000), 1 forced (XM_SYM_TCG), -1 off (XM_NO_SYM_TCG)
   void* persist_sym_plan = nullptr;
   xm::DBuf<double> dir2;    // δ ping-pong partner of dir (persistent tCG)
@@ -233,6 +233,12 @@ void copy_out(xm_ctx* c, void* dst, const void* src_dev, size_t bytes);
 void sync(xm_ctx* c);
 inline void count_launch(xm_ctx* c, int k = 1) { c->stats.kernel_launches += k; }
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize for `kern` on the CURRENT device
+// (the attribute is per device context).  Cached per (thread, device, kernel):
+// no process-wide flag, so independent contexts on other devices / threads
+// (loopback ranks) each set it for themselves.
+void ensure_smem_attr(const void* kern, size_t smem);
+
 // Persistent named scratch (see xm_ctx::s_*).
 inline DBuf<int32_t>& scratch_i32(xm_ctx* c, const std::string& k) { return c->s_i32[k]; }
 inline DBuf<uint32_t>& scratch_u32(xm_ctx* c, const std::string& k) { return c->s_u32[k]; }
@@ -254,13 +260,14 @@ constexpr int kDotBlocks = 296;  // 2 × 148 SMs; fixed ⇒ deterministic sums
 void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr, const int32_t* lm,
                     const double* pts, const double* w);
 bool dense_cholesky(xm_ctx* c, double* A, int m, int64_t lda, double rel_tol,
-                    bool throw_on_fail = true);
+                    bool throw_on_fail = true, double* U = nullptr, int64_t ldu = 0);
 bool psd_test_cholesky(xm_ctx* c, double eps);
-void dense_trsm_lower_left(xm_ctx* c, const double* L, int m, int64_t ldl, double* B, int ncols,
-                           int64_t ldb);
-void dgemm(xm_ctx* c, bool ta, bool tb, bool lower, int M, int N, int K, double alpha,
-           const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
-           int64_t ldc);
+void dense_trsm_lower_left(xm_ctx* c, const double* L, int m, int64_t ldl, const double* U,
+                           int64_t ldu, double* B, int ncols, int64_t ldb);
+// C = β·C + α·Σ_k A[k·lda + m]·B[k·ldb + n] on the fp64 tensor cores (dgemm_tn.cu);
+// lower ⇒ only the lower-triangle tiles (M == N)
+void dgemm_tn(xm_ctx* c, bool lower, int M, int N, int K, double alpha, const double* A,
+              int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc);
 void mirror_lower(xm_ctx* c, double* Q, int n, int64_t ldq);
 
 // ------------------------------------------------------------ SpMM (spmm.cu)
@@ -346,12 +353,6 @@ void nccl_allgather(xm_ctx* c, const double* send, double* recv, size_t count_pe
 void nccl_allreduce_sum(xm_ctx* c, double* buf, size_t count);
 void sym_plan_destroy(xm_ctx* c);
 void sym_tcg_plan_destroy(xm_ctx* c);
-// cuBLAS (blas.cu) for plain dense GEMM / SYRK; false ⇒ not available
-bool blas_dgemm(xm_ctx* c, bool ta, bool tb, int M, int N, int K, double alpha, const double* A,
-                int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc);
-bool blas_dsyrk_lower(xm_ctx* c, bool trans_x, int n, int k, double alpha, const double* X,
-                      int64_t ldx, double beta, double* C, int64_t ldc);
-void blas_destroy(xm_ctx* c);
 
 // Row sharding: rank q owns frames [q·nfpr, min(N, (q+1)·nfpr)),
 // nfpr = ⌈N/world⌉; vectors exchanged by the all-gather hold world·3·nfpr rows.
