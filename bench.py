@@ -31,7 +31,6 @@ sys.path.insert(0, ROOT)
 
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback ("of fallback")
-COUNTS_FILE = os.path.join(ROOT, "profiles", "workload_counts.json")
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "spmm_traffic.json")
 METRIC = "solve_to_certificate_s"
 
@@ -100,52 +99,131 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- oracle timing
-def load_counts(cfg):
+# The oracle (reference arm, cpu_baseline) is timed as it stands on this
+# host's cores.  Its full solve at config E takes ~10 min, so a bench run
+# times: the oracle's FULL Q build (once), plus bounded samples of its unit
+# operations (oracle HVPs at each rank the oracle's own trajectory visits,
+# oracle Lanczos steps), scaled by the counts of the oracle's OWN full
+# trajectory (profiles/r2_oracle_full_<cfg>.json, written by
+# tools/oracle_full.py, which also times the full solve and records how close
+# this model comes to it).  The value is labelled an estimate.  bench.py never
+# writes tracked files.
+
+def oracle_threads() -> int:
     try:
-        with open(COUNTS_FILE) as f:
-            return json.load(f).get(cfg)
+        from threadpoolctl import threadpool_info
+        return max([p.get("num_threads", 1) for p in threadpool_info()] + [1])
     except Exception:
-        return None
+        return os.cpu_count() or 1
 
 
-def oracle_sample(scene, hvps: int, lanczos_steps: int, spmms: int, n_hvp_sample=12,
-                  n_lz_sample=24):
-    """Time the oracle as it stands on this host on a bounded sample of the
-    workload: the full oracle Q build (validate + Schur complement) plus
-    n_hvp_sample oracle Hessian-vector products and n_lz_sample oracle Lanczos
-    steps at the workload's size, scaled to the solve's counts."""
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def oracle_counts(cfg):
+    path = os.path.join(ROOT, "profiles", f"r2_oracle_full_{cfg}.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d, os.path.relpath(path, ROOT)
+    except Exception:
+        return None, None
+
+
+def oracle_unit_times(dm, ranks, n_lanczos, n_hvp=4):
+    """Per-unit oracle times on the full-size Q: one oracle Riemannian HVP
+    (xo.hess: Q·V + projection) at a random feasible Y of rank r, for each r;
+    the O(n·r) work of one outer TR iteration (retraction + gradient); and the
+    oracle's Lanczos run of n_lanczos steps (its full re-orthogonalisation
+    makes step k cost a + b·k): timed in full when n_lanczos ≤ 64, else from
+    two timed runs of 16 and 64 steps, T(k) = a·k + b·k²/2 fitted and
+    evaluated at n_lanczos."""
     import numpy as np
     from oracle import xm_oracle as xo
+    from synth.scenes import random_factor, random_tangent_ambient
+    Q = np.asarray(dm.Q)
+    N = dm.N
+    t_hvp = {}
+    for r in ranks:
+        Y = random_factor(N, r, 1)
+        g, Lam = xo.rgrad(Y, Q @ Y)
+        V = xo.project(Y, random_tangent_ambient(N, r, 2))
+        t0 = time.perf_counter()
+        for _ in range(n_hvp):
+            xo.hess(Q, Y, Lam, V)
+        t_hvp[r] = (time.perf_counter() - t0) / n_hvp
+    Y = random_factor(N, 3, 1)
+    QY = Q @ Y
+    _, Lam = xo.rgrad(Y, QY)
+    V = 1e-3 * xo.project(Y, random_tangent_ambient(N, 3, 3))
     t0 = time.perf_counter()
-    dm = xo.build_Q(scene.N, scene.M, scene.frame, scene.landmark, scene.pts, scene.w)
-    t_build = time.perf_counter() - t0
-    n = dm.n
-    Y = np.zeros((n, 3))
-    for i in range(scene.N):
-        Y[3 * i:3 * i + 3, :] = np.eye(3)
-    g, Lam = xo.rgrad(Y, dm.Q @ Y)
-    t0 = time.perf_counter()
-    for _ in range(n_hvp_sample):
-        xo.hess(dm.Q, Y, Lam, g)
-    t_hvp = (time.perf_counter() - t0) / n_hvp_sample
+    for _ in range(n_hvp):                   # the O(n·r) work of one outer TR iteration
+        xo.retract(Y, V)
+        xo.rgrad(Y, QY)
+    t_outer = (time.perf_counter() - t0) / n_hvp
 
     def apply_Z(x):
         X = x.reshape(-1, 1)
-        return (dm.Q @ X - xo.block_apply(Lam, X)).ravel()
-    t0 = time.perf_counter()
-    xo.lanczos_min_eig(apply_Z, n, 0.0, max_steps=n_lz_sample)
-    t_lz = (time.perf_counter() - t0) / n_lz_sample
-    est = t_build + t_hvp * max(spmms - lanczos_steps, hvps) + t_lz * lanczos_steps
-    try:
-        from threadpoolctl import threadpool_info
-        cores = max([p.get("num_threads", 1) for p in threadpool_info()] + [1])
-    except Exception:
-        cores = os.cpu_count() or 1
-    sample = (f"oracle build_Q on the full workload ({t_build:.2f}s) + {n_hvp_sample} oracle HVPs "
-              f"({t_hvp*1e3:.1f} ms each) + {n_lz_sample} oracle Lanczos steps ({t_lz*1e3:.1f} ms "
-              f"each), scaled to {max(spmms - lanczos_steps, hvps)} products + {lanczos_steps} "
-              f"Lanczos steps of the solve")
-    return est, cores, sample
+        return (Q @ X - xo.block_apply(Lam, X)).ravel()
+
+    def lz_time(k):
+        t0 = time.perf_counter()
+        xo.lanczos_min_eig(apply_Z, dm.n, 0.0, max_steps=k)
+        return time.perf_counter() - t0
+    if n_lanczos <= 64:
+        t_lz_total, how = (lz_time(n_lanczos) if n_lanczos > 0 else 0.0), f"{n_lanczos} steps timed"
+    else:
+        T1, T2 = lz_time(16), lz_time(64)
+        b = 2.0 * (T2 / 64 - T1 / 16) / (64 - 16)
+        a = T1 / 16 - b * 16 / 2
+        t_lz_total = a * n_lanczos + b * n_lanczos * n_lanczos / 2
+        how = f"16 and 64 steps timed ({T1:.2f} s, {T2:.2f} s), a·k + b·k²/2 at k = {n_lanczos}"
+    return {"t_hvp": t_hvp, "t_outer": t_outer, "t_lz_total": t_lz_total, "lz_how": how}
+
+
+class OracleEstimate:
+    """Oracle solve-to-certificate time on this host: the measured full Q
+    build + sampled unit times × the oracle trajectory's own counts."""
+
+    def __init__(self, scene, cfg):
+        self.sc, self.cfg = scene, cfg
+        self.full, self.src = oracle_counts(cfg)
+        self.dm = None
+        self.t_build = None
+
+    def available(self):
+        return self.full is not None
+
+    def step(self, n_hvp=4):
+        from oracle import xm_oracle as xo
+        sc = self.sc
+        if self.dm is None:
+            t0 = time.perf_counter()
+            self.dm = xo.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+            self.t_build = time.perf_counter() - t0
+        c = self.full["counts"]
+        by_r = {int(r): int(v) for r, v in c["products_by_r"].items() if int(r) > 1 and int(v) > 0}
+        u = oracle_unit_times(self.dm, sorted(by_r), c["lanczos_steps"], n_hvp)
+        est = (self.t_build + sum(by_r[r] * u["t_hvp"][r] for r in by_r)
+               + u["t_lz_total"] + c["outer"] * u["t_outer"])
+        sample = (f"oracle build_Q timed in full on this workload ({self.t_build:.1f} s, once) + "
+                  f"{n_hvp} oracle HVPs per rank {sorted(by_r)} ("
+                  + ", ".join(f"r={r}: {u['t_hvp'][r] * 1e3:.0f} ms" for r in sorted(by_r))
+                  + f") + the oracle's Lanczos ({u['lz_how']}; {u['t_lz_total']:.1f} s) + {n_hvp} "
+                  f"retraction+gradient passes ({u['t_outer'] * 1e3:.0f} ms each), scaled by the "
+                  f"oracle's own trajectory counts ({sum(by_r.values())} products, "
+                  f"{c['lanczos_steps']} Lanczos steps, {c['outer']} outer iterations; {self.src}, "
+                  f"whose full timed oracle run took "
+                  f"{self.full['measured_s']['total']:.0f} s with this model at "
+                  f"{self.full['model_over_measured']:.3f}x)")
+        return est, sample
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -155,16 +233,18 @@ def run_reference(args):
         return 0
     from synth.scenes import CONFIG_DESCRIPTIONS, config_scene
     sc = config_scene(args.config, seed=args.seed)
-    counts = load_counts(args.config) or {"hvps": 12000, "lanczos_steps": 1000, "spmms": 25000}
-    if counts.get("lanczos_steps_full"):
-        counts = dict(counts, lanczos_steps=counts["lanczos_steps_full"])
+    est = OracleEstimate(sc, args.config)
+    if not est.available():
+        print(json.dumps({"impl": "reference", "unavailable":
+                          f"no oracle trajectory counts for config {args.config} "
+                          f"(run tools/oracle_full.py {args.config})"}), flush=True)
+        return 0
     times = []
+    sample = ""
     for i in range(args.warmup + args.steps):
-        est, cores, sample = oracle_sample(sc, counts["hvps"], counts["lanczos_steps"],
-                                           counts["spmms"], n_hvp_sample=4 if i < args.warmup else 12,
-                                           n_lz_sample=8 if i < args.warmup else 24)
+        v, sample = est.step(n_hvp=2 if i < args.warmup else 4)
         if i >= args.warmup:
-            times.append(est)
+            times.append(v)
     v = sum(times) / len(times)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
@@ -172,9 +252,9 @@ def run_reference(args):
             "data": "synthetic",
             "config": {"workload": f"config {args.config}: {CONFIG_DESCRIPTIONS[args.config]}",
                        "N": sc.N, "M": sc.M, "E": sc.E, "seed": args.seed,
-                       "counts_source": "profiles/workload_counts.json (GPU solve of the same scene)"},
-            "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "oracle",
-                             "sample": sample},
+                       "counts_source": est.src + " (the oracle's own full trajectory)"},
+            "cpu_baseline": {"value": v, "unit": "s", "cores": oracle_threads(), "kind": "oracle",
+                             "estimate": True, "cpu": cpu_model(), "sample": sample},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -210,7 +290,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="B", choices=list("ABCDE"))
+    ap.add_argument("--config", default="E", choices=list("ABCDE"))
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--impl", default="xm", choices=["xm", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -288,7 +368,8 @@ def main():
     torch.cuda.synchronize()
     ctx.reset_stats()
     barrier()
-    for _ in range(args.steps):
+    aux_steps = min(args.steps, 5)          # roofline / e2e passes: at most 5 steps each
+    for _ in range(aux_steps):
         step(dev_in, out_dev)
     torch.cuda.synchronize()
     barrier()
@@ -304,12 +385,12 @@ def main():
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        for _ in range(args.steps):
+        for _ in range(aux_steps):
             step(h_in, out_host)
         torch.cuda.synchronize()
         barrier()
-        e2e_s = max_over_ranks(dist, (time.perf_counter() - t0) / args.steps, dev)
-        e2e = {"value": e2e_s, "unit": "s",
+        e2e_s = max_over_ranks(dist, (time.perf_counter() - t0) / aux_steps, dev)
+        e2e = {"value": e2e_s, "unit": "s", "steps": aux_steps,
                "h2d_bytes_per_step": int(sum(a.numel() * a.element_size() for a in h_in)),
                "d2h_bytes_per_step": int(sum(v.numel() * 8 for v in out_host.values()))}
 
@@ -325,7 +406,7 @@ def main():
             traffic = json.load(f).get(args.config, {}).get("dram_bytes_per_launch")
     except Exception:
         pass
-    spmm_share = pstats["spmm_ms"] / (ms * args.steps) if ms > 0 else None
+    spmm_share = pstats["spmm_ms"] / (ms * aux_steps) if ms > 0 else None
     result = {
         "metric": METRIC, "value": value, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
@@ -338,9 +419,10 @@ def main():
                   "outer_iters": info["outer_iters"], "r": info["r"], "escapes": info["escapes"],
                   "certified": info["certified"], "f": info["f"], "s_min": info["s_min"],
                   "lambda_min": cert["lambda_min"], "lambda_min_rel": cert["lambda_min"] / max(1.0, cert["normQ"]),
-                  "lambda_lower": cert["lambda_lower"],
-                  "cert_method": ["lanczos", "cholesky(Z+eps*I)"][cert["method"]],
-                  "eta": cert["eta"], "rho_hat": cert["rho_hat"], "status": st},
+                  "lambda_lower": cert["lambda_lower"], "lower_rigorous": cert["lower_rigorous"],
+                  "cert_method": ["lanczos(Z)", "cholesky(Z+eps*I) + shift-invert lanczos"][cert["method"]],
+                  "eta": cert["eta"], "eta_rigorous": cert["eta_rigorous"],
+                  "rho_hat": cert["rho_hat"], "status": st},
         "phases_ms": {k: stats[k] / args.steps for k in ("ms_build", "ms_solve", "ms_certify", "ms_round")},
         "roofline": {"kernel": ("k_tcg_persist_sym (lower-triangle Q stream, timed per tCG iteration "
                                 "incl. its barriers and camera update) + k_spmm_sym (other products)"
@@ -352,34 +434,22 @@ def main():
                      "alg_bytes_per_launch": bytes_per_launch, "launch_ms": spmm_ms_per_launch,
                      "launches": pstats["spmm_timed"], "share_of_step": spmm_share,
                      "timing": "CUDA events around every Q-streaming launch (persistent tCG: per launch "
-                               "÷ its iterations), on the library's stream, over a second run of the "
-                               "same K steps"},
+                               "÷ its iterations), on the library's stream, over a second run of "
+                               "min(K, 5) steps"},
         "gpu_launches": int(stats["kernel_launches"]),
         "e2e": e2e,
     }
-    if rank == 0:
-        os.makedirs(os.path.dirname(COUNTS_FILE), exist_ok=True)
-        try:
-            counts = json.load(open(COUNTS_FILE)) if os.path.exists(COUNTS_FILE) else {}
-        except Exception:
-            counts = {}
-        prev = counts.get(args.config, {})
-        full = info["lanczos_steps"] if cert["method"] == 0 else prev.get("lanczos_steps_full")
-        counts[args.config] = {"hvps": info["hvps"], "spmms": info["spmms"],
-                               "lanczos_steps": info["lanczos_steps"],
-                               "lanczos_steps_full": full, "N": sc.N}
-        with open(COUNTS_FILE, "w") as f:
-            json.dump(counts, f, indent=1)
     clocks = clk.summary()
     result["clocks"] = clocks
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        # the oracle certifies with Lanczos to convergence (it has no Cholesky test)
-        lz = info["lanczos_steps"]
-        if cert["method"] != 0:
-            lz = (load_counts(args.config) or {}).get("lanczos_steps_full") or lz
-        est, cores, sample = oracle_sample(sc, info["hvps"], lz, info["spmms"])
-        result["cpu_baseline"] = {"value": est, "unit": "s", "cores": cores, "kind": "oracle",
-                                  "sample": sample}
+        est = OracleEstimate(sc, args.config)
+        if est.available():
+            v, sample = est.step()
+            result["cpu_baseline"] = {"value": v, "unit": "s", "cores": oracle_threads(),
+                                      "kind": "oracle", "estimate": True, "cpu": cpu_model(),
+                                      "sample": sample}
+        else:
+            result["cpu_baseline"] = None
     if rank == 0:
         print(json.dumps(result), flush=True)
     ctx.close()

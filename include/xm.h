@@ -116,21 +116,27 @@ typedef struct {
 } xm_solve_info;
 
 typedef struct {
-  double lambda_min;      /* λ_min(Z(y)), Z = Q − blkdiag(Λ) (Eq. (16)); if    */
-                          /* method == 1 the smallest Ritz value (upper bound)  */
-  double lambda_lower;    /* certified lower bound on λ_min (= λ_min, or −ε)    */
+  double lambda_min;      /* λ_min(Z(y)), Z = Q − blkdiag(Λ) (Eq. (16)): converged */
+                          /* Lanczos on Z (method 0) or shift-invert Lanczos on  */
+                          /* (Z + εI)⁻¹ after its Cholesky (method 1)            */
+  double lambda_lower;    /* lower bound on λ_min: if lower_rigorous, proven by a */
+                          /* completed Cholesky of Z + δI and its backward error */
+                          /* (−δ − γ_{n+1}·tr(Z+δI) − u‖Z‖_F); else = λ_min      */
   double rho_dual;        /* b·y = tr Λ_0 (dual objective, Eq. (16))      */
   double rho_hat;         /* objective at the rounded, recovered solution        */
-  double rho_lower;       /* ρ_dual + min(0, λ_lower)·tr X̂ (reading C10)        */
+  double rho_lower;       /* ρ_dual + min(0, λ_min)·tr X̂ (reading C10)          */
   double eta;             /* (ρ̂ − ρ_lower)/(1 + |ρ̂| + |ρ_lower|)  (Eq. (13))    */
   double eta_E;           /* App. E formula as printed: max(0, λ_min)·tr X       */
+  double rho_lower_rigorous; /* ρ_dual + min(0, λ_lower)·tr X̂                   */
+  double eta_rigorous;    /* Eq. (13) with rho_lower_rigorous                    */
   double kkt_resid;       /* ‖Z(y) Y‖_F (Thm 1 Eq. (18))                         */
   double grad_norm;
   double trace_X;         /* tr X = ‖Y‖_F²                                      */
   double normQ;
   int32_t lanczos_steps;
   int32_t certified;
-  int32_t method;         /* 0: Lanczos converged; 1: Cholesky of Z + εI        */
+  int32_t method;         /* 0: Lanczos on Z; 1: Cholesky of Z + εI + shift-invert */
+  int32_t lower_rigorous; /* 1: lambda_lower is the Cholesky-proven bound        */
 } xm_certificate;
 
 typedef struct {
@@ -242,6 +248,20 @@ xm_status xm_spmm(xm_ctx* ctx, const double* V, double* out, int32_t r);
 xm_status xm_grad(xm_ctx* ctx, const double* Y, double* grad, double* f, int32_t r);
 /* Riemannian Hessian-vector product at Y along tangent V: P_Y(2QV − 2ΛV). */
 xm_status xm_hvp(xm_ctx* ctx, const double* Y, const double* V, double* HV, int32_t r);
+/* One Steihaug–Toint truncated-CG solve ("truncated conjugate
+ * gradient") of the TR subproblem at Y (n×r,
+ * caller memory, host or device): g = grad f(Y), Hess as xm_hvp, radius
+ * Delta > 0, the context's κ / θ / max-inner options.  Outputs (caller
+ * memory, n×r): eta = the step, Heta = Hess[eta] as accumulated by the
+ * recurrence (may be NULL); *n_hvp = HVPs used; *stop = 1 negative curvature,
+ * 2 boundary exceeded, 3 converged, 4 max inner.  path selects the device
+ * implementation: 0 the library's choice, 1 persistent lower-triangle kernel
+ * (k_tcg_persist_sym), 2 persistent full-row kernel (k_tcg_persist), 3 one
+ * fused launch per iteration, 4 three kernels per iteration (CUDA graphs).
+ * XM_EINVAL if that path is not available for (N, r).  Side effects: the
+ * factor becomes Y (as xm_set_factor); certificate / rounding invalidated. */
+xm_status xm_tcg(xm_ctx* ctx, const double* Y, int32_t r, double Delta, int32_t path, double* eta,
+                 double* Heta, int32_t* n_hvp, int32_t* stop);
 /* Tangent projection P_Y(W) and retraction R_Y(V). */
 xm_status xm_project(xm_ctx* ctx, const double* Y, const double* W, double* out, int32_t r);
 xm_status xm_retract(xm_ctx* ctx, const double* Y, const double* V, double* out, int32_t r);

@@ -852,18 +852,16 @@ def suboptimality(rho_hat, rho_lower):
 
 
 def report(cert: Certificate, rho_hat: float, normQ: float = 1.0, cert_tol: float = 1e-6):
-    """η per Eq. (13) with ρ_SDP estimated by (reading C10):
-      * at a certified point (λ_min ≥ −cert_tol·max(1,‖Q‖_F)): the dual value
-        ρ_dual = b·y (strong duality; Thm 1) — η is the relative
-        duality gap between the rounded primal ρ̂ and the dual;
-      * otherwise ρ_lower = ρ_dual + min(0, λ_min)·tr X̂ (heuristic, C10).
-    η_E per App. E as printed (max(0, λ_min))."""
-    certified = cert.lambda_min >= -cert_tol * max(1.0, normQ)
-    rho_lower = cert.rho_dual if certified else \
-        cert.rho_dual + min(0.0, cert.lambda_min) * cert.trace_X
+    """η per Eq. (13) with ρ_SDP bounded below as SURVEY §8(c) O9 /
+    reading C10 state it:  ρ_lower = ρ_dual + min(0, λ_min)·tr X̂  (ρ_dual =
+    b·y = tr Λ_0, strong duality P:340, Thm 1; the min(0, ·) term is the
+    correction for a Z(y) that is not exactly PSD — a heuristic when λ_min < 0,
+    C10).  η_E per App. E as printed (max(0, λ_min))."""
+    rho_lower = cert.rho_dual + min(0.0, cert.lambda_min) * cert.trace_X
     lowE = max(0.0, cert.lambda_min) * cert.trace_X + cert.rho_dual
     return dict(rho_lower=rho_lower, eta=suboptimality(rho_hat, rho_lower),
-                eta_E=(rho_hat - lowE) / (1.0 + abs(rho_hat) + abs(lowE)))
+                eta_E=(rho_hat - lowE) / (1.0 + abs(rho_hat) + abs(lowE)),
+                certified=cert.lambda_min >= -cert_tol * max(1.0, normQ))
 
 
 def solve(scene_or_arrays, opts: Options = None, Y0=None, dense_cert=False):

@@ -450,17 +450,67 @@ __global__ void k_form_z_shift(const double* __restrict__ Q, int64_t ldq, int n,
   Z[(int64_t)i * ldq + j] = v;
 }
 
-// PSD test of Z(y) (Alg. 1): Cholesky of Z + εI succeeds ⇔ λ_min(Z) > −ε
-// (up to the backward error of Cholesky, O(n·u·‖Z‖) ≪ ε).  Single-rank Q only.
-bool psd_test_cholesky(xm_ctx* c, double eps) {
+// tr(A) and ‖A‖_F² of a symmetric A from its lower triangle (one block, fixed order)
+__global__ void k_sym_stats(const double* __restrict__ A, int64_t lda, int n, double* out) {
+  __shared__ double st[256], sf[256];
+  double tr = 0.0, fr = 0.0;
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    const double* row = A + (int64_t)i * lda;
+    for (int j = threadIdx.x; j <= i; j += blockDim.x) {
+      const double v = row[j];
+      fr = fma(j == i ? 1.0 : 2.0, v * v, fr);
+      if (j == i) tr += v;
+    }
+  }
+  st[threadIdx.x] = tr;
+  sf[threadIdx.x] = fr;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      st[threadIdx.x] += st[threadIdx.x + s];
+      sf[threadIdx.x] += sf[threadIdx.x + s];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[2 * blockIdx.x] = st[0];
+    out[2 * blockIdx.x + 1] = sf[0];
+  }
+}
+
+// PSD test of Z(y) (Alg. 1): Cholesky of Z + sI runs to completion ⇔
+// (in exact arithmetic) λ_min(Z) > −s.  In floating point, completion means
+// Z̃ + sI + ΔA = L̂L̂ᵀ with |ΔA| ≤ γ_{n+1}|L̂||L̂ᵀ| (Cholesky backward error,
+// any summation order), and ‖|L̂||L̂ᵀ|‖₂ ≤ ‖L̂‖_F² = tr(L̂L̂ᵀ) ≈ tr(Z + sI); Z̃ =
+// fl(Q − Λ) differs from Z by ≤ u|Z|.  So success certifies
+//   λ_min(Z) ≥ −s − γ_{n+1}·tr(Z + sI)·(1 + 2γ_{n+1}) − u‖Z‖_F   (= *lower).
+// Single-rank Q only.  Zw ← L (lower), U ← Lᵀ if `U` is given.
+bool psd_test_cholesky(xm_ctx* c, double s, double* lower, double* U, int64_t ldu) {
   if (c->world != 1) throw Error(XM_EINVAL, "Cholesky PSD test needs the full Q on one rank");
   const int n = c->n;
   c->Zw.alloc((size_t)n * c->ldq);
   k_form_z_shift<<<ceil_div((int64_t)n * n, 256), 256, 0, c->stream>>>(c->Q.p, c->ldq, n,
-                                                                      c->lam.p, eps, c->Zw.p);
+                                                                      c->lam.p, s, c->Zw.p);
   XM_CHECK_LAUNCH();
   count_launch(c);
-  return dense_cholesky(c, c->Zw.p, n, c->ldq, 0.0, false);
+  DBuf<double>& sp = scratch_f64(c, "zstats");
+  constexpr int kSB = 148;
+  sp.alloc(2 * kSB);
+  k_sym_stats<<<kSB, 256, 0, c->stream>>>(c->Zw.p, c->ldq, n, sp.p);
+  XM_CHECK_LAUNCH();
+  count_launch(c);
+  std::vector<double> hs(2 * kSB);
+  XM_CUDA(cudaMemcpyAsync(hs.data(), sp.p, 2 * kSB * 8, cudaMemcpyDeviceToHost, c->stream));
+  const bool ok = dense_cholesky(c, c->Zw.p, n, c->ldq, 0.0, false, U, ldu);  // syncs
+  double tr = 0.0, fr2 = 0.0;
+  for (int b = 0; b < kSB; ++b) {
+    tr += hs[2 * b];
+    fr2 += hs[2 * b + 1];
+  }
+  const double u = 1.1102230246251565e-16;
+  const double g = (n + 1) * u / (1.0 - (n + 1) * u);
+  if (lower) *lower = -s - g * std::fabs(tr) * (1.0 + 2.0 * g) - u * std::sqrt(fr2);
+  return ok;
 }
 
 // Forward substitution of a diagonal block for many right-hand sides:
@@ -494,11 +544,23 @@ __global__ void __launch_bounds__(128) k_trsm_block_cols(const double* __restric
     if (j < nb) B[(int64_t)j * ldb + col] = x[j];
 }
 
+__global__ void k_set_diag(double* A, int n, int64_t lda) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) A[(int64_t)i * lda + i] = 1.0;
+}
+
 __global__ void k_eye(double* T, int m, int64_t ld) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= m * m) return;
   const int i = t / m, j = t % m;
   T[(int64_t)i * ld + j] = (i == j) ? 1.0 : 0.0;
+}
+
+void identity(xm_ctx* c, double* A, int n, int64_t lda) {
+  XM_CUDA(cudaMemsetAsync(A, 0, (size_t)n * lda * sizeof(double), c->stream));
+  k_set_diag<<<ceil_div(n, 256), 256, 0, c->stream>>>(A, n, lda);
+  XM_CHECK_LAUNCH();
+  count_launch(c);
 }
 
 __global__ void k_transpose(const double* __restrict__ S, int64_t lds, double* __restrict__ D,

@@ -195,8 +195,30 @@ static void tridiag_min(const std::vector<double>& a, const std::vector<double>&
   s = x;
 }
 
+// y = X v for a lower-triangular X (row-major, ld): one block per row, x ≤ row
+__global__ void __launch_bounds__(256) k_trmv_lower(const double* __restrict__ X, int64_t ldx,
+                                                    int64_t n, const double* __restrict__ v,
+                                                    double* __restrict__ y) {
+  __shared__ double sh[256];
+  const int64_t row = blockIdx.x;
+  const double* xr = X + row * ldx;
+  double acc = 0.0;
+  for (int64_t x = threadIdx.x; x <= row; x += 256) acc = fma(xr[x], v[x], acc);
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) y[row] = sh[0];
+}
+
+// Lanczos (full re-orthogonalisation) for the smallest eigenpair of
+//   op.X == nullptr : Z = Q − blkdiag(Λ)               (Alg. 1 l.9-12, C19)
+//   op.X != nullptr : −Xᵀ X  with X = L⁻¹, LLᵀ = Z + sI  (shift-invert: its
+//                     smallest Ritz value is −1/(λ_min(Z) + s))
 bool lanczos(xm_ctx* c, double tol_abs, int max_steps, double* lambda, int* steps,
-             double* vec_dev) {
+             double* vec_dev, const LanczosOp& op) {
   const int64_t n = c->n;
   const int kmax = (int)std::max<int64_t>(1, std::min<int64_t>(max_steps, n));
   const int64_t ldv = round_up(n, 32);
@@ -204,6 +226,7 @@ bool lanczos(xm_ctx* c, double tol_abs, int max_steps, double* lambda, int* step
   c->lz_w.alloc(round_up(n, 32) * std::max(1, c->world) + 64);
   c->lz_c.alloc((size_t)2 * (kmax + 1) + 64);
   int nchunk_max = ceil_div(kmax + 1, kGemvChunk);
+  if (op.X) nchunk_max = std::max(nchunk_max, ceil_div(n, kGemvChunk));
   c->lz_part.alloc((size_t)nchunk_max * n + 4096);
   c->tmp.alloc((size_t)c->n_alloc * 4);
   double* alphas = c->lz_c.p;                    // device α_j
@@ -231,8 +254,20 @@ bool lanczos(xm_ctx* c, double tol_abs, int max_steps, double* lambda, int* step
     int batch_end = std::min(kmax, k + check_every);
     for (; k < batch_end; ++k) {
       const double* vk = c->lz_V.p + (int64_t)k * ldv;
-      // w = Z v_k = Q v_k − Λ v_k
-      if (c->world == 1) {
+      // w = Z v_k = Q v_k − Λ v_k   (or −Xᵀ X v_k)
+      if (op.X) {
+        double* y = c->tmp.p;
+        k_trmv_lower<<<(unsigned)n, 256, 0, c->stream>>>(op.X, op.ldx, n, vk, y);
+        const int nch = ceil_div(n, kGemvChunk);
+        k_gemv_n_part<<<dim3(ceil_div(n, 256), nch), 256, 0, c->stream>>>(op.X, op.ldx, n, (int)n, y,
+                                                                         c->lz_part.p);
+        k_gemv_n_fin<<<ceil_div(n, 256), 256, 0, c->stream>>>(n, nch, c->lz_part.p, -1.0, 0.0,
+                                                            c->lz_w.p);
+        XM_CHECK_LAUNCH();
+        count_launch(c, 3);
+        dot_flat(c, vk, c->lz_w.p, n, dots, kDotBlocks);
+        reduce_partials(c, dots, kDotBlocks, 1, alphas + k);
+      } else if (c->world == 1) {
         SpmmEpiArgs ep{};
         ep.out = c->lz_w.p;
         ep.lam = c->lam.p;
@@ -272,8 +307,11 @@ bool lanczos(xm_ctx* c, double tol_abs, int max_steps, double* lambda, int* step
     sync(c);
     tridiag_min(ha, hb, kk, lam, s);
     double res = std::fabs(hb[kk - 1] * s[kk - 1]);
-    bool breakdown = hb[kk - 1] <= 1e-14 * std::max(1.0, c->normQ);
-    converged = res <= tol_abs || breakdown || kk >= (int)n;
+    // shift-invert: θ = −1/(λ + s) ⇒ |dλ| = |dθ|/θ², so the Z-tolerance maps to tol·θ²
+    const double tol_k = op.X ? tol_abs * lam * lam : tol_abs;
+    const double scale_k = op.X ? std::fabs(lam) : std::max(1.0, c->normQ);
+    bool breakdown = hb[kk - 1] <= 1e-14 * scale_k;
+    converged = res <= tol_k || breakdown || kk >= (int)n;
     if (converged || kk >= kmax) done = true;
   }
   *lambda = lam;

@@ -142,7 +142,8 @@ std::vector<uintptr_t> graph_signature(xm_ctx* c) {
           (uintptr_t)c->Y.p, (uintptr_t)c->dir.p, (uintptr_t)c->lam.p, (uintptr_t)c->tcg.p,
           (uintptr_t)c->part1.p, (uintptr_t)c->part2.p, (uintptr_t)c->opt.profile,
           (uintptr_t)c->f0, (uintptr_t)c->f1, (uintptr_t)c->sym_part.p, (uintptr_t)c->gbar.p,
-          (uintptr_t)c->sym_plan, (uintptr_t)c->gsync.p};
+          (uintptr_t)c->sym_plan, (uintptr_t)c->gsync.p, (uintptr_t)c->fused_tcg,
+          (uintptr_t)c->opt.spmm_kernel};
 }
 
 void destroy_graph(xm_ctx::TcgGraph& g) {
@@ -232,6 +233,56 @@ struct PhaseClock {
 static const char* kPhaseNames[8] = {"tcg", "retract+df", "accept+grad", "eval_point",
                                      "certify", "escape", "lanczos", "cholesky"};
 
+// One Steihaug–Toint tCG solve (O5) at the current c->Y, c->grad, c->lam (the
+// last gradient pass) with radius Delta; returns the final device state
+// (η in c->eta, Hη in c->Heta).  Path: the whole loop in one cooperative
+// launch (tcg_persist.cu) when supported, else CUDA-graph batches of
+// iterations (fused or three-kernel, manifold.cu).
+TcgState run_tcg(xm_ctx* c, int r, double Delta) {
+  tcg_init(c, r, Delta);
+  TcgState hs{};
+  const bool persist = tcg_persist_supported(c, r);
+  xm_ctx::TcgGraph* g = !persist && c->use_graphs && c->world == 1 ? tcg_graph(c, r) : nullptr;
+  if (persist) {  // the whole tCG loop in one cooperative launch (tcg_persist.cu)
+    const bool timed = c->opt.profile != 0;
+    if (timed && !c->ev_persist[0]) {
+      XM_CUDA(cudaEventCreate(&c->ev_persist[0]));
+      XM_CUDA(cudaEventCreate(&c->ev_persist[1]));
+    }
+    if (timed) XM_CUDA(cudaEventRecord(c->ev_persist[0], c->stream));
+    tcg_persist_launch(c, r);
+    if (timed) XM_CUDA(cudaEventRecord(c->ev_persist[1], c->stream));
+    XM_CUDA(cudaMemcpyAsync(&hs, c->tcg.p, sizeof(TcgState), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    c->stats.spmm_calls += hs.n_hvp;
+    if (timed && hs.n_hvp > 0) {  // per-iteration figures: one Q stream per iteration
+      float ms = 0.f;
+      XM_CUDA(cudaEventElapsedTime(&ms, c->ev_persist[0], c->ev_persist[1]));
+      c->stats.spmm_ms += ms;
+      c->stats.spmm_timed += hs.n_hvp;
+      c->stats.spmm_alg_bytes += hs.n_hvp * tcg_persist_bytes_per_iter(c, r);
+    }
+  }
+  const int64_t s0 = c->stats.spmm_calls;
+  while (!persist) {
+    if (g) {
+      XM_CUDA(cudaGraphLaunch(g->exec, c->stream));
+      c->stats.kernel_launches += g->launches;
+    } else {
+      for (int b = 0; b < c->tcg_batch; ++b) tcg_iteration(c, r);
+    }
+    XM_CUDA(cudaMemcpyAsync(&hs, c->tcg.p, sizeof(TcgState), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    if (g && c->opt.profile) harvest_graph(c, *g);
+    if (hs.stop) {
+      // products that actually ran (batched iterations after the stop exit early)
+      c->stats.spmm_calls = s0 + hs.n_hvp;
+      break;
+    }
+  }
+  return hs;
+}
+
 struct RtrOut {
   bool converged = false;
   int64_t outer = 0;
@@ -260,44 +311,8 @@ RtrOut rtr(xm_ctx* c, double tol_abs) {
       break;
     }
     if (it >= o.max_outer) break;
-    // ---- tCG (device-resident, double-buffered state; 3 kernels / iteration)
-    tcg_init(c, r, Delta);
-    TcgState hs{};
-    const bool persist = tcg_persist_supported(c, r);
-    xm_ctx::TcgGraph* g = !persist && c->use_graphs && c->world == 1 ? tcg_graph(c, r) : nullptr;
-    if (persist) {  // the whole tCG loop in one cooperative launch (tcg_persist.cu)
-      const bool timed = c->opt.profile != 0;
-      if (timed && !c->ev_persist[0]) {
-        XM_CUDA(cudaEventCreate(&c->ev_persist[0]));
-        XM_CUDA(cudaEventCreate(&c->ev_persist[1]));
-      }
-      if (timed) XM_CUDA(cudaEventRecord(c->ev_persist[0], c->stream));
-      tcg_persist_launch(c, r);
-      if (timed) XM_CUDA(cudaEventRecord(c->ev_persist[1], c->stream));
-      XM_CUDA(cudaMemcpyAsync(&hs, c->tcg.p, sizeof(TcgState), cudaMemcpyDeviceToHost, c->stream));
-      sync(c);
-      c->stats.spmm_calls += hs.n_hvp;
-      if (timed && hs.n_hvp > 0) {  // per-iteration figures: one Q stream per iteration
-        float ms = 0.f;
-        XM_CUDA(cudaEventElapsedTime(&ms, c->ev_persist[0], c->ev_persist[1]));
-        c->stats.spmm_ms += ms;
-        c->stats.spmm_timed += hs.n_hvp;
-        c->stats.spmm_alg_bytes += hs.n_hvp * tcg_persist_bytes_per_iter(c, r);
-      }
-    }
-    while (!persist) {
-      if (g) {
-        XM_CUDA(cudaGraphLaunch(g->exec, c->stream));
-        c->stats.kernel_launches += g->launches;
-        c->stats.spmm_calls += g->spmms;
-      } else {
-        for (int b = 0; b < c->tcg_batch; ++b) tcg_iteration(c, r);
-      }
-      XM_CUDA(cudaMemcpyAsync(&hs, c->tcg.p, sizeof(TcgState), cudaMemcpyDeviceToHost, c->stream));
-      sync(c);
-      if (g && c->opt.profile) harvest_graph(c, *g);
-      if (hs.stop) break;
-    }
+    // ---- tCG (device-resident state; persistent / fused / three-kernel)
+    const TcgState hs = run_tcg(c, r, Delta);
     c->info.hvps += hs.n_hvp;
     pc.lap(0);
     // ---- retraction (+ ⟨g,η⟩, ⟨η,Hη⟩) and cancellation-free Δf (reading C21)
@@ -351,24 +366,54 @@ RtrOut rtr(xm_ctx* c, double tol_abs) {
 }
 
 // Certificate at the current point (Alg. 1 lines 9-12): Λ from the last gradient
-// pass; λ_min(Z) by Lanczos.  If Lanczos has not converged within ≈ the cost of
-// one dense factorisation (n/72 steps), Z ⪰ −εI is decided by Cholesky of Z + εI
-// (single GPU); only if that fails does Lanczos continue to convergence (the
-// escape direction v is needed then).
+// pass; λ_min(Z) by Lanczos on Z.  If Lanczos has not converged within ≈ the
+// cost of one dense factorisation (n/72 steps) — the clustered small end of
+// Z's spectrum on banded scenes — Z ⪰ −εI is decided by Cholesky of Z + εI
+// (single GPU), and λ_min is then computed by shift-invert Lanczos on
+// (Z + εI)⁻¹ = L⁻ᵀL⁻¹ (X = L⁻¹ by the DMMA TRSM; a handful of steps: the
+// inverted spectrum is well separated).  A second Cholesky at a small shift δ
+// (just above max(0, −λ_min) and the backward-error floor) then proves the
+// tight lower bound λ_min ≥ −δ − γ·tr(Z+δI) − u‖Z‖_F (lower_rigorous).  Only
+// if Z + εI is not PD does Lanczos on Z continue to convergence (the escape
+// needs v).
 void certify_current(xm_ctx* c, double* lambda, int* steps) {
   const double tol = c->opt.eig_tol * std::max(1.0, c->normQ);
   const double eps = c->opt.cert_tol * std::max(1.0, c->normQ);
   c->cert_method = 0;
+  c->cert_rigorous = 0;
   if (c->world == 1 && c->opt.cert_cholesky) {
     int budget = std::min(c->opt.lanczos_max, std::max(32, c->n / 72));
     PhaseClock pc(c);
     bool conv = lanczos(c, tol, budget, lambda, steps, c->cert_v.p);
     pc.lap(6);
+    double low_eps = 0.0;
+    DBuf<double>& U = scratch_f64(c, "zw_U");
     if (conv) {
       c->cert_lower = *lambda;
-    } else if (psd_test_cholesky(c, eps) && (pc.lap(7), true)) {
+    } else if (U.alloc((size_t)c->n * c->ldq),
+               psd_test_cholesky(c, eps, &low_eps, U.p, c->ldq) && (pc.lap(7), true)) {
       c->cert_method = 1;
-      c->cert_lower = -eps;
+      c->cert_lower = low_eps;
+      c->cert_rigorous = 1;
+      DBuf<double>& X = scratch_f64(c, "zw_X");
+      X.alloc((size_t)c->n * c->ldq);
+      identity(c, X.p, c->n, c->ldq);
+      dense_trsm_lower_left(c, c->Zw.p, c->n, c->ldq, U.p, c->ldq, X.p, c->n, c->ldq);
+      double th = 0.0;
+      int s2 = 0;
+      LanczosOp op;
+      op.X = X.p;
+      op.ldx = c->ldq;
+      lanczos(c, tol, c->opt.lanczos_max, &th, &s2, c->cert_v.p, op);
+      *steps += s2;
+      *lambda = (th < 0.0) ? -1.0 / th - eps : -eps;
+      pc.lap(6);
+      // tight proven bound: Cholesky at δ just above max(0, −λ_min) and the backward-error floor
+      const double floor_b = -(low_eps + eps);
+      const double delta = std::max(8.0 * floor_b, 2.0 * std::max(0.0, -*lambda));
+      double low_d = 0.0;
+      if (delta < eps && psd_test_cholesky(c, delta, &low_d)) c->cert_lower = low_d;
+      pc.lap(7);
     } else {
       int s1 = *steps;
       lanczos(c, tol, c->opt.lanczos_max, lambda, steps, c->cert_v.p);
@@ -744,18 +789,23 @@ xm_status xm_certify(xm_ctx* c, xm_certificate* out, double* min_eigvec) {
     ce.rho_dual = l0[0] + l0[1] + l0[2];
     ce.rho_hat = d[0];
     ce.trace_X = trX;
-    // η (Eq. (13)): ρ_SDP estimated by the dual value at a certified point,
-    // ρ_dual + min(0, λ_min)·tr X̂ otherwise (reading C10)
-    const bool psd_ok = c->cert_lower >= -c->opt.cert_tol * std::max(1.0, c->normQ);
-    ce.rho_lower = psd_ok ? ce.rho_dual : ce.rho_dual + std::min(0.0, lam) * trX;
-    ce.eta = (ce.rho_hat - ce.rho_lower) / (1.0 + std::fabs(ce.rho_hat) + std::fabs(ce.rho_lower));
-    double lowE = std::max(0.0, c->cert_lower) * trX + ce.rho_dual;
-    ce.eta_E = (ce.rho_hat - lowE) / (1.0 + std::fabs(ce.rho_hat) + std::fabs(lowE));
+    // η (Eq. (13)) with ρ_SDP bounded below by ρ_dual + min(0, λ)·tr X̂ (reading
+    // C10): once with the converged λ_min (estimate), once with the proven λ_lower
+    auto eta_of = [&](double lo) {
+      return (ce.rho_hat - lo) / (1.0 + std::fabs(ce.rho_hat) + std::fabs(lo));
+    };
+    ce.rho_lower = ce.rho_dual + std::min(0.0, lam) * trX;
+    ce.eta = eta_of(ce.rho_lower);
+    ce.rho_lower_rigorous = ce.rho_dual + std::min(0.0, c->cert_lower) * trX;
+    ce.eta_rigorous = eta_of(ce.rho_lower_rigorous);
+    ce.lower_rigorous = c->cert_rigorous;
+    double lowE = std::max(0.0, lam) * trX + ce.rho_dual;
+    ce.eta_E = eta_of(lowE);
     ce.kkt_resid = 0.5 * std::sqrt(g2);  // grad = 2 Z Y
     ce.grad_norm = std::sqrt(g2);
     ce.normQ = c->normQ;
     ce.lanczos_steps = steps;
-    ce.certified = (c->cert_lower >= -c->opt.cert_tol * std::max(1.0, c->normQ)) &&
+    ce.certified = (std::min(lam, c->cert_lower) >= -c->opt.cert_tol * std::max(1.0, c->normQ)) &&
                    std::sqrt(g2) <= c->opt.grad_tol * std::max(1.0, c->normQ) * 1.0001;
     c->cert = ce;
     c->have_cert = true;
@@ -888,6 +938,47 @@ xm_status xm_hvp(xm_ctx* c, const double* Y, const double* V, double* HV, int32_
     copy_out(c, HV, c->hO.p, len * 8);
     sync(c);
     c->cert_valid = false;
+  });
+}
+
+xm_status xm_tcg(xm_ctx* c, const double* Y, int32_t r, double Delta, int32_t path, double* eta,
+                 double* Heta, int32_t* n_hvp, int32_t* stop) {
+  if (!c || !Y || !eta || r < 1 || r > XM_MAX_R || !(Delta > 0.0) || path < 0 || path > 4)
+    return XM_EINVAL;
+  return guard(c, [&] {
+    require_stage(c, 1);
+    const bool f0 = c->fused_tcg, p0 = c->persist_tcg;
+    const int s0 = c->persist_sym;
+    struct Restore {
+      xm_ctx* c; bool f, p; int s;
+      ~Restore() { c->fused_tcg = f; c->persist_tcg = p; c->persist_sym = s; }
+    } restore{c, f0, p0, s0};
+    switch (path) {
+      case 1: c->fused_tcg = c->persist_tcg = true; c->persist_sym = 1; break;
+      case 2: c->fused_tcg = c->persist_tcg = true; c->persist_sym = -1; break;
+      case 3: c->fused_tcg = true; c->persist_tcg = false; break;
+      case 4: c->fused_tcg = false; break;
+      default: break;
+    }
+    const bool ok = path == 0 ||
+                    (path == 1 && tcg_persist_sym_supported(c, r)) ||
+                    (path == 2 && !tcg_persist_sym_supported(c, r) && tcg_persist_supported(c, r)) ||
+                    (path == 3 && !tcg_persist_supported(c, r) && tcg_fused_supported(c, r)) ||
+                    (path == 4 && !tcg_persist_supported(c, r));
+    if (!ok) throw Error(XM_EINVAL, "tCG path not available for this problem / rank");
+    const int64_t len = (int64_t)c->n * r;
+    c->r = r;
+    copy_in(c, c->Y.p, Y, len * 8);
+    c->factor_set = true;
+    c->cert_valid = false;
+    c->have_round = false;
+    grad_fused(c, r, c->Y.p, c->QY.p, c->grad.p, c->scal.p);   // g, Λ, ‖g‖² (scal[1])
+    const TcgState hs = run_tcg(c, r, Delta);
+    copy_out(c, eta, c->eta.p, len * 8);
+    if (Heta) copy_out(c, Heta, c->Heta.p, len * 8);
+    sync(c);
+    if (n_hvp) *n_hvp = hs.n_hvp;
+    if (stop) *stop = hs.stop;
   });
 }
 

@@ -176,7 +176,8 @@ struct xm_ctx {
   xm::DBuf<double> cert_v;
   xm::DBuf<double> Zw;       // Z + εI work copy for the Cholesky PSD test
   double cert_lower = 0.0;   // certified lower bound on λ_min(Z)
-  int cert_method = 0;       // 0 Lanczos converged, 1 Cholesky of Z + εI
+  int cert_method = 0;       // 0 Lanczos converged, 1 Cholesky of Z + εI + shift-invert Lanczos
+  int cert_rigorous = 0;     // 1: cert_lower proven by a completed Cholesky
   int tcg_batch = 8;
   // CUDA graph of `tcg_batch` tCG iterations per rank r (captured once, replayed)
   struct TcgGraph {
@@ -261,7 +262,8 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr, const
                     const double* pts, const double* w);
 bool dense_cholesky(xm_ctx* c, double* A, int m, int64_t lda, double rel_tol,
                     bool throw_on_fail = true, double* U = nullptr, int64_t ldu = 0);
-bool psd_test_cholesky(xm_ctx* c, double eps);
+bool psd_test_cholesky(xm_ctx* c, double shift, double* lower = nullptr, double* U = nullptr,
+                       int64_t ldu = 0);
 void dense_trsm_lower_left(xm_ctx* c, const double* L, int m, int64_t ldl, const double* U,
                            int64_t ldu, double* B, int ncols, int64_t ldb);
 // C = β·C + α·Σ_k A[k·lda + m]·B[k·ldb + n] on the fp64 tensor cores (dgemm_tn.cu);
@@ -269,6 +271,7 @@ void dense_trsm_lower_left(xm_ctx* c, const double* L, int m, int64_t ldl, const
 void dgemm_tn(xm_ctx* c, bool lower, int M, int N, int K, double alpha, const double* A,
               int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc);
 void mirror_lower(xm_ctx* c, double* Q, int n, int64_t ldq);
+void identity(xm_ctx* c, double* A, int n, int64_t lda);  // A ← I (n×n, row-major)
 
 // ------------------------------------------------------------ SpMM (spmm.cu)
 enum { EPI_STORE = 0, EPI_HVP = 1, EPI_ZMUL = 2, EPI_DF = 3, EPI_GRAD = 4, EPI_TCG = 5 };
@@ -301,6 +304,7 @@ int spmm_grid(xm_ctx* c, int r);  // number of scalar partials written by spmm()
 bool spmm_sym_supported(xm_ctx* c, int r);
 bool tcg_fused_supported(xm_ctx* c, int r);  // one-launch tCG iteration (EPI_TCG)
 bool tcg_persist_supported(xm_ctx* c, int r);  // whole tCG solve in one launch
+bool tcg_persist_sym_supported(xm_ctx* c, int r);  // ... with the lower-triangle stream
 void tcg_persist_launch(xm_ctx* c, int r);
 double tcg_persist_bytes_per_iter(xm_ctx* c, int r);
 int spmm_sym_partials(xm_ctx* c);
@@ -338,8 +342,12 @@ void zmul(xm_ctx* c, const double* x, const double* Zx_q, double* out);  // Zx =
 
 // ------------------------------------------------------------ Lanczos / rounding (cert.cu)
 // returns true if the smallest Ritz pair converged (|β_k s_k| ≤ tol_abs)
+struct LanczosOp {
+  const double* X = nullptr;  // non-null: shift-invert operator −XᵀX (X = L⁻¹ lower, row-major)
+  int64_t ldx = 0;
+};
 bool lanczos(xm_ctx* c, double tol_abs, int max_steps, double* lambda, int* steps,
-             double* vec_dev);
+             double* vec_dev, const LanczosOp& op = LanczosOp());
 void round_recover_device(xm_ctx* c);
 // xm2.cu
 void edge_residuals_user(xm_ctx* c, double* out_dev);

@@ -55,10 +55,11 @@ class Certificate(ctypes.Structure):
                 ("rho_dual", ctypes.c_double),
                 ("rho_hat", ctypes.c_double), ("rho_lower", ctypes.c_double),
                 ("eta", ctypes.c_double), ("eta_E", ctypes.c_double),
+                ("rho_lower_rigorous", ctypes.c_double), ("eta_rigorous", ctypes.c_double),
                 ("kkt_resid", ctypes.c_double), ("grad_norm", ctypes.c_double),
                 ("trace_X", ctypes.c_double), ("normQ", ctypes.c_double),
                 ("lanczos_steps", ctypes.c_int32), ("certified", ctypes.c_int32),
-                ("method", ctypes.c_int32)]
+                ("method", ctypes.c_int32), ("lower_rigorous", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -95,6 +96,7 @@ _SIGS = {
     "xm_spmm": (ctypes.c_int, [_P, _P, _P, ctypes.c_int32]),
     "xm_grad": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_int32]),
     "xm_hvp": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_int32]),
+    "xm_tcg": (ctypes.c_int, [_P, _P, ctypes.c_int32, ctypes.c_double, ctypes.c_int32, _P, _P, _P, _P]),
     "xm_project": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_int32]),
     "xm_retract": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_int32]),
     "xm_get_factor": (ctypes.c_int, [_P, _P, _P]),
@@ -350,6 +352,21 @@ class Context:
         self._check(self.lib.xm_hvp(self.h, _in_ptr(Y, np.float64, keep), _in_ptr(V, np.float64, keep),
                                     p, r), "xm_hvp")
         return arr
+
+    TCG_STOP = {1: "negcurv", 2: "exceeded", 3: "converged", 4: "maxinner"}
+    TCG_PATHS = {"auto": 0, "persist_sym": 1, "persist": 2, "fused": 3, "three_kernel": 4}
+
+    def tcg(self, Y, Delta, path="auto"):
+        """One tCG solve at Y (xm_tcg): returns (eta, Heta, n_hvp, stop)."""
+        keep = []
+        r = int(Y.shape[1])
+        eta = np.empty((self.n, r))
+        Heta = np.empty((self.n, r))
+        nh, st = ctypes.c_int32(), ctypes.c_int32()
+        self._check(self.lib.xm_tcg(self.h, _in_ptr(Y, np.float64, keep), r, float(Delta),
+                                    self.TCG_PATHS[path], eta.ctypes.data, Heta.ctypes.data,
+                                    ctypes.byref(nh), ctypes.byref(st)), "xm_tcg")
+        return eta, Heta, nh.value, self.TCG_STOP.get(st.value, str(st.value))
 
     def project(self, Y, W, out=None):
         return self._vec_op(self.lib.xm_project, "xm_project", [Y, W], int(Y.shape[1]), out)

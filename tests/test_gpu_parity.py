@@ -159,11 +159,12 @@ def test_end_to_end_solve_parity(xm, cfg, kernel, path, monkeypatch):
     assert abs(info["f"] - st.f) <= 1e-8 * (1.0 + abs(st.f))
     assert x_rel_err(Yg, st.Y) <= 1e-6
     nQ = dm.normF
-    if cert["method"] == 0:     # Lanczos converged: same λ_min
-        assert abs(cert["lambda_min"] - st.cert.lambda_min) <= 1e-6 * nQ
-    else:                       # Cholesky of Z + εI: a valid lower bound, Ritz value above λ_min
+    # converged λ_min (Lanczos on Z, or shift-invert after the Cholesky of Z + εI)
+    assert abs(cert["lambda_min"] - st.cert.lambda_min) <= 1e-6 * nQ
+    if cert["lower_rigorous"]:  # Cholesky-proven bound: valid and tight
         assert cert["lambda_lower"] <= st.cert.lambda_min + 1e-9 * nQ
-        assert cert["lambda_min"] >= st.cert.lambda_min - 1e-9 * nQ
+        assert cert["lambda_lower"] >= cert["lambda_min"] - 1e-6 * nQ
+        assert cert["eta_rigorous"] >= cert["eta"] - 1e-12
     assert abs(cert["rho_hat"] - sol.rho_hat) <= 1e-8 * (1.0 + abs(sol.rho_hat))
     assert abs(cert["rho_dual"] - st.cert.rho_dual) <= 1e-8 * (1.0 + abs(st.cert.rho_dual))
     assert cert["eta"] <= 1e-6
