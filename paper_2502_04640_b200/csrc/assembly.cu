@@ -246,6 +246,222 @@ __global__ void __launch_bounds__(128) k_clique_scatter(
   }
 }
 
+// ------------------------------------------------------------ H4 v2: exact fixed-point
+// Row-owned like k_clique_scatter, but the accumulation order no longer
+// matters: every term of an output entry is added EXACTLY, as an 88-bit
+// fixed-point integer (two signed 44-bit limbs, integer shared-memory
+// atomics), and rounded to fp64 once at the end.  So all the (landmark,
+// partner) pairs of a frame are processed in parallel (no per-landmark
+// barrier chain), every read-modify-write hits shared memory, each output
+// entry is written once, and the result is bitwise deterministic (and more
+// accurate than any fixed fp64 summation order).  Scale: every term of H
+// (App. A) is bounded by T = max_e w_e(1 + |ũ_e|²)
+// (|w_e w_f a_e[a] a_f[b]/W_k| ≤ √(w_e w_f)|a_e||a_f|), so with x = term·2^s,
+// 2^s·T ≤ 2^70, a sum of up to 2^17 terms stays below 2^87 < 2^88 and each
+// limb sum below 2^61; resolution 2^-s ≈ T·2^-70 (≈ 8e-22·T, vs fp64's
+// 1.1e-16·T per rounding).
+//
+// CTA = frame i (row band: S rows 3i..3i+2, C̄ row i−1, K̄ row i−1); output
+// columns in chunks of WCF frames.  Per chunk and batch of ≤ SC_THREADS
+// landmarks of frame i: (1) one thread per landmark advances its cursor
+// through the track (sorted by frame) to the chunk end and caches a_e, w_e,
+// w_e/W_k; (2) a block prefix sum flattens the (landmark, partner) pairs;
+// (3) one thread per pair adds its ≤ 13 terms.
+constexpr int kFxEntries = 13;
+template <int WCF, int SC_THREADS>
+constexpr size_t scatter_smem() {
+  return (size_t)kFxEntries * 2 * WCF * sizeof(long long) +      // accumulators
+         (size_t)SC_THREADS * (5 * sizeof(double) + 3 * sizeof(int));  // landmark batch cache
+}
+
+template <int WCF>
+__device__ __forceinline__ void fx_add(unsigned long long* acc, int entry, int col, double x) {
+  // x = term·2^s (|x| < 2^88); two signed limbs of 44 bits, truncated below 2^0
+  const double d1 = trunc(x * 0x1p-44);
+  const double d0 = trunc(x - d1 * 0x1p44);
+  unsigned long long* p = acc + (size_t)entry * 2 * WCF + col;
+  atomicAdd(p, (unsigned long long)(long long)d0);
+  if (d1 != 0.0) atomicAdd(p + WCF, (unsigned long long)(long long)d1);
+}
+
+template <int WCF>
+__device__ __forceinline__ double fx_value(const unsigned long long* acc, int entry, int col,
+                                           double inv_scale) {
+  const unsigned long long* p = acc + (size_t)entry * 2 * WCF + col;
+  long long l0 = (long long)p[0], l1 = (long long)p[WCF];
+  const long long c = l0 >> 44;  // normalise: l0 ∈ [0, 2^44)
+  l0 -= c * (1ll << 44);
+  l1 += c;
+  return ((double)l1 * 0x1p44 + (double)l0) * inv_scale;
+}
+
+// T = max_e w_e (1 + |ũ_e|²)  (one block)
+__global__ void k_term_bound(int64_t E, const double* __restrict__ pts, const double* __restrict__ w,
+                             double* out) {
+  __shared__ double sh[256];
+  double m = 0.0;
+  for (int64_t e = threadIdx.x; e < E; e += 256) {
+    const double x = pts[3 * e], y = pts[3 * e + 1], z = pts[3 * e + 2];
+    m = fmax(m, w[e] * (1.0 + x * x + y * y + z * z));
+  }
+  sh[threadIdx.x] = m;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
+// S_lower: with one rank the SYRK + mirror read only S[3i+a][3j+b] for j ≤ i
+template <int WCF, int SC_THREADS>
+__global__ void __launch_bounds__(SC_THREADS) k_clique_scatter_fx(
+    int N, int f0, int f1, int s_lower_only, const int32_t* __restrict__ fr_off,
+    const int32_t* __restrict__ fr_edge, const int32_t* __restrict__ lm_off,
+    const int32_t* __restrict__ e_fr, const double* __restrict__ e_pts,
+    const double* __restrict__ e_w, const double* __restrict__ W, const int32_t* __restrict__ e_lm,
+    double* __restrict__ S, int64_t ldq, int row0, double* __restrict__ Cb,
+    double* __restrict__ Kb, int64_t ldk, int32_t* __restrict__ cursor, double scale,
+    double inv_scale) {
+  extern __shared__ unsigned long long acc[];
+  double* l_ae = reinterpret_cast<double*>(acc + (size_t)kFxEntries * 2 * WCF);  // [3][T]
+  double* l_we = l_ae + 3 * SC_THREADS;
+  double* l_coef = l_we + SC_THREADS;
+  int* l_p = reinterpret_cast<int*>(l_coef + SC_THREADS);  // first partner in chunk
+  int* l_e = l_p + SC_THREADS;                           // the frame's own edge
+  int* l_off = l_e + SC_THREADS;                         // exclusive prefix of pair counts
+  __shared__ int warp_tot[SC_THREADS / 32];
+  __shared__ int batch_pairs;
+  const int i = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const bool own = (i >= f0 && i < f1);
+  const int e0 = fr_off[i], nl = fr_off[i + 1] - e0;
+  for (int l = tid; l < nl; l += SC_THREADS) cursor[e0 + l] = lm_off[e_lm[fr_edge[e0 + l]]];
+  for (int c0 = 0; c0 < N; c0 += WCF) {
+    const int c1 = min(N, c0 + WCF);
+    const bool needS = own && (!s_lower_only || c0 <= i);
+    const bool needK = i >= 1 && c0 <= i;
+    for (int t = tid; t < kFxEntries * 2 * WCF; t += SC_THREADS) acc[t] = 0ull;
+    for (int lb = 0; lb < nl; lb += SC_THREADS) {
+      // (1) per landmark: partners of this chunk = [p, q) of its frame-sorted track
+      const int l = lb + tid;
+      int cnt = 0;
+      if (l < nl) {
+        const int e = fr_edge[e0 + l];
+        const int k = e_lm[e];
+        const int end = lm_off[k + 1];
+        const int p = cursor[e0 + l];
+        int q = p;
+        while (q < end) {  // 4 independent loads per round
+          int v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[u] = (q + u < end) ? e_fr[q + u] : INT32_MAX;
+          int adv = 0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) adv += (v[u] < c1);
+          q += adv;
+          if (adv < 4) break;
+        }
+        cursor[e0 + l] = q;
+        cnt = q - p;
+        l_p[tid] = p;
+        l_e[tid] = e;
+        l_ae[tid] = e_pts[3 * e];
+        l_ae[SC_THREADS + tid] = e_pts[3 * e + 1];
+        l_ae[2 * SC_THREADS + tid] = e_pts[3 * e + 2];
+        const double we = e_w[e];
+        l_we[tid] = we;
+        l_coef[tid] = we / W[k];
+      }
+      // (2) block exclusive scan of the pair counts
+      int x = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) warp_tot[wid] = x;
+      __syncthreads();
+      if (wid == 0) {
+        int t = lane < SC_THREADS / 32 ? warp_tot[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, t, o);
+          if (lane >= o) t += y;
+        }
+        if (lane < SC_THREADS / 32) warp_tot[lane] = t;  // inclusive
+        if (lane == SC_THREADS / 32 - 1) batch_pairs = t;
+      }
+      __syncthreads();
+      l_off[tid] = x - cnt + (wid > 0 ? warp_tot[wid - 1] : 0);
+      __syncthreads();
+      // (3) one thread per (landmark, partner) pair
+      const int npairs = batch_pairs;
+      const int nlb = min(SC_THREADS, nl - lb);
+      for (int t = tid; t < npairs; t += SC_THREADS) {
+        int lo = 0, hi = nlb - 1;  // last landmark slot with l_off ≤ t
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (l_off[mid] <= t) lo = mid; else hi = mid - 1;
+        }
+        const int s = lo;
+        const int f = l_p[s] + (t - l_off[s]);
+        const int jf = e_fr[f];
+        const double ae[4] = {l_ae[s], l_ae[SC_THREADS + s], l_ae[2 * SC_THREADS + s], 1.0};
+        const double we = l_we[s];
+        const double af[4] = {e_pts[3 * f], e_pts[3 * f + 1], e_pts[3 * f + 2], 1.0};
+        const double cf = l_coef[s] * e_w[f];
+        const int col = jf - c0;
+        const bool diag = (f == l_e[s]);
+        // h[a][b] = −cf·a_e[a]·a_f[b] (+ w_e a_e[a] a_e[b] on the diagonal), ×2^s
+        if (needS && (!s_lower_only || jf <= i)) {
+#pragma unroll
+          for (int a2 = 0; a2 < 3; ++a2)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+              double h = -cf * ae[a2] * af[b];
+              if (diag) h += we * ae[a2] * ae[b];
+              fx_add<WCF>(acc, 3 * a2 + b, col, h * scale);
+            }
+        }
+        if (i >= 1) {
+#pragma unroll
+          for (int b = 0; b < 3; ++b) {
+            double h = -cf * af[b];
+            if (diag) h += we * ae[b];
+            fx_add<WCF>(acc, 9 + b, col, h * scale);
+          }
+          if (jf >= 1 && jf <= i) {
+            double h = -cf;
+            if (diag) h += we;
+            fx_add<WCF>(acc, 12, col, h * scale);
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // write the chunk: S rows 3i..3i+2 (cols 3c0..), C̄ row i−1, K̄ row i−1 (lower part)
+    const int w3 = 3 * (c1 - c0);
+    if (needS) {
+      const int jmax = s_lower_only ? min(c1, i + 1) : c1;  // frames c0..jmax−1
+      const int wS = 3 * (jmax - c0);
+      for (int t = tid; t < 3 * wS; t += SC_THREADS) {
+        const int a2 = t / wS, x = t % wS, col = x / 3, b = x % 3;
+        S[(int64_t)(3 * i + a2 - row0) * ldq + 3 * c0 + x] = fx_value<WCF>(acc, 3 * a2 + b, col, inv_scale);
+      }
+    }
+    if (i >= 1) {
+      for (int x = tid; x < w3; x += SC_THREADS)
+        Cb[(int64_t)(i - 1) * ldq + 3 * c0 + x] = fx_value<WCF>(acc, 9 + x % 3, x / 3, inv_scale);
+      if (needK) {
+        const int jlo = max(c0, 1), jhi = min(c1, i + 1);
+        for (int j = jlo + tid; j < jhi; j += SC_THREADS)
+          Kb[(int64_t)(i - 1) * ldk + (j - 1)] = fx_value<WCF>(acc, 12, j - c0, inv_scale);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ============================================================ dense fp64 kernels
 // The O(N³) updates are the DMMA kernel of dgemm_tn.cu (TN shape, see there).
 
@@ -877,12 +1093,45 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
     c->L.alloc(1);
   }
   phase("zero S,C,K");
-  k_clique_scatter<<<N, 128, 0, c->stream>>>(N, c->f0, c->f1, c->fr_off.p, c->fr_edge.p,
-                                             c->lm_off.p, c->e_fr.p, c->e_pts.p, c->e_w.p, c->W.p,
-                                             c->e_lm.p, c->Q.p, c->ldq, c->row0, c->G.p, c->L.p,
-                                             c->ldk);
-  XM_CHECK_LAUNCH();
-  count_launch(c);
+  if (std::getenv("XM_SCATTER_V1")) {  // round-1 kernel (A/B)
+    k_clique_scatter<<<N, 128, 0, c->stream>>>(N, c->f0, c->f1, c->fr_off.p, c->fr_edge.p,
+                                               c->lm_off.p, c->e_fr.p, c->e_pts.p, c->e_w.p, c->W.p,
+                                               c->e_lm.p, c->Q.p, c->ldq, c->row0, c->G.p, c->L.p,
+                                               c->ldk);
+    XM_CHECK_LAUNCH();
+    count_launch(c);
+  } else {
+    c->scal.alloc(64);
+    double* d_T = c->scal.p + 60;
+    k_term_bound<<<1, 256, 0, c->stream>>>(Ek, c->e_pts.p, c->e_w.p, d_T);
+    XM_CHECK_LAUNCH();
+    double T = 0.0;
+    XM_CUDA(cudaMemcpyAsync(&T, d_T, 8, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    if (!(T > 0.0) || !std::isfinite(T)) throw Error(XM_EINVAL, "non-finite measurement scale");
+    const int ex = 70 - (int)std::ceil(std::log2(T));
+    const double scale = std::ldexp(1.0, ex), inv_scale = std::ldexp(1.0, -ex);
+    DBuf<int32_t>& cursor = scratch_i32(c, "scatter_cursor");
+    cursor.alloc(Ek);
+#define XM_SCATTER_LAUNCH(WC_, NT_)                                                             \
+  do {                                                                                           \
+    constexpr size_t sm_ = scatter_smem<WC_, NT_>();                                             \
+    ensure_smem_attr((const void*)k_clique_scatter_fx<WC_, NT_>, sm_);                           \
+    k_clique_scatter_fx<WC_, NT_><<<N, NT_, sm_, c->stream>>>(                                   \
+        N, c->f0, c->f1, c->world == 1 ? 1 : 0, c->fr_off.p, c->fr_edge.p, c->lm_off.p, c->e_fr.p, \
+        c->e_pts.p, c->e_w.p, c->W.p, c->e_lm.p, c->Q.p, c->ldq, c->row0, c->G.p, c->L.p, c->ldk,  \
+        cursor.p, scale, inv_scale);                                                             \
+  } while (0)
+    const char* cfg = std::getenv("XM_SCATTER_CFG");
+    // 768 frames × 1024 threads (213 KB, 1 CTA / SM) measured best at E and D
+    // (E: 55.9 vs 60.9 ms for 384 × 512 with 2 CTAs / SM, 67 ms for 256 × 256)
+    if (cfg && std::string(cfg) == "384") XM_SCATTER_LAUNCH(384, 512);
+    else if (cfg && std::string(cfg) == "256") XM_SCATTER_LAUNCH(256, 256);
+    else XM_SCATTER_LAUNCH(768, 1024);
+#undef XM_SCATTER_LAUNCH
+    XM_CHECK_LAUNCH();
+    count_launch(c, 2);
+  }
 
   phase("scatter");
   // ---- H5: K̄ = LLᵀ, G = L⁻¹C̄, Q = S − GᵀG
