@@ -394,21 +394,67 @@ def block_apply(Lam, V):
     return np.einsum("iab,ibr->iar", Lam, blocks(V)).reshape(V.shape)
 
 
-def cost(Q, Y):
-    """f(Y) = tr(Q U Uᵀ)… = tr(Yᵀ Q Y) = ⟨Y, QY⟩ (Eq. (17)/(23) objective)."""
-    return float(np.vdot(Y, Q @ Y))
+# Scale regularisation (App. D; reading C23):
+# F(X) = λ Σ_{i≥2} (X_{3i,3i} − 1)², and on the feasible set X_ii = α_i I₃, so on
+# the BM factor F = λ Σ_{i≥1} (α_i − 1)² (0-based frames, α_i = ‖Y_i‖²/3).
+# Its Euclidean gradient is 2 d_i Y_i with d_i = (2λ/3)(α_i − 1) (d_0 = 0), its
+# Hessian along V is 2 d_i V_i + (8λ/9)⟨Y_i, V_i⟩ Y_i.
+
+def reg_d(Y, lam):
+    """d_i = (2λ/3)(α_i − 1) for i ≥ 1, d_0 = 0."""
+    d = (2.0 * lam / 3.0) * (alphas(Y) - 1.0)
+    d[0] = 0.0
+    return d
 
 
-def rgrad(Y, QY):
-    """Riemannian gradient = P(2QY) = 2(QY − blkdiag(Λ)Y) = 2 Z(y)Y (C5)."""
+def reg_value(Y, lam):
+    """λ Σ_{i≥1} (α_i − 1)²  (App. D objective term)."""
+    if lam == 0.0:
+        return 0.0
+    a = alphas(Y)[1:]
+    return lam * float(np.sum((a - 1.0) ** 2))
+
+
+def reg_delta(Y, D, lam):
+    """F(Y + D) − F(Y) without cancellation: λ Σ (α'_i − α_i)(α'_i + α_i − 2),
+    α'_i − α_i = ⟨D_i, 2Y_i + D_i⟩/3."""
+    if lam == 0.0:
+        return 0.0
+    B, Db = blocks(Y)[1:], blocks(D)[1:]
+    da = np.einsum("iar,iar->i", Db, 2.0 * B + Db) / 3.0
+    a = alphas(Y)[1:]
+    return lam * float(np.sum(da * (2.0 * a + da - 2.0)))
+
+
+def cost(Q, Y, lam=0.0):
+    """f(Y) = tr(Q U Uᵀ)… = tr(Yᵀ Q Y) = ⟨Y, QY⟩ (Eq. (17)/(23) objective),
+    plus the App. D term λ Σ_{i≥1} (α_i − 1)² when λ > 0."""
+    return float(np.vdot(Y, Q @ Y)) + reg_value(Y, lam)
+
+
+def rgrad(Y, QY, lam=0.0):
+    """Riemannian gradient = P(2QY) = 2(QY − blkdiag(Λ)Y) = 2 Z(y)Y (C5).
+    With λ > 0 (App. D) the regulariser's gradient 2 d_i Y_i is radial, hence
+    tangent for i ≥ 1 and without effect on Λ (sym₀ of a multiple of I₃):
+    grad = 2(QY + dY − ΛY) = 2 Z_λ(y) Y."""
     Lam = multipliers(Y, QY)
-    return 2.0 * (QY - block_apply(Lam, Y)), Lam
+    g = 2.0 * (QY - block_apply(Lam, Y))
+    if lam != 0.0:
+        g = g + 2.0 * (reg_d(Y, lam)[:, None, None] * blocks(Y)).reshape(Y.shape)
+    return g, Lam
 
 
-def hess(Q, Y, Lam, V):
+def hess(Q, Y, Lam, V, lam=0.0):
     """Riemannian Hessian (analytic HVP; reading C5):
-    Hess[V] = P(2QV − 2 blkdiag(Λ) V)."""
-    return project(Y, 2.0 * (Q @ V) - 2.0 * block_apply(Lam, V))
+    Hess[V] = P(2QV − 2 blkdiag(Λ) V  [+ 2 d V + (8λ/9)⟨Y_i,V_i⟩ Y_i, App. D])."""
+    W = 2.0 * (Q @ V) - 2.0 * block_apply(Lam, V)
+    if lam != 0.0:
+        B, Vb = blocks(Y), blocks(V)
+        yv = np.einsum("iar,iar->i", B, Vb)
+        yv[0] = 0.0
+        W = W + (2.0 * reg_d(Y, lam)[:, None, None] * Vb
+                 + (8.0 * lam / 9.0) * yv[:, None, None] * B).reshape(V.shape)
+    return project(Y, W)
 
 
 def _gram_schmidt_rows(Mx):
@@ -523,6 +569,7 @@ class Options:
     lanczos_max: int = 3000
     rank_cap: int = 10
     seed: int = 0
+    scale_reg: float = 0.0           # λ of App. D, 0 = the plain problem
 
 
 @dataclasses.dataclass
@@ -541,7 +588,8 @@ def rtr(Q, Y0, opts: Options, normQ: Optional[float] = None) -> RTRResult:
     """Riemannian trust region with tCG (Manopt structure; O4).
 
     TR ratio with the cancellation-free Δf = 2⟨QY, D⟩ + ⟨D, QD⟩, D = Y′ − Y
-    (reading C21)."""
+    (reading C21), plus the App. D term's change (reg_delta) when λ > 0."""
+    lam = opts.scale_reg
     n = Q.shape[0]
     N = n // 3
     normQ = float(np.linalg.norm(Q)) if normQ is None else normQ
@@ -551,8 +599,8 @@ def rtr(Q, Y0, opts: Options, normQ: Optional[float] = None) -> RTRResult:
     Y = Y0.copy()
     QY = Q @ Y
     n_spmm = 1
-    g, Lam = rgrad(Y, QY)
-    f = float(np.vdot(Y, QY))
+    g, Lam = rgrad(Y, QY, lam)
+    f = float(np.vdot(Y, QY)) + reg_value(Y, lam)
     n_hvp = 0
     accepts = 0
     converged = False
@@ -566,7 +614,7 @@ def rtr(Q, Y0, opts: Options, normQ: Optional[float] = None) -> RTRResult:
             break
 
         def hvp(V):
-            return hess(Q, Y, Lam, V)
+            return hess(Q, Y, Lam, V, lam)
 
         eta, Heta, nh, stop = tcg(hvp, Y, g, Delta, opts.tcg_kappa, opts.tcg_theta,
                                   opts.tcg_max_inner)
@@ -576,7 +624,7 @@ def rtr(Q, Y0, opts: Options, normQ: Optional[float] = None) -> RTRResult:
         D = Yn - Y
         QD = Q @ D
         n_spmm += 1
-        df = 2.0 * float(np.vdot(QY, D)) + float(np.vdot(D, QD))
+        df = 2.0 * float(np.vdot(QY, D)) + float(np.vdot(D, QD)) + reg_delta(Y, D, lam)
         model_dec = -float(np.vdot(g, eta)) - 0.5 * float(np.vdot(eta, Heta))
         reg = max(1.0, abs(f)) * EPS * 1e3
         rho = (-df + reg) / (model_dec + reg)
@@ -592,12 +640,13 @@ def rtr(Q, Y0, opts: Options, normQ: Optional[float] = None) -> RTRResult:
                 n_spmm += 1
             else:
                 QY = QY + QD
-            f = float(np.vdot(Y, QY))
-            g, Lam = rgrad(Y, QY)
+            f = float(np.vdot(Y, QY)) + reg_value(Y, lam)
+            g, Lam = rgrad(Y, QY, lam)
     QY = Q @ Y                      # fresh before any certificate (O4)
     n_spmm += 1
-    g, _ = rgrad(Y, QY)
-    return RTRResult(Y=Y, QY=QY, f=float(np.vdot(Y, QY)), grad_norm=float(np.linalg.norm(g)),
+    g, _ = rgrad(Y, QY, lam)
+    return RTRResult(Y=Y, QY=QY, f=float(np.vdot(Y, QY)) + reg_value(Y, lam),
+                     grad_norm=float(np.linalg.norm(g)),
                      converged=converged, outer=it, n_hvp=n_hvp, n_spmm=n_spmm)
 
 
@@ -680,21 +729,39 @@ class Certificate:
 
 
 def certificate(Q, Y, opts: Options, QY=None, dense: bool = False, normQ=None) -> Certificate:
+    """Λ, Z(y) = Q − blkdiag(Λ) and its smallest eigenpair (Alg. 1 l.9-12).
+    With λ > 0 (App. D): Z_λ = Q + λ∇F(X) − Σ y_i A_i = Q + blkdiag(d_i I₃) −
+    blkdiag(Λ), and the dual value (App. D/E, "Σ y_i b_i + F(X) − ⟨∇F(X), X⟩")
+    ρ_dual = tr Λ_0 + λΣ(α_i − 1)² − Σ 3 d_i α_i = tr Λ_0 − λ Σ_{i≥1}(α_i² − 1)."""
+    lam_r = opts.scale_reg
     QY = Q @ Y if QY is None else QY
-    g, Lam = rgrad(Y, QY)
+    g, Lam = rgrad(Y, QY, lam_r)
     normQ = float(np.linalg.norm(Q)) if normQ is None else normQ
+    d = reg_d(Y, lam_r) if lam_r != 0.0 else None
     ZY = QY - block_apply(Lam, Y)
+    if d is not None:
+        ZY = ZY + (d[:, None, None] * blocks(Y)).reshape(Y.shape)
     if dense:
-        lam, v = dense_min_eig(z_matrix(Q, Lam))
+        Z = z_matrix(Q, Lam)
+        if d is not None:
+            Z = Z + np.diag(np.repeat(d, 3))
+        lam, v = dense_min_eig(Z)
         steps = 0
     else:
         def apply_Z(x):
             X = x.reshape(-1, 1)
-            return (Q @ X - block_apply(Lam, X)).ravel()
+            out = (Q @ X - block_apply(Lam, X)).ravel()
+            if d is not None:
+                out = out + np.repeat(d, 3) * x
+            return out
         lam, v, steps, _ = lanczos_min_eig(apply_Z, Q.shape[0],
                                            opts.eig_tol * max(1.0, normQ),
                                            opts.lanczos_max, opts.seed)
-    return Certificate(lambda_min=lam, v=v, rho_dual=float(np.trace(Lam[0])), Lam=Lam,
+    rho_dual = float(np.trace(Lam[0]))
+    if lam_r != 0.0:
+        a = alphas(Y)[1:]
+        rho_dual -= lam_r * float(np.sum(a * a - 1.0))
+    return Certificate(lambda_min=lam, v=v, rho_dual=rho_dual, Lam=Lam,
                        kkt_resid=float(np.linalg.norm(ZY)), grad_norm=float(np.linalg.norm(g)),
                        lanczos_steps=steps, trace_X=float(np.vdot(Y, Y)))
 
@@ -703,7 +770,7 @@ def certificate(Q, Y, opts: Options, QY=None, dense: bool = False, normQ=None) -
 # O7  Riemannian staircase (Algorithm 1; Thm 2; C9)
 # =============================================================================
 
-def escape(Q, Y, QY, v, max_halvings=60, c_floor=1e-3):
+def escape(Q, Y, QY, v, max_halvings=60, c_floor=1e-3, lam=0.0):
     """Y₊ = Retr_{[Y,0]}(α[0, v]) with α = 1, ½, … until f decreases
     (Alg. 1 l.14-22; D = [0; vᵀ] is tangent at [Y, 0], Thm 2, reading C9).
     Δf computed cancellation-free (C21).  Returns (Y₊, α, Δf)."""
@@ -716,7 +783,7 @@ def escape(Q, Y, QY, v, max_halvings=60, c_floor=1e-3):
     for _ in range(max_halvings + 1):
         Yp = retract(Yz, alpha * Dir, c_floor)
         D = Yp - Yz
-        df = 2.0 * float(np.vdot(QYz, D)) + float(np.vdot(D, Q @ D))
+        df = 2.0 * float(np.vdot(QYz, D)) + float(np.vdot(D, Q @ D)) + reg_delta(Yz, D, lam)
         if df < 0.0:
             return Yp, alpha, df
         alpha *= 0.5
@@ -766,7 +833,7 @@ def staircase(dm_or_Q, opts: Options = None, Y0=None, r0=3, dense_cert=False) ->
                                    certified=bool(ok and res.converged),
                                    converged=res.converged, cert=cert, ranks=ranks,
                                    n_hvp=n_hvp, n_spmm=n_spmm, outer=outer)
-        Y, _, _ = escape(Q, res.Y, res.QY, cert.v, c_floor=opts.scale_floor)
+        Y, _, _ = escape(Q, res.Y, res.QY, cert.v, c_floor=opts.scale_floor, lam=opts.scale_reg)
         ranks.append(Y.shape[1])
 
 
@@ -792,7 +859,7 @@ class Solution:
     edge_objective: float  # Eq. (3) evaluated directly at (R, s, t, p)
 
 
-def round_recover(dm: DataMatrix, Y) -> Solution:
+def round_recover(dm: DataMatrix, Y, lam: float = 0.0) -> Solution:
     """Rounding: top-3 eigenvectors of X = YYᵀ via the r×r Gram YᵀY,
     Y₃ = Y W₃; per block: s_i = ‖B_i‖_F/√3, polar → O(3); gauge fix
     U* = R̄_0ᵀ Ū (Eq. (12), P:273) with s_0 renormalised to 1 (C16);
@@ -839,7 +906,8 @@ def round_recover(dm: DataMatrix, Y) -> Solution:
     p[obs] = acc[obs] / dm.W[obs, None]
     edge_obj = edge_objective(dm.frame, dm.landmark, dm.pts, dm.w, s, R, t, p)
     return Solution(R=R, s=s, t=t, p=p, n_flipped=flips, Yr=Yr,
-                    rho_hat=float(np.vdot(Yr, dm.Q @ Yr)), edge_objective=edge_obj)
+                    rho_hat=float(np.vdot(Yr, dm.Q @ Yr)) + reg_value(Yr, lam),
+                    edge_objective=edge_obj)
 
 
 # =============================================================================
@@ -869,7 +937,7 @@ def solve(scene_or_arrays, opts: Options = None, Y0=None, dense_cert=False):
     s = scene_or_arrays
     dm = build_Q(s.N, s.M, s.frame, s.landmark, s.pts, s.w)
     st = staircase(dm, opts, Y0=Y0, dense_cert=dense_cert)
-    sol = round_recover(dm, st.Y)
+    sol = round_recover(dm, st.Y, (opts or Options()).scale_reg)
     rep = report(st.cert, sol.rho_hat, dm.normF, (opts or Options()).cert_tol)
     return dm, st, sol, rep
 

@@ -180,3 +180,95 @@ def test_E_noisy_certified_and_recovery_optimal(xm, E_noisy):
     scale = np.abs(res).sum() + 1e-300
     assert np.abs(gp).max() <= 1e-9 * scale
     assert np.abs(gt[1:]).max() <= 1e-9 * scale
+
+
+# ----------------------------------------------------------------------------- C, D
+# The noisy configurations have no known optimum (parity
+# unpinned beyond KKT), so GPU-vs-oracle agreement on the same generated input
+# is the check: f, X = YYᵀ, λ_min, ρ̂, and the recovered R, s, t, p.
+def _end_to_end(xm, sc, opts, Y0=None):
+    dm = xo.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+    st = xo.staircase(dm, xo.Options(**opts), Y0=Y0)
+    sol = xo.round_recover(dm, st.Y)
+    with xm.Context(profile=1, **opts) as ctx:
+        ctx.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+        if Y0 is not None:
+            ctx.set_factor(Y0)
+        status, info = ctx.solve()
+        cert = ctx.certify()
+        gsol = ctx.round_recover()
+        Yg = ctx.get_factor()
+    return dm, st, sol, status, info, cert, gsol, Yg
+
+
+def _compare(dm, st, sol, status, info, cert, gsol, Yg):
+    assert status == 0 and info["certified"] == 1 and st.certified
+    assert info["r"] == st.r
+    assert abs(info["f"] - st.f) <= 1e-8 * (1.0 + abs(st.f))
+    Xo = st.Y @ st.Y.T
+    assert np.linalg.norm(Yg @ Yg.T - Xo) <= 1e-6 * np.linalg.norm(Xo)
+    assert abs(cert["lambda_min"] - st.cert.lambda_min) <= 1e-6 * dm.normF
+    assert abs(cert["rho_hat"] - sol.rho_hat) <= 1e-8 * (1.0 + abs(sol.rho_hat))
+    assert cert["eta"] <= 1e-6
+    np.testing.assert_allclose(gsol["s"], sol.s, rtol=1e-6, atol=1e-9)
+    np.testing.assert_allclose(gsol["R"], sol.R, atol=1e-6)
+    np.testing.assert_allclose(gsol["t"], sol.t, atol=1e-6 * max(1.0, np.abs(sol.t).max()))
+    ok = np.isfinite(sol.p[:, 0])
+    np.testing.assert_allclose(gsol["p"][ok], sol.p[ok], atol=1e-6 * max(1.0, np.abs(sol.p[ok]).max()))
+    assert gsol["n_flipped"] == sol.n_flipped
+
+
+@pytest.mark.parametrize("cfg", ["C", "D"])
+def test_noisy_configs_end_to_end_vs_oracle(xm, cfg):
+    sc = config_scene(cfg)
+    opts = dict(rank_cap=5) if cfg == "D" else {}
+    _compare(*_end_to_end(xm, sc, opts))
+
+
+def test_D_random_init_escalates_at_scale(xm):
+    """Thm 2/3 at config D's size: a random feasible r = 3 start
+    escalates through the staircase (rank cap 5, BASELINE config D) on both
+    sides, to the same certified X."""
+    from synth.scenes import random_factor
+    sc = config_scene("D")
+    Y0 = random_factor(sc.N, 3, 4)
+    dm, st, sol, status, info, cert, gsol, Yg = _end_to_end(xm, sc, dict(rank_cap=5), Y0=Y0)
+    assert len(st.ranks) >= 2 and info["escapes"] >= 1
+    _compare(dm, st, sol, status, info, cert, gsol, Yg)
+
+
+# ----------------------------------------------------------------------------- E, identical Q
+def test_E_identical_Q_spmm_and_hvp(xm):
+    """Reading C13 at the north-star size: a host-generated symmetric
+    30465 × 30465 Q uploaded with xm_set_Q; single products Q·V (r = 1, 3, 4,
+    every streaming kernel) and one Riemannian HVP checked on sampled rows /
+    frames against numpy on the host, ≤ 1e-12 relative."""
+    N = 10155
+    n = 3 * N
+    rng = np.random.default_rng(77)
+    Q = rng.standard_normal((n, n))
+    Q += Q.T
+    Q *= 0.5
+    rows = _sample_rows(N, 16, 5)
+    frames = np.unique(rows // 3)                    # includes frame 0 (the anchor)
+    for kernel in (0, 1, 2):
+        with xm.Context(spmm_kernel=kernel) as ctx:
+            ctx.set_Q(Q)
+            for r in (1, 3, 4):
+                V = rng.standard_normal((n, r))
+                out = ctx.spmm(V)
+                ref = Q[rows] @ V
+                assert rel(out[rows], ref) <= 1e-12, (kernel, r, rel(out[rows], ref))
+            if kernel == 0:
+                from synth.scenes import random_factor
+                r = 3
+                Y = random_factor(N, r, 6)
+                V = xo.project(Y, rng.standard_normal((n, r)))
+                HV = ctx.hvp(Y, V)
+                sub = (3 * frames[:, None] + np.arange(3)).ravel()   # block 0 first = anchor
+                Ys, Vs = Y[sub], V[sub]
+                QYs, QVs = Q[sub] @ Y, Q[sub] @ V
+                Lam = xo.multipliers(Ys, QYs)
+                ref = xo.project(Ys, 2.0 * QVs - 2.0 * xo.block_apply(Lam, Vs))
+                assert rel(HV[sub], ref) <= 1e-12, rel(HV[sub], ref)
+    del Q

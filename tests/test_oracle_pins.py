@@ -736,3 +736,105 @@ def test_tcg_negative_curvature_first_step_is_steepest_descent_to_boundary():
     eta, Heta, nh, stop = xo.tcg(lambda V: -V, Y, g, 0.37)
     assert stop == "negcurv" and nh == 1
     np.testing.assert_allclose(eta, -0.37 * g / np.linalg.norm(g), rtol=0, atol=1e-14)
+
+
+# ----------------------------------------------------------------------------- App. D (NEXT-3)
+# Scale regularisation λ Σ_{i≥2}(X_{3i,3i} − 1)² (App. D);
+# on the feasible set X_ii = α_i I₃, so on the factor F = λ Σ_{i≥1}(α_i − 1)².
+
+def _collapse_scene():
+    """A noisy forward trajectory whose unregularised optimum collapses the
+    scales (F14; App. D's motivation, "collapse all cameras ... into a
+    single point"); weights × 1e-3 put ‖Q‖_F ≈ 39 on the scale of λ."""
+    sc = make_scene(30, 400, "road", seed=1, sigma_d=0.3, sigma_u=0.05, track_mean=4.0)
+    return sc, sc.w * 1e-3
+
+
+def test_scale_reg_zero_is_the_plain_problem():
+    """λ = 0 → the plain solve, bit for bit."""
+    sc = make_scene(10, 300, "unordered", seed=3, vis_prob=0.6, sigma_d=0.05, sigma_u=1e-3)
+    dm, st, sol, rep = xo.solve(sc)
+    dm2, st2, sol2, rep2 = xo.solve(sc, xo.Options(scale_reg=0.0))
+    assert np.array_equal(st.Y, st2.Y) and st.f == st2.f and rep["eta"] == rep2["eta"]
+
+
+@pytest.mark.parametrize("r", [3, 4])
+def test_scale_reg_gradient_and_hessian_finite_differences(small_problem, r):
+    """d/dh f_λ(R(hV)) = ⟨grad f_λ, V⟩; Euclidean FD of F alone; Hess f_λ[V] =
+    P(D grad f_λ[V]); self-adjoint (λ = 2.5 on a random feasible point)."""
+    sc, dm = small_problem
+    lam = 2.5
+    Y = random_factor(sc.N, r, 80 + r)
+    V = xo.project(Y, random_tangent_ambient(sc.N, r, 90 + r))
+    W = xo.project(Y, random_tangent_ambient(sc.N, r, 95 + r))
+    g, Lam = xo.rgrad(Y, dm.Q @ Y, lam)
+    h = 1e-5
+    fd = (xo.cost(dm.Q, xo.retract(Y, h * V), lam) - xo.cost(dm.Q, xo.retract(Y, -h * V), lam)) / (2 * h)
+    assert abs(fd - np.vdot(g, V)) <= 1e-6 * max(1.0, abs(fd))
+    # F alone, ambient: ∇F = 2 d_i Y_i (d_0 = 0) — brute force from the definition
+    A = random_tangent_ambient(sc.N, r, 99 + r)
+    F = lambda Z: lam * sum((np.sum(Z[3 * i:3 * i + 3] ** 2) / 3.0 - 1.0) ** 2 for i in range(1, sc.N))
+    fdF = (F(Y + h * A) - F(Y - h * A)) / (2 * h)
+    gF = (2.0 * xo.reg_d(Y, lam)[:, None, None] * xo.blocks(Y)).reshape(Y.shape)
+    assert abs(fdF - np.vdot(gF, A)) <= 1e-7 * max(1.0, abs(fdF))
+    HV = xo.hess(dm.Q, Y, Lam, V, lam)
+    h = 1e-6
+    gp, _ = xo.rgrad(Y + h * V, dm.Q @ (Y + h * V), lam)
+    gm, _ = xo.rgrad(Y - h * V, dm.Q @ (Y - h * V), lam)
+    fdH = xo.project(Y, (gp - gm) / (2 * h))
+    assert np.linalg.norm(fdH - HV) <= 1e-5 * np.linalg.norm(HV)
+    HW = xo.hess(dm.Q, Y, Lam, W, lam)
+    assert abs(np.vdot(HV, W) - np.vdot(V, HW)) <= 1e-10 * np.linalg.norm(HV) * np.linalg.norm(W)
+
+
+def test_scale_reg_prevents_scale_collapse():
+    """the unregularised optimum collapses the scales (min s < 0.1); the
+    regularised one (λ = 10 ≈ 0.26‖Q‖_F) keeps them (min s ≥ 0.5), certified
+    with η ≤ 1e-6."""
+    sc, w = _collapse_scene()
+    dm = xo.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, w)
+    st0 = xo.staircase(dm, xo.Options())
+    sol0 = xo.round_recover(dm, st0.Y)
+    assert st0.certified and sol0.s.min() < 0.1
+    st = xo.staircase(dm, xo.Options(scale_reg=10.0))
+    sol = xo.round_recover(dm, st.Y, 10.0)
+    rep = xo.report(st.cert, sol.rho_hat, dm.normF)
+    assert st.certified and sol.s.min() >= 0.5
+    assert rep["eta"] <= 1e-6
+    # the regulariser only adds a nonnegative term: f_λ ≥ f_0 at the λ-optimum
+    assert st.f >= xo.cost(dm.Q, st.Y) - 1e-12 * dm.normF
+
+
+def test_scale_reg_unit_scale_scene_keeps_the_optimum():
+    """noise-free scene with ground-truth scales all 1 ⇒ F vanishes at
+    the optimum, λ = 1 gives the same X as λ = 0 (f* = 0, η ≤ 1e-6)."""
+    sc = make_scene(12, 300, "unordered", seed=5, vis_prob=0.5, log_scale_range=0.0)
+    dm = xo.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+    st0 = xo.staircase(dm, xo.Options())
+    st1 = xo.staircase(dm, xo.Options(scale_reg=1.0))
+    sol1 = xo.round_recover(dm, st1.Y, 1.0)
+    rep1 = xo.report(st1.cert, sol1.rho_hat, dm.normF)
+    assert st1.certified and abs(st1.f) <= 1e-8 * dm.normF and rep1["eta"] <= 1e-6
+    X0, X1 = st0.Y @ st0.Y.T, st1.Y @ st1.Y.T
+    assert np.linalg.norm(X1 - X0) <= 1e-6 * np.linalg.norm(X0)
+    np.testing.assert_allclose(sol1.s, 1.0, atol=1e-6)
+
+
+def test_scale_reg_dual_value_and_Z_by_convexity_identity():
+    """App. E proof with F quadratic: for every feasible X′ and the
+    certificate (Z_λ, ρ_dual) at x,  f_λ(X′) − ⟨Z_λ, X′⟩ − ρ_dual = F(X′) − F(x) −
+    ⟨∇F(x), X′ − x⟩ = λ Σ_{i≥1} (α′_i − α_i)²  (exact Bregman divergence), and
+    = ⟨Z_λ, X⟩-gap 0 at x itself when x is critical (strong duality)."""
+    sc, w = _collapse_scene()
+    dm = xo.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, w)
+    lam = 10.0
+    st = xo.staircase(dm, xo.Options(scale_reg=lam))
+    cert = st.cert
+    Z = xo.z_matrix(dm.Q, cert.Lam) + np.diag(np.repeat(xo.reg_d(st.Y, lam), 3))
+    a = xo.alphas(st.Y)
+    for k in range(6):
+        Yp = random_factor(sc.N, st.r, 200 + k) if k else st.Y
+        ap = xo.alphas(Yp)
+        gap = xo.cost(dm.Q, Yp, lam) - np.vdot(Yp, Z @ Yp) - cert.rho_dual
+        breg = lam * float(np.sum((ap[1:] - a[1:]) ** 2))
+        assert abs(gap - breg) <= 1e-9 * (abs(xo.cost(dm.Q, Yp, lam)) + 1.0), (k, gap, breg)
