@@ -142,8 +142,8 @@ def oracle_unit_times(dm, ranks, n_lanczos, n_hvp=4):
     (xo.hess: Q·V + projection) at a random feasible Y of rank r, for each r;
     the O(n·r) work of one outer TR iteration (retraction + gradient); and the
     oracle's Lanczos run of n_lanczos steps (its full re-orthogonalisation
-    makes step k cost a + b·k): timed in full when n_lanczos ≤ 64, else from
-    two timed runs of 16 and 64 steps, T(k) = a·k + b·k²/2 fitted and
+    makes step k cost a + b·k): timed in full when n_lanczos ≤ 256, else from
+    two timed runs of 64 and 256 steps, T(k) = a·k + b·k²/2 fitted and
     evaluated at n_lanczos."""
     import numpy as np
     from oracle import xm_oracle as xo
@@ -177,14 +177,16 @@ def oracle_unit_times(dm, ranks, n_lanczos, n_hvp=4):
         t0 = time.perf_counter()
         xo.lanczos_min_eig(apply_Z, dm.n, 0.0, max_steps=k)
         return time.perf_counter() - t0
-    if n_lanczos <= 64:
+    if n_lanczos <= 256:
         t_lz_total, how = (lz_time(n_lanczos) if n_lanczos > 0 else 0.0), f"{n_lanczos} steps timed"
     else:
-        T1, T2 = lz_time(16), lz_time(64)
-        b = 2.0 * (T2 / 64 - T1 / 16) / (64 - 16)
-        a = T1 / 16 - b * 16 / 2
+        k1, k2 = 64, 256
+        T1, T2 = lz_time(k1), lz_time(k2)
+        b = max(0.0, 2.0 * (T2 / k2 - T1 / k1) / (k2 - k1))
+        a = T1 / k1 - b * k1 / 2
         t_lz_total = a * n_lanczos + b * n_lanczos * n_lanczos / 2
-        how = f"16 and 64 steps timed ({T1:.2f} s, {T2:.2f} s), a·k + b·k²/2 at k = {n_lanczos}"
+        how = (f"{k1} and {k2} steps timed ({T1:.2f} s, {T2:.2f} s), a·k + b·k²/2 at "
+               f"k = {n_lanczos}")
     return {"t_hvp": t_hvp, "t_outer": t_outer, "t_lz_total": t_lz_total, "lz_how": how}
 
 

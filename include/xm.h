@@ -97,6 +97,11 @@ typedef struct {
                           /* 2 lower-triangle (symmetric) stream — one GPU and */
                           /* r ≤ 5 only, else falls back to 1 [0] */
   uint64_t seed;          /* Lanczos start vector (splitmix64 stream)         [0]  */
+  double scale_reg;       /* λ of the scale-regularised objective of App. D  */
+                          /* (P:1612-1655): f + λ Σ_{i≥1} (α_i − 1)², Z_λ =   */
+                          /* Q + blkdiag(2λ/3 (α_i−1) I) − blkdiag(Λ), dual   */
+                          /* tr Λ_0 − λ Σ (α_i² − 1).  λ > 0 uses the unfused */
+                          /* product + epilogue kernels (no persistent tCG)  [0]  */
 } xm_options;
 
 typedef struct {

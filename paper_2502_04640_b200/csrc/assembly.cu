@@ -411,30 +411,21 @@ __global__ void __launch_bounds__(SC_THREADS) k_clique_scatter_fx(
         const double af[4] = {e_pts[3 * f], e_pts[3 * f + 1], e_pts[3 * f + 2], 1.0};
         const double cf = l_coef[s] * e_w[f];
         const int col = jf - c0;
-        const bool diag = (f == l_e[s]);
-        // h[a][b] = −cf·a_e[a]·a_f[b] (+ w_e a_e[a] a_e[b] on the diagonal), ×2^s
+        // h[a][b] = c·a_e[a]·a_f[b], c = −w_e w_f/W_k, or w_e − w_e²/W_k on the
+        // diagonal (f = e; exactly 0 for a single-view landmark, W_k = w_e), ×2^s
+        const double cp = (f == l_e[s]) ? (we - cf) : -cf;
         if (needS && (!s_lower_only || jf <= i)) {
 #pragma unroll
-          for (int a2 = 0; a2 < 3; ++a2)
+          for (int a2 = 0; a2 < 3; ++a2) {
+            const double ca = cp * ae[a2];
 #pragma unroll
-            for (int b = 0; b < 3; ++b) {
-              double h = -cf * ae[a2] * af[b];
-              if (diag) h += we * ae[a2] * ae[b];
-              fx_add<WCF>(acc, 3 * a2 + b, col, h * scale);
-            }
+            for (int b = 0; b < 3; ++b) fx_add<WCF>(acc, 3 * a2 + b, col, ca * af[b] * scale);
+          }
         }
         if (i >= 1) {
 #pragma unroll
-          for (int b = 0; b < 3; ++b) {
-            double h = -cf * af[b];
-            if (diag) h += we * ae[b];
-            fx_add<WCF>(acc, 9 + b, col, h * scale);
-          }
-          if (jf >= 1 && jf <= i) {
-            double h = -cf;
-            if (diag) h += we;
-            fx_add<WCF>(acc, 12, col, h * scale);
-          }
+          for (int b = 0; b < 3; ++b) fx_add<WCF>(acc, 9 + b, col, cp * af[b] * scale);
+          if (jf >= 1 && jf <= i) fx_add<WCF>(acc, 12, col, cp * scale);
         }
       }
       __syncthreads();
@@ -650,7 +641,8 @@ bool dense_cholesky(xm_ctx* c, double* A, int m, int64_t lda, double rel_tol, bo
 
 // Z + εI with Z = Q − blkdiag(Λ) (Eq. (16)); lower triangle incl. diagonal is all potrf reads.
 __global__ void k_form_z_shift(const double* __restrict__ Q, int64_t ldq, int n,
-                               const double* __restrict__ lam, double eps, double* __restrict__ Z) {
+                               const double* __restrict__ lam, double eps, double* __restrict__ Z,
+                               const double* __restrict__ regd) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= (int64_t)n * n) return;
   int i = (int)(t / n), j = (int)(t % n);
@@ -661,7 +653,7 @@ __global__ void k_form_z_shift(const double* __restrict__ Q, int64_t ldq, int n,
     int a = i % 3, b = j % 3;
     const int idx[3][3] = {{0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
     v -= L[idx[a][b]];
-    if (i == j) v += eps;
+    if (i == j) v += eps + (regd ? regd[i / 3] : 0.0);  // Z_λ = Q + blkdiag(d I) − blkdiag(Λ)
   }
   Z[(int64_t)i * ldq + j] = v;
 }
@@ -705,8 +697,8 @@ bool psd_test_cholesky(xm_ctx* c, double s, double* lower, double* U, int64_t ld
   if (c->world != 1) throw Error(XM_EINVAL, "Cholesky PSD test needs the full Q on one rank");
   const int n = c->n;
   c->Zw.alloc((size_t)n * c->ldq);
-  k_form_z_shift<<<ceil_div((int64_t)n * n, 256), 256, 0, c->stream>>>(c->Q.p, c->ldq, n,
-                                                                      c->lam.p, s, c->Zw.p);
+  k_form_z_shift<<<ceil_div((int64_t)n * n, 256), 256, 0, c->stream>>>(
+      c->Q.p, c->ldq, n, c->lam.p, s, c->Zw.p, c->opt.scale_reg != 0.0 ? c->regd.p : nullptr);
   XM_CHECK_LAUNCH();
   count_launch(c);
   DBuf<double>& sp = scratch_f64(c, "zstats");

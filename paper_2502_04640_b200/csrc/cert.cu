@@ -267,7 +267,7 @@ bool lanczos(xm_ctx* c, double tol_abs, int max_steps, double* lambda, int* step
         count_launch(c, 3);
         dot_flat(c, vk, c->lz_w.p, n, dots, kDotBlocks);
         reduce_partials(c, dots, kDotBlocks, 1, alphas + k);
-      } else if (c->world == 1) {
+      } else if (c->world == 1 && c->opt.scale_reg == 0.0) {
         SpmmEpiArgs ep{};
         ep.out = c->lz_w.p;
         ep.lam = c->lam.p;

@@ -11,6 +11,8 @@
 //   grad     = 2(QY − ΛY)                                   (= P(2QY), reading C5)
 //   Hess[V]  = P(2QV − 2ΛV)                                  (analytic HVP)
 //   Retr     : s′ = max(s + ⟨V_i,R̂⟩/3, c·s), R̂′ = MGS(R̂ + W/s)   (C6, C7)
+//   App. D (λ > 0, i ≥ 1, d_i = 2λ/3 (α_i − 1)):  f += λ(α_i − 1)²,
+//     grad_i += 2 d_i Y_i,  Hess[V]_i += P_i(2 d_i V_i + 8λ/9 ⟨Y_i,V_i⟩ Y_i),  (ZX)_i += d_i X_i
 //
 // tCG (Steihaug–Toint in Manopt's form) runs as THREE kernels
 // per iteration with the scalar recurrences folded in: every block recomputes
@@ -31,7 +33,7 @@ template <int R>
 __global__ void __launch_bounds__(kFT) k_grad(int N, const double* __restrict__ Y,
                                               const double* __restrict__ QY,
                                               double* __restrict__ lam, double* __restrict__ grad,
-                                              double* __restrict__ partials) {
+                                              double* __restrict__ partials, double reg) {
   int i = blockIdx.x * kFT + threadIdx.x;
   double v[3] = {0.0, 0.0, 1.0e300};
   if (i < N) {
@@ -46,8 +48,16 @@ __global__ void __launch_bounds__(kFT) k_grad(int N, const double* __restrict__ 
     for (int q = 0; q < 6; ++q) lam[6 * i + q] = L[q];
     Blk<R> gr;
     sub_lam<R>(g, L, y, 2.0, 2.0, gr);
-    store_blk<R>(grad, i, gr);
     v[0] = dotb<R>(y, g);
+    if (reg != 0.0 && i > 0) {  // App. D: radial (tangent) gradient 2 d_i Y_i, f += λ(α−1)²
+      const double d = (2.0 * reg / 3.0) * (alpha - 1.0);
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int cc = 0; cc < R; ++cc) gr.v[a][cc] = fma(2.0 * d, y.v[a][cc], gr.v[a][cc]);
+      v[0] += reg * (alpha - 1.0) * (alpha - 1.0);
+    }
+    store_blk<R>(grad, i, gr);
     v[1] = frob2<R>(gr);
     if (i > 0) v[2] = alpha;
   }
@@ -75,7 +85,7 @@ __global__ void __launch_bounds__(kFT) k_hvp(int N, const double* __restrict__ Y
                                              const double* __restrict__ V,
                                              const double* __restrict__ QV,
                                              double* __restrict__ HV, double* __restrict__ partials,
-                                             const int* __restrict__ stop) {
+                                             const int* __restrict__ stop, double reg) {
   if (stop && *stop) return;
   int i = blockIdx.x * kFT + threadIdx.x;
   double v[1] = {0.0};
@@ -88,6 +98,16 @@ __global__ void __launch_bounds__(kFT) k_hvp(int N, const double* __restrict__ Y
 #pragma unroll
     for (int q = 0; q < 6; ++q) L[q] = lam[6 * i + q];
     sub_lam<R>(qv, L, vv, 2.0, 2.0, w);
+    if (reg != 0.0 && i > 0) {  // App. D: + 2 d_i V_i + (8λ/9)⟨Y_i, V_i⟩ Y_i
+      const double alpha = frob2<R>(y) / 3.0;
+      const double d2 = 2.0 * (2.0 * reg / 3.0) * (alpha - 1.0);
+      const double yv = (8.0 * reg / 9.0) * dotb<R>(y, vv);
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int cc = 0; cc < R; ++cc)
+          w.v[a][cc] = fma(d2, vv.v[a][cc], fma(yv, y.v[a][cc], w.v[a][cc]));
+    }
     project_blk<R>(y, i == 0, w);
     store_blk<R>(HV, i, w);
     v[0] = dotb<R>(vv, w);
@@ -333,16 +353,56 @@ __global__ void k_pad_column(int64_t n, int r, const double* __restrict__ Y, dou
 __global__ void __launch_bounds__(kFT) k_zmul(int N, const double* __restrict__ lam,
                                               const double* __restrict__ x,
                                               const double* __restrict__ qx,
-                                              double* __restrict__ out) {
+                                              double* __restrict__ out,
+                                              const double* __restrict__ regd) {
   int i = blockIdx.x * kFT + threadIdx.x;
   if (i >= N) return;
   double L[6];
 #pragma unroll
   for (int q = 0; q < 6; ++q) L[q] = lam[6 * i + q];
+  if (regd) {  // Z_λ = Q + blkdiag(d_i I) − blkdiag(Λ)  (App. D)
+    L[0] -= regd[i];
+    L[1] -= regd[i];
+    L[2] -= regd[i];
+  }
   double x0 = x[3 * i], x1 = x[3 * i + 1], x2 = x[3 * i + 2];
   out[3 * i] = qx[3 * i] - (L[0] * x0 + L[3] * x1 + L[4] * x2);
   out[3 * i + 1] = qx[3 * i + 1] - (L[3] * x0 + L[1] * x1 + L[5] * x2);
   out[3 * i + 2] = qx[3 * i + 2] - (L[4] * x0 + L[5] * x1 + L[2] * x2);
+}
+
+// App. D per-frame helpers: d_i = 2λ/3 (α_i − 1) (d_0 = 0), and partial sums of
+// λ(α_i−1)² [0], α_i² − 1 [1] over i ≥ 1, and of F(Y + D) − F(Y) computed
+// without cancellation, λ(α′−α)(α′+α−2) with α′−α = ⟨D_i, 2Y_i + D_i⟩/3 [2]
+template <int R>
+__global__ void __launch_bounds__(kFT) k_reg_frames(int N, const double* __restrict__ Y,
+                                                    const double* __restrict__ D, double reg,
+                                                    double* __restrict__ regd,
+                                                    double* __restrict__ partials) {
+  int i = blockIdx.x * kFT + threadIdx.x;
+  double v[3] = {0.0, 0.0, 0.0};
+  if (i < N) {
+    Blk<R> y;
+    load_blk<R>(Y, i, y);
+    const double alpha = frob2<R>(y) / 3.0;
+    if (regd) regd[i] = (i > 0) ? (2.0 * reg / 3.0) * (alpha - 1.0) : 0.0;
+    if (i > 0) {
+      v[0] = reg * (alpha - 1.0) * (alpha - 1.0);
+      v[1] = alpha * alpha - 1.0;
+      if (D) {
+        Blk<R> dd;
+        load_blk<R>(D, i, dd);
+        double s = 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int cc = 0; cc < R; ++cc) s = fma(dd.v[a][cc], fma(2.0, y.v[a][cc], dd.v[a][cc]), s);
+        const double da = s / 3.0;
+        v[2] = reg * da * (2.0 * alpha + da - 2.0);
+      }
+    }
+  }
+  block_reduce_store<3, kFT>(v, partials);
 }
 
 // ================================================================== host wrappers
@@ -369,7 +429,8 @@ void grad_and_multipliers(xm_ctx* c, int r, const double* Y, const double* QY, d
                           double* scal_out) {
   int nb = frame_blocks(c);
   c->red.alloc((size_t)nb * 4 + 1024);
-  XM_DISPATCH_R(r, (k_grad<R><<<nb, kFT, 0, c->stream>>>(c->N, Y, QY, c->lam.p, grad, c->red.p)));
+  XM_DISPATCH_R(r, (k_grad<R><<<nb, kFT, 0, c->stream>>>(c->N, Y, QY, c->lam.p, grad, c->red.p,
+                                                         c->opt.scale_reg)));
   XM_CHECK_LAUNCH();
   count_launch(c);
   reduce_partials(c, c->red.p, nb, 3, scal_out, 4u);
@@ -392,14 +453,15 @@ void retract(xm_ctx* c, int r, const double* Y, const double* V, double step, do
 void hvp_epilogue(xm_ctx* c, int r, const double* Y, const double* V, const double* QV,
                   double* HV, double* partials, const int* stop) {
   XM_DISPATCH_R(r, (k_hvp<R><<<frame_blocks(c), kFT, 0, c->stream>>>(c->N, Y, c->lam.p, V, QV, HV,
-                                                                     partials, stop)));
+                                                                     partials, stop,
+                                                                     c->opt.scale_reg)));
   XM_CHECK_LAUNCH();
   count_launch(c);
 }
 
 int hvp_product(xm_ctx* c, int r, const double* Y, const double* V, double* HV, double* partials,
                 const int* stop) {
-  if (c->world == 1) {
+  if (c->world == 1 && c->opt.scale_reg == 0.0) {
     SpmmEpiArgs ep{};
     ep.Y = Y;
     ep.lam = c->lam.p;
@@ -490,8 +552,23 @@ void pad_column(xm_ctx* c, int r, const double* Y, double* Yz, const double* v, 
   count_launch(c);
 }
 
+// App. D sums at Y (and F(Y + D) − F(Y) if D): scal_out[0] = F(Y), [1] = Σ_{i≥1}(α_i²−1),
+// [2] = ΔF; d_i into c->regd.
+void reg_frames(xm_ctx* c, int r, const double* Y, const double* D, double* scal_out) {
+  const int nb = frame_blocks(c);
+  c->regd.alloc((size_t)c->N + 8);
+  DBuf<double>& part = scratch_f64(c, "reg_part");
+  part.alloc((size_t)nb * 3 + 8);
+  XM_DISPATCH_R(r, (k_reg_frames<R><<<nb, kFT, 0, c->stream>>>(c->N, Y, D, c->opt.scale_reg,
+                                                              c->regd.p, part.p)));
+  XM_CHECK_LAUNCH();
+  count_launch(c);
+  reduce_partials(c, part.p, nb, 3, scal_out);
+}
+
 void zmul(xm_ctx* c, const double* x, const double* Zx_q, double* out) {
-  k_zmul<<<frame_blocks(c), kFT, 0, c->stream>>>(c->N, c->lam.p, x, Zx_q, out);
+  k_zmul<<<frame_blocks(c), kFT, 0, c->stream>>>(c->N, c->lam.p, x, Zx_q, out,
+                                                 c->opt.scale_reg != 0.0 ? c->regd.p : nullptr);
   XM_CHECK_LAUNCH();
   count_launch(c);
 }

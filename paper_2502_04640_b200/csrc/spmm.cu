@@ -483,7 +483,8 @@ static void launch_tcg(xm_ctx* c, const double* V, int r, const SpmmEpiArgs& ep)
 }
 
 bool tcg_fused_supported(xm_ctx* c, int r) {
-  if (!c->fused_tcg || c->world != 1 || r < 1 || r > 6 || !tcg_fullrow_ok(c) || c->N < 1)
+  if (!c->fused_tcg || c->world != 1 || r < 1 || r > 6 || !tcg_fullrow_ok(c) || c->N < 1 ||
+      c->opt.scale_reg != 0.0)  // App. D terms live in the unfused epilogues only
     return false;
   const int G = spmm_fullrow_grid(c);
   return ceil_div(c->N, G) <= kSpmmThreads;

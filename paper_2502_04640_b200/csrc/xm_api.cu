@@ -75,7 +75,7 @@ void read_scal(xm_ctx* c, int first, int count, double* out) {
 
 // QY = Q·Y, Λ, grad, and scal_out[0..2] = f, ‖g‖², min α  (fused on one GPU)
 void grad_fused(xm_ctx* c, int r, const double* Y, double* QY, double* grad, double* scal_out) {
-  if (c->world == 1) {
+  if (c->world == 1 && c->opt.scale_reg == 0.0) {
     c->part1.alloc(2048);
     SpmmEpiArgs ep{};
     ep.out = QY;
@@ -137,13 +137,19 @@ void dots(xm_ctx* c, int64_t len, int npair, const double* const* a, const doubl
 // early-exits once the device-side tCG state says stop, so a replay past the
 // end of tCG is a cheap no-op.  With profile=1 each SpMM is bracketed by event
 // nodes owned by the graph (harvested after every replay).
+uintptr_t reg_bits(xm_ctx* c) {
+  uint64_t b;
+  std::memcpy(&b, &c->opt.scale_reg, 8);
+  return (uintptr_t)b;
+}
+
 std::vector<uintptr_t> graph_signature(xm_ctx* c) {
   return {(uintptr_t)c->N, (uintptr_t)c->n, (uintptr_t)c->ldq, (uintptr_t)c->Q.p,
           (uintptr_t)c->Y.p, (uintptr_t)c->dir.p, (uintptr_t)c->lam.p, (uintptr_t)c->tcg.p,
           (uintptr_t)c->part1.p, (uintptr_t)c->part2.p, (uintptr_t)c->opt.profile,
           (uintptr_t)c->f0, (uintptr_t)c->f1, (uintptr_t)c->sym_part.p, (uintptr_t)c->gbar.p,
           (uintptr_t)c->sym_plan, (uintptr_t)c->gsync.p, (uintptr_t)c->fused_tcg,
-          (uintptr_t)c->opt.spmm_kernel};
+          (uintptr_t)c->opt.spmm_kernel, reg_bits(c)};
 }
 
 void destroy_graph(xm_ctx::TcgGraph& g) {
@@ -323,14 +329,17 @@ RtrOut rtr(xm_ctx* c, double tol_abs) {
             c->red.p);
     reduce_partials(c, c->red.p, nb, 2, c->scal.p + 10);
     df_product(c, r, c->Dv.p, c->QY.p, c->QD.p, c->scal.p + 8);
+    if (o.scale_reg != 0.0) reg_frames(c, r, c->Y.p, c->Dv.p, c->scal.p + 24);
     double d[4];
     read_scal(c, 8, 4, d);
+    double dreg = 0.0;
+    if (o.scale_reg != 0.0) read_scal(c, 26, 1, &dreg);
     int rerr = 0;
     XM_CUDA(cudaMemcpyAsync(&rerr, c->flags.p, 4, cudaMemcpyDeviceToHost, c->stream));
     sync(c);
     if (rerr) throw Error(XM_ERETRACT, "retraction failure");
     pc.lap(1);
-    const double df = 2.0 * d[0] + d[1];
+    const double df = 2.0 * d[0] + d[1] + dreg;
     const double model_dec = -d[2] - 0.5 * d[3];
     const double reg = std::max(1.0, std::fabs(f)) * eps * 1e3;
     const double rho = (-df + reg) / (model_dec + reg);
@@ -381,6 +390,7 @@ void certify_current(xm_ctx* c, double* lambda, int* steps) {
   const double eps = c->opt.cert_tol * std::max(1.0, c->normQ);
   c->cert_method = 0;
   c->cert_rigorous = 0;
+  if (c->opt.scale_reg != 0.0) reg_frames(c, c->r, c->Y.p, nullptr, c->scal.p + 24);  // d_i at Y
   if (c->world == 1 && c->opt.cert_cholesky) {
     int budget = std::min(c->opt.lanczos_max, std::max(32, c->n / 72));
     PhaseClock pc(c);
@@ -444,7 +454,12 @@ void escape(xm_ctx* c) {
     df_product(c, r1, c->Dv.p, c->Heta.p, c->QD.p, c->scal.p + 8);
     double d[2];
     read_scal(c, 8, 2, d);
-    double df = 2.0 * d[0] + d[1];
+    double dreg = 0.0;
+    if (c->opt.scale_reg != 0.0) {
+      reg_frames(c, r1, c->Ynew.p, c->Dv.p, c->scal.p + 24);
+      read_scal(c, 26, 1, &dreg);
+    }
+    double df = 2.0 * d[0] + d[1] + dreg;
     if (df < 0.0) {
       XM_CUDA(cudaMemcpyAsync(c->Y.p, c->eta.p, len1 * 8, cudaMemcpyDeviceToDevice, c->stream));
       c->r = r1;
@@ -782,12 +797,21 @@ xm_status xm_certify(xm_ctx* c, xm_certificate* out, double* min_eigvec) {
     double l0[3];
     XM_CUDA(cudaMemcpyAsync(l0, c->lam.p, 24, cudaMemcpyDeviceToHost, c->stream));
     sync(c);
+    double reg_dual = 0.0, reg_hat = 0.0;
+    if (c->opt.scale_reg != 0.0) {  // App. D: ρ_dual −= λΣ(α²−1) at Y; ρ̂ += F(Ŷ)
+      double t[3];
+      reg_frames(c, 3, c->Yr.p, nullptr, c->scal.p + 24);
+      read_scal(c, 24, 1, &reg_hat);
+      reg_frames(c, c->r, c->Y.p, nullptr, c->scal.p + 24);  // leaves d_i at Y in c->regd
+      read_scal(c, 24, 3, t);
+      reg_dual = -c->opt.scale_reg * t[1];
+    }
     xm_certificate ce{};
     ce.lambda_min = lam;
     ce.lambda_lower = c->cert_lower;
     ce.method = c->cert_method;
-    ce.rho_dual = l0[0] + l0[1] + l0[2];
-    ce.rho_hat = d[0];
+    ce.rho_dual = l0[0] + l0[1] + l0[2] + reg_dual;
+    ce.rho_hat = d[0] + reg_hat;
     ce.trace_X = trX;
     // η (Eq. (13)) with ρ_SDP bounded below by ρ_dual + min(0, λ)·tr X̂ (reading
     // C10): once with the converged λ_min (estimate), once with the proven λ_lower

@@ -130,6 +130,7 @@ struct xm_ctx {
   int64_t n_alloc = 0;  // rows allocated for vectors (≥ world·3·nfpr)
   xm::DBuf<double> Y, QY, grad, eta, Heta, res, dir, Hdir, Ynew, Dv, QD, tmp, tmp2;
   xm::DBuf<double> alpha;  // N
+  xm::DBuf<double> regd;   // N: App. D diagonal shifts d_i = 2λ/3 (α_i − 1) at the current factor
   xm::DBuf<double> lam;    // N × 6 (xx, yy, zz, xy, xz, yz)
   xm::DBuf<double> part;   // SpMM split-K partials: nsplit × nrows × r
   xm::DBuf<double> red;    // block partials for reductions
@@ -339,6 +340,9 @@ void tcg_iteration(xm_ctx* c, int r);
 void axpy(xm_ctx* c, int64_t len, double a, const double* x, double* y);
 void pad_column(xm_ctx* c, int r, const double* Y, double* Yz, const double* v, double* Dz);
 void zmul(xm_ctx* c, const double* x, const double* Zx_q, double* out);  // Zx = Qx − Λx (r = 1)
+// App. D (scale_reg λ): scal_out[0] = F(Y), [1] = Σ_{i≥1}(α_i² − 1), [2] = F(Y+D) − F(Y) (D may
+// be NULL); d_i = 2λ/3 (α_i − 1) into c->regd
+void reg_frames(xm_ctx* c, int r, const double* Y, const double* D, double* scal_out);
 
 // ------------------------------------------------------------ Lanczos / rounding (cert.cu)
 // returns true if the smallest Ritz pair converged (|β_k s_k| ≤ tol_abs)

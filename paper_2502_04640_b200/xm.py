@@ -38,7 +38,8 @@ class Options(ctypes.Structure):
                 ("max_outer", ctypes.c_int32), ("rank_cap", ctypes.c_int32),
                 ("lanczos_max", ctypes.c_int32), ("refresh_every", ctypes.c_int32),
                 ("profile", ctypes.c_int32), ("cert_cholesky", ctypes.c_int32),
-                ("spmm_kernel", ctypes.c_int32), ("seed", ctypes.c_uint64)]
+                ("spmm_kernel", ctypes.c_int32), ("seed", ctypes.c_uint64),
+                ("scale_reg", ctypes.c_double)]
 
 
 class SolveInfo(ctypes.Structure):
