@@ -965,17 +965,26 @@ def edge_residuals(frame, landmark, pts, w, sol: Solution) -> np.ndarray:
     return res
 
 
-def xm2_select(N: int, M: int, frame, landmark, res, drop_fraction: float = 0.1) -> np.ndarray:
-    """Which measurements XM² keeps (reading C22).
+def xm2_select(N: int, M: int, frame, landmark, res, drop_fraction: float = 0.1,
+               min_obs: int = 3) -> np.ndarray:
+    """Which measurements XM² keeps (readings C22, C22b).
 
     1. Order the E measurements by residual, largest first; equal residuals
        by (landmark, frame) ascending.  Drop the first ⌊drop_fraction·E⌋.
-    2. Never disconnect: if some frame is no longer in the
+    2. Keep every frame determined (C22b): a frame needs ≥ min_obs kept
+       measurements of landmarks that have ≥ 2 kept measurements (its pose
+       and scale then follow from ≥ 3 shared points).  Frames in ascending
+       order; a deficient frame gets its dropped measurements back in the
+       reverse of the drop order (smallest residual first) until it has
+       min_obs such measurements (or none are left).
+    3. Never disconnect: if some frame is no longer in the
        component of the others (bipartite frame–landmark graph of the kept
        measurements), restore dropped measurements in the reverse of the drop
-       order (smallest residual first), each one only if it joins two
-       components, until all frames are in one component (S:518's "restore
-       minimal edges by ascending residual until connected").
+       order, each one only if it joins two components, until all frames are
+       in one component (S:518's "restore minimal edges by ascending residual
+       until connected").
+    4. Minimality: a restored measurement whose landmark ends with a
+       single kept measurement adds nothing to Q (F10) — dropped again.
     Returns a boolean keep mask over the E measurements."""
     frame = np.asarray(frame, np.int64)
     landmark = np.asarray(landmark, np.int64)
@@ -985,6 +994,25 @@ def xm2_select(N: int, M: int, frame, landmark, res, drop_fraction: float = 0.1)
     dropped = order[:nd]
     keep = np.ones(E, dtype=bool)
     keep[dropped] = False
+    restored = np.zeros(E, dtype=bool)
+    # 2. determined frames
+    kcnt = np.bincount(landmark[keep], minlength=M)
+    rank = np.empty(E, dtype=np.int64)
+    rank[np.asarray(order, dtype=np.int64)] = np.arange(E)
+    by_frame = [[] for _ in range(N)]
+    for e in range(E):
+        by_frame[int(frame[e])].append(e)
+    for i in range(N):
+        def useful():
+            return sum(1 for e in by_frame[i] if keep[e] and kcnt[landmark[e]] >= 2)
+        cand = sorted((e for e in by_frame[i] if not keep[e]), key=lambda e: -rank[e])
+        for e in cand:
+            if useful() >= min_obs:
+                break
+            keep[e] = True
+            restored[e] = True
+            kcnt[landmark[e]] += 1
+    # 3. connectivity (Kruskal over the remaining dropped list, smallest residual first)
     parent = list(range(N + M))                      # frames 0..N-1, landmarks N..N+M-1
 
     def find(x):
@@ -1003,6 +1031,8 @@ def xm2_select(N: int, M: int, frame, landmark, res, drop_fraction: float = 0.1)
     for e in reversed(dropped):                      # smallest residual first
         if n_frame_comps == 1:
             break
+        if keep[e]:
+            continue
         a, b = find(int(frame[e])), find(N + int(landmark[e]))
         if a == b:
             continue
@@ -1010,8 +1040,13 @@ def xm2_select(N: int, M: int, frame, landmark, res, drop_fraction: float = 0.1)
         parent[b] = a
         has_frame[a] = fa or fb
         keep[e] = True
+        restored[e] = True
         if fa and fb:
             n_frame_comps -= 1
+    # 4. minimality: restored leaves (landmark with one kept measurement) go again
+    kcnt = np.bincount(landmark[keep], minlength=M)
+    leaf = restored & keep & (kcnt[landmark] == 1)
+    keep[leaf] = False
     return keep
 
 

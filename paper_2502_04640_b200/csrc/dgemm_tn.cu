@@ -49,8 +49,11 @@ struct TileCfg {
   static constexpr size_t SMEM = STAGE * STAGES * sizeof(double);
 };
 using BigTile = TileCfg<8, 2, 4>;
-using BigTile32 = TileCfg<8, 2, 4, 32, 3>;   // k-block 32, 3 stages (default for K > 64)
+using BigTile32 = TileCfg<8, 2, 4, 32, 3>;   // k-block 32, 3 stages, 8 warps (A/B: XM_GEMM_TILE=w8)
 using MidTile = TileCfg<8, 1, 4, 16, 4>;     // 64 × 128, 2 CTAs / SM (A/B: XM_GEMM_TILE=mid)
+using W16Tile = TileCfg<4, 4, 4, 32, 3>;     // 128 × 128, 16 warps of 32 × 32: the default for
+                                             // K > 64 (E: SYRK 297 vs 301 ms, TRSM 125 vs 134 ms
+                                             // for 8 warps of 64 × 32, XM_GEMM_TILE=w8)
 using SmallTile = TileCfg<4, 2, 2>;
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int bytes) {
@@ -260,7 +263,8 @@ void dgemm_tn(xm_ctx* c, bool lower, int M, int N, int K, double alpha, const do
   if (K <= 64) dispatch<SmallTile>(c, lower, v16, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
   else if (c->gemm_tile == 1) dispatch<BigTile>(c, lower, v16, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
   else if (c->gemm_tile == 2 && !lower) dispatch<MidTile>(c, lower, v16, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-  else dispatch<BigTile32>(c, lower, v16, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else if (c->gemm_tile == 3) dispatch<BigTile32>(c, lower, v16, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else dispatch<W16Tile>(c, lower, v16, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
 }
 
 }  // namespace xm

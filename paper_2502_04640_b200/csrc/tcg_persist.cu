@@ -78,10 +78,22 @@ __device__ __forceinline__ void cgrid_sync(unsigned long long* cnt, unsigned G) 
 }
 }  // namespace
 
+// Cross-warp flags in shared memory (producer / consumer hand-offs): every
+// access after the CTA's initial barrier is an atomic, so the protocol is
+// race-free in the memory model (and clean under compute-sanitizer racecheck).
+__device__ __forceinline__ int flag_ld(volatile int* p) { return atomicAdd((int*)p, 0); }
+__device__ __forceinline__ void flag_st(volatile int* p, int v) { atomicExch((int*)p, v); }
+__device__ __forceinline__ long long flag_ld64(volatile long long* p) {
+  return (long long)atomicAdd((unsigned long long*)p, 0ull);
+}
+__device__ __forceinline__ void flag_st64(volatile long long* p, long long v) {
+  atomicExch((unsigned long long*)p, (unsigned long long)v);
+}
+
 __device__ __forceinline__ void tcg_final(const TcgState& s, int t, volatile int* sh_stop,
                                           TcgState* st) {
   if (t == 0) {
-    *sh_stop = 1;
+    flag_st(sh_stop, 1);
     if (blockIdx.x == 0) *st = s;
   }
 }
@@ -169,19 +181,20 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(const __grid_const
       const unsigned ph = (unsigned)((iq / S) & 1);
       bool go;
       while (!(go = mbar_try_wait(&empty[s], ph ^ 1u)))
-        if (sh_stop) break;
-      if (!go || sh_stop) break;
+        if (flag_ld(&sh_stop)) break;
+      if (!go || flag_ld(&sh_stop)) break;
       const int tt = (int)(iq % tiles);
       const int b = tt / nchunks, j = tt % nchunks;
       mbar_expect_tx(&fullQ[s], qbytes);
       tma_load_2d(stage_base + (size_t)s * stage_dbl, &tmq, j * kPCols, row_base + b * bh,
                   &fullQ[s], pol_q);
-      sh_iq = iq + 1;
+      flag_st64(&sh_iq, iq + 1);
     }
     // Q copies issued for tiles nobody will consume must land first
-    while (sh_ivdone < 0) {
+    long long ivdone;
+    while ((ivdone = flag_ld64(&sh_ivdone)) < 0) {
     }
-    for (long long tq = sh_ivdone; tq < iq; ++tq) mbar_wait(&fullQ[tq % S], (unsigned)((tq / S) & 1));
+    for (long long tq = ivdone; tq < iq; ++tq) mbar_wait(&fullQ[tq % S], (unsigned)((tq / S) & 1));
     return;
   }
   if (warp == kPW + 1) {
@@ -193,8 +206,8 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(const __grid_const
     for (;; ++iv) {
       const int kv = (int)(iv / tiles);
       bool stop = false;
-      while (!(iv < sh_iq && kv <= sh_vgen)) {
-        if (sh_stop) {
+      while (!(iv < flag_ld64(&sh_iq) && kv <= flag_ld(&sh_vgen))) {
+        if (flag_ld(&sh_stop)) {
           stop = true;
           break;
         }
@@ -216,7 +229,7 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(const __grid_const
       tma_load_1d(st, a.res + (int64_t)k0 * R, vb, &fullV[s], pol_v);
       tma_load_1d(st + kPCols * R, dprev + (int64_t)k0 * R, vb, &fullV[s], pol_v);
     }
-    sh_ivdone = iv;  // tiles ≥ iv got no r / δ copy (and were never consumed)
+    flag_st64(&sh_ivdone, iv);  // tiles ≥ iv got no r / δ copy (and were never consumed)
     return;
   }
 
@@ -439,7 +452,7 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tcg_persist(const __grid_const
     if (t == 0) {
       ts = s;
       __threadfence_block();
-      sh_vgen = k + 1;  // r_{k+1} and δ_k are final everywhere (barrier B)
+      flag_st(&sh_vgen, k + 1);  // r_{k+1} and δ_k are final everywhere (barrier B)
     }
   }
   // (the break paths leave `s` in the loop scope: CTA 0 re-derives nothing —
@@ -606,6 +619,10 @@ __global__ void __launch_bounds__(kPC, 1) k_tcg_persist_sym(const __grid_constan
   };
   auto issue_q = [&]() {
     const long long g = pr.iq;
+    // the slot's previous tile (g − S) must be released by every consumer
+    // warp (one completed phase of empty[s]; waited on every time, so no
+    // phase of the barrier goes unobserved)
+    if (g >= S) mbar_wait(&empty[g % S], (unsigned)(((g - S) / S) & 1));
     int J = pr.qJ, pend = pr.qpend;
     const int rt = geo(g, J, pend);
     pr.qJ = J;
@@ -798,8 +815,7 @@ __global__ void __launch_bounds__(kPC, 1) k_tcg_persist_sym(const __grid_constan
         // the next iteration's first tiles are issued after the assembly
         // (in flight during barriers they would queue ahead of its L2 reads)
         if (it + S < (long long)(k + 1) * T) {
-          mbar_wait(&empty[s], ph);
-          issue_q();
+          issue_q();  // waits for empty[s] (phase ph) itself
           if (pr.iv < pr.iq) issue_v(k);
         }
         if (pr.ic < (long long)(k + 1) * nseg) issue_col(k);
@@ -876,7 +892,7 @@ __global__ void __launch_bounds__(kPC, 1) k_tcg_persist_sym(const __grid_constan
     // -------------------------------------------------- α, boundary / τ, update
     const double dHd = csum(pa_mine, ws);  // its cbar also publishes yown
     XM_PSTAMP(7);
-    if (t == 0)  // Q prefetch of the next iteration (every warp has released every slot)
+    if (t == 0 && T > 0)  // Q prefetch of the next iteration (every warp has released every slot)
       while (pr.iq < it + S) issue_q();
     s.d_Hd = dHd;
     s.n_hvp += 1;

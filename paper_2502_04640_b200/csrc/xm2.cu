@@ -9,10 +9,16 @@
 //   radix sort         key = ~bits(res) (descending residual), stable over the
 //                      canonical index ⇒ ties by (landmark, frame) ascending
 //   k_xm2_drop         the first ⌊frac·E⌋ of that order are dropped
+//   k_xm2_useful       per frame: kept measurements of landmarks with ≥ 2 kept
+//                      measurements; k_xm2_determine (one thread, deficient
+//                      frames only) restores their dropped measurements,
+//                      smallest residual first, until each has 3 (C22b)
 //   k_cc_*_masked      label propagation over the kept measurements
 //   k_xm2_restore      one thread: Kruskal over the dropped list backwards
 //                      (smallest residual first) until the frames are in one
 //                      component — only runs when the kept graph is split
+//   k_xm2_prune        restored measurements whose landmark ends with one kept
+//                      measurement are dropped again (minimality, C22b)
 //   k_xm2_compact      kept measurements (canonical order) → the input arrays
 //                      of the rebuild, with their caller-side input indices
 #include "xm_internal.cuh"
@@ -56,6 +62,61 @@ __global__ void k_xm2_drop(int64_t E, int64_t nd, const uint32_t* __restrict__ o
   if (j < nd) keep[order[j]] = 0;
 }
 
+__global__ void k_xm2_rank(int64_t E, const uint32_t* __restrict__ order, int32_t* __restrict__ rank) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < E) rank[order[j]] = (int32_t)j;
+}
+__global__ void k_xm2_lmcount(int64_t E, const int32_t* __restrict__ lm, const int32_t* __restrict__ keep,
+                              int32_t* __restrict__ kcnt) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < E && keep[e]) atomicAdd(&kcnt[lm[e]], 1);
+}
+// per frame: 1 if it has fewer than min_obs kept measurements of landmarks with ≥ 2 kept
+__global__ void k_xm2_useful(int N, const int32_t* __restrict__ fr_off, const int32_t* __restrict__ fr_edge,
+                             const int32_t* __restrict__ lm, const int32_t* __restrict__ keep,
+                             const int32_t* __restrict__ kcnt, int min_obs, int32_t* __restrict__ deficient) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  int u = 0;
+  for (int q = fr_off[i]; q < fr_off[i + 1]; ++q) {
+    const int e = fr_edge[q];
+    u += (keep[e] && kcnt[lm[e]] >= 2) ? 1 : 0;
+  }
+  deficient[i] = u < min_obs ? 1 : 0;
+}
+// one thread: deficient frames in ascending order get dropped measurements
+// back, smallest residual (largest drop rank) first, until min_obs useful
+__global__ void k_xm2_determine(int N, const int32_t* __restrict__ fr_off, const int32_t* __restrict__ fr_edge,
+                                const int32_t* __restrict__ lm, const int32_t* __restrict__ rank,
+                                const int32_t* __restrict__ deficient, int min_obs, int32_t* __restrict__ keep,
+                                int32_t* __restrict__ restored, int32_t* __restrict__ kcnt) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  for (int i = 0; i < N; ++i) {
+    if (!deficient[i]) continue;
+    for (;;) {
+      int u = 0, best = -1, best_rank = -1;
+      for (int q = fr_off[i]; q < fr_off[i + 1]; ++q) {
+        const int e = fr_edge[q];
+        if (keep[e]) {
+          u += kcnt[lm[e]] >= 2 ? 1 : 0;
+        } else if (rank[e] > best_rank) {
+          best_rank = rank[e];
+          best = e;
+        }
+      }
+      if (u >= min_obs || best < 0) break;
+      keep[best] = 1;
+      restored[best] = 1;
+      kcnt[lm[best]] += 1;
+    }
+  }
+}
+__global__ void k_xm2_prune(int64_t E, const int32_t* __restrict__ lm, const int32_t* __restrict__ kcnt,
+                            const int32_t* __restrict__ restored, int32_t* __restrict__ keep) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < E && restored[e] && keep[e] && kcnt[lm[e]] == 1) keep[e] = 0;
+}
+
 __global__ void k_cc_init_m(int n, int32_t* parent) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v < n) parent[v] = v;
@@ -84,7 +145,8 @@ __global__ void k_cc_jump_m(int n, int32_t* parent) {
 __global__ void k_xm2_restore(int N, int M, int64_t nd, const int32_t* __restrict__ fr,
                               const int32_t* __restrict__ lm, const uint32_t* __restrict__ order,
                               const int32_t* __restrict__ label, int32_t* __restrict__ uf,
-                              uint8_t* __restrict__ hf, int32_t* __restrict__ keep, int64_t* out) {
+                              uint8_t* __restrict__ hf, int32_t* __restrict__ keep,
+                              int32_t* __restrict__ restored_flag, int64_t* out) {
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
   const int n = N + M;
   for (int v = 0; v < n; ++v) {
@@ -104,12 +166,14 @@ __global__ void k_xm2_restore(int N, int M, int64_t nd, const int32_t* __restric
   int64_t restored = 0;
   for (int64_t j = nd - 1; j >= 0 && comps > 1; --j) {  // smallest residual first
     const int e = (int)order[j];
+    if (keep[e]) continue;  // already back (determined-frame step)
     const int a = find(fr[e]), b = find(N + lm[e]);
     if (a == b) continue;
     const uint8_t fa = hf[a], fb = hf[b];
     uf[b] = a;
     hf[a] = fa | fb;
     keep[e] = 1;
+    restored_flag[e] = 1;
     ++restored;
     if (fa && fb) --comps;
   }
@@ -207,6 +271,26 @@ void xm2_device(xm_ctx* c, double frac, uint8_t* keep_user_dev, int64_t* n_dropp
   k_xm2_drop<<<ceil_div(E, T), T, 0, c->stream>>>(E, nd, ord.p, keep.p);
   XM_CHECK_LAUNCH();
   count_launch(c);
+  // determined frames (reading C22b)
+  constexpr int kMinObs = 3;
+  DBuf<int32_t>& rank = scratch_i32(c, "xm2_rank");
+  DBuf<int32_t>& restored = scratch_i32(c, "xm2_restored");
+  DBuf<int32_t>& kcnt = scratch_i32(c, "xm2_kcnt");
+  DBuf<int32_t>& defi = scratch_i32(c, "xm2_deficient");
+  rank.alloc(E);
+  restored.alloc(E);
+  kcnt.alloc(M);
+  defi.alloc(N);
+  XM_CUDA(cudaMemsetAsync(restored.p, 0, (size_t)E * 4, c->stream));
+  XM_CUDA(cudaMemsetAsync(kcnt.p, 0, (size_t)M * 4, c->stream));
+  k_xm2_rank<<<ceil_div(E, T), T, 0, c->stream>>>(E, ord.p, rank.p);
+  k_xm2_lmcount<<<ceil_div(E, T), T, 0, c->stream>>>(E, c->e_lm.p, keep.p, kcnt.p);
+  k_xm2_useful<<<ceil_div(N, T), T, 0, c->stream>>>(N, c->fr_off.p, c->fr_edge.p, c->e_lm.p, keep.p, kcnt.p,
+                                                   kMinObs, defi.p);
+  k_xm2_determine<<<1, 1, 0, c->stream>>>(N, c->fr_off.p, c->fr_edge.p, c->e_lm.p, rank.p, defi.p, kMinObs,
+                                          keep.p, restored.p, kcnt.p);
+  XM_CHECK_LAUNCH();
+  count_launch(c, 4);
   // connectivity of the kept graph (frames ∪ landmarks), then restoration
   DBuf<int32_t>& label = scratch_i32(c, "xm2_label");
   label.alloc(N + M);
@@ -231,7 +315,7 @@ void xm2_device(xm_ctx* c, double frac, uint8_t* keep_user_dev, int64_t* n_dropp
   DBuf<uint64_t>& outb = scratch_u64(c, "xm2_out");
   outb.alloc(2);
   k_xm2_restore<<<1, 1, 0, c->stream>>>(N, M, nd, c->e_fr.p, c->e_lm.p, ord.p, label.p, uf.p,
-                                        reinterpret_cast<uint8_t*>(hf.p), keep.p,
+                                        reinterpret_cast<uint8_t*>(hf.p), keep.p, restored.p,
                                         reinterpret_cast<int64_t*>(outb.p));
   XM_CHECK_LAUNCH();
   count_launch(c);
@@ -239,8 +323,12 @@ void xm2_device(xm_ctx* c, double frac, uint8_t* keep_user_dev, int64_t* n_dropp
   XM_CUDA(cudaMemcpyAsync(h_out, outb.p, 16, cudaMemcpyDeviceToHost, c->stream));
   sync(c);
   if (h_out[1] != 1) throw Error(XM_EDISCONNECTED, "XM²: graph disconnected even with every measurement");
-  if (n_dropped) *n_dropped = nd - h_out[0];
-  if (n_restored) *n_restored = h_out[0];
+  // minimality: restored leaves go again
+  XM_CUDA(cudaMemsetAsync(kcnt.p, 0, (size_t)M * 4, c->stream));
+  k_xm2_lmcount<<<ceil_div(E, T), T, 0, c->stream>>>(E, c->e_lm.p, keep.p, kcnt.p);
+  k_xm2_prune<<<ceil_div(E, T), T, 0, c->stream>>>(E, c->e_lm.p, kcnt.p, restored.p, keep.p);
+  XM_CHECK_LAUNCH();
+  count_launch(c, 2);
   const int32_t* orig = c->orig_in.p ? c->orig_in.p : nullptr;
   if (keep_user_dev) {
     XM_CUDA(cudaMemsetAsync(keep_user_dev, 0, (size_t)c->E_user, c->stream));
@@ -256,6 +344,8 @@ void xm2_device(xm_ctx* c, double frac, uint8_t* keep_user_dev, int64_t* n_dropp
   int32_t Ek = 0;
   XM_CUDA(cudaMemcpyAsync(&Ek, d_total, 4, cudaMemcpyDeviceToHost, c->stream));
   sync(c);
+  if (n_dropped) *n_dropped = E - Ek;
+  if (n_restored) *n_restored = nd - (E - Ek);
   DBuf<int32_t>& nfr = scratch_i32(c, "xm2_fr");
   DBuf<int32_t>& nlm = scratch_i32(c, "xm2_lm");
   DBuf<double>& npts = scratch_f64(c, "xm2_pts");

@@ -575,7 +575,7 @@ xm_status xm_create(xm_ctx** out, int device, int rank, int world, const void* n
   if (std::getenv("XM_NO_FUSED_TCG")) c->fused_tcg = false;
   if (std::getenv("XM_NO_PERSIST_TCG")) c->persist_tcg = false;
   if (const char* e = std::getenv("XM_GEMM_TILE"))
-    c->gemm_tile = std::string(e) == "bk16" ? 1 : std::string(e) == "mid" ? 2 : 0;
+    c->gemm_tile = std::string(e) == "bk16" ? 1 : std::string(e) == "mid" ? 2 : std::string(e) == "w8" ? 3 : 0;
   if (const char* e = std::getenv("XM_TRSM_SB")) c->trsm_sb = std::max(64, atoi(e) / 64 * 64);
   if (std::getenv("XM_SYM_TCG")) c->persist_sym = 1;
   if (std::getenv("XM_NO_SYM_TCG")) c->persist_sym = -1;
@@ -887,7 +887,16 @@ xm_status xm_xm2(xm_ctx* c, double drop_fraction, uint8_t* keep, int64_t* n_drop
     DBuf<uint32_t>& kb = scratch_u32(c, "xm2_user_keep");
     kb.alloc((size_t)c->E_user / 4 + 2);
     uint8_t* kd = reinterpret_cast<uint8_t*>(kb.p);
-    xm2_device(c, drop_fraction, kd, n_dropped, n_restored);
+    try {
+      xm2_device(c, drop_fraction, kd, n_dropped, n_restored);
+    } catch (...) {
+      // the measurement mapping / canonical arrays may be half-rebuilt: no Q
+      // to solve on until the next xm_build_Q (xm.h: a failed call must not
+      // leave a context whose stage and data disagree)
+      c->stage = 0;
+      c->have_recovery = false;
+      throw;
+    }
     reset_after_new_Q(c);
     if (keep) copy_out(c, keep, kd, (size_t)c->E_user);
     sync(c);

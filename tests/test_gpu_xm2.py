@@ -77,10 +77,19 @@ def test_xm2_parity(xm, case):
         sc0 = make_scene(150, 3000, "unordered", seed=11, track_mean=8.0, sigma_u=1e-3, sigma_d=0.01)
         sc, bad = corrupt(sc0, 0.03, seed=11)
         frac = 0.1
-    else:  # sparse road scene where dropping half the measurements splits the graph
-        sc = make_scene(12, 60, "road", seed=3, sigma_u=1e-3, sigma_d=0.01, track_mean=3.0)
+    else:  # sparse road scene where dropping half the measurements splits the graph;
+        # random weights: the two residuals of a two-view landmark differ (no ties)
+        sc = make_scene(12, 60, "road", seed=3, sigma_u=1e-3, sigma_d=0.01, track_mean=3.0,
+                        weights="uniform")
         frac = 0.5
-    first, okeep, ores, second = xo.xm2(sc, drop_fraction=frac)
+    if case == "restoration":   # selection + rebuild only (half the measurements dropped)
+        dm1, st1, osol, _ = xo.solve(sc)
+        ores = xo.edge_residuals(sc.frame, sc.landmark, sc.pts, sc.w, osol)
+        okeep = xo.xm2_select(sc.N, sc.M, sc.frame, sc.landmark, ores, frac)
+        k = okeep
+        second = (xo.build_Q(sc.N, sc.M, sc.frame[k], sc.landmark[k], sc.pts[k], sc.w[k]),)
+    else:
+        first, okeep, ores, second = xo.xm2(sc, drop_fraction=frac)
     ctx, st, info, sol = _gpu_first(xm, sc)
     with ctx:
         assert st == 0
@@ -92,22 +101,22 @@ def test_xm2_parity(xm, case):
         assert (~keep).sum() == (~okeep).sum()
         a, b = np.sort(ores[~keep]), np.sort(ores[~okeep])
         assert np.all(np.abs(a - b) <= 1e-9 * np.maximum(np.abs(b), 1e-12)), (a, b)
+        assert np.array_equal(keep, okeep)           # no ties near the cut in these scenes
         if case != "restoration":
-            assert np.array_equal(keep, okeep)       # no ties near the cut here
             assert keep[bad].mean() < 0.2            # the outliers are among the dropped
         assert xo.connected_components(sc.N, sc.M, sc.frame[keep], sc.landmark[keep]) == 1
-        # the rebuilt Q is the data matrix of the kept measurements: equal to
-        # the oracle's second Q when the kept sets coincide; otherwise (equal
-        # residuals ordered differently) the two differ in tied measurements only
+        # reading C22b: every frame keeps ≥ 3 measurements of landmarks seen ≥ 2
+        # times, or (best effort) all of its measurements
+        kc = np.bincount(sc.landmark[keep], minlength=sc.M)
+        for i in range(sc.N):
+            mine = sc.frame == i
+            assert np.sum(keep & mine & (kc[sc.landmark] >= 2)) >= 3 or keep[mine].all() or \
+                np.all(keep[mine] | (kc[sc.landmark[mine]] == 0)), i
+        # the rebuilt Q is the data matrix of the kept measurements (= the oracle's second Q)
         Qg = ctx.Q_rows(0, 3 * sc.N)
-        if np.array_equal(keep, okeep):
-            dmk = second[0]
-            assert np.linalg.norm(Qg - dmk.Q) <= 1e-10 * dmk.normF
-        assert np.allclose(Qg, Qg.T, rtol=0, atol=1e-12 * np.abs(Qg).max())
-        if case != "outliers":
-            # a frame whose every measurement ranked in the dropped set comes
-            # back with the single restored one: underdetermined, the second
-            # optimum collapses its scale (C18) — selection and rebuild only
+        dmk = second[0]
+        assert np.linalg.norm(Qg - dmk.Q) <= 1e-10 * dmk.normF
+        if case == "restoration":
             return
         st2, info2 = ctx.solve(r0=3)
         cert2 = ctx.certify()

@@ -838,3 +838,37 @@ def test_scale_reg_dual_value_and_Z_by_convexity_identity():
         gap = xo.cost(dm.Q, Yp, lam) - np.vdot(Yp, Z @ Yp) - cert.rho_dual
         breg = lam * float(np.sum((ap[1:] - a[1:]) ** 2))
         assert abs(gap - breg) <= 1e-9 * (abs(xo.cost(dm.Q, Yp, lam)) + 1.0), (k, gap, breg)
+
+
+def test_xm2_select_keeps_every_frame_determined_and_minimal():
+    """Readings C22b: after the drop, a frame keeps ≥ 3 measurements of
+    landmarks with ≥ 2 kept measurements (pose + scale determined by ≥ 3
+    shared points), got back smallest residual first; restored measurements
+    whose landmark ends with one kept measurement are dropped again (they add
+    nothing to Q, F10 — S:518 minimality)."""
+    sc = make_scene(12, 300, "unordered", seed=8, vis_prob=0.5)
+    fr, lm = sc.frame.astype(np.int64), sc.landmark.astype(np.int64)
+    E = len(fr)
+    rng = np.random.default_rng(0)
+    res = rng.uniform(0.0, 1.0, E)
+    victim = 5
+    mine = np.nonzero(fr == victim)[0]
+    res[mine] = 10.0 + rng.uniform(0.0, 1.0, mine.size)      # all of frame 5 ranks worst
+    # add private (single-view) landmarks of the victim with the worst residuals of all
+    extra = 4
+    fr = np.concatenate([fr, np.full(extra, victim)])
+    lm = np.concatenate([lm, sc.M + np.arange(extra)])
+    res = np.concatenate([res, 100.0 + np.arange(extra)])
+    M = sc.M + extra
+    keep = xo.xm2_select(sc.N, M, fr, lm, res, 0.1)
+    kcnt = np.bincount(lm[keep], minlength=M)
+    for i in range(sc.N):
+        useful = np.sum(keep & (fr == i) & (kcnt[lm] >= 2))
+        assert useful >= 3, (i, useful)
+    # the victim got back exactly its 3 smallest-residual shared measurements
+    back = mine[keep[mine]]
+    assert back.size == 3
+    assert set(back) == set(mine[np.argsort(res[mine])[:3]])
+    # no kept measurement of a private landmark (each would be a single-view leaf)
+    assert not keep[E:].any()
+    assert xo.connected_components(sc.N, M, fr[keep], lm[keep]) == 1
