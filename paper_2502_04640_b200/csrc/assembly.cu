@@ -891,7 +891,9 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
   const int T = 256;
   const bool verbose = std::getenv("XM_VERBOSE") != nullptr;
   double tph = 0.0;
+  NvtxRange nvtx_all("build_Q");
   auto phase = [&](const char* nm) {
+    nvtxMarkA(nm);
     if (!verbose) return;
     sync(c);
     double t = std::chrono::duration<double, std::milli>(

@@ -394,7 +394,11 @@ void certify_current(xm_ctx* c, double* lambda, int* steps) {
   if (c->world == 1 && c->opt.cert_cholesky) {
     int budget = std::min(c->opt.lanczos_max, std::max(32, c->n / 72));
     PhaseClock pc(c);
-    bool conv = lanczos(c, tol, budget, lambda, steps, c->cert_v.p);
+    bool conv;
+    {
+      NvtxRange r_("lanczos(Z)");
+      conv = lanczos(c, tol, budget, lambda, steps, c->cert_v.p);
+    }
     pc.lap(6);
     double low_eps = 0.0;
     DBuf<double>& U = scratch_f64(c, "zw_U");
@@ -619,6 +623,7 @@ xm_status xm_build_Q(xm_ctx* c, int32_t N, int32_t M, int64_t E, const int32_t* 
   if (!c) return XM_EINVAL;
   if (!frame || !landmark || !lifted_pts) return XM_EINVAL;
   return guard(c, [&] {
+    NvtxRange nvtx_("xm_build_Q");
     double t0 = now_ms();
     c->stage = 0;
     c->orig_in.release();  // the caller's input order
@@ -641,6 +646,7 @@ __global__ void k_copy_rows(int rows, int n, const double* __restrict__ src, int
 xm_status xm_set_Q(xm_ctx* c, int32_t N, const double* Q_full) {
   if (!c || N < 1 || !Q_full) return XM_EINVAL;
   return guard(c, [&] {
+    NvtxRange nvtx_("xm_set_Q");
     c->N = N;
     c->M = 0;
     c->E = 0;
@@ -683,6 +689,7 @@ xm_status xm_solve(xm_ctx* c, int32_t r0, double tol, xm_solve_info* info) {
   if (!c) return XM_EINVAL;
   xm_status result = XM_OK;
   xm_status st = guard(c, [&] {
+    NvtxRange nvtx_("xm_solve");
     require_stage(c, 1);
     double t0 = now_ms();
     c->info = xm_solve_info{};
@@ -768,6 +775,7 @@ xm_status xm_solve(xm_ctx* c, int32_t r0, double tol, xm_solve_info* info) {
 xm_status xm_certify(xm_ctx* c, xm_certificate* out, double* min_eigvec) {
   if (!c) return XM_EINVAL;
   return guard(c, [&] {
+    NvtxRange nvtx_("xm_certify");
     require_stage(c, 1);
     if (c->r == 0) throw Error(XM_ESTATE, "no factor: call xm_solve or xm_set_factor first");
     double t0 = now_ms();
@@ -843,6 +851,7 @@ xm_status xm_round_recover(xm_ctx* c, double* R, double* s, double* t, double* p
                            int32_t* n_flipped) {
   if (!c) return XM_EINVAL;
   return guard(c, [&] {
+    NvtxRange nvtx_("xm_round_recover");
     require_stage(c, 1);
     if (c->r == 0) throw Error(XM_ESTATE, "no factor");
     double t0 = now_ms();
@@ -864,6 +873,7 @@ xm_status xm_round_recover(xm_ctx* c, double* R, double* s, double* t, double* p
 xm_status xm_edge_residuals(xm_ctx* c, double* res) {
   if (!c || !res) return XM_EINVAL;
   return guard(c, [&] {
+    NvtxRange nvtx_("xm_edge_residuals");
     require_stage(c, 1);
     if (c->r == 0) throw Error(XM_ESTATE, "no factor");
     if (!c->have_recovery) throw Error(XM_ESTATE, "no view graph (Q was set directly)");
@@ -879,6 +889,7 @@ xm_status xm_edge_residuals(xm_ctx* c, double* res) {
 xm_status xm_xm2(xm_ctx* c, double drop_fraction, uint8_t* keep, int64_t* n_dropped, int64_t* n_restored) {
   if (!c || !(drop_fraction >= 0.0 && drop_fraction < 1.0)) return XM_EINVAL;
   return guard(c, [&] {
+    NvtxRange nvtx_("xm_xm2");
     require_stage(c, 1);
     if (c->r == 0) throw Error(XM_ESTATE, "no factor");
     if (!c->have_recovery) throw Error(XM_ESTATE, "no view graph (Q was set directly)");
@@ -979,6 +990,7 @@ xm_status xm_tcg(xm_ctx* c, const double* Y, int32_t r, double Delta, int32_t pa
   if (!c || !Y || !eta || r < 1 || r > XM_MAX_R || !(Delta > 0.0) || path < 0 || path > 4)
     return XM_EINVAL;
   return guard(c, [&] {
+    NvtxRange nvtx_("xm_tcg");
     require_stage(c, 1);
     const bool f0 = c->fused_tcg, p0 = c->persist_tcg;
     const int s0 = c->persist_sym;

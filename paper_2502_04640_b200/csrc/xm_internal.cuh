@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "../../include/xm.h"
+#include <nvtx3/nvToolsExt.h>
 
 #define XM_MAX_R 12
 
@@ -34,6 +35,14 @@ struct Error : public std::runtime_error {
   } while (0)
 
 #define XM_CHECK_LAUNCH() XM_CUDA(cudaGetLastError())
+
+// NVTX range for profilers (nsys / ncu --nvtx); no-op without an attached tool
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // ---------------------------------------------------------------- device buffers
 template <typename T>
