@@ -180,11 +180,14 @@ xm_status xm_nccl_unique_id(void* out128);
 
 /* Row shard of `rank` among `world` ranks.  Host-only: no
  * device work, callable without a GPU.  Rank q owns frames [*f0, *f1) ⇒ Q rows
- * [3·f0, 3·f1): contiguous ranges of nfpr = ⌈N/world⌉ frames
- * (*frames_per_rank, may be NULL); trailing ranks may be short or empty.
- * Replicated n×r vectors are all-gathered in a padded layout of world·3·nfpr
- * rows (rank q's shard at row 3·q·nfpr), whose first n rows are the natural
- * row-major order.  XM_EINVAL on N < 1, world < 1 or rank ∉ [0, world). */
+ * [3·f0, 3·f1), and stores only their lower trapezoid (columns ≤ row): the
+ * band layout that composes row sharding with the symmetric (lower-triangle)
+ * stream.  Bands are contiguous, start at F_q = N·√(q/world) rounded to a
+ * multiple of 32 frames (equal lower-triangle areas ⇒ equal Q bytes per
+ * product on every rank); some may be empty.  *frames_per_rank (may be NULL)
+ * = the largest band.  Each product is one all-reduce of the ranks' n×r
+ * partials (row parts of the band, column parts above it).  XM_EINVAL on
+ * N < 1, world < 1 or rank ∉ [0, world). */
 xm_status xm_shard_rows(int32_t N, int32_t world, int32_t rank, int32_t* f0, int32_t* f1,
                         int32_t* frames_per_rank);
 
@@ -242,7 +245,9 @@ xm_status xm_xm2(xm_ctx* ctx, double drop_fraction, uint8_t* keep, int64_t* n_dr
 /* S's co-visibility BSR pattern (H3): rowptr N+1 (int64), colidx nnzb (int32,
  * sorted per row).  Call with colidx == NULL to query *nnzb. */
 xm_status xm_get_S_pattern(xm_ctx* ctx, int64_t* rowptr, int32_t* colidx, int64_t* nnzb);
-/* Rows [row0, row0+nrows) of Q (this rank must own them): nrows × n. */
+/* Rows [row0, row0+nrows) of Q (this rank must own them): nrows × n.  world > 1
+ * after xm_build_Q: entries right of the diagonal are not stored (band
+ * layout, xm_shard_rows) and come back as NaN. */
 xm_status xm_get_Q_rows(xm_ctx* ctx, int32_t row0, int32_t nrows, double* out);
 /* Replace Q by caller data (full n×n, row-major); this rank keeps its rows.
  * N is implied by n = 3N.  Allows parity tests on an identical Q. */

@@ -863,8 +863,10 @@ void mirror_lower(xm_ctx* c, double* Q, int n, int64_t ldq) {
   count_launch(c);
 }
 
+// Σ Q_ij² over this rank's rows; band layout (row0 ≥ 0): only the lower
+// trapezoid is stored, so Σ = Σ_{j<i} 2Q_ij² + Σ_{j=i} Q_ii² over global rows i
 __global__ void k_sumsq_rows(const double* __restrict__ Q, int rows, int n, int64_t ldq,
-                             double* __restrict__ partials) {
+                             double* __restrict__ partials, int row0) {
   __shared__ double sh[256];
   double acc = 0.0;
   int64_t tot = (int64_t)rows * n;
@@ -872,6 +874,10 @@ __global__ void k_sumsq_rows(const double* __restrict__ Q, int rows, int n, int6
        t += (int64_t)gridDim.x * blockDim.x) {
     int i = (int)(t / n), j = (int)(t % n);
     double v = Q[(int64_t)i * ldq + j];
+    if (row0 >= 0) {
+      const int gi = row0 + i;
+      v = (j < gi) ? v * 1.4142135623730951 : (j == gi ? v : 0.0);
+    }
     acc = fma(v, v, acc);
   }
   sh[threadIdx.x] = acc;
@@ -1138,11 +1144,16 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
     dense_trsm_lower_left(c, c->L.p, N - 1, c->ldk, U.p, c->ldk, c->G.p, n, c->ldq);
     phase("trsm");
     const double* Gown = c->G.p + c->row0;  // columns of this rank's rows
-    bool lower = (c->world == 1);
     // Q = S − GᵀG: Q[i][j] −= Σ_k G[k][i] G[k][j]
-    dgemm_tn(c, lower, c->nrows, n, N - 1, -1.0, Gown, c->ldq, c->G.p, c->ldq, 1.0, c->Q.p,
-             c->ldq);
-    if (lower) mirror_lower(c, c->Q.p, n, c->ldq);
+    if (c->world == 1) {  // lower triangle + mirror: Q exactly symmetric, full storage
+      dgemm_tn(c, true, n, n, N - 1, -1.0, Gown, c->ldq, c->G.p, c->ldq, 1.0, c->Q.p, c->ldq);
+      mirror_lower(c, c->Q.p, n, c->ldq);
+    } else if (c->nrows > 0) {  // the band's lower trapezoid: columns < row0, then its diagonal square
+      dgemm_tn(c, false, c->nrows, c->row0, N - 1, -1.0, Gown, c->ldq, c->G.p, c->ldq, 1.0, c->Q.p,
+               c->ldq);
+      dgemm_tn(c, true, c->nrows, c->nrows, N - 1, -1.0, Gown, c->ldq, Gown, c->ldq, 1.0,
+               c->Q.p + c->row0, c->ldq);
+    }
   } else if (c->world == 1) {
     mirror_lower(c, c->Q.p, n, c->ldq);
   }
@@ -1152,7 +1163,8 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
   {
     DBuf<double>& part = scratch_f64(c, "normq_part");
     part.alloc(kDotBlocks);
-    k_sumsq_rows<<<kDotBlocks, 256, 0, c->stream>>>(c->Q.p, c->nrows, n, c->ldq, part.p);
+    k_sumsq_rows<<<kDotBlocks, 256, 0, c->stream>>>(c->Q.p, c->nrows, n, c->ldq, part.p,
+                                                    c->world > 1 ? c->row0 : -1);
     XM_CHECK_LAUNCH();
     c->scal.alloc(64);
     reduce_partials(c, part.p, kDotBlocks, 1, c->scal.p);

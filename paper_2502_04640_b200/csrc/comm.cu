@@ -1,9 +1,11 @@
 // comm.cu — NCCL over NVLink 5 / NVSwitch for the row-sharded path.
 //
-// The only exchange of the solve is the all-gather of the Q·V row shards after
-// every product (one per HVP / Δf / Lanczos step); all O(N·r) per-camera work
-// and every dot product then run redundantly (and bitwise identically) on the
-// replicated full vectors, so no all-reduce is needed in the inner loop.
+// The only exchange of the solve is ONE all-reduce of the n×r partial products
+// after every product (one per HVP / Δf / Lanczos step): each rank streams the
+// lower trapezoid of its band of Q rows (row parts of its rows, column parts of
+// the rows above — spmm.cu spmm_full); all O(N·r) per-camera work and every
+// dot product then run redundantly (and bitwise identically) on the replicated
+// full vectors, so the inner loop needs no other collective.
 // NCCL is loaded with dlopen only when world > 1 (single-GPU runs do not
 // depend on it); the communicator is bootstrapped from an ncclUniqueId that
 // the caller broadcasts (torch.distributed in the Python harness).
@@ -140,26 +142,6 @@ void nccl_destroy(xm_ctx* c) {
   c->nccl_comm = nullptr;
 }
 
-void nccl_allgather(xm_ctx* c, const double* send, double* recv, size_t count_per_rank) {
-  if (c->loop) {
-    LoopGroup* g = static_cast<LoopGroup*>(c->loop);
-    XM_CUDA(cudaStreamSynchronize(c->stream));  // our shard is complete
-    g->ptr[c->rank] = send;
-    g->barrier();                               // every shard is complete
-    for (int q = 0; q < c->world; ++q) {
-      double* dst = recv + (size_t)q * count_per_rank;
-      if (g->ptr[q] != dst)
-        XM_CUDA(cudaMemcpyAsync(dst, g->ptr[q], count_per_rank * 8, cudaMemcpyDefault, c->stream));
-    }
-    XM_CUDA(cudaStreamSynchronize(c->stream));
-    g->barrier();                               // nobody overwrites a shard still being read
-    return;
-  }
-  check(g_nccl.AllGather(send, recv, count_per_rank, ncclFloat64, (ncclComm_t)c->nccl_comm,
-                         c->stream),
-        "ncclAllGather");
-}
-
 void nccl_allreduce_sum(xm_ctx* c, double* buf, size_t count) {
   if (c->world <= 1) return;
   if (c->loop) {
@@ -179,15 +161,6 @@ void nccl_allreduce_sum(xm_ctx* c, double* buf, size_t count) {
   check(g_nccl.AllReduce(buf, buf, count, ncclFloat64, ncclSum, (ncclComm_t)c->nccl_comm,
                          c->stream),
         "ncclAllReduce");
-}
-
-// Row shards are contiguous frame ranges of equal size nfpr (the last one
-// padded), so gathering the padded shards in rank order yields the natural
-// row-major n×r layout (vectors are allocated with world·3·nfpr rows).
-void allgather_rows(xm_ctx* c, double* full, int r) {
-  if (c->world <= 1) return;
-  size_t per = (size_t)3 * c->nfpr * r;
-  nccl_allgather(c, full + (size_t)c->rank * per, full, per);
 }
 
 }  // namespace xm

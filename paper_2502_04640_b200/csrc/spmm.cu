@@ -496,8 +496,14 @@ bool tcg_fused_supported(xm_ctx* c, int r) {
 // writes η, Hη, r, δ (+ Λ): 8·n·n + 9·8·n·r + 48·N.
 static double alg_bytes(xm_ctx* c, int r, int mode) {
   const double n = c->n;
-  const double qb = (mode != EPI_TCG && spmm_sym_supported(c, r)) ? 8.0 * n * (n + 1) / 2
-                                                                  : 8.0 * (double)c->nrows * n;
+  double qb;
+  if (c->world > 1) {  // this rank's band: rows [a, b), columns ≤ row (lower trapezoid)
+    const double a = c->row0, b = (double)c->row0 + c->nrows;
+    qb = 8.0 * ((b * (b + 1) - a * (a + 1)) / 2);
+    return qb + 8.0 * n * r + 8.0 * n * r;  // V in, the full-length partial out
+  }
+  qb = (mode != EPI_TCG && spmm_sym_supported(c, r)) ? 8.0 * n * (n + 1) / 2
+                                                     : 8.0 * (double)c->nrows * n;
   if (mode == EPI_TCG) return qb + 9.0 * 8.0 * n * r + 48.0 * c->N;
   return qb + 8.0 * n * r + 8.0 * (double)c->nrows * r;
 }
@@ -561,13 +567,52 @@ void spmm(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep_in)
   c->stats.spmm_rows = c->nrows;
 }
 
-// Full product into out (replicated n × r): this rank's rows, then all-gather.
+__global__ void k_pack_cols(int64_t n, int r, int c0, int w, const double* __restrict__ V,
+                            double* __restrict__ out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n * w) return;
+  const int64_t i = t / w;
+  out[t] = V[i * r + c0 + (int)(t - i * w)];
+}
+__global__ void k_unpack_cols(int64_t n, int r, int c0, int w, const double* __restrict__ in,
+                              double* __restrict__ out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n * w) return;
+  const int64_t i = t / w;
+  out[i * r + c0 + (int)(t - i * w)] = in[t];
+}
+
+// Full product into out (replicated n × r).  One GPU: one launch.  world > 1
+// (band layout, SURVEY §8(e) composed with the symmetric stream): every rank
+// streams the lower trapezoid of its band with the lower-triangle kernel,
+// which yields the band rows' row parts and the column parts of every row
+// above (a full-length n × r partial, zero below the band); ONE all-reduce of
+// those partials (n·r·8 bytes, ≈ 1 MB at E) replaces the all-gather of full-row
+// shards and halves each rank's Q bytes.  r > 5: column groups of ≤ 5.
 void spmm_full(xm_ctx* c, const double* V, int r, double* out_full, const int* stop) {
   SpmmEpiArgs ep{};
-  ep.out = out_full;
   ep.stop = stop;
-  spmm(c, V, r, EPI_STORE, ep);
-  if (c->world > 1) allgather_rows(c, out_full, r);
+  if (c->world == 1 || r <= 5) {
+    ep.out = out_full;
+    spmm(c, V, r, EPI_STORE, ep);
+  } else {
+    const int64_t n = c->n;
+    DBuf<double>& pv = scratch_f64(c, "band_pack_v");
+    DBuf<double>& po = scratch_f64(c, "band_pack_o");
+    pv.alloc((size_t)n * 5 + 64);
+    po.alloc((size_t)n * 5 + 64);
+    for (int c0 = 0; c0 < r; c0 += 5) {
+      const int w = std::min(5, r - c0);
+      k_pack_cols<<<ceil_div(n * w, 256), 256, 0, c->stream>>>(n, r, c0, w, V, pv.p);
+      XM_CHECK_LAUNCH();
+      ep.out = po.p;
+      spmm(c, pv.p, w, EPI_STORE, ep);
+      k_unpack_cols<<<ceil_div(n * w, 256), 256, 0, c->stream>>>(n, r, c0, w, po.p, out_full);
+      XM_CHECK_LAUNCH();
+      count_launch(c, 2);
+    }
+  }
+  if (c->world > 1) nccl_allreduce_sum(c, out_full, (size_t)c->n * r);
 }
 
 // Accumulate the CUDA-event time of every profiled SpMM launch that actually

@@ -157,7 +157,8 @@ __device__ __forceinline__ void warp_rows_reduce(double (&a)[RP][R], int lane) {
 // segments of one panel are consecutive — fixed summation order for the finish).
 struct SymPlan {
   int n = 0, G = 0, TRt = 0, TCb = 0, S = 0;
-  int64_t W = 0;
+  int rt_a = 0, rt_b = 0, row0 = 0;  // this rank's band of row tiles (one GPU: all of them)
+  int64_t W = 0, W_full = 0;         // tiles of the band / of the whole lower triangle
   const void* qptr = nullptr;  // Q the tensor map was encoded for
   int64_t ldq = 0;
   CUtensorMap tmq;
@@ -172,7 +173,11 @@ static SymPlan& sym_plan(xm_ctx* c) {
   int sms = 148;
   XM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
   const int n = c->n, G = std::min(148, sms);
-  if (p.n == n && p.G == G && p.pbase.p && p.qptr == c->Q.p && p.ldq == c->ldq) return p;
+  // band of row tiles: [row0, row0 + nrows) is frame- and tile-aligned (32 frames) on world > 1
+  const int rt_a = c->row0 / TR;
+  const int rt_b = (c->row0 + c->nrows >= n) ? ceil_div(n, TR) : (c->row0 + c->nrows) / TR;
+  const bool same_band = p.rt_a == rt_a && p.rt_b == rt_b && p.row0 == c->row0;
+  if (p.n == n && p.G == G && p.pbase.p && p.qptr == c->Q.p && p.ldq == c->ldq && same_band) return p;
   // Q tensor map: dims {n columns, n rows}, row pitch ldq·8 B, box BC × TR,
   // OOB → zero fill (rows / columns ≥ n read as 0)
   {
@@ -186,7 +191,7 @@ static SymPlan& sym_plan(xm_ctx* c) {
       return f;
     }();
     if (!encode) throw Error(XM_ECUDA, "cuTensorMapEncodeTiled unavailable");
-    cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)n};
+    cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)std::max(c->nrows, 1)};  // local rows
     cuuint64_t strides[1] = {(cuuint64_t)c->ldq * 8};
     cuuint32_t box[2] = {(cuuint32_t)BC, (cuuint32_t)TR};
     cuuint32_t estr[2] = {1, 1};
@@ -197,14 +202,21 @@ static SymPlan& sym_plan(xm_ctx* c) {
     p.qptr = c->Q.p;
     p.ldq = c->ldq;
   }
-  if (p.n == n && p.G == G && p.pbase.p) return p;
+  if (p.n == n && p.G == G && p.pbase.p && same_band) return p;
   p.n = n;
   p.G = G;
   p.TRt = ceil_div(n, TR);
   p.TCb = ceil_div(n, BC);
+  p.rt_a = rt_a;
+  p.rt_b = rt_b;
+  p.row0 = c->row0;
+  // panel J: row tiles max(8J, rt_a) … rt_b − 1 of the band (none once 8J ≥ rt_b)
   std::vector<int> pb(p.TCb + 1, 0);
-  for (int J = 0; J < p.TCb; ++J) pb[J + 1] = pb[J] + (p.TRt - kDiagTiles * J);
+  for (int J = 0; J < p.TCb; ++J)
+    pb[J + 1] = pb[J] + std::max(0, rt_b - std::max(kDiagTiles * J, rt_a));
   p.W = pb[p.TCb];
+  p.W_full = 0;
+  for (int J = 0; J < p.TCb; ++J) p.W_full += p.TRt - kDiagTiles * J;
   std::vector<int> segbase(G + 1, 0), segpanel;
   for (int cta = 0; cta < G; ++cta) {
     const int64_t t0 = (int64_t)cta * p.W / G, t1 = (int64_t)(cta + 1) * p.W / G;
@@ -245,7 +257,8 @@ struct SymCfg {
 
 template <int R, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
-    const __grid_constant__ CUtensorMap tmq, int N, int n, int TRt, int TCb, int64_t W,
+    const __grid_constant__ CUtensorMap tmq, int N, int n, int rt_a, int rt_b, int row0, int TCb,
+    int64_t W,
     const int* __restrict__ pbase, const int* __restrict__ segbase, const int* __restrict__ colptr,
     const double* __restrict__ V, double* __restrict__ rowpart, double* __restrict__ colpart,
     GridBar* __restrict__ gbar, SpmmEpiArgs ep) {
@@ -288,13 +301,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
       ++pJ;
       ppend = pbase[pJ + 1];
     }
-    const int rt = kDiagTiles * pJ + (int)(t - pbase[pJ]);  // row tile
+    const int rt = max(kDiagTiles * pJ, rt_a) + (int)(t - pbase[pJ]);  // row tile (global)
     const int s = it_load % kStages;
     const int ni = min(TR, n - rt * TR);
     const unsigned bv = (unsigned)(((ni * R + 1) & ~1) * 8);
     bar_expect(&full[s], (unsigned)kTileBytes + bv);
     double* st = stages + (size_t)s * kStageDoubles;
-    tma_tile(st, &tmq, pJ * BC, rt * TR, &full[s], pq);
+    tma_tile(st, &tmq, pJ * BC, rt * TR - row0, &full[s], pq);  // local row of this rank's Q
     bulk_g2s(st + TR * BC, V + (int64_t)rt * TR * R, bv, &full[s], pv);
   };
   const int ntiles = (int)(t1 - t0);
@@ -395,8 +408,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
           }
         ++seg;
       }
-      const int pt = (int)(t - pbase[J]);  // tile index within the panel
-      const int rt = kDiagTiles * J + pt;
+      const int rt = max(kDiagTiles * J, rt_a) + (int)(t - pbase[J]);  // row tile (global)
+      const int pt = rt - kDiagTiles * J;  // tile index within the full panel (< 8: diagonal block)
       const int s = it % kStages;
       bar_wait(&full[s], (unsigned)((it / kStages) & 1));
       const double* st = stages + (size_t)s * kStageDoubles;
@@ -442,7 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
     const int Jc = row / BC, m = row % BC;
     const double* p = rowpart + (rtile_base(K) * TR + l) * R + cc;
     double acc = 0.0;
-    int q = 0;
+    int q = (K >= rt_a && K < rt_b) ? 0 : Jc + 1;  // row parts exist for the band's rows only
     for (; q + 4 <= Jc + 1; q += 4) {  // 4 loads in flight, summed in order
       const double a0 = p[(int64_t)q * TR * R], a1 = p[(int64_t)(q + 1) * TR * R];
       const double a2 = p[(int64_t)(q + 2) * TR * R], a3 = p[(int64_t)(q + 3) * TR * R];
@@ -527,8 +540,9 @@ void sym_plan_destroy(xm_ctx* c) {
 // full-row kernel below N = 4000 (tcg_fullrow_ok), where one fused launch per
 // TR step beats a three-kernel iteration around this one.
 bool spmm_sym_supported(xm_ctx* c, int r) {
-  if (c->world != 1 || r < 1 || r > 5 || c->opt.spmm_kernel == 1) return false;
-  return true;
+  if (r < 1 || r > 5) return false;
+  if (c->world > 1) return true;  // the band layout stores only the lower trapezoid
+  return c->opt.spmm_kernel != 1;
 }
 
 bool tcg_fullrow_ok(xm_ctx* c) { return c->opt.spmm_kernel != 2 && c->N < 4000; }
@@ -541,8 +555,8 @@ static void launch_sym(xm_ctx* c, const double* V, const SpmmEpiArgs& ep) {
   // sized for the largest supported r once, so the address never changes when
   // the staircase climbs (the tCG graphs of lower ranks captured it)
   constexpr int kRmax = 5;
-  const size_t rp = (size_t)p.W * TR * R;
-  c->sym_part.alloc((size_t)p.W * TR * kRmax + (size_t)std::max(p.S, 1) * BC * kRmax + 64);
+  const size_t rp = (size_t)p.W_full * TR * R;  // row parts indexed over the whole triangle
+  c->sym_part.alloc((size_t)p.W_full * TR * kRmax + (size_t)std::max(p.S, 1) * BC * kRmax + 64);
   double* rowpart = c->sym_part.p;
   double* colpart = c->sym_part.p + rp;
   if (!c->gbar.p) {
@@ -563,8 +577,9 @@ static void launch_sym(xm_ctx* c, const double* V, const SpmmEpiArgs& ep) {
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  XM_CUDA(cudaLaunchKernelEx(&cfg, k_spmm_sym<R, MODE>, p.tmq, (int)c->N, (int)c->n, p.TRt, p.TCb,
-                             p.W, p.pbase.p, p.segbase.p, p.colptr.p, V, rowpart, colpart,
+  XM_CUDA(cudaLaunchKernelEx(&cfg, k_spmm_sym<R, MODE>, p.tmq, (int)c->N, (int)c->n, p.rt_a, p.rt_b,
+                             p.row0, p.TCb, p.W, p.pbase.p, p.segbase.p, p.colptr.p, V, rowpart,
+                             colpart,
                              reinterpret_cast<GridBar*>(c->gbar.p), ep));
   XM_CHECK_LAUNCH();
   count_launch(c, 1);

@@ -940,6 +940,11 @@ xm_status xm_get_Q_rows(xm_ctx* c, int32_t row0, int32_t nrows, double* out) {
                               is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                               c->stream));
     sync(c);
+    if (c->world > 1 && c->have_recovery && !is_device_ptr(out)) {
+      // band layout: only the lower trapezoid (columns ≤ row) is this rank's data
+      for (int32_t i = 0; i < nrows; ++i)
+        for (int64_t j = row0 + i + 1; j < c->n; ++j) out[(int64_t)i * c->n + j] = NAN;
+    }
   });
 }
 

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <map>
@@ -323,7 +324,6 @@ void spmm_sym_launch(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiA
 void spmm(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep);
 // Full product into out (n × r, replicated): this rank's rows + all-gather.
 void spmm_full(xm_ctx* c, const double* V, int r, double* out_full, const int* stop = nullptr);
-void allgather_rows(xm_ctx* c, double* full, int r);
 void harvest_events(xm_ctx* c);
 
 // ------------------------------------------------------------ manifold (manifold.cu)
@@ -370,17 +370,33 @@ void xm2_device(xm_ctx* c, double frac, uint8_t* keep_user_dev, int64_t* n_dropp
 void nccl_unique_id(void* out128);
 void nccl_init(xm_ctx* c, const void* id);
 void nccl_destroy(xm_ctx* c);
-void nccl_allgather(xm_ctx* c, const double* send, double* recv, size_t count_per_rank);
 void nccl_allreduce_sum(xm_ctx* c, double* buf, size_t count);
 void sym_plan_destroy(xm_ctx* c);
 void sym_tcg_plan_destroy(xm_ctx* c);
 
 // Row sharding: rank q owns frames [q·nfpr, min(N, (q+1)·nfpr)),
 // nfpr = ⌈N/world⌉; vectors exchanged by the all-gather hold world·3·nfpr rows.
+// Row bands of the world > 1 layout (composed with the
+// lower-triangle stream): rank p owns frames [F_p, F_{p+1}) and stores only
+// the lower trapezoid of their rows (columns ≤ row).  Its share of the lower
+// triangle is ∝ F_{p+1}² − F_p², so F_p = N·√(p/world) balances the bytes per
+// product; bands are aligned to 32 frames (= 96 rows = 3 tiles of 32 rows, so
+// the streaming kernel's tiles never straddle two ranks).  nfpr = the largest
+// band (buffer sizing).
+inline int band_start(int N, int world, int p) {
+  if (p <= 0) return 0;
+  if (p >= world) return N;
+  const double x = (double)N * std::sqrt((double)p / (double)world);
+  const int a = (int)std::lround(x / 32.0) * 32;
+  return std::min(N, std::max(0, a));
+}
 inline void shard_of(int N, int world, int rank, int* f0, int* f1, int* nfpr) {
-  *nfpr = (N + world - 1) / world;
-  *f0 = std::min(N, rank * *nfpr);
-  *f1 = std::min(N, *f0 + *nfpr);
+  *f0 = band_start(N, world, rank);
+  *f1 = std::max(*f0, band_start(N, world, rank + 1));
+  int m = 0;
+  for (int p = 0; p < world; ++p)
+    m = std::max(m, band_start(N, world, p + 1) - band_start(N, world, p));
+  *nfpr = std::max(m, 1);
 }
 inline void set_shard(xm_ctx* c, int N) {
   shard_of(N, c->world, c->rank, &c->f0, &c->f1, &c->nfpr);

@@ -136,8 +136,9 @@ def default_options(**overrides) -> Options:
 
 
 def shard_rows(N: int, world: int, rank: int):
-    """(f0, f1, nfpr): frames [f0, f1) of `rank`, nfpr = ⌈N/world⌉ (xm_shard_rows;
-    host-only, no GPU needed)."""
+    """(f0, f1, nfpr): frames [f0, f1) of `rank` (area-balanced, 32-frame
+    aligned bands of the lower triangle), nfpr = the largest band
+    (xm_shard_rows; host-only, no GPU needed)."""
     f0, f1, nf = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
     st = load_library().xm_shard_rows(int(N), int(world), int(rank), ctypes.byref(f0),
                                       ctypes.byref(f1), ctypes.byref(nf))

@@ -1,10 +1,12 @@
 """World-size-2 gloo worker for tests/test_dist_gloo.py (launched by torchrun).
 
 CPU stand-in for the N > 1 path's host logic: the ncclUniqueId broadcast and
-max-over-ranks timing of bench.py, and the row sharding + padded all-gather
-layout of include/xm.h xm_shard_rows (each rank multiplies its Q rows, the
-shards are all-gathered in rank order, the first n rows must be Q·V), plus the
-all-reduce of ‖Q‖² partials.  Exits non-zero on any mismatch.
+max-over-ranks timing of bench.py, and the band layout of include/xm.h
+xm_shard_rows composed with the symmetric stream: each rank holds the lower
+trapezoid of its band of rows, forms the row parts of its rows and the column
+parts of every row above (a full-length partial), and ONE all-reduce of the
+partials must give Q·V; plus the all-reduce of the ‖Q‖² partials (2× the
+strictly lower entries + the diagonal).  Exits non-zero on any mismatch.
 """
 import os
 import sys
@@ -34,36 +36,43 @@ def main():
     # 2. max over ranks (bench.max_over_ranks)
     assert bench.max_over_ranks(dist, 1.5 + rank, "cpu") == 2.5
 
-    # 3. row shards tile [0, n); padded all-gather reproduces Q·V
+    # 3. bands tile [0, n); one all-reduce of the band partials reproduces Q·V
     for N, r, kw in ((7, 3, dict(kind="unordered", vis_prob=0.6, sigma_d=0.05)),
-                     (10, 1, dict(kind="unordered", vis_prob=0.5)),
-                     (37, 5, dict(kind="loop", window=6))):
+                     (70, 1, dict(kind="unordered", vis_prob=0.2)),
+                     (137, 5, dict(kind="loop", window=6))):
         sc = make_scene(N, 25 * N, seed=N, **kw)
         dm = xo.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
         n = 3 * N
         f0, f1, nfpr = xm.shard_rows(N, world, rank)
+        a, b = 3 * f0, 3 * f1
         V = random_tangent_ambient(N, r, 5)
-        part = np.zeros((3 * nfpr, r))
-        part[: 3 * (f1 - f0)] = dm.Q[3 * f0:3 * f1] @ V
-        bufs = [torch.zeros(3 * nfpr, r, dtype=torch.float64) for _ in range(world)]
-        dist.all_gather(bufs, torch.from_numpy(part))
-        full = torch.cat(bufs).numpy()
-        assert full.shape[0] == world * 3 * nfpr >= n
+        band = np.tril(dm.Q)[a:b, :]                     # the lower trapezoid this rank stores
+        strict = band.copy()
+        strict[np.arange(b - a), np.arange(a, b)] = 0.0  # column parts exclude the diagonal
+        part = np.zeros((n, r))
+        part[a:b] += band @ V                            # row parts (j ≤ i)
+        part += strict.T @ V[a:b]                        # column parts (j < i)
+        t = torch.from_numpy(part)
+        dist.all_reduce(t)
         ref = dm.Q @ V
-        assert np.abs(full[:n] - ref).max() <= 1e-13 * max(1.0, np.abs(ref).max()), (N, r)
-        assert np.all(full[n:] == 0.0)
-        # ‖Q‖_F² from per-rank partials (assembly's all-reduce)
-        s2 = torch.tensor([float(np.sum(dm.Q[3 * f0:3 * f1] ** 2))], dtype=torch.float64)
+        assert np.abs(t.numpy() - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()), (N, r)
+        # ‖Q‖_F² from the trapezoids (assembly's all-reduce, k_sumsq_rows band mode)
+        s2 = torch.tensor([2.0 * float(np.sum(strict ** 2)) + float(np.sum(np.diag(dm.Q)[a:b] ** 2))],
+                          dtype=torch.float64)
         dist.all_reduce(s2)
         assert abs(float(s2) - dm.normF ** 2) <= 1e-12 * dm.normF ** 2
-        # ranks agree on the plan
+        # ranks agree on the plan: contiguous, 32-frame aligned, area-balanced
         plan = torch.tensor([f0, f1, nfpr], dtype=torch.int64)
         plans = [torch.zeros(3, dtype=torch.int64) for _ in range(world)]
         dist.all_gather(plans, plan)
         spans = [tuple(p.tolist()) for p in plans]
         assert spans[0][0] == 0 and spans[-1][1] == N
         assert all(spans[q][1] == spans[q + 1][0] for q in range(world - 1))
-        assert len({s[2] for s in spans}) == 1
+        assert all(s[0] % 32 == 0 for s in spans)
+        assert len({s[2] for s in spans}) == 1 and spans[0][2] == max(s[1] - s[0] for s in spans)
+        if N >= 128:  # lower-triangle shares within one 32-frame step of equal
+            areas = [s[1] ** 2 - s[0] ** 2 for s in spans]
+            assert max(areas) - min(areas) <= 2 * 32 * N + 32 * 32
     dist.barrier()
     dist.destroy_process_group()
     if rank == 0:

@@ -1,10 +1,11 @@
 """The world > 1 (row-sharded) path on ONE GPU, through the C ABI.
 
 `world` contexts in one process, one host thread each, joined by the
-loopback group (include/xm.h XM_LOOPBACK_MAGIC) in place of NCCL: sharded
-assembly (each rank its frame range of Q rows), partial-row SpMM + padded
-all-gather, the all-reduce of ‖Q‖², replicated per-camera work and dots, the
-world > 1 Lanczos and recovery.  Checked against the oracle with the
+loopback group (include/xm.h XM_LOOPBACK_MAGIC) in place of NCCL: band
+assembly (each rank the lower trapezoid of its area-balanced band of Q rows,
+xm_shard_rows), the lower-triangle stream over the band + ONE all-reduce of
+the n×r partials per product, the all-reduce of ‖Q‖², replicated per-camera
+work and dots, the world > 1 Lanczos and recovery.  Checked against the oracle with the
 end-to-end tolerances of test_gpu_parity.py, and across ranks: every rank
 holds the same (bitwise) factor, certificate and recovered solution.
 """
@@ -51,38 +52,53 @@ def run_ranks(xm, world, token, fn):
 
 
 SCENES = [
-    dict(N=37, M=900, kind="loop", window=6),                                   # ragged shards
+    dict(N=37, M=900, kind="loop", window=6),                                   # ragged bands
     dict(N=130, M=2500, kind="unordered", track_mean=10.0, zipf=0.8, sigma_d=0.05, sigma_u=1e-3),
+    dict(N=300, M=6000, kind="loop", window=8),              # > 2 panels per band, 8 ranks busy
 ]
 
 
-@pytest.mark.parametrize("world", [2, 3])
+def tril_rows(Q, a, b):
+    """Rows a..b−1 of Q with the (unstored) entries right of the diagonal as NaN."""
+    out = Q[a:b].copy()
+    for i in range(b - a):
+        out[i, a + i + 1:] = np.nan
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
 @pytest.mark.parametrize("cfg", SCENES, ids=lambda c: f"{c['kind']}{c['N']}")
 def test_sharded_solve_matches_oracle(xm, cfg, world):
     sc = make_scene(seed=3, **cfg)
     dm, st, sol, rep = xo.solve(sc)
     N, n = sc.N, 3 * sc.N
-    nfpr = -(-N // world)
     V = random_tangent_ambient(N, 3, 17)
+    V7 = random_tangent_ambient(N, 7, 18)                  # r > 5: column groups of ≤ 5
 
     def fn(ctx, q):
         ctx.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
-        f0, f1 = min(N, q * nfpr), min(N, (q + 1) * nfpr)
+        f0, f1, _ = xm.shard_rows(N, world, q)
         Qrows = ctx.Q_rows(3 * f0, 3 * (f1 - f0)) if f1 > f0 else np.zeros((0, n))
         QV = ctx.spmm(V)
+        QV7 = ctx.spmm(V7)
         status, info = ctx.solve()
         cert = ctx.certify()
         g = ctx.round_recover()
-        return dict(f0=f0, f1=f1, Qrows=Qrows, QV=QV, status=status, info=info, cert=cert,
-                    g=g, Y=ctx.get_factor())
+        return dict(f0=f0, f1=f1, Qrows=Qrows, QV=QV, QV7=QV7, status=status, info=info,
+                    cert=cert, g=g, Y=ctx.get_factor())
 
     res = run_ranks(xm, world, f"solve-{N}-{world}", fn)
-    # the shards tile Q's rows, and each matches the oracle's rows
+    # the bands tile Q's rows; each rank's lower trapezoid matches the oracle
     Qg = np.concatenate([r["Qrows"] for r in res])
     assert Qg.shape == (n, n)
-    assert np.linalg.norm(Qg - dm.Q) <= 1e-10 * dm.normF
+    Qt = tril_rows(dm.Q, 0, n)
+    ok = ~np.isnan(Qt)
+    assert np.array_equal(np.isnan(Qg), ~ok)
+    assert np.linalg.norm(Qg[ok] - Qt[ok]) <= 1e-10 * dm.normF
     for r in res:
         assert np.linalg.norm(r["QV"] - dm.Q @ V) <= 1e-10 * np.linalg.norm(dm.Q @ V)
+        assert np.linalg.norm(r["QV7"] - dm.Q @ V7) <= 1e-10 * np.linalg.norm(dm.Q @ V7)
+        assert np.array_equal(r["QV"], res[0]["QV"])     # one all-reduce: identical everywhere
     # replicated state is bitwise identical on every rank
     for r in res[1:]:
         assert np.array_equal(r["Y"], res[0]["Y"])
@@ -151,4 +167,7 @@ def test_xm2_sharded(xm, world):
         assert abs(info2["f"] - st_o.f) <= 1e-8 * (1.0 + abs(st_o.f))
         assert np.max(np.abs(sol2["R"] - osol2.R)) <= 1e-6
     Qg = np.concatenate([o[2] for o in out], axis=0)
-    assert np.linalg.norm(Qg - dm2.Q) <= 1e-10 * dm2.normF
+    Qt = tril_rows(dm2.Q, 0, 3 * sc.N)
+    ok = ~np.isnan(Qt)
+    assert np.array_equal(np.isnan(Qg), ~ok)
+    assert np.linalg.norm(Qg[ok] - Qt[ok]) <= 1e-10 * dm2.normF
