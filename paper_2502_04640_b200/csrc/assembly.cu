@@ -295,12 +295,13 @@ __device__ __forceinline__ double fx_value(const unsigned long long* acc, int en
   return ((double)l1 * 0x1p44 + (double)l0) * inv_scale;
 }
 
-// T = max_e w_e (1 + |ũ_e|²)  (one block)
+// −T per block, T = max_e w_e (1 + |ũ_e|²)  (min-reduced afterwards: max = −min(−·))
 __global__ void k_term_bound(int64_t E, const double* __restrict__ pts, const double* __restrict__ w,
-                             double* out) {
+                             double* __restrict__ partials) {
   __shared__ double sh[256];
   double m = 0.0;
-  for (int64_t e = threadIdx.x; e < E; e += 256) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x) {
     const double x = pts[3 * e], y = pts[3 * e + 1], z = pts[3 * e + 2];
     m = fmax(m, w[e] * (1.0 + x * x + y * y + z * z));
   }
@@ -310,7 +311,7 @@ __global__ void k_term_bound(int64_t E, const double* __restrict__ pts, const do
     if (threadIdx.x < s) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + s]);
     __syncthreads();
   }
-  if (threadIdx.x == 0) *out = sh[0];
+  if (threadIdx.x == 0) partials[blockIdx.x] = -sh[0];
 }
 
 // S_lower: with one rank the SYRK + mirror read only S[3i+a][3j+b] for j ≤ i
@@ -864,21 +865,22 @@ void mirror_lower(xm_ctx* c, double* Q, int n, int64_t ldq) {
 }
 
 // Σ Q_ij² over this rank's rows; band layout (row0 ≥ 0): only the lower
-// trapezoid is stored, so Σ = Σ_{j<i} 2Q_ij² + Σ_{j=i} Q_ii² over global rows i
+// trapezoid is stored, so Σ = Σ_{j<i} 2Q_ij² + Σ_{j=i} Q_ii² over global rows i.
+// Rows are distributed over the blocks, columns over the threads (coalesced,
+// no per-element index division).
 __global__ void k_sumsq_rows(const double* __restrict__ Q, int rows, int n, int64_t ldq,
                              double* __restrict__ partials, int row0) {
   __shared__ double sh[256];
   double acc = 0.0;
-  int64_t tot = (int64_t)rows * n;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    int i = (int)(t / n), j = (int)(t % n);
-    double v = Q[(int64_t)i * ldq + j];
-    if (row0 >= 0) {
-      const int gi = row0 + i;
-      v = (j < gi) ? v * 1.4142135623730951 : (j == gi ? v : 0.0);
+  for (int i = blockIdx.x; i < rows; i += gridDim.x) {
+    const double* q = Q + (int64_t)i * ldq;
+    const int gi = row0 + i;
+    const int jend = (row0 >= 0) ? min(n, gi + 1) : n;
+    for (int j = threadIdx.x; j < jend; j += blockDim.x) {
+      double v = q[j];
+      if (row0 >= 0 && j < gi) v *= 1.4142135623730951;
+      acc = fma(v, v, acc);
     }
-    acc = fma(v, v, acc);
   }
   sh[threadIdx.x] = acc;
   __syncthreads();
@@ -1103,11 +1105,15 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
   } else {
     c->scal.alloc(64);
     double* d_T = c->scal.p + 60;
-    k_term_bound<<<1, 256, 0, c->stream>>>(Ek, c->e_pts.p, c->e_w.p, d_T);
+    DBuf<double>& tb = scratch_f64(c, "term_bound");
+    tb.alloc(kDotBlocks);
+    k_term_bound<<<kDotBlocks, 256, 0, c->stream>>>(Ek, c->e_pts.p, c->e_w.p, tb.p);
     XM_CHECK_LAUNCH();
+    reduce_partials(c, tb.p, kDotBlocks, 1, d_T, 1u);  // min of −T_b
     double T = 0.0;
     XM_CUDA(cudaMemcpyAsync(&T, d_T, 8, cudaMemcpyDeviceToHost, c->stream));
     sync(c);
+    T = -T;
     if (!(T > 0.0) || !std::isfinite(T)) throw Error(XM_EINVAL, "non-finite measurement scale");
     const int ex = 70 - (int)std::ceil(std::log2(T));
     const double scale = std::ldexp(1.0, ex), inv_scale = std::ldexp(1.0, -ex);

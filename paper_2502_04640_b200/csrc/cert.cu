@@ -561,33 +561,47 @@ __global__ void k_g_times_y3(int m, int64_t n, int64_t ldg, const double* __rest
   }
 }
 
-// Solve Lᵀ x = rhs in place (3 right-hand sides), t_{j+1} = −x_j; one CTA.
-__global__ void __launch_bounds__(1024) k_backsub_lt(int m, int64_t ldl, const double* __restrict__ L,
-                                                     double* __restrict__ rhs,
-                                                     double* __restrict__ t) {
-  __shared__ double xj[3];
-  for (int j = m - 1; j >= 0; --j) {
-    if (threadIdx.x < 3) {
-      double v = rhs[j * 3 + threadIdx.x] / L[(int64_t)j * ldl + j];
-      xj[threadIdx.x] = v;
-      rhs[j * 3 + threadIdx.x] = v;
-    }
-    __syncthreads();
-    const double* row = L + (int64_t)j * ldl;
-    for (int l = threadIdx.x; l < j; l += blockDim.x) {
-      double lv = row[l];
-      rhs[l * 3] -= lv * xj[0];
-      rhs[l * 3 + 1] -= lv * xj[1];
-      rhs[l * 3 + 2] -= lv * xj[2];
-    }
-    __syncthreads();
+// Lᵀ x = rhs (3 right-hand sides), t_{j+1} = −x_j: blocked back substitution,
+// one launch per 64-row block from the bottom.  Every CTA solves the block's
+// 64 × 64 triangle redundantly from its (final) right-hand sides (smem), CTA 0
+// writes x_b as t, and each CTA updates its slice of the rows above,
+// rhs_l −= Σ_{j ∈ b} L_jl x_j (rows j of L: coalesced in l).
+constexpr int kBS = 64;
+__global__ void __launch_bounds__(256) k_backsub_block(int kb, int nb, int64_t ldl,
+                                                       const double* __restrict__ L,
+                                                       double* __restrict__ rhs,
+                                                       double* __restrict__ t) {
+  __shared__ double Ld[kBS][kBS + 1];
+  __shared__ double xb[kBS][3];
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    const int i = e / nb, j = e % nb;
+    Ld[i][j] = (j <= i) ? L[(int64_t)(kb + i) * ldl + kb + j] : 0.0;
   }
-  for (int j = threadIdx.x; j < m; j += blockDim.x) {
-    t[(j + 1) * 3] = -rhs[j * 3];
-    t[(j + 1) * 3 + 1] = -rhs[j * 3 + 1];
-    t[(j + 1) * 3 + 2] = -rhs[j * 3 + 2];
+  for (int e = threadIdx.x; e < nb * 3; e += blockDim.x) xb[e / 3][e % 3] = rhs[(int64_t)kb * 3 + e];
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    const int cc = threadIdx.x;
+    for (int i = nb - 1; i >= 0; --i) {
+      double v = xb[i][cc];
+      for (int k = i + 1; k < nb; ++k) v = fma(-Ld[k][i], xb[k][cc], v);
+      xb[i][cc] = v / Ld[i][i];
+    }
   }
-  if (threadIdx.x < 3) t[threadIdx.x] = 0.0;
+  __syncthreads();
+  if (blockIdx.x == 0)
+    for (int e = threadIdx.x; e < nb * 3; e += blockDim.x) t[(int64_t)(kb + 1) * 3 + e] = -xb[e / 3][e % 3];
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= kb) return;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  for (int i = 0; i < nb; ++i) {
+    const double lv = L[(int64_t)(kb + i) * ldl + l];
+    a0 = fma(lv, xb[i][0], a0);
+    a1 = fma(lv, xb[i][1], a1);
+    a2 = fma(lv, xb[i][2], a2);
+  }
+  rhs[(int64_t)l * 3] -= a0;
+  rhs[(int64_t)l * 3 + 1] -= a1;
+  rhs[(int64_t)l * 3 + 2] -= a2;
 }
 
 // p_k = Σ_{e ∈ track k} w_e (s_i R_i ũ_e + t_i) / W_k
@@ -702,9 +716,14 @@ void round_recover_device(xm_ctx* c) {
   if (N > 1 && c->have_recovery) {
     int m = N - 1;
     k_g_times_y3<<<ceil_div(m, 8), 256, 0, c->stream>>>(m, n, c->ldq, c->G.p, c->Yr.p, c->rhs.p);
-    k_backsub_lt<<<1, 1024, 0, c->stream>>>(m, c->ldk, c->L.p, c->rhs.p, c->t_out.p);
+    XM_CUDA(cudaMemsetAsync(c->t_out.p, 0, 3 * sizeof(double), c->stream));  // t_0 = 0
+    for (int kb = ((m - 1) / kBS) * kBS; kb >= 0; kb -= kBS) {
+      const int nb = std::min(kBS, m - kb);
+      k_backsub_block<<<std::max(1, ceil_div(kb, 256)), 256, 0, c->stream>>>(kb, nb, c->ldk, c->L.p,
+                                                                           c->rhs.p, c->t_out.p);
+    }
     XM_CHECK_LAUNCH();
-    count_launch(c, 2);
+    count_launch(c, 1 + (m - 1) / kBS + 1);
   } else {
     XM_CUDA(cudaMemsetAsync(c->t_out.p, 0, (size_t)N * 3 * 8, c->stream));
   }
