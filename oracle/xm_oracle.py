@@ -322,6 +322,81 @@ def q_rows(N: int, M: int, frame, landmark, pts, w=None, rows=(), info: Optional
     return S_I - CtX.T
 
 
+# =============================================================================
+# NEXT-1: Q·V without forming Q  ("Extending the XM solver to
+# support sparse matrix-vector multiplications")
+# =============================================================================
+
+class ImplicitQ:
+    """Q = S − C̄ᵀK̄⁻¹C̄ applied to V by the two eliminations of App. A
+     on V itself, per edge — the envelope theorem on Eq. (3):
+    Q·V = ½∇_V min_{t,p} Σ_e w_e‖V_iᵀũ_e + t_i − p_k‖² (t_0 = 0, reading C2):
+
+      z_e = V_iᵀ ũ_e                        (r-vector per measurement)
+      m_k = Σ_{e∈k} w_e z_e / W_k           (landmark mean; H_pp = diag(W))
+      b_i = Σ_{e∈i} w_e (z_e − m_k)  = (C̄V)_i,   i ≥ 1
+      t   = −K̄⁻¹ b,  t_0 = 0                (the optimal translations, Eq. (4))
+      p_k = m_k + Σ_{e∈k} w_e t_{i_e} / W_k  (the optimal landmarks, Eq. (4))
+      (QV)_i = Σ_{e∈i} w_e ũ_e (z_e + t_i − p_k)ᵀ
+
+    K̄ = H_tt − H_tp diag(1/W) H_pt without the anchor row / column, factored
+    once (Cholesky)."""
+
+    def __init__(self, N: int, M: int, frame, landmark, pts, w=None):
+        frame, landmark, pts, w, _ = validate(N, M, frame, landmark, pts, w)
+        self.N, self.M, self.n = N, M, 3 * N
+        self.frame, self.landmark, self.pts, self.w = frame, landmark, pts, w
+        self.W = np.bincount(landmark, weights=w, minlength=M)
+        self.Winv = np.zeros(M)
+        self.Winv[self.W > 0] = 1.0 / self.W[self.W > 0]
+        if N > 1:
+            F = sp.csr_matrix((w, (frame, landmark)), shape=(N, M))
+            K = -(F @ sp.diags(self.Winv) @ F.T).toarray()
+            K[np.arange(N), np.arange(N)] += np.bincount(frame, weights=w, minlength=N)
+            self.chol = sla.cho_factor(K[1:, 1:], lower=True)
+
+    def _lm_mean(self, x_e):
+        m = np.zeros((self.M, x_e.shape[1]))
+        np.add.at(m, self.landmark, self.w[:, None] * x_e)
+        return m * self.Winv[:, None]
+
+    def apply(self, V):
+        V = np.asarray(V, np.float64)
+        r = V.shape[1]
+        Vb = V.reshape(self.N, 3, r)
+        z = np.einsum("ea,ear->er", self.pts, Vb[self.frame])          # z_e = V_iᵀ ũ_e
+        m = self._lm_mean(z)
+        t = np.zeros((self.N, r))
+        if self.N > 1:
+            b = np.zeros((self.N, r))
+            np.add.at(b, self.frame, self.w[:, None] * (z - m[self.landmark]))
+            t[1:] = -sla.cho_solve(self.chol, b[1:])
+        p = m + self._lm_mean(t[self.frame])
+        res = self.w[:, None] * (z + t[self.frame] - p[self.landmark])  # w_e (z_e + t_i − p_k)
+        out = np.zeros((self.N, 3, r))
+        np.add.at(out, self.frame, self.pts[:, :, None] * res[:, None, :])
+        return out.reshape(self.n, r)
+
+    def __matmul__(self, V):
+        return self.apply(V)
+
+    @property
+    def shape(self):
+        return (self.n, self.n)
+
+
+def hutchinson_normF(apply, n: int, probes: int = 16, seed: int = 0x48C0) -> float:
+    """‖Q‖_F ≈ √((1/k) Σ_j ‖Q z_j‖²), z_j ∈ {±1}ⁿ = sign of the shared
+    counter-based stream (synth.scenes.splitmix64_uniform, seed + j), E[‖Qz‖²]
+    = ‖Q‖_F²: the tolerance scale of the implicit mode (reading C24), where Q
+    is never formed.  Both sides draw the same probes."""
+    from synth.scenes import splitmix64_uniform
+    Z = np.stack([np.where(splitmix64_uniform(seed + j, n) < 0.0, -1.0, 1.0) for j in range(probes)],
+                 axis=1)
+    QZ = apply(Z)
+    return math.sqrt(float(np.sum(QZ * QZ)) / probes)
+
+
 def edge_objective(frame, landmark, pts, w, s, R, t, p) -> float:
     """Eq. (3) evaluated directly: Σ_e w_e ‖s_i R_i ũ_e + t_i − p_k‖²."""
     frame = np.asarray(frame, np.int64)
@@ -805,13 +880,16 @@ class StaircaseResult:
     outer: int
 
 
-def staircase(dm_or_Q, opts: Options = None, Y0=None, r0=3, dense_cert=False) -> StaircaseResult:
-    """Algorithm 1: init U⁰ = [I₃,…,I₃] at r = 3 unless Y0 is given."""
+def staircase(dm_or_Q, opts: Options = None, Y0=None, r0=3, dense_cert=False,
+              normQ: Optional[float] = None) -> StaircaseResult:
+    """Algorithm 1: init U⁰ = [I₃,…,I₃] at r = 3 unless Y0 is given.
+    `normQ` overrides ‖Q‖_F as the tolerance scale (the implicit mode's
+    estimate, reading C24); Q may be an ImplicitQ (matrix-free products)."""
     opts = opts or Options()
     Q = dm_or_Q.Q if isinstance(dm_or_Q, DataMatrix) else dm_or_Q
-    n = Q.shape[0]
+    n = Q.n if isinstance(Q, ImplicitQ) else Q.shape[0]
     N = n // 3
-    normQ = float(np.linalg.norm(Q))
+    normQ = float(np.linalg.norm(Q)) if normQ is None else float(normQ)
     if Y0 is None:
         Y = np.zeros((n, r0))
         for i in range(N):

@@ -872,3 +872,55 @@ def test_xm2_select_keeps_every_frame_determined_and_minimal():
     # no kept measurement of a private landmark (each would be a single-view leaf)
     assert not keep[E:].any()
     assert xo.connected_components(sc.N, M, fr[keep], lm[keep]) == 1
+
+
+# ----------------------------------------------------------------------------- NEXT-1
+@pytest.mark.parametrize("cfg", [dict(N=10, M=300, kind="unordered", vis_prob=0.6),
+                                 dict(N=37, M=900, kind="loop", window=6, sigma_d=0.02,
+                                      weights="uniform")], ids=["unordered10", "loop37"])
+def test_implicit_Q_apply_equals_the_schur_complement(cfg):
+    """NEXT-1: Q·V by the per-edge eliminations of App. A equals the
+    dense Schur complement (pinned by brute-force least squares in
+    test_prop1_equivalence_brute_force) for r = 1, 3, 5; and ⟨V, QV⟩ = the
+    brute-force min_{t,p} Eq. (3) at fixed V (envelope theorem)."""
+    sc = make_scene(seed=4, **cfg)
+    dm = xo.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+    iq = xo.ImplicitQ(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+    for r in (1, 3, 5):
+        V = random_tangent_ambient(sc.N, r, 60 + r)
+        ref = dm.Q @ V
+        assert np.linalg.norm(iq @ V - ref) <= 1e-12 * np.linalg.norm(dm.Q) * np.linalg.norm(V)
+    V = random_factor(sc.N, 3, 61)
+    assert abs(np.vdot(V, iq @ V) - brute_marginal_objective(sc, V)) <= 1e-8 * (
+        1.0 + abs(brute_marginal_objective(sc, V)))
+
+
+def test_hutchinson_norm_is_unbiased_and_shared():
+    """Reading C24: the implicit mode's tolerance scale.  E‖Qz‖² = ‖Q‖_F² for
+    Rademacher z: the 16-probe estimate is within its standard error of the
+    exact norm, and the implicit and dense products give the same estimate."""
+    sc = make_scene(12, 300, "unordered", seed=2, vis_prob=0.5)
+    dm = xo.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+    iq = xo.ImplicitQ(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+    est_d = xo.hutchinson_normF(lambda Z: dm.Q @ Z, dm.n)
+    est_i = xo.hutchinson_normF(iq.apply, dm.n)
+    assert abs(est_d - est_i) <= 1e-12 * est_d
+    # Var‖Qz‖² = 2(‖Q‖_F⁴ − Σ Q_ii⁴)·… ≤ 2‖Q‖_F⁴: 16 probes ⇒ rel. std of ‖·‖² ≤ √(2/16)
+    assert abs(est_d ** 2 - dm.normF ** 2) <= 3 * math.sqrt(2 / 16) * dm.normF ** 2
+    many = xo.hutchinson_normF(lambda Z: dm.Q @ Z, dm.n, probes=400)
+    assert abs(many ** 2 - dm.normF ** 2) <= 3 * math.sqrt(2 / 400) * dm.normF ** 2
+
+
+def test_implicit_staircase_reaches_the_dense_optimum():
+    """The staircase on the matrix-free operator certifies the same X as on the
+    dense Q with the same tolerance scale."""
+    sc = make_scene(10, 400, "unordered", seed=6, vis_prob=0.6, sigma_d=0.05, sigma_u=1e-3)
+    dm = xo.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+    iq = xo.ImplicitQ(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+    nq = xo.hutchinson_normF(iq.apply, dm.n)
+    st_i = xo.staircase(iq, normQ=nq)
+    st_d = xo.staircase(dm, normQ=nq)
+    assert st_i.certified and st_d.certified
+    Xi, Xd = st_i.Y @ st_i.Y.T, st_d.Y @ st_d.Y.T
+    assert np.linalg.norm(Xi - Xd) <= 1e-6 * np.linalg.norm(Xd)
+    assert abs(st_i.f - st_d.f) <= 1e-8 * (1.0 + abs(st_d.f))
