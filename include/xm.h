@@ -102,6 +102,10 @@ typedef struct {
                           /* Q + blkdiag(2λ/3 (α_i−1) I) − blkdiag(Λ), dual   */
                           /* tr Λ_0 − λ Σ (α_i² − 1).  λ > 0 uses the unfused */
                           /* product + epilogue kernels (no persistent tCG)  [0]  */
+  int32_t implicit_q;     /* 1: never form Q: each   */
+                          /* Q·V by per-measurement elimination passes + K̄⁻¹ */
+                          /* (one GPU); ‖Q‖_F by a 16-probe estimate (C24);   */
+                          /* certificate by Lanczos on Z only              [0]  */
 } xm_options;
 
 typedef struct {

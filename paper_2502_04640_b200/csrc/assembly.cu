@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_clique_scatter_fx(
     const double* __restrict__ e_w, const double* __restrict__ W, const int32_t* __restrict__ e_lm,
     double* __restrict__ S, int64_t ldq, int row0, double* __restrict__ Cb,
     double* __restrict__ Kb, int64_t ldk, int32_t* __restrict__ cursor, double scale,
-    double inv_scale) {
+    double inv_scale, int k_only) {
   extern __shared__ unsigned long long acc[];
   double* l_ae = reinterpret_cast<double*>(acc + (size_t)kFxEntries * 2 * WCF);  // [3][T]
   double* l_we = l_ae + 3 * SC_THREADS;
@@ -339,8 +339,9 @@ __global__ void __launch_bounds__(SC_THREADS) k_clique_scatter_fx(
   for (int l = tid; l < nl; l += SC_THREADS) cursor[e0 + l] = lm_off[e_lm[fr_edge[e0 + l]]];
   for (int c0 = 0; c0 < N; c0 += WCF) {
     const int c1 = min(N, c0 + WCF);
-    const bool needS = own && (!s_lower_only || c0 <= i);
+    const bool needS = !k_only && own && (!s_lower_only || c0 <= i);
     const bool needK = i >= 1 && c0 <= i;
+    if (k_only && !needK) break;  // K̄ lower only: no chunk right of the diagonal
     for (int t = tid; t < kFxEntries * 2 * WCF; t += SC_THREADS) acc[t] = 0ull;
     for (int lb = 0; lb < nl; lb += SC_THREADS) {
       // (1) per landmark: partners of this chunk = [p, q) of its frame-sorted track
@@ -424,8 +425,10 @@ __global__ void __launch_bounds__(SC_THREADS) k_clique_scatter_fx(
           }
         }
         if (i >= 1) {
+          if (!k_only) {
 #pragma unroll
-          for (int b = 0; b < 3; ++b) fx_add<WCF>(acc, 9 + b, col, cp * af[b] * scale);
+            for (int b = 0; b < 3; ++b) fx_add<WCF>(acc, 9 + b, col, cp * af[b] * scale);
+          }
           if (jf >= 1 && jf <= i) fx_add<WCF>(acc, 12, col, cp * scale);
         }
       }
@@ -442,8 +445,9 @@ __global__ void __launch_bounds__(SC_THREADS) k_clique_scatter_fx(
       }
     }
     if (i >= 1) {
-      for (int x = tid; x < w3; x += SC_THREADS)
-        Cb[(int64_t)(i - 1) * ldq + 3 * c0 + x] = fx_value<WCF>(acc, 9 + x % 3, x / 3, inv_scale);
+      if (!k_only)
+        for (int x = tid; x < w3; x += SC_THREADS)
+          Cb[(int64_t)(i - 1) * ldq + 3 * c0 + x] = fx_value<WCF>(acc, 9 + x % 3, x / 3, inv_scale);
       if (needK) {
         const int jlo = max(c0, 1), jhi = min(c1, i + 1);
         for (int j = jlo + tid; j < jhi; j += SC_THREADS)
@@ -1083,12 +1087,19 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
   c->ldq = round_up(std::max(n, 1), 32);
   c->ldk = round_up(std::max(N - 1, 1), 32);
   set_shard(c, N);
-  c->Q.alloc((size_t)std::max(c->nrows, 1) * c->ldq);
-  XM_CUDA(cudaMemsetAsync(c->Q.p, 0, (size_t)std::max(c->nrows, 1) * c->ldq * 8, c->stream));
+  // NEXT-1 (implicit.cu): Q, S, C̄ and G are never formed — only K̄, its factor and inverse
+  const bool implicit = c->opt.implicit_q != 0 && c->world == 1;
+  c->implicit_active = implicit;
+  if (!implicit) {
+    c->Q.alloc((size_t)std::max(c->nrows, 1) * c->ldq);
+    XM_CUDA(cudaMemsetAsync(c->Q.p, 0, (size_t)std::max(c->nrows, 1) * c->ldq * 8, c->stream));
+  } else {
+    c->Q.alloc(1);
+  }
   if (N > 1) {
-    c->G.alloc((size_t)(N - 1) * c->ldq);
+    c->G.alloc(implicit ? 1 : (size_t)(N - 1) * c->ldq);
     c->L.alloc((size_t)(N - 1) * c->ldk);
-    XM_CUDA(cudaMemsetAsync(c->G.p, 0, (size_t)(N - 1) * c->ldq * 8, c->stream));
+    if (!implicit) XM_CUDA(cudaMemsetAsync(c->G.p, 0, (size_t)(N - 1) * c->ldq * 8, c->stream));
     XM_CUDA(cudaMemsetAsync(c->L.p, 0, (size_t)(N - 1) * c->ldk * 8, c->stream));
   } else {
     c->G.alloc(1);
@@ -1126,7 +1137,7 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
     k_clique_scatter_fx<WC_, NT_><<<N, NT_, sm_, c->stream>>>(                                   \
         N, c->f0, c->f1, c->world == 1 ? 1 : 0, c->fr_off.p, c->fr_edge.p, c->lm_off.p, c->e_fr.p, \
         c->e_pts.p, c->e_w.p, c->W.p, c->e_lm.p, c->Q.p, c->ldq, c->row0, c->G.p, c->L.p, c->ldk,  \
-        cursor.p, scale, inv_scale);                                                             \
+        cursor.p, scale, inv_scale, implicit ? 1 : 0);                                           \
   } while (0)
     const char* cfg = std::getenv("XM_SCATTER_CFG");
     // 768 frames × 1024 threads (213 KB, 1 CTA / SM) measured best at E and D
@@ -1140,6 +1151,22 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
   }
 
   phase("scatter");
+  if (implicit) {
+    if (N > 1) {
+      DBuf<double>& U = scratch_f64(c, "chol_U");
+      U.alloc((size_t)(N - 1) * c->ldk);
+      dense_cholesky(c, c->L.p, N - 1, c->ldk, 1e-12, true, U.p, c->ldk);
+    }
+    phase("cholesky");
+    implicit_prepare(c);  // frame-sorted measurements, K̄⁻¹
+    phase("K^-1");
+    c->have_recovery = true;
+    c->normQ = implicit_normF(c);
+    phase("normQ (16 probes)");
+    c->stats.E = c->E;
+    c->stats.q_bytes = 0;
+    return;
+  }
   // ---- H5: K̄ = LLᵀ, G = L⁻¹C̄, Q = S − GᵀG
   if (N > 1) {
     // pivot test relative to max diag(K̄); a disconnected graph gives a ~0 pivot

@@ -30,6 +30,12 @@ __global__ void k_splitmix(int64_t n, uint64_t seed, double* __restrict__ out) {
   out[j] = 2.0 * ((double)(z >> 11) * (1.0 / 9007199254740992.0)) - 1.0;
 }
 
+void splitmix_uniform(xm_ctx* c, int64_t n, uint64_t seed, double* out) {
+  k_splitmix<<<ceil_div(n, 256), 256, 0, c->stream>>>(n, seed, out);
+  XM_CHECK_LAUNCH();
+  count_launch(c);
+}
+
 // x ← x / sqrt(*sumsq);  optionally record sqrt into beta_out
 __global__ void k_normalize(int64_t n, const double* __restrict__ sumsq, const double* __restrict__ x,
                             double* __restrict__ out, double* __restrict__ beta_out) {
@@ -267,7 +273,7 @@ bool lanczos(xm_ctx* c, double tol_abs, int max_steps, double* lambda, int* step
         count_launch(c, 3);
         dot_flat(c, vk, c->lz_w.p, n, dots, kDotBlocks);
         reduce_partials(c, dots, kDotBlocks, 1, alphas + k);
-      } else if (c->world == 1 && c->opt.scale_reg == 0.0) {
+      } else if (fused_epilogues(c)) {
         SpmmEpiArgs ep{};
         ep.out = c->lz_w.p;
         ep.lam = c->lam.p;
@@ -713,7 +719,9 @@ void round_recover_device(xm_ctx* c) {
   XM_CHECK_LAUNCH();
   count_launch(c, 3);
   // translations: T = −L⁻ᵀ (G Y_r), t_0 = 0
-  if (N > 1 && c->have_recovery) {
+  if (c->implicit_active) {
+    implicit_translations(c, c->Yr.p, c->t_out.p);  // t = −K̄⁻¹ C̄ Y₃, t_0 = 0
+  } else if (N > 1 && c->have_recovery) {
     int m = N - 1;
     k_g_times_y3<<<ceil_div(m, 8), 256, 0, c->stream>>>(m, n, c->ldq, c->G.p, c->Yr.p, c->rhs.p);
     XM_CUDA(cudaMemsetAsync(c->t_out.p, 0, 3 * sizeof(double), c->stream));  // t_0 = 0

@@ -461,7 +461,7 @@ void hvp_epilogue(xm_ctx* c, int r, const double* Y, const double* V, const doub
 
 int hvp_product(xm_ctx* c, int r, const double* Y, const double* V, double* HV, double* partials,
                 const int* stop) {
-  if (c->world == 1 && c->opt.scale_reg == 0.0) {
+  if (fused_epilogues(c)) {
     SpmmEpiArgs ep{};
     ep.Y = Y;
     ep.lam = c->lam.p;

@@ -484,7 +484,7 @@ static void launch_tcg(xm_ctx* c, const double* V, int r, const SpmmEpiArgs& ep)
 
 bool tcg_fused_supported(xm_ctx* c, int r) {
   if (!c->fused_tcg || c->world != 1 || r < 1 || r > 6 || !tcg_fullrow_ok(c) || c->N < 1 ||
-      c->opt.scale_reg != 0.0)  // App. D terms live in the unfused epilogues only
+      !fused_epilogues(c))  // App. D terms / matrix-free products: unfused epilogues only
     return false;
   const int G = spmm_fullrow_grid(c);
   return ceil_div(c->N, G) <= kSpmmThreads;
@@ -590,6 +590,12 @@ __global__ void k_unpack_cols(int64_t n, int r, int c0, int w, const double* __r
 // those partials (n·r·8 bytes, ≈ 1 MB at E) replaces the all-gather of full-row
 // shards and halves each rank's Q bytes.  r > 5: column groups of ≤ 5.
 void spmm_full(xm_ctx* c, const double* V, int r, double* out_full, const int* stop) {
+  if (c->implicit_active) {  // NEXT-1: matrix-free (implicit.cu); after a tCG stop the
+    // passes still run inside a graph replay, their result is ignored by the update kernels
+    implicit_product(c, V, r, out_full);
+    c->stats.spmm_calls++;
+    return;
+  }
   SpmmEpiArgs ep{};
   ep.stop = stop;
   if (c->world == 1 || r <= 5) {

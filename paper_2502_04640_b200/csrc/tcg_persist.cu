@@ -1029,7 +1029,7 @@ bool tcg_persist_sym_supported(xm_ctx* c, int r);
 bool tcg_persist_supported(xm_ctx* c, int r) {
   if (tcg_persist_sym_supported(c, r)) return true;
   if (!c->fused_tcg || !c->persist_tcg || c->world != 1 || r < 1 || r > 5 ||
-      !tcg_fullrow_ok(c) || c->N < 1 || c->opt.scale_reg != 0.0)
+      !tcg_fullrow_ok(c) || c->N < 1 || !fused_epilogues(c))
     return false;
   const int G = std::min(148, c->N);
   return ceil_div(c->N, G) <= kPC && persist_smem_r(r, c->n, G) <= kSmemCap;
@@ -1258,7 +1258,7 @@ size_t persist_sym_smem_r(int r, int N, int G) {
 // assemble, spills at r = 4).
 bool tcg_persist_sym_supported(xm_ctx* c, int r) {
   if (c->persist_sym < 0 || !c->fused_tcg || !c->persist_tcg || c->world != 1 || r < 1 || r > 5 ||
-      c->N < 1 || c->opt.spmm_kernel == 1 || c->opt.scale_reg != 0.0)
+      c->N < 1 || c->opt.spmm_kernel == 1 || !fused_epilogues(c))
     return false;
   if (c->persist_sym == 0 && c->N >= 4000) return false;
   const int G = std::min(148, c->N);

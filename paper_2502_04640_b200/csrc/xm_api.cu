@@ -75,7 +75,7 @@ void read_scal(xm_ctx* c, int first, int count, double* out) {
 
 // QY = Q·Y, Λ, grad, and scal_out[0..2] = f, ‖g‖², min α  (fused on one GPU)
 void grad_fused(xm_ctx* c, int r, const double* Y, double* QY, double* grad, double* scal_out) {
-  if (c->world == 1 && c->opt.scale_reg == 0.0) {
+  if (fused_epilogues(c)) {
     c->part1.alloc(2048);
     SpmmEpiArgs ep{};
     ep.out = QY;
@@ -103,7 +103,7 @@ void eval_point(xm_ctx* c, double* f, double* g2, double* amin) {
 // D ↦ (QD, ⟨QY, D⟩, ⟨D, QD⟩) → scal_out[0..1]
 void df_product(xm_ctx* c, int r, const double* D, const double* QY, double* QD, double* scal_out) {
   const int64_t len = (int64_t)c->n * r;
-  if (c->world == 1) {
+  if (dense_fused(c)) {
     c->part2.alloc(4096);
     SpmmEpiArgs ep{};
     ep.out = QD;
@@ -149,7 +149,8 @@ std::vector<uintptr_t> graph_signature(xm_ctx* c) {
           (uintptr_t)c->part1.p, (uintptr_t)c->part2.p, (uintptr_t)c->opt.profile,
           (uintptr_t)c->f0, (uintptr_t)c->f1, (uintptr_t)c->sym_part.p, (uintptr_t)c->gbar.p,
           (uintptr_t)c->sym_plan, (uintptr_t)c->gsync.p, (uintptr_t)c->fused_tcg,
-          (uintptr_t)c->opt.spmm_kernel, reg_bits(c)};
+          (uintptr_t)c->opt.spmm_kernel, reg_bits(c), (uintptr_t)c->implicit_active,
+          (uintptr_t)c->Kinv.p, (uintptr_t)c->imp_lm.p, (uintptr_t)c->e_fr.p};
 }
 
 void destroy_graph(xm_ctx::TcgGraph& g) {
@@ -391,7 +392,7 @@ void certify_current(xm_ctx* c, double* lambda, int* steps) {
   c->cert_method = 0;
   c->cert_rigorous = 0;
   if (c->opt.scale_reg != 0.0) reg_frames(c, c->r, c->Y.p, nullptr, c->scal.p + 24);  // d_i at Y
-  if (c->world == 1 && c->opt.cert_cholesky) {
+  if (dense_fused(c) && c->opt.cert_cholesky) {
     int budget = std::min(c->opt.lanczos_max, std::max(32, c->n / 72));
     PhaseClock pc(c);
     bool conv;
@@ -647,6 +648,7 @@ xm_status xm_set_Q(xm_ctx* c, int32_t N, const double* Q_full) {
   if (!c || N < 1 || !Q_full) return XM_EINVAL;
   return guard(c, [&] {
     NvtxRange nvtx_("xm_set_Q");
+    c->implicit_active = false;  // a dense Q from the caller
     c->N = N;
     c->M = 0;
     c->E = 0;
@@ -932,6 +934,7 @@ xm_status xm_get_Q_rows(xm_ctx* c, int32_t row0, int32_t nrows, double* out) {
   if (!c || !out) return XM_EINVAL;
   return guard(c, [&] {
     require_stage(c, 1);
+    if (c->implicit_active) throw Error(XM_EINVAL, "Q is not formed in the implicit (NEXT-1) mode");
     if (row0 < c->row0 || row0 + nrows > c->row0 + c->nrows || nrows < 0)
       throw Error(XM_EINVAL, "rows not owned by this rank");
     if (nrows == 0) return;

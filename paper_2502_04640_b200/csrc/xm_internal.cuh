@@ -141,6 +141,10 @@ struct xm_ctx {
   xm::DBuf<double> Y, QY, grad, eta, Heta, res, dir, Hdir, Ynew, Dv, QD, tmp, tmp2;
   xm::DBuf<double> alpha;  // N
   xm::DBuf<double> regd;   // N: App. D diagonal shifts d_i = 2λ/3 (α_i − 1) at the current factor
+  // NEXT-1 matrix-free mode (implicit.cu): frame-sorted measurement copies, K̄⁻¹
+  bool implicit_active = false;
+  xm::DBuf<int32_t> imp_lm;
+  xm::DBuf<double> imp_pts, imp_w, Kinv;
   xm::DBuf<double> lam;    // N × 6 (xx, yy, zz, xy, xz, yz)
   xm::DBuf<double> part;   // SpMM split-K partials: nsplit × nrows × r
   xm::DBuf<double> red;    // block partials for reductions
@@ -349,6 +353,15 @@ void tcg_iteration(xm_ctx* c, int r);
 void axpy(xm_ctx* c, int64_t len, double a, const double* x, double* y);
 void pad_column(xm_ctx* c, int r, const double* Y, double* Yz, const double* v, double* Dz);
 void zmul(xm_ctx* c, const double* x, const double* Zx_q, double* out);  // Zx = Qx − Λx (r = 1)
+// NEXT-1 (implicit.cu)
+void implicit_prepare(xm_ctx* c);
+void implicit_product(xm_ctx* c, const double* V, int r, double* out);
+void implicit_translations(xm_ctx* c, const double* Y3, double* t_out);
+double implicit_normF(xm_ctx* c);
+void splitmix_uniform(xm_ctx* c, int64_t n, uint64_t seed, double* out);  // cert.cu
+// products may use the dense fused kernels (one GPU, Q formed) / fused epilogues too (no App. D)
+inline bool dense_fused(xm_ctx* c) { return c->world == 1 && !c->implicit_active; }
+inline bool fused_epilogues(xm_ctx* c) { return dense_fused(c) && c->opt.scale_reg == 0.0; }
 // App. D (scale_reg λ): scal_out[0] = F(Y), [1] = Σ_{i≥1}(α_i² − 1), [2] = F(Y+D) − F(Y) (D may
 // be NULL); d_i = 2λ/3 (α_i − 1) into c->regd
 void reg_frames(xm_ctx* c, int r, const double* Y, const double* D, double* scal_out);

@@ -39,7 +39,7 @@ class Options(ctypes.Structure):
                 ("lanczos_max", ctypes.c_int32), ("refresh_every", ctypes.c_int32),
                 ("profile", ctypes.c_int32), ("cert_cholesky", ctypes.c_int32),
                 ("spmm_kernel", ctypes.c_int32), ("seed", ctypes.c_uint64),
-                ("scale_reg", ctypes.c_double)]
+                ("scale_reg", ctypes.c_double), ("implicit_q", ctypes.c_int32)]
 
 
 class SolveInfo(ctypes.Structure):
