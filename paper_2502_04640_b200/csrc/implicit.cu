@@ -19,6 +19,8 @@
 // K̄ (N × N), its Cholesky factor and inverse.
 #include "frame_ops.cuh"
 
+#include <cstdlib>
+
 namespace xm {
 
 namespace {
@@ -40,7 +42,9 @@ __global__ void __launch_bounds__(kIT) k_imp_lm_mean(int M, const int32_t* __res
                                                      const double* __restrict__ e_w,
                                                      const double* __restrict__ W,
                                                      const double* __restrict__ V,
-                                                     double* __restrict__ m) {
+                                                     double* __restrict__ m,
+    const int* __restrict__ stop) {
+  if (stop && *stop) return;  // a tCG graph replay past the stop
   const int k = blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (k >= M) return;
   double acc[R];
@@ -69,7 +73,9 @@ __global__ void __launch_bounds__(kIT) k_imp_fr_b(int N, const int32_t* __restri
                                                   const double* __restrict__ f_w,
                                                   const double* __restrict__ V,
                                                   const double* __restrict__ m,
-                                                  double* __restrict__ b) {
+                                                  double* __restrict__ b,
+    const int* __restrict__ stop) {
+  if (stop && *stop) return;  // a tCG graph replay past the stop
   const int i = blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (i >= N) return;
   double vi[3][R], acc[R];
@@ -98,25 +104,170 @@ __global__ void __launch_bounds__(kIT) k_imp_fr_b(int N, const int32_t* __restri
 template <int R>
 __global__ void __launch_bounds__(kIT) k_imp_gemv(int m_, const double* __restrict__ Kinv, int64_t ldk,
                                                   const double* __restrict__ b,
-                                                  double* __restrict__ t) {
+                                                  double* __restrict__ t,
+    const int* __restrict__ stop) {
+  if (stop && *stop) return;  // a tCG graph replay past the stop
   const int j = blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (j >= m_) {
     if (j == m_ && lane < R) t[lane] = 0.0;
     return;
   }
-  const double* row = Kinv + (int64_t)j * ldk;
+  const double* row = Kinv + (int64_t)j * ldk;  // 256-B aligned rows (ldk % 32 == 0)
   double acc[R];
 #pragma unroll
   for (int c = 0; c < R; ++c) acc[c] = 0.0;
-  for (int l = lane; l < m_; l += 32) {
-    const double kv = row[l];
+  // 16-B loads, 4 in flight per lane (2 KB per warp and round)
+  const int m2 = m_ & ~1;
+  int l = 2 * lane;
+  for (; l + 192 < m2; l += 256) {
+    double2 kv[4];
 #pragma unroll
-    for (int c = 0; c < R; ++c) acc[c] = fma(kv, b[(int64_t)(l + 1) * R + c], acc[c]);
+    for (int u = 0; u < 4; ++u) kv[u] = *reinterpret_cast<const double2*>(row + l + 64 * u);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int l0 = l + 64 * u;
+#pragma unroll
+      for (int c = 0; c < R; ++c)
+        acc[c] = fma(kv[u].x, b[(int64_t)(l0 + 1) * R + c], fma(kv[u].y, b[(int64_t)(l0 + 2) * R + c], acc[c]));
+    }
+  }
+  for (; l < m2; l += 64) {
+    const double2 kv = *reinterpret_cast<const double2*>(row + l);
+#pragma unroll
+    for (int c = 0; c < R; ++c)
+      acc[c] = fma(kv.x, b[(int64_t)(l + 1) * R + c], fma(kv.y, b[(int64_t)(l + 2) * R + c], acc[c]));
+  }
+  if (lane == 0 && (m_ & 1)) {
+#pragma unroll
+    for (int c = 0; c < R; ++c) acc[c] = fma(row[m_ - 1], b[(int64_t)m_ * R + c], acc[c]);
   }
   warp_sum<R>(acc);
   if (lane == 0)
 #pragma unroll
     for (int c = 0; c < R; ++c) t[(int64_t)(j + 1) * R + c] = -acc[c];
+}
+
+// Symmetric K̄⁻¹ product over its LOWER triangle only (half the bytes of the
+// row GEMV): CTA = one 64 × 64 tile (I, J ≤ I) of the lower triangle, 256
+// threads (thread = column quarter-row...): row part  Σ_{l∈J} K[i][l] b_l  for
+// its 64 rows → rowp[I][J], and (J < I) column part Σ_{i∈I} K[i][l] b_i for its
+// 64 columns → colp[J][I]; k_imp_symv_fin sums a row's partials in a fixed
+// order (deterministic), t = −(·).
+constexpr int kST = 64;
+__device__ __forceinline__ void tile_of(int64_t tt, int& I, int& J) {
+  int a = (int)((sqrt(8.0 * (double)tt + 1.0) - 1.0) * 0.5);
+  while ((int64_t)(a + 1) * (a + 2) / 2 <= tt) ++a;
+  while ((int64_t)a * (a + 1) / 2 > tt) --a;
+  I = a;
+  J = (int)(tt - (int64_t)a * (a + 1) / 2);
+}
+
+// persistent: CTA c handles tiles c, c + G, …; the next tile's 8 16-B loads per
+// thread are issued before the current tile is reduced (register double buffer)
+template <int R>
+__global__ void __launch_bounds__(256) k_imp_symv_tiles(int m_, int nb, const double* __restrict__ Kinv,
+                                                         int64_t ldk, const double* __restrict__ b,
+                                                         double* __restrict__ rowp,
+                                                         double* __restrict__ colp,
+                                                         const int* __restrict__ stop) {
+  if (stop && *stop) return;
+  const int64_t ntile = (int64_t)nb * (nb + 1) / 2;
+  __shared__ double bJ[kST][R], bI[kST][R];
+  __shared__ double red[8][kST][4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = 2 * lane;
+  auto load = [&](int64_t tt, double2 (&v)[8]) {
+    int I, J;
+    tile_of(tt, I, J);
+    const int r0 = I * kST, c0 = J * kST;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int gr = r0 + warp + 8 * u, gc = c0 + q;
+      v[u] = make_double2(0.0, 0.0);
+      if (gr < m_ && gc + 1 < m_) v[u] = __ldcs(reinterpret_cast<const double2*>(Kinv + (int64_t)gr * ldk + gc));
+      else if (gr < m_ && gc < m_) v[u].x = Kinv[(int64_t)gr * ldk + gc];
+    }
+  };
+  double2 v[8], vn[8];
+  int64_t tt = blockIdx.x;
+  if (tt < ntile) load(tt, v);
+  for (; tt < ntile; tt += gridDim.x) {
+    const int64_t tn = tt + gridDim.x;
+    if (tn < ntile) load(tn, vn);
+    int I, J;
+    tile_of(tt, I, J);
+    const bool diag = (I == J);
+    const int r0 = I * kST, c0 = J * kST;
+    for (int e = threadIdx.x; e < kST * R; e += 256) {
+      const int a = e / R, cc = e % R;
+      bJ[a][cc] = (c0 + a < m_) ? b[(int64_t)(c0 + a + 1) * R + cc] : 0.0;
+      bI[a][cc] = (r0 + a < m_) ? b[(int64_t)(r0 + a + 1) * R + cc] : 0.0;
+    }
+    __syncthreads();
+    double cpa[R], cpb[R];
+#pragma unroll
+    for (int cc = 0; cc < R; ++cc) cpa[cc] = cpb[cc] = 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int aa = warp + 8 * u;
+      const double ka = (!diag || q <= aa) ? v[u].x : 0.0;
+      const double kb = (!diag || q + 1 <= aa) ? v[u].y : 0.0;
+      double rp[R];
+#pragma unroll
+      for (int cc = 0; cc < R; ++cc) rp[cc] = fma(ka, bJ[q][cc], kb * bJ[q + 1][cc]);
+      warp_sum<R>(rp);
+      if (lane == 0)
+#pragma unroll
+        for (int cc = 0; cc < R; ++cc) rowp[(tt * kST + aa) * R + cc] = rp[cc];
+      const double sa = (!diag || q < aa) ? v[u].x : 0.0;
+      const double sb = (!diag || q + 1 < aa) ? v[u].y : 0.0;
+#pragma unroll
+      for (int cc = 0; cc < R; ++cc) {
+        cpa[cc] = fma(sa, bI[aa][cc], cpa[cc]);
+        cpb[cc] = fma(sb, bI[aa][cc], cpb[cc]);
+      }
+    }
+#pragma unroll
+    for (int c0r = 0; c0r < R; c0r += 4) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (c0r + k < R) {
+          red[warp][q][k] = cpa[c0r + k];
+          red[warp][q + 1][k] = cpb[c0r + k];
+        }
+      __syncthreads();
+      for (int e = threadIdx.x; e < kST * 4; e += 256) {
+        const int l = e >> 2, k = e & 3;
+        if (c0r + k < R) {
+          double sum = 0.0;
+#pragma unroll
+          for (int w = 0; w < 8; ++w) sum += red[w][l][k];
+          colp[(tt * kST + l) * R + c0r + k] = sum;
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = vn[u];
+  }
+}
+
+// t_{g+1} = −( Σ_{J ≤ I} rowp[tile(I,J)][a] + Σ_{I' ≥ I} colp[tile(I',I)][a] ),  g = I·64 + a
+template <int R>
+__global__ void k_imp_symv_fin(int m_, int nb, const double* __restrict__ rowp,
+                               const double* __restrict__ colp, double* __restrict__ t,
+                               const int* __restrict__ stop) {
+  if (stop && *stop) return;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e == 0)
+#pragma unroll
+    for (int cc = 0; cc < R; ++cc) t[cc] = 0.0;
+  if (e >= (int64_t)m_ * R) return;
+  const int g = (int)(e / R), cc = (int)(e % R);
+  const int I = g / kST, a = g % kST;
+  double s = 0.0;
+  for (int J = 0; J <= I; ++J) s += rowp[(((int64_t)I * (I + 1) / 2 + J) * kST + a) * R + cc];
+  for (int I2 = I; I2 < nb; ++I2) s += colp[(((int64_t)I2 * (I2 + 1) / 2 + I) * kST + a) * R + cc];
+  t[(int64_t)(g + 1) * R + cc] = -s;
 }
 
 // p_k = m_k + Σ_{e∈k} w_e t_{i_e} / W_k
@@ -127,7 +278,9 @@ __global__ void __launch_bounds__(kIT) k_imp_lm_p(int M, const int32_t* __restri
                                                   const double* __restrict__ W,
                                                   const double* __restrict__ t,
                                                   const double* __restrict__ m,
-                                                  double* __restrict__ p) {
+                                                  double* __restrict__ p,
+    const int* __restrict__ stop) {
+  if (stop && *stop) return;  // a tCG graph replay past the stop
   const int k = blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (k >= M) return;
   double acc[R];
@@ -156,7 +309,9 @@ __global__ void __launch_bounds__(kIT) k_imp_fr_out(int N, const int32_t* __rest
                                                     const double* __restrict__ V,
                                                     const double* __restrict__ t,
                                                     const double* __restrict__ p,
-                                                    double* __restrict__ out) {
+                                                    double* __restrict__ out,
+    const int* __restrict__ stop) {
+  if (stop && *stop) return;  // a tCG graph replay past the stop
   const int i = blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (i >= N) return;
   double vi[3][R], ti[R], acc[3 * R];
@@ -250,7 +405,7 @@ void implicit_prepare(xm_ctx* c) {
   }
 }
 
-void implicit_product(xm_ctx* c, const double* V, int r, double* out) {
+void implicit_product(xm_ctx* c, const double* V, int r, double* out, const int* stop) {
   const int N = c->N, M = c->M;
   DBuf<double>& m = scratch_f64(c, "imp_m");
   DBuf<double>& p = scratch_f64(c, "imp_p");
@@ -262,19 +417,37 @@ void implicit_product(xm_ctx* c, const double* V, int r, double* out) {
   t.alloc((size_t)N * XM_MAX_R + 8);
   const int gM = ceil_div(M, kIT / 32), gN = ceil_div(N, kIT / 32), gK = ceil_div(N, kIT / 32);
   XM_IMP_DISPATCH(r, (k_imp_lm_mean<R><<<gM, kIT, 0, c->stream>>>(M, c->lm_off.p, c->e_fr.p, c->e_pts.p,
-                                                                  c->e_w.p, c->W.p, V, m.p)));
+                                                                  c->e_w.p, c->W.p, V, m.p, stop)));
   XM_IMP_DISPATCH(r, (k_imp_fr_b<R><<<gN, kIT, 0, c->stream>>>(N, c->fr_off.p, c->imp_lm.p, c->imp_pts.p,
-                                                               c->imp_w.p, V, m.p, b.p)));
-  if (N > 1) {
-    XM_IMP_DISPATCH(r, (k_imp_gemv<R><<<gK, kIT, 0, c->stream>>>(N - 1, c->Kinv.p, c->ldk, b.p, t.p)));
+                                                               c->imp_w.p, V, m.p, b.p, stop)));
+  // K̄⁻¹ b: the row GEMV over the full (mirrored) K̄⁻¹ (E: 826 MB, 217 µs) is the
+  // default; the lower-triangle variant (XM_IMP_SYMV=1: 415 MB + 39 MB of
+  // partials) measured 195 + 37 µs — it is bound by its per-tile reductions,
+  // not by the bytes (profiles/r2_implicit_E.txt)
+  if (N > 1 && std::getenv("XM_IMP_SYMV")) {
+    const int mK = N - 1, nb = ceil_div(mK, kST);
+    const int64_t ntile = (int64_t)nb * (nb + 1) / 2;
+    DBuf<double>& rp = scratch_f64(c, "imp_rowp");
+    DBuf<double>& cp = scratch_f64(c, "imp_colp");
+    rp.alloc((size_t)ntile * kST * XM_MAX_R + 8);
+    cp.alloc((size_t)ntile * kST * XM_MAX_R + 8);
+    const unsigned gsym = (unsigned)std::min<int64_t>(ntile, 148 * 8);
+    XM_IMP_DISPATCH(r, (k_imp_symv_tiles<R><<<gsym, 256, 0, c->stream>>>(
+                           mK, nb, c->Kinv.p, c->ldk, b.p, rp.p, cp.p, stop)));
+    XM_IMP_DISPATCH(r, (k_imp_symv_fin<R><<<ceil_div((int64_t)mK * r, 256), 256, 0, c->stream>>>(
+                           mK, nb, rp.p, cp.p, t.p, stop)));
+    count_launch(c);
+  } else if (N > 1) {
+    XM_IMP_DISPATCH(r, (k_imp_gemv<R><<<gK, kIT, 0, c->stream>>>(N - 1, c->Kinv.p, c->ldk, b.p, t.p,
+                                                                 stop)));
   } else {
     XM_CUDA(cudaMemsetAsync(t.p, 0, (size_t)r * 8, c->stream));
   }
   XM_IMP_DISPATCH(r, (k_imp_lm_p<R><<<gM, kIT, 0, c->stream>>>(M, c->lm_off.p, c->e_fr.p, c->e_w.p, c->W.p,
-                                                               t.p, m.p, p.p)));
+                                                               t.p, m.p, p.p, stop)));
   XM_IMP_DISPATCH(r, (k_imp_fr_out<R><<<gN, kIT, 0, c->stream>>>(N, c->fr_off.p, c->imp_lm.p,
                                                                  c->imp_pts.p, c->imp_w.p, V, t.p, p.p,
-                                                                 out)));
+                                                                 out, stop)));
   XM_CHECK_LAUNCH();
   count_launch(c, 5);
 }
@@ -288,10 +461,10 @@ void implicit_translations(xm_ctx* c, const double* Y3, double* t_out) {
   b.alloc((size_t)N * XM_MAX_R + 8);
   const int gM = ceil_div(M, kIT / 32), gN = ceil_div(N, kIT / 32);
   k_imp_lm_mean<3><<<gM, kIT, 0, c->stream>>>(M, c->lm_off.p, c->e_fr.p, c->e_pts.p, c->e_w.p, c->W.p, Y3,
-                                              m.p);
+                                              m.p, nullptr);
   k_imp_fr_b<3><<<gN, kIT, 0, c->stream>>>(N, c->fr_off.p, c->imp_lm.p, c->imp_pts.p, c->imp_w.p, Y3, m.p,
-                                           b.p);
-  if (N > 1) k_imp_gemv<3><<<gN, kIT, 0, c->stream>>>(N - 1, c->Kinv.p, c->ldk, b.p, t_out);
+                                           b.p, nullptr);
+  if (N > 1) k_imp_gemv<3><<<gN, kIT, 0, c->stream>>>(N - 1, c->Kinv.p, c->ldk, b.p, t_out, nullptr);
   else XM_CUDA(cudaMemsetAsync(t_out, 0, 3 * 8, c->stream));
   XM_CHECK_LAUNCH();
   count_launch(c, 3);
@@ -318,7 +491,7 @@ double implicit_normF(xm_ctx* c) {
       XM_CHECK_LAUNCH();
       count_launch(c);
     }
-    implicit_product(c, Z.p, kBatch, QZ.p);
+    implicit_product(c, Z.p, kBatch, QZ.p, nullptr);
     dot_flat(c, QZ.p, QZ.p, n * kBatch, part.p, kDotBlocks);
     reduce_partials(c, part.p, kDotBlocks, 1, c->scal.p + 30);
     double s = 0.0;

@@ -592,7 +592,7 @@ __global__ void k_unpack_cols(int64_t n, int r, int c0, int w, const double* __r
 void spmm_full(xm_ctx* c, const double* V, int r, double* out_full, const int* stop) {
   if (c->implicit_active) {  // NEXT-1: matrix-free (implicit.cu); after a tCG stop the
     // passes still run inside a graph replay, their result is ignored by the update kernels
-    implicit_product(c, V, r, out_full);
+    implicit_product(c, V, r, out_full, stop);
     c->stats.spmm_calls++;
     return;
   }

@@ -355,7 +355,7 @@ void pad_column(xm_ctx* c, int r, const double* Y, double* Yz, const double* v, 
 void zmul(xm_ctx* c, const double* x, const double* Zx_q, double* out);  // Zx = Qx − Λx (r = 1)
 // NEXT-1 (implicit.cu)
 void implicit_prepare(xm_ctx* c);
-void implicit_product(xm_ctx* c, const double* V, int r, double* out);
+void implicit_product(xm_ctx* c, const double* V, int r, double* out, const int* stop = nullptr);
 void implicit_translations(xm_ctx* c, const double* Y3, double* t_out);
 double implicit_normF(xm_ctx* c);
 void splitmix_uniform(xm_ctx* c, int64_t n, uint64_t seed, double* out);  // cert.cu
