@@ -297,6 +297,9 @@ def main():
     ap.add_argument("--impl", default="xm", choices=["xm", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="dense", choices=["dense", "implicit"],
+                    help="headline mode: dense Q (default) or the matrix-free NEXT-1 products; "
+                         "the other mode is measured too (one GPU) and reported under 'other_mode'")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -328,8 +331,9 @@ def main():
                    t=torch.empty((sc.N, 3), dtype=torch.float64, device=dev),
                    p=torch.empty((sc.M, 3), dtype=torch.float64, device=dev))
     stream = torch.cuda.current_stream(dev)
+    implicit = 1 if (args.mode == "implicit" and world == 1) else 0
     ctx = xm.Context(device=local, rank=rank, world=world, nccl_id=nccl_id,
-                     stream=stream.cuda_stream, profile=0)
+                     stream=stream.cuda_stream, profile=0, implicit_q=implicit)
 
     def step(inputs, outputs):
         ctx.build_Q(sc.N, sc.M, *inputs)
@@ -415,7 +419,8 @@ def main():
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"config {args.config}: {CONFIG_DESCRIPTIONS[args.config]}",
                    "N": sc.N, "M": sc.M, "E": sc.E, "seed": args.seed,
-                   "parallelism": f"rows{world}", "l2": "inputs larger than L2 (Q > 126 MB)"},
+                   "mode": "implicit (NEXT-1)" if implicit else "dense Q",
+                   "parallelism": f"bands{world}", "l2": "inputs larger than L2 (Q > 126 MB)"},
         "hvp_per_s": info["hvps"] / value if value > 0 else None,
         "solve": {"hvps": info["hvps"], "spmms": info["spmms"], "lanczos_steps": info["lanczos_steps"],
                   "outer_iters": info["outer_iters"], "r": info["r"], "escapes": info["escapes"],
@@ -443,6 +448,39 @@ def main():
     }
     clocks = clk.summary()
     result["clocks"] = clocks
+    if world == 1:
+        # the other product mode on the same workload (SURVEY §8(f) NEXT-1 vs the dense stream)
+        other = 1 - implicit
+        with xm.Context(device=local, stream=stream.cuda_stream, profile=0, implicit_q=other) as c2:
+            def step2():
+                c2.build_Q(sc.N, sc.M, *dev_in)
+                st2, info2 = c2.solve(3)
+                cert2 = c2.certify()
+                c2.round_recover_into(**out_dev)
+                return st2, info2, cert2
+            for _ in range(2):
+                step2()
+            torch.cuda.synchronize()
+            c2.reset_stats()
+            o0 = torch.cuda.Event(enable_timing=True)
+            o1 = torch.cuda.Event(enable_timing=True)
+            o0.record(stream)
+            k2 = min(args.steps, 5)
+            for _ in range(k2):
+                st2, info2, cert2 = step2()
+            o1.record(stream)
+            torch.cuda.synchronize()
+            s2 = c2.stats()
+            n_ = 3 * sc.N
+            per_product = (8.0 * n_ * (n_ + 1) / 2 + 16.0 * n_ * 3) if other == 0 else \
+                (sc.E * (36 + 36 + 12 + 36) + 8.0 * (sc.N - 1) ** 2)
+            result["other_mode"] = {
+                "mode": "dense" if other == 0 else "implicit (NEXT-1, Q never formed)",
+                "value": o0.elapsed_time(o1) / k2 / 1e3, "unit": "s", "steps": k2,
+                "phases_ms": {k: s2[k] / k2 for k in ("ms_build", "ms_solve", "ms_certify", "ms_round")},
+                "hvps": info2["hvps"], "spmms": info2["spmms"], "r": info2["r"],
+                "certified": info2["certified"], "eta": cert2["eta"], "status": st2,
+                "alg_bytes_per_product": per_product}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         est = OracleEstimate(sc, args.config)
         if est.available():
