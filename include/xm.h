@@ -245,6 +245,35 @@ xm_status xm_edge_residuals(xm_ctx* ctx, double* res);
 xm_status xm_xm2(xm_ctx* ctx, double drop_fraction, uint8_t* keep, int64_t* n_dropped,
                  int64_t* n_restored);
 
+/* ------------------------------------------- batched small instances (NEXT-4) */
+typedef struct {
+  double f;               /* final objective ⟨Y, QY⟩                              */
+  double grad_norm;
+  double lambda_min;      /* λ_min(Z) by Lanczos (O6) at the final point          */
+  double normQ;           /* ‖Q‖_F of the instance (tolerance scale)              */
+  int32_t r;              /* final rank                                          */
+  int32_t certified;
+  int32_t status;         /* 0, XM_UNCERTIFIED, XM_NOT_CONVERGED, XM_ERETRACT,    */
+                          /* XM_EESCAPE (per instance)                            */
+  int32_t hvps;
+  int32_t outer_iters;
+  int32_t lanczos_steps;
+} xm_batch_result;
+/* B independent small instances, each the whole Algorithm 1 from
+ * its own start — Thm 3's random-initialisation trials and App. G's
+ * noise sweeps — in ONE launch: one CTA per instance, Q and all
+ * vectors in shared memory.  Q: B matrices n×n
+ * (row-major, n = 3N, caller memory, host or device), instance b at
+ * Q + b·q_stride (q_stride = 0: one Q shared by every instance); Y0: B × n × r0
+ * feasible starts; Y_out: B × n × 8 (row-major, stride 8, columns ≥ r zero);
+ * res: B results.  Options (tolerances, TR / tCG constants, rank_cap ≤ 8,
+ * seed) from the context; no App. D term.  Needs a context (for its device and
+ * stream) but no xm_build_Q.  XM_EINVAL unless 1 ≤ N ≤ 24, 3 ≤ r0 ≤
+ * min(rank_cap, 8), B ≥ 1.  Per-instance failures are reported in res, not as
+ * the call's status. */
+xm_status xm_solve_batch(xm_ctx* ctx, int32_t B, int32_t N, const double* Q, int64_t q_stride,
+                         const double* Y0, int32_t r0, double* Y_out, xm_batch_result* res);
+
 /* ----------------------------------------------------- test / bench hooks */
 /* S's co-visibility BSR pattern (H3): rowptr N+1 (int64), colidx nnzb (int32,
  * sorted per row).  Call with colidx == NULL to query *nnzb. */

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libxm.so")
 OBJ = os.path.join(HERE, "build")
-SOURCES = ["util.cu", "assembly.cu", "spmm.cu", "spmm_sym.cu", "tcg_persist.cu", "manifold.cu", "cert.cu", "comm.cu", "dgemm_tn.cu", "implicit.cu", "xm2.cu", "xm_api.cu"]
+SOURCES = ["util.cu", "assembly.cu", "spmm.cu", "spmm_sym.cu", "tcg_persist.cu", "manifold.cu", "cert.cu", "comm.cu", "dgemm_tn.cu", "implicit.cu", "batch.cu", "xm2.cu", "xm_api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include")]

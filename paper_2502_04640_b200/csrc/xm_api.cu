@@ -1035,6 +1035,44 @@ xm_status xm_tcg(xm_ctx* c, const double* Y, int32_t r, double Delta, int32_t pa
   });
 }
 
+xm_status xm_solve_batch(xm_ctx* c, int32_t B, int32_t N, const double* Q, int64_t q_stride,
+                         const double* Y0, int32_t r0, double* Y_out, xm_batch_result* res) {
+  if (!c || B < 1 || N < 1 || !Q || !Y0 || !Y_out || !res || q_stride < 0) return XM_EINVAL;
+  return guard(c, [&] {
+    NvtxRange nvtx_("xm_solve_batch");
+    const int64_t n = 3 * (int64_t)N;
+    const int64_t qcount = q_stride == 0 ? n * n : (B - 1) * q_stride + n * n;
+    const double* Qd = Q;
+    const double* Yd = Y0;
+    DBuf<double>& qb = scratch_f64(c, "batch_q");
+    DBuf<double>& yb = scratch_f64(c, "batch_y0");
+    DBuf<double>& yo = scratch_f64(c, "batch_yout");
+    DBuf<uint64_t>& rb = scratch_u64(c, "batch_res");
+    if (!is_device_ptr(Q)) {
+      qb.alloc((size_t)qcount);
+      copy_in(c, qb.p, Q, (size_t)qcount * 8);
+      Qd = qb.p;
+    }
+    if (!is_device_ptr(Y0)) {
+      yb.alloc((size_t)B * n * r0);
+      copy_in(c, yb.p, Y0, (size_t)B * n * r0 * 8);
+      Yd = yb.p;
+    }
+    const bool dev_out = is_device_ptr(Y_out);
+    double* Yo = Y_out;
+    if (!dev_out) {
+      yo.alloc((size_t)B * n * 8);
+      Yo = yo.p;
+    }
+    rb.alloc((sizeof(xm_batch_result) * (size_t)B + 7) / 8);
+    xm_batch_result* rd = reinterpret_cast<xm_batch_result*>(rb.p);
+    batch_staircase(c, B, N, Qd, q_stride, Yd, r0, Yo, rd);
+    if (!dev_out) copy_out(c, Y_out, Yo, (size_t)B * n * 8 * 8);
+    copy_out(c, res, rd, sizeof(xm_batch_result) * (size_t)B);
+    sync(c);
+  });
+}
+
 xm_status xm_project(xm_ctx* c, const double* Y, const double* W, double* out, int32_t r) {
   if (!c || !Y || !W || !out || r < 1 || r > XM_MAX_R) return XM_EINVAL;
   return guard(c, [&] {

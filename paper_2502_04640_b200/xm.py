@@ -63,6 +63,14 @@ class Certificate(ctypes.Structure):
                 ("method", ctypes.c_int32), ("lower_rigorous", ctypes.c_int32)]
 
 
+class BatchResult(ctypes.Structure):
+    _fields_ = [("f", ctypes.c_double), ("grad_norm", ctypes.c_double),
+                ("lambda_min", ctypes.c_double), ("normQ", ctypes.c_double),
+                ("r", ctypes.c_int32), ("certified", ctypes.c_int32), ("status", ctypes.c_int32),
+                ("hvps", ctypes.c_int32), ("outer_iters", ctypes.c_int32),
+                ("lanczos_steps", ctypes.c_int32)]
+
+
 class Stats(ctypes.Structure):
     _fields_ = [("kernel_launches", ctypes.c_int64), ("spmm_calls", ctypes.c_int64),
                 ("spmm_rows", ctypes.c_int64), ("spmm_ms", ctypes.c_double),
@@ -99,6 +107,8 @@ _SIGS = {
     "xm_hvp": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_int32]),
     "xm_tcg": (ctypes.c_int, [_P, _P, ctypes.c_int32, ctypes.c_double, ctypes.c_int32, _P, _P, _P, _P]),
     "xm_project": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_int32]),
+    "xm_solve_batch": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int32, _P, ctypes.c_int64, _P,
+                                      ctypes.c_int32, _P, _P]),
     "xm_retract": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_int32]),
     "xm_get_factor": (ctypes.c_int, [_P, _P, _P]),
     "xm_set_factor": (ctypes.c_int, [_P, _P, ctypes.c_int32]),
@@ -354,6 +364,21 @@ class Context:
         self._check(self.lib.xm_hvp(self.h, _in_ptr(Y, np.float64, keep), _in_ptr(V, np.float64, keep),
                                     p, r), "xm_hvp")
         return arr
+
+    def solve_batch(self, Q, Y0, shared_Q: bool = False):
+        """B small instances at once (xm_solve_batch, NEXT-4).  Q: (B, n, n) or,
+        with shared_Q, one (n, n); Y0: (B, n, r0).  Returns (Y (B, n, 8), results
+        as a list of dicts)."""
+        Q = np.ascontiguousarray(Q, dtype=np.float64)
+        Y0 = np.ascontiguousarray(Y0, dtype=np.float64)
+        B, n, r0 = Y0.shape
+        Yo = np.empty((B, n, 8))
+        res = (BatchResult * B)()
+        stride = 0 if shared_Q else n * n
+        self._check(self.lib.xm_solve_batch(self.h, B, n // 3, Q.ctypes.data, stride, Y0.ctypes.data, r0,
+                                            Yo.ctypes.data, ctypes.cast(res, ctypes.c_void_p)),
+                    "xm_solve_batch")
+        return Yo, [_to_dict(r) for r in res]
 
     TCG_STOP = {1: "negcurv", 2: "exceeded", 3: "converged", 4: "maxinner"}
     TCG_PATHS = {"auto": 0, "persist_sym": 1, "persist": 2, "fused": 3, "three_kernel": 4}

@@ -55,6 +55,7 @@ def test_struct_layouts_match_header():
     src = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
     structs = {name: body for body, name in re.findall(r"typedef struct \{([^{}]*)\}\s*(\w+);", src)}
     for cname, py in (("xm_options", xm.Options), ("xm_solve_info", xm.SolveInfo),
+                      ("xm_batch_result", xm.BatchResult),
                       ("xm_certificate", xm.Certificate), ("xm_stats", xm.Stats)):
         body = structs[cname]
         names = re.findall(r"\b([a-zA-Z_][a-zA-Z_0-9]*)\s*[,;]", body)
