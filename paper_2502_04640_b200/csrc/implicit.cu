@@ -19,12 +19,14 @@
 // K̄ (N × N), its Cholesky factor and inverse.
 #include "frame_ops.cuh"
 
+#include <cstdio>
 #include <cstdlib>
 
 namespace xm {
 
 namespace {
 constexpr int kIT = 256;  // threads per block (8 warps)
+constexpr int kU = 4;     // measurements per lane in flight (ILP of the gather passes)
 
 template <int K>
 __device__ __forceinline__ void warp_sum(double (&a)[K]) {
@@ -34,325 +36,332 @@ __device__ __forceinline__ void warp_sum(double (&a)[K]) {
     for (int q = 0; q < K; ++q) a[q] += __shfl_xor_sync(0xffffffffu, a[q], o);
 }
 
-// m_k = Σ_{e∈k} w_e z_e / W_k, z_e = V_iᵀ ũ_e
+// Every pass is one warp per landmark or frame walking its contiguous run of
+// measurements.  The tail of a run is handled by CLAMPED unconditional loads
+// with zeroed weights, never by predicated loads: the predicated-load form of
+// this unrolled loop faulted on sm_100a with data-dependent addresses (the
+// gathered index register picking up a V value; reproduced only for
+// non-integer V, fixed by this form — DESIGN.md §5).
+//
+// measurements, kU per lane in flight (all index / coefficient loads of a
+// round issued before the dependent L2 gathers), then a fixed-order warp
+// reduction: deterministic.  Per-measurement streams are read evict-first
+// (__ldcs) so the gathered n × r arrays (≤ 1.5 MB) stay in L2.
+
+// m_k = Σ_{e∈k} (w_e ũ_e)ᵀ V_{i_e} / W_k          (landmark-sorted, 28 B / measurement)
 template <int R>
 __global__ void __launch_bounds__(kIT) k_imp_lm_mean(int M, const int32_t* __restrict__ lm_off,
-                                                     const int32_t* __restrict__ e_fr,
-                                                     const double* __restrict__ e_pts,
-                                                     const double* __restrict__ e_w,
+                                                     const int32_t* __restrict__ L_i,
+                                                     const double* __restrict__ L_wx,
+                                                     const double* __restrict__ L_wy,
+                                                     const double* __restrict__ L_wz,
                                                      const double* __restrict__ W,
                                                      const double* __restrict__ V,
                                                      double* __restrict__ m,
-    const int* __restrict__ stop) {
+                                                     const int* __restrict__ stop) {
   if (stop && *stop) return;  // a tCG graph replay past the stop
   const int k = blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (k >= M) return;
   double acc[R];
 #pragma unroll
   for (int c = 0; c < R; ++c) acc[c] = 0.0;
-  for (int e = lm_off[k] + lane; e < lm_off[k + 1]; e += 32) {
-    const int i = e_fr[e];
-    const double u0 = e_pts[3 * e], u1 = e_pts[3 * e + 1], u2 = e_pts[3 * e + 2], we = e_w[e];
-    const double* vi = V + (int64_t)3 * i * R;
+  const int lo = lm_off[k], hi = lm_off[k + 1];
+  for (int e0 = lo + lane; e0 < hi; e0 += 32 * kU) {
+    int ii[kU];
+    double a0[kU], a1[kU], a2[kU];
 #pragma unroll
-    for (int c = 0; c < R; ++c) acc[c] = fma(we, fma(vi[c], u0, fma(vi[R + c], u1, vi[2 * R + c] * u2)), acc[c]);
-  }
-  warp_sum<R>(acc);
-  if (lane == 0) {
-    const double wk = W[k], inv = wk > 0.0 ? 1.0 / wk : 0.0;
+    for (int q = 0; q < kU; ++q) {
+      const int e = min(e0 + 32 * q, hi - 1);  // clamped: loads unconditional, tail weights zeroed
+      const double okw = (e0 + 32 * q < hi) ? 1.0 : 0.0;
+      ii[q] = __ldcs(L_i + e);
+      a0[q] = okw * __ldcs(L_wx + e);
+      a1[q] = okw * __ldcs(L_wy + e);
+      a2[q] = okw * __ldcs(L_wz + e);
+    }
 #pragma unroll
-    for (int c = 0; c < R; ++c) m[(int64_t)k * R + c] = acc[c] * inv;
-  }
-}
-
-// b_i = Σ_{e∈i} w_e (z_e − m_k), i ≥ 1 (frame-sorted copies f_lm, f_pts, f_w)
-template <int R>
-__global__ void __launch_bounds__(kIT) k_imp_fr_b(int N, const int32_t* __restrict__ fr_off,
-                                                  const int32_t* __restrict__ f_lm,
-                                                  const double* __restrict__ f_pts,
-                                                  const double* __restrict__ f_w,
-                                                  const double* __restrict__ V,
-                                                  const double* __restrict__ m,
-                                                  double* __restrict__ b,
-    const int* __restrict__ stop) {
-  if (stop && *stop) return;  // a tCG graph replay past the stop
-  const int i = blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (i >= N) return;
-  double vi[3][R], acc[R];
+    for (int q = 0; q < kU; ++q) {
+      const double* vi = V + (int64_t)3 * ii[q] * R;
 #pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int c = 0; c < R; ++c) vi[a][c] = V[((int64_t)3 * i + a) * R + c];
-#pragma unroll
-  for (int c = 0; c < R; ++c) acc[c] = 0.0;
-  for (int q = fr_off[i] + lane; q < fr_off[i + 1]; q += 32) {
-    const int k = f_lm[q];
-    const double u0 = f_pts[3 * q], u1 = f_pts[3 * q + 1], u2 = f_pts[3 * q + 2], we = f_w[q];
-#pragma unroll
-    for (int c = 0; c < R; ++c) {
-      const double z = fma(vi[0][c], u0, fma(vi[1][c], u1, vi[2][c] * u2));
-      acc[c] = fma(we, z - m[(int64_t)k * R + c], acc[c]);
+      for (int c = 0; c < R; ++c) acc[c] = fma(a0[q], vi[c], fma(a1[q], vi[R + c], fma(a2[q], vi[2 * R + c], acc[c])));
     }
   }
   warp_sum<R>(acc);
-  if (lane == 0)
+  if (lane < R) {
+    const double wk = W[k], inv = wk > 0.0 ? 1.0 / wk : 0.0;
+    double v = acc[0];
 #pragma unroll
-    for (int c = 0; c < R; ++c) b[(int64_t)i * R + c] = acc[c];
+    for (int c = 1; c < R; ++c) v = (lane == c) ? acc[c] : v;
+    m[(int64_t)k * R + lane] = v * inv;
+  }
 }
 
-// t_{j+1} = −Σ_l Kinv[j][l] b_{l+1}  (rows j = 0..N−2), t_0 = 0
+// b_i = Σ_{e∈i} w_e (z_e − m_k) = c_iᵀ V_i − Σ_{e∈i} w_e m_k  (c_i = Σ_{e∈i} w_e ũ_e),
+// i ≥ 1, written to bs[i − 1] (the K̄ ordering: the anchor row is dropped)
+// (frame-sorted, 12 B / measurement)
+template <int R>
+__global__ void __launch_bounds__(kIT) k_imp_fr_b(int N, const int32_t* __restrict__ fr_off,
+                                                  const int32_t* __restrict__ F_k,
+                                                  const double* __restrict__ F_w,
+                                                  const double* __restrict__ cfr,
+                                                  const double* __restrict__ V,
+                                                  const double* __restrict__ m,
+                                                  double* __restrict__ bs,
+                                                  const int* __restrict__ stop) {
+  if (stop && *stop) return;  // a tCG graph replay past the stop
+  const int i = 1 + blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (i >= N) return;
+  double acc[R];
+#pragma unroll
+  for (int c = 0; c < R; ++c) acc[c] = 0.0;
+  const int lo = fr_off[i], hi = fr_off[i + 1];
+  for (int q0 = lo + lane; q0 < hi; q0 += 32 * kU) {
+    int kk[kU];
+    double we[kU];
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const int e = min(q0 + 32 * q, hi - 1);
+      kk[q] = __ldcs(F_k + e);
+      we[q] = ((q0 + 32 * q < hi) ? 1.0 : 0.0) * __ldcs(F_w + e);
+    }
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const double* mk = m + (int64_t)kk[q] * R;
+#pragma unroll
+      for (int c = 0; c < R; ++c) acc[c] = fma(we[q], mk[c], acc[c]);
+    }
+  }
+  warp_sum<R>(acc);
+  if (lane < R) {
+    double s = acc[0];
+#pragma unroll
+    for (int c = 1; c < R; ++c) s = (lane == c) ? acc[c] : s;
+    const double* vi = V + (int64_t)3 * i * R + lane;
+    const double* ci = cfr + 3 * (int64_t)i;
+    bs[(int64_t)(i - 1) * R + lane] = fma(ci[0], vi[0], fma(ci[1], vi[R], ci[2] * vi[2 * R])) - s;
+  }
+}
+
+// Row GEMV over the full (mirrored) K̄⁻¹ for r > 5 (the lower-triangle stream
+// of spmm_sym.cu covers r ≤ 5):  tb[j + 1] = Σ_l K̄⁻¹[j][l] bs[l]  (tb[0] = 0;
+// the translations are t_i = −tb[i])
 template <int R>
 __global__ void __launch_bounds__(kIT) k_imp_gemv(int m_, const double* __restrict__ Kinv, int64_t ldk,
-                                                  const double* __restrict__ b,
-                                                  double* __restrict__ t,
-    const int* __restrict__ stop) {
+                                                  const double* __restrict__ bs,
+                                                  double* __restrict__ tb,
+                                                  const int* __restrict__ stop) {
   if (stop && *stop) return;  // a tCG graph replay past the stop
   const int j = blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (j >= m_) {
-    if (j == m_ && lane < R) t[lane] = 0.0;
-    return;
-  }
+  if (j >= m_) return;
   const double* row = Kinv + (int64_t)j * ldk;  // 256-B aligned rows (ldk % 32 == 0)
   double acc[R];
 #pragma unroll
   for (int c = 0; c < R; ++c) acc[c] = 0.0;
-  // 16-B loads, 4 in flight per lane (2 KB per warp and round)
   const int m2 = m_ & ~1;
   int l = 2 * lane;
   for (; l + 192 < m2; l += 256) {
     double2 kv[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) kv[u] = *reinterpret_cast<const double2*>(row + l + 64 * u);
+    for (int u = 0; u < 4; ++u) kv[u] = __ldcs(reinterpret_cast<const double2*>(row + l + 64 * u));
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int l0 = l + 64 * u;
 #pragma unroll
       for (int c = 0; c < R; ++c)
-        acc[c] = fma(kv[u].x, b[(int64_t)(l0 + 1) * R + c], fma(kv[u].y, b[(int64_t)(l0 + 2) * R + c], acc[c]));
+        acc[c] = fma(kv[u].x, bs[(int64_t)l0 * R + c], fma(kv[u].y, bs[(int64_t)(l0 + 1) * R + c], acc[c]));
     }
   }
   for (; l < m2; l += 64) {
     const double2 kv = *reinterpret_cast<const double2*>(row + l);
 #pragma unroll
     for (int c = 0; c < R; ++c)
-      acc[c] = fma(kv.x, b[(int64_t)(l + 1) * R + c], fma(kv.y, b[(int64_t)(l + 2) * R + c], acc[c]));
+      acc[c] = fma(kv.x, bs[(int64_t)l * R + c], fma(kv.y, bs[(int64_t)(l + 1) * R + c], acc[c]));
   }
   if (lane == 0 && (m_ & 1)) {
 #pragma unroll
-    for (int c = 0; c < R; ++c) acc[c] = fma(row[m_ - 1], b[(int64_t)m_ * R + c], acc[c]);
+    for (int c = 0; c < R; ++c) acc[c] = fma(row[m_ - 1], bs[(int64_t)(m_ - 1) * R + c], acc[c]);
   }
   warp_sum<R>(acc);
   if (lane == 0)
 #pragma unroll
-    for (int c = 0; c < R; ++c) t[(int64_t)(j + 1) * R + c] = -acc[c];
+    for (int c = 0; c < R; ++c) tb[(int64_t)(j + 1) * R + c] = acc[c];
 }
 
-// Symmetric K̄⁻¹ product over its LOWER triangle only (half the bytes of the
-// row GEMV): CTA = one 64 × 64 tile (I, J ≤ I) of the lower triangle, 256
-// threads (thread = column quarter-row...): row part  Σ_{l∈J} K[i][l] b_l  for
-// its 64 rows → rowp[I][J], and (J < I) column part Σ_{i∈I} K[i][l] b_i for its
-// 64 columns → colp[J][I]; k_imp_symv_fin sums a row's partials in a fixed
-// order (deterministic), t = −(·).
-constexpr int kST = 64;
-__device__ __forceinline__ void tile_of(int64_t tt, int& I, int& J) {
-  int a = (int)((sqrt(8.0 * (double)tt + 1.0) - 1.0) * 0.5);
-  while ((int64_t)(a + 1) * (a + 2) / 2 <= tt) ++a;
-  while ((int64_t)a * (a + 1) / 2 > tt) --a;
-  I = a;
-  J = (int)(tt - (int64_t)a * (a + 1) / 2);
-}
-
-// persistent: CTA c handles tiles c, c + G, …; the next tile's 8 16-B loads per
-// thread are issued before the current tile is reduced (register double buffer)
-template <int R>
-__global__ void __launch_bounds__(256) k_imp_symv_tiles(int m_, int nb, const double* __restrict__ Kinv,
-                                                         int64_t ldk, const double* __restrict__ b,
-                                                         double* __restrict__ rowp,
-                                                         double* __restrict__ colp,
-                                                         const int* __restrict__ stop) {
-  if (stop && *stop) return;
-  const int64_t ntile = (int64_t)nb * (nb + 1) / 2;
-  __shared__ double bJ[kST][R], bI[kST][R];
-  __shared__ double red[8][kST][4];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = 2 * lane;
-  auto load = [&](int64_t tt, double2 (&v)[8]) {
-    int I, J;
-    tile_of(tt, I, J);
-    const int r0 = I * kST, c0 = J * kST;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int gr = r0 + warp + 8 * u, gc = c0 + q;
-      v[u] = make_double2(0.0, 0.0);
-      if (gr < m_ && gc + 1 < m_) v[u] = __ldcs(reinterpret_cast<const double2*>(Kinv + (int64_t)gr * ldk + gc));
-      else if (gr < m_ && gc < m_) v[u].x = Kinv[(int64_t)gr * ldk + gc];
-    }
-  };
-  double2 v[8], vn[8];
-  int64_t tt = blockIdx.x;
-  if (tt < ntile) load(tt, v);
-  for (; tt < ntile; tt += gridDim.x) {
-    const int64_t tn = tt + gridDim.x;
-    if (tn < ntile) load(tn, vn);
-    int I, J;
-    tile_of(tt, I, J);
-    const bool diag = (I == J);
-    const int r0 = I * kST, c0 = J * kST;
-    for (int e = threadIdx.x; e < kST * R; e += 256) {
-      const int a = e / R, cc = e % R;
-      bJ[a][cc] = (c0 + a < m_) ? b[(int64_t)(c0 + a + 1) * R + cc] : 0.0;
-      bI[a][cc] = (r0 + a < m_) ? b[(int64_t)(r0 + a + 1) * R + cc] : 0.0;
-    }
-    __syncthreads();
-    double cpa[R], cpb[R];
-#pragma unroll
-    for (int cc = 0; cc < R; ++cc) cpa[cc] = cpb[cc] = 0.0;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int aa = warp + 8 * u;
-      const double ka = (!diag || q <= aa) ? v[u].x : 0.0;
-      const double kb = (!diag || q + 1 <= aa) ? v[u].y : 0.0;
-      double rp[R];
-#pragma unroll
-      for (int cc = 0; cc < R; ++cc) rp[cc] = fma(ka, bJ[q][cc], kb * bJ[q + 1][cc]);
-      warp_sum<R>(rp);
-      if (lane == 0)
-#pragma unroll
-        for (int cc = 0; cc < R; ++cc) rowp[(tt * kST + aa) * R + cc] = rp[cc];
-      const double sa = (!diag || q < aa) ? v[u].x : 0.0;
-      const double sb = (!diag || q + 1 < aa) ? v[u].y : 0.0;
-#pragma unroll
-      for (int cc = 0; cc < R; ++cc) {
-        cpa[cc] = fma(sa, bI[aa][cc], cpa[cc]);
-        cpb[cc] = fma(sb, bI[aa][cc], cpb[cc]);
-      }
-    }
-#pragma unroll
-    for (int c0r = 0; c0r < R; c0r += 4) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (c0r + k < R) {
-          red[warp][q][k] = cpa[c0r + k];
-          red[warp][q + 1][k] = cpb[c0r + k];
-        }
-      __syncthreads();
-      for (int e = threadIdx.x; e < kST * 4; e += 256) {
-        const int l = e >> 2, k = e & 3;
-        if (c0r + k < R) {
-          double sum = 0.0;
-#pragma unroll
-          for (int w = 0; w < 8; ++w) sum += red[w][l][k];
-          colp[(tt * kST + l) * R + c0r + k] = sum;
-        }
-      }
-      __syncthreads();
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = vn[u];
-  }
-}
-
-// t_{g+1} = −( Σ_{J ≤ I} rowp[tile(I,J)][a] + Σ_{I' ≥ I} colp[tile(I',I)][a] ),  g = I·64 + a
-template <int R>
-__global__ void k_imp_symv_fin(int m_, int nb, const double* __restrict__ rowp,
-                               const double* __restrict__ colp, double* __restrict__ t,
-                               const int* __restrict__ stop) {
-  if (stop && *stop) return;
-  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e == 0)
-#pragma unroll
-    for (int cc = 0; cc < R; ++cc) t[cc] = 0.0;
-  if (e >= (int64_t)m_ * R) return;
-  const int g = (int)(e / R), cc = (int)(e % R);
-  const int I = g / kST, a = g % kST;
-  double s = 0.0;
-  for (int J = 0; J <= I; ++J) s += rowp[(((int64_t)I * (I + 1) / 2 + J) * kST + a) * R + cc];
-  for (int I2 = I; I2 < nb; ++I2) s += colp[(((int64_t)I2 * (I2 + 1) / 2 + I) * kST + a) * R + cc];
-  t[(int64_t)(g + 1) * R + cc] = -s;
-}
-
-// p_k = m_k + Σ_{e∈k} w_e t_{i_e} / W_k
+// p_k = m_k + Σ_{e∈k} w_e t_{i_e} / W_k = m_k − Σ_{e∈k} w_e tb_{i_e} / W_k
+// (landmark-sorted, 12 B / measurement)
 template <int R>
 __global__ void __launch_bounds__(kIT) k_imp_lm_p(int M, const int32_t* __restrict__ lm_off,
-                                                  const int32_t* __restrict__ e_fr,
-                                                  const double* __restrict__ e_w,
+                                                  const int32_t* __restrict__ L_i,
+                                                  const double* __restrict__ L_w,
                                                   const double* __restrict__ W,
-                                                  const double* __restrict__ t,
+                                                  const double* __restrict__ tb,
                                                   const double* __restrict__ m,
                                                   double* __restrict__ p,
-    const int* __restrict__ stop) {
+                                                  const int* __restrict__ stop) {
   if (stop && *stop) return;  // a tCG graph replay past the stop
   const int k = blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (k >= M) return;
   double acc[R];
 #pragma unroll
   for (int c = 0; c < R; ++c) acc[c] = 0.0;
-  for (int e = lm_off[k] + lane; e < lm_off[k + 1]; e += 32) {
-    const double we = e_w[e];
-    const double* ti = t + (int64_t)e_fr[e] * R;
+  const int lo = lm_off[k], hi = lm_off[k + 1];
+  for (int e0 = lo + lane; e0 < hi; e0 += 32 * kU) {
+    int ii[kU];
+    double we[kU];
 #pragma unroll
-    for (int c = 0; c < R; ++c) acc[c] = fma(we, ti[c], acc[c]);
+    for (int q = 0; q < kU; ++q) {
+      const int e = min(e0 + 32 * q, hi - 1);
+      ii[q] = __ldcs(L_i + e);
+      we[q] = ((e0 + 32 * q < hi) ? 1.0 : 0.0) * __ldcs(L_w + e);
+    }
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const double wq = (ii[q] != 0) ? we[q] : 0.0;  // t_0 = 0 (anchor)
+      const double* ti = tb + (int64_t)ii[q] * R;
+#pragma unroll
+      for (int c = 0; c < R; ++c) acc[c] = fma(wq, ti[c], acc[c]);
+    }
   }
   warp_sum<R>(acc);
-  if (lane == 0) {
+  if (lane < R) {
     const double wk = W[k], inv = wk > 0.0 ? 1.0 / wk : 0.0;
+    double v = acc[0];
 #pragma unroll
-    for (int c = 0; c < R; ++c) p[(int64_t)k * R + c] = fma(acc[c], inv, m[(int64_t)k * R + c]);
+    for (int c = 1; c < R; ++c) v = (lane == c) ? acc[c] : v;
+    p[(int64_t)k * R + lane] = fma(-v, inv, m[(int64_t)k * R + lane]);
   }
 }
 
-// (QV)_i = Σ_{e∈i} w_e ũ_e (z_e + t_i − p_k)ᵀ
+// (QV)_i = Σ_{e∈i} w_e ũ_e (z_e + t_i − p_k)ᵀ = A_i V_i + c_i t_iᵀ − Σ_{e∈i} (w_e ũ_e) p_kᵀ
+// (A_i = Σ_{e∈i} w_e ũ_e ũ_eᵀ, t_i = −tb_i; frame-sorted, 28 B / measurement)
 template <int R>
 __global__ void __launch_bounds__(kIT) k_imp_fr_out(int N, const int32_t* __restrict__ fr_off,
-                                                    const int32_t* __restrict__ f_lm,
-                                                    const double* __restrict__ f_pts,
-                                                    const double* __restrict__ f_w,
+                                                    const int32_t* __restrict__ F_k,
+                                                    const double* __restrict__ F_wx,
+                                                    const double* __restrict__ F_wy,
+                                                    const double* __restrict__ F_wz,
+                                                    const double* __restrict__ cfr,
+                                                    const double* __restrict__ Afr,
                                                     const double* __restrict__ V,
-                                                    const double* __restrict__ t,
+                                                    const double* __restrict__ tb,
                                                     const double* __restrict__ p,
                                                     double* __restrict__ out,
-    const int* __restrict__ stop) {
+                                                    const int* __restrict__ stop) {
   if (stop && *stop) return;  // a tCG graph replay past the stop
   const int i = blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (i >= N) return;
-  double vi[3][R], ti[R], acc[3 * R];
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int c = 0; c < R; ++c) vi[a][c] = V[((int64_t)3 * i + a) * R + c];
-#pragma unroll
-  for (int c = 0; c < R; ++c) ti[c] = t[(int64_t)i * R + c];
+  double acc[3 * R];
 #pragma unroll
   for (int q = 0; q < 3 * R; ++q) acc[q] = 0.0;
-  for (int q = fr_off[i] + lane; q < fr_off[i + 1]; q += 32) {
-    const int k = f_lm[q];
-    const double u[3] = {f_pts[3 * q], f_pts[3 * q + 1], f_pts[3 * q + 2]};
-    const double we = f_w[q];
+  const int lo = fr_off[i], hi = fr_off[i + 1];
+  for (int q0 = lo + lane; q0 < hi; q0 += 32 * kU) {
+    int kk[kU];
+    double a0[kU], a1[kU], a2[kU];
 #pragma unroll
-    for (int c = 0; c < R; ++c) {
-      const double z = fma(vi[0][c], u[0], fma(vi[1][c], u[1], vi[2][c] * u[2]));
-      const double rr = we * (z + ti[c] - p[(int64_t)k * R + c]);
+    for (int q = 0; q < kU; ++q) {
+      const int e = min(q0 + 32 * q, hi - 1);
+      const double okw = (q0 + 32 * q < hi) ? 1.0 : 0.0;
+      kk[q] = __ldcs(F_k + e);
+      a0[q] = okw * __ldcs(F_wx + e);
+      a1[q] = okw * __ldcs(F_wy + e);
+      a2[q] = okw * __ldcs(F_wz + e);
+    }
 #pragma unroll
-      for (int a = 0; a < 3; ++a) acc[a * R + c] = fma(u[a], rr, acc[a * R + c]);
+    for (int q = 0; q < kU; ++q) {
+      const double* pk = p + (int64_t)kk[q] * R;
+#pragma unroll
+      for (int c = 0; c < R; ++c) {
+        const double pc = pk[c];
+        acc[c] = fma(a0[q], pc, acc[c]);
+        acc[R + c] = fma(a1[q], pc, acc[R + c]);
+        acc[2 * R + c] = fma(a2[q], pc, acc[2 * R + c]);
+      }
     }
   }
   warp_sum<3 * R>(acc);
-  if (lane == 0)
 #pragma unroll
-    for (int q = 0; q < 3 * R; ++q) out[(int64_t)3 * i * R + q] = acc[q];
+  for (int l0 = 0; l0 < 3 * R; l0 += 32) {  // 3R > 32 for r ≥ 11
+    const int x = l0 + lane;
+    if (x >= 3 * R) break;
+    const int a = x / R, c = x % R;
+    double s = acc[l0];
+#pragma unroll
+    for (int q = l0 + 1; q < 3 * R && q < l0 + 32; ++q) s = (x == q) ? acc[q] : s;
+    const double* Ai = Afr + 6 * (int64_t)i;  // xx yy zz xy xz yz
+    const double A0 = a == 0 ? Ai[0] : (a == 1 ? Ai[3] : Ai[4]);
+    const double A1 = a == 0 ? Ai[3] : (a == 1 ? Ai[1] : Ai[5]);
+    const double A2 = a == 0 ? Ai[4] : (a == 1 ? Ai[5] : Ai[2]);
+    const double* vi = V + (int64_t)3 * i * R + c;
+    const double av = fma(A0, vi[0], fma(A1, vi[R], A2 * vi[2 * R]));
+    const double tbi = (i > 0) ? tb[(int64_t)i * R + c] : 0.0;  // t_0 = 0 (anchor)
+    out[(int64_t)3 * i * R + x] = fma(-cfr[3 * (int64_t)i + a], tbi, av) - s;
+  }
 }
 
-__global__ void k_frame_sorted_copy(int64_t E, const int32_t* __restrict__ fr_edge,
-                                    const int32_t* __restrict__ e_lm, const double* __restrict__ e_pts,
-                                    const double* __restrict__ e_w, int32_t* __restrict__ f_lm,
-                                    double* __restrict__ f_pts, double* __restrict__ f_w) {
+// Matrix-free layout (once per build): landmark-sorted w·ũ (SoA), the
+// frame-sorted landmark ids, weights and w·ũ (SoA).
+__global__ void k_imp_layout(int64_t E, const int32_t* __restrict__ fr_edge,
+                             const int32_t* __restrict__ e_lm, const double* __restrict__ e_pts,
+                             const double* __restrict__ e_w, double* __restrict__ L_wx,
+                             double* __restrict__ L_wy, double* __restrict__ L_wz,
+                             int32_t* __restrict__ F_k, double* __restrict__ F_w,
+                             double* __restrict__ F_wx, double* __restrict__ F_wy,
+                             double* __restrict__ F_wz) {
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= E) return;
+  {
+    const double w = e_w[q];
+    L_wx[q] = w * e_pts[3 * q];
+    L_wy[q] = w * e_pts[3 * q + 1];
+    L_wz[q] = w * e_pts[3 * q + 2];
+  }
   const int e = fr_edge[q];
-  f_lm[q] = e_lm[e];
-  f_pts[3 * q] = e_pts[3 * e];
-  f_pts[3 * q + 1] = e_pts[3 * e + 1];
-  f_pts[3 * q + 2] = e_pts[3 * e + 2];
-  f_w[q] = e_w[e];
+  const double w = e_w[e];
+  F_k[q] = e_lm[e];
+  F_w[q] = w;
+  F_wx[q] = w * e_pts[3 * e];
+  F_wy[q] = w * e_pts[3 * e + 1];
+  F_wz[q] = w * e_pts[3 * e + 2];
+}
+
+// Per-frame moments c_i = Σ_{e∈i} w_e ũ_e and A_i = Σ_{e∈i} w_e ũ_e ũ_eᵀ
+// (xx yy zz xy xz yz); warp per frame, fixed order
+__global__ void __launch_bounds__(kIT) k_imp_frame_moments(int N, const int32_t* __restrict__ fr_off,
+                                                           const int32_t* __restrict__ fr_edge,
+                                                           const double* __restrict__ e_pts,
+                                                           const double* __restrict__ e_w,
+                                                           double* __restrict__ cfr,
+                                                           double* __restrict__ Afr) {
+  const int i = blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (i >= N) return;
+  double a[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) a[q] = 0.0;
+  for (int q = fr_off[i] + lane; q < fr_off[i + 1]; q += 32) {
+    const int e = fr_edge[q];
+    const double w = e_w[e], u0 = e_pts[3 * e], u1 = e_pts[3 * e + 1], u2 = e_pts[3 * e + 2];
+    a[0] = fma(w, u0, a[0]);
+    a[1] = fma(w, u1, a[1]);
+    a[2] = fma(w, u2, a[2]);
+    a[3] = fma(w * u0, u0, a[3]);
+    a[4] = fma(w * u1, u1, a[4]);
+    a[5] = fma(w * u2, u2, a[5]);
+    a[6] = fma(w * u0, u1, a[6]);
+    a[7] = fma(w * u0, u2, a[7]);
+    a[8] = fma(w * u1, u2, a[8]);
+  }
+  warp_sum<9>(a);
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) cfr[3 * (int64_t)i + q] = a[q];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) Afr[6 * (int64_t)i + q] = a[3 + q];
+  }
+}
+
+// t_i = −tb_i (the rounded solution's translations, t_0 = 0)
+__global__ void k_imp_neg(int64_t n, const double* __restrict__ tb, double* __restrict__ t) {
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x < n) t[x] = (x < 3) ? 0.0 : -tb[x];
 }
 
 __global__ void k_rademacher_pack(int64_t n, int r, int col, const double* __restrict__ u,
@@ -379,18 +388,37 @@ __global__ void k_rademacher_pack(int64_t n, int r, int col, const double* __res
   }
 }  // namespace
 
-// Matrix-free assembly state: frame-sorted measurement copies and K̄⁻¹.
+// XM_IMP_DEBUG=1: synchronise after every pass and name the failing one
+static void imp_dbg(xm_ctx* c, const char* what) {
+  static const bool on = std::getenv("XM_IMP_DEBUG") != nullptr;
+  if (!on) return;
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) throw Error(XM_ECUDA, std::string("implicit pass ") + what + ": " + cudaGetErrorString(e));
+}
+
+// Matrix-free assembly state: the pass layouts, per-frame moments and K̄⁻¹.
 void implicit_prepare(xm_ctx* c) {
   const int64_t E = c->E;
   const int N = c->N;
   c->imp_lm.alloc(E);
-  c->imp_pts.alloc(3 * E);
   c->imp_w.alloc(E);
-  k_frame_sorted_copy<<<ceil_div(E, 256), 256, 0, c->stream>>>(E, c->fr_edge.p, c->e_lm.p, c->e_pts.p,
-                                                              c->e_w.p, c->imp_lm.p, c->imp_pts.p,
-                                                              c->imp_w.p);
+  c->imp_pts.alloc(6 * E);           // L_wx L_wy L_wz F_wx F_wy F_wz
+  c->imp_mom.alloc(9 * (size_t)N);   // c_i (N × 3), A_i (N × 6)
+  double* P = c->imp_pts.p;
+  k_imp_layout<<<ceil_div(E, 256), 256, 0, c->stream>>>(E, c->fr_edge.p, c->e_lm.p, c->e_pts.p, c->e_w.p,
+                                                         P, P + E, P + 2 * E, c->imp_lm.p, c->imp_w.p,
+                                                         P + 3 * E, P + 4 * E, P + 5 * E);
+  imp_dbg(c, "layout");
+  k_imp_frame_moments<<<ceil_div(N, kIT / 32), kIT, 0, c->stream>>>(N, c->fr_off.p, c->fr_edge.p, c->e_pts.p,
+                                                                    c->e_w.p, c->imp_mom.p,
+                                                                    c->imp_mom.p + 3 * (size_t)N);
   XM_CHECK_LAUNCH();
-  count_launch(c);
+  imp_dbg(c, "moments");
+  count_launch(c, 2);
+  // tb = [0; K̄⁻¹ bs] with room for the padded rows of the lower-triangle stream
+  c->imp_tb.alloc((size_t)(3 * ceil_div(N, 3) + 6) * XM_MAX_R + 8);
+  XM_CUDA(cudaMemsetAsync(c->imp_tb.p, 0, c->imp_tb.n * 8, c->stream));
   if (N > 1) {  // K̄⁻¹ = L⁻ᵀ L⁻¹ with X = L⁻¹ (c->L, U = Lᵀ from the Cholesky)
     const int m = N - 1;
     DBuf<double>& U = scratch_f64(c, "chol_U");
@@ -399,75 +427,87 @@ void implicit_prepare(xm_ctx* c) {
     identity(c, X.p, m, c->ldk);
     dense_trsm_lower_left(c, c->L.p, m, c->ldk, U.p, c->ldk, X.p, m, c->ldk);
     c->Kinv.alloc((size_t)m * c->ldk);
-    // Kinv[i][j] = Σ_k X[k][i] X[k][j]  (lower tiles, then mirrored)
+    // Kinv[i][j] = Σ_k X[k][i] X[k][j]  (lower tiles, then mirrored for the r > 5 row GEMV)
     dgemm_tn(c, true, m, m, m, 1.0, X.p, c->ldk, X.p, c->ldk, 0.0, c->Kinv.p, c->ldk);
     mirror_lower(c, c->Kinv.p, m, c->ldk);
+    imp_dbg(c, "K^-1");
+    X.release();
+  }
+}
+
+// tb[1..N) = K̄⁻¹ bs: the lower-triangle stream (r ≤ 5) or the row GEMV.  Row 0
+// of tb is never read as data (t_0 = 0 is applied by the readers: a product
+// at another r leaves other values there)
+static void kinv_product(xm_ctx* c, const double* bs, int r, const int* stop) {
+  const int mK = c->N - 1;
+  if (mK < 1) return;  // tb stays 0 (N = 1)
+  static const bool force_gemv = std::getenv("XM_IMP_GEMV") != nullptr;
+  if (r <= 5 && !force_gemv) {
+    spmm_sym_matrix(c, c->imp_sym_plan, c->imp_sym_part, c->Kinv.p, mK, c->ldk, bs, r, c->imp_tb.p + r,
+                    stop);
+  } else {
+    XM_IMP_DISPATCH(r, (k_imp_gemv<R><<<ceil_div(mK, kIT / 32), kIT, 0, c->stream>>>(mK, c->Kinv.p, c->ldk,
+                                                                                     bs, c->imp_tb.p, stop)));
+    XM_CHECK_LAUNCH();
+    count_launch(c);
   }
 }
 
 void implicit_product(xm_ctx* c, const double* V, int r, double* out, const int* stop) {
   const int N = c->N, M = c->M;
+  const int64_t E = c->E;
   DBuf<double>& m = scratch_f64(c, "imp_m");
   DBuf<double>& p = scratch_f64(c, "imp_p");
-  DBuf<double>& b = scratch_f64(c, "imp_b");
-  DBuf<double>& t = scratch_f64(c, "imp_t");
+  DBuf<double>& bs = scratch_f64(c, "imp_bs");
   m.alloc((size_t)M * XM_MAX_R + 8);
   p.alloc((size_t)M * XM_MAX_R + 8);
-  b.alloc((size_t)N * XM_MAX_R + 8);
-  t.alloc((size_t)N * XM_MAX_R + 8);
-  const int gM = ceil_div(M, kIT / 32), gN = ceil_div(N, kIT / 32), gK = ceil_div(N, kIT / 32);
-  XM_IMP_DISPATCH(r, (k_imp_lm_mean<R><<<gM, kIT, 0, c->stream>>>(M, c->lm_off.p, c->e_fr.p, c->e_pts.p,
-                                                                  c->e_w.p, c->W.p, V, m.p, stop)));
-  XM_IMP_DISPATCH(r, (k_imp_fr_b<R><<<gN, kIT, 0, c->stream>>>(N, c->fr_off.p, c->imp_lm.p, c->imp_pts.p,
-                                                               c->imp_w.p, V, m.p, b.p, stop)));
-  // K̄⁻¹ b: the row GEMV over the full (mirrored) K̄⁻¹ (E: 826 MB, 217 µs) is the
-  // default; the lower-triangle variant (XM_IMP_SYMV=1: 415 MB + 39 MB of
-  // partials) measured 195 + 37 µs — it is bound by its per-tile reductions,
-  // not by the bytes (profiles/r2_implicit_E.txt)
-  if (N > 1 && std::getenv("XM_IMP_SYMV")) {
-    const int mK = N - 1, nb = ceil_div(mK, kST);
-    const int64_t ntile = (int64_t)nb * (nb + 1) / 2;
-    DBuf<double>& rp = scratch_f64(c, "imp_rowp");
-    DBuf<double>& cp = scratch_f64(c, "imp_colp");
-    rp.alloc((size_t)ntile * kST * XM_MAX_R + 8);
-    cp.alloc((size_t)ntile * kST * XM_MAX_R + 8);
-    const unsigned gsym = (unsigned)std::min<int64_t>(ntile, 148 * 8);
-    XM_IMP_DISPATCH(r, (k_imp_symv_tiles<R><<<gsym, 256, 0, c->stream>>>(
-                           mK, nb, c->Kinv.p, c->ldk, b.p, rp.p, cp.p, stop)));
-    XM_IMP_DISPATCH(r, (k_imp_symv_fin<R><<<ceil_div((int64_t)mK * r, 256), 256, 0, c->stream>>>(
-                           mK, nb, rp.p, cp.p, t.p, stop)));
-    count_launch(c);
-  } else if (N > 1) {
-    XM_IMP_DISPATCH(r, (k_imp_gemv<R><<<gK, kIT, 0, c->stream>>>(N - 1, c->Kinv.p, c->ldk, b.p, t.p,
-                                                                 stop)));
-  } else {
-    XM_CUDA(cudaMemsetAsync(t.p, 0, (size_t)r * 8, c->stream));
-  }
-  XM_IMP_DISPATCH(r, (k_imp_lm_p<R><<<gM, kIT, 0, c->stream>>>(M, c->lm_off.p, c->e_fr.p, c->e_w.p, c->W.p,
-                                                               t.p, m.p, p.p, stop)));
-  XM_IMP_DISPATCH(r, (k_imp_fr_out<R><<<gN, kIT, 0, c->stream>>>(N, c->fr_off.p, c->imp_lm.p,
-                                                                 c->imp_pts.p, c->imp_w.p, V, t.p, p.p,
-                                                                 out, stop)));
+  bs.alloc((size_t)(3 * ceil_div(N, 3) + 6) * XM_MAX_R + 8);
+  const double* P = c->imp_pts.p;
+  const double* cfr = c->imp_mom.p;
+  const double* Afr = c->imp_mom.p + 3 * (size_t)N;
+  const int gM = ceil_div(M, kIT / 32), gN = ceil_div(N, kIT / 32);
+  imp_dbg(c, "entry");
+  XM_IMP_DISPATCH(r, (k_imp_lm_mean<R><<<gM, kIT, 0, c->stream>>>(M, c->lm_off.p, c->e_fr.p, P, P + E,
+                                                                  P + 2 * E, c->W.p, V, m.p, stop)));
+  imp_dbg(c, "lm_mean");
+  if (N > 1)
+    XM_IMP_DISPATCH(r, (k_imp_fr_b<R><<<ceil_div(N - 1, kIT / 32), kIT, 0, c->stream>>>(
+                           N, c->fr_off.p, c->imp_lm.p, c->imp_w.p, cfr, V, m.p, bs.p, stop)));
   XM_CHECK_LAUNCH();
-  count_launch(c, 5);
+  imp_dbg(c, "fr_b");
+  kinv_product(c, bs.p, r, stop);
+  imp_dbg(c, "kinv");
+  XM_IMP_DISPATCH(r, (k_imp_lm_p<R><<<gM, kIT, 0, c->stream>>>(M, c->lm_off.p, c->e_fr.p, c->e_w.p, c->W.p,
+                                                               c->imp_tb.p, m.p, p.p, stop)));
+  imp_dbg(c, "lm_p");
+  XM_IMP_DISPATCH(r, (k_imp_fr_out<R><<<gN, kIT, 0, c->stream>>>(N, c->fr_off.p, c->imp_lm.p, P + 3 * E,
+                                                                 P + 4 * E, P + 5 * E, cfr, Afr, V,
+                                                                 c->imp_tb.p, p.p, out, stop)));
+  XM_CHECK_LAUNCH();
+  imp_dbg(c, "fr_out");
+  count_launch(c, N > 1 ? 4 : 3);
 }
 
 // translations of the rounded solution, t = −K̄⁻¹ C̄ Y₃ (Eq. (4)), from the same passes
 void implicit_translations(xm_ctx* c, const double* Y3, double* t_out) {
   const int N = c->N, M = c->M;
+  const int64_t E = c->E;
   DBuf<double>& m = scratch_f64(c, "imp_m");
-  DBuf<double>& b = scratch_f64(c, "imp_b");
+  DBuf<double>& bs = scratch_f64(c, "imp_bs");
   m.alloc((size_t)M * XM_MAX_R + 8);
-  b.alloc((size_t)N * XM_MAX_R + 8);
-  const int gM = ceil_div(M, kIT / 32), gN = ceil_div(N, kIT / 32);
-  k_imp_lm_mean<3><<<gM, kIT, 0, c->stream>>>(M, c->lm_off.p, c->e_fr.p, c->e_pts.p, c->e_w.p, c->W.p, Y3,
+  bs.alloc((size_t)(3 * ceil_div(N, 3) + 6) * XM_MAX_R + 8);
+  const double* P = c->imp_pts.p;
+  const int gM = ceil_div(M, kIT / 32);
+  k_imp_lm_mean<3><<<gM, kIT, 0, c->stream>>>(M, c->lm_off.p, c->e_fr.p, P, P + E, P + 2 * E, c->W.p, Y3,
                                               m.p, nullptr);
-  k_imp_fr_b<3><<<gN, kIT, 0, c->stream>>>(N, c->fr_off.p, c->imp_lm.p, c->imp_pts.p, c->imp_w.p, Y3, m.p,
-                                           b.p, nullptr);
-  if (N > 1) k_imp_gemv<3><<<gN, kIT, 0, c->stream>>>(N - 1, c->Kinv.p, c->ldk, b.p, t_out, nullptr);
-  else XM_CUDA(cudaMemsetAsync(t_out, 0, 3 * 8, c->stream));
+  if (N > 1)
+    k_imp_fr_b<3><<<ceil_div(N - 1, kIT / 32), kIT, 0, c->stream>>>(N, c->fr_off.p, c->imp_lm.p, c->imp_w.p,
+                                                                    c->imp_mom.p, Y3, m.p, bs.p, nullptr);
   XM_CHECK_LAUNCH();
-  count_launch(c, 3);
+  kinv_product(c, bs.p, 3, nullptr);
+  k_imp_neg<<<ceil_div((int64_t)3 * N, 256), 256, 0, c->stream>>>((int64_t)3 * N, c->imp_tb.p, t_out);
+  XM_CHECK_LAUNCH();
+  count_launch(c, N > 1 ? 3 : 2);
 }
 
 // ‖Q‖_F by the shared 16-probe Rademacher estimate (reading C24; oracle

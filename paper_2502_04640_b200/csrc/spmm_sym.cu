@@ -167,17 +167,27 @@ struct SymPlan {
   DBuf<int> colptr;   // TCb + 1: segments [colptr[J], colptr[J+1]) belong to panel J
 };
 
-static SymPlan& sym_plan(xm_ctx* c) {
-  if (!c->sym_plan) c->sym_plan = new SymPlan();
-  SymPlan& p = *static_cast<SymPlan*>(c->sym_plan);
+// The symmetric matrix a plan streams: Q (this rank's band of rows) or, in
+// the matrix-free mode, K̄⁻¹ (implicit.cu) — any n × n symmetric matrix whose
+// rows [row0, row0 + nrows) are stored with pitch ld (lower triangle read).
+struct SymSrc {
+  const double* ptr;
+  int n;
+  int64_t ld;
+  int row0, nrows;
+};
+
+static SymPlan& sym_plan_for(xm_ctx* c, void*& slot, const SymSrc& src) {
+  if (!slot) slot = new SymPlan();
+  SymPlan& p = *static_cast<SymPlan*>(slot);
   int sms = 148;
   XM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
-  const int n = c->n, G = std::min(148, sms);
+  const int n = src.n, G = std::min(148, sms);
   // band of row tiles: [row0, row0 + nrows) is frame- and tile-aligned (32 frames) on world > 1
-  const int rt_a = c->row0 / TR;
-  const int rt_b = (c->row0 + c->nrows >= n) ? ceil_div(n, TR) : (c->row0 + c->nrows) / TR;
-  const bool same_band = p.rt_a == rt_a && p.rt_b == rt_b && p.row0 == c->row0;
-  if (p.n == n && p.G == G && p.pbase.p && p.qptr == c->Q.p && p.ldq == c->ldq && same_band) return p;
+  const int rt_a = src.row0 / TR;
+  const int rt_b = (src.row0 + src.nrows >= n) ? ceil_div(n, TR) : (src.row0 + src.nrows) / TR;
+  const bool same_band = p.rt_a == rt_a && p.rt_b == rt_b && p.row0 == src.row0;
+  if (p.n == n && p.G == G && p.pbase.p && p.qptr == src.ptr && p.ldq == src.ld && same_band) return p;
   // Q tensor map: dims {n columns, n rows}, row pitch ldq·8 B, box BC × TR,
   // OOB → zero fill (rows / columns ≥ n read as 0)
   {
@@ -191,16 +201,17 @@ static SymPlan& sym_plan(xm_ctx* c) {
       return f;
     }();
     if (!encode) throw Error(XM_ECUDA, "cuTensorMapEncodeTiled unavailable");
-    cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)std::max(c->nrows, 1)};  // local rows
-    cuuint64_t strides[1] = {(cuuint64_t)c->ldq * 8};
+    cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)std::max(src.nrows, 1)};  // local rows
+    cuuint64_t strides[1] = {(cuuint64_t)src.ld * 8};
     cuuint32_t box[2] = {(cuuint32_t)BC, (cuuint32_t)TR};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = encode(&p.tmq, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, c->Q.p, dims, strides, box, estr,
+    CUresult r = encode(&p.tmq, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(src.ptr), dims,
+                        strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(XM_ECUDA, "cuTensorMapEncodeTiled failed");
-    p.qptr = c->Q.p;
-    p.ldq = c->ldq;
+    p.qptr = src.ptr;
+    p.ldq = src.ld;
   }
   if (p.n == n && p.G == G && p.pbase.p && same_band) return p;
   p.n = n;
@@ -209,7 +220,7 @@ static SymPlan& sym_plan(xm_ctx* c) {
   p.TCb = ceil_div(n, BC);
   p.rt_a = rt_a;
   p.rt_b = rt_b;
-  p.row0 = c->row0;
+  p.row0 = src.row0;
   // panel J: row tiles max(8J, rt_a) … rt_b − 1 of the band (none once 8J ≥ rt_b)
   std::vector<int> pb(p.TCb + 1, 0);
   for (int J = 0; J < p.TCb; ++J)
@@ -243,6 +254,10 @@ static SymPlan& sym_plan(xm_ctx* c) {
   XM_CUDA(cudaMemcpy(p.segbase.p, segbase.data(), segbase.size() * 4, cudaMemcpyHostToDevice));
   XM_CUDA(cudaMemcpy(p.colptr.p, colptr.data(), colptr.size() * 4, cudaMemcpyHostToDevice));
   return p;
+}
+
+static SymPlan& sym_plan(xm_ctx* c) {
+  return sym_plan_for(c, c->sym_plan, SymSrc{c->Q.p, (int)c->n, c->ldq, c->row0, c->nrows});
 }
 
 template <int R>
@@ -451,6 +466,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
   double* qrow = stages;  // pipeline smem is free now: [rows][R]
   for (int e = threadIdx.x; e < 3 * (fb - fa) * R; e += kThreads) {
     const int row = 3 * fa + e / R, cc = e % R;
+    if (row >= n) {  // a matrix of order n < 3N (K̄⁻¹): the padding rows read as 0
+      qrow[e] = 0.0;
+      continue;
+    }
     const int K = row / TR, l = row % TR;
     const int Jc = row / BC, m = row % BC;
     const double* p = rowpart + (rtile_base(K) * TR + l) * R + cc;
@@ -549,16 +568,17 @@ bool tcg_fullrow_ok(xm_ctx* c) { return c->opt.spmm_kernel != 2 && c->N < 4000; 
 
 int spmm_sym_partials(xm_ctx* c) { return sym_plan(c).G; }
 
+// part: row / column partials, sized once for the largest supported r so the
+// address never changes when the staircase climbs (the tCG graphs of lower
+// ranks captured it).  Nf = frames of the finish (3 rows each; rows ≥ n skipped).
 template <int R, int MODE>
-static void launch_sym(xm_ctx* c, const double* V, const SpmmEpiArgs& ep) {
-  SymPlan& p = sym_plan(c);
-  // sized for the largest supported r once, so the address never changes when
-  // the staircase climbs (the tCG graphs of lower ranks captured it)
+static void launch_sym_on(xm_ctx* c, SymPlan& p, DBuf<double>& part, int Nf, const double* V,
+                          const SpmmEpiArgs& ep) {
   constexpr int kRmax = 5;
   const size_t rp = (size_t)p.W_full * TR * R;  // row parts indexed over the whole triangle
-  c->sym_part.alloc((size_t)p.W_full * TR * kRmax + (size_t)std::max(p.S, 1) * BC * kRmax + 64);
-  double* rowpart = c->sym_part.p;
-  double* colpart = c->sym_part.p + rp;
+  part.alloc((size_t)p.W_full * TR * kRmax + (size_t)std::max(p.S, 1) * BC * kRmax + 64);
+  double* rowpart = part.p;
+  double* colpart = part.p + rp;
   if (!c->gbar.p) {
     c->gbar.alloc(4);
     XM_CUDA(cudaMemset(c->gbar.p, 0, 4 * sizeof(int)));
@@ -577,12 +597,41 @@ static void launch_sym(xm_ctx* c, const double* V, const SpmmEpiArgs& ep) {
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  XM_CUDA(cudaLaunchKernelEx(&cfg, k_spmm_sym<R, MODE>, p.tmq, (int)c->N, (int)c->n, p.rt_a, p.rt_b,
-                             p.row0, p.TCb, p.W, p.pbase.p, p.segbase.p, p.colptr.p, V, rowpart,
-                             colpart,
+  XM_CUDA(cudaLaunchKernelEx(&cfg, k_spmm_sym<R, MODE>, p.tmq, Nf, p.n, p.rt_a, p.rt_b, p.row0, p.TCb,
+                             p.W, p.pbase.p, p.segbase.p, p.colptr.p, V, rowpart, colpart,
                              reinterpret_cast<GridBar*>(c->gbar.p), ep));
   XM_CHECK_LAUNCH();
   count_launch(c, 1);
+}
+
+template <int R, int MODE>
+static void launch_sym(xm_ctx* c, const double* V, const SpmmEpiArgs& ep) {
+  launch_sym_on<R, MODE>(c, sym_plan(c), c->sym_part, (int)c->N, V, ep);
+}
+
+// out = A·V for a symmetric m × m matrix A (pitch lda, lower triangle read),
+// V and out m × r row-major with ≥ 3·⌈m/3⌉ rows of room (r ≤ 5).  NEXT-1:
+// the K̄⁻¹ product of the matrix-free Q·V (implicit.cu).
+void spmm_sym_matrix(xm_ctx* c, void*& plan_slot, DBuf<double>& part, const double* A, int m,
+                     int64_t lda, const double* V, int r, double* out, const int* stop) {
+  SymPlan& p = sym_plan_for(c, plan_slot, SymSrc{A, m, lda, 0, m});
+  SpmmEpiArgs ep{};
+  ep.out = out;
+  ep.stop = stop;
+  const int Nf = ceil_div(m, 3);
+  switch (r) {
+    case 1: launch_sym_on<1, EPI_STORE>(c, p, part, Nf, V, ep); break;
+    case 2: launch_sym_on<2, EPI_STORE>(c, p, part, Nf, V, ep); break;
+    case 3: launch_sym_on<3, EPI_STORE>(c, p, part, Nf, V, ep); break;
+    case 4: launch_sym_on<4, EPI_STORE>(c, p, part, Nf, V, ep); break;
+    case 5: launch_sym_on<5, EPI_STORE>(c, p, part, Nf, V, ep); break;
+    default: throw Error(XM_EINVAL, "symmetric product supports r ≤ 5");
+  }
+}
+
+void sym_plan_slot_destroy(void*& slot) {
+  delete static_cast<SymPlan*>(slot);
+  slot = nullptr;
 }
 
 template <int MODE>

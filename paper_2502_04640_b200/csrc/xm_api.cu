@@ -150,7 +150,9 @@ std::vector<uintptr_t> graph_signature(xm_ctx* c) {
           (uintptr_t)c->f0, (uintptr_t)c->f1, (uintptr_t)c->sym_part.p, (uintptr_t)c->gbar.p,
           (uintptr_t)c->sym_plan, (uintptr_t)c->gsync.p, (uintptr_t)c->fused_tcg,
           (uintptr_t)c->opt.spmm_kernel, reg_bits(c), (uintptr_t)c->implicit_active,
-          (uintptr_t)c->Kinv.p, (uintptr_t)c->imp_lm.p, (uintptr_t)c->e_fr.p};
+          (uintptr_t)c->Kinv.p, (uintptr_t)c->imp_lm.p, (uintptr_t)c->e_fr.p,
+          (uintptr_t)c->imp_pts.p, (uintptr_t)c->imp_mom.p, (uintptr_t)c->imp_tb.p,
+          (uintptr_t)c->imp_sym_part.p, (uintptr_t)c->imp_sym_plan};
 }
 
 void destroy_graph(xm_ctx::TcgGraph& g) {
@@ -614,6 +616,7 @@ void xm_destroy(xm_ctx* c) {
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   nccl_destroy(c);
   sym_plan_destroy(c);
+  sym_plan_slot_destroy(c->imp_sym_plan);
   sym_tcg_plan_destroy(c);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;

@@ -143,8 +143,11 @@ struct xm_ctx {
   xm::DBuf<double> regd;   // N: App. D diagonal shifts d_i = 2λ/3 (α_i − 1) at the current factor
   // NEXT-1 matrix-free mode (implicit.cu): frame-sorted measurement copies, K̄⁻¹
   bool implicit_active = false;
-  xm::DBuf<int32_t> imp_lm;
-  xm::DBuf<double> imp_pts, imp_w, Kinv;
+  xm::DBuf<int32_t> imp_lm;                // frame-sorted landmark ids
+  xm::DBuf<double> imp_pts, imp_w, Kinv;   // w·ũ (landmark- and frame-sorted SoA), frame-sorted w
+  xm::DBuf<double> imp_mom, imp_tb;        // per-frame c_i, A_i; [0; K̄⁻¹ b]
+  void* imp_sym_plan = nullptr;            // lower-triangle stream plan of K̄⁻¹
+  xm::DBuf<double> imp_sym_part;
   xm::DBuf<double> lam;    // N × 6 (xx, yy, zz, xy, xz, yz)
   xm::DBuf<double> part;   // SpMM split-K partials: nsplit × nrows × r
   xm::DBuf<double> red;    // block partials for reductions
@@ -389,6 +392,9 @@ void nccl_init(xm_ctx* c, const void* id);
 void nccl_destroy(xm_ctx* c);
 void nccl_allreduce_sum(xm_ctx* c, double* buf, size_t count);
 void sym_plan_destroy(xm_ctx* c);
+void sym_plan_slot_destroy(void*& slot);
+void spmm_sym_matrix(xm_ctx* c, void*& plan_slot, DBuf<double>& part, const double* A, int m,
+                     int64_t lda, const double* V, int r, double* out, const int* stop);
 void sym_tcg_plan_destroy(xm_ctx* c);
 
 // Row sharding: rank q owns frames [q·nfpr, min(N, (q+1)·nfpr)),
