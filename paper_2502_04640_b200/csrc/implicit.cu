@@ -37,16 +37,37 @@ __device__ __forceinline__ void warp_sum(double (&a)[K]) {
 }
 
 // Every pass is one warp per landmark or frame walking its contiguous run of
-// measurements.  The tail of a run is handled by CLAMPED unconditional loads
-// with zeroed weights, never by predicated loads: the predicated-load form of
-// this unrolled loop faulted on sm_100a with data-dependent addresses (the
-// gathered index register picking up a V value; reproduced only for
-// non-integer V, fixed by this form — DESIGN.md §5).
-//
-// measurements, kU per lane in flight (all index / coefficient loads of a
-// round issued before the dependent L2 gathers), then a fixed-order warp
-// reduction: deterministic.  Per-measurement streams are read evict-first
-// (__ldcs) so the gathered n × r arrays (≤ 1.5 MB) stay in L2.
+// measurements in the COLUMN-OWNER layout: a group of R lanes per measurement,
+// lane j of a group owning column j (⌊32/R⌋ measurements per warp round), so
+// the gathered row of a measurement (V_i: 3R doubles, m_k / t_i / p_k: R
+// doubles) is read by R adjacent lanes — one or two 32-B sectors per group —
+// instead of one scattered sector per lane and element; the L1 wavefronts of
+// the gathers, which bound these passes, drop by ≈ R×.  Each lane accumulates
+// its own column; the groups are summed at the end by a fixed shuffle tree
+// (deterministic).  kU rounds in flight per lane; run tails use CLAMPED
+// unconditional loads with zeroed weights, never predicated loads (the
+// predicated-load form of the unrolled loop faulted on sm_100a with
+// data-dependent gathered addresses — DESIGN.md §5).  Per-measurement
+// streams are read evict-first (__ldcs) so the gathered n × r arrays
+// (≤ 1.5 MB) stay in L2.
+template <int R>
+struct Grp {
+  static constexpr int NG = 32 / R;  // measurements per warp round
+};
+
+// sum over the groups of the lanes owning the same column (result in group 0)
+template <int R, int K>
+__device__ __forceinline__ void group_sum(double (&v)[K], int g) {
+  constexpr int NG = Grp<R>::NG;
+#pragma unroll
+  for (int s = 1; s < NG; s <<= 1) {
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      const double o = __shfl_down_sync(0xffffffffu, v[q], s * R);
+      if ((g % (2 * s)) == 0 && g + s < NG) v[q] += o;
+    }
+  }
+}
 
 // m_k = Σ_{e∈k} (w_e ũ_e)ᵀ V_{i_e} / W_k          (landmark-sorted, 28 B / measurement)
 template <int R>
@@ -60,19 +81,21 @@ __global__ void __launch_bounds__(kIT) k_imp_lm_mean(int M, const int32_t* __res
                                                      double* __restrict__ m,
                                                      const int* __restrict__ stop) {
   if (stop && *stop) return;  // a tCG graph replay past the stop
+  constexpr int NG = Grp<R>::NG;
   const int k = blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (k >= M) return;
-  double acc[R];
-#pragma unroll
-  for (int c = 0; c < R; ++c) acc[c] = 0.0;
+  const int g = lane / R, j = lane - g * R;
+  const bool act = g < NG;
+  double acc[1] = {0.0};
   const int lo = lm_off[k], hi = lm_off[k + 1];
-  for (int e0 = lo + lane; e0 < hi; e0 += 32 * kU) {
+  for (int base = lo; base < hi; base += NG * kU) {
     int ii[kU];
     double a0[kU], a1[kU], a2[kU];
 #pragma unroll
     for (int q = 0; q < kU; ++q) {
-      const int e = min(e0 + 32 * q, hi - 1);  // clamped: loads unconditional, tail weights zeroed
-      const double okw = (e0 + 32 * q < hi) ? 1.0 : 0.0;
+      const int e0 = base + q * NG + g;
+      const int e = min(e0, hi - 1);  // clamped: loads unconditional, tail weights zeroed
+      const double okw = (act && e0 < hi) ? 1.0 : 0.0;
       ii[q] = __ldcs(L_i + e);
       a0[q] = okw * __ldcs(L_wx + e);
       a1[q] = okw * __ldcs(L_wy + e);
@@ -80,18 +103,15 @@ __global__ void __launch_bounds__(kIT) k_imp_lm_mean(int M, const int32_t* __res
     }
 #pragma unroll
     for (int q = 0; q < kU; ++q) {
-      const double* vi = V + (int64_t)3 * ii[q] * R;
-#pragma unroll
-      for (int c = 0; c < R; ++c) acc[c] = fma(a0[q], vi[c], fma(a1[q], vi[R + c], fma(a2[q], vi[2 * R + c], acc[c])));
+      const double* vi = V + (int64_t)3 * ii[q] * R + j;
+      acc[0] = fma(a0[q], vi[0], fma(a1[q], vi[R], fma(a2[q], vi[2 * R], acc[0])));
     }
   }
-  warp_sum<R>(acc);
+  group_sum<R, 1>(acc, g);
   if (lane < R) {
+    const double sum = acc[0];
     const double wk = W[k], inv = wk > 0.0 ? 1.0 / wk : 0.0;
-    double v = acc[0];
-#pragma unroll
-    for (int c = 1; c < R; ++c) v = (lane == c) ? acc[c] : v;
-    m[(int64_t)k * R + lane] = v * inv;
+    m[(int64_t)k * R + lane] = sum * inv;
   }
 }
 
@@ -108,36 +128,33 @@ __global__ void __launch_bounds__(kIT) k_imp_fr_b(int N, const int32_t* __restri
                                                   double* __restrict__ bs,
                                                   const int* __restrict__ stop) {
   if (stop && *stop) return;  // a tCG graph replay past the stop
+  constexpr int NG = Grp<R>::NG;
   const int i = 1 + blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (i >= N) return;
-  double acc[R];
-#pragma unroll
-  for (int c = 0; c < R; ++c) acc[c] = 0.0;
+  const int g = lane / R, j = lane - g * R;
+  const bool act = g < NG;
+  double acc[1] = {0.0};
   const int lo = fr_off[i], hi = fr_off[i + 1];
-  for (int q0 = lo + lane; q0 < hi; q0 += 32 * kU) {
+  for (int base = lo; base < hi; base += NG * kU) {
     int kk[kU];
     double we[kU];
 #pragma unroll
     for (int q = 0; q < kU; ++q) {
-      const int e = min(q0 + 32 * q, hi - 1);
+      const int e0 = base + q * NG + g;
+      const int e = min(e0, hi - 1);
       kk[q] = __ldcs(F_k + e);
-      we[q] = ((q0 + 32 * q < hi) ? 1.0 : 0.0) * __ldcs(F_w + e);
+      we[q] = ((act && e0 < hi) ? 1.0 : 0.0) * __ldcs(F_w + e);
     }
 #pragma unroll
-    for (int q = 0; q < kU; ++q) {
-      const double* mk = m + (int64_t)kk[q] * R;
-#pragma unroll
-      for (int c = 0; c < R; ++c) acc[c] = fma(we[q], mk[c], acc[c]);
-    }
+    for (int q = 0; q < kU; ++q) acc[0] = fma(we[q], m[(int64_t)kk[q] * R + j], acc[0]);
   }
-  warp_sum<R>(acc);
+  group_sum<R, 1>(acc, g);
   if (lane < R) {
-    double s = acc[0];
-#pragma unroll
-    for (int c = 1; c < R; ++c) s = (lane == c) ? acc[c] : s;
-    const double* vi = V + (int64_t)3 * i * R + lane;
+    const double sum = acc[0];
+    const int jj = lane;
+    const double* vi = V + (int64_t)3 * i * R + jj;
     const double* ci = cfr + 3 * (int64_t)i;
-    bs[(int64_t)(i - 1) * R + lane] = fma(ci[0], vi[0], fma(ci[1], vi[R], ci[2] * vi[2 * R])) - s;
+    bs[(int64_t)(i - 1) * R + jj] = fma(ci[0], vi[0], fma(ci[1], vi[R], ci[2] * vi[2 * R])) - sum;
   }
 }
 
@@ -198,43 +215,41 @@ __global__ void __launch_bounds__(kIT) k_imp_lm_p(int M, const int32_t* __restri
                                                   double* __restrict__ p,
                                                   const int* __restrict__ stop) {
   if (stop && *stop) return;  // a tCG graph replay past the stop
+  constexpr int NG = Grp<R>::NG;
   const int k = blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (k >= M) return;
-  double acc[R];
-#pragma unroll
-  for (int c = 0; c < R; ++c) acc[c] = 0.0;
+  const int g = lane / R, j = lane - g * R;
+  const bool act = g < NG;
+  double acc[1] = {0.0};
   const int lo = lm_off[k], hi = lm_off[k + 1];
-  for (int e0 = lo + lane; e0 < hi; e0 += 32 * kU) {
+  for (int base = lo; base < hi; base += NG * kU) {
     int ii[kU];
     double we[kU];
 #pragma unroll
     for (int q = 0; q < kU; ++q) {
-      const int e = min(e0 + 32 * q, hi - 1);
+      const int e0 = base + q * NG + g;
+      const int e = min(e0, hi - 1);
       ii[q] = __ldcs(L_i + e);
-      we[q] = ((e0 + 32 * q < hi) ? 1.0 : 0.0) * __ldcs(L_w + e);
+      we[q] = ((act && e0 < hi) ? 1.0 : 0.0) * __ldcs(L_w + e);
     }
 #pragma unroll
     for (int q = 0; q < kU; ++q) {
       const double wq = (ii[q] != 0) ? we[q] : 0.0;  // t_0 = 0 (anchor)
-      const double* ti = tb + (int64_t)ii[q] * R;
-#pragma unroll
-      for (int c = 0; c < R; ++c) acc[c] = fma(wq, ti[c], acc[c]);
+      acc[0] = fma(wq, tb[(int64_t)ii[q] * R + j], acc[0]);
     }
   }
-  warp_sum<R>(acc);
+  group_sum<R, 1>(acc, g);
   if (lane < R) {
+    const double sum = acc[0];
     const double wk = W[k], inv = wk > 0.0 ? 1.0 / wk : 0.0;
-    double v = acc[0];
-#pragma unroll
-    for (int c = 1; c < R; ++c) v = (lane == c) ? acc[c] : v;
-    p[(int64_t)k * R + lane] = fma(-v, inv, m[(int64_t)k * R + lane]);
+    p[(int64_t)k * R + lane] = fma(-sum, inv, m[(int64_t)k * R + lane]);
   }
 }
 
 // (QV)_i = Σ_{e∈i} w_e ũ_e (z_e + t_i − p_k)ᵀ = A_i V_i + c_i t_iᵀ − Σ_{e∈i} (w_e ũ_e) p_kᵀ
 // (A_i = Σ_{e∈i} w_e ũ_e ũ_eᵀ, t_i = −tb_i; frame-sorted, 28 B / measurement)
 template <int R>
-__global__ void __launch_bounds__(kIT) k_imp_fr_out(int N, const int32_t* __restrict__ fr_off,
+__global__ void __launch_bounds__(kIT, (R <= 5) ? 4 : 1) k_imp_fr_out(int N, const int32_t* __restrict__ fr_off,
                                                     const int32_t* __restrict__ F_k,
                                                     const double* __restrict__ F_wx,
                                                     const double* __restrict__ F_wy,
@@ -249,6 +264,7 @@ __global__ void __launch_bounds__(kIT) k_imp_fr_out(int N, const int32_t* __rest
   if (stop && *stop) return;  // a tCG graph replay past the stop
   const int i = blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (i >= N) return;
+  constexpr int kU = (R <= 3) ? 4 : 2;  // register budget: 3R accumulators (6 CTAs / SM)
   double acc[3 * R];
 #pragma unroll
   for (int q = 0; q < 3 * R; ++q) acc[q] = 0.0;
@@ -465,9 +481,8 @@ void implicit_product(xm_ctx* c, const double* V, int r, double* out, const int*
   const double* P = c->imp_pts.p;
   const double* cfr = c->imp_mom.p;
   const double* Afr = c->imp_mom.p + 3 * (size_t)N;
-  const int gM = ceil_div(M, kIT / 32), gN = ceil_div(N, kIT / 32);
   imp_dbg(c, "entry");
-  XM_IMP_DISPATCH(r, (k_imp_lm_mean<R><<<gM, kIT, 0, c->stream>>>(M, c->lm_off.p, c->e_fr.p, P, P + E,
+  XM_IMP_DISPATCH(r, (k_imp_lm_mean<R><<<ceil_div(M, kIT / 32), kIT, 0, c->stream>>>(M, c->lm_off.p, c->e_fr.p, P, P + E,
                                                                   P + 2 * E, c->W.p, V, m.p, stop)));
   imp_dbg(c, "lm_mean");
   if (N > 1)
@@ -477,10 +492,10 @@ void implicit_product(xm_ctx* c, const double* V, int r, double* out, const int*
   imp_dbg(c, "fr_b");
   kinv_product(c, bs.p, r, stop);
   imp_dbg(c, "kinv");
-  XM_IMP_DISPATCH(r, (k_imp_lm_p<R><<<gM, kIT, 0, c->stream>>>(M, c->lm_off.p, c->e_fr.p, c->e_w.p, c->W.p,
+  XM_IMP_DISPATCH(r, (k_imp_lm_p<R><<<ceil_div(M, kIT / 32), kIT, 0, c->stream>>>(M, c->lm_off.p, c->e_fr.p, c->e_w.p, c->W.p,
                                                                c->imp_tb.p, m.p, p.p, stop)));
   imp_dbg(c, "lm_p");
-  XM_IMP_DISPATCH(r, (k_imp_fr_out<R><<<gN, kIT, 0, c->stream>>>(N, c->fr_off.p, c->imp_lm.p, P + 3 * E,
+  XM_IMP_DISPATCH(r, (k_imp_fr_out<R><<<ceil_div(N, kIT / 32), kIT, 0, c->stream>>>(N, c->fr_off.p, c->imp_lm.p, P + 3 * E,
                                                                  P + 4 * E, P + 5 * E, cfr, Afr, V,
                                                                  c->imp_tb.p, p.p, out, stop)));
   XM_CHECK_LAUNCH();
@@ -497,8 +512,7 @@ void implicit_translations(xm_ctx* c, const double* Y3, double* t_out) {
   m.alloc((size_t)M * XM_MAX_R + 8);
   bs.alloc((size_t)(3 * ceil_div(N, 3) + 6) * XM_MAX_R + 8);
   const double* P = c->imp_pts.p;
-  const int gM = ceil_div(M, kIT / 32);
-  k_imp_lm_mean<3><<<gM, kIT, 0, c->stream>>>(M, c->lm_off.p, c->e_fr.p, P, P + E, P + 2 * E, c->W.p, Y3,
+  k_imp_lm_mean<3><<<ceil_div(M, kIT / 32), kIT, 0, c->stream>>>(M, c->lm_off.p, c->e_fr.p, P, P + E, P + 2 * E, c->W.p, Y3,
                                               m.p, nullptr);
   if (N > 1)
     k_imp_fr_b<3><<<ceil_div(N - 1, kIT / 32), kIT, 0, c->stream>>>(N, c->fr_off.p, c->imp_lm.p, c->imp_w.p,
