@@ -287,6 +287,65 @@ def max_over_ranks(dist, x: float, device) -> float:
 
 
 # ----------------------------------------------------------------------------- xm arm
+def dense_bytes(N: int, r: int) -> float:
+    """Algorithmic bytes of one lower-triangle Q·V product."""
+    n = 3 * N
+    return 8.0 * n * (n + 1) / 2 + 16.0 * n * r
+
+
+def implicit_bytes(N: int, E: int, r: int) -> float:
+    """Algorithmic bytes of one matrix-free Q·V product (implicit_alg_bytes)."""
+    m = N - 1
+    return 80.0 * E + 8.0 * m * (m + 1) / 2 + 16.0 * 3 * N * r
+
+
+def roofline_pass(ctx, step, dev_in, out_dev, steps, barrier):
+    """K steps with CUDA events around every Q·V product (event records inside
+    the graphs add a few µs per launch, so timed regions run without them)."""
+    import torch
+    ctx.set_profile(True)
+    step(dev_in, out_dev)                    # recapture the graphs with event nodes
+    torch.cuda.synchronize()
+    ctx.reset_stats()
+    barrier()
+    for _ in range(steps):
+        step(dev_in, out_dev)
+    torch.cuda.synchronize()
+    barrier()
+    pstats = ctx.stats()
+    ctx.set_profile(False)
+    return pstats
+
+
+def roofline_obj(pstats, kernel, traffic, step_ms, steps):
+    ms_per = pstats["spmm_ms"] / max(pstats["spmm_timed"], 1)
+    bytes_per = pstats["spmm_alg_bytes"] / max(pstats["spmm_timed"], 1)
+    achieved = bytes_per / (ms_per / 1e3) / 1e9 if pstats["spmm_timed"] else None
+    peak, peak_kind = hbm_peak()
+    return {"kernel": kernel, "bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
+            "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+            "alg_bytes_per_launch": bytes_per, "launch_ms": ms_per, "launches": pstats["spmm_timed"],
+            "share_of_step": pstats["spmm_ms"] / (step_ms * steps) if step_ms > 0 else None,
+            "timing": "CUDA events around every Q·V product (persistent tCG: per launch ÷ its "
+                      "iterations; graph replays past a tCG stop excluded), on the library's stream, "
+                      "over a second run of min(K, 5) steps"}
+
+
+def traffic_of(key):
+    try:
+        with open(TRAFFIC_FILE) as f:
+            return json.load(f).get(key, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+KERNEL_DENSE_B = ("k_tcg_persist_sym (lower-triangle Q stream, timed per tCG iteration incl. its "
+                  "barriers and camera update) + k_spmm_sym (other products)")
+KERNEL_DENSE = "k_spmm_sym (lower-triangle Q stream, every product incl. the tCG HVP)"
+KERNEL_IMPLICIT = ("matrix-free Q·V product, timed as one unit: k_imp_lm_mean, k_imp_fr_b, "
+                   "k_spmm_sym on the lower triangle of K̄⁻¹, k_imp_lm_p, k_imp_fr_out")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -297,9 +356,11 @@ def main():
     ap.add_argument("--impl", default="xm", choices=["xm", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--mode", default="dense", choices=["dense", "implicit"],
-                    help="headline mode: dense Q (default) or the matrix-free NEXT-1 products; "
-                         "the other mode is measured too (one GPU) and reported under 'other_mode'")
+    ap.add_argument("--mode", default="auto", choices=["auto", "dense", "implicit"],
+                    help="headline product mode: dense Q, the matrix-free NEXT-1 products, or auto "
+                         "(default: matrix-free on one GPU when its bytes per product are under half "
+                         "the lower-triangle Q stream's); the other mode is measured too (one GPU) "
+                         "and reported under 'other_mode'")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -332,6 +393,8 @@ def main():
                    p=torch.empty((sc.M, 3), dtype=torch.float64, device=dev))
     stream = torch.cuda.current_stream(dev)
     implicit = 1 if (args.mode == "implicit" and world == 1) else 0
+    if args.mode == "auto" and world == 1:
+        implicit = 1 if implicit_bytes(sc.N, sc.E, 3) < 0.5 * dense_bytes(sc.N, 3) else 0
     ctx = xm.Context(device=local, rank=rank, world=world, nccl_id=nccl_id,
                      stream=stream.cuda_stream, profile=0, implicit_q=implicit)
 
@@ -366,21 +429,9 @@ def main():
     ms = max_over_ranks(dist, e0.elapsed_time(e1) / args.steps, dev)
     stats = ctx.stats()
 
-    # ---- roofline pass: the same K steps with CUDA events around every Q·V
-    # launch (event records inside the graphs add a few µs per launch, so the
-    # timed region above runs without them)
-    ctx.set_profile(True)
-    step(dev_in, out_dev)                    # recapture the graphs with event nodes
-    torch.cuda.synchronize()
-    ctx.reset_stats()
-    barrier()
+    # ---- roofline pass: the same steps with CUDA events around every Q·V product
     aux_steps = min(args.steps, 5)          # roofline / e2e passes: at most 5 steps each
-    for _ in range(aux_steps):
-        step(dev_in, out_dev)
-    torch.cuda.synchronize()
-    barrier()
-    pstats = ctx.stats()
-    ctx.set_profile(False)
+    pstats = roofline_pass(ctx, step, dev_in, out_dev, aux_steps, barrier)
 
     # ---- end to end through the public API with pinned host buffers
     e2e = None
@@ -402,17 +453,9 @@ def main():
 
     st, info, cert = infos[-1]
     value = ms / 1e3
-    spmm_ms_per_launch = pstats["spmm_ms"] / max(pstats["spmm_timed"], 1)
-    bytes_per_launch = pstats["spmm_alg_bytes"] / max(pstats["spmm_timed"], 1)
-    achieved = bytes_per_launch / (spmm_ms_per_launch / 1e3) / 1e9 if pstats["spmm_timed"] else None
-    peak, peak_kind = hbm_peak()
-    traffic = None
-    try:
-        with open(TRAFFIC_FILE) as f:
-            traffic = json.load(f).get(args.config, {}).get("dram_bytes_per_launch")
-    except Exception:
-        pass
-    spmm_share = pstats["spmm_ms"] / (ms * aux_steps) if ms > 0 else None
+    tkey = f"{args.config}_implicit" if implicit else args.config
+    kname = KERNEL_IMPLICIT if implicit else (KERNEL_DENSE_B if sc.N < 4000 else KERNEL_DENSE)
+    roof = roofline_obj(pstats, kname, traffic_of(tkey), ms, aux_steps)
     result = {
         "metric": METRIC, "value": value, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
@@ -420,7 +463,10 @@ def main():
         "config": {"workload": f"config {args.config}: {CONFIG_DESCRIPTIONS[args.config]}",
                    "N": sc.N, "M": sc.M, "E": sc.E, "seed": args.seed,
                    "mode": "implicit (NEXT-1)" if implicit else "dense Q",
-                   "parallelism": f"bands{world}", "l2": "inputs larger than L2 (Q > 126 MB)"},
+                   "parallelism": f"bands{world}",
+                   "l2": ("inputs larger than L2 (per-measurement streams 0.4 GB + K̄⁻¹ lower triangle "
+                          "0.41 GB per product > 126 MB)" if implicit else
+                          "inputs larger than L2 (Q > 126 MB)")},
         "hvp_per_s": info["hvps"] / value if value > 0 else None,
         "solve": {"hvps": info["hvps"], "spmms": info["spmms"], "lanczos_steps": info["lanczos_steps"],
                   "outer_iters": info["outer_iters"], "r": info["r"], "escapes": info["escapes"],
@@ -431,18 +477,7 @@ def main():
                   "eta": cert["eta"], "eta_rigorous": cert["eta_rigorous"],
                   "rho_hat": cert["rho_hat"], "status": st},
         "phases_ms": {k: stats[k] / args.steps for k in ("ms_build", "ms_solve", "ms_certify", "ms_round")},
-        "roofline": {"kernel": ("k_tcg_persist_sym (lower-triangle Q stream, timed per tCG iteration "
-                                "incl. its barriers and camera update) + k_spmm_sym (other products)"
-                                if sc.N < 4000 else
-                                "k_spmm_sym (lower-triangle Q stream, every product incl. the tCG HVP)"),
-                     "bound": "hbm", "achieved": achieved,
-                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "alg_bytes_per_launch": bytes_per_launch, "launch_ms": spmm_ms_per_launch,
-                     "launches": pstats["spmm_timed"], "share_of_step": spmm_share,
-                     "timing": "CUDA events around every Q-streaming launch (persistent tCG: per launch "
-                               "÷ its iterations), on the library's stream, over a second run of "
-                               "min(K, 5) steps"},
+        "roofline": roof,
         "gpu_launches": int(stats["kernel_launches"]),
         "e2e": e2e,
     }
@@ -471,12 +506,15 @@ def main():
             o1.record(stream)
             torch.cuda.synchronize()
             s2 = c2.stats()
-            n_ = 3 * sc.N
-            per_product = (8.0 * n_ * (n_ + 1) / 2 + 16.0 * n_ * 3) if other == 0 else \
-                (sc.E * (36 + 36 + 12 + 36) + 8.0 * (sc.N - 1) ** 2)
+            v2 = o0.elapsed_time(o1) / k2
+            ps2 = roofline_pass(c2, lambda a, b: step2(), dev_in, out_dev, k2, lambda: None)
+            roof2 = roofline_obj(ps2, KERNEL_IMPLICIT if other else (KERNEL_DENSE_B if sc.N < 4000
+                                                                     else KERNEL_DENSE),
+                                 traffic_of(f"{args.config}_implicit" if other else args.config), v2, k2)
+            per_product = dense_bytes(sc.N, 3) if other == 0 else implicit_bytes(sc.N, sc.E, 3)
             result["other_mode"] = {
                 "mode": "dense" if other == 0 else "implicit (NEXT-1, Q never formed)",
-                "value": o0.elapsed_time(o1) / k2 / 1e3, "unit": "s", "steps": k2,
+                "value": v2 / 1e3, "unit": "s", "steps": k2, "roofline": roof2,
                 "phases_ms": {k: s2[k] / k2 for k in ("ms_build", "ms_solve", "ms_certify", "ms_round")},
                 "hvps": info2["hvps"], "spmms": info2["spmms"], "r": info2["r"],
                 "certified": info2["certified"], "eta": cert2["eta"], "status": st2,

@@ -79,8 +79,10 @@ __global__ void __launch_bounds__(kIT) k_imp_lm_mean(int M, const int32_t* __res
                                                      const double* __restrict__ W,
                                                      const double* __restrict__ V,
                                                      double* __restrict__ m,
-                                                     const int* __restrict__ stop) {
+                                                     const int* __restrict__ stop,
+                                                     int* __restrict__ exec) {
   if (stop && *stop) return;  // a tCG graph replay past the stop
+  if (exec && blockIdx.x == 0 && threadIdx.x == 0) *exec = 1;  // profiling: this product ran
   constexpr int NG = Grp<R>::NG;
   const int k = blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (k >= M) return;
@@ -469,7 +471,17 @@ static void kinv_product(xm_ctx* c, const double* bs, int r, const int* stop) {
   }
 }
 
-void implicit_product(xm_ctx* c, const double* V, int r, double* out, const int* stop) {
+// Algorithmic bytes of one matrix-free product: the four passes'
+// per-measurement streams (28 + 12 + 12 + 28 B), the lower triangle of K̄⁻¹
+// (r ≤ 5; the full matrix for the row GEMV) and V in / Q·V out; the gathered
+// n × r / M × r arrays are L2-resident and not counted.
+double implicit_alg_bytes(xm_ctx* c, int r) {
+  const double m = (double)c->N - 1.0;
+  const double kb = (r <= 5) ? 8.0 * m * (m + 1.0) / 2.0 : 8.0 * m * m;
+  return 80.0 * (double)c->E + kb + 16.0 * (double)c->n * r;
+}
+
+void implicit_product(xm_ctx* c, const double* V, int r, double* out, const int* stop, int* exec) {
   const int N = c->N, M = c->M;
   const int64_t E = c->E;
   DBuf<double>& m = scratch_f64(c, "imp_m");
@@ -483,7 +495,7 @@ void implicit_product(xm_ctx* c, const double* V, int r, double* out, const int*
   const double* Afr = c->imp_mom.p + 3 * (size_t)N;
   imp_dbg(c, "entry");
   XM_IMP_DISPATCH(r, (k_imp_lm_mean<R><<<ceil_div(M, kIT / 32), kIT, 0, c->stream>>>(M, c->lm_off.p, c->e_fr.p, P, P + E,
-                                                                  P + 2 * E, c->W.p, V, m.p, stop)));
+                                                                  P + 2 * E, c->W.p, V, m.p, stop, exec)));
   imp_dbg(c, "lm_mean");
   if (N > 1)
     XM_IMP_DISPATCH(r, (k_imp_fr_b<R><<<ceil_div(N - 1, kIT / 32), kIT, 0, c->stream>>>(
@@ -513,7 +525,7 @@ void implicit_translations(xm_ctx* c, const double* Y3, double* t_out) {
   bs.alloc((size_t)(3 * ceil_div(N, 3) + 6) * XM_MAX_R + 8);
   const double* P = c->imp_pts.p;
   k_imp_lm_mean<3><<<ceil_div(M, kIT / 32), kIT, 0, c->stream>>>(M, c->lm_off.p, c->e_fr.p, P, P + E, P + 2 * E, c->W.p, Y3,
-                                              m.p, nullptr);
+                                              m.p, nullptr, nullptr);
   if (N > 1)
     k_imp_fr_b<3><<<ceil_div(N - 1, kIT / 32), kIT, 0, c->stream>>>(N, c->fr_off.p, c->imp_lm.p, c->imp_w.p,
                                                                     c->imp_mom.p, Y3, m.p, bs.p, nullptr);

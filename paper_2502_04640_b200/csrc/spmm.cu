@@ -508,28 +508,33 @@ static double alg_bytes(xm_ctx* c, int r, int mode) {
   return qb + 8.0 * n * r + 8.0 * (double)c->nrows * r;
 }
 
-// One (optionally profiled) SpMM launch with epilogue `mode` on this rank's rows.
-void spmm(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep_in) {
-  if (mode != EPI_STORE && c->world > 1)
-    throw Error(XM_EINVAL, "fused epilogues need world == 1 (use spmm_full + epilogue kernels)");
-  SpmmEpiArgs ep = ep_in;
-  bool timed = c->opt.profile != 0;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (timed && c->cap_target) {
-    // capturing a graph: the event pair and exec flag belong to the graph
+// Profiling (opt.profile): a CUDA event pair around one product on the
+// library's stream plus an exec flag the product's first kernel sets when it
+// really runs (graph replays past a tCG stop early-exit and are not counted);
+// inside a graph capture the events and flag belong to the graph.
+struct ProdTimer {
+  cudaEvent_t e1 = nullptr;
+  int* exec = nullptr;
+};
+
+static ProdTimer prod_timer_begin(xm_ctx* c, double bytes) {
+  ProdTimer t;
+  if (!c->opt.profile) return t;
+  cudaEvent_t e0 = nullptr;
+  if (c->cap_target) {
     auto* g = c->cap_target;
     size_t pair = g->bytes.size();
     if ((pair + 1) * sizeof(int) > g->execf.n * sizeof(int))
       throw Error(XM_EINVAL, "graph profiling slots exhausted");
     XM_CUDA(cudaEventCreate(&e0));
-    XM_CUDA(cudaEventCreate(&e1));
+    XM_CUDA(cudaEventCreate(&t.e1));
     g->ev.push_back(e0);
-    g->ev.push_back(e1);
-    g->bytes.push_back(alg_bytes(c, r, mode));
-    ep.exec = g->execf.p + pair;
+    g->ev.push_back(t.e1);
+    g->bytes.push_back(bytes);
+    t.exec = g->execf.p + pair;
     // External ⇒ captured as an event-record node (plain records are capture markers)
     XM_CUDA(cudaEventRecordWithFlags(e0, c->stream, cudaEventRecordExternal));
-  } else if (timed) {
+  } else {
     if (c->ev_pool.empty()) {
       for (int q = 0; q < 1024; ++q) {
         cudaEvent_t e;
@@ -542,12 +547,28 @@ void spmm(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep_in)
     }
     if (c->ev_used + 2 > c->ev_pool.size()) harvest_events(c);
     e0 = c->ev_pool[c->ev_used++];
-    e1 = c->ev_pool[c->ev_used++];
+    t.e1 = c->ev_pool[c->ev_used++];
     size_t pair = c->ev_used / 2 - 1;
-    ep.exec = c->ev_exec.p + pair;
-    c->ev_bytes[pair] = alg_bytes(c, r, mode);
+    t.exec = c->ev_exec.p + pair;
+    c->ev_bytes[pair] = bytes;
     XM_CUDA(cudaEventRecord(e0, c->stream));
   }
+  return t;
+}
+
+static void prod_timer_end(xm_ctx* c, const ProdTimer& t) {
+  if (!t.e1) return;
+  if (c->cap_target) XM_CUDA(cudaEventRecordWithFlags(t.e1, c->stream, cudaEventRecordExternal));
+  else XM_CUDA(cudaEventRecord(t.e1, c->stream));
+}
+
+// One (optionally profiled) SpMM launch with epilogue `mode` on this rank's rows.
+void spmm(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep_in) {
+  if (mode != EPI_STORE && c->world > 1)
+    throw Error(XM_EINVAL, "fused epilogues need world == 1 (use spmm_full + epilogue kernels)");
+  SpmmEpiArgs ep = ep_in;
+  const ProdTimer tm = prod_timer_begin(c, alg_bytes(c, r, mode));
+  if (tm.exec) ep.exec = tm.exec;
   if (mode != EPI_TCG && spmm_sym_supported(c, r)) {
     spmm_sym_launch(c, V, r, mode, ep);
   } else switch (mode) {
@@ -559,10 +580,7 @@ void spmm(xm_ctx* c, const double* V, int r, int mode, const SpmmEpiArgs& ep_in)
     case EPI_TCG: launch_tcg(c, V, r, ep); break;
     default: throw Error(XM_EINVAL, "bad epilogue");
   }
-  if (timed) {
-    if (c->cap_target) XM_CUDA(cudaEventRecordWithFlags(e1, c->stream, cudaEventRecordExternal));
-    else XM_CUDA(cudaEventRecord(e1, c->stream));
-  }
+  prod_timer_end(c, tm);
   c->stats.spmm_calls++;
   c->stats.spmm_rows = c->nrows;
 }
@@ -591,8 +609,10 @@ __global__ void k_unpack_cols(int64_t n, int r, int c0, int w, const double* __r
 // shards and halves each rank's Q bytes.  r > 5: column groups of ≤ 5.
 void spmm_full(xm_ctx* c, const double* V, int r, double* out_full, const int* stop) {
   if (c->implicit_active) {  // NEXT-1: matrix-free (implicit.cu); after a tCG stop the
-    // passes still run inside a graph replay, their result is ignored by the update kernels
-    implicit_product(c, V, r, out_full, stop);
+    // passes of a graph replay early-exit, their result is ignored by the update kernels
+    const ProdTimer tm = prod_timer_begin(c, implicit_alg_bytes(c, r));
+    implicit_product(c, V, r, out_full, stop, tm.exec);
+    prod_timer_end(c, tm);
     c->stats.spmm_calls++;
     return;
   }

@@ -362,7 +362,9 @@ void batch_staircase(xm_ctx* c, int B, int N, const double* Q_dev, int64_t qstri
                      const double* Y0_dev, int r0, double* Yout_dev, xm_batch_result* res_dev);
 // NEXT-1 (implicit.cu)
 void implicit_prepare(xm_ctx* c);
-void implicit_product(xm_ctx* c, const double* V, int r, double* out, const int* stop = nullptr);
+void implicit_product(xm_ctx* c, const double* V, int r, double* out, const int* stop = nullptr,
+                      int* exec = nullptr);
+double implicit_alg_bytes(xm_ctx* c, int r);
 void implicit_translations(xm_ctx* c, const double* Y3, double* t_out);
 double implicit_normF(xm_ctx* c);
 void splitmix_uniform(xm_ctx* c, int64_t n, uint64_t seed, double* out);  // cert.cu
