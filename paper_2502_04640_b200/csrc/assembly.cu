@@ -815,8 +815,11 @@ static void trsm_block_inner(xm_ctx* c, const double* L, int64_t ldl, const doub
 // rows below get ONE TN DMMA update with K = SB (U = Lᵀ from the
 // factorisation is the A operand: L₂₁[i][k] = U[k][i]).  The serial 64-row
 // solves only ever touch SB columns.
+// lower_rhs: B is lower triangular (B[i][j] = 0 for j > i, e.g. the identity
+// when inverting L) — then so is the solution, and super-block rows sb..se only
+// carry columns < se: m³/3 instead of m³ flops.
 void dense_trsm_lower_left(xm_ctx* c, const double* L, int m, int64_t ldl, const double* U,
-                           int64_t ldu, double* B, int ncols, int64_t ldb) {
+                           int64_t ldu, double* B, int ncols, int64_t ldb, bool lower_rhs) {
   const int SB = c->trsm_sb;
   DBuf<double>& T = scratch_f64(c, "trsm_inv");
   DBuf<double>& Tt = scratch_f64(c, "trsm_invT");
@@ -833,12 +836,13 @@ void dense_trsm_lower_left(xm_ctx* c, const double* L, int m, int64_t ldl, const
                                                                                        SB, s, s);
     XM_CHECK_LAUNCH();
     count_launch(c, 2);
+    const int nc = lower_rhs ? std::min(ncols, se) : ncols;  // columns ≥ se of rows < se are 0
     // X = L_ss⁻¹ B_s :  X[i][j] = Σ_k Tt[k][i] B[sb + k][j]
-    dgemm_tn(c, false, s, ncols, s, 1.0, Tt.p, SB, B + (int64_t)sb * ldb, ldb, 0.0, X.p, ldb);
-    XM_CUDA(cudaMemcpyAsync(B + (int64_t)sb * ldb, X.p, (size_t)s * ldb * sizeof(double),
-                            cudaMemcpyDeviceToDevice, c->stream));
+    dgemm_tn(c, false, s, nc, s, 1.0, Tt.p, SB, B + (int64_t)sb * ldb, ldb, 0.0, X.p, ldb);
+    XM_CUDA(cudaMemcpy2DAsync(B + (int64_t)sb * ldb, ldb * sizeof(double), X.p, ldb * sizeof(double),
+                              (size_t)nc * sizeof(double), s, cudaMemcpyDeviceToDevice, c->stream));
     if (se < m)
-      dgemm_tn(c, false, m - se, ncols, s, -1.0, U + (int64_t)sb * ldu + se, ldu,
+      dgemm_tn(c, false, m - se, nc, s, -1.0, U + (int64_t)sb * ldu + se, ldu,
                B + (int64_t)sb * ldb, ldb, 1.0, B + (int64_t)se * ldb, ldb);
   }
 }

@@ -125,6 +125,9 @@ __global__ void __launch_bounds__(T::THREADS)
     tn = blockIdx.x % tiles_n;
   }
   const int m0 = tm * T::BM, n0 = tn * T::BN;
+  // TRI == 2: A = B lower triangular in (k, m) (A[k][m] = 0 for k < m, e.g.
+  // X = L⁻¹ read transposed): the output rows m ≥ m0 only see k ≥ m0
+  const int kbeg = (TRI == 2) ? m0 / BK : 0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tig = lane & 3;
   const int wm = warp % T::WMW, wn = warp / T::WMW;
@@ -143,10 +146,10 @@ __global__ void __launch_bounds__(T::THREADS)
 #pragma unroll
     for (int t = 0; t < 4; ++t) acc[s][t][0] = acc[s][t][1] = 0.0;
 
-  const int nk = (K + BK - 1) / BK;
+  const int nk = (K + BK - 1) / BK - kbeg;
 #pragma unroll
   for (int st = 0; st < ST - 1; ++st) {
-    if (st < nk) load(st, st);
+    if (st < nk) load(st, kbeg + st);
     cp_commit();
   }
   // per-lane shared offsets (doubles) of its fragment pairs
@@ -157,7 +160,7 @@ __global__ void __launch_bounds__(T::THREADS)
     __syncthreads();
     {  // refill the slot consumed in iteration kt−1
       const int nx = kt + ST - 1;
-      if (nx < nk) load(nx % ST, nx);
+      if (nx < nk) load(nx % ST, kbeg + nx);
       cp_commit();
     }
     const double* As = smem + (kt % ST) * T::STAGE;
@@ -225,7 +228,7 @@ void launch_tn(xm_ctx* c, int M, int N, int K, double alpha, const double* A, in
                const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
   ensure_smem_attr((const void*)k_dgemm_tn<T, TRI, V>, T::SMEM);
   const int tm = ceil_div(M, T::BM), tn = ceil_div(N, T::BN);
-  const int64_t tiles = TRI ? (int64_t)tm * (tm + 1) / 2 : (int64_t)tm * tn;
+  const int64_t tiles = TRI ? (int64_t)tm * (tm + 1) / 2 : (int64_t)tm * tn;  // TRI 1, 2: lower tiles
   if (tiles <= 0) return;
   if (tiles > INT32_MAX) throw Error(XM_EINVAL, "dgemm_tn: too many tiles");
   const int vec_out = ((reinterpret_cast<uintptr_t>(C) & 31) == 0 && (ldc & 3) == 0) ? 1 : 0;
@@ -248,6 +251,17 @@ void dispatch(xm_ctx* c, bool lower, bool v16, int M, int N, int K, double alpha
 }
 
 }  // namespace
+
+// C (lower tiles) = α XᵀX + β C for X lower triangular (X[k][m] = 0 for k < m):
+// the k-loop of output row block m0 starts at m0 — m³/3 instead of m³ flops
+// (NEXT-1: K̄⁻¹ = L⁻ᵀL⁻¹, implicit.cu)
+void dsyrk_tn_lowtri(xm_ctx* c, int M, double alpha, const double* X, int64_t ldx, double beta, double* C,
+                     int64_t ldc) {
+  if (M <= 0) return;
+  const bool v16 = (reinterpret_cast<uintptr_t>(X) & 15) == 0 && (ldx % 2) == 0;
+  if (v16) launch_tn<W16Tile, 2, true>(c, M, M, M, alpha, X, ldx, X, ldx, beta, C, ldc);
+  else launch_tn<W16Tile, 2, false>(c, M, M, M, alpha, X, ldx, X, ldx, beta, C, ldc);
+}
 
 void dgemm_tn(xm_ctx* c, bool lower, int M, int N, int K, double alpha, const double* A,
               int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {

@@ -415,7 +415,7 @@ void certify_current(xm_ctx* c, double* lambda, int* steps) {
       DBuf<double>& X = scratch_f64(c, "zw_X");
       X.alloc((size_t)c->n * c->ldq);
       identity(c, X.p, c->n, c->ldq);
-      dense_trsm_lower_left(c, c->Zw.p, c->n, c->ldq, U.p, c->ldq, X.p, c->n, c->ldq);
+      dense_trsm_lower_left(c, c->Zw.p, c->n, c->ldq, U.p, c->ldq, X.p, c->n, c->ldq, true);
       double th = 0.0;
       int s2 = 0;
       LanczosOp op;

@@ -283,7 +283,10 @@ bool dense_cholesky(xm_ctx* c, double* A, int m, int64_t lda, double rel_tol,
 bool psd_test_cholesky(xm_ctx* c, double shift, double* lower = nullptr, double* U = nullptr,
                        int64_t ldu = 0);
 void dense_trsm_lower_left(xm_ctx* c, const double* L, int m, int64_t ldl, const double* U,
-                           int64_t ldu, double* B, int ncols, int64_t ldb);
+                           int64_t ldu, double* B, int ncols, int64_t ldb, bool lower_rhs = false);
+// C (lower tiles) = α XᵀX + β C for lower-triangular X (k-loop from the tile row)
+void dsyrk_tn_lowtri(xm_ctx* c, int M, double alpha, const double* X, int64_t ldx, double beta, double* C,
+                     int64_t ldc);
 // C = β·C + α·Σ_k A[k·lda + m]·B[k·ldb + n] on the fp64 tensor cores (dgemm_tn.cu);
 // lower ⇒ only the lower-triangle tiles (M == N)
 void dgemm_tn(xm_ctx* c, bool lower, int M, int N, int K, double alpha, const double* A,
