@@ -356,6 +356,8 @@ def main():
     ap.add_argument("--impl", default="xm", choices=["xm", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-other-mode", action="store_true",
+                    help="skip the measurement of the other product mode (profiling runs)")
     ap.add_argument("--mode", default="auto", choices=["auto", "dense", "implicit"],
                     help="headline product mode: dense Q, the matrix-free NEXT-1 products, or auto "
                          "(default: matrix-free on one GPU when its bytes per product are under half "
@@ -483,7 +485,7 @@ def main():
     }
     clocks = clk.summary()
     result["clocks"] = clocks
-    if world == 1:
+    if world == 1 and not args.no_other_mode:
         # the other product mode on the same workload (SURVEY §8(f) NEXT-1 vs the dense stream)
         other = 1 - implicit
         with xm.Context(device=local, stream=stream.cuda_stream, profile=0, implicit_q=other) as c2:

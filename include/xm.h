@@ -239,8 +239,11 @@ xm_status xm_round_recover(xm_ctx* ctx, double* R, double* s, double* t, double*
  *   keep (E bytes, caller's input order, host or device, or NULL): 1 for the
  *   measurements the rebuilt Q uses.  n_dropped / n_restored (or NULL): net
  *   drops and restorations.  drop_fraction ∉ [0, 1) ⇒ XM_EINVAL; a graph that
- *   no restoration reconnects ⇒ XM_EDISCONNECTED.  Repeated calls compose
- *   (indices always refer to the caller's original input). */
+ *   no restoration reconnects ⇒ XM_EDISCONNECTED (context unchanged).  A
+ *   failure while the rebuild replaces the data (e.g. XM_ENOMEM) leaves the
+ *   context with no data (as after xm_create): rebuild with xm_build_Q.
+ *   Repeated calls compose (indices always refer to the caller's original
+ *   input). */
 xm_status xm_edge_residuals(xm_ctx* ctx, double* res);
 xm_status xm_xm2(xm_ctx* ctx, double drop_fraction, uint8_t* keep, int64_t* n_dropped,
                  int64_t* n_restored);

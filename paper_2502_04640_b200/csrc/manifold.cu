@@ -302,14 +302,21 @@ __global__ void __launch_bounds__(kFT) k_tcg_update(int N, const TcgState* __res
 }
 
 // K3: stop tests, β, recurrences; δ ← −r + βδ.  Grid over n·r elements.
+// cond ≠ 0: the kernel is the last node of the body of a conditional WHILE
+// graph node (one graph launch runs the whole tCG loop, xm_api.cu tcg_graph):
+// it clears the loop condition once the state says stop.
 __global__ void __launch_bounds__(256) k_tcg_dir(int64_t len, const TcgState* __restrict__ sin,
                                                  TcgState* __restrict__ sout,
                                                  const double* __restrict__ p2, int n2,
                                                  const double* __restrict__ res,
-                                                 double* __restrict__ dir) {
+                                                 double* __restrict__ dir,
+                                                 cudaGraphConditionalHandle cond, int use_cond) {
   TcgState s = *sin;
   if (s.stop) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) *sout = s;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      *sout = s;
+      if (use_cond) cudaGraphSetConditional(cond, 0);
+    }
     return;
   }
   const double z = block_sum_all<256>(p2, n2);
@@ -325,7 +332,10 @@ __global__ void __launch_bounds__(256) k_tcg_dir(int64_t len, const TcgState* __
     s.d_Pd = s.z + s.beta * s.beta * s.d_Pd;
     if (s.j >= s.max_inner) s.stop = TCG_MAXINNER;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *sout = s;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *sout = s;
+    if (use_cond && s.stop) cudaGraphSetConditional(cond, 0);
+  }
   if (s.stop) return;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < len;
        t += (int64_t)gridDim.x * blockDim.x)
@@ -534,7 +544,7 @@ void tcg_iteration(xm_ctx* c, int r) {
   XM_CHECK_LAUNCH();
   int g3 = std::max(1, std::min(ceil_div(len, 256), 148));
   k_tcg_dir<<<g3, 256, 0, c->stream>>>(len, c->tcg.p + 1, c->tcg.p, c->part2.p, nb, c->res.p,
-                                       c->dir.p);
+                                       c->dir.p, c->cap_cond, c->cap_cond_on ? 1 : 0);
   XM_CHECK_LAUNCH();
   count_launch(c, 2);
 }

@@ -360,9 +360,18 @@ void xm2_device(xm_ctx* c, double frac, uint8_t* keep_user_dev, int64_t* n_dropp
                                                      c->e_in.p, orig, nfr.p, nlm.p, npts.p, nw.p, norig.p);
   XM_CHECK_LAUNCH();
   count_launch(c);
-  c->orig_in.alloc(std::max<int32_t>(Ek, 1));
-  XM_CUDA(cudaMemcpyAsync(c->orig_in.p, norig.p, (size_t)Ek * 4, cudaMemcpyDeviceToDevice, c->stream));
-  build_Q_device(c, N, M, Ek, nfr.p, nlm.p, npts.p, nw.p);
+  // from here the context's measurement mapping and data matrix are replaced
+  // step by step: a failure (e.g. XM_ENOMEM) leaves no consistent previous
+  // stage to fall back to, so the context drops to "no data" (stage 0) and a
+  // later call must rebuild (xm.h: xm_xm2 error behaviour)
+  try {
+    c->orig_in.alloc(std::max<int32_t>(Ek, 1));
+    XM_CUDA(cudaMemcpyAsync(c->orig_in.p, norig.p, (size_t)Ek * 4, cudaMemcpyDeviceToDevice, c->stream));
+    build_Q_device(c, N, M, Ek, nfr.p, nlm.p, npts.p, nw.p);
+  } catch (...) {
+    c->stage = 0;
+    throw;
+  }
 }
 
 }  // namespace xm

@@ -163,6 +163,74 @@ void destroy_graph(xm_ctx::TcgGraph& g) {
   g.bytes.clear();
   g.sig.clear();
   g.batch = 0;
+  g.loop = false;
+}
+
+// The whole tCG loop as ONE graph launch: a conditional WHILE node whose body
+// is one three-kernel iteration (product + HVP epilogue, k_tcg_update,
+// k_tcg_dir); k_tcg_dir clears the condition when the device state says stop,
+// so no iteration past the stop is launched and the host syncs once per tCG
+// solve instead of once per batch.  Profiling runs keep the batched graphs
+// (event-record nodes are not allowed in conditional bodies).  Returns false
+// (nothing built) where unsupported.
+static bool capture_tcg_loop(xm_ctx* c, int r, xm_ctx::TcgGraph& g) {
+  if (c->opt.profile || tcg_fused_supported(c, r) || std::getenv("XM_NO_COND_GRAPH")) return false;
+  cudaGraph_t graph = nullptr;
+  XM_CUDA(cudaGraphCreate(&graph, 0));
+  cudaGraphConditionalHandle h = 0;
+  cudaGraph_t body = nullptr;
+  cudaGraphNode_t node = nullptr;
+  if (cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault) != cudaSuccess) {
+    cudaGetLastError();
+    cudaGraphDestroy(graph);
+    return false;
+  }
+  cudaGraphNodeParams cp{};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  if (cudaGraphAddNode(&node, graph, nullptr, 0, &cp) != cudaSuccess) {
+    cudaGetLastError();
+    cudaGraphDestroy(graph);
+    return false;
+  }
+  body = cp.conditional.phGraph_out[0];
+  cudaStream_t orig = c->stream;
+  const int64_t l0 = c->stats.kernel_launches, s0 = c->stats.spmm_calls;
+  c->stream = c->cap_stream;
+  c->cap_cond = h;
+  c->cap_cond_on = true;
+  bool ok = true;
+  try {
+    XM_CUDA(cudaStreamBeginCaptureToGraph(c->cap_stream, body, nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeRelaxed));
+    tcg_iteration(c, r);
+    cudaGraph_t out = nullptr;
+    XM_CUDA(cudaStreamEndCapture(c->cap_stream, &out));
+  } catch (...) {
+    cudaGraph_t out = nullptr;
+    cudaStreamEndCapture(c->cap_stream, &out);
+    cudaGetLastError();
+    ok = false;
+  }
+  c->stream = orig;
+  c->cap_cond_on = false;
+  c->cap_cond = 0;
+  g.launches = c->stats.kernel_launches - l0;
+  g.spmms = c->stats.spmm_calls - s0;
+  c->stats.kernel_launches = l0;
+  c->stats.spmm_calls = s0;
+  if (ok && cudaGraphInstantiate(&g.exec, graph, 0) != cudaSuccess) {
+    cudaGetLastError();
+    g.exec = nullptr;
+    ok = false;
+  }
+  cudaGraphDestroy(graph);
+  if (!ok) return false;
+  g.loop = true;
+  g.batch = 0;
+  return true;
 }
 
 xm_ctx::TcgGraph* tcg_graph(xm_ctx* c, int r) {
@@ -172,6 +240,8 @@ xm_ctx::TcgGraph* tcg_graph(xm_ctx* c, int r) {
   destroy_graph(g);
   g.sig = sig;
   if (!c->cap_stream) XM_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  sync(c);
+  if (capture_tcg_loop(c, r, g)) return &g;
   g.batch = c->tcg_batch;
   g.execf.alloc((size_t)g.batch * 4 + 8);
   XM_CUDA(cudaMemsetAsync(g.execf.p, 0, g.execf.n * sizeof(int), c->stream));
@@ -274,7 +344,16 @@ TcgState run_tcg(xm_ctx* c, int r, double Delta) {
   }
   const int64_t s0 = c->stats.spmm_calls;
   while (!persist) {
-    if (g) {
+    if (g && g->loop) {  // the whole loop in one launch (the condition ends it)
+      XM_CUDA(cudaGraphLaunch(g->exec, c->stream));
+      XM_CUDA(cudaMemcpyAsync(&hs, c->tcg.p, sizeof(TcgState), cudaMemcpyDeviceToHost, c->stream));
+      sync(c);
+      // iterations launched: one per HVP plus the final one whose update saw the stop
+      c->stats.kernel_launches += g->launches * std::max<int64_t>(1, hs.n_hvp);
+      if (!hs.stop) throw Error(XM_ECUDA, "tCG loop graph returned before its stop");
+      c->stats.spmm_calls = s0 + hs.n_hvp;
+      break;
+    } else if (g) {
       XM_CUDA(cudaGraphLaunch(g->exec, c->stream));
       c->stats.kernel_launches += g->launches;
     } else {

@@ -146,6 +146,7 @@ struct xm_ctx {
   xm::DBuf<int32_t> imp_lm;                // frame-sorted landmark ids
   xm::DBuf<double> imp_pts, imp_w, Kinv;   // w·ũ (landmark- and frame-sorted SoA), frame-sorted w
   xm::DBuf<double> imp_mom, imp_tb;        // per-frame c_i, A_i; [0; K̄⁻¹ b]
+  xm::DBuf<double> imp_rec;                // 32-B measurement records (landmark / frame order)
   void* imp_sym_plan = nullptr;            // lower-triangle stream plan of K̄⁻¹
   xm::DBuf<double> imp_sym_part;
   xm::DBuf<double> lam;    // N × 6 (xx, yy, zz, xy, xz, yz)
@@ -200,8 +201,9 @@ struct xm_ctx {
   // CUDA graph of `tcg_batch` tCG iterations per rank r (captured once, replayed)
   struct TcgGraph {
     cudaGraphExec_t exec = nullptr;
-    int batch = 0;
-    int64_t launches = 0, spmms = 0;              // kernels / SpMMs per replay
+    int batch = 0;                                // iterations per replay (0: conditional loop)
+    bool loop = false;                            // conditional WHILE node: the whole tCG per replay
+    int64_t launches = 0, spmms = 0;              // kernels / SpMMs per replay (loop: per iteration)
     std::vector<cudaEvent_t> ev;                  // profiling event pairs (captured)
     std::vector<double> bytes;                    // algorithmic bytes per pair
     xm::DBuf<int> execf;                          // per pair: 1 if the SpMM ran
@@ -209,6 +211,10 @@ struct xm_ctx {
   };
   TcgGraph tcg_graphs[XM_MAX_R + 1];
   TcgGraph* cap_target = nullptr;                 // non-null while capturing
+  // capturing the body of a conditional WHILE node (the whole tCG loop in one
+  // graph launch): k_tcg_dir clears `cap_cond` when the tCG state says stop
+  cudaGraphConditionalHandle cap_cond = 0;
+  bool cap_cond_on = false;
   cudaStream_t cap_stream = nullptr;
   bool use_graphs = true;
   xm::DBuf<double> sym_part;       // per-unit row / column partials of the symmetric SpMM

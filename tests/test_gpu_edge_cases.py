@@ -110,3 +110,62 @@ def test_duplicates_keep_first(xm):
         st = ctx.stats()
     assert st["n_dup"] == len(dup)
     assert rel(Qg, dm.Q) <= 1e-10 and rel(dm.Q, dm0.Q) <= 1e-12
+
+
+# ---------------------------------------------------------------- matrix-free (NEXT-1)
+def _products(ctx, n, rs=(1, 3, 4, 5, 7)):
+    rng = np.random.default_rng(17)
+    return {r: (V := rng.standard_normal((n, r)), ctx.spmm(V)) for r in rs}
+
+
+@pytest.mark.parametrize("case", ["N1", "N2", "singleton", "duplicates"])
+def test_implicit_edge_cases(xm, case):
+    """The same degenerate inputs through the matrix-free products
+    (xm_options.implicit_q): every product Q·V ≤ 1e-12·‖Q‖‖V‖ against the
+    oracle's dense Q (r up to 7: the lower-triangle K̄⁻¹ stream and the row
+    GEMV), and the solve certifies at the oracle's optimum (N = 1: Q = 0,
+    Y = I; N = 2: the tight Umeyama case)."""
+    if case == "N1":
+        sc = make_scene(1, 7, "unordered", seed=0, vis_prob=1.0)
+        fr, lm, pts, w, N, M = sc.frame, sc.landmark, sc.pts, sc.w, sc.N, sc.M
+    elif case == "N2":
+        sc = make_scene(2, 40, "unordered", seed=1, vis_prob=0.9, sigma_d=0.05, sigma_u=0.01,
+                        weights="uniform")
+        fr, lm, pts, w, N, M = sc.frame, sc.landmark, sc.pts, sc.w, sc.N, sc.M
+    elif case == "singleton":
+        base = make_scene(40, 900, "loop", seed=4, window=6, sigma_d=0.02, sigma_u=1e-3)
+        rng = np.random.default_rng(9)
+        extra = 50
+        src = rng.integers(0, len(base.frame), extra)
+        fr = np.concatenate([base.frame, rng.integers(0, base.N, extra)])
+        lm = np.concatenate([base.landmark, base.M + np.arange(extra)])
+        pts = np.concatenate([base.pts, base.pts[src]])
+        w = np.concatenate([base.w, base.w[src]])
+        N, M = base.N, base.M + extra
+    else:
+        sc = make_scene(12, 300, "unordered", seed=2, vis_prob=0.5)
+        dup = np.arange(0, len(sc.frame), 7)
+        fr = np.concatenate([sc.frame, sc.frame[dup]])
+        lm = np.concatenate([sc.landmark, sc.landmark[dup]])
+        pts = np.concatenate([sc.pts, sc.pts[dup] * 1.5])
+        w = np.concatenate([sc.w, sc.w[dup]])
+        N, M = sc.N, sc.M
+    dm = xo.build_Q(N, M, fr, lm, pts, w)
+    st = None
+    if N > 1:  # the implicit mode's tolerance scale: the shared Hutchinson estimate (C24)
+        iq = xo.ImplicitQ(N, M, fr, lm, pts, w)
+        st = xo.staircase(dm, normQ=xo.hutchinson_normF(iq.apply, dm.n))
+    with xm.Context(implicit_q=1) as ctx:
+        ctx.build_Q(N, M, fr, lm, pts, w)
+        prods = _products(ctx, 3 * N)
+        status, info = ctx.solve()
+        cert = ctx.certify()
+    scale = max(dm.normF, 1e-300)
+    for r, (V, out) in prods.items():
+        assert np.linalg.norm(out - dm.Q @ V) <= 1e-12 * scale * np.linalg.norm(V), (case, r)
+    assert status == 0 and info["certified"] == 1
+    if N == 1:
+        assert abs(info["f"]) <= 1e-13 and abs(cert["lambda_min"]) <= 1e-12
+    else:
+        assert abs(info["f"] - st.f) <= 1e-8 * (1.0 + abs(st.f))
+        assert cert["eta"] <= 1e-6
