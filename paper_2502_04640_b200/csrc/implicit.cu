@@ -341,129 +341,6 @@ __global__ void k_imp_layout(int64_t E, const int32_t* __restrict__ fr_edge,
   F_wz[q] = w * e_pts[3 * e + 2];
 }
 
-// 32-B measurement records {w·ũ_x, w·ũ_y, w·ũ_z, index bits} in landmark order
-// (index = frame) and in frame order (index = landmark): one sector per record
-__global__ void k_imp_records(int64_t E, const int32_t* __restrict__ fr_edge,
-                              const int32_t* __restrict__ e_fr, const int32_t* __restrict__ e_lm,
-                              const double* __restrict__ e_pts, const double* __restrict__ e_w,
-                              double4* __restrict__ L_rec, double4* __restrict__ F_rec) {
-  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= E) return;
-  {
-    const double w = e_w[q];
-    L_rec[q] = make_double4(w * e_pts[3 * q], w * e_pts[3 * q + 1], w * e_pts[3 * q + 2],
-                            __longlong_as_double((long long)e_fr[q]));
-  }
-  const int e = fr_edge[q];
-  const double w = e_w[e];
-  F_rec[q] = make_double4(w * e_pts[3 * e], w * e_pts[3 * e + 1], w * e_pts[3 * e + 2],
-                          __longlong_as_double((long long)e_lm[e]));
-}
-
-// ROW-OWNER landmark mean (r ≤ 10): a group of 3r lanes per measurement, lane
-// x = a·r + j owning V element (a, j), so the whole gathered row V_i (3r
-// contiguous doubles) is ONE access per group, and each lane streams only its
-// coefficient (w·ũ)_a and the frame id from the measurement's 32-B record.
-template <int R>
-__global__ void __launch_bounds__(kIT) k_imp_lm_mean_ro(int M, const int32_t* __restrict__ lm_off,
-                                                        const double4* __restrict__ L_rec,
-                                                        const double* __restrict__ W,
-                                                        const double* __restrict__ V,
-                                                        double* __restrict__ m,
-                                                        const int* __restrict__ stop,
-                                                        int* __restrict__ exec) {
-  if (stop && *stop) return;
-  if (exec && blockIdx.x == 0 && threadIdx.x == 0) *exec = 1;
-  constexpr int GW = 3 * R, NG = (32 / GW) > 0 ? 32 / GW : 1;  // r ≤ 10 only
-  const int k = blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (k >= M) return;
-  const int g = lane / GW, x = lane - g * GW, a = x / R;
-  const bool act = g < NG;
-  const int xa = act ? a : 0;
-  double acc = 0.0;
-  const int lo = lm_off[k], hi = lm_off[k + 1];
-  for (int base = lo; base < hi; base += NG * kU) {
-    long long ii[kU];
-    double cf[kU];
-#pragma unroll
-    for (int q = 0; q < kU; ++q) {
-      const int e0 = base + q * NG + g;
-      const int e = min(e0, hi - 1);
-      const double* rec = reinterpret_cast<const double*>(L_rec + e);
-      cf[q] = ((act && e0 < hi) ? 1.0 : 0.0) * __ldcs(rec + xa);
-      ii[q] = __double_as_longlong(__ldcs(rec + 3));
-    }
-#pragma unroll
-    for (int q = 0; q < kU; ++q) acc = fma(cf[q], V[(int64_t)3 * ii[q] * R + (act ? x : 0)], acc);
-  }
-  // sum over a (lanes x, x + R, x + 2R of a group), then over the groups
-  const double a1 = __shfl_down_sync(0xffffffffu, acc, R);
-  const double a2 = __shfl_down_sync(0xffffffffu, acc, 2 * R);
-  double v = (acc + a1) + a2;  // valid at a = 0 lanes
-#pragma unroll
-  for (int s = 1; s < NG; s <<= 1) {
-    const double o = __shfl_down_sync(0xffffffffu, v, s * GW);
-    if ((g % (2 * s)) == 0 && g + s < NG) v += o;
-  }
-  if (lane < R) {
-    const double wk = W[k], inv = wk > 0.0 ? 1.0 / wk : 0.0;
-    m[(int64_t)k * R + lane] = v * inv;
-  }
-}
-
-// COLUMN-OWNER frame output from the 32-B records (A/B variant, XM_IMP_FRCO=1)
-template <int R>
-__global__ void __launch_bounds__(kIT) k_imp_fr_out_co(int N, const int32_t* __restrict__ fr_off,
-                                                       const double4* __restrict__ F_rec,
-                                                       const double* __restrict__ cfr,
-                                                       const double* __restrict__ Afr,
-                                                       const double* __restrict__ V,
-                                                       const double* __restrict__ tb,
-                                                       const double* __restrict__ p,
-                                                       double* __restrict__ out,
-                                                       const int* __restrict__ stop) {
-  if (stop && *stop) return;
-  constexpr int NG = Grp<R>::NG;
-  const int i = blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (i >= N) return;
-  const int g = lane / R, j = lane - g * R;
-  const bool act = g < NG;
-  double acc[3] = {0.0, 0.0, 0.0};
-  const int lo = fr_off[i], hi = fr_off[i + 1];
-  for (int base = lo; base < hi; base += NG * kU) {
-    double2 r0[kU], r1[kU];
-    double okw[kU];
-#pragma unroll
-    for (int q = 0; q < kU; ++q) {
-      const int e0 = base + q * NG + g;
-      const int e = min(e0, hi - 1);
-      const double2* rec = reinterpret_cast<const double2*>(F_rec + e);
-      r0[q] = __ldcs(rec);
-      r1[q] = __ldcs(rec + 1);
-      okw[q] = (act && e0 < hi) ? 1.0 : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < kU; ++q) {
-      const double pc = okw[q] * p[(int64_t)__double_as_longlong(r1[q].y) * R + j];
-      acc[0] = fma(r0[q].x, pc, acc[0]);
-      acc[1] = fma(r0[q].y, pc, acc[1]);
-      acc[2] = fma(r1[q].x, pc, acc[2]);
-    }
-  }
-  group_sum<R, 3>(acc, g);
-  if (lane < R) {
-    const double* Ai = Afr + 6 * (int64_t)i;  // xx yy zz xy xz yz
-    const double* vi = V + (int64_t)3 * i * R + lane;
-    const double v0 = vi[0], v1 = vi[R], v2 = vi[2 * R];
-    const double tbi = (i > 0) ? tb[(int64_t)i * R + lane] : 0.0;  // t_0 = 0 (anchor)
-    const double* ci = cfr + 3 * (int64_t)i;
-    double* o = out + (int64_t)3 * i * R + lane;
-    o[0] = fma(-ci[0], tbi, fma(Ai[0], v0, fma(Ai[3], v1, Ai[4] * v2))) - acc[0];
-    o[R] = fma(-ci[1], tbi, fma(Ai[3], v0, fma(Ai[1], v1, Ai[5] * v2))) - acc[1];
-    o[2 * R] = fma(-ci[2], tbi, fma(Ai[4], v0, fma(Ai[5], v1, Ai[2] * v2))) - acc[2];
-  }
-}
-
 // Per-frame moments c_i = Σ_{e∈i} w_e ũ_e and A_i = Σ_{e∈i} w_e ũ_e ũ_eᵀ
 // (xx yy zz xy xz yz); warp per frame, fixed order
 __global__ void __launch_bounds__(kIT) k_imp_frame_moments(int N, const int32_t* __restrict__ fr_off,
@@ -551,10 +428,6 @@ void implicit_prepare(xm_ctx* c) {
                                                          P, P + E, P + 2 * E, c->imp_lm.p, c->imp_w.p,
                                                          P + 3 * E, P + 4 * E, P + 5 * E);
   imp_dbg(c, "layout");
-  c->imp_rec.alloc(8 * E);            // L_rec, F_rec (E × 4 doubles each)
-  k_imp_records<<<ceil_div(E, 256), 256, 0, c->stream>>>(E, c->fr_edge.p, c->e_fr.p, c->e_lm.p, c->e_pts.p,
-                                                          c->e_w.p, reinterpret_cast<double4*>(c->imp_rec.p),
-                                                          reinterpret_cast<double4*>(c->imp_rec.p + 4 * E));
   k_imp_frame_moments<<<ceil_div(N, kIT / 32), kIT, 0, c->stream>>>(N, c->fr_off.p, c->fr_edge.p, c->e_pts.p,
                                                                     c->e_w.p, c->imp_mom.p,
                                                                     c->imp_mom.p + 3 * (size_t)N);
@@ -622,18 +495,8 @@ void implicit_product(xm_ctx* c, const double* V, int r, double* out, const int*
   const double* cfr = c->imp_mom.p;
   const double* Afr = c->imp_mom.p + 3 * (size_t)N;
   imp_dbg(c, "entry");
-  static const bool lm_ro = std::getenv("XM_IMP_LMRO") != nullptr;
-  static const bool fr_co = std::getenv("XM_IMP_FRCO") != nullptr;
-  const double4* L_rec = reinterpret_cast<const double4*>(c->imp_rec.p);
-  const double4* F_rec = reinterpret_cast<const double4*>(c->imp_rec.p + 4 * E);
-  if (lm_ro && r <= 10) {
-    XM_IMP_DISPATCH(r, (k_imp_lm_mean_ro<R><<<ceil_div(M, kIT / 32), kIT, 0, c->stream>>>(
-                           M, c->lm_off.p, L_rec, c->W.p, V, m.p, stop, exec)));
-  } else {
-    XM_IMP_DISPATCH(r, (k_imp_lm_mean<R><<<ceil_div(M, kIT / 32), kIT, 0, c->stream>>>(
-                           M, c->lm_off.p, c->e_fr.p, P, P + E, P + 2 * E, c->W.p, V, m.p, stop, exec)));
-  }
-  
+  XM_IMP_DISPATCH(r, (k_imp_lm_mean<R><<<ceil_div(M, kIT / 32), kIT, 0, c->stream>>>(
+                         M, c->lm_off.p, c->e_fr.p, P, P + E, P + 2 * E, c->W.p, V, m.p, stop, exec)));
   imp_dbg(c, "lm_mean");
   if (N > 1)
     XM_IMP_DISPATCH(r, (k_imp_fr_b<R><<<ceil_div(N - 1, kIT / 32), kIT, 0, c->stream>>>(
@@ -645,15 +508,9 @@ void implicit_product(xm_ctx* c, const double* V, int r, double* out, const int*
   XM_IMP_DISPATCH(r, (k_imp_lm_p<R><<<ceil_div(M, kIT / 32), kIT, 0, c->stream>>>(M, c->lm_off.p, c->e_fr.p, c->e_w.p, c->W.p,
                                                                c->imp_tb.p, m.p, p.p, stop)));
   imp_dbg(c, "lm_p");
-  if (fr_co) {
-    XM_IMP_DISPATCH(r, (k_imp_fr_out_co<R><<<ceil_div(N, kIT / 32), kIT, 0, c->stream>>>(
-                           N, c->fr_off.p, F_rec, cfr, Afr, V, c->imp_tb.p, p.p, out, stop)));
-  } else {
-  XM_IMP_DISPATCH(r, (k_imp_fr_out<R><<<ceil_div(N, kIT / 32), kIT, 0, c->stream>>>(N, c->fr_off.p, c->imp_lm.p, P + 3 * E,
-                                                                   P + 4 * E, P + 5 * E, cfr, Afr, V,
-                                                                   c->imp_tb.p, p.p, out, stop)));
-    XM_CHECK_LAUNCH();
-  }
+  XM_IMP_DISPATCH(r, (k_imp_fr_out<R><<<ceil_div(N, kIT / 32), kIT, 0, c->stream>>>(
+                         N, c->fr_off.p, c->imp_lm.p, P + 3 * E, P + 4 * E, P + 5 * E, cfr, Afr, V,
+                         c->imp_tb.p, p.p, out, stop)));
   XM_CHECK_LAUNCH();
   imp_dbg(c, "fr_out");
   count_launch(c, N > 1 ? 4 : 3);

@@ -146,7 +146,6 @@ struct xm_ctx {
   xm::DBuf<int32_t> imp_lm;                // frame-sorted landmark ids
   xm::DBuf<double> imp_pts, imp_w, Kinv;   // w·ũ (landmark- and frame-sorted SoA), frame-sorted w
   xm::DBuf<double> imp_mom, imp_tb;        // per-frame c_i, A_i; [0; K̄⁻¹ b]
-  xm::DBuf<double> imp_rec;                // 32-B measurement records (landmark / frame order)
   void* imp_sym_plan = nullptr;            // lower-triangle stream plan of K̄⁻¹
   xm::DBuf<double> imp_sym_part;
   xm::DBuf<double> lam;    // N × 6 (xx, yy, zz, xy, xz, yz)

@@ -1,3 +1,4 @@
+timeout 600 python -m pytest tests/test_gpu_edge_cases.py -q -x 2>&1 | tail -3
 # A/B: record-based pass variants; conditional-graph tCG loop
 for v in "" "XM_IMP_LMRO=1 XM_IMP_FRCO=1"; do
   echo "=== variant [$v]"
