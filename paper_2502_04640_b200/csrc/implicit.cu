@@ -70,7 +70,7 @@ __device__ __forceinline__ void group_sum(double (&v)[K], int g) {
 }
 
 // m_k = Σ_{e∈k} (w_e ũ_e)ᵀ V_{i_e} / W_k          (landmark-sorted, 28 B / measurement)
-template <int R>
+template <int R, int U = kU>
 __global__ void __launch_bounds__(kIT) k_imp_lm_mean(int M, const int32_t* __restrict__ lm_off,
                                                      const int32_t* __restrict__ L_i,
                                                      const double* __restrict__ L_wx,
@@ -90,11 +90,11 @@ __global__ void __launch_bounds__(kIT) k_imp_lm_mean(int M, const int32_t* __res
   const bool act = g < NG;
   double acc[1] = {0.0};
   const int lo = lm_off[k], hi = lm_off[k + 1];
-  for (int base = lo; base < hi; base += NG * kU) {
-    int ii[kU];
-    double a0[kU], a1[kU], a2[kU];
+  for (int base = lo; base < hi; base += NG * U) {
+    int ii[U];
+    double a0[U], a1[U], a2[U];
 #pragma unroll
-    for (int q = 0; q < kU; ++q) {
+    for (int q = 0; q < U; ++q) {
       const int e0 = base + q * NG + g;
       const int e = min(e0, hi - 1);  // clamped: loads unconditional, tail weights zeroed
       const double okw = (act && e0 < hi) ? 1.0 : 0.0;
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kIT) k_imp_lm_mean(int M, const int32_t* __res
       a2[q] = okw * __ldcs(L_wz + e);
     }
 #pragma unroll
-    for (int q = 0; q < kU; ++q) {
+    for (int q = 0; q < U; ++q) {
       const double* vi = V + (int64_t)3 * ii[q] * R + j;
       acc[0] = fma(a0[q], vi[0], fma(a1[q], vi[R], fma(a2[q], vi[2 * R], acc[0])));
     }
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kIT) k_imp_lm_mean(int M, const int32_t* __res
 // b_i = Σ_{e∈i} w_e (z_e − m_k) = c_iᵀ V_i − Σ_{e∈i} w_e m_k  (c_i = Σ_{e∈i} w_e ũ_e),
 // i ≥ 1, written to bs[i − 1] (the K̄ ordering: the anchor row is dropped)
 // (frame-sorted, 12 B / measurement)
-template <int R>
+template <int R, int U = kU>
 __global__ void __launch_bounds__(kIT) k_imp_fr_b(int N, const int32_t* __restrict__ fr_off,
                                                   const int32_t* __restrict__ F_k,
                                                   const double* __restrict__ F_w,
@@ -137,18 +137,18 @@ __global__ void __launch_bounds__(kIT) k_imp_fr_b(int N, const int32_t* __restri
   const bool act = g < NG;
   double acc[1] = {0.0};
   const int lo = fr_off[i], hi = fr_off[i + 1];
-  for (int base = lo; base < hi; base += NG * kU) {
-    int kk[kU];
-    double we[kU];
+  for (int base = lo; base < hi; base += NG * U) {
+    int kk[U];
+    double we[U];
 #pragma unroll
-    for (int q = 0; q < kU; ++q) {
+    for (int q = 0; q < U; ++q) {
       const int e0 = base + q * NG + g;
       const int e = min(e0, hi - 1);
       kk[q] = __ldcs(F_k + e);
       we[q] = ((act && e0 < hi) ? 1.0 : 0.0) * __ldcs(F_w + e);
     }
 #pragma unroll
-    for (int q = 0; q < kU; ++q) acc[0] = fma(we[q], m[(int64_t)kk[q] * R + j], acc[0]);
+    for (int q = 0; q < U; ++q) acc[0] = fma(we[q], m[(int64_t)kk[q] * R + j], acc[0]);
   }
   group_sum<R, 1>(acc, g);
   if (lane < R) {
@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(kIT) k_imp_gemv(int m_, const double* __restri
 
 // p_k = m_k + Σ_{e∈k} w_e t_{i_e} / W_k = m_k − Σ_{e∈k} w_e tb_{i_e} / W_k
 // (landmark-sorted, 12 B / measurement)
-template <int R>
+template <int R, int U = kU>
 __global__ void __launch_bounds__(kIT) k_imp_lm_p(int M, const int32_t* __restrict__ lm_off,
                                                   const int32_t* __restrict__ L_i,
                                                   const double* __restrict__ L_w,
@@ -224,18 +224,18 @@ __global__ void __launch_bounds__(kIT) k_imp_lm_p(int M, const int32_t* __restri
   const bool act = g < NG;
   double acc[1] = {0.0};
   const int lo = lm_off[k], hi = lm_off[k + 1];
-  for (int base = lo; base < hi; base += NG * kU) {
-    int ii[kU];
-    double we[kU];
+  for (int base = lo; base < hi; base += NG * U) {
+    int ii[U];
+    double we[U];
 #pragma unroll
-    for (int q = 0; q < kU; ++q) {
+    for (int q = 0; q < U; ++q) {
       const int e0 = base + q * NG + g;
       const int e = min(e0, hi - 1);
       ii[q] = __ldcs(L_i + e);
       we[q] = ((act && e0 < hi) ? 1.0 : 0.0) * __ldcs(L_w + e);
     }
 #pragma unroll
-    for (int q = 0; q < kU; ++q) {
+    for (int q = 0; q < U; ++q) {
       const double wq = (ii[q] != 0) ? we[q] : 0.0;  // t_0 = 0 (anchor)
       acc[0] = fma(wq, tb[(int64_t)ii[q] * R + j], acc[0]);
     }
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(kIT) k_imp_lm_p(int M, const int32_t* __restri
 
 // (QV)_i = Σ_{e∈i} w_e ũ_e (z_e + t_i − p_k)ᵀ = A_i V_i + c_i t_iᵀ − Σ_{e∈i} (w_e ũ_e) p_kᵀ
 // (A_i = Σ_{e∈i} w_e ũ_e ũ_eᵀ, t_i = −tb_i; frame-sorted, 28 B / measurement)
-template <int R>
+template <int R, int U = ((R <= 3) ? 4 : 2)>
 __global__ void __launch_bounds__(kIT, (R <= 5) ? 4 : 1) k_imp_fr_out(int N, const int32_t* __restrict__ fr_off,
                                                     const int32_t* __restrict__ F_k,
                                                     const double* __restrict__ F_wx,
@@ -266,16 +266,15 @@ __global__ void __launch_bounds__(kIT, (R <= 5) ? 4 : 1) k_imp_fr_out(int N, con
   if (stop && *stop) return;  // a tCG graph replay past the stop
   const int i = blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (i >= N) return;
-  constexpr int kU = (R <= 3) ? 4 : 2;  // register budget: 3R accumulators (6 CTAs / SM)
   double acc[3 * R];
 #pragma unroll
   for (int q = 0; q < 3 * R; ++q) acc[q] = 0.0;
   const int lo = fr_off[i], hi = fr_off[i + 1];
-  for (int q0 = lo + lane; q0 < hi; q0 += 32 * kU) {
-    int kk[kU];
-    double a0[kU], a1[kU], a2[kU];
+  for (int q0 = lo + lane; q0 < hi; q0 += 32 * U) {
+    int kk[U];
+    double a0[U], a1[U], a2[U];
 #pragma unroll
-    for (int q = 0; q < kU; ++q) {
+    for (int q = 0; q < U; ++q) {
       const int e = min(q0 + 32 * q, hi - 1);
       const double okw = (q0 + 32 * q < hi) ? 1.0 : 0.0;
       kk[q] = __ldcs(F_k + e);
@@ -284,7 +283,7 @@ __global__ void __launch_bounds__(kIT, (R <= 5) ? 4 : 1) k_imp_fr_out(int N, con
       a2[q] = okw * __ldcs(F_wz + e);
     }
 #pragma unroll
-    for (int q = 0; q < kU; ++q) {
+    for (int q = 0; q < U; ++q) {
       const double* pk = p + (int64_t)kk[q] * R;
 #pragma unroll
       for (int c = 0; c < R; ++c) {
@@ -498,8 +497,8 @@ void implicit_product(xm_ctx* c, const double* V, int r, double* out, const int*
   XM_IMP_DISPATCH(r, (k_imp_lm_mean<R><<<ceil_div(M, kIT / 32), kIT, 0, c->stream>>>(
                          M, c->lm_off.p, c->e_fr.p, P, P + E, P + 2 * E, c->W.p, V, m.p, stop, exec)));
   imp_dbg(c, "lm_mean");
-  if (N > 1)
-    XM_IMP_DISPATCH(r, (k_imp_fr_b<R><<<ceil_div(N - 1, kIT / 32), kIT, 0, c->stream>>>(
+  if (N > 1)  // 16 rounds in flight (E: 43 → 36 µs; the other passes measured flat or slower)
+    XM_IMP_DISPATCH(r, (k_imp_fr_b<R, 16><<<ceil_div(N - 1, kIT / 32), kIT, 0, c->stream>>>(
                            N, c->fr_off.p, c->imp_lm.p, c->imp_w.p, cfr, V, m.p, bs.p, stop)));
   XM_CHECK_LAUNCH();
   imp_dbg(c, "fr_b");
@@ -528,7 +527,7 @@ void implicit_translations(xm_ctx* c, const double* Y3, double* t_out) {
   k_imp_lm_mean<3><<<ceil_div(M, kIT / 32), kIT, 0, c->stream>>>(M, c->lm_off.p, c->e_fr.p, P, P + E, P + 2 * E, c->W.p, Y3,
                                               m.p, nullptr, nullptr);
   if (N > 1)
-    k_imp_fr_b<3><<<ceil_div(N - 1, kIT / 32), kIT, 0, c->stream>>>(N, c->fr_off.p, c->imp_lm.p, c->imp_w.p,
+    k_imp_fr_b<3, 16><<<ceil_div(N - 1, kIT / 32), kIT, 0, c->stream>>>(N, c->fr_off.p, c->imp_lm.p, c->imp_w.p,
                                                                     c->imp_mom.p, Y3, m.p, bs.p, nullptr);
   XM_CHECK_LAUNCH();
   kinv_product(c, bs.p, 3, nullptr);
