@@ -54,6 +54,13 @@ template <int R>
 struct Grp {
   static constexpr int NG = 32 / R;  // measurements per warp round
 };
+// row stride of the landmark array p (M × PR): r rounded up to even, so the
+// frame-output pass gathers a landmark's row with 16-B loads (⌈r/2⌉ instead of
+// r scattered accesses per measurement)
+template <int R>
+struct PStride {
+  static constexpr int PR = (R + 1) & ~1;
+};
 
 // sum over the groups of the lanes owning the same column (result in group 0)
 template <int R, int K>
@@ -244,7 +251,8 @@ __global__ void __launch_bounds__(kIT) k_imp_lm_p(int M, const int32_t* __restri
   if (lane < R) {
     const double sum = acc[0];
     const double wk = W[k], inv = wk > 0.0 ? 1.0 / wk : 0.0;
-    p[(int64_t)k * R + lane] = fma(-sum, inv, m[(int64_t)k * R + lane]);
+    p[(int64_t)k * PStride<R>::PR + lane] = fma(-sum, inv, m[(int64_t)k * R + lane]);
+    if (PStride<R>::PR != R && lane == R - 1) p[(int64_t)k * PStride<R>::PR + R] = 0.0;
   }
 }
 
@@ -284,10 +292,18 @@ __global__ void __launch_bounds__(kIT, (R <= 5) ? 4 : 1) k_imp_fr_out(int N, con
     }
 #pragma unroll
     for (int q = 0; q < U; ++q) {
-      const double* pk = p + (int64_t)kk[q] * R;
+      constexpr int PR = PStride<R>::PR;
+      const double2* pk = reinterpret_cast<const double2*>(p + (int64_t)kk[q] * PR);
+      double pv[PR];
+#pragma unroll
+      for (int h = 0; h < PR / 2; ++h) {
+        const double2 t2 = pk[h];
+        pv[2 * h] = t2.x;
+        pv[2 * h + 1] = t2.y;
+      }
 #pragma unroll
       for (int c = 0; c < R; ++c) {
-        const double pc = pk[c];
+        const double pc = pv[c];
         acc[c] = fma(a0[q], pc, acc[c]);
         acc[R + c] = fma(a1[q], pc, acc[R + c]);
         acc[2 * R + c] = fma(a2[q], pc, acc[2 * R + c]);
