@@ -847,6 +847,17 @@ void dense_trsm_lower_left(xm_ctx* c, const double* L, int m, int64_t ldl, const
   }
 }
 
+// out[k][j] = B[k][j] for j < wv, 0 for wv ≤ j < w (k < m): a column slice packed
+// contiguous for the all-gather of the column-sharded TRSM
+__global__ void k_pack_block(int m, int w, int wv, const double* __restrict__ B, int64_t ldb,
+                             double* __restrict__ out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)m * w) return;
+  const int64_t k = t / w;
+  const int j = (int)(t - k * w);
+  out[t] = (j < wv) ? B[k * ldb + j] : 0.0;
+}
+
 // Q[i][j] (j > i) ← Q[j][i]: exact symmetry after a lower-triangle SYRK.
 __global__ void k_mirror(double* Q, int n, int64_t ldq) {
   __shared__ double tile[32][33];
@@ -1178,7 +1189,37 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
     U.alloc((size_t)(N - 1) * c->ldk);
     dense_cholesky(c, c->L.p, N - 1, c->ldk, 1e-12, true, U.p, c->ldk);
     phase("cholesky");
-    dense_trsm_lower_left(c, c->L.p, N - 1, c->ldk, U.p, c->ldk, c->G.p, n, c->ldq);
+    if (c->world == 1) {
+      dense_trsm_lower_left(c, c->L.p, N - 1, c->ldk, U.p, c->ldk, c->G.p, n, c->ldq);
+    } else {
+      // column-sharded TRSM: G = L⁻¹C̄ splits by columns, so rank p solves
+      // columns [p·w, (p+1)·w) (w a multiple of 32) and ONE all-gather of the
+      // packed slices gives every rank all of G (its band rows need G up to
+      // the band end; the last band needs all of it) — 3N³/P flop per rank
+      // instead of 3N³, plus 8(N−1)n bytes over NVLink
+      const int P = c->world, m = N - 1;
+      const int w = round_up(ceil_div(n, P), 32);
+      const int c0 = std::min(n, c->rank * w), c1 = std::min(n, c0 + w);
+      if (c1 > c0)
+        dense_trsm_lower_left(c, c->L.p, m, c->ldk, U.p, c->ldk, c->G.p + c0, c1 - c0, c->ldq);
+      DBuf<double>& sl = scratch_f64(c, "trsm_slice");
+      DBuf<double>& all = scratch_f64(c, "trsm_gather");
+      sl.alloc((size_t)m * w);
+      all.alloc((size_t)P * m * w);
+      k_pack_block<<<ceil_div((int64_t)m * w, 256), 256, 0, c->stream>>>(m, w, c1 - c0, c->G.p + c0, c->ldq,
+                                                                          sl.p);
+      XM_CHECK_LAUNCH();
+      nccl_allgather_f64(c, sl.p, all.p, (size_t)m * w);
+      for (int q = 0; q < P; ++q) {
+        const int q0 = std::min(n, q * w), q1 = std::min(n, q0 + w);
+        if (q == c->rank || q1 <= q0) continue;
+        XM_CUDA(cudaMemcpy2DAsync(c->G.p + q0, c->ldq * sizeof(double), all.p + (size_t)q * m * w,
+                                  (size_t)w * sizeof(double), (size_t)(q1 - q0) * sizeof(double), m,
+                                  cudaMemcpyDeviceToDevice, c->stream));
+      }
+      count_launch(c);
+      all.release();  // 8(N−1)n bytes: not kept past the build
+    }
     phase("trsm");
     const double* Gown = c->G.p + c->row0;  // columns of this rank's rows
     // Q = S − GᵀG: Q[i][j] −= Σ_k G[k][i] G[k][j]

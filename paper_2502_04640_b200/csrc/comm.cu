@@ -163,4 +163,24 @@ void nccl_allreduce_sum(xm_ctx* c, double* buf, size_t count) {
         "ncclAllReduce");
 }
 
+// recv[q·count … (q+1)·count) = rank q's send (count doubles per rank)
+void nccl_allgather_f64(xm_ctx* c, const double* send, double* recv, size_t count) {
+  if (c->world <= 1) {
+    if (recv != send) XM_CUDA(cudaMemcpyAsync(recv, send, count * 8, cudaMemcpyDeviceToDevice, c->stream));
+    return;
+  }
+  if (c->loop) {
+    LoopGroup* g = static_cast<LoopGroup*>(c->loop);
+    XM_CUDA(cudaStreamSynchronize(c->stream));
+    g->ptr[c->rank] = send;
+    g->barrier();
+    for (int q = 0; q < c->world; ++q)
+      XM_CUDA(cudaMemcpy(recv + (size_t)q * count, g->ptr[q], count * 8, cudaMemcpyDefault));
+    g->barrier();
+    return;
+  }
+  check(g_nccl.AllGather(send, recv, count, ncclFloat64, (ncclComm_t)c->nccl_comm, c->stream),
+        "ncclAllGather");
+}
+
 }  // namespace xm

@@ -401,6 +401,7 @@ void nccl_unique_id(void* out128);
 void nccl_init(xm_ctx* c, const void* id);
 void nccl_destroy(xm_ctx* c);
 void nccl_allreduce_sum(xm_ctx* c, double* buf, size_t count);
+void nccl_allgather_f64(xm_ctx* c, const double* send, double* recv, size_t count);
 void sym_plan_destroy(xm_ctx* c);
 void sym_plan_slot_destroy(void*& slot);
 void spmm_sym_matrix(xm_ctx* c, void*& plan_slot, DBuf<double>& part, const double* A, int m,

@@ -6,7 +6,8 @@ xm_shard_rows composed with the symmetric stream: each rank holds the lower
 trapezoid of its band of rows, forms the row parts of its rows and the column
 parts of every row above (a full-length partial), and ONE all-reduce of the
 partials must give Q·V; plus the all-reduce of the ‖Q‖² partials (2× the
-strictly lower entries + the diagonal).  Exits non-zero on any mismatch.
+strictly lower entries + the diagonal), and the column-sharded TRSM's
+all-gather of packed G = L⁻¹C̄ slices.  Exits non-zero on any mismatch.
 """
 import os
 import sys
@@ -73,6 +74,24 @@ def main():
         if N >= 128:  # lower-triangle shares within one 32-frame step of equal
             areas = [s[1] ** 2 - s[0] ** 2 for s in spans]
             assert max(areas) - min(areas) <= 2 * 32 * N + 32 * 32
+        # 4. column-sharded TRSM (assembly.cu, world > 1): rank p solves columns
+        #    [p·w, (p+1)·w) of G = L⁻¹C̄ (w = ⌈n/P⌉ rounded up to 32), packs them
+        #    zero-padded to w columns, and ONE all-gather gives every rank all of G
+        m = N - 1
+        w = -(-(-(-n // world)) // 32) * 32
+        c0, c1 = min(n, rank * w), min(n, rank * w + w)
+        Cbar = dm.C[1:, :]
+        sl = np.zeros((m, w))
+        if c1 > c0:
+            sl[:, : c1 - c0] = np.linalg.solve(np.tril(dm.L), Cbar[:, c0:c1])
+        parts = [torch.zeros(m * w, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(sl.ravel().copy()))
+        G = np.zeros((m, n))
+        for q in range(world):
+            q0, q1 = min(n, q * w), min(n, q * w + w)
+            if q1 > q0:
+                G[:, q0:q1] = parts[q].numpy().reshape(m, w)[:, : q1 - q0]
+        assert np.abs(G - dm.G).max() <= 1e-10 * max(1.0, np.abs(dm.G).max()), ("trsm shard", N)
     dist.barrier()
     dist.destroy_process_group()
     if rank == 0:
