@@ -612,6 +612,19 @@ bool dense_cholesky(xm_ctx* c, double* A, int m, int64_t lda, double rel_tol, bo
     ldu = round_up(std::max(m, 1), 32);
     panel.alloc((size_t)NB * ldu);
   }
+  // Look-ahead: the trailing update of panel k is split into (a) the next
+  // panel's 64 columns (all rows below) on the main stream, and (b) the rest on
+  // a side stream, so the latency-bound factorisation of panel k+1 runs
+  // concurrently with the big update (b) of panel k.  (a) of panel k+1 waits
+  // for (b) of panel k (both write the columns of panel k+2).  Without a U
+  // buffer (the scratch panel is reused every step) the plain order is kept.
+  const bool look = U != nullptr && c->cap_target == nullptr && !std::getenv("XM_NO_CHOL_LOOKAHEAD");
+  if (look && !c->aux_stream) {
+    XM_CUDA(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
+    XM_CUDA(cudaEventCreateWithFlags(&c->ev_la, cudaEventDisableTiming));
+    XM_CUDA(cudaEventCreateWithFlags(&c->ev_lb, cudaEventDisableTiming));
+  }
+  bool pending_b = false;
   for (int kb = 0; kb < m; kb += NB) {
     int nb = std::min(NB, m - kb);
     double* Akk = A + (int64_t)kb * lda + kb;
@@ -623,11 +636,36 @@ bool dense_cholesky(xm_ctx* c, double* A, int m, int64_t lda, double rel_tol, bo
         Up, ldu);
     XM_CHECK_LAUNCH();
     count_launch(c);
-    if (rows > 0) {
-      double* A22 = A + (int64_t)(kb + nb) * lda + (kb + nb);
+    if (rows <= 0) continue;
+    double* A22 = A + (int64_t)(kb + nb) * lda + (kb + nb);
+    if (!look) {
       dgemm_tn(c, true, rows, rows, nb, -1.0, Up, ldu, Up, ldu, 1.0, A22, lda);
+      continue;
+    }
+    const int nb2 = std::min(NB, rows);
+    if (pending_b) XM_CUDA(cudaStreamWaitEvent(c->stream, c->ev_lb, 0));  // (b) of panel k−1
+    // (a) the next panel's columns, every row below (its diagonal block's upper part
+    // is scratch: k_chol_panel reads the lower part, k_chol_diag_back rewrites it)
+    dgemm_tn(c, false, rows, nb2, nb, -1.0, Up, ldu, Up, ldu, 1.0, A22, lda);
+    pending_b = false;
+    if (rows > nb2) {
+      XM_CUDA(cudaEventRecord(c->ev_la, c->stream));
+      XM_CUDA(cudaStreamWaitEvent(c->aux_stream, c->ev_la, 0));
+      cudaStream_t main = c->stream;
+      c->stream = c->aux_stream;  // (b) the rest of the trailing matrix, lower tiles
+      try {
+        dgemm_tn(c, true, rows - nb2, rows - nb2, nb, -1.0, Up + nb2, ldu, Up + nb2, ldu, 1.0,
+                 A22 + (int64_t)nb2 * lda + nb2, lda);
+      } catch (...) {
+        c->stream = main;
+        throw;
+      }
+      c->stream = main;
+      XM_CUDA(cudaEventRecord(c->ev_lb, c->aux_stream));
+      pending_b = true;
     }
   }
+  if (pending_b) XM_CUDA(cudaStreamWaitEvent(c->stream, c->ev_lb, 0));
   k_chol_diag_back<<<ceil_div(m, NB), 256, 0, c->stream>>>(slots.p, A, lda, m);
   XM_CHECK_LAUNCH();
   count_launch(c);

@@ -693,6 +693,9 @@ void xm_destroy(xm_ctx* c) {
     if (e) cudaEventDestroy(e);
   destroy_graphs(c);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
+  if (c->ev_la) cudaEventDestroy(c->ev_la);
+  if (c->ev_lb) cudaEventDestroy(c->ev_lb);
   nccl_destroy(c);
   sym_plan_destroy(c);
   sym_plan_slot_destroy(c->imp_sym_plan);

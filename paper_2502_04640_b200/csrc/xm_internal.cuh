@@ -215,6 +215,9 @@ struct xm_ctx {
   cudaGraphConditionalHandle cap_cond = 0;
   bool cap_cond_on = false;
   cudaStream_t cap_stream = nullptr;
+  // side stream + events of the look-ahead Cholesky (assembly.cu dense_cholesky)
+  cudaStream_t aux_stream = nullptr;
+  cudaEvent_t ev_la = nullptr, ev_lb = nullptr;
   bool use_graphs = true;
   xm::DBuf<double> sym_part;       // per-unit row / column partials of the symmetric SpMM
   // XM_PHASES=1: host wall-clock breakdown of xm_solve (synchronises; diagnostics only)
