@@ -475,6 +475,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
     const double* p = rowpart + (rtile_base(K) * TR + l) * R + cc;
     double acc = 0.0;
     int q = (K >= rt_a && K < rt_b) ? 0 : Jc + 1;  // row parts exist for the band's rows only
+    for (; q + 16 <= Jc + 1; q += 16) {  // 16 loads in flight, summed in order (the
+      // finish is latency-bound: ≈ n/256 partials per element, one element per thread)
+      double v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) v[u] = p[(int64_t)(q + u) * TR * R];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) acc += v[u];
+    }
     for (; q + 4 <= Jc + 1; q += 4) {  // 4 loads in flight, summed in order
       const double a0 = p[(int64_t)q * TR * R], a1 = p[(int64_t)(q + 1) * TR * R];
       const double a2 = p[(int64_t)(q + 2) * TR * R], a3 = p[(int64_t)(q + 3) * TR * R];
