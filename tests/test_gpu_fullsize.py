@@ -286,3 +286,74 @@ def test_E_identical_Q_spmm_and_hvp(xm):
                 ref = xo.project(Ys, 2.0 * QVs - 2.0 * xo.block_apply(Lam, Vs))
                 assert rel(HV[sub], ref) <= 1e-12, rel(HV[sub], ref)
     del Q
+
+
+# ----------------------------------------------------------------------------- matrix-free (NEXT-1)
+# The bench headline at E runs the matrix-free products (bench.py --mode auto);
+# the same full-size checks through them.
+def test_B_implicit_products_and_solve_vs_oracle(xm, B):
+    """B matrix-free: Q·V (r = 1, 3, 4, 7) against the oracle's dense Q, and the
+    whole solve → certificate → recovery against the oracle's staircase run
+    with the same tolerance scale (the shared 16-probe estimate, reading C24)."""
+    sc, dm = B
+    iq = xo.ImplicitQ(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+    est = xo.hutchinson_normF(iq.apply, dm.n)
+    st = xo.staircase(dm, normQ=est)
+    sol = xo.round_recover(dm, st.Y)
+    with xm.Context(implicit_q=1) as ctx:
+        ctx.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+        for r in (1, 3, 4, 7):
+            V = random_tangent_ambient(sc.N, r, 30 + r)
+            assert rel(ctx.spmm(V), dm.Q @ V) <= 1e-10, r
+        status, info = ctx.solve()
+        cert = ctx.certify()
+        gsol = ctx.round_recover()
+        Yg = ctx.get_factor()
+    assert abs(info["normQ"] - est) <= 1e-10 * est
+    assert status == 0 and info["certified"] == 1 and st.certified
+    assert abs(info["f"] - st.f) <= 1e-8 * (1.0 + abs(st.f))
+    Xo = st.Y @ st.Y.T
+    assert np.linalg.norm(Yg @ Yg.T - Xo) <= 1e-6 * np.linalg.norm(Xo)
+    assert cert["eta"] <= 1e-6
+    np.testing.assert_allclose(gsol["s"], sol.s, rtol=1e-6, atol=1e-9)
+    np.testing.assert_allclose(gsol["R"], sol.R, atol=1e-6)
+    np.testing.assert_allclose(gsol["t"], sol.t, atol=1e-6 * max(1.0, np.abs(sol.t).max()))
+
+
+def test_E_implicit_noisy_sampled_rows_certified_and_optimal(xm, E_noisy):
+    """E with noise through the matrix-free products (the headline mode): sampled
+    rows of Q·V against the oracle's row-wise Schur complement (reading C13
+    tolerance), a certified zero duality gap, Eq. (3) at the recovered
+    (s, R, t, p) = ρ̂, and first-order optimality of the recovered t, p."""
+    sc = E_noisy
+    rows = _sample_rows(sc.N, 12, 5)
+    info_q = {}
+    QI = xo.q_rows(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w, rows, info=info_q)
+    tol = max(1e-10, 8 * np.finfo(float).eps * info_q["kappa_K"] * info_q["S_I_norm"]
+              / np.linalg.norm(QI))
+    with xm.Context(implicit_q=1) as ctx:
+        ctx.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+        for r in (1, 3, 4):
+            V = random_tangent_ambient(sc.N, r, 41 + r)
+            assert rel(ctx.spmm(V)[rows], QI @ V) <= tol, r
+        status, info = ctx.solve()
+        cert = ctx.certify()
+        g = ctx.round_recover()
+    assert status == 0 and info["certified"] == 1
+    assert cert["eta"] <= 1e-6
+    s, R, t, p = g["s"], g["R"], g["t"], g["p"]
+    assert np.abs(np.einsum("iab,icb->iac", R, R) - np.eye(3)).max() <= 1e-12
+    assert np.all(np.linalg.det(R) > 0) and s[0] == 1.0
+    fr, lm, w = sc.frame.astype(np.int64), sc.landmark.astype(np.int64), sc.w
+    x = s[fr, None] * np.einsum("eab,eb->ea", R[fr], sc.pts) + t[fr]
+    d = x - p[lm]
+    rho_edge = float(np.sum(w * np.sum(d * d, axis=1)))
+    assert abs(rho_edge - cert["rho_hat"]) <= 1e-8 * (1.0 + abs(rho_edge))
+    res = w[:, None] * d
+    gp = np.zeros((sc.M, 3))
+    np.add.at(gp, lm, res)
+    gt = np.zeros((sc.N, 3))
+    np.add.at(gt, fr, res)
+    scale = np.abs(res).sum() + 1e-300
+    assert np.abs(gp).max() <= 1e-9 * scale
+    assert np.abs(gt[1:]).max() <= 1e-9 * scale
