@@ -264,14 +264,16 @@ typedef struct {
 } xm_batch_result;
 /* B independent small instances, each the whole Algorithm 1 from
  * its own start — Thm 3's random-initialisation trials and App. G's
- * noise sweeps — in ONE launch: one CTA per instance, Q and all
- * vectors in shared memory.  Q: B matrices n×n
+ * noise sweeps — in ONE launch: one CTA per instance (SURVEY
+ * §8(f) NEXT-4); N ≤ 24: Q and all vectors in shared memory; 24 < N ≤ 400 (e.g.
+ * the paper's BAL-93 trials): Q read from global memory (L2-resident when
+ * shared), vectors in a per-instance device scratch.  Q: B matrices n×n
  * (row-major, n = 3N, caller memory, host or device), instance b at
  * Q + b·q_stride (q_stride = 0: one Q shared by every instance); Y0: B × n × r0
  * feasible starts; Y_out: B × n × 8 (row-major, stride 8, columns ≥ r zero);
  * res: B results.  Options (tolerances, TR / tCG constants, rank_cap ≤ 8,
  * seed) from the context; no App. D term.  Needs a context (for its device and
- * stream) but no xm_build_Q.  XM_EINVAL unless 1 ≤ N ≤ 24, 3 ≤ r0 ≤
+ * stream) but no xm_build_Q.  XM_EINVAL unless 1 ≤ N ≤ 400, 3 ≤ r0 ≤
  * min(rank_cap, 8), B ≥ 1.  Per-instance failures are reported in res, not as
  * the call's status. */
 xm_status xm_solve_batch(xm_ctx* ctx, int32_t B, int32_t N, const double* Q, int64_t q_stride,

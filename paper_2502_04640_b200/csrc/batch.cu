@@ -23,8 +23,8 @@ namespace xm {
 namespace {
 constexpr int kBT = 256;   // threads per instance
 constexpr int kBR = 8;     // column stride (max rank)
-constexpr int kBNmax = 24; // frames per instance
-constexpr int kBn = 3 * kBNmax;
+constexpr int kBNmax = 24; // frames per instance with everything in shared memory
+constexpr int kBNmaxGM = 400;  // frames per instance in the global-memory layout
 
 struct BatchArgs {
   int B, N, n, r0, rcap;
@@ -36,6 +36,8 @@ struct BatchArgs {
   double grad_tol, delta0_coef, delta_max_mult, rho_prime, kappa, theta, eig_tol, cert_tol, c_floor;
   int max_inner, max_outer, refresh_every, lanczos_max;
   uint64_t seed;
+  double* scratch;         // GM layout: per-instance vectors / Lanczos basis in global memory
+  int64_t scratch_stride;  // doubles per instance
 };
 
 struct Sm {
@@ -67,14 +69,19 @@ __device__ double bdot(const double* a, const double* b, int len, double* red) {
   for (int x = threadIdx.x; x < len; x += kBT) s = fma(a[x], b[x], s);
   return bsum(s, red);
 }
-// out (n × 8) = Q (n × n) · X (n × 8)
-__device__ void bmatvec(const double* Q, int n, const double* X, double* out) {
-  for (int e = threadIdx.x; e < n * kBR; e += kBT) {
-    const int row = e / kBR, c = e % kBR;
-    const double* q = Q + row * n;
+// out (n × 8) = Q (n × n) · X (n × 8) for the rc leading columns (the others of X
+// are zero, so are those of out)
+__device__ void bmatvec(const double* Q, int n, const double* X, double* out, int rc) {
+  for (int e = threadIdx.x; e < n * rc; e += kBT) {
+    const int row = e / rc, c = e - row * rc;
+    const double* q = Q + (int64_t)row * n;
     double s = 0.0;
     for (int k = 0; k < n; ++k) s = fma(q[k], X[k * kBR + c], s);
-    out[e] = s;
+    out[row * kBR + c] = s;
+  }
+  for (int e = threadIdx.x; e < n * (kBR - rc); e += kBT) {
+    const int row = e / (kBR - rc), c = rc + (e - row * (kBR - rc));
+    out[row * kBR + c] = 0.0;
   }
   __syncthreads();
 }
@@ -138,8 +145,8 @@ __device__ void bproject(const double* Y, double* W, int N) {
   __syncthreads();
 }
 // Hess[V] = P(2QV − 2ΛV) (reading C5) → out
-__device__ void bhess(const Sm& s, const double* V, double* out, int n, int N) {
-  bmatvec(s.Q, n, V, s.TMP);
+__device__ void bhess(const Sm& s, const double* V, double* out, int n, int N, int rc) {
+  bmatvec(s.Q, n, V, s.TMP, rc);
   bsublam(s.TMP, s.LAM, V, 2.0, 2.0, out, n);
   bproject(s.Y, out, N);
 }
@@ -363,7 +370,7 @@ __device__ int blanczos(const Sm& s, const BatchArgs& a, double tol, double* lam
 }
 
 // one tCG solve (O5): ETA, HETA; returns stop (1 negcurv, 2 exceeded, 3 converged, 4 maxinner)
-__device__ int btcg(const Sm& s, const BatchArgs& a, double Delta, int* nh) {
+__device__ int btcg(const Sm& s, const BatchArgs& a, double Delta, int* nh, int rc) {
   const int n = a.n, len = n * kBR;
   for (int e = threadIdx.x; e < len; e += kBT) {
     s.ETA[e] = 0.0;
@@ -377,7 +384,7 @@ __device__ int btcg(const Sm& s, const BatchArgs& a, double Delta, int* nh) {
   double e_Pe = 0.0, e_Pd = 0.0, d_Pd = z;
   int stop = 4;
   for (int j = 0; j < a.max_inner; ++j) {
-    bhess(s, s.DEL, s.HDEL, n, a.N);
+    bhess(s, s.DEL, s.HDEL, n, a.N, rc);
     ++*nh;
     const double dHd = bdot(s.DEL, s.HDEL, len, s.red);
     const double alpha = dHd != 0.0 ? z / dHd : INFINITY;
@@ -415,29 +422,42 @@ __device__ int btcg(const Sm& s, const BatchArgs& a, double Delta, int* nh) {
   return stop;
 }
 
+// GM = false: Q, the 12 vectors and the Lanczos basis in shared memory (n ≤ 72).
+// GM = true (n > 72, e.g. Thm 3's BAL-93 trials, n = 279): Q is read from
+// global memory (L2-resident: one shared Q serves every trial), the vectors and
+// the basis live in a per-instance global scratch (L1 / L2); only the reduction
+// buffer stays in shared memory.  Same arithmetic, same order.
+template <bool GM>
 __global__ void __launch_bounds__(kBT, 1) k_batch_staircase(BatchArgs a) {
   extern __shared__ __align__(16) double smem[];
   const int n = a.n, N = a.N, len = n * kBR;
+  const int inst = blockIdx.x;
+  const double* Qg = a.Q + (int64_t)inst * a.qstride;
   Sm s;
-  double* p = smem;
-  s.Q = p; p += n * n;
+  double* p = GM ? a.scratch + (int64_t)inst * a.scratch_stride : smem;
+  if (GM) {
+    s.Q = const_cast<double*>(Qg);
+  } else {
+    s.Q = p;
+    p += n * n;
+  }
   double** vecs[12] = {&s.Y, &s.QY, &s.G, &s.ETA, &s.HETA, &s.RR, &s.DEL, &s.HDEL, &s.TMP, &s.YN, &s.DD, &s.QD};
   for (int q = 0; q < 12; ++q) {
     *vecs[q] = p;
     p += len;
   }
   s.LAM = p; p += 6 * N;
-  s.V = p; p += n * n;
+  s.V = p; p += (int64_t)min(a.lanczos_max, n) * n;
   s.w = p; p += n;
   s.al = p; p += n;
   s.be = p; p += n;
   s.sv = p; p += n;
+  if (GM) p = smem;
   s.red = p; p += kBT;
   s.scal = p; p += 8;
 
-  const int inst = blockIdx.x;
-  const double* Qg = a.Q + (int64_t)inst * a.qstride;
-  for (int e = threadIdx.x; e < n * n; e += kBT) s.Q[e] = Qg[e];
+  if (!GM)
+    for (int e = threadIdx.x; e < n * n; e += kBT) s.Q[e] = Qg[e];
   for (int e = threadIdx.x; e < len; e += kBT) {
     const int row = e / kBR, c = e % kBR;
     s.Y[e] = (c < a.r0) ? a.Y0[((int64_t)inst * n + row) * a.r0 + c] : 0.0;
@@ -455,7 +475,7 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_staircase(BatchArgs a) {
     // ---------------------------------------------------------------- RTR (O4)
     const double Delta0 = a.delta0_coef * sqrt(3.0 * N), Dbar = a.delta_max_mult * Delta0;
     double Delta = Delta0;
-    bmatvec(s.Q, n, s.Y, s.QY);
+    bmatvec(s.Q, n, s.Y, s.QY, r);
     bmult(s.Y, s.QY, s.LAM, N);
     bsublam(s.QY, s.LAM, s.Y, 2.0, 2.0, s.G, n);
     f = bdot(s.Y, s.QY, len, s.red);
@@ -468,12 +488,12 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_staircase(BatchArgs a) {
         break;
       }
       if (it == a.max_outer) break;
-      const int stop = btcg(s, a, Delta, &hvps);
+      const int stop = btcg(s, a, Delta, &hvps, r);
       if (bretract(s.Y, s.ETA, 1.0, a.c_floor, s.YN, s.DD, N, s.red)) {
         status = XM_ERETRACT;
         break;
       }
-      bmatvec(s.Q, n, s.DD, s.QD);
+      bmatvec(s.Q, n, s.DD, s.QD, r);
       const double df = 2.0 * bdot(s.QY, s.DD, len, s.red) + bdot(s.DD, s.QD, len, s.red);
       const double mdec = -bdot(s.G, s.ETA, len, s.red) - 0.5 * bdot(s.ETA, s.HETA, len, s.red);
       const double reg = fmax(1.0, fabs(f)) * eps * 1e3;
@@ -485,7 +505,7 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_staircase(BatchArgs a) {
         for (int e = threadIdx.x; e < len; e += kBT) s.Y[e] = s.YN[e];
         __syncthreads();
         if (a.refresh_every > 0 && accepts % a.refresh_every == 0) {
-          bmatvec(s.Q, n, s.Y, s.QY);
+          bmatvec(s.Q, n, s.Y, s.QY, r);
         } else {
           for (int e = threadIdx.x; e < len; e += kBT) s.QY[e] += s.QD[e];
           __syncthreads();
@@ -498,7 +518,7 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_staircase(BatchArgs a) {
     outer_tot += it;
     if (status) break;
     // fresh QY, Λ, gradient before the certificate
-    bmatvec(s.Q, n, s.Y, s.QY);
+    bmatvec(s.Q, n, s.Y, s.QY, r);
     bmult(s.Y, s.QY, s.LAM, N);
     bsublam(s.QY, s.LAM, s.Y, 2.0, 2.0, s.G, n);
     f = bdot(s.Y, s.QY, len, s.red);
@@ -522,7 +542,7 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_staircase(BatchArgs a) {
     int done = 0;
     for (int h = 0; h <= 60; ++h) {
       bretract(s.Y, s.ETA, alpha, a.c_floor, s.YN, s.DD, N, s.red);
-      bmatvec(s.Q, n, s.DD, s.QD);
+      bmatvec(s.Q, n, s.DD, s.QD, r + 1);  // the escape fills column r
       const double df = 2.0 * bdot(s.QY, s.DD, len, s.red) + bdot(s.DD, s.QD, len, s.red);
       if (df < 0.0) {
         for (int e = threadIdx.x; e < len; e += kBT) s.Y[e] = s.YN[e];
@@ -556,14 +576,21 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_staircase(BatchArgs a) {
 }
 }  // namespace
 
-size_t batch_smem_bytes(int N) {
+// doubles of one instance's vectors, multipliers and Lanczos basis
+static size_t batch_vec_doubles(int N, int lanczos_max) {
   const int n = 3 * N;
-  return sizeof(double) * ((size_t)n * n * 2 + 12 * (size_t)n * kBR + 6 * N + 4 * n + kBT + 8);
+  return 12 * (size_t)n * kBR + 6 * (size_t)N + (size_t)std::min(lanczos_max, n) * n + 4 * (size_t)n;
+}
+size_t batch_smem_bytes(int N, int lanczos_max) {
+  const int n = 3 * N;
+  if (N > kBNmax) return sizeof(double) * (kBT + 8);  // GM layout
+  return sizeof(double) * ((size_t)n * n + batch_vec_doubles(N, lanczos_max) + kBT + 8);
 }
 
 void batch_staircase(xm_ctx* c, int B, int N, const double* Q_dev, int64_t qstride,
                      const double* Y0_dev, int r0, double* Yout_dev, xm_batch_result* res_dev) {
-  if (N < 1 || N > kBNmax) throw Error(XM_EINVAL, "batched solve: 1 ≤ N ≤ 24 frames per instance");
+  if (N < 1 || N > kBNmaxGM)
+    throw Error(XM_EINVAL, "batched solve: 1 ≤ N ≤ 400 frames per instance");
   const int rcap = std::min(c->opt.rank_cap, kBR);
   if (r0 < 3 || r0 > rcap) throw Error(XM_EINVAL, "batched solve: 3 ≤ r0 ≤ min(rank_cap, 8)");
   BatchArgs a{};
@@ -592,9 +619,17 @@ void batch_staircase(xm_ctx* c, int B, int N, const double* Q_dev, int64_t qstri
   a.refresh_every = o.refresh_every;
   a.lanczos_max = o.lanczos_max;
   a.seed = o.seed;
-  const size_t smem = batch_smem_bytes(N);
-  ensure_smem_attr((const void*)k_batch_staircase, smem);
-  k_batch_staircase<<<B, kBT, smem, c->stream>>>(a);
+  const size_t smem = batch_smem_bytes(N, a.lanczos_max);
+  if (N <= kBNmax) {
+    ensure_smem_attr((const void*)k_batch_staircase<false>, smem);
+    k_batch_staircase<false><<<B, kBT, smem, c->stream>>>(a);
+  } else {
+    a.scratch_stride = (int64_t)round_up((int64_t)batch_vec_doubles(N, a.lanczos_max), 32);
+    DBuf<double>& sc = scratch_f64(c, "batch_scratch");
+    sc.alloc((size_t)B * a.scratch_stride);
+    a.scratch = sc.p;
+    k_batch_staircase<true><<<B, kBT, smem, c->stream>>>(a);
+  }
   XM_CHECK_LAUNCH();
   count_launch(c);
 }

@@ -368,7 +368,7 @@ void axpy(xm_ctx* c, int64_t len, double a, const double* x, double* y);
 void pad_column(xm_ctx* c, int r, const double* Y, double* Yz, const double* v, double* Dz);
 void zmul(xm_ctx* c, const double* x, const double* Zx_q, double* out);  // Zx = Qx − Λx (r = 1)
 // NEXT-4 (batch.cu)
-size_t batch_smem_bytes(int N);
+size_t batch_smem_bytes(int N, int lanczos_max);
 void batch_staircase(xm_ctx* c, int B, int N, const double* Q_dev, int64_t qstride,
                      const double* Y0_dev, int r0, double* Yout_dev, xm_batch_result* res_dev);
 // NEXT-1 (implicit.cu)

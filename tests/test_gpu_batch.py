@@ -2,7 +2,9 @@
 one CTA runs the whole Algorithm 1 per instance), against the pinned oracle's
 staircase instance by instance: Thm 3's random-initialisation trials
 on one shared Q, and an App. G-style noise sweep with one Q per
-instance.  Tolerances as the single-instance end-to-end parity (C12, C14):
+instance, in the shared-memory layout (N ≤ 24) and the global-memory layout
+(BAL-93's N = 93, the size of the paper's 1000 trials).  Tolerances as the
+single-instance end-to-end parity (C12, C14):
 f ≤ 1e-8(1 + |f|), X = YYᵀ ≤ 1e-6, same certification, λ_min ≤ 1e-6‖Q‖_F."""
 import numpy as np
 import pytest
@@ -96,8 +98,52 @@ def test_batch_matches_the_single_instance_path(xm):
     assert np.linalg.norm(Yb @ Yb.T - Xs) <= 1e-6 * np.linalg.norm(Xs)
 
 
+def bal93_scene(seed=0):
+    """BAL-93-shaped (Thm 3's "1000 trials" ran on BAL-93): 93 cameras,
+    61203 points, mean track 4.7 (≈ 287k observations), small keypoint / depth
+    noise — n = 279, past the shared-memory layout (global-memory layout)."""
+    return make_scene(93, 61203, "unordered", seed=seed, track_mean=4.7, sigma_u=1e-3, sigma_d=0.01)
+
+
+def test_large_instances_random_init_trials(xm):
+    """Thm 3 at the paper's size (BAL-93): random feasible starts on one shared
+    Q (global-memory layout), every trial certified at the same X, and a sample
+    equal to the oracle's staircase from the same start."""
+    sc = bal93_scene()
+    dm = xo.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+    B = 24
+    Y0 = np.stack([random_factor(sc.N, 3, 2000 + b) for b in range(B)])
+    with xm.Context() as ctx:
+        Yg, res = ctx.solve_batch(dm.Q, Y0, shared_Q=True)
+    Xref = None
+    for b in range(B):
+        assert res[b]["certified"] == 1 and res[b]["status"] == 0, (b, res[b])
+        Y = Yg[b][:, :res[b]["r"]]
+        X = Y @ Y.T
+        Xref = X if Xref is None else Xref
+        assert np.linalg.norm(X - Xref) <= 1e-6 * np.linalg.norm(Xref)
+    for b in (0, 7, 23):
+        check_against_oracle(dm.Q, Y0[b], Yg[b], res[b])
+
+
+def test_large_instance_matches_the_single_instance_path(xm):
+    """Global-memory layout vs xm_solve (streaming path) from the identity start."""
+    sc = make_scene(40, 2000, "unordered", seed=5, track_mean=6.0, sigma_u=1e-3, sigma_d=0.01)
+    dm = xo.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+    with xm.Context() as ctx:
+        Yg, res = ctx.solve_batch(dm.Q, identity_start(40)[None], shared_Q=True)
+        ctx.set_Q(dm.Q)
+        st, info = ctx.solve()
+        Ys = ctx.get_factor()
+    Yb = Yg[0][:, :res[0]["r"]]
+    Xs = Ys @ Ys.T
+    assert st == 0 and res[0]["certified"] == 1
+    assert np.linalg.norm(Yb @ Yb.T - Xs) <= 1e-6 * np.linalg.norm(Xs)
+    check_against_oracle(dm.Q, identity_start(40), Yg[0], res[0])
+
+
 def test_batch_rejects_oversized_instances(xm):
     with xm.Context() as ctx:
         with pytest.raises(xm.XMError) as e:
-            ctx.solve_batch(np.zeros((75, 75)), identity_start(25)[None], shared_Q=True)
+            ctx.solve_batch(np.zeros((1203, 1203)), identity_start(401)[None], shared_Q=True)
     assert e.value.code == -1
