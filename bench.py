@@ -299,6 +299,18 @@ def implicit_bytes(N: int, E: int, r: int) -> float:
     return 80.0 * E + 8.0 * m * (m + 1) / 2 + 16.0 * 3 * N * r
 
 
+def pick_implicit(N: int, E: int, world: int) -> bool:
+    """--mode auto: the mode with the smaller modelled time per product — the
+    dense band streams 1/world of the lower triangle at ≈ 6.1 TB/s plus ONE
+    all-reduce; the matrix-free product moves 1/world of its bytes at the
+    measured ≈ 2.85 TB/s plus FIVE all-reduces (≈ 20 µs each assumed, 1 MB over
+    NVLink).  E: matrix-free on 1 and 2 GPUs, dense band at 4 and 8; B, C, D: dense."""
+    ar = 20e-6
+    t_dense = dense_bytes(N, 3) / world / 6.1e12 + (ar if world > 1 else 0.0)
+    t_imp = implicit_bytes(N, E, 3) / world / 2.85e12 + 15e-6 + (5 * ar if world > 1 else 0.0)
+    return t_imp < t_dense  # + 15 µs: five dependent launches per matrix-free product
+
+
 def roofline_pass(ctx, step, dev_in, out_dev, steps, barrier):
     """K steps with CUDA events around every Q·V product (event records inside
     the graphs add a few µs per launch, so timed regions run without them)."""
@@ -394,9 +406,9 @@ def main():
                    t=torch.empty((sc.N, 3), dtype=torch.float64, device=dev),
                    p=torch.empty((sc.M, 3), dtype=torch.float64, device=dev))
     stream = torch.cuda.current_stream(dev)
-    implicit = 1 if (args.mode == "implicit" and world == 1) else 0
-    if args.mode == "auto" and world == 1:
-        implicit = 1 if implicit_bytes(sc.N, sc.E, 3) < 0.5 * dense_bytes(sc.N, 3) else 0
+    implicit = 1 if args.mode == "implicit" else 0
+    if args.mode == "auto":
+        implicit = 1 if pick_implicit(sc.N, sc.E, world) else 0
     ctx = xm.Context(device=local, rank=rank, world=world, nccl_id=nccl_id,
                      stream=stream.cuda_stream, profile=0, implicit_q=implicit)
 

@@ -1141,7 +1141,7 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
   c->ldk = round_up(std::max(N - 1, 1), 32);
   set_shard(c, N);
   // NEXT-1 (implicit.cu): Q, S, C̄ and G are never formed — only K̄, its factor and inverse
-  const bool implicit = c->opt.implicit_q != 0 && c->world == 1;
+  const bool implicit = c->opt.implicit_q != 0;
   c->implicit_active = implicit;
   if (!implicit) {
     c->Q.alloc((size_t)std::max(c->nrows, 1) * c->ldq);

@@ -19,7 +19,9 @@
 // K̄ (N × N), its Cholesky factor and inverse.
 #include "frame_ops.cuh"
 
+#include <algorithm>
 #include <cstdio>
+#include <vector>
 #include <cstdlib>
 
 namespace xm {
@@ -78,7 +80,7 @@ __device__ __forceinline__ void group_sum(double (&v)[K], int g) {
 
 // m_k = Σ_{e∈k} (w_e ũ_e)ᵀ V_{i_e} / W_k          (landmark-sorted, 28 B / measurement)
 template <int R, int U = kU>
-__global__ void __launch_bounds__(kIT) k_imp_lm_mean(int M, const int32_t* __restrict__ lm_off,
+__global__ void __launch_bounds__(kIT) k_imp_lm_mean(int k0, int k1, const int32_t* __restrict__ lm_off,
                                                      const int32_t* __restrict__ L_i,
                                                      const double* __restrict__ L_wx,
                                                      const double* __restrict__ L_wy,
@@ -91,8 +93,8 @@ __global__ void __launch_bounds__(kIT) k_imp_lm_mean(int M, const int32_t* __res
   if (stop && *stop) return;  // a tCG graph replay past the stop
   if (exec && blockIdx.x == 0 && threadIdx.x == 0) *exec = 1;  // profiling: this product ran
   constexpr int NG = Grp<R>::NG;
-  const int k = blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (k >= M) return;
+  const int k = k0 + blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (k >= k1) return;
   const int g = lane / R, j = lane - g * R;
   const bool act = g < NG;
   double acc[1] = {0.0};
@@ -128,7 +130,7 @@ __global__ void __launch_bounds__(kIT) k_imp_lm_mean(int M, const int32_t* __res
 // i ≥ 1, written to bs[i − 1] (the K̄ ordering: the anchor row is dropped)
 // (frame-sorted, 12 B / measurement)
 template <int R, int U = kU>
-__global__ void __launch_bounds__(kIT) k_imp_fr_b(int N, const int32_t* __restrict__ fr_off,
+__global__ void __launch_bounds__(kIT) k_imp_fr_b(int f0, int f1, const int32_t* __restrict__ fr_off,
                                                   const int32_t* __restrict__ F_k,
                                                   const double* __restrict__ F_w,
                                                   const double* __restrict__ cfr,
@@ -138,8 +140,8 @@ __global__ void __launch_bounds__(kIT) k_imp_fr_b(int N, const int32_t* __restri
                                                   const int* __restrict__ stop) {
   if (stop && *stop) return;  // a tCG graph replay past the stop
   constexpr int NG = Grp<R>::NG;
-  const int i = 1 + blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (i >= N) return;
+  const int i = max(f0, 1) + blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (i >= f1) return;
   const int g = lane / R, j = lane - g * R;
   const bool act = g < NG;
   double acc[1] = {0.0};
@@ -171,13 +173,13 @@ __global__ void __launch_bounds__(kIT) k_imp_fr_b(int N, const int32_t* __restri
 // of spmm_sym.cu covers r ≤ 5):  tb[j + 1] = Σ_l K̄⁻¹[j][l] bs[l]  (tb[0] = 0;
 // the translations are t_i = −tb[i])
 template <int R>
-__global__ void __launch_bounds__(kIT) k_imp_gemv(int m_, const double* __restrict__ Kinv, int64_t ldk,
-                                                  const double* __restrict__ bs,
+__global__ void __launch_bounds__(kIT) k_imp_gemv(int m_, int j0, int j1, const double* __restrict__ Kinv,
+                                                  int64_t ldk, const double* __restrict__ bs,
                                                   double* __restrict__ tb,
                                                   const int* __restrict__ stop) {
   if (stop && *stop) return;  // a tCG graph replay past the stop
-  const int j = blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (j >= m_) return;
+  const int j = j0 + blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (j >= j1) return;
   const double* row = Kinv + (int64_t)j * ldk;  // 256-B aligned rows (ldk % 32 == 0)
   double acc[R];
 #pragma unroll
@@ -215,7 +217,7 @@ __global__ void __launch_bounds__(kIT) k_imp_gemv(int m_, const double* __restri
 // p_k = m_k + Σ_{e∈k} w_e t_{i_e} / W_k = m_k − Σ_{e∈k} w_e tb_{i_e} / W_k
 // (landmark-sorted, 12 B / measurement)
 template <int R, int U = kU>
-__global__ void __launch_bounds__(kIT) k_imp_lm_p(int M, const int32_t* __restrict__ lm_off,
+__global__ void __launch_bounds__(kIT) k_imp_lm_p(int k0, int k1, const int32_t* __restrict__ lm_off,
                                                   const int32_t* __restrict__ L_i,
                                                   const double* __restrict__ L_w,
                                                   const double* __restrict__ W,
@@ -225,8 +227,8 @@ __global__ void __launch_bounds__(kIT) k_imp_lm_p(int M, const int32_t* __restri
                                                   const int* __restrict__ stop) {
   if (stop && *stop) return;  // a tCG graph replay past the stop
   constexpr int NG = Grp<R>::NG;
-  const int k = blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (k >= M) return;
+  const int k = k0 + blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (k >= k1) return;
   const int g = lane / R, j = lane - g * R;
   const bool act = g < NG;
   double acc[1] = {0.0};
@@ -259,7 +261,7 @@ __global__ void __launch_bounds__(kIT) k_imp_lm_p(int M, const int32_t* __restri
 // (QV)_i = Σ_{e∈i} w_e ũ_e (z_e + t_i − p_k)ᵀ = A_i V_i + c_i t_iᵀ − Σ_{e∈i} (w_e ũ_e) p_kᵀ
 // (A_i = Σ_{e∈i} w_e ũ_e ũ_eᵀ, t_i = −tb_i; frame-sorted, 28 B / measurement)
 template <int R, int U = ((R <= 3) ? 4 : 2)>
-__global__ void __launch_bounds__(kIT, (R <= 5) ? 4 : 1) k_imp_fr_out(int N, const int32_t* __restrict__ fr_off,
+__global__ void __launch_bounds__(kIT, (R <= 5) ? 4 : 1) k_imp_fr_out(int f0, int f1, const int32_t* __restrict__ fr_off,
                                                     const int32_t* __restrict__ F_k,
                                                     const double* __restrict__ F_wx,
                                                     const double* __restrict__ F_wy,
@@ -272,8 +274,8 @@ __global__ void __launch_bounds__(kIT, (R <= 5) ? 4 : 1) k_imp_fr_out(int N, con
                                                     double* __restrict__ out,
                                                     const int* __restrict__ stop) {
   if (stop && *stop) return;  // a tCG graph replay past the stop
-  const int i = blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (i >= N) return;
+  const int i = f0 + blockIdx.x * (kIT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (i >= f1) return;
   double acc[3 * R];
 #pragma unroll
   for (int q = 0; q < 3 * R; ++q) acc[q] = 0.0;
@@ -430,10 +432,13 @@ static void imp_dbg(xm_ctx* c, const char* what) {
   if (e != cudaSuccess) throw Error(XM_ECUDA, std::string("implicit pass ") + what + ": " + cudaGetErrorString(e));
 }
 
+static void implicit_shards(xm_ctx* c);
+
 // Matrix-free assembly state: the pass layouts, per-frame moments and K̄⁻¹.
 void implicit_prepare(xm_ctx* c) {
   const int64_t E = c->E;
   const int N = c->N;
+  implicit_shards(c);
   c->imp_lm.alloc(E);
   c->imp_w.alloc(E);
   c->imp_pts.alloc(6 * E);           // L_wx L_wy L_wz F_wx F_wy F_wz
@@ -469,19 +474,64 @@ void implicit_prepare(xm_ctx* c) {
   }
 }
 
-// tb[1..N) = K̄⁻¹ bs: the lower-triangle stream (r ≤ 5) or the row GEMV.  Row 0
-// of tb is never read as data (t_0 = 0 is applied by the readers: a product
-// at another r leaves other values there)
-static void kinv_product(xm_ctx* c, const double* bs, int r, const int* stop) {
+// world > 1 (SURVEY §8(e) for the matrix-free products): every rank holds all
+// measurements, the per-frame moments and the full K̄⁻¹ (as on one GPU), and
+// computes its share of each pass — landmarks [k0, k1) and frames [f0, f1)
+// balanced by measurement count, the K̄⁻¹ rows [ka, kb) of an area-balanced,
+// 32-row-aligned band of its lower triangle — then ONE all-reduce of the
+// zero-padded pass output (m, b, t, p, Q·V: ≤ 1.2 MB each at E) gives every
+// rank the replicated result: five all-reduces per product, no other exchange.
+static void implicit_shards(xm_ctx* c) {
+  const int P = c->world, q = c->rank, N = c->N, M = c->M;
+  const int64_t E = c->E;
+  if (P <= 1) {
+    c->imp_k0 = 0, c->imp_k1 = M, c->imp_f0 = 0, c->imp_f1 = N, c->imp_ka = 0, c->imp_kb = std::max(N - 1, 0);
+    c->imp_el = c->imp_ef = E;
+    return;
+  }
+  std::vector<int32_t> lo(M + 1), fo(N + 1);
+  XM_CUDA(cudaMemcpy(lo.data(), c->lm_off.p, (M + 1) * 4, cudaMemcpyDeviceToHost));
+  XM_CUDA(cudaMemcpy(fo.data(), c->fr_off.p, (N + 1) * 4, cudaMemcpyDeviceToHost));
+  auto split = [&](const std::vector<int32_t>& off, int cnt, int p) {  // first segment at ≥ E·p/P
+    if (p <= 0) return 0;
+    if (p >= P) return cnt;
+    const int64_t target = E * p / P;
+    return (int)(std::lower_bound(off.begin(), off.begin() + cnt, (int32_t)target) - off.begin());
+  };
+  c->imp_k0 = split(lo, M, q);
+  c->imp_k1 = std::max(c->imp_k0, split(lo, M, q + 1));
+  c->imp_f0 = split(fo, N, q);
+  c->imp_f1 = std::max(c->imp_f0, split(fo, N, q + 1));
+  const int m = std::max(N - 1, 0);
+  c->imp_ka = band_start(m, P, q);
+  c->imp_kb = std::max(c->imp_ka, band_start(m, P, q + 1));
+  c->imp_el = lo[c->imp_k1] - lo[c->imp_k0];
+  c->imp_ef = fo[c->imp_f1] - fo[c->imp_f0];
+}
+
+// tb[1..N) = K̄⁻¹ bs: the lower-triangle stream (r ≤ 5; on world > 1 this rank's
+// band of rows, all-reduced by the caller) or the full row GEMV.  Row 0 of tb is
+// never read as data (t_0 = 0 is applied by the readers: a product at another r
+// leaves other values there)
+static void kinv_product(xm_ctx* c, const double* bs, int r, const int* stop, bool local_full = false) {
   const int mK = c->N - 1;
   if (mK < 1) return;  // tb stays 0 (N = 1)
   static const bool force_gemv = std::getenv("XM_IMP_GEMV") != nullptr;
-  if (r <= 5 && !force_gemv) {
+  if (r <= 5 && !force_gemv && !local_full) {
+    const int ka = c->world > 1 ? c->imp_ka : 0, kb = c->world > 1 ? c->imp_kb : mK;
+    if (c->world > 1 && kb <= ka) {  // empty band: a zero partial
+      XM_CUDA(cudaMemsetAsync(c->imp_tb.p + r, 0, (size_t)mK * r * 8, c->stream));
+      return;
+    }
     spmm_sym_matrix(c, c->imp_sym_plan, c->imp_sym_part, c->Kinv.p, mK, c->ldk, bs, r, c->imp_tb.p + r,
-                    stop);
-  } else {
-    XM_IMP_DISPATCH(r, (k_imp_gemv<R><<<ceil_div(mK, kIT / 32), kIT, 0, c->stream>>>(mK, c->Kinv.p, c->ldk,
-                                                                                     bs, c->imp_tb.p, stop)));
+                    stop, ka, kb - ka);
+  } else {  // full rows; world > 1 (r > 5): this rank's rows only, the others zero for the all-reduce
+    const bool part = c->world > 1 && !local_full;
+    const int j0 = part ? c->imp_ka : 0, j1 = part ? c->imp_kb : mK;
+    if (part) XM_CUDA(cudaMemsetAsync(c->imp_tb.p + r, 0, (size_t)mK * r * 8, c->stream));
+    if (j1 > j0)
+      XM_IMP_DISPATCH(r, (k_imp_gemv<R><<<ceil_div(j1 - j0, kIT / 32), kIT, 0, c->stream>>>(
+                             mK, j0, j1, c->Kinv.p, c->ldk, bs, c->imp_tb.p, stop)));
     XM_CHECK_LAUNCH();
     count_launch(c);
   }
@@ -490,16 +540,18 @@ static void kinv_product(xm_ctx* c, const double* bs, int r, const int* stop) {
 // Algorithmic bytes of one matrix-free product: the four passes'
 // per-measurement streams (28 + 12 + 12 + 28 B), the lower triangle of K̄⁻¹
 // (r ≤ 5; the full matrix for the row GEMV) and V in / Q·V out; the gathered
-// n × r / M × r arrays are L2-resident and not counted.
+// n × r / M × r arrays are L2-resident and not counted.  Per rank on world > 1.
 double implicit_alg_bytes(xm_ctx* c, int r) {
-  const double m = (double)c->N - 1.0;
-  const double kb = (r <= 5) ? 8.0 * m * (m + 1.0) / 2.0 : 8.0 * m * m;
-  return 80.0 * (double)c->E + kb + 16.0 * (double)c->n * r;
+  // this rank's share: its landmarks' and frames' measurements, its band of K̄⁻¹
+  const double a = c->imp_ka, b = c->imp_kb;
+  const double kb = (r <= 5) ? 8.0 * ((b * (b + 1.0)) - (a * (a + 1.0))) / 2.0 : 8.0 * (b - a) * ((double)c->N - 1.0);
+  return 40.0 * (double)c->imp_el + 40.0 * (double)c->imp_ef + kb + 16.0 * (double)c->n * r;
 }
 
 void implicit_product(xm_ctx* c, const double* V, int r, double* out, const int* stop, int* exec) {
   const int N = c->N, M = c->M;
   const int64_t E = c->E;
+  const bool sh = c->world > 1;
   DBuf<double>& m = scratch_f64(c, "imp_m");
   DBuf<double>& p = scratch_f64(c, "imp_p");
   DBuf<double>& bs = scratch_f64(c, "imp_bs");
@@ -509,29 +561,45 @@ void implicit_product(xm_ctx* c, const double* V, int r, double* out, const int*
   const double* P = c->imp_pts.p;
   const double* cfr = c->imp_mom.p;
   const double* Afr = c->imp_mom.p + 3 * (size_t)N;
+  const int k0 = c->imp_k0, k1 = c->imp_k1, f0 = c->imp_f0, f1 = c->imp_f1;
+  const int PR = (r + 1) & ~1;  // p's row stride (PStride)
   imp_dbg(c, "entry");
-  XM_IMP_DISPATCH(r, (k_imp_lm_mean<R><<<ceil_div(M, kIT / 32), kIT, 0, c->stream>>>(
-                         M, c->lm_off.p, c->e_fr.p, P, P + E, P + 2 * E, c->W.p, V, m.p, stop, exec)));
+  if (sh) XM_CUDA(cudaMemsetAsync(m.p, 0, (size_t)M * r * 8, c->stream));
+  if (k1 > k0)
+    XM_IMP_DISPATCH(r, (k_imp_lm_mean<R><<<ceil_div(k1 - k0, kIT / 32), kIT, 0, c->stream>>>(
+                           k0, k1, c->lm_off.p, c->e_fr.p, P, P + E, P + 2 * E, c->W.p, V, m.p, stop, exec)));
+  if (sh) nccl_allreduce_sum(c, m.p, (size_t)M * r);
   imp_dbg(c, "lm_mean");
-  if (N > 1)  // 16 rounds in flight (E: 43 → 36 µs; the other passes measured flat or slower)
-    XM_IMP_DISPATCH(r, (k_imp_fr_b<R, 16><<<ceil_div(N - 1, kIT / 32), kIT, 0, c->stream>>>(
-                           N, c->fr_off.p, c->imp_lm.p, c->imp_w.p, cfr, V, m.p, bs.p, stop)));
+  const int fb0 = std::max(f0, 1);
+  if (sh) XM_CUDA(cudaMemsetAsync(bs.p, 0, (size_t)std::max(N - 1, 1) * r * 8, c->stream));
+  if (f1 > fb0)  // 16 rounds in flight (E: 43 → 36 µs; the other passes measured flat or slower)
+    XM_IMP_DISPATCH(r, (k_imp_fr_b<R, 16><<<ceil_div(f1 - fb0, kIT / 32), kIT, 0, c->stream>>>(
+                           f0, f1, c->fr_off.p, c->imp_lm.p, c->imp_w.p, cfr, V, m.p, bs.p, stop)));
   XM_CHECK_LAUNCH();
+  if (sh && N > 1) nccl_allreduce_sum(c, bs.p, (size_t)(N - 1) * r);
   imp_dbg(c, "fr_b");
   kinv_product(c, bs.p, r, stop);
+  if (sh && N > 1) nccl_allreduce_sum(c, c->imp_tb.p + r, (size_t)(N - 1) * r);
   imp_dbg(c, "kinv");
-  XM_IMP_DISPATCH(r, (k_imp_lm_p<R><<<ceil_div(M, kIT / 32), kIT, 0, c->stream>>>(M, c->lm_off.p, c->e_fr.p, c->e_w.p, c->W.p,
-                                                               c->imp_tb.p, m.p, p.p, stop)));
+  if (sh) XM_CUDA(cudaMemsetAsync(p.p, 0, (size_t)M * PR * 8, c->stream));
+  if (k1 > k0)
+    XM_IMP_DISPATCH(r, (k_imp_lm_p<R><<<ceil_div(k1 - k0, kIT / 32), kIT, 0, c->stream>>>(
+                           k0, k1, c->lm_off.p, c->e_fr.p, c->e_w.p, c->W.p, c->imp_tb.p, m.p, p.p, stop)));
+  if (sh) nccl_allreduce_sum(c, p.p, (size_t)M * PR);
   imp_dbg(c, "lm_p");
-  XM_IMP_DISPATCH(r, (k_imp_fr_out<R><<<ceil_div(N, kIT / 32), kIT, 0, c->stream>>>(
-                         N, c->fr_off.p, c->imp_lm.p, P + 3 * E, P + 4 * E, P + 5 * E, cfr, Afr, V,
-                         c->imp_tb.p, p.p, out, stop)));
+  if (sh) XM_CUDA(cudaMemsetAsync(out, 0, (size_t)3 * N * r * 8, c->stream));
+  if (f1 > f0)
+    XM_IMP_DISPATCH(r, (k_imp_fr_out<R><<<ceil_div(f1 - f0, kIT / 32), kIT, 0, c->stream>>>(
+                           f0, f1, c->fr_off.p, c->imp_lm.p, P + 3 * E, P + 4 * E, P + 5 * E, cfr, Afr, V,
+                           c->imp_tb.p, p.p, out, stop)));
   XM_CHECK_LAUNCH();
+  if (sh) nccl_allreduce_sum(c, out, (size_t)3 * N * r);
   imp_dbg(c, "fr_out");
   count_launch(c, N > 1 ? 4 : 3);
 }
 
 // translations of the rounded solution, t = −K̄⁻¹ C̄ Y₃ (Eq. (4)), from the same passes
+// (one-shot: every rank runs them over all landmarks / frames, no exchange)
 void implicit_translations(xm_ctx* c, const double* Y3, double* t_out) {
   const int N = c->N, M = c->M;
   const int64_t E = c->E;
@@ -540,13 +608,14 @@ void implicit_translations(xm_ctx* c, const double* Y3, double* t_out) {
   m.alloc((size_t)M * XM_MAX_R + 8);
   bs.alloc((size_t)(3 * ceil_div(N, 3) + 6) * XM_MAX_R + 8);
   const double* P = c->imp_pts.p;
-  k_imp_lm_mean<3><<<ceil_div(M, kIT / 32), kIT, 0, c->stream>>>(M, c->lm_off.p, c->e_fr.p, P, P + E, P + 2 * E, c->W.p, Y3,
-                                              m.p, nullptr, nullptr);
+  k_imp_lm_mean<3><<<ceil_div(M, kIT / 32), kIT, 0, c->stream>>>(0, M, c->lm_off.p, c->e_fr.p, P, P + E,
+                                                                 P + 2 * E, c->W.p, Y3, m.p, nullptr, nullptr);
   if (N > 1)
-    k_imp_fr_b<3, 16><<<ceil_div(N - 1, kIT / 32), kIT, 0, c->stream>>>(N, c->fr_off.p, c->imp_lm.p, c->imp_w.p,
-                                                                    c->imp_mom.p, Y3, m.p, bs.p, nullptr);
+    k_imp_fr_b<3, 16><<<ceil_div(N - 1, kIT / 32), kIT, 0, c->stream>>>(0, N, c->fr_off.p, c->imp_lm.p,
+                                                                        c->imp_w.p, c->imp_mom.p, Y3, m.p,
+                                                                        bs.p, nullptr);
   XM_CHECK_LAUNCH();
-  kinv_product(c, bs.p, 3, nullptr);
+  kinv_product(c, bs.p, 3, nullptr, c->world > 1);  // world > 1: the full-row GEMV (band plan is partial)
   k_imp_neg<<<ceil_div((int64_t)3 * N, 256), 256, 0, c->stream>>>((int64_t)3 * N, c->imp_tb.p, t_out);
   XM_CHECK_LAUNCH();
   count_launch(c, N > 1 ? 3 : 2);

@@ -621,8 +621,12 @@ static void launch_sym(xm_ctx* c, const double* V, const SpmmEpiArgs& ep) {
 // V and out m × r row-major with ≥ 3·⌈m/3⌉ rows of room (r ≤ 5).  NEXT-1:
 // the K̄⁻¹ product of the matrix-free Q·V (implicit.cu).
 void spmm_sym_matrix(xm_ctx* c, void*& plan_slot, DBuf<double>& part, const double* A, int m,
-                     int64_t lda, const double* V, int r, double* out, const int* stop) {
-  SymPlan& p = sym_plan_for(c, plan_slot, SymSrc{A, m, lda, 0, m});
+                     int64_t lda, const double* V, int r, double* out, const int* stop, int row0,
+                     int nrows) {
+  // band [row0, row0 + nrows) (32-row aligned; world > 1): the partial of its
+  // lower trapezoid, full length (row parts of its rows, column parts above)
+  if (nrows < 0) nrows = m;
+  SymPlan& p = sym_plan_for(c, plan_slot, SymSrc{A + (int64_t)row0 * lda, m, lda, row0, nrows});
   SpmmEpiArgs ep{};
   ep.out = out;
   ep.stop = stop;

@@ -147,6 +147,9 @@ struct xm_ctx {
   xm::DBuf<double> imp_pts, imp_w, Kinv;   // w·ũ (landmark- and frame-sorted SoA), frame-sorted w
   xm::DBuf<double> imp_mom, imp_tb;        // per-frame c_i, A_i; [0; K̄⁻¹ b]
   void* imp_sym_plan = nullptr;            // lower-triangle stream plan of K̄⁻¹
+  // world > 1: this rank's landmarks [k0, k1), frames [f0, f1), K̄⁻¹ rows [ka, kb)
+  int imp_k0 = 0, imp_k1 = 0, imp_f0 = 0, imp_f1 = 0, imp_ka = 0, imp_kb = 0;
+  int64_t imp_el = 0, imp_ef = 0;  // measurements of this rank's landmarks / frames
   xm::DBuf<double> imp_sym_part;
   xm::DBuf<double> lam;    // N × 6 (xx, yy, zz, xy, xz, yz)
   xm::DBuf<double> part;   // SpMM split-K partials: nsplit × nrows × r
@@ -408,7 +411,8 @@ void nccl_allgather_f64(xm_ctx* c, const double* send, double* recv, size_t coun
 void sym_plan_destroy(xm_ctx* c);
 void sym_plan_slot_destroy(void*& slot);
 void spmm_sym_matrix(xm_ctx* c, void*& plan_slot, DBuf<double>& part, const double* A, int m,
-                     int64_t lda, const double* V, int r, double* out, const int* stop);
+                     int64_t lda, const double* V, int r, double* out, const int* stop, int row0 = 0,
+                     int nrows = -1);
 void sym_tcg_plan_destroy(xm_ctx* c);
 
 // Row sharding: rank q owns frames [q·nfpr, min(N, (q+1)·nfpr)),

@@ -6,8 +6,10 @@ xm_shard_rows composed with the symmetric stream: each rank holds the lower
 trapezoid of its band of rows, forms the row parts of its rows and the column
 parts of every row above (a full-length partial), and ONE all-reduce of the
 partials must give Q·V; plus the all-reduce of the ‖Q‖² partials (2× the
-strictly lower entries + the diagonal), and the column-sharded TRSM's
-all-gather of packed G = L⁻¹C̄ slices.  Exits non-zero on any mismatch.
+strictly lower entries + the diagonal), the column-sharded TRSM's
+all-gather of packed G = L⁻¹C̄ slices, and the sharded matrix-free product
+(landmark / frame shares + a K̄⁻¹ band, five all-reduces).  Exits non-zero on
+any mismatch.
 """
 import os
 import sys
@@ -92,6 +94,53 @@ def main():
             if q1 > q0:
                 G[:, q0:q1] = parts[q].numpy().reshape(m, w)[:, : q1 - q0]
         assert np.abs(G - dm.G).max() <= 1e-10 * max(1.0, np.abs(dm.G).max()), ("trsm shard", N)
+        # 5. sharded matrix-free product (implicit.cu, world > 1): landmarks and
+        #    frames split by measurement count, K̄⁻¹ by an area-balanced 32-row
+        #    band of its lower triangle; five all-reduces of zero-padded pass
+        #    outputs reproduce Q·V (the passes follow reading C24)
+        E = len(sc.frame)
+        fr, lmk, w, pts = sc.frame, sc.landmark, sc.w, sc.pts
+        order_l = np.lexsort((fr, lmk))
+        lm_off = np.searchsorted(lmk[order_l], np.arange(sc.M + 1))
+        order_f = np.lexsort((lmk, fr))
+        fr_off = np.searchsorted(fr[order_f], np.arange(N + 1))
+        split = lambda off, cnt, p: 0 if p <= 0 else (cnt if p >= world else int(np.searchsorted(off[:cnt], E * p // world)))
+        k0, k1 = split(lm_off, sc.M, rank), split(lm_off, sc.M, rank + 1)
+        f0, f1 = split(fr_off, N, rank), split(fr_off, N, rank + 1)
+        mK = N - 1
+        bs = lambda p: 0 if p <= 0 else (mK if p >= world else min(mK, max(0, int(round(mK * np.sqrt(p / world) / 32.0)) * 32)))
+        ka, kb = bs(rank), max(bs(rank), bs(rank + 1))
+        Kinv = np.linalg.inv(dm.K[1:, 1:])
+        Vb = V.reshape(N, 3, r)
+        z = np.einsum("ea,ear->er", w[:, None] * pts, Vb[fr])              # (wũ)_eᵀ V_i
+        Wk = np.bincount(lmk, weights=w, minlength=sc.M)
+        inl = (lmk >= k0) & (lmk < k1)
+        m = np.zeros((sc.M, r))
+        np.add.at(m, lmk[inl], z[inl])
+        m[k0:k1] /= Wk[k0:k1, None]
+        tm = torch.from_numpy(m); dist.all_reduce(tm); m = tm.numpy()
+        inf = (fr >= max(f0, 1)) & (fr < f1)
+        b = np.zeros((N, r))
+        np.add.at(b, fr[inf], w[inf, None] * (np.einsum("ea,ear->er", pts[inf], Vb[fr[inf]]) - m[lmk[inf]]))
+        tb = torch.from_numpy(b); dist.all_reduce(tb); b = tb.numpy()
+        L = np.tril(Kinv)[ka:kb]
+        strict = L.copy()
+        strict[np.arange(kb - ka), np.arange(ka, kb)] = 0.0
+        tpart = np.zeros((mK, r))
+        tpart[ka:kb] += L @ b[1:]
+        tpart += strict.T @ b[1:][ka:kb]
+        tt = torch.from_numpy(tpart); dist.all_reduce(tt)
+        t = np.zeros((N, r)); t[1:] = -tt.numpy()
+        p = np.zeros((sc.M, r))
+        np.add.at(p, lmk[inl], w[inl, None] * t[fr[inl]])
+        p[k0:k1] = m[k0:k1] + p[k0:k1] / Wk[k0:k1, None]
+        tp = torch.from_numpy(p); dist.all_reduce(tp); p = tp.numpy()
+        ino = (fr >= f0) & (fr < f1)
+        res = w[ino, None] * (np.einsum("ea,ear->er", pts[ino], Vb[fr[ino]]) + t[fr[ino]] - p[lmk[ino]])
+        out = np.zeros((N, 3, r))
+        np.add.at(out, fr[ino], pts[ino, :, None] * res[:, None, :])
+        to = torch.from_numpy(out.reshape(n, r)); dist.all_reduce(to)
+        assert np.abs(to.numpy() - ref).max() <= 1e-10 * max(1.0, np.abs(ref).max()), ("implicit shard", N, r)
     dist.barrier()
     dist.destroy_process_group()
     if rank == 0:
