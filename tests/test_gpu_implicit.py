@@ -48,6 +48,27 @@ def test_implicit_products_and_norm(xm, cfg):
 
 
 @pytest.mark.parametrize("cfg", SCENES, ids=lambda c: f"{c['kind']}{c['N']}")
+def test_implicit_grad_and_hvp(xm, cfg):
+    """The Riemannian gradient and HVP (reading C5) through the
+    matrix-free products: ≤ 1e-12 relative against the oracle's rgrad / hess
+    on the dense Q, at random feasible points, r = 3, 4, 5."""
+    sc = make_scene(seed=3, **cfg)
+    dm = xo.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+    with xm.Context(implicit_q=1) as ctx:
+        ctx.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+        for r in (3, 4, 5):
+            Y = random_factor(sc.N, r, 200 + r)
+            V = xo.project(Y, random_tangent_ambient(sc.N, r, 300 + r))
+            g, f = ctx.grad(Y)
+            g_o, Lam = xo.rgrad(Y, dm.Q @ Y)
+            assert np.linalg.norm(g - g_o) <= 1e-12 * np.linalg.norm(g_o), r
+            assert abs(f - xo.cost(dm.Q, Y)) <= 1e-12 * abs(xo.cost(dm.Q, Y)), r
+            hv = ctx.hvp(Y, V)
+            h_o = xo.hess(dm.Q, Y, Lam, V)
+            assert np.linalg.norm(hv - h_o) <= 1e-12 * np.linalg.norm(h_o), r
+
+
+@pytest.mark.parametrize("cfg", SCENES, ids=lambda c: f"{c['kind']}{c['N']}")
 def test_implicit_solve_matches_dense_oracle(xm, cfg):
     sc = make_scene(seed=3, **cfg)
     dm = xo.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
