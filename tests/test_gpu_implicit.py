@@ -117,3 +117,24 @@ def test_implicit_E_sampled_products_and_known_optimum(xm):
     assert abs(info["f"]) <= 1e-8 * info["normQ"] and cert["eta"] <= 1e-6
     np.testing.assert_allclose(g["s"], sc.s, atol=1e-7)
     np.testing.assert_allclose(g["R"], sc.R, atol=1e-7)
+
+
+def test_conditional_graph_loop_equals_batched_graphs(xm, monkeypatch):
+    """The tCG loop as ONE conditional-WHILE graph launch runs exactly the
+    kernels of the batched graphs up to the stop: the same trajectory, bitwise
+    (matrix-free products, three-kernel tCG iterations)."""
+    sc = make_scene(seed=7, N=300, M=4000, kind="unordered", track_mean=12.0, sigma_d=0.01, sigma_u=1e-3)
+    runs = []
+    for flag in (None, "1"):
+        if flag:
+            monkeypatch.setenv("XM_NO_COND_GRAPH", flag)
+        else:
+            monkeypatch.delenv("XM_NO_COND_GRAPH", raising=False)
+        with xm.Context(implicit_q=1) as ctx:
+            ctx.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+            status, info = ctx.solve()
+            runs.append((status, info, ctx.get_factor()))
+    (s0, i0, Y0), (s1, i1, Y1) = runs
+    assert s0 == s1 == 0
+    assert i0["hvps"] == i1["hvps"] and i0["outer_iters"] == i1["outer_iters"]
+    assert i0["f"] == i1["f"] and np.array_equal(Y0, Y1)
