@@ -7,16 +7,22 @@
 //
 //   z_e = V_iᵀ ũ_e,   m_k = Σ_{e∈k} w_e z_e / W_k           k_imp_lm_mean  (landmark pass)
 //   b_i = Σ_{e∈i} w_e (z_e − m_k)          (= (C̄V)_i)        k_imp_fr_b     (frame pass)
-//   t   = −K̄⁻¹ b,  t_0 = 0                                   k_imp_gemv     (dense K̄⁻¹)
+//   t   = −K̄⁻¹ b,  t_0 = 0                                   k_spmm_sym on the lower triangle
+//                                                             of K̄⁻¹ (spmm_sym.cu; r ≤ 5) or
+//                                                             k_imp_gemv (full rows, r > 5)
 //   p_k = m_k + Σ_{e∈k} w_e t_{i_e} / W_k                    k_imp_lm_p     (landmark pass)
 //   (QV)_i = Σ_{e∈i} w_e ũ_e (z_e + t_i − p_k)ᵀ               k_imp_fr_out   (frame pass)
 //
-// Landmark passes walk the canonical (landmark-sorted) measurement arrays,
-// frame passes a frame-sorted copy (both coalesced); one warp per landmark /
-// frame, fixed-order warp reductions (deterministic).  Bytes per product ≈ 4
-// passes over 40 B / measurement + 8(N−1)² for K̄⁻¹ (E: ≈ 1.6 GB vs 3.7 GB for
-// the lower triangle of Q), and the assembly never forms S, C̄, G or Q — only
-// K̄ (N × N), its Cholesky factor and inverse.
+// evaluated through per-frame moments c_i = Σ_{e∈i} w_e ũ_e, A_i = Σ_{e∈i} w_e ũ_e ũ_eᵀ
+// and w·ũ premultiplied per measurement (b_i = c_iᵀV_i − Σ w_e m_k;
+// (QV)_i = A_iV_i + c_i t_iᵀ − Σ (wũ)_e p_kᵀ).  Landmark passes walk the canonical
+// (landmark-sorted) measurement arrays, frame passes frame-sorted copies (both
+// coalesced); one warp per landmark / frame, fixed-order reductions
+// (deterministic).  Bytes per product: 80 B per measurement over the four passes
+// + 8·m(m+1)/2 for the lower triangle of K̄⁻¹ (E: 0.81 GB vs 3.71 GB for the
+// lower triangle of Q); the assembly never forms S, C̄, G or Q — only K̄
+// (N × N), its Cholesky factor and inverse.  world > 1: each rank runs its
+// share of every pass and a band of K̄⁻¹, one all-reduce per pass.
 #include "frame_ops.cuh"
 
 #include <algorithm>
