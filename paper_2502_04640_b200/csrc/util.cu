@@ -91,6 +91,41 @@ __global__ void k_dot_flat(const double* __restrict__ a, const double* __restric
   if (threadIdx.x == 0) partials[blockIdx.x] = sh[0];
 }
 
+// two dot products in one pass (same per-pair arithmetic and order as two
+// k_dot_flat launches): partials[blk·2 + q] = block sum of ⟨a_q, b_q⟩
+__global__ void k_dot2_flat(const double* __restrict__ a0, const double* __restrict__ b0,
+                            const double* __restrict__ a1, const double* __restrict__ b1, int64_t len,
+                            double* __restrict__ partials) {
+  __shared__ double sh[2][256];
+  double acc0 = 0.0, acc1 = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    acc0 = fma(a0[i], b0[i], acc0);
+    acc1 = fma(a1[i], b1[i], acc1);
+  }
+  sh[0][threadIdx.x] = acc0;
+  sh[1][threadIdx.x] = acc1;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      sh[0][threadIdx.x] += sh[0][threadIdx.x + s];
+      sh[1][threadIdx.x] += sh[1][threadIdx.x + s];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    partials[2 * blockIdx.x] = sh[0][0];
+    partials[2 * blockIdx.x + 1] = sh[1][0];
+  }
+}
+
+void dot2_flat(xm_ctx* c, const double* a0, const double* b0, const double* a1, const double* b1,
+               int64_t len, double* partials, int nblk) {
+  k_dot2_flat<<<nblk, 256, 0, c->stream>>>(a0, b0, a1, b1, len, partials);
+  XM_CHECK_LAUNCH();
+  count_launch(c);
+}
+
 void dot_flat(xm_ctx* c, const double* a, const double* b, int64_t len, double* partials,
               int nblk) {
   k_dot_flat<<<nblk, 256, 0, c->stream>>>(a, b, len, partials);

@@ -114,10 +114,8 @@ void df_product(xm_ctx* c, int r, const double* D, const double* QY, double* QD,
   } else {
     spmm_full(c, D, r, QD, nullptr);
     c->lz_part.alloc((size_t)kDotBlocks * 4 + 64);
-    dot_flat(c, QY, D, len, c->lz_part.p, kDotBlocks);
-    reduce_partials(c, c->lz_part.p, kDotBlocks, 1, scal_out);
-    dot_flat(c, D, QD, len, c->lz_part.p, kDotBlocks);
-    reduce_partials(c, c->lz_part.p, kDotBlocks, 1, scal_out + 1);
+    dot2_flat(c, QY, D, D, QD, len, c->lz_part.p, kDotBlocks);  // ⟨QY, D⟩, ⟨D, QD⟩
+    reduce_partials(c, c->lz_part.p, kDotBlocks, 2, scal_out);
   }
 }
 
@@ -317,9 +315,14 @@ static const char* kPhaseNames[8] = {"tcg", "retract+df", "accept+grad", "eval_p
 // (η in c->eta, Hη in c->Heta).  Path: the whole loop in one cooperative
 // launch (tcg_persist.cu) when supported, else CUDA-graph batches of
 // iterations (fused or three-kernel, manifold.cu).
-TcgState run_tcg(xm_ctx* c, int r, double Delta) {
+// defer (conditional-graph path only): the final state is copied into the
+// pinned host scalars without a sync and *deferred is set; the caller reads it
+// after its next sync (tcg_deferred_state) — one host round trip per outer
+// iteration instead of three.
+TcgState run_tcg(xm_ctx* c, int r, double Delta, bool* deferred = nullptr) {
   tcg_init(c, r, Delta);
   TcgState hs{};
+  if (deferred) *deferred = false;
   const bool persist = tcg_persist_supported(c, r);
   xm_ctx::TcgGraph* g = !persist && c->use_graphs && c->world == 1 ? tcg_graph(c, r) : nullptr;
   if (persist) {  // the whole tCG loop in one cooperative launch (tcg_persist.cu)
@@ -346,6 +349,13 @@ TcgState run_tcg(xm_ctx* c, int r, double Delta) {
   while (!persist) {
     if (g && g->loop) {  // the whole loop in one launch (the condition ends it)
       XM_CUDA(cudaGraphLaunch(g->exec, c->stream));
+      if (deferred && c->hpin) {
+        XM_CUDA(cudaMemcpyAsync(c->hpin + kPinTcg, c->tcg.p, sizeof(TcgState), cudaMemcpyDeviceToHost,
+                                c->stream));
+        c->tcg_defer_launches = g->launches;
+        *deferred = true;
+        return hs;
+      }
       XM_CUDA(cudaMemcpyAsync(&hs, c->tcg.p, sizeof(TcgState), cudaMemcpyDeviceToHost, c->stream));
       sync(c);
       // iterations launched: one per HVP plus the final one whose update saw the stop
@@ -368,6 +378,16 @@ TcgState run_tcg(xm_ctx* c, int r, double Delta) {
       break;
     }
   }
+  return hs;
+}
+
+// the state of a deferred conditional-graph tCG, after the caller's sync
+TcgState tcg_deferred_state(xm_ctx* c) {
+  TcgState hs;
+  std::memcpy(&hs, c->hpin + kPinTcg, sizeof(TcgState));
+  c->stats.kernel_launches += c->tcg_defer_launches * std::max<int64_t>(1, hs.n_hvp);
+  if (!hs.stop) throw Error(XM_ECUDA, "tCG loop graph returned before its stop");
+  c->stats.spmm_calls += hs.n_hvp;  // graph replays do not count products host-side
   return hs;
 }
 
@@ -400,8 +420,9 @@ RtrOut rtr(xm_ctx* c, double tol_abs) {
     }
     if (it >= o.max_outer) break;
     // ---- tCG (device-resident state; persistent / fused / three-kernel)
-    const TcgState hs = run_tcg(c, r, Delta);
-    c->info.hvps += hs.n_hvp;
+    bool deferred = false;
+    TcgState hs = run_tcg(c, r, Delta, c->phases_on ? nullptr : &deferred);
+    if (!deferred) c->info.hvps += hs.n_hvp;
     pc.lap(0);
     // ---- retraction (+ ⟨g,η⟩, ⟨η,Hη⟩) and cancellation-free Δf (reading C21)
     XM_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int), c->stream));
@@ -412,13 +433,22 @@ RtrOut rtr(xm_ctx* c, double tol_abs) {
     reduce_partials(c, c->red.p, nb, 2, c->scal.p + 10);
     df_product(c, r, c->Dv.p, c->QY.p, c->QD.p, c->scal.p + 8);
     if (o.scale_reg != 0.0) reg_frames(c, r, c->Y.p, c->Dv.p, c->scal.p + 24);
-    double d[4];
-    read_scal(c, 8, 4, d);
-    double dreg = 0.0;
-    if (o.scale_reg != 0.0) read_scal(c, 26, 1, &dreg);
-    int rerr = 0;
-    XM_CUDA(cudaMemcpyAsync(&rerr, c->flags.p, 4, cudaMemcpyDeviceToHost, c->stream));
+    // one host round trip: Δf terms, the App. D term, the retraction flag and
+    // (deferred) the tCG state, all through the pinned host scalars
+    double* hp = c->hpin;
+    XM_CUDA(cudaMemcpyAsync(hp + kPinD, c->scal.p + 8, 4 * 8, cudaMemcpyDeviceToHost, c->stream));
+    if (o.scale_reg != 0.0)
+      XM_CUDA(cudaMemcpyAsync(hp + kPinD + 4, c->scal.p + 26, 8, cudaMemcpyDeviceToHost, c->stream));
+    XM_CUDA(cudaMemcpyAsync(hp + kPinD + 5, c->flags.p, 4, cudaMemcpyDeviceToHost, c->stream));
     sync(c);
+    if (deferred) {
+      hs = tcg_deferred_state(c);
+      c->info.hvps += hs.n_hvp;
+    }
+    const double d[4] = {hp[kPinD], hp[kPinD + 1], hp[kPinD + 2], hp[kPinD + 3]};
+    const double dreg = (o.scale_reg != 0.0) ? hp[kPinD + 4] : 0.0;
+    int rerr = 0;
+    std::memcpy(&rerr, hp + kPinD + 5, 4);
     if (rerr) throw Error(XM_ERETRACT, "retraction failure");
     pc.lap(1);
     const double df = 2.0 * d[0] + d[1] + dreg;
@@ -674,6 +704,7 @@ xm_status xm_create(xm_ctx** out, int device, int rank, int world, const void* n
       XM_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
       c->own_stream = true;
     }
+    XM_CUDA(cudaMallocHost(reinterpret_cast<void**>(&c->hpin), kPinDoubles * sizeof(double)));
     nccl_init(c, nccl_id);
   });
   if (st != XM_OK) {
@@ -694,6 +725,7 @@ void xm_destroy(xm_ctx* c) {
   destroy_graphs(c);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
+  if (c->hpin) cudaFreeHost(c->hpin);
   if (c->ev_la) cudaEventDestroy(c->ev_la);
   if (c->ev_lb) cudaEventDestroy(c->ev_lb);
   nccl_destroy(c);

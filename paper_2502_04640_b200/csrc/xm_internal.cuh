@@ -99,6 +99,9 @@ struct Launcher;  // fwd
 }  // namespace xm
 
 // The context (opaque in the ABI).
+namespace xm {
+constexpr int kPinD = 0, kPinTcg = 16, kPinDoubles = 512;
+}
 struct xm_ctx {
   int device = 0, rank = 0, world = 1;
   cudaStream_t stream = nullptr;
@@ -220,6 +223,10 @@ struct xm_ctx {
   cudaStream_t cap_stream = nullptr;
   // side stream + events of the look-ahead Cholesky (assembly.cu dense_cholesky)
   cudaStream_t aux_stream = nullptr;
+  // pinned host scalars: several device → host reads completed by ONE sync
+  // (kPinD: the outer iteration's Δf terms; kPinTcg: a deferred tCG state)
+  double* hpin = nullptr;
+  int64_t tcg_defer_launches = 0;
   cudaEvent_t ev_la = nullptr, ev_lb = nullptr;
   bool use_graphs = true;
   xm::DBuf<double> sym_part;       // per-unit row / column partials of the symmetric SpMM
@@ -283,6 +290,8 @@ void reduce_partials(xm_ctx* c, const double* partials, int nblk, int ncomp, dou
 void exclusive_scan_i32(xm_ctx* c, const int32_t* in, int32_t* out, int64_t n, int32_t* total_dev);
 void radix_sort_u64(xm_ctx* c, uint64_t* keys, uint32_t* vals, int64_t n, int bits,
                     DBuf<uint64_t>& tmp_k, DBuf<uint32_t>& tmp_v);
+void dot2_flat(xm_ctx* c, const double* a0, const double* b0, const double* a1, const double* b1,
+               int64_t len, double* partials, int nblk);
 void dot_flat(xm_ctx* c, const double* a, const double* b, int64_t len, double* partials, int nblk);
 constexpr int kDotBlocks = 296;  // 2 × 148 SMs; fixed ⇒ deterministic sums
 
