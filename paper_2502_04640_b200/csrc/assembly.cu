@@ -166,12 +166,12 @@ __global__ void k_pattern_count(int N, int W32, const unsigned* __restrict__ bit
 }
 // one warp per row: enumerate set bits in ascending column order
 __global__ void k_pattern_cols(int N, int W32, const unsigned* __restrict__ bits,
-                               const int32_t* __restrict__ off32, int32_t* __restrict__ colidx,
+                               const int64_t* __restrict__ off, int32_t* __restrict__ colidx,
                                int64_t* __restrict__ rowptr) {
   int i = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   int lane = threadIdx.x & 31;
   if (i >= N) return;
-  int base = off32[i];
+  int64_t base = off[i];  // 64-bit: a near-full pattern has ~N² blocks (> 2³¹ past N ≈ 46 k)
   if (lane == 0) rowptr[i] = base;
   for (int w0 = 0; w0 < W32; w0 += 32) {
     int w = w0 + lane;
@@ -182,7 +182,7 @@ __global__ void k_pattern_cols(int N, int W32, const unsigned* __restrict__ bits
       int t = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += t;
     }
-    int pos = base + incl - c;
+    int64_t pos = base + incl - c;
     while (b) {
       int bit = __ffs(b) - 1;
       colidx[pos++] = w * 32 + bit;
@@ -948,6 +948,43 @@ __global__ void k_sumsq_rows(const double* __restrict__ Q, int rows, int n, int6
   if (threadIdx.x == 0) partials[blockIdx.x] = sh[0];
 }
 
+// H3: the co-visibility BSR pattern of S (bitmap per row → counts → 64-bit
+// row offsets (host prefix sum) → sorted column lists)
+void build_s_pattern(xm_ctx* c, int N) {
+  int W32 = ceil_div(N, 32);
+  DBuf<uint32_t>& bits = scratch_u32(c, "pattern_bits");
+  bits.alloc((size_t)N * W32);
+  XM_CUDA(cudaMemsetAsync(bits.p, 0, (size_t)N * W32 * 4, c->stream));
+  k_pattern_bits<<<N, 128, 0, c->stream>>>(N, W32, c->fr_off.p, c->fr_edge.p, c->e_lm.p,
+                                           c->lm_off.p, c->e_fr.p, bits.p);
+  XM_CHECK_LAUNCH();
+  DBuf<int32_t>& rc = scratch_i32(c, "pattern_rc");
+  DBuf<int64_t>& ro = scratch_i64(c, "pattern_ro");
+  rc.alloc(N);
+  ro.alloc(N + 1);
+  k_pattern_count<<<N, 256, 0, c->stream>>>(N, W32, bits.p, rc.p);
+  XM_CHECK_LAUNCH();
+  std::vector<int32_t> cnt(N);
+  std::vector<int64_t> off(N + 1, 0);
+  XM_CUDA(cudaMemcpyAsync(cnt.data(), rc.p, (size_t)N * 4, cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  for (int i = 0; i < N; ++i) off[i + 1] = off[i] + cnt[i];
+  const int64_t nnzb = off[N];
+  XM_CUDA(cudaMemcpyAsync(ro.p, off.data(), (size_t)(N + 1) * 8, cudaMemcpyHostToDevice, c->stream));
+  c->nnzb = nnzb;
+  c->stats.nnzb_S = nnzb;
+  c->s_rowptr.alloc(N + 1);
+  c->s_colidx.alloc((size_t)std::max<int64_t>(nnzb, 1));
+  k_pattern_cols<<<ceil_div(N, 8), 256, 0, c->stream>>>(N, W32, bits.p, ro.p, c->s_colidx.p,
+                                                       c->s_rowptr.p);
+  XM_CHECK_LAUNCH();
+  XM_CUDA(cudaMemcpyAsync(c->s_rowptr.p + N, ro.p + N, 8, cudaMemcpyDeviceToDevice, c->stream));
+  count_launch(c, 3);
+  sync(c);
+  bits.release();
+  c->pattern_valid = true;
+}
+
 // ============================================================ driver
 void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, const int32_t* lm_in,
                     const double* pts_in, const double* w_in) {
@@ -1099,37 +1136,10 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
   }
 
   phase("connectivity");
-  // ---- H3: S pattern
-  {
-    int W32 = ceil_div(N, 32);
-    DBuf<uint32_t>& bits = scratch_u32(c, "pattern_bits");
-    bits.alloc((size_t)N * W32);
-    XM_CUDA(cudaMemsetAsync(bits.p, 0, (size_t)N * W32 * 4, c->stream));
-    k_pattern_bits<<<N, 128, 0, c->stream>>>(N, W32, c->fr_off.p, c->fr_edge.p, c->e_lm.p,
-                                             c->lm_off.p, c->e_fr.p, bits.p);
-    XM_CHECK_LAUNCH();
-    DBuf<int32_t>& rc = scratch_i32(c, "pattern_rc");
-    DBuf<int32_t>& ro = scratch_i32(c, "pattern_ro");
-    rc.alloc(N);
-    ro.alloc(N);
-    k_pattern_count<<<N, 256, 0, c->stream>>>(N, W32, bits.p, rc.p);
-    XM_CHECK_LAUNCH();
-    exclusive_scan_i32(c, rc.p, ro.p, N, c->flags.p + 6);
-    int32_t nnzb = 0;
-    XM_CUDA(cudaMemcpyAsync(&nnzb, c->flags.p + 6, 4, cudaMemcpyDeviceToHost, c->stream));
-    sync(c);
-    c->nnzb = nnzb;
-    c->stats.nnzb_S = nnzb;
-    c->s_rowptr.alloc(N + 1);
-    c->s_colidx.alloc(nnzb);
-    k_pattern_cols<<<ceil_div(N, 8), 256, 0, c->stream>>>(N, W32, bits.p, ro.p, c->s_colidx.p,
-                                                         c->s_rowptr.p);
-    XM_CHECK_LAUNCH();
-    int64_t last = nnzb;
-    XM_CUDA(cudaMemcpyAsync(c->s_rowptr.p + N, &last, 8, cudaMemcpyHostToDevice, c->stream));
-    count_launch(c, 3);
-    sync(c);
-  }
+  // ---- H3: S pattern (the matrix-free mode never forms S: built on demand by
+  // xm_get_S_pattern)
+  if (c->opt.implicit_q == 0) build_s_pattern(c, N);
+  else c->pattern_valid = false;
 
   phase("pattern");
   // ---- H4: dense S (own rows, in the Q buffer), C̄ (in the G buffer), K̄ (in L)

@@ -1040,6 +1040,7 @@ xm_status xm_get_S_pattern(xm_ctx* c, int64_t* rowptr, int32_t* colidx, int64_t*
   return guard(c, [&] {
     require_stage(c, 1);
     if (!c->have_recovery) throw Error(XM_ESTATE, "no view graph (Q was set directly)");
+    if (!c->pattern_valid) build_s_pattern(c, c->N);  // matrix-free builds: on demand
     if (nnzb) *nnzb = c->nnzb;
     if (rowptr) copy_out(c, rowptr, c->s_rowptr.p, (size_t)(c->N + 1) * 8);
     if (colidx) copy_out(c, colidx, c->s_colidx.p, (size_t)c->nnzb * 4);

@@ -132,6 +132,7 @@ struct xm_ctx {
   xm::DBuf<int64_t> s_rowptr;
   xm::DBuf<int32_t> s_colidx;
   int64_t nnzb = 0;
+  bool pattern_valid = false;  // S pattern built (eagerly with dense Q, on demand matrix-free)
   // dense assembly products
   xm::DBuf<double> Q;   // nrows × ldq (this rank's rows)
   xm::DBuf<double> L;   // (N−1) × ldk  Cholesky of K̄
@@ -254,6 +255,7 @@ struct xm_ctx {
   std::map<std::string, xm::DBuf<int32_t>> s_i32;
   std::map<std::string, xm::DBuf<uint32_t>> s_u32;
   std::map<std::string, xm::DBuf<uint64_t>> s_u64;
+  std::map<std::string, xm::DBuf<int64_t>> s_i64;
   std::map<std::string, xm::DBuf<double>> s_f64;
   std::string last_error;
 };
@@ -280,6 +282,7 @@ void ensure_smem_attr(const void* kern, size_t smem);
 inline DBuf<int32_t>& scratch_i32(xm_ctx* c, const std::string& k) { return c->s_i32[k]; }
 inline DBuf<uint32_t>& scratch_u32(xm_ctx* c, const std::string& k) { return c->s_u32[k]; }
 inline DBuf<uint64_t>& scratch_u64(xm_ctx* c, const std::string& k) { return c->s_u64[k]; }
+inline DBuf<int64_t>& scratch_i64(xm_ctx* c, const std::string& k) { return c->s_i64[k]; }
 inline DBuf<double>& scratch_f64(xm_ctx* c, const std::string& k) { return c->s_f64[k]; }
 
 // ------------------------------------------------------------ util kernels (util.cu)
@@ -385,6 +388,7 @@ void batch_staircase(xm_ctx* c, int B, int N, const double* Q_dev, int64_t qstri
                      const double* Y0_dev, int r0, double* Yout_dev, xm_batch_result* res_dev);
 // NEXT-1 (implicit.cu)
 void implicit_prepare(xm_ctx* c);
+void build_s_pattern(xm_ctx* c, int N);
 void implicit_product(xm_ctx* c, const double* V, int r, double* out, const int* stop = nullptr,
                       int* exec = nullptr);
 double implicit_alg_bytes(xm_ctx* c, int r);
