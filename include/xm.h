@@ -104,8 +104,11 @@ typedef struct {
                           /* product + epilogue kernels (no persistent tCG)  [0]  */
   int32_t implicit_q;     /* 1: never form Q: each   */
                           /* Q·V by per-measurement elimination passes + K̄⁻¹ */
-                          /* (one GPU); ‖Q‖_F by a 16-probe estimate (C24);   */
-                          /* certificate by Lanczos on Z only              [0]  */
+                          /* (world > 1: pass shares + a K̄⁻¹ band, five       */
+                          /* all-reduces); ‖Q‖_F by a 16-probe estimate (C24); */
+                          /* certificate by Lanczos on Z only.  0: dense Q.   */
+                          /* −1: by a per-product time model at xm_build_Q    */
+                          /* (E: matrix-free on 1–2 GPUs; A–D: dense)   [−1]  */
 } xm_options;
 
 typedef struct {

@@ -948,6 +948,23 @@ __global__ void k_sumsq_rows(const double* __restrict__ Q, int rows, int n, int6
   if (threadIdx.x == 0) partials[blockIdx.x] = sh[0];
 }
 
+// The matrix-free mode's per-product time model (one rank): 1/world of each
+// mode's algorithmic bytes at its measured rate — the dense lower-triangle
+// stream at ≈ 6.1 TB/s plus one all-reduce, the matrix-free product at
+// ≈ 2.85 TB/s plus five dependent launches and five all-reduces (≈ 20 µs each
+// assumed over NVLink) — and the dense layout must fit (Q rows, G, K̄ factor).
+// E: matrix-free on 1–2 GPUs, the dense band at 4–8; A–D: dense.
+bool prefer_implicit(int N, int64_t E, int world) {
+  const double n = 3.0 * N, m = N - 1.0, P = world, ar = 20e-6;
+  const double t_dense = 8.0 * n * (n + 1.0) / 2.0 / P / 6.1e12 + (world > 1 ? ar : 0.0);
+  const double t_imp = (80.0 * (double)E + 8.0 * m * (m + 1.0) / 2.0) / P / 2.85e12 + 15e-6 +
+                       (world > 1 ? 5.0 * ar : 0.0);
+  const double dense_bytes = 8.0 * n * n / P + 8.0 * m * n + 3.0 * 8.0 * m * m;  // Q rows, G, K̄ (+L, U)
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && dense_bytes > 0.9 * (double)total_b) return true;
+  return t_imp < t_dense;
+}
+
 // H3: the co-visibility BSR pattern of S (bitmap per row → counts → 64-bit
 // row offsets (host prefix sum) → sorted column lists)
 void build_s_pattern(xm_ctx* c, int N) {
@@ -1138,7 +1155,11 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
   phase("connectivity");
   // ---- H3: S pattern (the matrix-free mode never forms S: built on demand by
   // xm_get_S_pattern)
-  if (c->opt.implicit_q == 0) build_s_pattern(c, N);
+  // NEXT-1 (implicit.cu): Q, S, C̄ and G are never formed — only K̄, its factor
+  // and inverse.  implicit_q < 0 (the default): the mode with the smaller
+  // modelled time per product (the model of bench.py --mode auto)
+  const bool implicit = c->opt.implicit_q > 0 || (c->opt.implicit_q < 0 && prefer_implicit(N, E, c->world));
+  if (!implicit) build_s_pattern(c, N);
   else c->pattern_valid = false;
 
   phase("pattern");
@@ -1150,8 +1171,6 @@ void build_Q_device(xm_ctx* c, int N, int M, int64_t E, const int32_t* fr_in, co
   c->ldq = round_up(std::max(n, 1), 32);
   c->ldk = round_up(std::max(N - 1, 1), 32);
   set_shard(c, N);
-  // NEXT-1 (implicit.cu): Q, S, C̄ and G are never formed — only K̄, its factor and inverse
-  const bool implicit = c->opt.implicit_q != 0;
   c->implicit_active = implicit;
   if (!implicit) {
     c->Q.alloc((size_t)std::max(c->nrows, 1) * c->ldq);

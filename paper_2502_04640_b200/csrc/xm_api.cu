@@ -633,6 +633,8 @@ void xm_default_options(xm_options* o) {
   o->cert_cholesky = 1;
   o->spmm_kernel = 0;
   o->seed = 0;
+  o->scale_reg = 0.0;
+  o->implicit_q = -1;  // auto: matrix-free where its modelled product time is smaller
 }
 
 const char* xm_strerror(xm_status s) {

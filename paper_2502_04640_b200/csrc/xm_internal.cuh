@@ -389,6 +389,7 @@ void batch_staircase(xm_ctx* c, int B, int N, const double* Q_dev, int64_t qstri
 // NEXT-1 (implicit.cu)
 void implicit_prepare(xm_ctx* c);
 void build_s_pattern(xm_ctx* c, int N);
+bool prefer_implicit(int N, int64_t E, int world);
 void implicit_product(xm_ctx* c, const double* V, int r, double* out, const int* stop = nullptr,
                       int* exec = nullptr);
 double implicit_alg_bytes(xm_ctx* c, int r);

@@ -121,7 +121,7 @@ def test_E_sampled_Q_rows_and_spmm(xm, E_noisy):
     Vs = {r: random_tangent_ambient(sc.N, r, 21 + r) for r in (1, 3)}
     outs = {}
     for kernel in (0, 1, 2):
-        with xm.Context(profile=1, spmm_kernel=kernel) as ctx:
+        with xm.Context(profile=1, spmm_kernel=kernel, implicit_q=0) as ctx:
             ctx.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
             if kernel == 0:
                 Qg = np.concatenate([ctx.Q_rows(int(a), 3) for a in rows[::3]])
@@ -140,7 +140,7 @@ def test_E_noise_free_known_optimum(xm):
     """F1: noise-free ⇒ f* = 0, certified, rounded poses = ground truth."""
     sc = config_scene("E")
     assert sc.noise_free
-    with xm.Context(profile=1) as ctx:
+    with xm.Context(profile=1, implicit_q=0) as ctx:  # the dense path (matrix-free: test_gpu_implicit)
         ctx.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
         status, info = ctx.solve()
         cert = ctx.certify()
@@ -155,7 +155,7 @@ def test_E_noise_free_known_optimum(xm):
 
 def test_E_noisy_certified_and_recovery_optimal(xm, E_noisy):
     sc = E_noisy
-    with xm.Context(profile=1) as ctx:
+    with xm.Context(profile=1, implicit_q=0) as ctx:  # the dense path
         ctx.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
         status, info = ctx.solve()
         cert = ctx.certify()
