@@ -150,7 +150,11 @@ std::vector<uintptr_t> graph_signature(xm_ctx* c) {
           (uintptr_t)c->opt.spmm_kernel, reg_bits(c), (uintptr_t)c->implicit_active,
           (uintptr_t)c->Kinv.p, (uintptr_t)c->imp_lm.p, (uintptr_t)c->e_fr.p,
           (uintptr_t)c->imp_pts.p, (uintptr_t)c->imp_mom.p, (uintptr_t)c->imp_tb.p,
-          (uintptr_t)c->imp_sym_part.p, (uintptr_t)c->imp_sym_plan};
+          (uintptr_t)c->imp_sym_part.p, (uintptr_t)c->imp_sym_plan,
+          // the matrix-free kernels take E / M by value (array offsets, loop
+          // bounds): an XM² rebuild at the same addresses must recapture
+          (uintptr_t)c->E, (uintptr_t)c->M, (uintptr_t)c->imp_k0, (uintptr_t)c->imp_k1,
+          (uintptr_t)c->imp_f0, (uintptr_t)c->imp_f1, (uintptr_t)c->imp_ka, (uintptr_t)c->imp_kb};
 }
 
 void destroy_graph(xm_ctx::TcgGraph& g) {

@@ -131,3 +131,33 @@ def test_xm2_parity(xm, case):
     assert np.max(np.abs(sol2["R"] - osol2.R)) <= 1e-6
     assert np.all(np.isnan(res2[~keep])) and np.all(np.isfinite(res2[keep]))
     assert cert2["eta"] <= 1e-6
+
+
+def test_xm2_matrix_free_rebuild_matches_dense(xm):
+    """XM² through the matrix-free products (the E headline mode): the rebuild
+    changes E / M at the same device addresses, so every captured tCG graph
+    must be recaptured (graph signature) — regression for stale graphs; the
+    second solve then equals the dense path's (same kept set, same certified
+    optimum) and the oracle's second solve of that kept set."""
+    sc0 = make_scene(150, 3000, "unordered", seed=11, track_mean=8.0, sigma_u=1e-3, sigma_d=0.01)
+    sc, bad = corrupt(sc0, 0.03, seed=11)
+    out = {}
+    for imp in (0, 1):
+        with xm.Context(device=0, implicit_q=imp) as ctx:
+            ctx.build_Q(sc.N, sc.M, sc.frame, sc.landmark, sc.pts, sc.w)
+            st, info = ctx.solve(r0=3)
+            ctx.round_recover()
+            keep, nd, nr = ctx.xm2(0.1)
+            st2, info2 = ctx.solve(r0=3)
+            cert2 = ctx.certify()
+            out[imp] = (st, keep, st2, info2, cert2, ctx.get_factor())
+    (s0, k0, s20, i20, c20, Y0), (s1, k1, s21, i21, c21, Y1) = out[0], out[1]
+    assert s0 == s1 == 0 and np.array_equal(k0, k1)
+    assert s20 == s21 == 0 and i20["certified"] == i21["certified"] == 1
+    assert abs(i21["f"] - i20["f"]) <= 1e-8 * (1.0 + abs(i20["f"]))
+    X0, X1 = Y0 @ Y0.T, Y1 @ Y1.T
+    assert np.linalg.norm(X1 - X0) <= 1e-6 * np.linalg.norm(X0)
+    k = k1
+    dm2 = xo.build_Q(sc.N, sc.M, sc.frame[k], sc.landmark[k], sc.pts[k], sc.w[k])
+    st_o = xo.staircase(dm2)
+    assert abs(i21["f"] - st_o.f) <= 1e-8 * (1.0 + abs(st_o.f))
