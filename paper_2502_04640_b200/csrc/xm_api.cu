@@ -395,6 +395,70 @@ TcgState tcg_deferred_state(xm_ctx* c) {
   return hs;
 }
 
+// The outer iteration's step after tCG: retraction of η (+ ⟨g,η⟩, ⟨η,Hη⟩ into
+// scal[10..11]), the cancellation-free Δf product (scal[8..9]) and the App. D
+// term.  One GPU with profiling off: replayed as ONE cached graph per rank
+// (the same kernels in the same order — bitwise the same results — minus the
+// per-kernel launch latencies).
+static void post_tcg_sequence(xm_ctx* c, int r) {
+  XM_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int), c->stream));
+  const int nb = frame_blocks(c);
+  retract(c, r, c->Y.p, c->eta.p, 1.0, c->Ynew.p, c->Dv.p, c->flags.p, c->grad.p, c->Heta.p, c->red.p);
+  reduce_partials(c, c->red.p, nb, 2, c->scal.p + 10);
+  df_product(c, r, c->Dv.p, c->QY.p, c->QD.p, c->scal.p + 8);
+  if (c->opt.scale_reg != 0.0) reg_frames(c, r, c->Y.p, c->Dv.p, c->scal.p + 24);
+}
+
+static void post_tcg(xm_ctx* c, int r) {
+  const int nb = frame_blocks(c);
+  c->red.alloc((size_t)nb * 4 + 1024);
+  if (c->opt.profile || !c->use_graphs || c->world != 1 || std::getenv("XM_NO_POST_GRAPH")) {
+    post_tcg_sequence(c, r);
+    return;
+  }
+  auto& g = c->post_graphs[r];
+  auto sig = graph_signature(c);
+  sig.push_back((uintptr_t)c->red.p);
+  sig.push_back((uintptr_t)c->scal.p);
+  sig.push_back((uintptr_t)c->flags.p);
+  if (!(g.exec && g.sig == sig)) {
+    destroy_graph(g);
+    g.sig = sig;
+    if (!c->cap_stream) XM_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+    // first use: run it eagerly (allocations / plans happen outside any capture)
+    post_tcg_sequence(c, r);
+    sync(c);
+    cudaStream_t orig = c->stream;
+    const int64_t l0 = c->stats.kernel_launches, s0 = c->stats.spmm_calls;
+    c->stream = c->cap_stream;
+    cudaGraph_t graph = nullptr;
+    bool ok = true;
+    try {
+      XM_CUDA(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeRelaxed));
+      post_tcg_sequence(c, r);
+      XM_CUDA(cudaStreamEndCapture(c->cap_stream, &graph));
+    } catch (...) {
+      cudaStreamEndCapture(c->cap_stream, &graph);
+      cudaGetLastError();
+      ok = false;
+    }
+    c->stream = orig;
+    g.launches = c->stats.kernel_launches - l0;
+    g.spmms = c->stats.spmm_calls - s0;
+    c->stats.kernel_launches = l0;
+    c->stats.spmm_calls = s0;
+    if (ok && cudaGraphInstantiate(&g.exec, graph, 0) != cudaSuccess) {
+      cudaGetLastError();
+      g.exec = nullptr;
+    }
+    if (graph) cudaGraphDestroy(graph);
+    return;  // this iteration's step already ran eagerly (and was counted)
+  }
+  XM_CUDA(cudaGraphLaunch(g.exec, c->stream));
+  c->stats.kernel_launches += g.launches;
+  c->stats.spmm_calls += g.spmms;
+}
+
 struct RtrOut {
   bool converged = false;
   int64_t outer = 0;
@@ -429,14 +493,7 @@ RtrOut rtr(xm_ctx* c, double tol_abs) {
     if (!deferred) c->info.hvps += hs.n_hvp;
     pc.lap(0);
     // ---- retraction (+ ⟨g,η⟩, ⟨η,Hη⟩) and cancellation-free Δf (reading C21)
-    XM_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int), c->stream));
-    const int nb = frame_blocks(c);
-    c->red.alloc((size_t)nb * 4 + 1024);
-    retract(c, r, c->Y.p, c->eta.p, 1.0, c->Ynew.p, c->Dv.p, c->flags.p, c->grad.p, c->Heta.p,
-            c->red.p);
-    reduce_partials(c, c->red.p, nb, 2, c->scal.p + 10);
-    df_product(c, r, c->Dv.p, c->QY.p, c->QD.p, c->scal.p + 8);
-    if (o.scale_reg != 0.0) reg_frames(c, r, c->Y.p, c->Dv.p, c->scal.p + 24);
+    post_tcg(c, r);
     // one host round trip: Δf terms, the App. D term, the retraction flag and
     // (deferred) the tCG state, all through the pinned host scalars
     double* hp = c->hpin;
@@ -601,6 +658,7 @@ __global__ void k_identity_init(int N, int r, double* Y) {
 
 void destroy_graphs(xm_ctx* c) {
   for (auto& g : c->tcg_graphs) destroy_graph(g);
+  for (auto& g : c->post_graphs) destroy_graph(g);
 }
 
 void reset_after_new_Q(xm_ctx* c) {

@@ -216,6 +216,9 @@ struct xm_ctx {
     std::vector<uintptr_t> sig;                   // buffers / sizes the capture baked in
   };
   TcgGraph tcg_graphs[XM_MAX_R + 1];
+  // the outer iteration's step after tCG (retraction, Δf product, dots) as one
+  // graph per rank r (profile off, one GPU)
+  TcgGraph post_graphs[XM_MAX_R + 1];
   TcgGraph* cap_target = nullptr;                 // non-null while capturing
   // capturing the body of a conditional WHILE node (the whole tCG loop in one
   // graph launch): k_tcg_dir clears `cap_cond` when the tCG state says stop
