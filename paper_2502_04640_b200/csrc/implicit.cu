@@ -62,9 +62,10 @@ template <int R>
 struct Grp {
   static constexpr int NG = 32 / R;  // measurements per warp round
 };
-// row stride of the landmark array p (M × PR): r rounded up to even, so the
-// frame-output pass gathers a landmark's row with 16-B loads (⌈r/2⌉ instead of
-// r scattered accesses per measurement)
+// row stride of the landmark arrays m and p (M × PR): r rounded up to even, so
+// the frame-output pass gathers a landmark's row of p with 16-B / 32-B loads and
+// a gathered row never straddles a 32-B sector for r ≤ 4 (the L1 data pipe of
+// these gathers costs about one wavefront per sector touched)
 template <int R>
 struct PStride {
   static constexpr int PR = (R + 1) & ~1;
@@ -84,8 +85,44 @@ __device__ __forceinline__ void group_sum(double (&v)[K], int g) {
   }
 }
 
+// Frame-block transpose of V for the landmark-mean gather (r ≤ 8): frame i's
+// block holds column j of V_i (3 rows + one pad) in the 32 B at Vt[i·FS + 4j],
+// blocks FS doubles apart (128 B for r ≤ 4, 256 B for r ≤ 8, line-aligned), so
+// the lane owning column j fetches its three values with ONE 256-bit load and a
+// measurement's R lanes touch one 128-B line (three sectors, one instruction)
+// instead of three row gathers straddling sectors; the L1 data pipe that bounds
+// this pass costs about one wavefront per sector touched (E, r = 3: 79 → 69 µs
+// with the 2-µs transpose).  Same products, same order: bitwise identical.
+template <int R>
+struct VtStride {
+  static constexpr int FS = ((4 * R + 15) / 16) * 16;
+};
+constexpr int kVtMaxR = 8;
+
+template <int R>
+__global__ void k_imp_vt(int N, const double* __restrict__ V, double* __restrict__ Vt,
+                         const int* __restrict__ stop) {
+  if (stop && *stop) return;
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;  // (frame i, column j)
+  if (x >= N * R) return;
+  const int i = x / R, j = x - i * R;
+  const double* vi = V + (int64_t)3 * i * R + j;
+  double* o = Vt + (int64_t)i * VtStride<R>::FS + 4 * j;
+  o[0] = vi[0];
+  o[1] = vi[R];
+  o[2] = vi[2 * R];
+  o[3] = 0.0;
+}
+
+__device__ __forceinline__ double4 ldg_v4(const double* p) {  // LDG.E.ENL2.256, 32-B aligned
+  double4 v;
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+
 // m_k = Σ_{e∈k} (w_e ũ_e)ᵀ V_{i_e} / W_k          (landmark-sorted, 28 B / measurement)
-template <int R, int U = kU>
+// VT: V given as the frame-block transpose Vt (k_imp_vt)
+template <int R, int U = kU, bool VT = false>
 __global__ void __launch_bounds__(kIT) k_imp_lm_mean(int k0, int k1, const int32_t* __restrict__ lm_off,
                                                      const int32_t* __restrict__ L_i,
                                                      const double* __restrict__ L_wx,
@@ -118,17 +155,25 @@ __global__ void __launch_bounds__(kIT) k_imp_lm_mean(int k0, int k1, const int32
       a1[q] = okw * __ldcs(L_wy + e);
       a2[q] = okw * __ldcs(L_wz + e);
     }
+    if constexpr (VT) {
+      double4 vv[U];
 #pragma unroll
-    for (int q = 0; q < U; ++q) {
-      const double* vi = V + (int64_t)3 * ii[q] * R + j;
-      acc[0] = fma(a0[q], vi[0], fma(a1[q], vi[R], fma(a2[q], vi[2 * R], acc[0])));
+      for (int q = 0; q < U; ++q) vv[q] = ldg_v4(V + (int64_t)ii[q] * VtStride<R>::FS + 4 * j);
+#pragma unroll
+      for (int q = 0; q < U; ++q) acc[0] = fma(a0[q], vv[q].x, fma(a1[q], vv[q].y, fma(a2[q], vv[q].z, acc[0])));
+    } else {
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const double* vi = V + (int64_t)3 * ii[q] * R + j;
+        acc[0] = fma(a0[q], vi[0], fma(a1[q], vi[R], fma(a2[q], vi[2 * R], acc[0])));
+      }
     }
   }
   group_sum<R, 1>(acc, g);
   if (lane < R) {
     const double sum = acc[0];
     const double wk = W[k], inv = wk > 0.0 ? 1.0 / wk : 0.0;
-    m[(int64_t)k * R + lane] = sum * inv;
+    m[(int64_t)k * PStride<R>::PR + lane] = sum * inv;
   }
 }
 
@@ -163,7 +208,7 @@ __global__ void __launch_bounds__(kIT) k_imp_fr_b(int f0, int f1, const int32_t*
       we[q] = ((act && e0 < hi) ? 1.0 : 0.0) * __ldcs(F_w + e);
     }
 #pragma unroll
-    for (int q = 0; q < U; ++q) acc[0] = fma(we[q], m[(int64_t)kk[q] * R + j], acc[0]);
+    for (int q = 0; q < U; ++q) acc[0] = fma(we[q], m[(int64_t)kk[q] * PStride<R>::PR + j], acc[0]);
   }
   group_sum<R, 1>(acc, g);
   if (lane < R) {
@@ -259,7 +304,7 @@ __global__ void __launch_bounds__(kIT) k_imp_lm_p(int k0, int k1, const int32_t*
   if (lane < R) {
     const double sum = acc[0];
     const double wk = W[k], inv = wk > 0.0 ? 1.0 / wk : 0.0;
-    p[(int64_t)k * PStride<R>::PR + lane] = fma(-sum, inv, m[(int64_t)k * R + lane]);
+    p[(int64_t)k * PStride<R>::PR + lane] = fma(-sum, inv, m[(int64_t)k * PStride<R>::PR + lane]);
     if (PStride<R>::PR != R && lane == R - 1) p[(int64_t)k * PStride<R>::PR + R] = 0.0;
   }
 }
@@ -301,13 +346,24 @@ __global__ void __launch_bounds__(kIT, (R <= 5) ? 4 : 1) k_imp_fr_out(int f0, in
 #pragma unroll
     for (int q = 0; q < U; ++q) {
       constexpr int PR = PStride<R>::PR;
-      const double2* pk = reinterpret_cast<const double2*>(p + (int64_t)kk[q] * PR);
       double pv[PR];
+      if constexpr (PR % 4 == 0) {  // 256-bit loads (32-B aligned rows): one access per 4 values
 #pragma unroll
-      for (int h = 0; h < PR / 2; ++h) {
-        const double2 t2 = pk[h];
-        pv[2 * h] = t2.x;
-        pv[2 * h + 1] = t2.y;
+        for (int h = 0; h < PR / 4; ++h) {
+          const double4 t4 = ldg_v4(p + (int64_t)kk[q] * PR + 4 * h);
+          pv[4 * h] = t4.x;
+          pv[4 * h + 1] = t4.y;
+          pv[4 * h + 2] = t4.z;
+          pv[4 * h + 3] = t4.w;
+        }
+      } else {
+        const double2* pk = reinterpret_cast<const double2*>(p + (int64_t)kk[q] * PR);
+#pragma unroll
+        for (int h = 0; h < PR / 2; ++h) {
+          const double2 t2 = pk[h];
+          pv[2 * h] = t2.x;
+          pv[2 * h + 1] = t2.y;
+        }
       }
 #pragma unroll
       for (int c = 0; c < R; ++c) {
@@ -428,6 +484,19 @@ __global__ void k_rademacher_pack(int64_t n, int r, int col, const double* __res
     default: throw Error(XM_EINVAL, "rank r out of range (1..12)");             \
   }
 }  // namespace
+
+// the transpose and the landmark-mean pass over it (r ≤ kVtMaxR)
+template <int R>
+static void lm_mean_vt(xm_ctx* c, int k0, int k1, const double* V, double* vt, double* m, const int* stop,
+                       int* exec) {
+  if constexpr (R <= kVtMaxR) {
+    const int64_t E = c->E;
+    const double* P = c->imp_pts.p;
+    k_imp_vt<R><<<ceil_div(c->N * R, 256), 256, 0, c->stream>>>(c->N, V, vt, stop);
+    k_imp_lm_mean<R, kU, true><<<ceil_div(k1 - k0, kIT / 32), kIT, 0, c->stream>>>(
+        k0, k1, c->lm_off.p, c->e_fr.p, P, P + E, P + 2 * E, c->W.p, vt, m, stop, exec);
+  }
+}
 
 // XM_IMP_DEBUG=1: synchronise after every pass and name the failing one
 static void imp_dbg(xm_ctx* c, const char* what) {
@@ -568,17 +637,26 @@ void implicit_product(xm_ctx* c, const double* V, int r, double* out, const int*
   const double* cfr = c->imp_mom.p;
   const double* Afr = c->imp_mom.p + 3 * (size_t)N;
   const int k0 = c->imp_k0, k1 = c->imp_k1, f0 = c->imp_f0, f1 = c->imp_f1;
-  const int PR = (r + 1) & ~1;  // p's row stride (PStride)
+  const int PR = (r + 1) & ~1;  // m's and p's row stride (PStride)
   imp_dbg(c, "entry");
-  if (sh) XM_CUDA(cudaMemsetAsync(m.p, 0, (size_t)M * r * 8, c->stream));
-  if (k1 > k0)
+  if (sh) XM_CUDA(cudaMemsetAsync(m.p, 0, (size_t)M * PR * 8, c->stream));
+  static const bool no_vt = std::getenv("XM_IMP_NO_VT") != nullptr;
+  if (k1 > k0 && r <= kVtMaxR && !no_vt) {
+    DBuf<double>& vt = scratch_f64(c, "imp_vt");
+    vt.alloc((size_t)N * VtStride<kVtMaxR>::FS + 8);
+    XM_IMP_DISPATCH(r, (lm_mean_vt<R>(c, k0, k1, V, vt.p, m.p, stop, exec)));
+    count_launch(c);
+  } else if (k1 > k0) {
     XM_IMP_DISPATCH(r, (k_imp_lm_mean<R><<<ceil_div(k1 - k0, kIT / 32), kIT, 0, c->stream>>>(
                            k0, k1, c->lm_off.p, c->e_fr.p, P, P + E, P + 2 * E, c->W.p, V, m.p, stop, exec)));
-  if (sh) nccl_allreduce_sum(c, m.p, (size_t)M * r);
+  }
+  if (sh) nccl_allreduce_sum(c, m.p, (size_t)M * PR);
   imp_dbg(c, "lm_mean");
   const int fb0 = std::max(f0, 1);
   if (sh) XM_CUDA(cudaMemsetAsync(bs.p, 0, (size_t)std::max(N - 1, 1) * r * 8, c->stream));
-  if (f1 > fb0)  // 16 rounds in flight (E: 43 → 36 µs; the other passes measured flat or slower)
+  // 16 rounds in flight (E: 43 → 36 µs; the other passes measured flat or slower; two
+  // frames per warp interleaved, to run the 10155 frames in one wave, measured slower: 43 vs 41 µs)
+  if (f1 > fb0)
     XM_IMP_DISPATCH(r, (k_imp_fr_b<R, 16><<<ceil_div(f1 - fb0, kIT / 32), kIT, 0, c->stream>>>(
                            f0, f1, c->fr_off.p, c->imp_lm.p, c->imp_w.p, cfr, V, m.p, bs.p, stop)));
   XM_CHECK_LAUNCH();
