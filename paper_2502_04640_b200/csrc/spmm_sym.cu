@@ -475,13 +475,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_sym(
     const double* p = rowpart + (rtile_base(K) * TR + l) * R + cc;
     double acc = 0.0;
     int q = (K >= rt_a && K < rt_b) ? 0 : Jc + 1;  // row parts exist for the band's rows only
-    for (; q + 16 <= Jc + 1; q += 16) {  // 16 loads in flight, summed in order (the
+#ifndef XM_SYM_FIN_INFLIGHT
+#define XM_SYM_FIN_INFLIGHT 32
+#endif
+    constexpr int kF = XM_SYM_FIN_INFLIGHT;
+    for (; q + kF <= Jc + 1; q += kF) {  // kF loads in flight, summed in order (the
       // finish is latency-bound: ≈ n/256 partials per element, one element per thread)
+      double v[kF];
+#pragma unroll
+      for (int u = 0; u < kF; ++u) v[u] = p[(int64_t)(q + u) * TR * R];
+#pragma unroll
+      for (int u = 0; u < kF; ++u) acc += v[u];
+    }
+    if (kF > 16 && q + 16 <= Jc + 1) {
       double v[16];
 #pragma unroll
       for (int u = 0; u < 16; ++u) v[u] = p[(int64_t)(q + u) * TR * R];
 #pragma unroll
       for (int u = 0; u < 16; ++u) acc += v[u];
+      q += 16;
     }
     for (; q + 4 <= Jc + 1; q += 4) {  // 4 loads in flight, summed in order
       const double a0 = p[(int64_t)q * TR * R], a1 = p[(int64_t)(q + 1) * TR * R];
