@@ -856,27 +856,67 @@ static void trsm_block_inner(xm_ctx* c, const double* L, int64_t ldl, const doub
 // lower_rhs: B is lower triangular (B[i][j] = 0 for j > i, e.g. the identity
 // when inverting L) — then so is the solution, and super-block rows sb..se only
 // carry columns < se: m³/3 instead of m³ flops.
+// The super-block inverses do not depend on B: they are all computed first,
+// round-robin on kTrsmStreams forked streams (each chain — 8 serial 64-row
+// solves of 4 CTAs and their small updates — is latency-bound, E: ≈ 1.4 ms per
+// super-block, 29 ms in series), then B's super-block chain runs on the main
+// stream.  Same kernels, same arithmetic (bitwise identical); XM_NO_TRSM_FORK=1:
+// in series on the main stream.
+static void trsm_superblock_inverse(xm_ctx* c, const double* L, int64_t ldl, const double* U,
+                                    int64_t ldu, int sb, int se, double* T, double* Tt, int SB) {
+  const int s = se - sb;
+  k_eye<<<ceil_div(s * s, 256), 256, 0, c->stream>>>(T, s, SB);
+  XM_CHECK_LAUNCH();
+  trsm_block_inner(c, L, ldl, U, ldu, sb, se, T, s, SB);  // T = L_ss⁻¹
+  k_transpose<<<dim3(ceil_div(s, 32), ceil_div(s, 32)), dim3(32, 8), 0, c->stream>>>(T, SB, Tt, SB, s, s);
+  XM_CHECK_LAUNCH();
+  count_launch(c, 2);
+}
+
 void dense_trsm_lower_left(xm_ctx* c, const double* L, int m, int64_t ldl, const double* U,
                            int64_t ldu, double* B, int ncols, int64_t ldb, bool lower_rhs) {
   const int SB = c->trsm_sb;
+  const int nsb = ceil_div(m, SB);
+  static const bool no_fork = std::getenv("XM_NO_TRSM_FORK") != nullptr;
+  const bool fork = !no_fork && nsb > 1 && c->cap_target == nullptr;  // not inside a graph capture
+  constexpr int kS = xm_ctx::kTrsmStreams;
   DBuf<double>& T = scratch_f64(c, "trsm_inv");
   DBuf<double>& Tt = scratch_f64(c, "trsm_invT");
   DBuf<double>& X = scratch_f64(c, "trsm_rows");
-  T.alloc((size_t)SB * SB);
-  Tt.alloc((size_t)SB * SB);
+  T.alloc((size_t)(fork ? kS : 1) * SB * SB);         // one per stream
+  Tt.alloc((size_t)(fork ? nsb : 1) * SB * SB);       // every super-block's L_ss⁻ᵀ
   X.alloc((size_t)SB * ldb);
+  if (fork) {
+    for (int q = 0; q < kS; ++q)
+      if (!c->trsm_streams[q]) XM_CUDA(cudaStreamCreateWithFlags(&c->trsm_streams[q], cudaStreamNonBlocking));
+    for (int q = 0; q <= kS; ++q)
+      if (!c->trsm_ev[q]) XM_CUDA(cudaEventCreateWithFlags(&c->trsm_ev[q], cudaEventDisableTiming));
+    XM_CUDA(cudaEventRecord(c->trsm_ev[kS], c->stream));
+    const cudaStream_t main = c->stream;
+    for (int q = 0; q < kS; ++q) XM_CUDA(cudaStreamWaitEvent(c->trsm_streams[q], c->trsm_ev[kS], 0));
+    try {
+      for (int b = 0; b < nsb; ++b) {
+        c->stream = c->trsm_streams[b % kS];
+        trsm_superblock_inverse(c, L, ldl, U, ldu, b * SB, std::min(m, (b + 1) * SB),
+                                T.p + (size_t)(b % kS) * SB * SB, Tt.p + (size_t)b * SB * SB, SB);
+      }
+    } catch (...) {
+      c->stream = main;
+      throw;
+    }
+    c->stream = main;
+    for (int q = 0; q < kS; ++q) {
+      XM_CUDA(cudaEventRecord(c->trsm_ev[q], c->trsm_streams[q]));
+      XM_CUDA(cudaStreamWaitEvent(c->stream, c->trsm_ev[q], 0));
+    }
+  }
   for (int sb = 0; sb < m; sb += SB) {
     const int se = std::min(m, sb + SB), s = se - sb;
-    k_eye<<<ceil_div(s * s, 256), 256, 0, c->stream>>>(T.p, s, SB);
-    XM_CHECK_LAUNCH();
-    trsm_block_inner(c, L, ldl, U, ldu, sb, se, T.p, s, SB);       // T = L_ss⁻¹
-    k_transpose<<<dim3(ceil_div(s, 32), ceil_div(s, 32)), dim3(32, 8), 0, c->stream>>>(T.p, SB, Tt.p,
-                                                                                       SB, s, s);
-    XM_CHECK_LAUNCH();
-    count_launch(c, 2);
+    const double* Ts = Tt.p + (fork ? (size_t)(sb / SB) * SB * SB : 0);
+    if (!fork) trsm_superblock_inverse(c, L, ldl, U, ldu, sb, se, T.p, Tt.p, SB);
     const int nc = lower_rhs ? std::min(ncols, se) : ncols;  // columns ≥ se of rows < se are 0
     // X = L_ss⁻¹ B_s :  X[i][j] = Σ_k Tt[k][i] B[sb + k][j]
-    dgemm_tn(c, false, s, nc, s, 1.0, Tt.p, SB, B + (int64_t)sb * ldb, ldb, 0.0, X.p, ldb);
+    dgemm_tn(c, false, s, nc, s, 1.0, Ts, SB, B + (int64_t)sb * ldb, ldb, 0.0, X.p, ldb);
     XM_CUDA(cudaMemcpy2DAsync(B + (int64_t)sb * ldb, ldb * sizeof(double), X.p, ldb * sizeof(double),
                               (size_t)nc * sizeof(double), s, cudaMemcpyDeviceToDevice, c->stream));
     if (se < m)

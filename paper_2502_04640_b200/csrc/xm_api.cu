@@ -790,6 +790,10 @@ void xm_destroy(xm_ctx* c) {
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
   if (c->hpin) cudaFreeHost(c->hpin);
+  for (int q = 0; q < xm_ctx::kTrsmStreams; ++q)
+    if (c->trsm_streams[q]) cudaStreamDestroy(c->trsm_streams[q]);
+  for (int q = 0; q <= xm_ctx::kTrsmStreams; ++q)
+    if (c->trsm_ev[q]) cudaEventDestroy(c->trsm_ev[q]);
   if (c->ev_la) cudaEventDestroy(c->ev_la);
   if (c->ev_lb) cudaEventDestroy(c->ev_lb);
   nccl_destroy(c);

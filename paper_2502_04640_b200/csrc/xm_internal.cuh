@@ -232,6 +232,11 @@ struct xm_ctx {
   double* hpin = nullptr;
   int64_t tcg_defer_launches = 0;
   cudaEvent_t ev_la = nullptr, ev_lb = nullptr;
+  // TRSM: the super-block inverses L_ss⁻¹ (independent of the right-hand side)
+  // are computed ahead on kTrsmStreams forked streams (dense_trsm_lower_left)
+  static constexpr int kTrsmStreams = 4;
+  cudaStream_t trsm_streams[kTrsmStreams] = {};
+  cudaEvent_t trsm_ev[kTrsmStreams + 1] = {};
   bool use_graphs = true;
   xm::DBuf<double> sym_part;       // per-unit row / column partials of the symmetric SpMM
   // XM_PHASES=1: host wall-clock breakdown of xm_solve (synchronises; diagnostics only)
