@@ -354,7 +354,7 @@ def traffic_of(key):
 KERNEL_DENSE_B = ("k_tcg_persist_sym (lower-triangle Q stream, timed per tCG iteration incl. its "
                   "barriers and camera update) + k_spmm_sym (other products)")
 KERNEL_DENSE = "k_spmm_sym (lower-triangle Q stream, every product incl. the tCG HVP)"
-KERNEL_IMPLICIT = ("matrix-free Q·V product, timed as one unit: k_imp_lm_mean, k_imp_fr_b, "
+KERNEL_IMPLICIT = ("matrix-free Q·V product, timed as one unit: k_imp_vt, k_imp_lm_mean, k_imp_fr_b, "
                    "k_spmm_sym on the lower triangle of K̄⁻¹, k_imp_lm_p, k_imp_fr_out")
 
 
